@@ -1,0 +1,318 @@
+/*
+ * mgcuda.h — C-ABI of the B200-native gradient meta-estimation hot path.
+ *
+ * Drop-in boundary for the reference `metagrad` library (arxiv 2309.15676,
+ * /root/reference/proj).  The reference boundary is a C++ value-semantics API
+ * (SURVEY.md §8(b)); every entry point below names the reference symbol it
+ * replaces (file:line, relative to /root/reference/proj).  INTEGRATION.md shows
+ * the C++ adapter (include/mgcuda.hpp) and the ctypes binding a maintainer adds.
+ *
+ * Conventions
+ *   - Every function returns an mg_status; MG_OK == 0.  The reference throws:
+ *       std::invalid_argument -> MG_EINVAL   (meta.hpp:99, moment2.hpp:33, harness.cpp:42-66)
+ *       std::logic_error      -> MG_ELOGIC   (meta.hpp:101, negative variance)
+ *       std::domain_error     -> MG_EDOMAIN  (problems.cpp:93, invalid params)
+ *     mg_last_error() returns the message of the last failure on this thread.
+ *   - Buffers are DEVICE pointers (cudaMalloc / torch CUDA storage), SoA, one
+ *     entry per parameter, element type given by the dtype argument
+ *     (MG_F32 = float, MG_F64 = double).  Host-side scalars are always double.
+ *   - A context owns one device and one CUDA stream; every call is
+ *     asynchronous on that stream unless it returns host data.  A context is
+ *     single-threaded: use one per host thread / device.
+ *   - No torch types, no C++ types cross this boundary.
+ *   - There is NO CPU fallback: on a machine without a usable sm_100 device
+ *     mg_ctx_create fails with MG_ECUDA.
+ */
+#ifndef MGCUDA_H_
+#define MGCUDA_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define MGCUDA_ABI_VERSION 1
+
+typedef enum mg_status {
+  MG_OK = 0,
+  MG_EINVAL = 1,   /* std::invalid_argument */
+  MG_ELOGIC = 2,   /* std::logic_error */
+  MG_EDOMAIN = 3,  /* std::domain_error */
+  MG_ECUDA = 4,    /* CUDA runtime failure / no device */
+  MG_ENOMEM = 5,
+  MG_EUNSUPPORTED = 6
+} mg_status;
+
+typedef enum mg_dtype { MG_F32 = 0, MG_F64 = 1 } mg_dtype;
+
+/* ExperimentConfig (harness.hpp:18-67).  Strings become enums. */
+typedef enum mg_problem_kind { MG_EXP_RATE = 0, MG_MULT_NOISE = 1, MG_MINI_RENDER = 2 } mg_problem_kind;
+typedef enum mg_optimizer_kind { MG_OPT_META = 0, MG_OPT_ADAM = 1 } mg_optimizer_kind;
+typedef enum mg_trajectory_kind {
+  MG_TRAJ_OPTIMISE = 0,
+  MG_TRAJ_SCRIPTED_LINEAR = 1,
+  MG_TRAJ_SCRIPTED_EXP = 2
+} mg_trajectory_kind;
+typedef enum mg_diff_norm_kind { MG_DIFF_NORM_GLOBAL = 0, MG_DIFF_NORM_PER_PARAM = 1 } mg_diff_norm_kind;
+typedef enum mg_rng_kind {
+  MG_RNG_MT64 = 0,   /* bit-exact std::mt19937_64 streams (rng.hpp:23-36) */
+  MG_RNG_PHILOX = 1  /* counter-based Philox4x32-10, statistically equivalent */
+} mg_rng_kind;
+
+typedef struct mg_experiment_config {
+  int32_t problem;     /* mg_problem_kind   (harness.hpp:19) */
+  int32_t optimizer;   /* mg_optimizer_kind (harness.hpp:20) */
+  int32_t iterations;  /* harness.hpp:21 */
+  int32_t replicates;  /* harness.hpp:22 */
+  uint64_t seed;       /* harness.hpp:23 */
+  double lr, beta_f, beta_delta, beta1, beta2, eps_step, eps_alpha, adam_eps; /* :26-33 */
+  int32_t dim;              /* mult-noise :36 */
+  int32_t samples_per_iter; /* :38 */
+  double sigma;             /* :37 */
+  double target_mean;       /* :39 */
+  double rate_init;         /* :40 */
+  int32_t pixel_count;      /* :41 */
+  int32_t spp;              /* :42 */
+  uint64_t problem_seed;    /* :43 */
+  double albedo_init;       /* :44 */
+  double exponent_max;      /* :45 */
+  int32_t trajectory;       /* mg_trajectory_kind :48 */
+  int32_t diff_norm;        /* mg_diff_norm_kind :57 */
+  double traj_rate;         /* :49 */
+  int32_t no_alpha_clip;                /* :52 */
+  int32_t independent_variance_samples; /* :53 */
+  int32_t non_zero_centred;             /* :54 (reserved; rejected) */
+  int32_t coord;                        /* :60 */
+  double converge_threshold;            /* :61 */
+  /* B200-only knobs (not in the reference) */
+  int32_t dtype;    /* mg_dtype of the device state/arithmetic; MG_F64 = parity mode */
+  int32_t rng;      /* mg_rng_kind */
+} mg_experiment_config;
+
+/* Fills the reference defaults (harness.hpp:18-67). */
+void mg_config_defaults(mg_experiment_config* cfg);
+/* ExperimentConfig::validate (harness.cpp:42-66): MG_EINVAL + message. */
+int mg_config_validate(const mg_experiment_config* cfg);
+
+const char* mg_last_error(void);
+int mg_abi_version(void);
+
+/* ---------------------------------------------------------------- context */
+typedef struct mg_ctx mg_ctx;
+/* stream: a cudaStream_t to adopt (not owned), or NULL to create one. */
+int mg_ctx_create(int device, void* stream, mg_ctx** out);
+int mg_ctx_destroy(mg_ctx* ctx);
+int mg_ctx_synchronize(mg_ctx* ctx);
+void* mg_ctx_stream(mg_ctx* ctx);
+/* Number of kernels this context has launched so far (bench gpu_launches). */
+int64_t mg_ctx_launch_count(mg_ctx* ctx);
+
+/* -------------------------------------------------- RNG streams (row A1) */
+/* mix64 splitmix64 finaliser (rng.hpp:9-14) — host helper. */
+uint64_t mg_mix64(uint64_t x);
+/* Replicate stream seed mix64(mix64(seed) ^ (r + 0x51ed2701e35f3a6d)) (rng.hpp:23-25). */
+uint64_t mg_stream_seed(uint64_t base_seed, uint64_t replicate);
+
+/* A batch of R independent std::mt19937_64 engines resident on the device
+ * (312 x u64 state each, SoA).  seeds[R] are ENGINE seeds (already mixed). */
+typedef struct mg_mt64 mg_mt64;
+int mg_mt64_create(mg_ctx* ctx, int32_t streams, const uint64_t* host_seeds, mg_mt64** out);
+int mg_mt64_destroy(mg_mt64* g);
+/* Draws n consecutive outputs from every stream into out[stream][n]:
+ * kind 0 = raw u64 (engine_()), 1 = uniform() double (rng.hpp:28),
+ * 2 = uniform_pos() double (rng.hpp:31). */
+int mg_mt64_draw(mg_ctx* ctx, mg_mt64* g, int64_t n, int32_t kind, void* out);
+
+/* ------------------------------------- fused estimator kernels (A8-A12) */
+/* Host-owned scalar state of one Moment2 (moment2.hpp:45-47).  The device
+ * only ever sees the per-step coefficient w/w_sum computed from it in fp64,
+ * exactly as moment2.hpp:35-38 does. */
+typedef struct mg_moment2_scalars {
+  double decay;
+  double decay_pow; /* decay^count by repeated multiplication (moment2.hpp:35) */
+  int64_t count;
+} mg_moment2_scalars;
+
+/* Moment2::step (moment2.hpp:30-39) on a device vector. */
+int mg_moment2_step(mg_ctx* ctx, int32_t dtype, int64_t n, mg_moment2_scalars* s, void* m2,
+                    const void* x);
+
+/* MetaEstimator hyper-parameters (meta.hpp:72-75). */
+typedef struct mg_meta_params {
+  double lr;
+  double eps_step;
+  double eps_alpha;
+  int32_t clip_enabled;
+} mg_meta_params;
+
+/* MetaEstimator::step (meta.hpp:90-113) on device buffers: updates mean, var,
+ * alpha_prev in place and writes delta.  first_call != 0 performs the lazy
+ * initialisation of meta.hpp:92-96 (mean=0, var=0, alpha_prev=-inf) first.
+ * Negative var_prop / var_diff -> MG_ELOGIC (meta.hpp:100-101); the check is
+ * a device reduction and this call synchronises the stream. */
+int mg_meta_step(mg_ctx* ctx, int32_t dtype, int64_t n, const mg_meta_params* p,
+                 int32_t first_call, void* mean, void* var, void* alpha_prev, const void* prop,
+                 const void* diff, const void* var_prop, const void* var_diff, void* delta);
+
+/* Adam::step (adam.hpp:23-37).  b1pow/b2pow/t live on the host like the
+ * reference's members (adam.hpp:47-48) and are advanced by this call. */
+typedef struct mg_adam_scalars {
+  double lr, beta1, beta2, eps;
+  double beta1_pow, beta2_pow;
+  int64_t t;
+} mg_adam_scalars;
+int mg_adam_step(mg_ctx* ctx, int32_t dtype, int64_t n, mg_adam_scalars* s, void* m, void* v,
+                 const void* grad, void* delta);
+
+/* ---------------------------------------------------------------------------
+ * The fused hot-path update: one HBM pass per iteration that does
+ *   Moment2(beta_f).step(prop)                         moment2.hpp:30-39, harness.cpp:144
+ *   global-norm diff decoupling + Moment2(beta_delta)  harness.cpp:153-157, meta.hpp:51-53
+ *   MetaEstimator::step                                meta.hpp:90-113
+ *   params += delta; project (max(p, lo) if enabled)   harness.cpp:182-188, problems.cpp:228
+ *   sum (p_new - p_old)^2  -> next iteration's step_sq_norm  (problems.cpp:214)
+ *   sum (p_new - target)^2 -> loss of the new params         (problems.cpp:225)
+ * The step_sq_norm that scales THIS step's diff is read from device memory
+ * (written by the previous step's reduction), so consecutive steps run with
+ * no host synchronisation and can be captured in a CUDA graph.  The diff-EMA
+ * count therefore lives on the device as well (it only advances when
+ * step_sq_norm > 0, harness.cpp:153).
+ * ------------------------------------------------------------------------- */
+typedef struct mg_update_scalars {
+  /* Reduced block, written by step t's epilogue for step t+1.  Plain element
+   * sums, contiguous, so a sharded step all-reduces them with one SUM. */
+  double ssn;       /* sum (p_new - p_old)^2 -> next step_sq_norm (problems.cpp:214) */
+  double changed;   /* count of p_new != p_old (problems.cpp:206, "same" test) */
+  double loss;      /* sum (p_new - target)^2 (problems.cpp:225), NaN without target */
+  double nonfinite; /* count of non-finite p_new (harness.cpp:116) */
+  /* Decoupled diff-EMA scalars (moment2.hpp:45-47), advanced on the device:
+   * the EMA only steps when step_sq_norm > 0 (harness.cpp:153). */
+  double diff_decay_pow;
+  int64_t diff_count;
+  /* What step t consumed, for recording (harness.cpp:174). */
+  double ssn_used;
+  double reserved;
+} mg_update_scalars;
+
+typedef struct mg_meta_update_args {
+  mg_meta_params meta;
+  double prop_coef;      /* (1-beta_f)/(1-beta_f^t), host fp64 (moment2.hpp:36-38) */
+  double beta_delta;     /* decay of the decoupled diff EMA (harness.hpp:28) */
+  int32_t first_step;    /* lazy init of Moment2 / MetaEstimator state (moment2.hpp:31, meta.hpp:92-96) */
+  int32_t diff_norm;     /* mg_diff_norm_kind (harness.cpp:146-158) */
+  int32_t project;       /* 1: p = max(p, proj_lo) (problems.cpp:228 uses 0.0) */
+  int32_t ssn_from_host; /* 1: step_sq_norm = ssn_host instead of scalars->ssn */
+  double proj_lo;
+  double ssn_host;
+} mg_meta_update_args;
+
+/* Optional side inputs/outputs of the fused update.  Any may be NULL. */
+typedef struct mg_meta_extras {
+  const void* vprop;       /* independent variance pair (harness.cpp:137-142) */
+  const void* vdiff;
+  const void* params_prev; /* pi_{t-1}, per-param diff norm only (harness.cpp:147) */
+  const void* target;      /* for the fused loss (problems.cpp:225) */
+  void* delta_out;         /* the step delta (harness.cpp:160) */
+} mg_meta_extras;
+
+/* One fused meta-estimator iteration over n parameters.
+ *   prop, diff            : this iteration's gradient sample pair (read)
+ *   m2_prop, m2_diff      : Moment2 states (read+write)
+ *   mean, var, alpha_prev : MetaEstimator state (read+write)
+ *   params_in             : pi_t (read);  params_out: pi_{t+1} (write; may == params_in)
+ *   scalars               : device mg_update_scalars (read ssn/diff state, write next)
+ *   x                     : optional extras (NULL for none)
+ * The host only supplies prop_coef (a pure function of the iteration count). */
+int mg_meta_update(mg_ctx* ctx, int32_t dtype, int64_t n, const mg_meta_update_args* a,
+                   const void* prop, const void* diff, void* m2_prop, void* m2_diff, void* mean,
+                   void* var, void* alpha_prev, const void* params_in, void* params_out,
+                   mg_update_scalars* scalars, const mg_meta_extras* x);
+
+/* Fused Adam baseline iteration (adam.hpp:23-37 + harness.cpp:165-166,
+ * 182-188): m, v updated, params_out = project(params_in + delta), with the
+ * same ssn/loss reductions into scalars. */
+int mg_adam_update(mg_ctx* ctx, int32_t dtype, int64_t n, mg_adam_scalars* s, int32_t project,
+                   double proj_lo, const void* grad, void* m, void* v, const void* params_in,
+                   void* params_out, const void* target, mg_update_scalars* scalars);
+
+/* Device -> host copy of a scalars block (synchronises the stream). */
+int mg_scalars_read(mg_ctx* ctx, const mg_update_scalars* dev, mg_update_scalars* host);
+int mg_scalars_write(mg_ctx* ctx, mg_update_scalars* dev, const mg_update_scalars* host);
+
+/* ------------------------------------ gradient-sample sources (A2-A7) */
+/* MiniRenderProblem (problems.hpp:157-195, problems.cpp:162-228).
+ * Construction draws b_j then T_j from Rng(mix64(gen_seed)) on the device
+ * (problems.cpp:168-172); out buffers are fp64 [P]. */
+int mg_minirender_generate(mg_ctx* ctx, int32_t pixel_count, uint64_t gen_seed, double exponent_max,
+                           double* exponents, double* target);
+
+/* MiniRenderProblem::sample_pair (problems.cpp:197-217) for R replicates at
+ * once.  Replicate r draws P*spp uniforms from stream r of g (pixel-major,
+ * problems.cpp:201-202), then per pixel computes kernel_terms (:177-195) and
+ *   prop = 2 a_now cross - 2 T mean_basis,  diff = 2 (a_now - a_prev) cross.
+ * now/prev/prop/diff are [R][P] of dtype; exponents/target fp64 [P] shared.
+ * ssn_out[R] (fp64, device) receives sum (a_now - a_prev)^2 (0 when equal).
+ * If now == prev bitwise for a replicate, diff = 0 and ssn = 0 exactly. */
+int mg_minirender_sample_pair(mg_ctx* ctx, int32_t dtype, int32_t replicates, int32_t pixel_count,
+                              int32_t spp, const double* exponents, const double* target,
+                              mg_mt64* g, const void* now, const void* prev, void* prop, void* diff,
+                              double* ssn_out);
+
+/* ExpRateProblem::sample_pair (problems.cpp:54-76), R replicates (dim 1).
+ * rate_now/rate_prev/prop/diff/ssn are fp64 [R].  Non-positive rates ->
+ * MG_EDOMAIN (synchronises). */
+int mg_exprate_sample_pair(mg_ctx* ctx, int32_t replicates, double target_mean,
+                           int32_t samples_per_iter, mg_mt64* g, const double* rate_now,
+                           const double* rate_prev, double* prop, double* diff, double* ssn);
+
+/* MultNoiseQuadratic::sample_pair (problems.cpp:121-139), R replicates,
+ * uniforms sample-major u[s*d+j].  All buffers fp64; target [d] shared,
+ * now/prev/prop/diff [R][d], ssn [R]. */
+int mg_multnoise_sample_pair(mg_ctx* ctx, int32_t replicates, int32_t dim, double sigma,
+                             int32_t samples_per_iter, const double* target, mg_mt64* g,
+                             const double* now, const double* prev, double* prop, double* diff,
+                             double* ssn);
+
+/* ------------------------------- device-resident run_single (A13, A14) */
+/* Per-replicate record of one coordinate plus scalars (harness.hpp:73-90;
+ * full vectors are O(iterations*N) and are not recorded on the device). */
+typedef struct mg_run_record {
+  int32_t iterations_run;
+  int32_t status;      /* 0 completed, 1 converged, 2 diverged (harness.hpp:74) */
+  int64_t draws_used;
+  int64_t evals_used;
+} mg_run_record;
+
+/* Series recorded per replicate per iteration, [R][iterations] fp64 each,
+ * for coordinate cfg->coord (harness.cpp:219-244 extractor set). */
+typedef struct mg_run_series {
+  double* param_err;   /* ||params - truth|| (harness.cpp:212-215) */
+  double* loss;
+  double* prop;
+  double* diff;
+  double* grad_est;    /* meta mean / Adam m_hat */
+  double* est_var;     /* meta var / Adam v_hat */
+  double* alpha;       /* meta only */
+  double* delta;
+  double* true_grad;
+  double* step_sq_norm;
+  double* param;       /* params[coord] */
+} mg_run_series;
+
+/* run_single for replicates [rep_begin, rep_begin + rep_count) of cfg, on the
+ * device, all replicates batched (harness.cpp:90-200 per replicate, the
+ * std::thread pool of harness.cpp:249-272 becomes the grid).  Host arrays:
+ * records[rep_count]; every non-NULL series pointer is a HOST array of
+ * rep_count*iterations doubles (entries past iterations_run are NaN).
+ * Optional final_params: host fp64 [rep_count][dim]. */
+int mg_run_replicates(mg_ctx* ctx, const mg_experiment_config* cfg, int32_t rep_begin,
+                      int32_t rep_count, mg_run_record* records, const mg_run_series* series,
+                      double* final_params);
+
+#ifdef __cplusplus
+}  /* extern "C" */
+#endif
+
+#endif /* MGCUDA_H_ */

@@ -1,0 +1,788 @@
+/*
+ * metagrad_oracle.c — CPU restatement (plain C, fp64, sequential) of the
+ * reference metagrad hot path.  TEST INFRASTRUCTURE ONLY: the checker for the
+ * CUDA path (see metagrad_oracle.h).  Pinned against tests/golden/, which
+ * oracle/gen_golden.py generates from the unmodified reference (oracle/_ref).
+ *
+ * Build: make -C oracle  (gcc -O2 -ffp-contract=off; no -march: the
+ * reference's Release build performs no FMA contraction).
+ */
+#include "metagrad_oracle.h"
+
+#include <math.h>
+#include <stdlib.h>
+#include <string.h>
+
+/* ------------------------------------------------------------------ RNG */
+
+/* rng.hpp:9-14 */
+uint64_t mgo_mix64(uint64_t x) {
+  x += 0x9e3779b97f4a7c15ULL;
+  x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ULL;
+  x = (x ^ (x >> 27)) * 0x94d049bb133111ebULL;
+  return x ^ (x >> 31);
+}
+
+/* std::mt19937_64 = mersenne_twister_engine<uint64_t, 64, 312, 156, 31,
+ * 0xb5026f5aa96619e9, 29, 0x5555555555555555, 17, 0x71d67fffeda60000, 37,
+ * 0xfff7eee000000000, 43, 6364136223846793005> (libstdc++ random.h:1620-1627).
+ * seed(): random.tcc:328-343; _M_gen_rand (twist): random.tcc:399;
+ * operator(): random.tcc:455-470. */
+enum { MT_N = 312, MT_M = 156 };
+#define MT_A 0xb5026f5aa96619e9ULL
+#define MT_UPPER 0xffffffff80000000ULL
+#define MT_LOWER 0x000000007fffffffULL
+
+void mgo_mt64_seed(mgo_mt64* g, uint64_t seed) {
+  g->mt[0] = seed;
+  for (int i = 1; i < MT_N; ++i) {
+    uint64_t x = g->mt[i - 1];
+    x ^= x >> 62;
+    g->mt[i] = 6364136223846793005ULL * x + (uint64_t)i;
+  }
+  g->idx = MT_N;
+}
+
+static void mt_twist(mgo_mt64* g) {
+  uint64_t* mt = g->mt;
+  for (int k = 0; k < MT_N; ++k) {
+    const uint64_t y = (mt[k] & MT_UPPER) | (mt[(k + 1) % MT_N] & MT_LOWER);
+    mt[k] = mt[(k + MT_M) % MT_N] ^ (y >> 1) ^ ((y & 1ULL) ? MT_A : 0ULL);
+  }
+  g->idx = 0;
+}
+
+uint64_t mgo_mt64_next(mgo_mt64* g) {
+  if (g->idx >= MT_N) mt_twist(g);
+  uint64_t z = g->mt[g->idx++];
+  z ^= (z >> 29) & 0x5555555555555555ULL;
+  z ^= (z << 17) & 0x71d67fffeda60000ULL;
+  z ^= (z << 37) & 0xfff7eee000000000ULL;
+  z ^= z >> 43;
+  return z;
+}
+
+/* rng.hpp:23-25 */
+void mgo_rng_stream(mgo_mt64* g, uint64_t base_seed, uint64_t replicate) {
+  mgo_mt64_seed(g, mgo_mix64(mgo_mix64(base_seed) ^ (replicate + 0x51ed2701e35f3a6dULL)));
+}
+
+/* rng.hpp:28 */
+double mgo_uniform(mgo_mt64* g) { return (double)(mgo_mt64_next(g) >> 11) * 0x1.0p-53; }
+/* rng.hpp:31 */
+double mgo_uniform_pos(mgo_mt64* g) { return 1.0 - mgo_uniform(g); }
+
+void mgo_rng_draws(uint64_t seed, uint64_t rep, int mode, int64_t n, void* out) {
+  mgo_mt64 g;
+  if (mode == 0 || mode == 4)
+    mgo_mt64_seed(&g, seed);
+  else
+    mgo_rng_stream(&g, seed, rep);
+  uint64_t* u = (uint64_t*)out;
+  double* d = (double*)out;
+  for (int64_t i = 0; i < n; ++i) {
+    if (mode == 0 || mode == 1)
+      u[i] = mgo_mt64_next(&g);
+    else if (mode == 2 || mode == 4)
+      d[i] = mgo_uniform(&g);
+    else
+      d[i] = mgo_uniform_pos(&g);
+  }
+}
+
+/* -------------------------------------------------------------- Moment2 */
+
+/* moment2.hpp:30-39: count++; decay_pow *= decay; m2 += (w/w_sum)*(x^2 - m2) */
+void mgo_moment2_step(int64_t n, double decay, double* decay_pow, int64_t* count, double* m2,
+                      const double* x) {
+  if (*count == 0) memset(m2, 0, (size_t)n * sizeof(double)); /* lazy Vec::Zero, :31 */
+  ++*count;
+  *decay_pow *= decay;
+  const double w = 1.0 - decay;
+  const double w_sum = 1.0 - *decay_pow;
+  const double c = w / w_sum;
+  for (int64_t i = 0; i < n; ++i) m2[i] = m2[i] + c * (x[i] * x[i] - m2[i]);
+}
+
+/* ---------------------------------------------------------- MetaEstimator */
+
+/* min(raw, 1/(2 - alpha_prev)) with std::min semantics (meta.hpp:30-32) */
+static inline double clip_alpha(double raw, double alpha_prev) {
+  const double bound = 1.0 / (2.0 - alpha_prev);
+  return (bound < raw) ? bound : raw;
+}
+
+/* meta.hpp:90-113 */
+int mgo_meta_step(int64_t n, double lr, double eps_step, double eps_alpha, int clip, int first_call,
+                  double* mean, double* var, double* alpha_prev, const double* prop,
+                  const double* diff, const double* var_prop, const double* var_diff,
+                  double* delta) {
+  if (first_call) {
+    for (int64_t i = 0; i < n; ++i) {
+      mean[i] = 0.0;
+      var[i] = 0.0;
+      alpha_prev[i] = -INFINITY;
+    }
+  }
+  for (int64_t i = 0; i < n; ++i)
+    if (var_prop[i] < 0.0 || var_diff[i] < 0.0) return MG_ELOGIC; /* :100-101 */
+  for (int64_t i = 0; i < n; ++i) {
+    double m = mean[i] + diff[i];  /* :103 */
+    double v = var[i] + var_diff[i]; /* :104 */
+    double a = var_prop[i] / ((var_prop[i] + v) + eps_alpha); /* :106 */
+    if (clip) a = clip_alpha(a, alpha_prev[i]);              /* :107 */
+    alpha_prev[i] = a;                                        /* :108 */
+    const double one_m = 1.0 - a;
+    m = a * m + one_m * prop[i];                     /* :110 */
+    v = (a * a) * v + (one_m * one_m) * var_prop[i]; /* :111 */
+    mean[i] = m;
+    var[i] = v;
+    delta[i] = ((-lr) * m) / (sqrt(v) + eps_step); /* :112 */
+  }
+  return 0;
+}
+
+/* ------------------------------------------------------------------- Adam */
+
+/* adam.hpp:23-37 */
+void mgo_adam_step(int64_t n, mg_adam_scalars* s, double* m, double* v, const double* grad,
+                   double* delta) {
+  if (s->t == 0) {
+    memset(m, 0, (size_t)n * sizeof(double));
+    memset(v, 0, (size_t)n * sizeof(double));
+  }
+  ++s->t;
+  s->beta1_pow *= s->beta1;
+  s->beta2_pow *= s->beta2;
+  const double c1 = 1.0 - s->beta1, c2 = 1.0 - s->beta2;
+  const double d1 = 1.0 - s->beta1_pow, d2 = 1.0 - s->beta2_pow;
+  for (int64_t i = 0; i < n; ++i) {
+    const double g = grad[i];
+    m[i] = s->beta1 * m[i] + c1 * g;
+    v[i] = s->beta2 * v[i] + c2 * (g * g);
+    const double mh = m[i] / d1, vh = v[i] / d2;
+    if (delta) delta[i] = ((-s->lr) * mh) / (sqrt(vh) + s->eps);
+  }
+}
+
+/* ---------------------------------------------- fused update iterations */
+
+/* The reduction epilogue shared by both fused updates (sequential order). */
+static void reduce_epilogue(int64_t n, const double* p_old, const double* p_new,
+                            const double* target, mg_update_scalars* sc) {
+  double ssn = 0.0, changed = 0.0, loss = 0.0, nonfinite = 0.0;
+  for (int64_t i = 0; i < n; ++i) {
+    const double d = p_new[i] - p_old[i];
+    ssn += d * d;                                    /* problems.cpp:214 */
+    changed += (p_new[i] != p_old[i]) ? 1.0 : 0.0;   /* problems.cpp:206 */
+    if (target) {
+      const double e = p_new[i] - target[i];
+      loss += e * e;                                 /* problems.cpp:225 */
+    }
+    nonfinite += isfinite(p_new[i]) ? 0.0 : 1.0;     /* harness.cpp:116 */
+  }
+  sc->ssn = ssn;
+  sc->changed = changed;
+  sc->loss = target ? loss : NAN;
+  sc->nonfinite = nonfinite;
+}
+
+/* harness.cpp:144 (Moment2 prop), :145-158 (diff decoupling), :160
+ * (MetaEstimator::step), :182-188 (update + projection). */
+int mgo_meta_update(int64_t n, const mg_meta_update_args* a, const double* prop, const double* diff,
+                    const double* vprop, const double* vdiff, double* m2_prop, double* m2_diff,
+                    double* mean, double* var, double* alpha_prev, const double* params_in,
+                    double* params_out, const double* params_prev, const double* target,
+                    mg_update_scalars* sc, double* delta_out) {
+  const double ssn = a->ssn_from_host ? a->ssn_host : sc->ssn;
+  const double* vp = vprop ? vprop : prop;
+  const double* vd = vdiff ? vdiff : diff;
+  const int per_param = a->diff_norm == MG_DIFF_NORM_PER_PARAM;
+  if (per_param && !params_prev) return MG_EINVAL;
+  /* diff EMA scalars (moment2.hpp:34-38), stepped only when ssn > 0 */
+  const int diff_active = ssn > 0.0;
+  const int64_t count_before = sc->diff_count;
+  double dpow = sc->diff_decay_pow;
+  int64_t dcount = sc->diff_count;
+  if (diff_active) {
+    ++dcount;
+    dpow *= a->beta_delta;
+  }
+  const double c_diff = (1.0 - a->beta_delta) / (1.0 - dpow);
+  const double norm = sqrt(ssn); /* harness.cpp:154: diff / std::sqrt(ssn) */
+  const double c_prop = a->prop_coef;
+  double* p_old = (double*)malloc((size_t)n * sizeof(double));
+  if (!p_old) return MG_ENOMEM;
+  memcpy(p_old, params_in, (size_t)n * sizeof(double));
+  for (int64_t i = 0; i < n; ++i) {
+    /* Moment2(beta_f).step(prop) (moment2.hpp:38) */
+    const double m2p_old = a->first_step ? 0.0 : m2_prop[i];
+    const double m2p = m2p_old + c_prop * (vp[i] * vp[i] - m2p_old);
+    m2_prop[i] = m2p;
+    /* decoupled diff variance (harness.cpp:146-157) */
+    double m2d = count_before > 0 ? m2_diff[i] : 0.0;
+    double var_diff = 0.0;
+    if (per_param) {
+      const double cs = fabs(params_in[i] - params_prev[i]);
+      if (diff_active) {
+        const double x = vd[i] / ((cs < 1e-150) ? 1e-150 : cs);
+        m2d = m2d + c_diff * (x * x - m2d);
+        m2_diff[i] = m2d;
+      }
+      if (dcount > 0) var_diff = m2d * (cs * cs);
+    } else {
+      if (diff_active) {
+        const double x = vd[i] / norm;
+        m2d = m2d + c_diff * (x * x - m2d);
+        m2_diff[i] = m2d;
+      }
+      if (dcount > 0) var_diff = m2d * ssn; /* rescale_diff_variance, meta.hpp:51-53 */
+    }
+    /* MetaEstimator::step (meta.hpp:103-112) */
+    double m = (a->first_step ? 0.0 : mean[i]) + diff[i];
+    double v = (a->first_step ? 0.0 : var[i]) + var_diff;
+    const double ap = a->first_step ? -INFINITY : alpha_prev[i];
+    double al = m2p / ((m2p + v) + a->meta.eps_alpha);
+    if (a->meta.clip_enabled) al = clip_alpha(al, ap);
+    alpha_prev[i] = al;
+    const double om = 1.0 - al;
+    m = al * m + om * prop[i];
+    v = (al * al) * v + (om * om) * m2p;
+    mean[i] = m;
+    var[i] = v;
+    const double delta = ((-a->meta.lr) * m) / (sqrt(v) + a->meta.eps_step);
+    if (delta_out) delta_out[i] = delta;
+    double p = params_in[i] + delta;
+    if (a->project) p = (p < a->proj_lo) ? a->proj_lo : p; /* std::max(p, lo) */
+    params_out[i] = p;
+  }
+  sc->ssn_used = ssn;
+  sc->diff_count = dcount;
+  sc->diff_decay_pow = dpow;
+  reduce_epilogue(n, p_old, params_out, target, sc);
+  free(p_old);
+  return 0;
+}
+
+void mgo_adam_update(int64_t n, mg_adam_scalars* s, int project, double proj_lo, const double* grad,
+                     double* m, double* v, const double* params_in, double* params_out,
+                     const double* target, mg_update_scalars* sc) {
+  double* delta = (double*)malloc((size_t)n * sizeof(double));
+  double* p_old = (double*)malloc((size_t)n * sizeof(double));
+  memcpy(p_old, params_in, (size_t)n * sizeof(double));
+  const double ssn = sc->ssn;
+  mgo_adam_step(n, s, m, v, grad, delta);
+  for (int64_t i = 0; i < n; ++i) {
+    double p = params_in[i] + delta[i];
+    if (project) p = (p < proj_lo) ? proj_lo : p;
+    params_out[i] = p;
+  }
+  sc->ssn_used = ssn;
+  reduce_epilogue(n, p_old, params_out, target, sc);
+  free(delta);
+  free(p_old);
+}
+
+/* ------------------------------------------------------------ problems */
+
+/* problems.cpp:162-173: gen = Rng(mix64(gen_seed)); all b_j, then all T_j */
+void mgo_minirender_generate(int32_t pixel_count, uint64_t gen_seed, double exponent_max,
+                             double* exponents, double* target) {
+  mgo_mt64 g;
+  mgo_mt64_seed(&g, mgo_mix64(gen_seed));
+  for (int32_t j = 0; j < pixel_count; ++j) exponents[j] = exponent_max * mgo_uniform(&g);
+  for (int32_t j = 0; j < pixel_count; ++j) target[j] = 0.2 + 0.8 * mgo_uniform(&g);
+}
+
+/* problems.cpp:177-195 */
+void mgo_minirender_kernel_terms(int32_t pixel_count, int32_t spp, const double* exponents,
+                                 const double* uniforms, double* cross, double* mean_basis) {
+  const double n = (double)spp;
+  for (int32_t j = 0; j < pixel_count; ++j) {
+    const double b = exponents[j];
+    double sum = 0.0, sum_sq = 0.0;
+    for (int32_t s = 0; s < spp; ++s) {
+      const double basis = (b + 1.0) * pow(uniforms[(size_t)j * spp + s], b);
+      sum += basis;
+      sum_sq += basis * basis;
+    }
+    cross[j] = (sum * sum - sum_sq) / (n * (n - 1.0));
+    mean_basis[j] = sum / n;
+  }
+}
+
+/* problems.cpp:197-217 */
+double mgo_minirender_sample_pair(int32_t pixel_count, int32_t spp, const double* exponents,
+                                  const double* target, mgo_mt64* g, const double* now,
+                                  const double* prev, double* prop, double* diff) {
+  const size_t draws = (size_t)pixel_count * (size_t)spp;
+  double* u = (double*)malloc(draws * sizeof(double));
+  double* cross = (double*)malloc((size_t)pixel_count * sizeof(double));
+  double* mb = (double*)malloc((size_t)pixel_count * sizeof(double));
+  for (size_t k = 0; k < draws; ++k) u[k] = mgo_uniform(g);
+  mgo_minirender_kernel_terms(pixel_count, spp, exponents, u, cross, mb);
+  int same = 1;
+  for (int32_t j = 0; j < pixel_count; ++j) same &= (now[j] == prev[j]);
+  double ssn = 0.0;
+  for (int32_t j = 0; j < pixel_count; ++j) {
+    prop[j] = (2.0 * now[j]) * cross[j] - (2.0 * target[j]) * mb[j]; /* :205 */
+    if (same) {
+      diff[j] = 0.0;
+    } else {
+      const double d = now[j] - prev[j];
+      diff[j] = (2.0 * d) * cross[j]; /* :213 */
+      ssn += d * d;                   /* :214 */
+    }
+  }
+  free(u);
+  free(cross);
+  free(mb);
+  return same ? 0.0 : ssn;
+}
+
+/* problems.cpp:44-52 */
+double mgo_exprate_gradient_from_batch(double target_mean, int32_t samples, double rate,
+                                       double sum_c, double sum_c_sq) {
+  const double n = (double)samples;
+  const double rate_sq = rate * rate;
+  return ((-2.0) * (sum_c * sum_c - sum_c_sq)) / (((n * (n - 1.0)) * rate_sq) * rate) +
+         ((2.0 * target_mean) * sum_c) / (n * rate_sq);
+}
+
+/* problems.cpp:54-76 (validate_params :91-94 first) */
+int mgo_exprate_sample_pair(double target_mean, int32_t samples, mgo_mt64* g, double rate_now,
+                            double rate_prev, double* prop, double* diff, double* ssn) {
+  if (!(rate_now > 0.0) || !(rate_prev > 0.0)) return MG_EDOMAIN;
+  double sum_c = 0.0, sum_c_sq = 0.0;
+  for (int32_t k = 0; k < samples; ++k) {
+    const double c = -log(mgo_uniform_pos(g));
+    sum_c += c;
+    sum_c_sq += c * c;
+  }
+  *prop = mgo_exprate_gradient_from_batch(target_mean, samples, rate_now, sum_c, sum_c_sq);
+  if (rate_now == rate_prev) {
+    *diff = 0.0;
+    *ssn = 0.0;
+  } else {
+    *diff = *prop - mgo_exprate_gradient_from_batch(target_mean, samples, rate_prev, sum_c, sum_c_sq);
+    *ssn = (rate_now - rate_prev) * (rate_now - rate_prev);
+  }
+  return 0;
+}
+
+/* problems.cpp:110-139 */
+double mgo_multnoise_sample_pair(int32_t dim, double sigma, int32_t samples,
+                                 const double* target, mgo_mt64* g, const double* now,
+                                 const double* prev, double* prop, double* diff) {
+  const size_t draws = (size_t)dim * (size_t)samples;
+  double* u = (double*)malloc(draws * sizeof(double));
+  double* f = (double*)calloc((size_t)dim, sizeof(double));
+  for (size_t k = 0; k < draws; ++k) u[k] = mgo_uniform(g);
+  for (int32_t s = 0; s < samples; ++s)
+    for (int32_t j = 0; j < dim; ++j)
+      f[j] += 1.0 + sigma * (2.0 * u[(size_t)s * dim + j] - 1.0);
+  for (int32_t j = 0; j < dim; ++j) f[j] = f[j] / (double)samples;
+  int same = 1;
+  for (int32_t j = 0; j < dim; ++j) same &= (now[j] == prev[j]);
+  double ssn = 0.0;
+  for (int32_t j = 0; j < dim; ++j) {
+    prop[j] = (now[j] - target[j]) * f[j];
+    if (same) {
+      diff[j] = 0.0;
+    } else {
+      const double d = now[j] - prev[j];
+      diff[j] = d * f[j];
+      ssn += d * d;
+    }
+  }
+  free(u);
+  free(f);
+  return same ? 0.0 : ssn;
+}
+
+/* ---------------------------------------------------------- run_single */
+
+int mgo_problem_dim(const mg_experiment_config* cfg) {
+  switch (cfg->problem) {
+    case MG_EXP_RATE: return 1;
+    case MG_MULT_NOISE: return cfg->dim;
+    case MG_MINI_RENDER: return cfg->pixel_count;
+  }
+  return -1;
+}
+
+typedef struct problem_state {
+  int kind;
+  int dim;
+  int64_t draws_per_sample;
+  double* target; /* truth: exp-rate 1/target_mean, mult-noise target, mini-render T */
+  double* exponents;
+  double* init;
+} problem_state;
+
+static int problem_init(const mg_experiment_config* cfg, problem_state* p) {
+  memset(p, 0, sizeof(*p));
+  p->kind = cfg->problem;
+  p->dim = mgo_problem_dim(cfg);
+  if (p->dim < 1) return MG_EINVAL;
+  p->target = (double*)calloc((size_t)p->dim, sizeof(double));
+  p->init = (double*)calloc((size_t)p->dim, sizeof(double));
+  switch (p->kind) {
+    case MG_EXP_RATE: /* problems.cpp:30-42 */
+      if (!(cfg->target_mean > 0.0) || cfg->samples_per_iter < 2 || !(cfg->rate_init > 0.0))
+        return MG_EINVAL;
+      p->target[0] = 1.0 / cfg->target_mean;
+      p->init[0] = cfg->rate_init;
+      p->draws_per_sample = cfg->samples_per_iter;
+      break;
+    case MG_MULT_NOISE: /* problems.cpp:99-108, harness.cpp:71-73 (target 0) */
+      if (cfg->sigma < 0.0 || cfg->samples_per_iter < 1) return MG_EINVAL;
+      for (int j = 0; j < p->dim; ++j) p->init[j] = p->target[j] + 2.0;
+      p->draws_per_sample = (int64_t)cfg->samples_per_iter * p->dim;
+      break;
+    case MG_MINI_RENDER: /* problems.cpp:162-175 */
+      if (cfg->spp < 2 || !(cfg->exponent_max >= 0.0)) return MG_EINVAL;
+      p->exponents = (double*)calloc((size_t)p->dim, sizeof(double));
+      mgo_minirender_generate(p->dim, cfg->problem_seed, cfg->exponent_max, p->exponents, p->target);
+      for (int j = 0; j < p->dim; ++j) p->init[j] = cfg->albedo_init;
+      p->draws_per_sample = (int64_t)cfg->pixel_count * cfg->spp;
+      break;
+    default:
+      return MG_EINVAL;
+  }
+  return 0;
+}
+
+static void problem_free(problem_state* p) {
+  free(p->target);
+  free(p->exponents);
+  free(p->init);
+}
+
+/* returns 0 or MG_EDOMAIN; fills prop/diff, returns ssn via *ssn */
+static int problem_sample(const mg_experiment_config* cfg, const problem_state* p, mgo_mt64* g,
+                          const double* now, const double* prev, double* prop, double* diff,
+                          double* ssn) {
+  switch (p->kind) {
+    case MG_EXP_RATE:
+      return mgo_exprate_sample_pair(cfg->target_mean, cfg->samples_per_iter, g, now[0], prev[0],
+                                     prop, diff, ssn);
+    case MG_MULT_NOISE:
+      *ssn = mgo_multnoise_sample_pair(p->dim, cfg->sigma, cfg->samples_per_iter, p->target, g, now,
+                                       prev, prop, diff);
+      return 0;
+    default:
+      *ssn = mgo_minirender_sample_pair(p->dim, cfg->spp, p->exponents, p->target, g, now, prev,
+                                        prop, diff);
+      return 0;
+  }
+}
+
+/* problems.cpp:84-87, :146-149, :223-226 */
+static double problem_loss(const problem_state* p, const mg_experiment_config* cfg,
+                           const double* x) {
+  if (p->kind == MG_EXP_RATE) {
+    const double err = 1.0 / x[0] - cfg->target_mean;
+    return err * err;
+  }
+  double s = 0.0;
+  for (int j = 0; j < p->dim; ++j) {
+    const double d = x[j] - p->target[j];
+    s += d * d;
+  }
+  return p->kind == MG_MULT_NOISE ? 0.5 * s : s;
+}
+
+/* problems.cpp:78-82, :141-144, :219-222 */
+static void problem_true_grad(const problem_state* p, const mg_experiment_config* cfg,
+                              const double* x, double* g) {
+  if (p->kind == MG_EXP_RATE) {
+    const double r = x[0];
+    g[0] = (2.0 * (1.0 / r - cfg->target_mean)) * (-1.0 / (r * r));
+    return;
+  }
+  for (int j = 0; j < p->dim; ++j) {
+    const double d = x[j] - p->target[j];
+    g[j] = p->kind == MG_MULT_NOISE ? d : 2.0 * d;
+  }
+}
+
+/* problems.cpp:89, :228 (mult-noise: identity) */
+static void problem_project(const problem_state* p, double* x) {
+  if (p->kind == MG_EXP_RATE) {
+    x[0] = (x[0] < 1e-4) ? 1e-4 : x[0];
+  } else if (p->kind == MG_MINI_RENDER) {
+    for (int j = 0; j < p->dim; ++j) x[j] = (x[j] < 0.0) ? 0.0 : x[j];
+  }
+}
+
+/* TrajectorySchedule::at (problems.hpp:207-215), from = init, to = truth */
+static void schedule_at(const mg_experiment_config* cfg, const problem_state* p, int i,
+                        double* out) {
+  const int horizon = cfg->iterations;
+  int clamped = i < horizon - 1 ? i : horizon - 1;
+  if (clamped < 0) clamped = 0;
+  if (cfg->trajectory == MG_TRAJ_SCRIPTED_LINEAR) {
+    const double f = horizon <= 1 ? 1.0 : (double)clamped / (double)(horizon - 1);
+    for (int j = 0; j < p->dim; ++j) out[j] = p->init[j] + (p->target[j] - p->init[j]) * f;
+  } else {
+    const double e = exp(-cfg->traj_rate * (double)clamped);
+    for (int j = 0; j < p->dim; ++j) out[j] = p->target[j] + (p->init[j] - p->target[j]) * e;
+  }
+}
+
+int mg_config_validate_oracle(const mg_experiment_config* c); /* below */
+
+int mg_config_validate_oracle(const mg_experiment_config* c) {
+  /* harness.cpp:42-66 */
+  if (c->problem < 0 || c->problem > 2) return MG_EINVAL;
+  if (c->optimizer < 0 || c->optimizer > 1) return MG_EINVAL;
+  if (c->trajectory < 0 || c->trajectory > 2) return MG_EINVAL;
+  if (c->diff_norm < 0 || c->diff_norm > 1) return MG_EINVAL;
+  if (c->iterations < 1 || c->replicates < 1) return MG_EINVAL;
+  if (!(c->lr > 0.0)) return MG_EINVAL;
+  if (!(c->beta_f >= 0.0 && c->beta_f < 1.0)) return MG_EINVAL;
+  if (!(c->beta_delta >= 0.0 && c->beta_delta < 1.0)) return MG_EINVAL;
+  if (!(c->beta1 >= 0.0 && c->beta1 < 1.0)) return MG_EINVAL;
+  if (!(c->beta2 >= 0.0 && c->beta2 < 1.0)) return MG_EINVAL;
+  if (c->coord < 0) return MG_EINVAL;
+  if (c->non_zero_centred) return MG_EINVAL;
+  return 0;
+}
+
+typedef struct iter_out {
+  double loss, ssn;
+  const double *params, *prop, *diff, *mean_est, *var_est, *alpha, *delta, *true_grad;
+} iter_out;
+
+typedef void (*record_fn)(void* ctx, int i, const iter_out* o, int dim);
+
+/* harness.cpp:90-200 */
+static int run_single_impl(const mg_experiment_config* cfg, int32_t replicate, mg_run_record* rec,
+                           record_fn record, void* rctx, double* final_params) {
+  int st = mg_config_validate_oracle(cfg);
+  if (st) return st;
+  problem_state p;
+  st = problem_init(cfg, &p);
+  if (st) {
+    problem_free(&p);
+    return st;
+  }
+  const int d = p.dim;
+  if (cfg->coord >= d) {
+    problem_free(&p);
+    return MG_EINVAL;
+  }
+  mgo_mt64 rng;
+  mgo_rng_stream(&rng, cfg->seed, (uint64_t)replicate);
+  const int scripted = cfg->trajectory != MG_TRAJ_OPTIMISE;
+  const int use_meta = cfg->optimizer == MG_OPT_META;
+  const size_t vb = (size_t)d * sizeof(double);
+  double* params = malloc(vb);
+  double* prev = malloc(vb);
+  double* prop = malloc(vb);
+  double* diff = malloc(vb);
+  double* iprop = malloc(vb);
+  double* idiff = malloc(vb);
+  double* m2p = calloc((size_t)d, sizeof(double));
+  double* m2d = calloc((size_t)d, sizeof(double));
+  double* mean = calloc((size_t)d, sizeof(double));
+  double* var = calloc((size_t)d, sizeof(double));
+  double* ap = calloc((size_t)d, sizeof(double));
+  double* am = calloc((size_t)d, sizeof(double));
+  double* av = calloc((size_t)d, sizeof(double));
+  double* delta = malloc(vb);
+  double* mest = malloc(vb);
+  double* vest = malloc(vb);
+  double* var_diff = malloc(vb);
+  double* tg = malloc(vb);
+  double* xs = malloc(vb);
+  if (scripted)
+    schedule_at(cfg, &p, 0, params);
+  else
+    memcpy(params, p.init, vb);
+  memcpy(prev, params, vb);
+  double pf_pow = 1.0, pd_pow = 1.0;
+  int64_t pf_cnt = 0, pd_cnt = 0;
+  mg_adam_scalars as = {cfg->lr, cfg->beta1, cfg->beta2, cfg->adam_eps, 1.0, 1.0, 0};
+  int meta_first = 1;
+  memset(rec, 0, sizeof(*rec));
+  rec->status = 0;
+  int err = 0;
+  for (int i = 0; i < cfg->iterations; ++i) {
+    int finite = 1;
+    for (int j = 0; j < d; ++j) finite &= isfinite(params[j]) ? 1 : 0;
+    if (!finite) { /* :116-119 */
+      rec->status = 2;
+      break;
+    }
+    double ssn = 0.0;
+    st = problem_sample(cfg, &p, &rng, params, use_meta ? prev : params, prop, diff, &ssn);
+    if (st == MG_EDOMAIN) { /* :125-128 */
+      rec->status = 2;
+      break;
+    }
+    int same = 1;
+    for (int j = 0; j < d; ++j) same &= (params[j] == prev[j]);
+    const int two_point = use_meta && !same; /* :129 */
+    rec->draws_used += p.draws_per_sample;
+    rec->evals_used += p.draws_per_sample * (two_point ? 2 : 1);
+    const double* alpha_rec = NULL;
+    if (use_meta) {
+      const double* vp = prop;
+      const double* vd = diff;
+      double vssn = ssn;
+      if (cfg->independent_variance_samples) { /* :137-142 */
+        st = problem_sample(cfg, &p, &rng, params, prev, iprop, idiff, &vssn);
+        if (st == MG_EDOMAIN) {
+          rec->status = 2;
+          break;
+        }
+        rec->draws_used += p.draws_per_sample;
+        rec->evals_used += p.draws_per_sample * (two_point ? 2 : 1);
+        vp = iprop;
+        vd = idiff;
+      }
+      mgo_moment2_step(d, cfg->beta_f, &pf_pow, &pf_cnt, m2p, vp); /* :144 */
+      if (cfg->diff_norm == MG_DIFF_NORM_PER_PARAM) {            /* :146-151 */
+        for (int j = 0; j < d; ++j) {
+          const double cs = fabs(params[j] - prev[j]);
+          xs[j] = cs; /* coord_step */
+        }
+        if (vssn > 0.0) {
+          double* x = malloc(vb);
+          for (int j = 0; j < d; ++j) x[j] = vd[j] / ((xs[j] < 1e-150) ? 1e-150 : xs[j]);
+          mgo_moment2_step(d, cfg->beta_delta, &pd_pow, &pd_cnt, m2d, x);
+          free(x);
+        }
+        for (int j = 0; j < d; ++j) var_diff[j] = pd_cnt > 0 ? m2d[j] * (xs[j] * xs[j]) : 0.0;
+      } else { /* :153-157 */
+        if (vssn > 0.0) {
+          double* x = malloc(vb);
+          const double s = sqrt(vssn);
+          for (int j = 0; j < d; ++j) x[j] = vd[j] / s;
+          mgo_moment2_step(d, cfg->beta_delta, &pd_pow, &pd_cnt, m2d, x);
+          free(x);
+        }
+        for (int j = 0; j < d; ++j) var_diff[j] = pd_cnt > 0 ? m2d[j] * ssn : 0.0;
+      }
+      st = mgo_meta_step(d, cfg->lr, cfg->eps_step, cfg->eps_alpha, !cfg->no_alpha_clip, meta_first,
+                         mean, var, ap, prop, diff, m2p, var_diff, delta); /* :160 */
+      meta_first = 0;
+      if (st) {
+        err = st;
+        break;
+      }
+      memcpy(mest, mean, vb);
+      memcpy(vest, var, vb);
+      alpha_rec = ap;
+    } else { /* :165-167 */
+      mgo_adam_step(d, &as, am, av, prop, delta);
+      for (int j = 0; j < d; ++j) {
+        mest[j] = am[j] / (1.0 - as.beta1_pow); /* adam.hpp:42 */
+        vest[j] = av[j] / (1.0 - as.beta2_pow); /* adam.hpp:43 */
+      }
+    }
+    problem_true_grad(&p, cfg, params, tg);
+    iter_out o = {problem_loss(&p, cfg, params), ssn, params, prop, diff, mest, vest, alpha_rec, delta, tg};
+    if (record) record(rctx, i, &o, d);
+    rec->iterations_run = i + 1;
+    memcpy(prev, params, vb); /* :182 */
+    if (scripted) {
+      schedule_at(cfg, &p, i + 1, params);
+    } else {
+      for (int j = 0; j < d; ++j) params[j] = params[j] + delta[j];
+      problem_project(&p, params);
+    }
+  }
+  if (!err && rec->status != 2 && cfg->converge_threshold > 0.0 && rec->iterations_run > 0) {
+    /* :191-198: err = ||rec.params.back() - truth|| */
+    double s = 0.0;
+    for (int j = 0; j < d; ++j) {
+      const double e = prev[j] - p.target[j];
+      s += e * e;
+    }
+    if (sqrt(s) < cfg->converge_threshold) rec->status = 1;
+  }
+  if (final_params) memcpy(final_params, prev, vb); /* last recorded params */
+  free(params); free(prev); free(prop); free(diff); free(iprop); free(idiff);
+  free(m2p); free(m2d); free(mean); free(var); free(ap); free(am); free(av);
+  free(delta); free(mest); free(vest); free(var_diff); free(tg); free(xs);
+  problem_free(&p);
+  return err;
+}
+
+typedef struct full_ctx {
+  const mgo_full_record* out;
+} full_ctx;
+
+static void put_vec(double* base, int i, int d, const double* v) {
+  if (base && v) memcpy(base + (size_t)i * d, v, (size_t)d * sizeof(double));
+}
+
+static void record_full(void* c, int i, const iter_out* o, int d) {
+  const mgo_full_record* r = ((full_ctx*)c)->out;
+  put_vec(r->params, i, d, o->params);
+  if (r->loss) r->loss[i] = o->loss;
+  put_vec(r->prop, i, d, o->prop);
+  put_vec(r->diff, i, d, o->diff);
+  if (r->ssn) r->ssn[i] = o->ssn;
+  put_vec(r->mean_est, i, d, o->mean_est);
+  put_vec(r->var_est, i, d, o->var_est);
+  put_vec(r->alpha, i, d, o->alpha);
+  put_vec(r->delta, i, d, o->delta);
+  put_vec(r->true_grad, i, d, o->true_grad);
+}
+
+int mgo_run_single(const mg_experiment_config* cfg, int32_t replicate, mg_run_record* rec,
+                   const mgo_full_record* out) {
+  full_ctx c = {out};
+  return run_single_impl(cfg, replicate, rec, out ? record_full : NULL, &c, NULL);
+}
+
+typedef struct series_ctx {
+  const mg_run_series* s;
+  int32_t stride;
+  int coord;
+  const double* truth;
+  int has_truth;
+} series_ctx;
+
+static void record_series(void* c, int i, const iter_out* o, int d) {
+  const series_ctx* sc = (const series_ctx*)c;
+  const mg_run_series* s = sc->s;
+  const int k = sc->coord;
+  const size_t at = (size_t)i * (size_t)sc->stride;
+  if (s->param_err) {
+    double acc = 0.0;
+    for (int j = 0; j < d; ++j) {
+      const double e = o->params[j] - sc->truth[j];
+      acc += e * e;
+    }
+    s->param_err[at] = sqrt(acc);
+  }
+  if (s->loss) s->loss[at] = o->loss;
+  if (s->prop) s->prop[at] = o->prop[k];
+  if (s->diff) s->diff[at] = o->diff[k];
+  if (s->grad_est) s->grad_est[at] = o->mean_est[k];
+  if (s->est_var) s->est_var[at] = o->var_est[k];
+  if (s->alpha) s->alpha[at] = o->alpha ? o->alpha[k] : NAN;
+  if (s->delta) s->delta[at] = o->delta[k];
+  if (s->true_grad) s->true_grad[at] = o->true_grad[k];
+  if (s->step_sq_norm) s->step_sq_norm[at] = o->ssn;
+  if (s->param) s->param[at] = o->params[k];
+}
+
+int mgo_run_single_series(const mg_experiment_config* cfg, int32_t replicate, mg_run_record* rec,
+                          const mg_run_series* series, int32_t stride, double* final_params) {
+  problem_state p;
+  int st = problem_init(cfg, &p);
+  if (st) {
+    problem_free(&p);
+    return st;
+  }
+  series_ctx c = {series, stride, cfg->coord, p.target, 1};
+  st = run_single_impl(cfg, replicate, rec, record_series, &c, final_params);
+  problem_free(&p);
+  return st;
+}

@@ -1,0 +1,120 @@
+/*
+ * metagrad_oracle.h — CPU restatement of the reference hot path (fp64).
+ *
+ * TEST INFRASTRUCTURE ONLY.  This is the parity checker for the CUDA path:
+ * only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline leg may
+ * load it.  It is pinned against golden vectors produced by the UNMODIFIED
+ * reference (oracle/_ref, built by oracle/ref/Makefile; fixtures in
+ * tests/golden/, generator oracle/gen_golden.py).
+ *
+ * Every function cites the reference file:line it restates (paths relative
+ * to /root/reference/proj).  Compiled with -ffp-contract=off so each a*b+c is
+ * two roundings, as in the reference's Release build.
+ */
+#ifndef METAGRAD_ORACLE_H_
+#define METAGRAD_ORACLE_H_
+
+#include <stdint.h>
+
+#include "../include/mgcuda.h" /* mg_experiment_config layout only */
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* std::mt19937_64 (rng.hpp:36; libstdc++ random.h:1620-1627, random.tcc:328-470) */
+typedef struct mgo_mt64 {
+  uint64_t mt[312];
+  int idx;
+} mgo_mt64;
+
+uint64_t mgo_mix64(uint64_t x);
+void mgo_mt64_seed(mgo_mt64* g, uint64_t seed);
+uint64_t mgo_mt64_next(mgo_mt64* g);
+void mgo_rng_stream(mgo_mt64* g, uint64_t base_seed, uint64_t replicate);
+double mgo_uniform(mgo_mt64* g);
+double mgo_uniform_pos(mgo_mt64* g);
+/* same modes as ref_rng_draws (oracle/ref/ref_capi.cpp) */
+void mgo_rng_draws(uint64_t seed, uint64_t rep, int mode, int64_t n, void* out);
+
+/* Moment2 (moment2.hpp:21-50) */
+void mgo_moment2_step(int64_t n, double decay, double* decay_pow, int64_t* count, double* m2,
+                      const double* x);
+
+/* MetaEstimator::step (meta.hpp:90-113); returns 0, 1 (invalid_argument) or
+ * 2 (logic_error). first_call performs the lazy init (:92-96). */
+int mgo_meta_step(int64_t n, double lr, double eps_step, double eps_alpha, int clip, int first_call,
+                  double* mean, double* var, double* alpha_prev, const double* prop,
+                  const double* diff, const double* var_prop, const double* var_diff,
+                  double* delta);
+
+/* Adam::step (adam.hpp:23-37); s->beta*_pow and t advanced. */
+void mgo_adam_step(int64_t n, mg_adam_scalars* s, double* m, double* v, const double* grad,
+                   double* delta);
+
+/* One fused meta-estimator iteration, the same computation as
+ * mg_meta_update (include/mgcuda.h) in fp64 sequential order:
+ * harness.cpp:144,153-157,160,182-188 + problems.cpp:214,225,228.
+ * vprop/vdiff/target/prev may be NULL.  Returns 0 or an mg_status. */
+int mgo_meta_update(int64_t n, const mg_meta_update_args* a, const double* prop, const double* diff,
+                    const double* vprop, const double* vdiff, double* m2_prop, double* m2_diff,
+                    double* mean, double* var, double* alpha_prev, const double* params_in,
+                    double* params_out, const double* params_prev, const double* target,
+                    mg_update_scalars* sc, double* delta_out);
+
+/* Fused Adam iteration (mg_adam_update). */
+void mgo_adam_update(int64_t n, mg_adam_scalars* s, int project, double proj_lo, const double* grad,
+                     double* m, double* v, const double* params_in, double* params_out,
+                     const double* target, mg_update_scalars* sc);
+
+/* MiniRenderProblem (problems.cpp:162-228) */
+void mgo_minirender_generate(int32_t pixel_count, uint64_t gen_seed, double exponent_max,
+                             double* exponents, double* target);
+void mgo_minirender_kernel_terms(int32_t pixel_count, int32_t spp, const double* exponents,
+                                 const double* uniforms, double* cross, double* mean_basis);
+/* draws P*spp uniforms from g; returns step_sq_norm */
+double mgo_minirender_sample_pair(int32_t pixel_count, int32_t spp, const double* exponents,
+                                  const double* target, mgo_mt64* g, const double* now,
+                                  const double* prev, double* prop, double* diff);
+
+/* ExpRateProblem (problems.cpp:30-94) */
+double mgo_exprate_gradient_from_batch(double target_mean, int32_t n, double rate, double sum_c,
+                                       double sum_c_sq);
+/* returns 0 or MG_EDOMAIN */
+int mgo_exprate_sample_pair(double target_mean, int32_t samples_per_iter, mgo_mt64* g,
+                            double rate_now, double rate_prev, double* prop, double* diff,
+                            double* ssn);
+
+/* MultNoiseQuadratic (problems.cpp:99-157) */
+double mgo_multnoise_sample_pair(int32_t dim, double sigma, int32_t samples_per_iter,
+                                 const double* target, mgo_mt64* g, const double* now,
+                                 const double* prev, double* prop, double* diff);
+
+/* run_single (harness.cpp:90-200) with full per-iteration vectors.
+ * Any output may be NULL; vector outputs are [iterations][dim].
+ * Returns 0 or an mg_status (config errors).  rec gets status/counters. */
+typedef struct mgo_full_record {
+  double* params;
+  double* loss;
+  double* prop;
+  double* diff;
+  double* ssn;
+  double* mean_est;
+  double* var_est;
+  double* alpha;
+  double* delta;
+  double* true_grad;
+} mgo_full_record;
+
+int mgo_problem_dim(const mg_experiment_config* cfg);
+int mgo_run_single(const mg_experiment_config* cfg, int32_t replicate, mg_run_record* rec,
+                   const mgo_full_record* out);
+/* run_single reduced to the device runner's coordinate series (mg_run_series). */
+int mgo_run_single_series(const mg_experiment_config* cfg, int32_t replicate, mg_run_record* rec,
+                          const mg_run_series* series, int32_t stride, double* final_params);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif
