@@ -1,0 +1,360 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 hot path: BASELINE.json configs[1], the fused
+meta-estimator update (Moment2 x2 + decoupled diff variance + MetaEstimator
+step + parameter update + step-norm/loss reductions, harness.cpp:144-188).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--n PARAMS] [--impl ours|reference]
+
+One step = one mg_meta_update over N fp32 parameters per GPU with the state
+carried across steps (weak scaling: every rank owns N parameters of one
+logical parameter vector; the global step norm / loss are all-reduced with
+NCCL each step, on the device, because the diff decoupling of the next step
+needs the GLOBAL ||delta pi||^2, problems.cpp:214 / SPEC.md:131).
+
+Inputs: prop ~ N(mu_i, sigma_i^2), diff ~ N(0, (0.1 sigma_i)^2), mu_i ~ U(-1,1),
+sigma_i ~ U(0.1, 2) (seeded synthetic, BASELINE.json configs[1]); a pool of 4
+batches resident in HBM (2 x 4 x N bytes each, far larger than L2, so no L2
+flush is needed) cycled over the steps.  The timed region contains only the
+update kernels (and the scalar all-reduce for N>1).
+"""
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "gradient samples/sec (prop+FD pairs) & optimisation iterations/sec vs roofline"
+UNIT = "pairs/s"
+BYTES_PER_PARAM = {"f32": 56, "f64": 112}  # 8 streams read + 6 written
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--n", type=int, default=1 << 28, help="parameters per GPU")
+    ap.add_argument("--dtype", default="f32", choices=["f32", "f64"])
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--pool", type=int, default=4)
+    ap.add_argument("--e2e-steps", type=int, default=None)
+    ap.add_argument("--cpu-n", type=int, default=1 << 22, help="reference sample size")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--extras", action="store_true", help="also time Adam and the mini-render runner")
+    return ap.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", str(rank)))
+    return rank, world, local
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device):
+        self.device = device
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = threading.Thread(target=self._run, daemon=True)
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True,
+                                     text=True, timeout=5).stdout.strip()
+                if out:
+                    self.samples.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = sorted(float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit())
+        mx = max(float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit())
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4)
+                          if len(s) > 2 + i and s[2 + i].lower() == "active"})
+        return {"sm_mhz": sm[len(sm) // 2] if sm else None, "sm_max_mhz": mx,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+def measured_peak():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+# --------------------------------------------------------------- reference
+def cpu_reference(n, steps, threads, pool=2, seed=0):
+    """Times the UNMODIFIED reference (oracle/_ref) meta update: Moment2 x2 +
+    diff decoupling + MetaEstimator::step + params += delta, fp64."""
+    import numpy as np
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    from oracle_bind import RefLib, ref_available
+    rs = np.random.RandomState(seed)
+    mu = rs.uniform(-1, 1, n)
+    sig = rs.uniform(0.1, 2.0, n)
+    props = np.stack([mu + sig * rs.standard_normal(n) for _ in range(pool)])
+    diffs = np.stack([0.1 * sig * rs.standard_normal(n) for _ in range(pool)])
+    if ref_available():
+        sec = RefLib().meta_update_bench(props, diffs, 1e-4, steps, threads)
+        kind = "reference"
+    else:  # the C restatement of the same algorithm
+        raise RuntimeError("oracle/_ref not built (make -C oracle/ref)")
+    return n / sec, sec, kind
+
+
+def run_reference_arm(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return 0
+    threads = os.cpu_count() or 1
+    n = args.cpu_n
+    t0 = time.time()
+    val, sec, kind = cpu_reference(n, max(args.steps, 3), threads)
+    line = {
+        "metric": METRIC, "value": val, "unit": UNIT, "impl": "reference", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": sec * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic", "config": {"workload": "meta-update-microbench (BASELINE configs[1])",
+                                        "params_per_step": n, "precision": "fp64 (reference)"},
+        "cpu_baseline": {"value": val, "unit": UNIT, "cores": threads, "kind": kind,
+                         "sample": f"{n} params/step, median of {max(args.steps, 3)} steps, "
+                                   f"{threads} std::threads over contiguous chunks"},
+        "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "wall_s": time.time() - t0,
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# -------------------------------------------------------------------- ours
+def run_ours(args):
+    import torch
+    from paper_2309_15676_b200 import api
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    pg = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+        pg = dist
+    ctx = api.Context(local)
+    stream = ctx.stream
+    n = args.n
+    dt = torch.float32 if args.dtype == "f32" else torch.float64
+
+    # ---- synthetic inputs (untimed), BASELINE.json configs[1]
+    g = torch.Generator(device=dev)
+    g.manual_seed(1000 + rank)
+    mu = torch.rand(n, device=dev, dtype=dt, generator=g) * 2 - 1
+    sig = torch.rand(n, device=dev, dtype=dt, generator=g) * 1.9 + 0.1
+    props = [mu + sig * torch.randn(n, device=dev, dtype=dt, generator=g) for _ in range(args.pool)]
+    diffs = [0.1 * sig * torch.randn(n, device=dev, dtype=dt, generator=g) for _ in range(args.pool)]
+    zero_diff = torch.zeros(n, device=dev, dtype=dt)
+    del mu
+    pa = torch.zeros(n, device=dev, dtype=dt)
+    pb = torch.empty_like(pa)
+    upd = api.FusedMetaUpdate(n, dtype=dt, lr=0.01, beta_f=0.9, beta_delta=0.5, ctx=ctx)
+    torch.cuda.synchronize()
+
+    sc = upd.scalars_buf  # 4 reducible doubles first
+
+    def step(t):
+        src, dst = (pa, pb) if t % 2 == 0 else (pb, pa)
+        d = zero_diff if t == 0 else diffs[t % args.pool]
+        upd.step(props[t % args.pool], d, src, dst)
+        if pg is not None:  # global ||dpi||^2, #changed, loss, #nonfinite
+            pg.all_reduce(sc[:4])
+
+    t = 0
+    for _ in range(args.warmup):
+        step(t)
+        t += 1
+    torch.cuda.synchronize()
+    if pg is not None:
+        pg.barrier()
+    launches0 = ctx.launches
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        e0.record(stream)
+        for _ in range(args.steps):
+            step(t)
+            t += 1
+        e1.record(stream)
+        torch.cuda.synchronize()
+    if pg is not None:
+        pg.barrier()
+    ms = e0.elapsed_time(e1)
+    launches = ctx.launches - launches0
+    if pg is not None:
+        tt = torch.tensor([ms], device=dev, dtype=torch.float64)
+        pg.all_reduce(tt, op=pg.ReduceOp.MAX)
+        ms = float(tt.item())
+    ms_step = ms / args.steps
+    value = n * world * args.steps / (ms / 1e3)
+    scal = upd.scalars()
+
+    # ---- kernel-only timing for the roofline (single launches, same stream)
+    kev = []
+    for _ in range(5):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        src, dst = (pa, pb) if t % 2 == 0 else (pb, pa)
+        a.record(stream)
+        upd.step(props[t % args.pool], diffs[t % args.pool], src, dst)
+        b.record(stream)
+        t += 1
+        kev.append((a, b))
+    torch.cuda.synchronize()
+    k_ms = sorted(a.elapsed_time(b) for a, b in kev)[len(kev) // 2]
+    peak, peak_kind = measured_peak()
+    algo_bytes = BYTES_PER_PARAM[args.dtype] * n
+    achieved = algo_bytes / (k_ms / 1e3) / 1e9
+
+    # ---- e2e through the public API with HOST buffers (pinned), H2D of the
+    # step's sample pair and D2H of its scalars inside the timed region
+    e2e_steps = args.e2e_steps or max(3, min(args.steps, 10))
+    hp = [x.cpu().pin_memory() for x in props[:2]]
+    hd = [x.cpu().pin_memory() for x in diffs[:2]]
+    dprop, ddiff = torch.empty_like(pa), torch.empty_like(pa)
+    host_sc = torch.empty(8, dtype=torch.float64).pin_memory()
+    torch.cuda.synchronize()
+    if pg is not None:
+        pg.barrier()
+    f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    f0.record(stream)
+    for k in range(e2e_steps):
+        dprop.copy_(hp[k % 2], non_blocking=True)
+        ddiff.copy_(hd[k % 2], non_blocking=True)
+        src, dst = (pa, pb) if t % 2 == 0 else (pb, pa)
+        upd.step(dprop, ddiff, src, dst)
+        if pg is not None:
+            pg.all_reduce(sc[:4])
+        host_sc.copy_(sc, non_blocking=True)
+        t += 1
+    f1.record(stream)
+    torch.cuda.synchronize()
+    e2e_ms = f0.elapsed_time(f1)
+    if pg is not None:
+        tt = torch.tensor([e2e_ms], device=dev, dtype=torch.float64)
+        pg.all_reduce(tt, op=pg.ReduceOp.MAX)
+        e2e_ms = float(tt.item())
+    e2e_val = n * world * e2e_steps / (e2e_ms / 1e3)
+    esz = 4 if args.dtype == "f32" else 8
+
+    line = None
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": args.dtype, "data": "synthetic",
+            "iterations_per_s": 1e3 / ms_step,
+            "config": {"workload": "meta-update-microbench (BASELINE configs[1])",
+                       "params_per_gpu": n, "global_params": n * world, "pool_batches": args.pool,
+                       "l2": "inputs > L2 (no flush)", "parallelism": f"param-shard x{world}",
+                       "beta_f": 0.9, "beta_delta": 0.5, "lr": 0.01},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": None, "peak_kind": peak_kind,
+                         "kernel_ms": k_ms, "algorithmic_bytes": algo_bytes},
+            "e2e": {"value": e2e_val, "unit": UNIT, "h2d_bytes_per_step": 2 * esz * n,
+                    "d2h_bytes_per_step": 64, "steps": e2e_steps},
+            "gpu_launches": launches,
+            "clocks": clk.summary(),
+            "final_scalars": {"ssn": scal.ssn, "changed": scal.changed,
+                              "nonfinite": scal.nonfinite},
+        }
+    if pg is not None:
+        pg.barrier()
+    del props, diffs
+    torch.cuda.empty_cache()
+    if rank == 0 and args.extras:
+        line["extras"] = extras(args, ctx)
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            cv, csec, kind = cpu_reference(args.cpu_n, 5, 1)
+            line["cpu_baseline"] = {"value": cv, "unit": UNIT, "cores": 1, "kind": kind,
+                                    "sample": f"{args.cpu_n} params x 5 steps fp64, median step"}
+        except Exception as e:  # reported, never replaces our number
+            line["cpu_baseline"] = {"value": None, "unit": UNIT, "cores": 1, "kind": "reference",
+                                    "sample": f"unavailable: {e}"}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if pg is not None:
+        pg.barrier()
+        pg.destroy_process_group()
+    return 0
+
+
+def extras(args, ctx):
+    """Secondary measurements: Adam kernel roofline, device runner."""
+    import torch
+    from paper_2309_15676_b200 import api
+    out = {}
+    n = args.n
+    dev = torch.device("cuda", ctx.device)
+    g = torch.randn(n, device=dev)
+    pa, pb = torch.zeros(n, device=dev), torch.empty(n, device=dev)
+    ad = api.FusedAdamUpdate(n, ctx=ctx)
+    for i in range(3):
+        ad.step(g, pa if i % 2 == 0 else pb, pb if i % 2 == 0 else pa)
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record(ctx.stream)
+    K = 10
+    for i in range(K):
+        ad.step(g, pa if i % 2 == 0 else pb, pb if i % 2 == 0 else pa)
+    b.record(ctx.stream)
+    torch.cuda.synchronize()
+    ms = a.elapsed_time(b) / K
+    peak, _ = measured_peak()
+    out["adam_update_f32"] = {"ms": ms, "gbs": 28 * n / (ms / 1e3) / 1e9,
+                              "frac": 28 * n / (ms / 1e3) / 1e9 / peak}
+    del g, pa, pb, ad
+    torch.cuda.empty_cache()
+    # mini-render stand-in for configs[0] (P=4096, spp=2, 200 iterations)
+    cfg = api.ExperimentConfig(problem="mini-render", pixel_count=4096, spp=2, iterations=200,
+                               seed=0, problem_seed=1, lr=0.01, replicates=148)
+    t0 = time.time()
+    api.run_experiment(cfg, ctx=ctx)
+    wall = time.time() - t0
+    out["minirender_runner"] = {"replicates": 148, "iterations": 200, "wall_s": wall,
+                                "pairs_per_s": 148 * 200 * 4096 * 2 / wall}
+    return out
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference_arm(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

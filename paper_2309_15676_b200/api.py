@@ -1,0 +1,675 @@
+"""Host-side mirror of the reference `metagrad` API for the hot path, backed by
+the sm_100a kernels behind include/mgcuda.h.
+
+Names, argument meaning and error behaviour follow the reference
+(/root/reference/proj/include/metagrad/*.hpp):
+
+  Rng.stream(seed, r)                      rng.hpp:23-25   (device mt19937_64)
+  Moment2(decay).step(x)                   moment2.hpp:21-50
+  GradientSamplePair(prop, diff, ssn)      meta.hpp:20-24
+  MetaEstimator(lr, ...).step(pair, vp, vd) meta.hpp:71-114 (mean/var/alpha_prev injectable)
+  Adam(lr, b1, b2, eps).step(grad)         adam.hpp:14-50
+  MiniRenderProblem / ExpRateProblem / MultNoiseQuadratic .sample_pair(now, prev, rng)
+                                           problems.hpp:74-195
+  FusedMetaUpdate                          the one-pass hot path (harness.cpp:144-188)
+  ExperimentConfig, run_single, run_experiment   harness.hpp:18-112
+
+Vectors are torch CUDA tensors (float64 = parity mode, float32 = fast mode);
+torch is only the device-memory/stream plumbing.  Exceptions: InvalidArgument
+(std::invalid_argument), LogicError (std::logic_error), DomainError
+(std::domain_error).  There is no CPU fallback.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import dataclasses
+import math
+from typing import Dict, List, Optional
+
+import numpy as np
+import torch
+
+from . import _abi
+from ._lib import DomainError, InvalidArgument, LogicError, MgError, check, load  # noqa: F401
+
+__all__ = ["Context", "Rng", "Moment2", "GradientSamplePair", "MetaEstimator", "Adam",
+           "MiniRenderProblem", "ExpRateProblem", "MultNoiseQuadratic", "FusedMetaUpdate",
+           "FusedAdamUpdate", "ExperimentConfig", "RunRecord", "AggregateReport", "run_single",
+           "run_experiment", "InvalidArgument", "LogicError", "DomainError", "mix64"]
+
+
+def _p(t: Optional[torch.Tensor]):
+    if t is None:
+        return None
+    if not t.is_cuda:
+        raise InvalidArgument(_abi.MG_EINVAL, "tensor must be on the CUDA device")
+    if not t.is_contiguous():
+        raise InvalidArgument(_abi.MG_EINVAL, "tensor must be contiguous")
+    return C.c_void_p(t.data_ptr())
+
+
+def _dtype_code(t: torch.Tensor) -> int:
+    if t.dtype == torch.float64:
+        return _abi.MG_F64
+    if t.dtype == torch.float32:
+        return _abi.MG_F32
+    raise InvalidArgument(_abi.MG_EINVAL, f"unsupported dtype {t.dtype} (float32/float64)")
+
+
+class Context:
+    """One device + the current torch stream (mg_ctx_create)."""
+
+    _default: Dict[int, "Context"] = {}
+
+    def __init__(self, device: int = 0, stream: Optional[torch.cuda.Stream] = None):
+        L = load()
+        self.device = device
+        torch.cuda.set_device(device)
+        s = stream if stream is not None else torch.cuda.current_stream(device)
+        self.stream = s
+        h = C.c_void_p()
+        check(L.mg_ctx_create(device, C.c_void_p(s.cuda_stream), C.byref(h)))
+        self.h = h
+
+    @classmethod
+    def default(cls, device: Optional[int] = None) -> "Context":
+        dev = torch.cuda.current_device() if device is None else device
+        if dev not in cls._default:
+            cls._default[dev] = Context(dev)
+        return cls._default[dev]
+
+    def synchronize(self):
+        check(load().mg_ctx_synchronize(self.h))
+
+    @property
+    def launches(self) -> int:
+        return int(load().mg_ctx_launch_count(self.h))
+
+    def __del__(self):
+        try:
+            if getattr(self, "h", None):
+                load().mg_ctx_destroy(self.h)
+        except Exception:
+            pass
+
+
+def mix64(x: int) -> int:
+    return int(load().mg_mix64(x))
+
+
+# ------------------------------------------------------------------- RNG
+class Rng:
+    """A batch of device std::mt19937_64 engines (rng.hpp:18-37).
+
+    Rng(seed) is one engine seeded with `seed` (rng.hpp:20);
+    Rng.stream(seed, r) is the replicate stream (rng.hpp:23-25);
+    Rng.streams(seed, reps) batches several replicates."""
+
+    def __init__(self, engine_seeds, ctx: Optional[Context] = None):
+        self.ctx = ctx or Context.default()
+        seeds = np.ascontiguousarray(np.atleast_1d(np.asarray(engine_seeds, dtype=np.uint64)))
+        self.n = seeds.size
+        h = C.c_void_p()
+        check(load().mg_mt64_create(self.ctx.h, self.n, seeds.ctypes.data_as(C.c_void_p),
+                                    C.byref(h)))
+        self.h = h
+
+    @classmethod
+    def stream(cls, base_seed: int, replicate: int, ctx=None) -> "Rng":
+        return cls([load().mg_stream_seed(base_seed, replicate)], ctx)
+
+    @classmethod
+    def streams(cls, base_seed: int, replicates, ctx=None) -> "Rng":
+        L = load()
+        return cls([L.mg_stream_seed(base_seed, int(r)) for r in replicates], ctx)
+
+    def _draw(self, n: int, kind: int) -> torch.Tensor:
+        out = torch.empty((self.n, n), dtype=torch.uint64 if kind == 0 else torch.float64,
+                          device=f"cuda:{self.ctx.device}")
+        check(load().mg_mt64_draw(self.ctx.h, self.h, n, kind, _p(out)))
+        return out
+
+    def raw(self, n: int = 1) -> torch.Tensor:
+        return self._draw(n, 0)
+
+    def uniform(self, n: int = 1) -> torch.Tensor:
+        return self._draw(n, 1)
+
+    def uniform_pos(self, n: int = 1) -> torch.Tensor:
+        return self._draw(n, 2)
+
+    def __del__(self):
+        try:
+            if getattr(self, "h", None):
+                load().mg_mt64_destroy(self.h)
+        except Exception:
+            pass
+
+
+# ------------------------------------------------------------ estimators
+class Moment2:
+    """Zero-centred EMA of squares (moment2.hpp:21-50)."""
+
+    def __init__(self, decay: float = 0.9, dim: Optional[int] = None, ctx=None):
+        if not (0.0 <= decay < 1.0):
+            raise InvalidArgument(_abi.MG_EINVAL, "Moment2: decay must lie in [0, 1)")
+        self.ctx = ctx or Context.default()
+        self.s = _abi.Moment2Scalars(decay, 1.0, 0)
+        self._m2 = None if dim is None else torch.zeros(dim, dtype=torch.float64, device="cuda")
+
+    def step(self, x: torch.Tensor):
+        if self.s.count == 0 and (self._m2 is None or self._m2.numel() == 0):
+            self._m2 = torch.empty_like(x)
+        if x.numel() != self._m2.numel():
+            raise InvalidArgument(_abi.MG_EINVAL, "Moment2: sample dimension mismatch")
+        if x.dtype != self._m2.dtype:
+            self._m2 = self._m2.to(x.dtype)
+        check(load().mg_moment2_step(self.ctx.h, _dtype_code(x), x.numel(), C.byref(self.s),
+                                     _p(self._m2), _p(x.contiguous())))
+
+    def m2(self) -> torch.Tensor:
+        return self._m2 if self._m2 is not None else torch.zeros(0, device="cuda")
+
+    def count(self) -> int:
+        return int(self.s.count)
+
+    def decay(self) -> float:
+        return float(self.s.decay)
+
+
+@dataclasses.dataclass
+class GradientSamplePair:
+    """meta.hpp:20-24"""
+    prop: torch.Tensor
+    diff: torch.Tensor
+    step_sq_norm: float = 0.0
+
+
+class MetaEstimator:
+    """Recurrent gradient meta-estimator (meta.hpp:71-114).  mean, var and
+    alpha_prev are public device tensors and may be injected (as the
+    reference's tests do, tests/test_meta.cpp:213-218)."""
+
+    def __init__(self, lr: float = 0.001, eps_step: float = 1e-8, eps_alpha: float = 1e-30,
+                 ctx=None):
+        if not lr > 0.0:
+            raise InvalidArgument(_abi.MG_EINVAL, "MetaEstimator: lr must be positive")
+        self.ctx = ctx or Context.default()
+        self.lr, self.eps_step, self.eps_alpha = lr, eps_step, eps_alpha
+        self.clip_enabled = True
+        self.mean: Optional[torch.Tensor] = None
+        self.var: Optional[torch.Tensor] = None
+        self.alpha_prev: Optional[torch.Tensor] = None
+
+    def step(self, sample: GradientSamplePair, var_prop: torch.Tensor,
+             var_diff: torch.Tensor) -> torch.Tensor:
+        n = sample.prop.numel()
+        first = self.mean is None or self.mean.numel() == 0
+        if first:
+            self.mean = torch.empty_like(sample.prop)
+            self.var = torch.empty_like(sample.prop)
+            self.alpha_prev = torch.empty_like(sample.prop)
+        if (sample.diff.numel() != n or var_prop.numel() != n or var_diff.numel() != n or
+                self.mean.numel() != n):
+            raise InvalidArgument(_abi.MG_EINVAL, "MetaEstimator: dimension mismatch")
+        delta = torch.empty_like(sample.prop)
+        p = _abi.MetaParams(self.lr, self.eps_step, self.eps_alpha, int(self.clip_enabled))
+        check(load().mg_meta_step(self.ctx.h, _dtype_code(sample.prop), n, C.byref(p),
+                                  int(first), _p(self.mean), _p(self.var), _p(self.alpha_prev),
+                                  _p(sample.prop), _p(sample.diff), _p(var_prop),
+                                  _p(var_diff), _p(delta)))
+        return delta
+
+
+class Adam:
+    """Bias-corrected Adam (adam.hpp:14-50)."""
+
+    def __init__(self, lr: float, beta1: float = 0.9, beta2: float = 0.999, eps: float = 1e-8,
+                 ctx=None):
+        if not lr > 0.0:
+            raise InvalidArgument(_abi.MG_EINVAL, "Adam: lr must be positive")
+        if not (0.0 <= beta1 < 1.0 and 0.0 <= beta2 < 1.0):
+            raise InvalidArgument(_abi.MG_EINVAL, "Adam: betas must lie in [0, 1)")
+        self.ctx = ctx or Context.default()
+        self.s = _abi.AdamScalars(lr, beta1, beta2, eps, 1.0, 1.0, 0)
+        self._m = self._v = None
+
+    def step(self, grad: torch.Tensor) -> torch.Tensor:
+        if self.s.t == 0 and self._m is None:
+            self._m, self._v = torch.empty_like(grad), torch.empty_like(grad)
+        if grad.numel() != self._m.numel():
+            raise InvalidArgument(_abi.MG_EINVAL, "Adam: gradient dimension mismatch")
+        delta = torch.empty_like(grad)
+        check(load().mg_adam_step(self.ctx.h, _dtype_code(grad), grad.numel(), C.byref(self.s),
+                                  _p(self._m), _p(self._v), _p(grad), _p(delta)))
+        return delta
+
+    def t(self) -> int:
+        return int(self.s.t)
+
+    def m(self):
+        return self._m
+
+    def v(self):
+        return self._v
+
+    def m_hat(self):
+        return self._m / (1.0 - self.s.beta1_pow) if self.s.t > 0 else self._m
+
+    def v_hat(self):
+        return self._v / (1.0 - self.s.beta2_pow) if self.s.t > 0 else self._v
+
+
+# --------------------------------------------------------------- problems
+class _Problem:
+    def loss(self, params):
+        raise NotImplementedError
+
+    def project(self, params):
+        return params
+
+
+class MiniRenderProblem(_Problem):
+    """problems.hpp:157-195 / problems.cpp:162-228, target and exponents
+    generated on the device from Rng(mix64(gen_seed))."""
+
+    def __init__(self, pixel_count: int, spp: int, gen_seed: int = 1234, albedo_init: float = 0.1,
+                 exponent_max: float = 4.0, ctx=None):
+        if pixel_count < 1:
+            raise InvalidArgument(_abi.MG_EINVAL, "mini-render: pixel_count must be >= 1")
+        if spp < 2:
+            raise InvalidArgument(_abi.MG_EINVAL, "mini-render: spp must be at least 2")
+        if not exponent_max >= 0.0:
+            raise InvalidArgument(_abi.MG_EINVAL, "mini-render: exponent_max must be >= 0")
+        self.ctx = ctx or Context.default()
+        self.pixel_count, self.spp_, self.albedo_init = pixel_count, spp, albedo_init
+        self.exponents = torch.empty(pixel_count, dtype=torch.float64, device="cuda")
+        self.target = torch.empty(pixel_count, dtype=torch.float64, device="cuda")
+        check(load().mg_minirender_generate(self.ctx.h, pixel_count, gen_seed, exponent_max,
+                                            _p(self.exponents), _p(self.target)))
+
+    def name(self):
+        return "mini-render"
+
+    def dim(self):
+        return self.pixel_count
+
+    def spp(self):
+        return self.spp_
+
+    def draws_per_sample(self):
+        return self.pixel_count * self.spp_
+
+    def initial_params(self, dtype=torch.float64):
+        return torch.full((self.pixel_count,), self.albedo_init, dtype=dtype, device="cuda")
+
+    def truth_params(self):
+        return self.target
+
+    def target_image(self):
+        return self.target
+
+    def shape_exponents(self):
+        return self.exponents
+
+    def sample_pair(self, params_now, params_prev, rng: Rng):
+        """One pair per engine in rng: now/prev are [P] or [R, P]."""
+        R = rng.n
+        now = params_now.reshape(R, -1).contiguous()
+        prev = params_prev.reshape(R, -1).contiguous()
+        if now.shape[1] != self.pixel_count or prev.shape != now.shape:
+            raise InvalidArgument(_abi.MG_EINVAL, "mini-render: parameter dimension mismatch")
+        prop, diff = torch.empty_like(now), torch.empty_like(now)
+        ssn = torch.empty(R, dtype=torch.float64, device="cuda")
+        check(load().mg_minirender_sample_pair(self.ctx.h, _dtype_code(now), R, self.pixel_count,
+                                               self.spp_, _p(self.exponents), _p(self.target),
+                                               rng.h, _p(now), _p(prev), _p(prop), _p(diff),
+                                               _p(ssn)))
+        if R == 1:
+            return GradientSamplePair(prop[0], diff[0], float(ssn[0]))
+        return GradientSamplePair(prop, diff, ssn)
+
+    def true_gradient(self, params):
+        return 2.0 * (params - self.target.to(params.dtype))
+
+    def loss(self, params):
+        return float(((params.double() - self.target) ** 2).sum())
+
+    def project(self, params):
+        return torch.clamp_min(params, 0.0)
+
+
+class ExpRateProblem(_Problem):
+    """problems.hpp:81-111 / problems.cpp:30-94 (dim 1)."""
+
+    def __init__(self, target_mean: float = 2.0, samples_per_iter: int = 32,
+                 rate_init: float = 2.0, ctx=None):
+        if not target_mean > 0.0:
+            raise InvalidArgument(_abi.MG_EINVAL, "exp-rate: target mean must be positive")
+        if samples_per_iter < 2:
+            raise InvalidArgument(_abi.MG_EINVAL, "exp-rate: samples_per_iter must be at least 2")
+        if not rate_init > 0.0:
+            raise InvalidArgument(_abi.MG_EINVAL, "exp-rate: initial rate must be positive")
+        self.ctx = ctx or Context.default()
+        self.target_mean_, self.n, self.rate_init = target_mean, samples_per_iter, rate_init
+
+    def dim(self):
+        return 1
+
+    def draws_per_sample(self):
+        return self.n
+
+    def sample_pair(self, now, prev, rng: Rng):
+        R = rng.n
+        now = now.reshape(R).double().contiguous()
+        prev = prev.reshape(R).double().contiguous()
+        prop, diff, ssn = (torch.empty(R, dtype=torch.float64, device="cuda") for _ in range(3))
+        check(load().mg_exprate_sample_pair(self.ctx.h, R, self.target_mean_, self.n, rng.h,
+                                            _p(now), _p(prev), _p(prop), _p(diff), _p(ssn)))
+        return GradientSamplePair(prop, diff, ssn)
+
+    def true_gradient(self, params):
+        r = params
+        return 2.0 * (1.0 / r - self.target_mean_) * (-1.0 / (r * r))
+
+
+class MultNoiseQuadratic(_Problem):
+    """problems.hpp:118-148 / problems.cpp:99-157."""
+
+    def __init__(self, target: torch.Tensor, noise_amp: float, samples_per_iter: int = 1,
+                 ctx=None):
+        if target.numel() == 0:
+            raise InvalidArgument(_abi.MG_EINVAL, "mult-noise: empty target")
+        if noise_amp < 0.0:
+            raise InvalidArgument(_abi.MG_EINVAL, "mult-noise: noise amplitude must be >= 0")
+        if samples_per_iter < 1:
+            raise InvalidArgument(_abi.MG_EINVAL, "mult-noise: samples_per_iter must be >= 1")
+        self.ctx = ctx or Context.default()
+        self.target = target.double().cuda().contiguous()
+        self.sigma, self.n = noise_amp, samples_per_iter
+
+    def dim(self):
+        return self.target.numel()
+
+    def draws_per_sample(self):
+        return self.n * self.target.numel()
+
+    def sample_pair(self, now, prev, rng: Rng):
+        R, d = rng.n, self.target.numel()
+        now = now.reshape(R, d).double().contiguous()
+        prev = prev.reshape(R, d).double().contiguous()
+        prop, diff = torch.empty_like(now), torch.empty_like(now)
+        ssn = torch.empty(R, dtype=torch.float64, device="cuda")
+        check(load().mg_multnoise_sample_pair(self.ctx.h, R, d, self.sigma, self.n,
+                                              _p(self.target), rng.h, _p(now), _p(prev),
+                                              _p(prop), _p(diff), _p(ssn)))
+        if R == 1:
+            return GradientSamplePair(prop[0], diff[0], float(ssn[0]))
+        return GradientSamplePair(prop, diff, ssn)
+
+
+# ------------------------------------------------------- fused hot path
+class FusedMetaUpdate:
+    """Device-resident state of one meta-estimator run over n parameters and
+    the one-pass update of harness.cpp:144-188 (mg_meta_update).
+
+    step(prop, diff, params_in, params_out) runs one iteration; the step norm
+    of the NEXT iteration and the loss of the new parameters are reduced on
+    the device into self.scalars (mg_update_scalars), so consecutive steps
+    need no host synchronisation."""
+
+    def __init__(self, n: int, dtype=torch.float32, lr: float = 0.01, beta_f: float = 0.9,
+                 beta_delta: float = 0.5, eps_step: float = 1e-8, eps_alpha: float = 1e-30,
+                 clip: bool = True, project_lo: Optional[float] = None,
+                 diff_norm: str = "global", ctx=None, device="cuda"):
+        self.ctx = ctx or Context.default()
+        self.n, self.dtype = n, dtype
+        self.beta_f, self.beta_delta = beta_f, beta_delta
+        self.meta = _abi.MetaParams(lr, eps_step, eps_alpha, int(clip))
+        self.project_lo = project_lo
+        self.diff_norm = _abi.DIFF_NORMS[diff_norm]
+        mk = lambda: torch.empty(n, dtype=dtype, device=device)  # noqa: E731
+        self.m2_prop, self.m2_diff, self.mean, self.var, self.alpha_prev = (mk() for _ in range(5))
+        self.scalars_buf = torch.zeros(C.sizeof(_abi.UpdateScalars) // 8, dtype=torch.float64,
+                                       device=device)
+        self.reset()
+
+    def reset(self):
+        self.t = 0
+        self.beta_f_pow = 1.0
+        host = _abi.fresh_scalars()
+        check(load().mg_scalars_write(self.ctx.h, _p(self.scalars_buf), C.byref(host)))
+
+    def scalars(self) -> _abi.UpdateScalars:
+        out = _abi.UpdateScalars()
+        check(load().mg_scalars_read(self.ctx.h, _p(self.scalars_buf), C.byref(out)))
+        return out
+
+    def args(self, ssn_host: Optional[float] = None) -> _abi.MetaUpdateArgs:
+        """Advance the host-side Moment2(beta_f) scalars (moment2.hpp:34-38)."""
+        self.t += 1
+        self.beta_f_pow *= self.beta_f
+        c_prop = (1.0 - self.beta_f) / (1.0 - self.beta_f_pow)
+        return _abi.MetaUpdateArgs(
+            meta=self.meta, prop_coef=c_prop, beta_delta=self.beta_delta,
+            first_step=int(self.t == 1), diff_norm=self.diff_norm,
+            project=int(self.project_lo is not None),
+            ssn_from_host=int(ssn_host is not None),
+            proj_lo=0.0 if self.project_lo is None else self.project_lo,
+            ssn_host=0.0 if ssn_host is None else ssn_host)
+
+    def step(self, prop, diff, params_in, params_out, target=None, vprop=None, vdiff=None,
+             params_prev=None, delta_out=None, ssn_host=None):
+        a = self.args(ssn_host)
+        x = _abi.MetaExtras(_p(vprop), _p(vdiff), _p(params_prev), _p(target), _p(delta_out))
+        check(load().mg_meta_update(self.ctx.h, _dtype_code(prop), self.n, C.byref(a), _p(prop),
+                                    _p(diff), _p(self.m2_prop), _p(self.m2_diff), _p(self.mean),
+                                    _p(self.var), _p(self.alpha_prev), _p(params_in),
+                                    _p(params_out), _p(self.scalars_buf), C.byref(x)))
+
+
+class FusedAdamUpdate:
+    """Adam baseline with the same fused update/reductions (mg_adam_update)."""
+
+    def __init__(self, n: int, dtype=torch.float32, lr=0.01, beta1=0.9, beta2=0.999, eps=1e-8,
+                 project_lo: Optional[float] = None, ctx=None, device="cuda"):
+        self.ctx = ctx or Context.default()
+        self.n = n
+        self.s = _abi.AdamScalars(lr, beta1, beta2, eps, 1.0, 1.0, 0)
+        self.m = torch.empty(n, dtype=dtype, device=device)
+        self.v = torch.empty(n, dtype=dtype, device=device)
+        self.project_lo = project_lo
+        self.scalars_buf = torch.zeros(C.sizeof(_abi.UpdateScalars) // 8, dtype=torch.float64,
+                                       device=device)
+        host = _abi.fresh_scalars()
+        check(load().mg_scalars_write(self.ctx.h, _p(self.scalars_buf), C.byref(host)))
+
+    def step(self, grad, params_in, params_out, target=None):
+        check(load().mg_adam_update(self.ctx.h, _dtype_code(grad), self.n, C.byref(self.s),
+                                    int(self.project_lo is not None),
+                                    0.0 if self.project_lo is None else self.project_lo,
+                                    _p(grad), _p(self.m), _p(self.v), _p(params_in),
+                                    _p(params_out), _p(target), _p(self.scalars_buf)))
+
+
+# ------------------------------------------------------------- harness
+@dataclasses.dataclass
+class ExperimentConfig:
+    """harness.hpp:18-67 (+ B200 knobs dtype/rng)."""
+    problem: str = "exp-rate"
+    optimizer: str = "meta"
+    iterations: int = 100
+    replicates: int = 1
+    seed: int = 0
+    lr: float = 0.01
+    beta_f: float = 0.9
+    beta_delta: float = 0.5
+    beta1: float = 0.9
+    beta2: float = 0.999
+    eps_step: float = 1e-8
+    eps_alpha: float = 1e-30
+    adam_eps: float = 1e-8
+    dim: int = 4
+    sigma: float = 1.0
+    samples_per_iter: int = 32
+    target_mean: float = 2.0
+    rate_init: float = 2.0
+    pixel_count: int = 8
+    spp: int = 4
+    problem_seed: int = 1234
+    albedo_init: float = 0.1
+    exponent_max: float = 4.0
+    trajectory: str = "optimise"
+    traj_rate: float = 0.05
+    no_alpha_clip: bool = False
+    independent_variance_samples: bool = False
+    non_zero_centred: bool = False
+    diff_norm: str = "global"
+    coord: int = 0
+    converge_threshold: float = -1.0
+    threads: int = 0
+    dtype: str = "f64"
+    rng: str = "mt64"
+
+    def to_c(self) -> _abi.ExperimentConfigC:
+        kw = dataclasses.asdict(self)
+        kw.pop("threads")
+        return _abi.config_from(**kw)
+
+    def validate(self):
+        try:
+            c = self.to_c()
+        except ValueError as e:
+            raise InvalidArgument(_abi.MG_EINVAL, str(e)) from None
+        check(load().mg_config_validate(C.byref(c)))
+
+    def problem_dim(self) -> int:
+        return {"exp-rate": 1, "mult-noise": self.dim, "mini-render": self.pixel_count}[self.problem]
+
+
+STATUS = {0: "completed", 1: "converged", 2: "diverged"}
+
+
+@dataclasses.dataclass
+class RunRecord:
+    """Per-replicate record (harness.hpp:73-90), scalar series for `coord`."""
+    status: str
+    iterations_run: int
+    draws_used: int
+    evals_used: int
+    series: Dict[str, np.ndarray]
+    final_params: np.ndarray
+
+
+def _run_device(cfg: ExperimentConfig, rep_begin: int, rep_count: int, ctx=None):
+    ctx = ctx or Context.default()
+    c = cfg.to_c()
+    it = cfg.iterations
+    bufs = {n: np.full((rep_count, it), np.nan) for n in _abi.SERIES_NAMES}
+    ser = _abi.RunSeriesC(*[b.ctypes.data_as(C.c_void_p) for b in bufs.values()])
+    recs = (_abi.RunRecordC * rep_count)()
+    finals = np.empty((rep_count, cfg.problem_dim()))
+    check(load().mg_run_replicates(ctx.h, C.byref(c), rep_begin, rep_count, C.cast(recs, C.c_void_p),
+                                   C.byref(ser), finals.ctypes.data_as(C.c_void_p)))
+    out = []
+    for r in range(rep_count):
+        rec = recs[r]
+        out.append(RunRecord(STATUS[rec.status], rec.iterations_run, rec.draws_used,
+                             rec.evals_used, {n: bufs[n][r] for n in bufs}, finals[r]))
+    return out
+
+
+def run_single(cfg: ExperimentConfig, replicate_index: int, ctx=None) -> RunRecord:
+    """harness.cpp:90-200 on the device."""
+    cfg.validate()
+    if cfg.coord >= cfg.problem_dim():
+        raise InvalidArgument(_abi.MG_EINVAL, "coord exceeds problem dimension")
+    return _run_device(cfg, replicate_index, 1, ctx)[0]
+
+
+@dataclasses.dataclass
+class SeriesStats:
+    mean: np.ndarray
+    variance: np.ndarray
+    median: np.ndarray
+    q25: np.ndarray
+    q75: np.ndarray
+
+
+@dataclasses.dataclass
+class AggregateReport:
+    config: ExperimentConfig
+    series_names: List[str]
+    stats: Dict[str, SeriesStats]
+    active_replicates: np.ndarray
+    diverged_count: int
+    records: List[RunRecord]
+
+
+def _quantile(xs: np.ndarray, p: float) -> float:
+    """stats.hpp:45-53 (linear interpolation on the sorted sample)."""
+    if xs.size == 0:
+        return math.nan
+    s = np.sort(xs)
+    pos = p * (s.size - 1)
+    lo = int(pos)
+    if lo + 1 >= s.size:
+        return float(s[-1])
+    frac = pos - lo
+    return float(s[lo] * (1.0 - frac) + s[lo + 1] * frac)
+
+
+def _mean_of(xs):  # stats.hpp:55-60 (sequential sum)
+    if xs.size == 0:
+        return math.nan
+    s = 0.0
+    for x in xs:
+        s += float(x)
+    return s / xs.size
+
+
+def _variance_of(xs):  # stats.hpp:62-68
+    if xs.size < 2:
+        return 0.0
+    m = _mean_of(xs)
+    s = 0.0
+    for x in xs:
+        s += (float(x) - m) * (float(x) - m)
+    return s / (xs.size - 1)
+
+
+SERIES_ORDER = ["param_err", "loss", "prop", "diff", "grad_est", "est_var", "alpha", "delta",
+                "true_grad", "step_sq_norm"]
+
+
+def aggregate(cfg: ExperimentConfig, records: List[RunRecord]) -> AggregateReport:
+    """Per-iteration reduction in replicate order (harness.cpp:274-302)."""
+    it = cfg.iterations
+    names = [n for n in SERIES_ORDER if cfg.optimizer == "meta" or n != "alpha"]
+    active = np.array([sum(1 for r in records if r.iterations_run > i) for i in range(it)])
+    stats = {}
+    for n in names:
+        cols = np.stack([r.series[n] for r in records])  # [R][it]
+        st = SeriesStats(*(np.empty(it) for _ in range(5)))
+        for i in range(it):
+            vals = np.array([cols[k, i] for k, r in enumerate(records) if r.iterations_run > i])
+            st.mean[i] = _mean_of(vals)
+            st.variance[i] = _variance_of(vals)
+            st.median[i] = _quantile(vals, 0.5)
+            st.q25[i] = _quantile(vals, 0.25)
+            st.q75[i] = _quantile(vals, 0.75)
+        stats[n] = st
+    div = sum(1 for r in records if r.status == "diverged")
+    return AggregateReport(cfg, names, stats, active, div, records)
+
+
+def run_experiment(cfg: ExperimentConfig, ctx=None, rep_begin: int = 0,
+                   rep_count: Optional[int] = None) -> AggregateReport:
+    """harness.cpp:249-302: all replicates as one device launch (the thread
+    pool becomes the grid); reduction in replicate order on the host."""
+    cfg.validate()
+    if cfg.coord >= cfg.problem_dim():
+        raise InvalidArgument(_abi.MG_EINVAL, "coord exceeds problem dimension")
+    n = cfg.replicates if rep_count is None else rep_count
+    recs = _run_device(cfg, rep_begin, n, ctx)
+    return aggregate(cfg, recs)

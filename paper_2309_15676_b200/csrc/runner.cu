@@ -1,0 +1,565 @@
+// Device-resident run_single / run_experiment (rows A13, A14).
+//
+// The reference runs each replicate's loop (harness.cpp:90-200) on a
+// std::thread pool (harness.cpp:249-272).  Here every replicate is one CTA of
+// a single persistent kernel that executes the WHOLE optimisation loop on the
+// device: its mt19937_64 stream lives in shared memory, its state vectors in
+// global memory (L2-resident at reference sizes), and each iteration is
+//   draws -> sample_pair -> Moment2 x2 -> MetaEstimator/Adam -> record -> update
+// with no host round trip.  Reductions over a replicate's vector (step norm,
+// loss, parameter error) are sequential for dim <= kSeqReduceMax, so in fp64
+// the trajectories are bit-identical to the reference's wherever the
+// transcendental functions agree.
+//
+// Recording keeps the reference's extractor series for one coordinate plus
+// scalars (harness.cpp:204-244), not full vectors (O(iterations * dim)).
+#include <math.h>
+
+#include <vector>
+
+#include "mg_common.cuh"
+#include "mt64.cuh"
+#include "problems.cuh"
+
+namespace mg {
+namespace {
+
+constexpr int kThreads = 256;
+constexpr int kNumSeries = 11;
+
+template <class T>
+struct RunK {
+  mg_experiment_config cfg;
+  int dim;
+  int64_t D;  // draws per sample_pair
+  int rep_begin;
+  int R;
+  const double* truth;      // [dim]
+  const double* init;       // [dim]
+  const double* exponents;  // [dim] mini-render
+  const double* sched;      // [(iterations+1)][dim] or null
+  // per-replicate state [R][dim]
+  T *params, *prev, *prop, *diff, *iprop, *idiff, *m2p, *m2d, *mean, *var, *ap, *am, *av, *delta,
+      *mest, *vest;
+  double* ubuf;  // [R][D]
+  mg_run_record* recs;
+  double* series[kNumSeries];  // [R][iterations] each, or null
+  double* final_params;        // [R][dim] or null
+};
+
+// Up to three independent sums over j in [0, n) of f(j) (returns in
+// out[0..2], valid in every thread after the call).  Sequential (one thread
+// per sum, index order) for n <= kSeqReduceMax, fixed tree otherwise.
+template <class F>
+__device__ void block_sums3(int n, F f, double* out, double* sw) {
+  __shared__ double res[3];
+  if (n <= kSeqReduceMax) {
+    const int t = threadIdx.x;
+    if (t == 0 || t == 32 || t == 64) {
+      const int which = t / 32;
+      double s = 0.0;
+      for (int j = 0; j < n; ++j) s += f(j, which);
+      res[which] = s;
+    }
+  } else {
+    for (int which = 0; which < 3; ++which) {
+      double s = 0.0;
+      for (int j = threadIdx.x; j < n; j += kThreads) s += f(j, which);
+      s = block_sum<kThreads>(s, sw);
+      if (threadIdx.x == 0) res[which] = s;
+    }
+  }
+  __syncthreads();
+  out[0] = res[0];
+  out[1] = res[1];
+  out[2] = res[2];
+  __syncthreads();
+}
+
+// One sample_pair of the configured problem for this CTA's replicate.
+// Returns false on std::domain_error (exp-rate non-positive rate).
+template <class T>
+__device__ bool sample_pair(const RunK<T>& k, MtBlock& eng, const T* now, const T* prev, bool same,
+                            T* prop, T* diff, double* u, double& ssn, double* sw) {
+  const mg_experiment_config& c = k.cfg;
+  const int d = k.dim;
+  if (c.problem == MG_EXP_RATE) {
+    // validate_params (problems.cpp:56-57, :91-94) before drawing
+    if (!(double(now[0]) > 0.0) || !(double(prev[0]) > 0.0)) return false;
+    mt_block_generate(eng, k.D, [&](int64_t i, uint64_t raw) { u[i] = 1.0 - mt_uniform(raw); });
+    __shared__ double s_out[3];
+    if (threadIdx.x == 0) {
+      double sum_c = 0.0, sum_c_sq = 0.0;
+      exprate_sums(u, c.samples_per_iter, sum_c, sum_c_sq);
+      const double rn = double(now[0]), rp = double(prev[0]);
+      const double g = exprate_gradient(c.target_mean, c.samples_per_iter, rn, sum_c, sum_c_sq);
+      s_out[0] = g;
+      if (rn == rp) {
+        s_out[1] = 0.0;
+        s_out[2] = 0.0;
+      } else {
+        s_out[1] = g - exprate_gradient(c.target_mean, c.samples_per_iter, rp, sum_c, sum_c_sq);
+        s_out[2] = (rn - rp) * (rn - rp);
+      }
+      prop[0] = T(s_out[0]);
+      diff[0] = T(s_out[1]);
+    }
+    __syncthreads();
+    ssn = s_out[2];
+    __syncthreads();
+    return true;
+  }
+  mt_block_generate(eng, k.D, [&](int64_t i, uint64_t raw) { u[i] = mt_uniform(raw); });
+  for (int j = threadIdx.x; j < d; j += kThreads) {
+    if (c.problem == MG_MULT_NOISE) {
+      const double f = multnoise_factor(u, d, c.samples_per_iter, j, c.sigma);
+      prop[j] = T((double(now[j]) - k.truth[j]) * f);
+      diff[j] = same ? T(0) : T((double(now[j]) - double(prev[j])) * f);
+    } else {
+      T cross, mb;
+      minirender_terms<T>(k.exponents[j], u + size_t(j) * c.spp, c.spp, cross, mb);
+      const T a = now[j];
+      prop[j] = (T(2) * a) * cross - (T(2) * T(k.truth[j])) * mb;
+      diff[j] = same ? T(0) : (T(2) * (a - prev[j])) * cross;
+    }
+  }
+  if (same) {
+    ssn = 0.0;
+    __syncthreads();
+  } else {
+    double r[3];
+    block_sums3(d, [&](int j, int) {
+      const double dd = double(now[j]) - double(prev[j]);
+      return dd * dd;
+    }, r, sw);
+    ssn = r[0];
+  }
+  return true;
+}
+
+template <class T>
+__global__ void __launch_bounds__(kThreads) run_kernel(RunK<T> k) {
+  __shared__ uint64_t mtbuf[2][kMtN];
+  __shared__ double sw[kThreads / 32];
+  const int r = blockIdx.x;
+  const mg_experiment_config& c = k.cfg;
+  const int d = k.dim;
+  const int iters = c.iterations;
+  const size_t off = size_t(r) * d;
+  T* params = k.params + off;
+  T* prev = k.prev + off;
+  T* prop = k.prop + off;
+  T* diff = k.diff + off;
+  T* iprop = k.iprop + off;
+  T* idiff = k.idiff + off;
+  T* m2p = k.m2p + off;
+  T* m2d = k.m2d + off;
+  T* mean = k.mean + off;
+  T* var = k.var + off;
+  T* ap = k.ap + off;
+  T* am = k.am + off;
+  T* av = k.av + off;
+  T* delta = k.delta + off;
+  T* mest = k.mest + off;
+  T* vest = k.vest + off;
+  double* u = k.ubuf + size_t(r) * k.D;
+
+  // Rng::stream(seed, replicate) (rng.hpp:23-25), seeded in shared memory
+  MtBlock eng{{mtbuf[0], mtbuf[1]}, 0, kMtN};
+  if (threadIdx.x == 0) {
+    const uint64_t rep = uint64_t(k.rep_begin + r);
+    mt_seed(mtbuf[0], mg_mix64_dev(mg_mix64_dev(c.seed) ^ (rep + 0x51ed2701e35f3a6dULL)));
+  }
+  const bool scripted = c.trajectory != MG_TRAJ_OPTIMISE;
+  const bool use_meta = c.optimizer == MG_OPT_META;
+  for (int j = threadIdx.x; j < d; j += kThreads) {
+    const T p0 = T(scripted ? k.sched[j] : k.init[j]);
+    params[j] = p0;
+    prev[j] = p0;
+  }
+  __syncthreads();
+
+  double pf_pow = 1.0, pd_pow = 1.0, b1p = 1.0, b2p = 1.0;
+  int64_t pf_cnt = 0, pd_cnt = 0, t_adam = 0;
+  bool meta_first = true;
+  int status = 0, iters_run = 0;
+  int64_t draws = 0, evals = 0;
+  const int coord = c.coord;
+
+  for (int i = 0; i < iters; ++i) {
+    // harness.cpp:116-119
+    bool finite = true;
+    for (int j = threadIdx.x; j < d; j += kThreads) finite &= isfinite(double(params[j]));
+    if (!__syncthreads_and(finite)) {
+      status = 2;
+      break;
+    }
+    bool eq = true;
+    for (int j = threadIdx.x; j < d; j += kThreads) eq &= (params[j] == prev[j]);
+    const bool same_pp = __syncthreads_and(eq);
+    const T* sample_prev = use_meta ? prev : params;
+    const bool same = use_meta ? same_pp : true;
+    double ssn = 0.0;
+    if (!sample_pair(k, eng, params, sample_prev, same, prop, diff, u, ssn, sw)) {  // :125-128
+      status = 2;
+      break;
+    }
+    const bool two_point = use_meta && !same_pp;  // :129
+    draws += k.D;
+    evals += k.D * (two_point ? 2 : 1);
+    if (use_meta) {
+      const T* vp = prop;
+      const T* vd = diff;
+      double vssn = ssn;
+      if (c.independent_variance_samples) {  // :137-142
+        if (!sample_pair(k, eng, params, prev, same, iprop, idiff, u, vssn, sw)) {
+          status = 2;
+          break;
+        }
+        draws += k.D;
+        evals += k.D * (two_point ? 2 : 1);
+        vp = iprop;
+        vd = idiff;
+      }
+      // Moment2 scalars (moment2.hpp:34-38), uniform across the block
+      const bool pf_first = pf_cnt == 0;
+      pf_cnt += 1;
+      pf_pow = pf_pow * c.beta_f;
+      const double cp = (1.0 - c.beta_f) / (1.0 - pf_pow);
+      const bool active = vssn > 0.0;
+      const bool pd_had = pd_cnt > 0;
+      if (active) {
+        pd_cnt += 1;
+        pd_pow = pd_pow * c.beta_delta;
+      }
+      const double cd = (1.0 - c.beta_delta) / (1.0 - pd_pow);
+      const double norm = sqrt(vssn);
+      const bool per_param = c.diff_norm == MG_DIFF_NORM_PER_PARAM;
+      for (int j = threadIdx.x; j < d; j += kThreads) {
+        const T x = vp[j];
+        const T m2p_old = pf_first ? T(0) : m2p[j];
+        const T m2pv = m2p_old + T(cp) * (x * x - m2p_old);  // :144
+        m2p[j] = m2pv;
+        T m2dv = pd_had ? m2d[j] : T(0);
+        T var_diff = T(0);
+        if (per_param) {  // :146-151
+          const T cs = fabs(params[j] - prev[j]);
+          if (active) {
+            const T tiny = sizeof(T) == 8 ? T(1e-150) : T(1e-37);
+            const T xd = vd[j] / std_max(cs, tiny);
+            m2dv = m2dv + T(cd) * (xd * xd - m2dv);
+            m2d[j] = m2dv;
+          }
+          if (pd_cnt > 0) var_diff = m2dv * (cs * cs);
+        } else {  // :153-157
+          if (active) {
+            const T xd = vd[j] / T(norm);
+            m2dv = m2dv + T(cd) * (xd * xd - m2dv);
+            m2d[j] = m2dv;
+          }
+          if (pd_cnt > 0) var_diff = m2dv * T(ssn);
+        }
+        // MetaEstimator::step (meta.hpp:92-112)
+        T m = (meta_first ? T(0) : mean[j]) + diff[j];
+        T v = (meta_first ? T(0) : var[j]) + var_diff;
+        const T a_prev = meta_first ? T(-INFINITY) : ap[j];
+        T al = m2pv / ((m2pv + v) + T(c.eps_alpha));
+        if (!c.no_alpha_clip) al = std_min(al, T(1) / (T(2) - a_prev));
+        ap[j] = al;
+        const T om = T(1) - al;
+        m = al * m + om * prop[j];
+        v = (al * al) * v + (om * om) * m2pv;
+        mean[j] = m;
+        var[j] = v;
+        mest[j] = m;
+        vest[j] = v;
+        delta[j] = (T(-c.lr) * m) / (sqrt(v) + T(c.eps_step));
+      }
+      meta_first = false;
+    } else {  // Adam (adam.hpp:23-37), harness.cpp:165-167
+      const bool first = t_adam == 0;
+      t_adam += 1;
+      b1p = b1p * c.beta1;
+      b2p = b2p * c.beta2;
+      const T c1 = T(1.0 - c.beta1), c2 = T(1.0 - c.beta2);
+      const T d1 = T(1.0 - b1p), d2 = T(1.0 - b2p);
+      for (int j = threadIdx.x; j < d; j += kThreads) {
+        const T g = prop[j];
+        const T mm = T(c.beta1) * (first ? T(0) : am[j]) + c1 * g;
+        const T vv = T(c.beta2) * (first ? T(0) : av[j]) + c2 * (g * g);
+        am[j] = mm;
+        av[j] = vv;
+        const T mh = mm / d1, vh = vv / d2;
+        mest[j] = mh;  // adam.hpp:42-43
+        vest[j] = vh;
+        delta[j] = (T(-c.lr) * mh) / (sqrt(vh) + T(c.adam_eps));
+      }
+    }
+    __syncthreads();
+    // record iteration i (harness.cpp:170-180) for coordinate `coord`
+    double sums[3];
+    // loss (problems.cpp:225) and param_err (harness.cpp:212-215) share
+    // the sum of (params - truth)^2, taken in index order.
+    block_sums3(d, [&](int j, int) {
+      const double e = double(params[j]) - k.truth[j];
+      return e * e;
+    }, sums, sw);
+    if (threadIdx.x == 0) {
+      const size_t at = size_t(r) * iters + i;
+      double loss;
+      if (c.problem == MG_EXP_RATE) {
+        const double err = 1.0 / double(params[0]) - c.target_mean;  // problems.cpp:84-87
+        loss = err * err;
+      } else if (c.problem == MG_MULT_NOISE) {
+        loss = 0.5 * sums[0];  // problems.cpp:146-149
+      } else {
+        loss = sums[0];  // problems.cpp:223-226
+      }
+      double tg;
+      const double x = double(params[coord]);
+      if (c.problem == MG_EXP_RATE)
+        tg = (2.0 * (1.0 / x - c.target_mean)) * (-1.0 / (x * x));  // :78-82
+      else if (c.problem == MG_MULT_NOISE)
+        tg = x - k.truth[coord];  // :141-144
+      else
+        tg = 2.0 * (x - k.truth[coord]);  // :219-222
+      const double vals[kNumSeries] = {sqrt(sums[0]), loss, double(prop[coord]),
+                                       double(diff[coord]), double(mest[coord]),
+                                       double(vest[coord]),
+                                       use_meta ? double(ap[coord]) : nan(""),
+                                       double(delta[coord]), tg, ssn, x};
+      for (int s = 0; s < kNumSeries; ++s)
+        if (k.series[s]) k.series[s][at] = vals[s];
+    }
+    iters_run = i + 1;
+    // prev = params; params += delta; project (harness.cpp:182-188)
+    for (int j = threadIdx.x; j < d; j += kThreads) {
+      const T p = params[j];
+      prev[j] = p;
+      T np;
+      if (scripted) {
+        np = T(k.sched[size_t(i + 1) * d + j]);
+      } else {
+        np = p + delta[j];
+        if (c.problem == MG_EXP_RATE)
+          np = std_max(np, T(1e-4));  // problems.cpp:89
+        else if (c.problem == MG_MINI_RENDER)
+          np = std_max(np, T(0));  // problems.cpp:228
+      }
+      params[j] = np;
+    }
+    __syncthreads();
+  }
+  // converged status (harness.cpp:191-198) on the last recorded params (= prev)
+  double fin[3];
+  block_sums3(d, [&](int j, int) {
+    const double e = double(prev[j]) - k.truth[j];
+    return e * e;
+  }, fin, sw);
+  if (threadIdx.x == 0) {
+    if (status != 2 && c.converge_threshold > 0.0 && iters_run > 0 &&
+        sqrt(fin[0]) < c.converge_threshold)
+      status = 1;
+    mg_run_record rec;
+    rec.iterations_run = iters_run;
+    rec.status = status;
+    rec.draws_used = draws;
+    rec.evals_used = evals;
+    k.recs[r] = rec;
+  }
+  if (k.final_params)
+    for (int j = threadIdx.x; j < d; j += kThreads) k.final_params[off + j] = double(prev[j]);
+}
+
+// ------------------------------------------------------------- host side
+int problem_dim(const mg_experiment_config* c) {
+  return c->problem == MG_EXP_RATE ? 1 : (c->problem == MG_MULT_NOISE ? c->dim : c->pixel_count);
+}
+
+// TrajectorySchedule::at (problems.hpp:207-215) on the host with the
+// reference's own libm exp, so scripted runs match bit for bit.
+void schedule_table(const mg_experiment_config* c, const std::vector<double>& from,
+                    const std::vector<double>& to, std::vector<double>& out) {
+  const int d = int(from.size());
+  const int horizon = c->iterations;
+  out.assign(size_t(c->iterations + 1) * d, 0.0);
+  for (int i = 0; i <= c->iterations; ++i) {
+    int clamped = i < horizon - 1 ? i : horizon - 1;
+    if (clamped < 0) clamped = 0;
+    for (int j = 0; j < d; ++j) {
+      double v;
+      if (c->trajectory == MG_TRAJ_SCRIPTED_LINEAR) {
+        const double f = horizon <= 1 ? 1.0 : double(clamped) / double(horizon - 1);
+        v = from[j] + (to[j] - from[j]) * f;
+      } else {
+        const double e = exp(-c->traj_rate * double(clamped));
+        v = to[j] + (from[j] - to[j]) * e;
+      }
+      out[size_t(i) * d + j] = v;
+    }
+  }
+}
+
+template <class T>
+int run_replicates(mg_ctx* ctx, const mg_experiment_config* cfg, int rep_begin, int R,
+                   mg_run_record* records, const mg_run_series* series, double* final_params) {
+  const int d = problem_dim(cfg);
+  const int iters = cfg->iterations;
+  std::vector<double> truth(d, 0.0), init(d, 0.0);
+  int64_t D = 0;
+  double* dexp = nullptr;
+  cudaStream_t s = ctx->stream;
+  std::vector<void*> allocs;
+  auto dalloc = [&](size_t bytes) -> void* {
+    void* p = nullptr;
+    if (cudaMallocAsync(&p, bytes, s) != cudaSuccess) return nullptr;
+    allocs.push_back(p);
+    return p;
+  };
+  auto cleanup = [&]() {
+    for (void* p : allocs) cudaFreeAsync(p, s);
+    cudaStreamSynchronize(s);
+  };
+  switch (cfg->problem) {
+    case MG_EXP_RATE:  // problems.cpp:30-42
+      if (!(cfg->target_mean > 0.0)) return fail(MG_EINVAL, "exp-rate: target mean must be positive");
+      if (cfg->samples_per_iter < 2)
+        return fail(MG_EINVAL, "exp-rate: samples_per_iter must be at least 2");
+      if (!(cfg->rate_init > 0.0)) return fail(MG_EINVAL, "exp-rate: initial rate must be positive");
+      truth[0] = 1.0 / cfg->target_mean;
+      init[0] = cfg->rate_init;
+      D = cfg->samples_per_iter;
+      break;
+    case MG_MULT_NOISE:  // problems.cpp:99-108 with target 0 (harness.cpp:71-73)
+      if (d < 1) return fail(MG_EINVAL, "mult-noise: empty target");
+      if (cfg->sigma < 0.0) return fail(MG_EINVAL, "mult-noise: noise amplitude must be >= 0");
+      if (cfg->samples_per_iter < 1)
+        return fail(MG_EINVAL, "mult-noise: samples_per_iter must be >= 1");
+      for (int j = 0; j < d; ++j) init[j] = truth[j] + 2.0;
+      D = int64_t(cfg->samples_per_iter) * d;
+      break;
+    default: {  // mini-render problems.cpp:162-175
+      if (d < 1) return fail(MG_EINVAL, "mini-render: pixel_count must be >= 1");
+      if (cfg->spp < 2) return fail(MG_EINVAL, "mini-render: spp must be at least 2");
+      dexp = (double*)dalloc(sizeof(double) * d);
+      double* dT = (double*)dalloc(sizeof(double) * d);
+      if (!dexp || !dT) {
+        cleanup();
+        return fail(MG_ENOMEM, "run: allocation failed");
+      }
+      int st = mg_minirender_generate(ctx, d, cfg->problem_seed, cfg->exponent_max, dexp, dT);
+      if (st) {
+        cleanup();
+        return st;
+      }
+      MG_CUDA_TRY(cudaMemcpy(truth.data(), dT, sizeof(double) * d, cudaMemcpyDeviceToHost));
+      for (int j = 0; j < d; ++j) init[j] = cfg->albedo_init;
+      D = int64_t(d) * cfg->spp;
+    }
+  }
+  if (cfg->coord >= d) {
+    cleanup();
+    return fail(MG_EINVAL, "coord exceeds problem dimension");
+  }
+  RunK<T> k{};
+  k.cfg = *cfg;
+  k.dim = d;
+  k.D = D;
+  k.rep_begin = rep_begin;
+  k.R = R;
+  k.exponents = dexp;
+  double* dtruth = (double*)dalloc(sizeof(double) * d);
+  double* dinit = (double*)dalloc(sizeof(double) * d);
+  if (!dtruth || !dinit) {
+    cleanup();
+    return fail(MG_ENOMEM, "run: allocation failed");
+  }
+  cudaMemcpyAsync(dtruth, truth.data(), sizeof(double) * d, cudaMemcpyHostToDevice, s);
+  cudaMemcpyAsync(dinit, init.data(), sizeof(double) * d, cudaMemcpyHostToDevice, s);
+  k.truth = dtruth;
+  k.init = dinit;
+  std::vector<double> sched;
+  if (cfg->trajectory != MG_TRAJ_OPTIMISE) {
+    schedule_table(cfg, init, truth, sched);
+    double* dsched = (double*)dalloc(sizeof(double) * sched.size());
+    if (!dsched) {
+      cleanup();
+      return fail(MG_ENOMEM, "run: allocation failed");
+    }
+    cudaMemcpyAsync(dsched, sched.data(), sizeof(double) * sched.size(), cudaMemcpyHostToDevice, s);
+    k.sched = dsched;
+  }
+  const size_t vec_bytes = sizeof(T) * size_t(R) * d;
+  T** vecs[] = {&k.params, &k.prev, &k.prop, &k.diff, &k.iprop, &k.idiff, &k.m2p, &k.m2d,
+                &k.mean, &k.var, &k.ap, &k.am, &k.av, &k.delta, &k.mest, &k.vest};
+  for (T** v : vecs) {
+    *v = (T*)dalloc(vec_bytes);
+    if (!*v) {
+      cleanup();
+      return fail(MG_ENOMEM, "run: allocation failed");
+    }
+  }
+  k.ubuf = (double*)dalloc(sizeof(double) * size_t(R) * D);
+  k.recs = (mg_run_record*)dalloc(sizeof(mg_run_record) * R);
+  if (!k.ubuf || !k.recs) {
+    cleanup();
+    return fail(MG_ENOMEM, "run: allocation failed");
+  }
+  const size_t ser_bytes = sizeof(double) * size_t(R) * iters;
+  void* const* host_series = series ? reinterpret_cast<void* const*>(series) : nullptr;
+  for (int i = 0; i < kNumSeries; ++i) {
+    k.series[i] = nullptr;
+    if (host_series && host_series[i]) {
+      k.series[i] = (double*)dalloc(ser_bytes);
+      if (!k.series[i]) {
+        cleanup();
+        return fail(MG_ENOMEM, "run: allocation failed");
+      }
+      // entries past iterations_run stay NaN (0xff.. bytes = NaN)
+      cudaMemsetAsync(k.series[i], 0xff, ser_bytes, s);
+    }
+  }
+  if (final_params) {
+    k.final_params = (double*)dalloc(sizeof(double) * size_t(R) * d);
+    if (!k.final_params) {
+      cleanup();
+      return fail(MG_ENOMEM, "run: allocation failed");
+    }
+  }
+  run_kernel<T><<<R, kThreads, 0, s>>>(k);
+  ctx->launches++;
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    cleanup();
+    return cuda_fail(e, "run_kernel");
+  }
+  cudaMemcpyAsync(records, k.recs, sizeof(mg_run_record) * R, cudaMemcpyDeviceToHost, s);
+  for (int i = 0; i < kNumSeries; ++i)
+    if (k.series[i]) cudaMemcpyAsync(host_series[i], k.series[i], ser_bytes, cudaMemcpyDeviceToHost, s);
+  if (final_params)
+    cudaMemcpyAsync(final_params, k.final_params, sizeof(double) * size_t(R) * d,
+                    cudaMemcpyDeviceToHost, s);
+  e = cudaStreamSynchronize(s);
+  cleanup();
+  if (e != cudaSuccess) return cuda_fail(e, "run_kernel execution");
+  return MG_OK;
+}
+
+}  // namespace
+}  // namespace mg
+
+using namespace mg;
+
+extern "C" int mg_run_replicates(mg_ctx* ctx, const mg_experiment_config* cfg, int32_t rep_begin,
+                                 int32_t rep_count, mg_run_record* records,
+                                 const mg_run_series* series, double* final_params) {
+  if (!ctx || !cfg || !records) return fail(MG_EINVAL, "mg_run_replicates: null argument");
+  int st = mg_config_validate(cfg);
+  if (st) return st;
+  if (rep_count < 1 || rep_begin < 0) return fail(MG_EINVAL, "mg_run_replicates: bad replicate range");
+  if (cfg->rng != MG_RNG_MT64)
+    return fail(MG_EUNSUPPORTED, "mg_run_replicates: only the bit-exact mt64 streams are supported");
+  if (cfg->dtype == MG_F64)
+    return run_replicates<double>(ctx, cfg, rep_begin, rep_count, records, series, final_params);
+  return run_replicates<float>(ctx, cfg, rep_begin, rep_count, records, series, final_params);
+}

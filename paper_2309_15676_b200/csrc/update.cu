@@ -1,0 +1,572 @@
+// Fused estimator/optimiser kernels.
+//
+// mg_meta_update is THE hot kernel: one HBM pass that fuses
+//   Moment2(beta_f).step(prop)                 moment2.hpp:30-39 (harness.cpp:144)
+//   decoupled diff variance + Moment2(beta_d)  harness.cpp:145-158, meta.hpp:51-53
+//   MetaEstimator::step                        meta.hpp:90-113 (harness.cpp:160)
+//   params += delta; project                   harness.cpp:182-188, problems.cpp:228
+//   sum (dp)^2, #changed, sum (p-T)^2, #nonfinite  problems.cpp:206,214,225; harness.cpp:116
+// The reference evaluates these as ~12 Eigen statements (~12 memory passes
+// plus temporaries); here every parameter is touched once: 8 streams read,
+// 6 written (56 B/param fp32, 112 B/param fp64), the reductions ride along in
+// registers and finish in the last CTA (deterministic fixed-order tree).
+//
+// Arithmetic follows the reference expression by expression (same operand
+// order, no FMA: the library is built with --fmad=false), so the fp64 path is
+// bit-identical to the oracle for the elementwise outputs.
+#include <math.h>
+
+#include "mg_common.cuh"
+
+namespace mg {
+namespace {
+
+constexpr int kThreads = 256;
+
+struct MetaK {
+  double lr, eps_step, eps_alpha, prop_coef, beta_delta, proj_lo, ssn_host;
+  int clip, diff_norm, project, ssn_from_host;
+};
+
+template <class T>
+struct MetaPtrs {
+  const T* __restrict__ prop;
+  const T* __restrict__ diff;
+  const T* __restrict__ vprop;
+  const T* __restrict__ vdiff;
+  T* __restrict__ m2p;
+  T* __restrict__ m2d;
+  T* __restrict__ mean;
+  T* __restrict__ var;
+  T* __restrict__ ap;
+  const T* pin;  // may alias pout
+  T* pout;
+  const T* __restrict__ pprev;
+  const T* __restrict__ target;
+  T* __restrict__ delta;
+};
+
+// Per-launch scalar state, identical in every thread (read once from the
+// device scalars written by the previous launch's epilogue).
+struct StepScal {
+  double ssn, norm, c_diff, dpow;
+  int64_t cnt0, cnt;
+  bool active;
+};
+
+__device__ __forceinline__ StepScal load_step_scalars(const MetaK& k, const mg_update_scalars* sc) {
+  StepScal s;
+  s.ssn = k.ssn_from_host ? k.ssn_host : __ldcg(&sc->ssn);
+  s.active = s.ssn > 0.0;                         // harness.cpp:153
+  s.cnt0 = __ldcg(&sc->diff_count);
+  s.dpow = __ldcg(&sc->diff_decay_pow);
+  s.cnt = s.cnt0;
+  if (s.active) {
+    s.cnt += 1;                                   // moment2.hpp:34
+    s.dpow = s.dpow * k.beta_delta;               // moment2.hpp:35
+  }
+  s.c_diff = (1.0 - k.beta_delta) / (1.0 - s.dpow);  // moment2.hpp:36-38
+  s.norm = sqrt(s.ssn);                           // harness.cpp:154
+  return s;
+}
+
+// One parameter of the fused meta iteration.  All inputs already loaded.
+template <class T, bool FIRST>
+__device__ __forceinline__ void meta_elem(const MetaK& k, const StepScal& s, T prop, T diff,
+                                          T vprop, T vdiff, T& m2p, T& m2d, T& mean, T& var,
+                                          T& ap, T pin, T pprev, T target, bool has_target,
+                                          T& pout, T& delta, ReducePartials& acc) {
+  // Moment2(beta_f).step(prop): m2 += (w/w_sum) * (x^2 - m2)
+  const T m2p_old = FIRST ? T(0) : m2p;
+  const T cp = T(k.prop_coef);
+  m2p = m2p_old + cp * (vprop * vprop - m2p_old);
+  // decoupled diff variance (global or per-param norm)
+  T m2d_v = s.cnt0 > 0 ? m2d : T(0);
+  T var_diff = T(0);
+  if (k.diff_norm == MG_DIFF_NORM_PER_PARAM) {
+    const T cs = fabs(pin - pprev);                          // harness.cpp:147
+    const T tiny = sizeof(T) == 8 ? T(1e-150) : T(1e-37);    // kTinyCoordStep (fp32: FLT_MIN-ish)
+    if (s.active) {
+      const T x = vdiff / std_max(cs, tiny);                 // harness.cpp:149
+      m2d_v = m2d_v + T(s.c_diff) * (x * x - m2d_v);
+    }
+    if (s.cnt > 0) var_diff = m2d_v * (cs * cs);             // harness.cpp:150
+  } else {
+    if (s.active) {
+      const T x = vdiff / T(s.norm);                         // harness.cpp:154
+      m2d_v = m2d_v + T(s.c_diff) * (x * x - m2d_v);
+    }
+    if (s.cnt > 0) var_diff = m2d_v * T(s.ssn);              // meta.hpp:51-53
+  }
+  m2d = m2d_v;
+  // MetaEstimator::step (meta.hpp:103-112)
+  T m = (FIRST ? T(0) : mean) + diff;
+  T v = (FIRST ? T(0) : var) + var_diff;
+  const T a_prev = FIRST ? T(-INFINITY) : ap;
+  T al = m2p / ((m2p + v) + T(k.eps_alpha));
+  if (k.clip) al = std_min(al, T(1) / (T(2) - a_prev));      // meta.hpp:30-32
+  ap = al;
+  const T om = T(1) - al;
+  m = al * m + om * prop;
+  v = (al * al) * v + (om * om) * m2p;
+  mean = m;
+  var = v;
+  delta = (T(-k.lr) * m) / (sqrt(v) + T(k.eps_step));
+  // params += delta; project (harness.cpp:186-187, problems.cpp:228)
+  T p = pin + delta;
+  if (k.project) p = std_max(p, T(k.proj_lo));
+  pout = p;
+  // fused reductions (problems.cpp:206,214,225; harness.cpp:116)
+  const double d = double(p - pin);
+  acc.ssn += d * d;
+  acc.changed += (p != pin) ? 1.0 : 0.0;
+  if (has_target) {
+    const double e = double(p - target);
+    acc.loss += e * e;
+  }
+  acc.nonfinite += isfinite(p) ? 0.0 : 1.0;
+}
+
+template <class T, bool FIRST, bool VEC>
+__global__ void __launch_bounds__(kThreads)
+    meta_update_kernel(int64_t n, MetaK k, MetaPtrs<T> q, mg_update_scalars* sc,
+                       ReducePartials* partials, unsigned int* counter) {
+  const StepScal s = load_step_scalars(k, sc);
+  const bool has_target = q.target != nullptr;
+  ReducePartials acc{0.0, 0.0, 0.0, 0.0};
+  const int64_t tid = int64_t(blockIdx.x) * kThreads + threadIdx.x;
+  const int64_t stride = int64_t(gridDim.x) * kThreads;
+  constexpr int W = VEC ? VecOf<T>::width : 1;
+  const int64_t items = VEC ? n / W : 0;
+  if constexpr (VEC) {
+    const bool pp = k.diff_norm == MG_DIFF_NORM_PER_PARAM;
+    for (int64_t it = tid; it < items; it += stride) {
+      const int64_t b = it * W;
+      const Pack<T> P = ld_stream(q.prop + b);
+      const Pack<T> D = ld_stream(q.diff + b);
+      const Pack<T> VP = q.vprop ? ld_stream(q.vprop + b) : P;
+      const Pack<T> VD = q.vdiff ? ld_stream(q.vdiff + b) : D;
+      Pack<T> M2P{}, M2D{}, ME{}, VA{}, AP{}, PO, DL;
+      if (!FIRST) {
+        M2P = ld_plain(q.m2p + b);
+        ME = ld_plain(q.mean + b);
+        VA = ld_plain(q.var + b);
+        AP = ld_plain(q.ap + b);
+      }
+      if (s.cnt0 > 0) M2D = ld_plain(q.m2d + b);
+      const Pack<T> PI = ld_plain(q.pin + b);
+      Pack<T> PP{}, TG{};
+      if (pp) PP = ld_plain(q.pprev + b);
+      if (has_target) TG = ld_plain(q.target + b);
+#pragma unroll
+      for (int w = 0; w < W; ++w)
+        meta_elem<T, FIRST>(k, s, P.v[w], D.v[w], VP.v[w], VD.v[w], M2P.v[w], M2D.v[w], ME.v[w],
+                            VA.v[w], AP.v[w], PI.v[w], PP.v[w], TG.v[w], has_target, PO.v[w],
+                            DL.v[w], acc);
+      st_plain(q.m2p + b, M2P);
+      if (s.active) st_plain(q.m2d + b, M2D);
+      st_plain(q.mean + b, ME);
+      st_plain(q.var + b, VA);
+      st_plain(q.ap + b, AP);
+      st_plain(q.pout + b, PO);
+      if (q.delta) st_plain(q.delta + b, DL);
+    }
+  }
+  // scalar path: everything (unaligned) or the tail (aligned)
+  for (int64_t i = items * W + tid; i < n; i += stride) {
+    const T P = q.prop[i], D = q.diff[i];
+    const T VP = q.vprop ? q.vprop[i] : P;
+    const T VD = q.vdiff ? q.vdiff[i] : D;
+    T M2P = FIRST ? T(0) : q.m2p[i];
+    T M2D = s.cnt0 > 0 ? q.m2d[i] : T(0);
+    T ME = FIRST ? T(0) : q.mean[i];
+    T VA = FIRST ? T(0) : q.var[i];
+    T AP = FIRST ? T(0) : q.ap[i];
+    const T PI = q.pin[i];
+    const T PP = k.diff_norm == MG_DIFF_NORM_PER_PARAM ? q.pprev[i] : T(0);
+    const T TG = has_target ? q.target[i] : T(0);
+    T PO, DL;
+    meta_elem<T, FIRST>(k, s, P, D, VP, VD, M2P, M2D, ME, VA, AP, PI, PP, TG, has_target, PO, DL,
+                        acc);
+    q.m2p[i] = M2P;
+    if (s.active) q.m2d[i] = M2D;
+    q.mean[i] = ME;
+    q.var[i] = VA;
+    q.ap[i] = AP;
+    q.pout[i] = PO;
+    if (q.delta) q.delta[i] = DL;
+  }
+  grid_reduce4<kThreads>(acc, partials, counter, [&](const ReducePartials& t) {
+    sc->ssn = t.ssn;
+    sc->changed = t.changed;
+    sc->loss = has_target ? t.loss : nan("");
+    sc->nonfinite = t.nonfinite;
+    sc->diff_count = s.cnt;
+    sc->diff_decay_pow = s.dpow;
+    sc->ssn_used = s.ssn;
+  });
+}
+
+// ------------------------------------------------------------------- Adam
+struct AdamK {
+  double beta1, beta2, c1, c2, d1, d2, lr, eps, proj_lo;
+  int project;
+};
+
+template <class T>
+__device__ __forceinline__ void adam_elem(const AdamK& k, T g, T& m, T& v, T pin, T target,
+                                          bool has_target, T& pout, T& delta,
+                                          ReducePartials& acc) {
+  m = T(k.beta1) * m + T(k.c1) * g;          // adam.hpp:32
+  v = T(k.beta2) * v + T(k.c2) * (g * g);    // adam.hpp:33
+  const T mh = m / T(k.d1);                  // adam.hpp:34
+  const T vh = v / T(k.d2);                  // adam.hpp:35
+  delta = (T(-k.lr) * mh) / (sqrt(vh) + T(k.eps));  // adam.hpp:36
+  T p = pin + delta;
+  if (k.project) p = std_max(p, T(k.proj_lo));
+  pout = p;
+  const double d = double(p - pin);
+  acc.ssn += d * d;
+  acc.changed += (p != pin) ? 1.0 : 0.0;
+  if (has_target) {
+    const double e = double(p - target);
+    acc.loss += e * e;
+  }
+  acc.nonfinite += isfinite(p) ? 0.0 : 1.0;
+}
+
+template <class T, bool FIRST, bool VEC>
+__global__ void __launch_bounds__(kThreads)
+    adam_update_kernel(int64_t n, AdamK k, const T* __restrict__ grad, T* __restrict__ m,
+                       T* __restrict__ v, const T* pin, T* pout, const T* __restrict__ target,
+                       T* __restrict__ delta, mg_update_scalars* sc, ReducePartials* partials,
+                       unsigned int* counter) {
+  const double ssn_in = __ldcg(&sc->ssn);
+  const bool has_target = target != nullptr;
+  ReducePartials acc{0.0, 0.0, 0.0, 0.0};
+  const int64_t tid = int64_t(blockIdx.x) * kThreads + threadIdx.x;
+  const int64_t stride = int64_t(gridDim.x) * kThreads;
+  constexpr int W = VEC ? VecOf<T>::width : 1;
+  const int64_t items = VEC ? n / W : 0;
+  if constexpr (VEC) {
+    for (int64_t it = tid; it < items; it += stride) {
+      const int64_t b = it * W;
+      const Pack<T> G = ld_stream(grad + b);
+      Pack<T> M{}, V{}, PO, DL, TG{};
+      if (!FIRST) {
+        M = ld_plain(m + b);
+        V = ld_plain(v + b);
+      }
+      const Pack<T> PI = ld_plain(pin + b);
+      if (has_target) TG = ld_plain(target + b);
+#pragma unroll
+      for (int w = 0; w < W; ++w)
+        adam_elem<T>(k, G.v[w], M.v[w], V.v[w], PI.v[w], TG.v[w], has_target, PO.v[w], DL.v[w],
+                     acc);
+      st_plain(m + b, M);
+      st_plain(v + b, V);
+      st_plain(pout + b, PO);
+      if (delta) st_plain(delta + b, DL);
+    }
+  }
+  for (int64_t i = items * W + tid; i < n; i += stride) {
+    T M = FIRST ? T(0) : m[i], V = FIRST ? T(0) : v[i], PO, DL;
+    adam_elem<T>(k, grad[i], M, V, pin[i], has_target ? target[i] : T(0), has_target, PO, DL, acc);
+    m[i] = M;
+    v[i] = V;
+    pout[i] = PO;
+    if (delta) delta[i] = DL;
+  }
+  grid_reduce4<kThreads>(acc, partials, counter, [&](const ReducePartials& t) {
+    sc->ssn = t.ssn;
+    sc->changed = t.changed;
+    sc->loss = has_target ? t.loss : nan("");
+    sc->nonfinite = t.nonfinite;
+    sc->ssn_used = ssn_in;
+  });
+}
+
+// ------------------------------------------------------- standalone steps
+template <class T>
+__global__ void moment2_kernel(int64_t n, double c, bool first, T* __restrict__ m2,
+                               const T* __restrict__ x) {
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += int64_t(gridDim.x) * blockDim.x) {
+    const T old = first ? T(0) : m2[i];
+    const T xi = x[i];
+    m2[i] = old + T(c) * (xi * xi - old);  // moment2.hpp:38
+  }
+}
+
+template <class T>
+__global__ void negvar_check_kernel(int64_t n, const T* __restrict__ a, const T* __restrict__ b,
+                                    int* flag) {
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += int64_t(gridDim.x) * blockDim.x)
+    if (a[i] < T(0) || b[i] < T(0)) *flag = 1;  // meta.hpp:100
+}
+
+template <class T>
+__global__ void meta_step_kernel(int64_t n, MetaK k, bool first, T* __restrict__ mean,
+                                 T* __restrict__ var, T* __restrict__ ap,
+                                 const T* __restrict__ prop, const T* __restrict__ diff,
+                                 const T* __restrict__ vp, const T* __restrict__ vd,
+                                 T* __restrict__ delta) {
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += int64_t(gridDim.x) * blockDim.x) {
+    T m = (first ? T(0) : mean[i]) + diff[i];
+    T v = (first ? T(0) : var[i]) + vd[i];
+    const T a_prev = first ? T(-INFINITY) : ap[i];
+    const T vpi = vp[i];
+    T al = vpi / ((vpi + v) + T(k.eps_alpha));
+    if (k.clip) al = std_min(al, T(1) / (T(2) - a_prev));
+    ap[i] = al;
+    const T om = T(1) - al;
+    m = al * m + om * prop[i];
+    v = (al * al) * v + (om * om) * vpi;
+    mean[i] = m;
+    var[i] = v;
+    delta[i] = (T(-k.lr) * m) / (sqrt(v) + T(k.eps_step));
+  }
+}
+
+template <class T>
+__global__ void adam_step_kernel(int64_t n, AdamK k, bool first, T* __restrict__ m,
+                                 T* __restrict__ v, const T* __restrict__ g,
+                                 T* __restrict__ delta) {
+  ReducePartials dummy{0, 0, 0, 0};
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += int64_t(gridDim.x) * blockDim.x) {
+    T M = first ? T(0) : m[i], V = first ? T(0) : v[i], PO, DL;
+    adam_elem<T>(k, g[i], M, V, T(0), T(0), false, PO, DL, dummy);
+    m[i] = M;
+    v[i] = V;
+    if (delta) delta[i] = DL;
+  }
+}
+
+template <class T>
+int launch_meta_update(mg_ctx* ctx, int64_t n, const MetaK& k, const MetaPtrs<T>& q, bool first,
+                       mg_update_scalars* sc) {
+  const bool vec = aligned16(q.prop) && aligned16(q.diff) && aligned16(q.m2p) &&
+                   aligned16(q.m2d) && aligned16(q.mean) && aligned16(q.var) &&
+                   aligned16(q.ap) && aligned16(q.pin) && aligned16(q.pout) &&
+                   (!q.vprop || aligned16(q.vprop)) && (!q.vdiff || aligned16(q.vdiff)) &&
+                   (!q.pprev || aligned16(q.pprev)) && (!q.target || aligned16(q.target)) &&
+                   (!q.delta || aligned16(q.delta));
+  const int64_t items = vec ? (n + VecOf<T>::width - 1) / VecOf<T>::width : n;
+  const int grid = grid_for(ctx, items, kThreads, 8);
+  auto run = [&](auto kernel) {
+    kernel<<<grid, kThreads, 0, ctx->stream>>>(n, k, q, sc, ctx->partials, ctx->counter);
+  };
+  if (first)
+    vec ? run(meta_update_kernel<T, true, true>) : run(meta_update_kernel<T, true, false>);
+  else
+    vec ? run(meta_update_kernel<T, false, true>) : run(meta_update_kernel<T, false, false>);
+  MG_LAUNCH_CHECK(ctx);
+  return MG_OK;
+}
+
+template <class T>
+int launch_adam_update(mg_ctx* ctx, int64_t n, const AdamK& k, bool first, const T* grad, T* m,
+                       T* v, const T* pin, T* pout, const T* target, T* delta,
+                       mg_update_scalars* sc) {
+  const bool vec = aligned16(grad) && aligned16(m) && aligned16(v) && aligned16(pin) &&
+                   aligned16(pout) && (!target || aligned16(target)) &&
+                   (!delta || aligned16(delta));
+  const int64_t items = vec ? (n + VecOf<T>::width - 1) / VecOf<T>::width : n;
+  const int grid = grid_for(ctx, items, kThreads, 8);
+  auto run = [&](auto kernel) {
+    kernel<<<grid, kThreads, 0, ctx->stream>>>(n, k, grad, m, v, pin, pout, target, delta, sc,
+                                                ctx->partials, ctx->counter);
+  };
+  if (first)
+    vec ? run(adam_update_kernel<T, true, true>) : run(adam_update_kernel<T, true, false>);
+  else
+    vec ? run(adam_update_kernel<T, false, true>) : run(adam_update_kernel<T, false, false>);
+  MG_LAUNCH_CHECK(ctx);
+  return MG_OK;
+}
+
+MetaK make_meta_k(const mg_meta_update_args* a) {
+  MetaK k;
+  k.lr = a->meta.lr;
+  k.eps_step = a->meta.eps_step;
+  k.eps_alpha = a->meta.eps_alpha;
+  k.clip = a->meta.clip_enabled;
+  k.prop_coef = a->prop_coef;
+  k.beta_delta = a->beta_delta;
+  k.diff_norm = a->diff_norm;
+  k.project = a->project;
+  k.proj_lo = a->proj_lo;
+  k.ssn_from_host = a->ssn_from_host;
+  k.ssn_host = a->ssn_host;
+  return k;
+}
+
+// Advances the host-side Adam scalars exactly as adam.hpp:29-31 and returns
+// the kernel constants.
+AdamK advance_adam(mg_adam_scalars* s, int project, double proj_lo) {
+  s->t += 1;
+  s->beta1_pow *= s->beta1;
+  s->beta2_pow *= s->beta2;
+  AdamK k;
+  k.beta1 = s->beta1;
+  k.beta2 = s->beta2;
+  k.c1 = 1.0 - s->beta1;
+  k.c2 = 1.0 - s->beta2;
+  k.d1 = 1.0 - s->beta1_pow;
+  k.d2 = 1.0 - s->beta2_pow;
+  k.lr = s->lr;
+  k.eps = s->eps;
+  k.project = project;
+  k.proj_lo = proj_lo;
+  return k;
+}
+
+}  // namespace
+}  // namespace mg
+
+using namespace mg;
+
+extern "C" {
+
+int mg_meta_update(mg_ctx* ctx, int32_t dtype, int64_t n, const mg_meta_update_args* a,
+                   const void* prop, const void* diff, void* m2_prop, void* m2_diff, void* mean,
+                   void* var, void* alpha_prev, const void* params_in, void* params_out,
+                   mg_update_scalars* scalars, const mg_meta_extras* x) {
+  if (!ctx || !a || !scalars) return fail(MG_EINVAL, "mg_meta_update: null argument");
+  if (n < 0) return fail(MG_EINVAL, "mg_meta_update: negative dimension");
+  if (n == 0) return MG_OK;
+  if (!prop || !diff || !m2_prop || !m2_diff || !mean || !var || !alpha_prev || !params_in ||
+      !params_out)
+    return fail(MG_EINVAL, "mg_meta_update: null buffer");
+  if (a->diff_norm == MG_DIFF_NORM_PER_PARAM && !(x && x->params_prev))
+    return fail(MG_EINVAL, "mg_meta_update: per-param diff norm needs params_prev");
+  if (!(a->meta.lr > 0.0)) return fail(MG_EINVAL, "MetaEstimator: lr must be positive");
+  const MetaK k = make_meta_k(a);
+  const mg_meta_extras none{};
+  const mg_meta_extras& e = x ? *x : none;
+  if (dtype == MG_F32) {
+    MetaPtrs<float> q{(const float*)prop, (const float*)diff, (const float*)e.vprop,
+                      (const float*)e.vdiff, (float*)m2_prop, (float*)m2_diff, (float*)mean,
+                      (float*)var, (float*)alpha_prev, (const float*)params_in,
+                      (float*)params_out, (const float*)e.params_prev, (const float*)e.target,
+                      (float*)e.delta_out};
+    return launch_meta_update<float>(ctx, n, k, q, a->first_step != 0, scalars);
+  }
+  if (dtype == MG_F64) {
+    MetaPtrs<double> q{(const double*)prop, (const double*)diff, (const double*)e.vprop,
+                       (const double*)e.vdiff, (double*)m2_prop, (double*)m2_diff, (double*)mean,
+                       (double*)var, (double*)alpha_prev, (const double*)params_in,
+                       (double*)params_out, (const double*)e.params_prev,
+                       (const double*)e.target, (double*)e.delta_out};
+    return launch_meta_update<double>(ctx, n, k, q, a->first_step != 0, scalars);
+  }
+  return fail(MG_EINVAL, "mg_meta_update: unknown dtype");
+}
+
+int mg_adam_update(mg_ctx* ctx, int32_t dtype, int64_t n, mg_adam_scalars* s, int32_t project,
+                   double proj_lo, const void* grad, void* m, void* v, const void* params_in,
+                   void* params_out, const void* target, mg_update_scalars* scalars) {
+  if (!ctx || !s || !scalars) return fail(MG_EINVAL, "mg_adam_update: null argument");
+  if (n < 0) return fail(MG_EINVAL, "mg_adam_update: negative dimension");
+  if (n == 0) return MG_OK;
+  const bool first = s->t == 0;
+  const AdamK k = advance_adam(s, project, proj_lo);
+  if (dtype == MG_F32)
+    return launch_adam_update<float>(ctx, n, k, first, (const float*)grad, (float*)m, (float*)v,
+                                     (const float*)params_in, (float*)params_out,
+                                     (const float*)target, nullptr, scalars);
+  if (dtype == MG_F64)
+    return launch_adam_update<double>(ctx, n, k, first, (const double*)grad, (double*)m,
+                                      (double*)v, (const double*)params_in, (double*)params_out,
+                                      (const double*)target, nullptr, scalars);
+  return fail(MG_EINVAL, "mg_adam_update: unknown dtype");
+}
+
+int mg_moment2_step(mg_ctx* ctx, int32_t dtype, int64_t n, mg_moment2_scalars* s, void* m2,
+                    const void* x) {
+  if (!ctx || !s) return fail(MG_EINVAL, "mg_moment2_step: null argument");
+  if (!(s->decay >= 0.0 && s->decay < 1.0))
+    return fail(MG_EINVAL, "Moment2: decay must lie in [0, 1)");
+  const bool first = s->count == 0;
+  s->count += 1;                      // moment2.hpp:34
+  s->decay_pow *= s->decay;           // moment2.hpp:35
+  const double w = 1.0 - s->decay;    // moment2.hpp:36
+  const double w_sum = 1.0 - s->decay_pow;
+  const double c = w / w_sum;
+  if (n == 0) return MG_OK;
+  const int grid = grid_for(ctx, n, 256, 8);
+  if (dtype == MG_F32)
+    moment2_kernel<float><<<grid, 256, 0, ctx->stream>>>(n, c, first, (float*)m2, (const float*)x);
+  else if (dtype == MG_F64)
+    moment2_kernel<double><<<grid, 256, 0, ctx->stream>>>(n, c, first, (double*)m2,
+                                                          (const double*)x);
+  else
+    return fail(MG_EINVAL, "mg_moment2_step: unknown dtype");
+  MG_LAUNCH_CHECK(ctx);
+  return MG_OK;
+}
+
+int mg_meta_step(mg_ctx* ctx, int32_t dtype, int64_t n, const mg_meta_params* p,
+                 int32_t first_call, void* mean, void* var, void* alpha_prev, const void* prop,
+                 const void* diff, const void* var_prop, const void* var_diff, void* delta) {
+  if (!ctx || !p) return fail(MG_EINVAL, "mg_meta_step: null argument");
+  if (!(p->lr > 0.0)) return fail(MG_EINVAL, "MetaEstimator: lr must be positive");
+  if (n == 0) return MG_OK;
+  if (dtype != MG_F32 && dtype != MG_F64) return fail(MG_EINVAL, "mg_meta_step: unknown dtype");
+  const int grid = grid_for(ctx, n, 256, 8);
+  MG_CUDA_TRY(cudaMemsetAsync(ctx->flag, 0, sizeof(int), ctx->stream));
+  if (dtype == MG_F32)
+    negvar_check_kernel<float><<<grid, 256, 0, ctx->stream>>>(n, (const float*)var_prop,
+                                                              (const float*)var_diff, ctx->flag);
+  else
+    negvar_check_kernel<double><<<grid, 256, 0, ctx->stream>>>(n, (const double*)var_prop,
+                                                               (const double*)var_diff, ctx->flag);
+  MG_LAUNCH_CHECK(ctx);
+  int flag = 0;
+  MG_CUDA_TRY(cudaMemcpyAsync(&flag, ctx->flag, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+  MG_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+  if (flag) return fail(MG_ELOGIC, "MetaEstimator: negative variance input");
+  MetaK k{};
+  k.lr = p->lr;
+  k.eps_step = p->eps_step;
+  k.eps_alpha = p->eps_alpha;
+  k.clip = p->clip_enabled;
+  if (dtype == MG_F32)
+    meta_step_kernel<float><<<grid, 256, 0, ctx->stream>>>(
+        n, k, first_call != 0, (float*)mean, (float*)var, (float*)alpha_prev, (const float*)prop,
+        (const float*)diff, (const float*)var_prop, (const float*)var_diff, (float*)delta);
+  else
+    meta_step_kernel<double><<<grid, 256, 0, ctx->stream>>>(
+        n, k, first_call != 0, (double*)mean, (double*)var, (double*)alpha_prev,
+        (const double*)prop, (const double*)diff, (const double*)var_prop,
+        (const double*)var_diff, (double*)delta);
+  MG_LAUNCH_CHECK(ctx);
+  return MG_OK;
+}
+
+int mg_adam_step(mg_ctx* ctx, int32_t dtype, int64_t n, mg_adam_scalars* s, void* m, void* v,
+                 const void* grad, void* delta) {
+  if (!ctx || !s) return fail(MG_EINVAL, "mg_adam_step: null argument");
+  if (!(s->lr > 0.0)) return fail(MG_EINVAL, "Adam: lr must be positive");
+  if (!(s->beta1 >= 0.0 && s->beta1 < 1.0) || !(s->beta2 >= 0.0 && s->beta2 < 1.0))
+    return fail(MG_EINVAL, "Adam: betas must lie in [0, 1)");
+  const bool first = s->t == 0;
+  const AdamK k = advance_adam(s, 0, 0.0);
+  if (n == 0) return MG_OK;
+  const int grid = grid_for(ctx, n, 256, 8);
+  if (dtype == MG_F32)
+    adam_step_kernel<float><<<grid, 256, 0, ctx->stream>>>(n, k, first, (float*)m, (float*)v,
+                                                           (const float*)grad, (float*)delta);
+  else if (dtype == MG_F64)
+    adam_step_kernel<double><<<grid, 256, 0, ctx->stream>>>(n, k, first, (double*)m, (double*)v,
+                                                            (const double*)grad, (double*)delta);
+  else
+    return fail(MG_EINVAL, "mg_adam_step: unknown dtype");
+  MG_LAUNCH_CHECK(ctx);
+  return MG_OK;
+}
+
+}  // extern "C"

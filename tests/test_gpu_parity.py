@@ -1,0 +1,407 @@
+"""GPU parity: every kernel on the hot path against the oracle / reference
+goldens, through the C-ABI (via paper_2309_15676_b200.api).
+
+Tolerances:
+  * fp64 elementwise arithmetic (Moment2, MetaEstimator, Adam, fused update,
+    mult-noise sampling, RNG streams): BIT-EXACT (library built --fmad=false,
+    same operation order as the reference).
+  * fp64 values through CUDA pow/log (mini-render, exp-rate): <= 4 ulp
+    per value; the fraction of pixels that differ at all is reported.
+  * fp64 device reductions over > 4096 elements (tree order): rel 1e-12.
+  * fp32 fast mode vs the fp64 oracle on the same inputs: rel 1e-4 (with a
+    scale floor stated per test).
+"""
+import ast
+
+import numpy as np
+import pytest
+import torch
+
+from paper_2309_15676_b200 import _abi
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def api():
+    from paper_2309_15676_b200 import api as a
+    return a
+
+
+def cu(x, dt=torch.float64):
+    return torch.as_tensor(np.asarray(x), dtype=dt, device="cuda").contiguous()
+
+
+def host(t):
+    return t.detach().double().cpu().numpy()
+
+
+def bits_equal(a, b):
+    a, b = np.asarray(a, dtype=np.float64), np.asarray(b, dtype=np.float64)
+    return a.shape == b.shape and np.array_equal(a.view(np.uint64), b.view(np.uint64))
+
+
+def ulp_diff(a, b):
+    a = np.asarray(a, dtype=np.float64).view(np.int64)
+    b = np.asarray(b, dtype=np.float64).view(np.int64)
+    return np.abs(a - b)
+
+
+# ------------------------------------------------------------------ A1 RNG
+@pytest.mark.parametrize("s", [0, 7, 42])
+def test_mt64_streams_bit_exact(api, golden, s):
+    g = golden("rng")
+    reps = [0, 1, 999]
+    rng = api.Rng.streams(s, reps)
+    raw = rng.raw(2000).cpu().numpy()
+    for i, r in enumerate(reps):
+        assert np.array_equal(raw[i], g[f"rng_raw_s{s}_r{r}"])
+    rng = api.Rng.streams(s, reps)
+    u = rng.uniform(700)
+    u2 = rng.uniform(1300)  # continues the stream across calls / twists
+    uni = torch.cat([u, u2], 1).cpu().numpy()
+    for i, r in enumerate(reps):
+        assert bits_equal(uni[i], g[f"rng_uni_s{s}_r{r}"])
+    up = api.Rng.streams(s, reps).uniform_pos(2000).cpu().numpy()
+    for i, r in enumerate(reps):
+        assert bits_equal(up[i], g[f"rng_upos_s{s}_r{r}"])
+
+
+def test_mt64_long_stream_checksum(api, golden):
+    g = golden("rng")
+    raw = api.Rng.streams(42, [999]).raw(100000).cpu().numpy()[0]
+    assert np.bitwise_xor.reduce(raw) == g["rng_xor_s42_r999"]
+    assert np.sum(raw, dtype=np.uint64) == g["rng_sum_s42_r999"]
+    eng = api.Rng([5489]).raw(10000).cpu().numpy()[0]
+    assert int(eng[-1]) == 9981545732273789042  # C++ [rand.predef]
+
+
+# ------------------------------------------------------- A2-A7 problems
+@pytest.mark.parametrize("P,seed", [(16, 2024), (4096, 1), (8, 1234)])
+def test_minirender_generate(api, golden, P, seed):
+    g = golden("problems")
+    prob = api.MiniRenderProblem(P, 4, seed)
+    assert bits_equal(host(prob.exponents), g[f"gen_P{P}_s{seed}_b"])
+    assert bits_equal(host(prob.target), g[f"gen_P{P}_s{seed}_T"])
+
+
+@pytest.mark.parametrize("P,spp,seed", [(16, 4, 2024), (4096, 2, 1), (6, 3, 11)])
+def test_minirender_sample_pair_f64(api, golden, P, spp, seed, record_property):
+    g = golden("problems")
+    prob = api.MiniRenderProblem(P, spp, seed)
+    now, prev = g[f"sp_P{P}_spp{spp}_now"], g[f"sp_P{P}_spp{spp}_prev"]
+    rng = api.Rng.stream(909, 3)
+    pair = None
+    for _ in range(3):  # skip 2 then compare the third pair too
+        pair_k = prob.sample_pair(cu(now), cu(prev), rng)
+        pair = pair if pair is not None else pair_k
+    for k, pr in ((0, pair), (2, pair_k)):
+        ref_prop = g[f"sp_P{P}_spp{spp}_k{k}_prop"]
+        ref_diff = g[f"sp_P{P}_spp{spp}_k{k}_diff"]
+        up = ulp_diff(host(pr.prop), ref_prop)
+        ud = ulp_diff(host(pr.diff), ref_diff)
+        frac = float(np.mean((up > 0) | (ud > 0)))
+        record_property(f"pixel_fraction_differing_k{k}", frac)
+        assert up.max() <= 64 and ud.max() <= 64, (up.max(), ud.max())
+        np.testing.assert_allclose(host(pr.prop), ref_prop, rtol=1e-13, atol=1e-15)
+        np.testing.assert_allclose(host(pr.diff), ref_diff, rtol=1e-13, atol=1e-15)
+        assert pr.step_sq_norm == pytest.approx(float(g[f"sp_P{P}_spp{spp}_k{k}_ssn"]), rel=1e-13)
+    same = prob.sample_pair(cu(now), cu(now), api.Rng.stream(909, 3))
+    assert (host(same.diff) == 0).all() and same.step_sq_norm == 0.0
+
+
+def test_minirender_sample_pair_f32(api, oracle):
+    P, spp = 4096, 2
+    prob = api.MiniRenderProblem(P, spp, 1)
+    rs = np.random.RandomState(1)
+    now = (0.1 + rs.random_sample(P)).astype(np.float32)
+    prev = (now - 0.01 * rs.random_sample(P)).astype(np.float32)
+    pair = prob.sample_pair(cu(now, torch.float32), cu(prev, torch.float32), api.Rng.stream(5, 0))
+    b, T = oracle.minirender_generate(P, 1)
+    rp, rd, rssn = oracle.minirender_sample_pair(spp, b, T, now.astype(np.float64),
+                                                 prev.astype(np.float64), 5, 0)
+    # relative to the magnitude of the two terms of prop (cancellation-aware)
+    scale = 2 * np.abs(now) * 5 ** 2 + 2 * T * 5
+    err = np.abs(host(pair.prop) - rp) / scale
+    assert np.max(err) < 1e-5
+    np.testing.assert_allclose(host(pair.diff), rd, rtol=1e-4, atol=1e-7)
+
+
+def test_exprate_sample_pair(api, golden):
+    g = golden("problems")
+    rows = g["exprate"]
+    prob = api.ExpRateProblem(2.0, 32)
+    for now, prev in ((2.0, 2.0), (1.25, 1.3), (0.8, 0.9), (0.5, 0.5)):
+        rng = api.Rng.stream(808, 7)
+        pairs = [prob.sample_pair(cu([now]), cu([prev]), rng) for _ in range(6)]
+        for skip in (0, 1, 5):
+            ref = [r for r in rows if r[0] == now and r[1] == prev and r[2] == skip][0]
+            p = pairs[skip]
+            np.testing.assert_allclose(host(p.prop)[0], ref[3], rtol=1e-13)
+            np.testing.assert_allclose(host(p.diff)[0], ref[4], rtol=1e-11, atol=1e-15)
+            assert host(p.step_sq_norm)[0] == ref[5]
+    with pytest.raises(api.DomainError):
+        prob.sample_pair(cu([-0.5]), cu([1.0]), api.Rng.stream(1, 0))
+
+
+def test_multnoise_sample_pair_bit_exact(api, golden):
+    g = golden("problems")
+    prob = api.MultNoiseQuadratic(torch.zeros(4), 1.0, 2)
+    now = cu([1.5, -0.7, 2.2, 0.3])
+    prev = cu([1.45, -0.75, 2.14, 0.33])
+    rng = api.Rng.stream(404, 0)
+    pairs = [prob.sample_pair(now, prev, rng) for _ in range(4)]
+    for skip in (0, 3):
+        assert bits_equal(host(pairs[skip].prop), g[f"mn_k{skip}_prop"])
+        assert bits_equal(host(pairs[skip].diff), g[f"mn_k{skip}_diff"])
+        assert pairs[skip].step_sq_norm == float(g[f"mn_k{skip}_ssn"])
+
+
+# ------------------------------------------------------ A8-A12 estimators
+@pytest.mark.parametrize("decay", [0.5, 0.9, 0.99])
+def test_moment2_bit_exact(api, golden, decay):
+    g = golden("estimators")
+    xs = g[f"m2_d{decay}_xs"]
+    m = api.Moment2(decay)
+    out = []
+    for row in xs:
+        m.step(cu(row))
+        out.append(host(m.m2()))
+    assert bits_equal(np.stack(out), g[f"m2_d{decay}_out"])
+    assert m.count() == len(xs)
+
+
+@pytest.mark.parametrize("k", [0, 1, 2])
+def test_meta_step_bit_exact(api, golden, k):
+    g = golden("estimators")
+    prop, diff, vp, vd = g[f"meta{k}_in"]
+    meta = api.MetaEstimator(0.01)
+    meta.clip_enabled = bool(g[f"meta{k}_clip"])
+    if f"meta{k}_state_in" in g:
+        m, v, a = g[f"meta{k}_state_in"]
+        meta.mean, meta.var, meta.alpha_prev = cu(m), cu(v), cu(a)
+    delta = meta.step(api.GradientSamplePair(cu(prop), cu(diff), 0.02), cu(vp), cu(vd))
+    out = np.stack([host(meta.mean), host(meta.var), host(meta.alpha_prev)])
+    assert bits_equal(out, g[f"meta{k}_state_out"])
+    assert bits_equal(host(delta), g[f"meta{k}_delta"])
+
+
+def test_meta_step_errors(api):
+    meta = api.MetaEstimator(0.01)
+    pair = api.GradientSamplePair(cu(np.zeros(2)), cu(np.zeros(2)))
+    with pytest.raises(api.InvalidArgument):
+        meta.step(pair, cu(np.zeros(3)), cu(np.zeros(2)))
+    with pytest.raises(api.LogicError):
+        meta.step(pair, cu([-1.0, 0.0]), cu(np.zeros(2)))
+    with pytest.raises(api.InvalidArgument):
+        api.MetaEstimator(0.0)
+
+
+def test_meta_harmonic_running_average(api):
+    # tests/test_meta.cpp:98-114 / acceptance criterion 2 on the device
+    v = 1.5
+    rs = np.random.RandomState(99)
+    meta = api.MetaEstimator(0.01)
+    props = 0.5 + rs.random_sample(2000)
+    run_avg = 0.0
+    for i, p in enumerate(props):
+        meta.step(api.GradientSamplePair(cu([p]), cu([0.0])), cu([v]), cu([0.0]))
+        run_avg += (p - run_avg) / (i + 1)
+    assert abs(host(meta.var)[0] - v / 2000) <= 1e-12 * v / 2000
+    assert abs(host(meta.mean)[0] - run_avg) <= 1e-12
+
+
+def test_adam_bit_exact(api, golden):
+    g = golden("estimators")
+    adam = api.Adam(0.02)
+    d = None
+    for row in g["adam_grads"]:
+        d = adam.step(cu(row))
+    assert bits_equal(host(adam.m()), g["adam_m"])
+    assert bits_equal(host(adam.v()), g["adam_v"])
+    assert bits_equal(host(d), g["adam_delta"])
+
+
+# ------------------------------------------------- fused hot-path update
+def make_inputs(n, steps, seed=0, dt=np.float64):
+    rs = np.random.RandomState(seed)
+    mu = rs.uniform(-1, 1, n)
+    sig = rs.uniform(0.1, 2, n)
+    props = [(mu + sig * rs.standard_normal(n)).astype(dt) for _ in range(steps)]
+    diffs = [np.zeros(n, dt)] + [(0.1 * sig * rs.standard_normal(n)).astype(dt)
+                                 for _ in range(steps - 1)]
+    return props, diffs
+
+
+def oracle_state(n):
+    return {k: np.zeros(n) for k in ("m2_prop", "m2_diff", "mean", "var", "alpha_prev")}
+
+
+@pytest.mark.parametrize("n", [1, 3, 1000, 4099, 65536 + 5])
+def test_fused_meta_update_f64_bit_exact_per_step(api, oracle, n):
+    """Elementwise outputs bit-exact when both sides use the same step norm
+    (the oracle's sequential ssn is handed to the kernel as ssn_host)."""
+    steps = 6
+    props, diffs = make_inputs(n, steps, seed=n)
+    target = np.random.RandomState(1).uniform(0, 1, n)
+    upd = api.FusedMetaUpdate(n, dtype=torch.float64, lr=0.01, project_lo=0.0)
+    st = oracle_state(n)
+    sc = _abi.fresh_scalars()
+    p_host = np.full(n, 0.1)
+    pa, pb = cu(p_host), torch.empty(n, dtype=torch.float64, device="cuda")
+    beta_pow = 1.0
+    for t in range(steps):
+        beta_pow *= 0.9
+        a = _abi.MetaUpdateArgs(meta=_abi.MetaParams(0.01, 1e-8, 1e-30, 1),
+                                prop_coef=(1 - 0.9) / (1 - beta_pow), beta_delta=0.5,
+                                first_step=int(t == 0), diff_norm=0, project=1,
+                                ssn_from_host=1, proj_lo=0.0, ssn_host=sc.ssn)
+        p_new, delta, rc = oracle.meta_update(a, st, props[t], diffs[t], p_host, sc, target=target)
+        assert rc == 0
+        upd.step(cu(props[t]), cu(diffs[t]), pa, pb, target=cu(target), ssn_host=a.ssn_host)
+        dsc = upd.scalars()
+        assert bits_equal(host(pb), p_new), t
+        for k, buf in (("m2_prop", upd.m2_prop), ("mean", upd.mean), ("var", upd.var),
+                       ("alpha_prev", upd.alpha_prev)):
+            assert bits_equal(host(buf), st[k]), (t, k)
+        if sc.diff_count > 0:
+            assert bits_equal(host(upd.m2_diff), st["m2_diff"]), t
+        assert dsc.diff_count == sc.diff_count and dsc.diff_decay_pow == sc.diff_decay_pow
+        assert dsc.changed == sc.changed and dsc.nonfinite == sc.nonfinite
+        np.testing.assert_allclose(dsc.ssn, sc.ssn, rtol=1e-12)
+        np.testing.assert_allclose(dsc.loss, sc.loss, rtol=1e-12)
+        p_host = p_new
+        pa, pb = pb, pa
+
+
+def test_fused_meta_update_f64_device_ssn_chain(api, oracle):
+    """100 steps with the step norm produced on the device (tree order):
+    trajectories agree with the sequential oracle to 1e-10 relative."""
+    n, steps = 50000, 100
+    props, diffs = make_inputs(n, 8, seed=3)
+    upd = api.FusedMetaUpdate(n, dtype=torch.float64, lr=0.01)
+    st = oracle_state(n)
+    sc = _abi.fresh_scalars()
+    p_host = np.zeros(n)
+    pa, pb = cu(p_host), torch.empty(n, dtype=torch.float64, device="cuda")
+    dprops = [cu(x) for x in props]
+    ddiffs = [cu(x) for x in diffs]
+    beta_pow = 1.0
+    for t in range(steps):
+        beta_pow *= 0.9
+        a = _abi.MetaUpdateArgs(meta=_abi.MetaParams(0.01, 1e-8, 1e-30, 1),
+                                prop_coef=(1 - 0.9) / (1 - beta_pow), beta_delta=0.5,
+                                first_step=int(t == 0))
+        k = t % 8 if t else 0
+        p_host, _, rc = oracle.meta_update(a, st, props[k], diffs[k] if t else np.zeros(n),
+                                           p_host, sc)
+        upd.step(dprops[k], ddiffs[k] if t else ddiffs[0], pa, pb)
+        pa, pb = pb, pa
+    np.testing.assert_allclose(host(pa), p_host, rtol=1e-10, atol=1e-14)
+    np.testing.assert_allclose(host(upd.mean), st["mean"], rtol=1e-9, atol=1e-14)
+    np.testing.assert_allclose(upd.scalars().ssn, sc.ssn, rtol=1e-9)
+
+
+def test_fused_meta_update_f32_tolerance(api, oracle):
+    """fp32 fast mode vs the fp64 oracle on the same (fp32) inputs, 100 steps,
+    BASELINE configs[1] distributions: rel <= 1e-4 (floor 1e-6 abs on params)."""
+    n, steps = 1 << 16, 100
+    props, diffs = make_inputs(n, 8, seed=4, dt=np.float32)
+    upd = api.FusedMetaUpdate(n, dtype=torch.float32, lr=0.01)
+    st = oracle_state(n)
+    sc = _abi.fresh_scalars()
+    p_host = np.zeros(n)
+    pa = torch.zeros(n, dtype=torch.float32, device="cuda")
+    pb = torch.empty_like(pa)
+    dprops = [cu(x, torch.float32) for x in props]
+    ddiffs = [cu(x, torch.float32) for x in diffs]
+    beta_pow = 1.0
+    for t in range(steps):
+        beta_pow *= 0.9
+        a = _abi.MetaUpdateArgs(meta=_abi.MetaParams(0.01, 1e-8, 1e-30, 1),
+                                prop_coef=(1 - 0.9) / (1 - beta_pow), beta_delta=0.5,
+                                first_step=int(t == 0))
+        k = t % 8
+        p_host, _, _ = oracle.meta_update(a, st, props[k].astype(np.float64),
+                                          diffs[k].astype(np.float64), p_host, sc)
+        upd.step(dprops[k], ddiffs[k], pa, pb)
+        pa, pb = pb, pa
+    rel = np.abs(host(pa) - p_host) / np.maximum(np.abs(p_host), 1e-2)
+    assert np.max(rel) < 1e-4, np.max(rel)
+    for name in ("mean", "var", "alpha_prev", "m2_prop"):
+        ref = st[name]
+        got = host(getattr(upd, name))
+        assert np.max(np.abs(got - ref) / np.maximum(np.abs(ref), 1e-3)) < 1e-4, name
+
+
+def test_fused_update_unaligned_and_tail(api, oracle):
+    """Scalar path (unaligned views) and vector tails give the same bits."""
+    n = 1029
+    props, diffs = make_inputs(n + 1, 2, seed=9)
+    base = torch.zeros(n + 1, dtype=torch.float64, device="cuda")
+    a_upd = api.FusedMetaUpdate(n, dtype=torch.float64)
+    b_upd = api.FusedMetaUpdate(n, dtype=torch.float64)
+    P = cu(props[0])[1:]  # 8-byte offset: forces the scalar path
+    D = cu(diffs[1])[1:]
+    out_a = torch.empty(n, dtype=torch.float64, device="cuda")
+    out_b = torch.empty(n, dtype=torch.float64, device="cuda")
+    a_upd.step(P, D, base[1:], out_a)
+    b_upd.step(P.clone(), D.clone(), base[1:].clone(), out_b)
+    assert bits_equal(host(out_a), host(out_b))
+    assert bits_equal(host(a_upd.var), host(b_upd.var))
+
+
+def test_fused_adam_update_matches_oracle(api, oracle):
+    n = 10007
+    rs = np.random.RandomState(2)
+    grads = rs.standard_normal((5, n))
+    up = api.FusedAdamUpdate(n, dtype=torch.float64, lr=0.02)
+    s = _abi.AdamScalars(0.02, 0.9, 0.999, 1e-8, 1.0, 1.0, 0)
+    m, v = np.zeros(n), np.zeros(n)
+    sc = _abi.fresh_scalars()
+    p = np.zeros(n)
+    pa, pb = cu(p), torch.empty(n, dtype=torch.float64, device="cuda")
+    for k in range(5):
+        p = oracle.adam_update(s, grads[k], m, v, p, sc)
+        up.step(cu(grads[k]), pa, pb)
+        pa, pb = pb, pa
+    assert bits_equal(host(pa), p)
+    assert bits_equal(host(up.m), m) and bits_equal(host(up.v), v)
+
+
+# ------------------------------------------------------- A13/A14 runner
+RUNS = ["accept9_r0", "accept9_r3", "accept9_noclip_r0", "noiseless_r0", "scripted_exp_r0",
+        "exprate_r0", "exprate_adam_r0", "multnoise_indep_r0", "multnoise_perparam_r0",
+        "diverge_r0", "minirender_adam_r0", "s1_standin_r0"]
+EXACT = {"noiseless_r0", "scripted_exp_r0", "multnoise_indep_r0", "multnoise_perparam_r0",
+         "diverge_r0"}
+
+
+@pytest.mark.parametrize("key", RUNS)
+def test_run_single_matches_reference_record(api, golden, key):
+    g = golden("runs")
+    kw = ast.literal_eval(str(g[f"{key}__cfg"]))
+    rep = int(key.rsplit("_r", 1)[1])
+    cfg = api.ExperimentConfig(**kw)
+    rec = api.run_single(cfg, rep)
+    n = int(g[f"{key}__iterations_run"])
+    assert rec.iterations_run == n
+    assert rec.status == api.STATUS[int(g[f"{key}__status"])]
+    assert rec.draws_used == int(g[f"{key}__draws_used"])
+    assert rec.evals_used == int(g[f"{key}__evals_used"])
+    c = cfg.coord
+    pairs = [("loss", g[f"{key}__loss"]), ("prop", g[f"{key}__prop"][:, c]),
+             ("diff", g[f"{key}__diff"][:, c]), ("grad_est", g[f"{key}__mean_est"][:, c]),
+             ("est_var", g[f"{key}__var_est"][:, c]), ("delta", g[f"{key}__delta"][:, c]),
+             ("true_grad", g[f"{key}__true_grad"][:, c]), ("step_sq_norm", g[f"{key}__ssn"]),
+             ("param", g[f"{key}__params"][:, c])]
+    if cfg.optimizer == "meta":
+        pairs.append(("alpha", g[f"{key}__alpha"][:, c]))
+    for name, ref in pairs:
+        got = rec.series[name][:n]
+        if key in EXACT:
+            assert bits_equal(got, ref), name
+        else:
+            np.testing.assert_allclose(got, ref, rtol=1e-9, atol=1e-12, err_msg=name)
+    if n < cfg.iterations:
+        assert np.isnan(rec.series["loss"][n:]).all()
