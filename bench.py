@@ -46,6 +46,7 @@ def parse():
     ap.add_argument("--cpu-n", type=int, default=1 << 22, help="reference sample size")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--extras", action="store_true", help="also time Adam and the mini-render runner")
+    ap.add_argument("--no-tma", action="store_true", help="register-streaming kernel instead of TMA")
     return ap.parse_args()
 
 
@@ -168,6 +169,9 @@ def run_ours(args):
         pg = dist
     ctx = api.Context(local)
     stream = ctx.stream
+    if args.no_tma:
+        from paper_2309_15676_b200 import _lib
+        _lib.load().mg_set_option(b"disable_tma", 1)
     n = args.n
     dt = torch.float32 if args.dtype == "f32" else torch.float64
 
@@ -279,7 +283,8 @@ def run_ours(args):
             "config": {"workload": "meta-update-microbench (BASELINE configs[1])",
                        "params_per_gpu": n, "global_params": n * world, "pool_batches": args.pool,
                        "l2": "inputs > L2 (no flush)", "parallelism": f"param-shard x{world}",
-                       "beta_f": 0.9, "beta_delta": 0.5, "lr": 0.01},
+                       "beta_f": 0.9, "beta_delta": 0.5, "lr": 0.01,
+                       "kernel": "register-streaming" if args.no_tma else "tma-bulk-pipeline"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": None, "peak_kind": peak_kind,
                          "kernel_ms": k_ms, "algorithmic_bytes": algo_bytes},

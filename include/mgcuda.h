@@ -98,10 +98,16 @@ int mg_config_validate(const mg_experiment_config* cfg);
 
 const char* mg_last_error(void);
 int mg_abi_version(void);
+/* Process-wide tuning switches (tests/benchmarks): "disable_tma" = 1 forces
+ * the register-streaming variant of mg_meta_update instead of the TMA
+ * bulk-copy pipeline.  Unknown names -> MG_EINVAL. */
+int mg_set_option(const char* name, int64_t value);
 
 /* ---------------------------------------------------------------- context */
 typedef struct mg_ctx mg_ctx;
-/* stream: a cudaStream_t to adopt (not owned), or NULL to create one. */
+/* stream: a cudaStream_t to adopt (not owned; pass cudaStreamLegacy, i.e.
+ * (void*)1, for the legacy default stream), or NULL to create a private
+ * non-blocking stream. */
 int mg_ctx_create(int device, void* stream, mg_ctx** out);
 int mg_ctx_destroy(mg_ctx* ctx);
 int mg_ctx_synchronize(mg_ctx* ctx);

@@ -5,15 +5,7 @@ Host-side mirror of the reference `metagrad` API for the hot path
 hand-written sm_100a CUDA kernels behind the C-ABI in include/mgcuda.h.
 There is no CPU fallback: every compute call goes through libmgcuda.so and
 fails loudly if it is missing or no B200 is visible.
+
+Import `paper_2309_15676_b200.api` for the reference-style API; importing the
+package itself loads nothing.
 """
-__all__ = ["api", "lib"]
-
-
-def __getattr__(name):
-    if name == "api":
-        from . import api
-        return api
-    if name == "lib":
-        from . import _lib
-        return _lib.load()
-    raise AttributeError(name)

@@ -52,6 +52,7 @@ def load():
     sig = {
         "mg_last_error": (C.c_char_p, []),
         "mg_abi_version": (C.c_int, []),
+        "mg_set_option": (C.c_int, [C.c_char_p, C.c_int64]),
         "mg_config_defaults": (None, [P(_abi.ExperimentConfigC)]),
         "mg_config_validate": (C.c_int, [P(_abi.ExperimentConfigC)]),
         "mg_ctx_create": (C.c_int, [C.c_int, _vp, P(_vp)]),

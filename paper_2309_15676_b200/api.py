@@ -68,7 +68,10 @@ class Context:
         s = stream if stream is not None else torch.cuda.current_stream(device)
         self.stream = s
         h = C.c_void_p()
-        check(L.mg_ctx_create(device, C.c_void_p(s.cuda_stream), C.byref(h)))
+        # torch's default stream is the legacy NULL stream: adopt it as
+        # cudaStreamLegacy ((void*)1) so our kernels stay ordered with torch's
+        # copies (NULL would make mg_ctx_create create a private stream).
+        check(L.mg_ctx_create(device, C.c_void_p(s.cuda_stream or 1), C.byref(h)))
         self.h = h
 
     @classmethod

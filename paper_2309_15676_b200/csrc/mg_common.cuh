@@ -38,6 +38,14 @@ constexpr int kMaxReduceBlocks = 148 * 16;
 struct ReducePartials {
   double ssn, changed, loss, nonfinite;
 };
+// Per-thread accumulators of the fused epilogue (counts kept as integers).
+struct Acc {
+  double ssn = 0.0, loss = 0.0;
+  unsigned int changed = 0, nonfinite = 0;
+  __host__ __device__ ReducePartials partials() const {
+    return ReducePartials{ssn, double(changed), loss, double(nonfinite)};
+  }
+};
 
 }  // namespace mg
 

@@ -16,9 +16,19 @@
 // bit-identical to the oracle for the elementwise outputs.
 #include <math.h>
 
+#include <string>
+#include <type_traits>
+
 #include "mg_common.cuh"
+#include "tma.cuh"
 
 namespace mg {
+// Test/benchmark switch: force the register-streaming kernel (mg_set_option).
+bool g_disable_tma = false;
+// -1: per-dtype default measured on B200 (tools/sweep_update_variants.py):
+// fp32 -> variant 4 (3 CTAs/SM x 256 thr, 2 stages; the fp32 body is
+// issue-heavy, more warps hide it), fp64 -> variant 0 (1 CTA/SM, 4 stages).
+int g_tma_variant = -1;
 namespace {
 
 constexpr int kThreads = 256;
@@ -75,7 +85,7 @@ template <class T, bool FIRST>
 __device__ __forceinline__ void meta_elem(const MetaK& k, const StepScal& s, T prop, T diff,
                                           T vprop, T vdiff, T& m2p, T& m2d, T& mean, T& var,
                                           T& ap, T pin, T pprev, T target, bool has_target,
-                                          T& pout, T& delta, ReducePartials& acc) {
+                                          T& pout, T& delta, Acc& acc) {
   // Moment2(beta_f).step(prop): m2 += (w/w_sum) * (x^2 - m2)
   const T m2p_old = FIRST ? T(0) : m2p;
   const T cp = T(k.prop_coef);
@@ -119,12 +129,12 @@ __device__ __forceinline__ void meta_elem(const MetaK& k, const StepScal& s, T p
   // fused reductions (problems.cpp:206,214,225; harness.cpp:116)
   const double d = double(p - pin);
   acc.ssn += d * d;
-  acc.changed += (p != pin) ? 1.0 : 0.0;
+  acc.changed += (p != pin) ? 1u : 0u;
   if (has_target) {
     const double e = double(p - target);
     acc.loss += e * e;
   }
-  acc.nonfinite += isfinite(p) ? 0.0 : 1.0;
+  acc.nonfinite += isfinite(p) ? 0u : 1u;
 }
 
 template <class T, bool FIRST, bool VEC>
@@ -133,7 +143,7 @@ __global__ void __launch_bounds__(kThreads)
                        ReducePartials* partials, unsigned int* counter) {
   const StepScal s = load_step_scalars(k, sc);
   const bool has_target = q.target != nullptr;
-  ReducePartials acc{0.0, 0.0, 0.0, 0.0};
+  Acc acc;
   const int64_t tid = int64_t(blockIdx.x) * kThreads + threadIdx.x;
   const int64_t stride = int64_t(gridDim.x) * kThreads;
   constexpr int W = VEC ? VecOf<T>::width : 1;
@@ -196,7 +206,148 @@ __global__ void __launch_bounds__(kThreads)
     q.pout[i] = PO;
     if (q.delta) q.delta[i] = DL;
   }
-  grid_reduce4<kThreads>(acc, partials, counter, [&](const ReducePartials& t) {
+  grid_reduce4<kThreads>(acc.partials(), partials, counter, [&](const ReducePartials& t) {
+    sc->ssn = t.ssn;
+    sc->changed = t.changed;
+    sc->loss = has_target ? t.loss : nan("");
+    sc->nonfinite = t.nonfinite;
+    sc->diff_count = s.cnt;
+    sc->diff_decay_pow = s.dpow;
+    sc->ssn_used = s.ssn;
+  });
+}
+
+// --------------------------------------------- TMA-pipelined fused update
+// Persistent variant for the common case (global diff norm, no independent
+// variance pair): every CTA streams 4 KB tiles of up to 9 input arrays into a
+// kStages-deep shared-memory ring with 1-D bulk copies (cp.async.bulk +
+// mbarrier complete_tx), so ~100 KB per SM are in flight regardless of
+// register pressure; the 6 outputs are written straight from registers.
+constexpr int kTmaArrays = 9;  // prop diff m2p m2d mean var ap pin target
+
+// Schedules of the TMA pipeline (threads per CTA, ring depth, CTAs per SM);
+// the tile is one 16-byte pack per thread per array.  Selected with
+// mg_set_option("tma_variant", i); default g_tma_variant.
+struct TmaVariant {
+  int threads, stages, ctas_per_sm;
+};
+__host__ __device__ constexpr TmaVariant tma_variant(int i) {
+  return i == 0 ? TmaVariant{256, 4, 1}
+       : i == 1 ? TmaVariant{256, 3, 2}
+       : i == 2 ? TmaVariant{512, 3, 1}
+       : i == 3 ? TmaVariant{128, 3, 4}
+                : TmaVariant{256, 2, 3};
+}
+constexpr int kNumTmaVariants = 5;
+
+template <class T, int THREADS>
+__host__ __device__ constexpr int tma_tile() { return THREADS * VecOf<T>::width; }
+template <class T, int THREADS, int STAGES>
+constexpr size_t tma_smem_bytes() {
+  return size_t(STAGES) * kTmaArrays * tma_tile<T, THREADS>() * sizeof(T);
+}
+
+template <class T, bool FIRST, int kTmaThreads, int kTmaStages, int kMinBlocks>
+__global__ void __launch_bounds__(kTmaThreads, kMinBlocks)
+    meta_update_tma_kernel(int64_t n, MetaK k, MetaPtrs<T> q, mg_update_scalars* sc,
+                           ReducePartials* partials, unsigned int* counter) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  __shared__ __align__(8) uint64_t full[kTmaStages];
+  constexpr int TILE = tma_tile<T, kTmaThreads>();
+  constexpr int W = VecOf<T>::width;
+  static_assert(TILE == kTmaThreads * W, "one 16-byte pack per thread per array");
+  T* sbuf = reinterpret_cast<T*>(smem_raw);
+  const StepScal s = load_step_scalars(k, sc);
+  const bool has_target = q.target != nullptr;
+  const T* src[kTmaArrays] = {q.prop, q.diff, q.m2p, q.m2d, q.mean, q.var, q.ap, q.pin, q.target};
+  const bool use[kTmaArrays] = {true,  true,  !FIRST, s.cnt0 > 0, !FIRST,
+                                !FIRST, !FIRST, true,  has_target};
+  uint32_t tx = 0;
+#pragma unroll
+  for (int a = 0; a < kTmaArrays; ++a) tx += use[a] ? uint32_t(TILE * sizeof(T)) : 0u;
+
+  const int64_t tiles = n / TILE;
+  const int64_t my_tiles =
+      int64_t(blockIdx.x) < tiles ? (tiles - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
+  if (threadIdx.x == 0) {
+    for (int st = 0; st < kTmaStages; ++st) mbar_init(&full[st], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  const uint64_t pol = l2_evict_first_policy();
+  auto issue = [&](int64_t li) {  // thread 0 only
+    const int st = int(li % kTmaStages);
+    const int64_t tile = int64_t(blockIdx.x) + li * gridDim.x;
+    mbar_arrive_expect_tx(&full[st], tx);
+#pragma unroll
+    for (int a = 0; a < kTmaArrays; ++a)
+      if (use[a])
+        bulk_g2s_hint(sbuf + (size_t(st) * kTmaArrays + a) * TILE, src[a] + tile * TILE,
+                      uint32_t(TILE * sizeof(T)), &full[st], pol);
+  };
+  if (threadIdx.x == 0)
+    for (int64_t li = 0; li < my_tiles && li < kTmaStages; ++li) issue(li);
+
+  Acc acc;
+  const int e = threadIdx.x * W;
+  for (int64_t li = 0; li < my_tiles; ++li) {
+    const int st = int(li % kTmaStages);
+    mbar_wait(&full[st], uint32_t((li / kTmaStages) & 1));
+    const T* sb = sbuf + size_t(st) * kTmaArrays * TILE + e;
+    const Pack<T> P = ld_plain(sb + 0 * TILE);
+    const Pack<T> D = ld_plain(sb + 1 * TILE);
+    Pack<T> M2P{}, M2D{}, ME{}, VA{}, AP{}, TG{}, PO, DL;
+    if (!FIRST) {
+      M2P = ld_plain(sb + 2 * TILE);
+      ME = ld_plain(sb + 4 * TILE);
+      VA = ld_plain(sb + 5 * TILE);
+      AP = ld_plain(sb + 6 * TILE);
+    }
+    if (s.cnt0 > 0) M2D = ld_plain(sb + 3 * TILE);
+    const Pack<T> PI = ld_plain(sb + 7 * TILE);
+    if (has_target) TG = ld_plain(sb + 8 * TILE);
+#pragma unroll
+    for (int w = 0; w < W; ++w)
+      meta_elem<T, FIRST>(k, s, P.v[w], D.v[w], P.v[w], D.v[w], M2P.v[w], M2D.v[w], ME.v[w],
+                          VA.v[w], AP.v[w], PI.v[w], T(0), TG.v[w], has_target, PO.v[w], DL.v[w],
+                          acc);
+    const int64_t b = (int64_t(blockIdx.x) + li * gridDim.x) * TILE + e;
+    st_plain(q.m2p + b, M2P);
+    if (s.active) st_plain(q.m2d + b, M2D);
+    st_plain(q.mean + b, ME);
+    st_plain(q.var + b, VA);
+    st_plain(q.ap + b, AP);
+    st_plain(q.pout + b, PO);
+    if (q.delta) st_plain(q.delta + b, DL);
+    __syncthreads();  // every thread is done reading stage st
+    if (threadIdx.x == 0 && li + kTmaStages < my_tiles) {
+      fence_proxy_async_smem();
+      issue(li + kTmaStages);
+    }
+  }
+  // tail elements [tiles*TILE, n)
+  const int64_t tid = int64_t(blockIdx.x) * kTmaThreads + threadIdx.x;
+  for (int64_t i = tiles * TILE + tid; i < n; i += int64_t(gridDim.x) * kTmaThreads) {
+    const T P = q.prop[i], D = q.diff[i];
+    T M2P = FIRST ? T(0) : q.m2p[i];
+    T M2D = s.cnt0 > 0 ? q.m2d[i] : T(0);
+    T ME = FIRST ? T(0) : q.mean[i];
+    T VA = FIRST ? T(0) : q.var[i];
+    T AP = FIRST ? T(0) : q.ap[i];
+    const T PI = q.pin[i];
+    const T TG = has_target ? q.target[i] : T(0);
+    T PO, DL;
+    meta_elem<T, FIRST>(k, s, P, D, P, D, M2P, M2D, ME, VA, AP, PI, T(0), TG, has_target, PO, DL,
+                        acc);
+    q.m2p[i] = M2P;
+    if (s.active) q.m2d[i] = M2D;
+    q.mean[i] = ME;
+    q.var[i] = VA;
+    q.ap[i] = AP;
+    q.pout[i] = PO;
+    if (q.delta) q.delta[i] = DL;
+  }
+  grid_reduce4<kTmaThreads>(acc.partials(), partials, counter, [&](const ReducePartials& t) {
     sc->ssn = t.ssn;
     sc->changed = t.changed;
     sc->loss = has_target ? t.loss : nan("");
@@ -216,7 +367,7 @@ struct AdamK {
 template <class T>
 __device__ __forceinline__ void adam_elem(const AdamK& k, T g, T& m, T& v, T pin, T target,
                                           bool has_target, T& pout, T& delta,
-                                          ReducePartials& acc) {
+                                          Acc& acc) {
   m = T(k.beta1) * m + T(k.c1) * g;          // adam.hpp:32
   v = T(k.beta2) * v + T(k.c2) * (g * g);    // adam.hpp:33
   const T mh = m / T(k.d1);                  // adam.hpp:34
@@ -227,12 +378,12 @@ __device__ __forceinline__ void adam_elem(const AdamK& k, T g, T& m, T& v, T pin
   pout = p;
   const double d = double(p - pin);
   acc.ssn += d * d;
-  acc.changed += (p != pin) ? 1.0 : 0.0;
+  acc.changed += (p != pin) ? 1u : 0u;
   if (has_target) {
     const double e = double(p - target);
     acc.loss += e * e;
   }
-  acc.nonfinite += isfinite(p) ? 0.0 : 1.0;
+  acc.nonfinite += isfinite(p) ? 0u : 1u;
 }
 
 template <class T, bool FIRST, bool VEC>
@@ -243,7 +394,7 @@ __global__ void __launch_bounds__(kThreads)
                        unsigned int* counter) {
   const double ssn_in = __ldcg(&sc->ssn);
   const bool has_target = target != nullptr;
-  ReducePartials acc{0.0, 0.0, 0.0, 0.0};
+  Acc acc;
   const int64_t tid = int64_t(blockIdx.x) * kThreads + threadIdx.x;
   const int64_t stride = int64_t(gridDim.x) * kThreads;
   constexpr int W = VEC ? VecOf<T>::width : 1;
@@ -277,7 +428,7 @@ __global__ void __launch_bounds__(kThreads)
     pout[i] = PO;
     if (delta) delta[i] = DL;
   }
-  grid_reduce4<kThreads>(acc, partials, counter, [&](const ReducePartials& t) {
+  grid_reduce4<kThreads>(acc.partials(), partials, counter, [&](const ReducePartials& t) {
     sc->ssn = t.ssn;
     sc->changed = t.changed;
     sc->loss = has_target ? t.loss : nan("");
@@ -334,7 +485,7 @@ template <class T>
 __global__ void adam_step_kernel(int64_t n, AdamK k, bool first, T* __restrict__ m,
                                  T* __restrict__ v, const T* __restrict__ g,
                                  T* __restrict__ delta) {
-  ReducePartials dummy{0, 0, 0, 0};
+  Acc dummy;
   for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
        i += int64_t(gridDim.x) * blockDim.x) {
     T M = first ? T(0) : m[i], V = first ? T(0) : v[i], PO, DL;
@@ -354,6 +505,36 @@ int launch_meta_update(mg_ctx* ctx, int64_t n, const MetaK& k, const MetaPtrs<T>
                    (!q.vprop || aligned16(q.vprop)) && (!q.vdiff || aligned16(q.vdiff)) &&
                    (!q.pprev || aligned16(q.pprev)) && (!q.target || aligned16(q.target)) &&
                    (!q.delta || aligned16(q.delta));
+  const bool tma_ok = vec && !q.vprop && !q.vdiff && k.diff_norm == MG_DIFF_NORM_GLOBAL &&
+                      n >= int64_t(tma_tile<T, 512>()) * ctx->sm_count && !g_disable_tma;
+  if (tma_ok) {
+    auto run_tma = [&](auto kernel, auto vc) {
+      constexpr TmaVariant v = tma_variant(decltype(vc)::value);
+      constexpr size_t smem = tma_smem_bytes<T, v.threads, v.stages>();
+      cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+      const int64_t tiles = n / tma_tile<T, v.threads>();
+      const int64_t want = int64_t(ctx->sm_count) * v.ctas_per_sm;
+      const int grid = int(tiles < want ? tiles : want);
+      kernel<<<grid, v.threads, smem, ctx->stream>>>(n, k, q, sc, ctx->partials, ctx->counter);
+    };
+    auto pick = [&](auto vc) {
+      constexpr TmaVariant v = tma_variant(decltype(vc)::value);
+      if (first)
+        run_tma(meta_update_tma_kernel<T, true, v.threads, v.stages, v.ctas_per_sm>, vc);
+      else
+        run_tma(meta_update_tma_kernel<T, false, v.threads, v.stages, v.ctas_per_sm>, vc);
+    };
+    const int variant = g_tma_variant >= 0 ? g_tma_variant : (sizeof(T) == 4 ? 4 : 0);
+    switch (variant) {
+      case 1: pick(std::integral_constant<int, 1>{}); break;
+      case 2: pick(std::integral_constant<int, 2>{}); break;
+      case 3: pick(std::integral_constant<int, 3>{}); break;
+      case 4: pick(std::integral_constant<int, 4>{}); break;
+      default: pick(std::integral_constant<int, 0>{}); break;
+    }
+    MG_LAUNCH_CHECK(ctx);
+    return MG_OK;
+  }
   const int64_t items = vec ? (n + VecOf<T>::width - 1) / VecOf<T>::width : n;
   const int grid = grid_for(ctx, items, kThreads, 8);
   auto run = [&](auto kernel) {
@@ -430,6 +611,20 @@ AdamK advance_adam(mg_adam_scalars* s, int project, double proj_lo) {
 using namespace mg;
 
 extern "C" {
+
+int mg_set_option(const char* name, int64_t value) {
+  if (!name) return fail(MG_EINVAL, "mg_set_option: null name");
+  if (std::string(name) == "disable_tma") {
+    g_disable_tma = value != 0;
+    return MG_OK;
+  }
+  if (std::string(name) == "tma_variant") {
+    if (value < -1 || value >= kNumTmaVariants) return fail(MG_EINVAL, "tma_variant out of range");
+    g_tma_variant = int(value);
+    return MG_OK;
+  }
+  return fail(MG_EINVAL, std::string("mg_set_option: unknown option ") + name);
+}
 
 int mg_meta_update(mg_ctx* ctx, int32_t dtype, int64_t n, const mg_meta_update_args* a,
                    const void* prop, const void* diff, void* m2_prop, void* m2_diff, void* mean,
