@@ -47,5 +47,5 @@ for name, opts in [("register", {"disable_tma": 1})] + [
     print(name, res[name], flush=True)
     del upd
 L.mg_set_option(b"disable_tma", 0)
-L.mg_set_option(b"tma_variant", 0)
+L.mg_set_option(b"tma_variant", -1)
 print(json.dumps(res))
