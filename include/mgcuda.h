@@ -115,6 +115,16 @@ void* mg_ctx_stream(mg_ctx* ctx);
 /* Number of kernels this context has launched so far (bench gpu_launches). */
 int64_t mg_ctx_launch_count(mg_ctx* ctx);
 
+/* Device memory helpers so host adapters need nothing but this library.
+ * mg_malloc/mg_free are stream-ordered on the context's stream; the copies
+ * synchronise the stream; mg_fill writes `value` (cast to dtype) n times. */
+int mg_malloc(mg_ctx* ctx, size_t bytes, void** out);
+int mg_free(mg_ctx* ctx, void* p);
+int mg_copy_to_device(mg_ctx* ctx, void* dst, const void* src, size_t bytes);
+int mg_copy_to_host(mg_ctx* ctx, void* dst, const void* src, size_t bytes);
+int mg_copy_device(mg_ctx* ctx, void* dst, const void* src, size_t bytes);
+int mg_fill(mg_ctx* ctx, int32_t dtype, int64_t n, void* dst, double value);
+
 /* -------------------------------------------------- RNG streams (row A1) */
 /* mix64 splitmix64 finaliser (rng.hpp:9-14) — host helper. */
 uint64_t mg_mix64(uint64_t x);

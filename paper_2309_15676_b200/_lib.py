@@ -60,6 +60,12 @@ def load():
         "mg_ctx_synchronize": (C.c_int, [_vp]),
         "mg_ctx_stream": (_vp, [_vp]),
         "mg_ctx_launch_count": (C.c_int64, [_vp]),
+        "mg_malloc": (C.c_int, [_vp, C.c_size_t, P(_vp)]),
+        "mg_free": (C.c_int, [_vp, _vp]),
+        "mg_copy_to_device": (C.c_int, [_vp, _vp, _vp, C.c_size_t]),
+        "mg_copy_to_host": (C.c_int, [_vp, _vp, _vp, C.c_size_t]),
+        "mg_copy_device": (C.c_int, [_vp, _vp, _vp, C.c_size_t]),
+        "mg_fill": (C.c_int, [_vp, C.c_int32, C.c_int64, _vp, C.c_double]),
         "mg_mix64": (C.c_uint64, [C.c_uint64]),
         "mg_stream_seed": (C.c_uint64, [C.c_uint64, C.c_uint64]),
         "mg_mt64_create": (C.c_int, [_vp, C.c_int32, _vp, P(_vp)]),

@@ -25,7 +25,30 @@ int cuda_fail(cudaError_t e, const char* what) {
 
 using namespace mg;
 
+namespace {
+template <class T>
+__global__ void fill_kernel(int64_t n, T* dst, T v) {
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += int64_t(gridDim.x) * blockDim.x)
+    dst[i] = v;
+}
+}  // namespace
+
 extern "C" {
+
+int mg_fill(mg_ctx* ctx, int32_t dtype, int64_t n, void* dst, double value) {
+  if (!ctx || (n && !dst)) return fail(MG_EINVAL, "mg_fill: null argument");
+  if (n <= 0) return MG_OK;
+  const int grid = grid_for(ctx, n, 256, 8);
+  if (dtype == MG_F32)
+    fill_kernel<float><<<grid, 256, 0, ctx->stream>>>(n, (float*)dst, float(value));
+  else if (dtype == MG_F64)
+    fill_kernel<double><<<grid, 256, 0, ctx->stream>>>(n, (double*)dst, value);
+  else
+    return fail(MG_EINVAL, "mg_fill: unknown dtype");
+  MG_LAUNCH_CHECK(ctx);
+  return MG_OK;
+}
 
 const char* mg_last_error(void) { return g_last_error.c_str(); }
 
@@ -169,6 +192,40 @@ int mg_scalars_write(mg_ctx* ctx, mg_update_scalars* dev, const mg_update_scalar
   if (!ctx || !dev || !host) return fail(MG_EINVAL, "mg_scalars_write: null argument");
   MG_CUDA_TRY(cudaMemcpyAsync(dev, host, sizeof(*host), cudaMemcpyHostToDevice, ctx->stream));
   MG_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+  return MG_OK;
+}
+
+int mg_malloc(mg_ctx* ctx, size_t bytes, void** out) {
+  if (!ctx || !out) return fail(MG_EINVAL, "mg_malloc: null argument");
+  *out = nullptr;
+  if (bytes == 0) return MG_OK;
+  MG_CUDA_TRY(cudaMallocAsync(out, bytes, ctx->stream));
+  return MG_OK;
+}
+
+int mg_free(mg_ctx* ctx, void* p) {
+  if (!ctx) return fail(MG_EINVAL, "mg_free: null ctx");
+  if (p) MG_CUDA_TRY(cudaFreeAsync(p, ctx->stream));
+  return MG_OK;
+}
+
+static int copy_sync(mg_ctx* ctx, void* dst, const void* src, size_t bytes, cudaMemcpyKind kind) {
+  if (!ctx || (bytes && (!dst || !src))) return fail(MG_EINVAL, "mg_copy: null argument");
+  if (bytes == 0) return MG_OK;
+  MG_CUDA_TRY(cudaMemcpyAsync(dst, src, bytes, kind, ctx->stream));
+  MG_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+  return MG_OK;
+}
+
+int mg_copy_to_device(mg_ctx* ctx, void* dst, const void* src, size_t bytes) {
+  return copy_sync(ctx, dst, src, bytes, cudaMemcpyHostToDevice);
+}
+int mg_copy_to_host(mg_ctx* ctx, void* dst, const void* src, size_t bytes) {
+  return copy_sync(ctx, dst, src, bytes, cudaMemcpyDeviceToHost);
+}
+int mg_copy_device(mg_ctx* ctx, void* dst, const void* src, size_t bytes) {
+  if (!ctx || (bytes && (!dst || !src))) return fail(MG_EINVAL, "mg_copy_device: null argument");
+  if (bytes) MG_CUDA_TRY(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToDevice, ctx->stream));
   return MG_OK;
 }
 
