@@ -36,7 +36,7 @@ BYTES_PER_PARAM = {"f32": 56, "f64": 112}  # 8 streams read + 6 written (DESIGN.
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=100)  # configs[1]: 100 steps, state carried
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--n", type=int, default=1 << 28, help="parameters per GPU")
     ap.add_argument("--dtype", default="f32", choices=["f32", "f64"])
