@@ -343,6 +343,27 @@ def extras(args, ctx):
                               "frac": 28 * n / (ms / 1e3) / 1e9 / peak}
     del g, pa, pb, ad
     torch.cuda.empty_cache()
+    # fused mini-render iteration at scale (config 5 image size x 16): one
+    # kernel per iteration, sample pair in registers, Philox draws
+    P, spp, iters = 1 << 24, 2, 50
+    run = api.MiniRenderRun(P, spp, gen_seed=1, lr=0.01, rng="philox", dtype=torch.float32,
+                            ctx=ctx)
+    for _ in range(3):
+        run.step()
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record(ctx.stream)
+    for _ in range(iters):
+        run.step()
+    b.record(ctx.stream)
+    torch.cuda.synchronize()
+    ms = a.elapsed_time(b) / iters
+    out["minirender_fused_philox_f32"] = {
+        "pixels": P, "spp": spp, "iterations": iters, "ms_per_iteration": ms,
+        "pairs_per_s": P * spp / (ms / 1e3), "gbs": 60 * P / (ms / 1e3) / 1e9,
+        "frac": 60 * P / (ms / 1e3) / 1e9 / peak, "loss": run.scalars().loss}
+    del run
+    torch.cuda.empty_cache()
     # mini-render stand-in for configs[0] (P=4096, spp=2, 200 iterations)
     cfg = api.ExperimentConfig(problem="mini-render", pixel_count=4096, spp=2, iterations=200,
                                seed=0, problem_seed=1, lr=0.01, replicates=148)

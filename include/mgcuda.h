@@ -291,6 +291,35 @@ int mg_multnoise_sample_pair(mg_ctx* ctx, int32_t replicates, int32_t dim, doubl
                              const double* now, const double* prev, double* prop, double* diff,
                              double* ssn);
 
+/* One FUSED mini-render meta iteration over P pixels: sample_pair
+ * (problems.cpp:197-217) at (pi_t, pi_{t-1}) on shared draws, then the fused
+ * update of mg_meta_update with projection max(p, 0) (problems.cpp:228); the
+ * sample pair stays in registers (optionally copied to prop_out/diff_out).
+ *   rng_kind MG_RNG_MT64 : uniforms[P*spp] are this iteration's draws of the
+ *                          replicate stream (mg_mt64_draw), pixel-major —
+ *                          the reference's exact sample stream.
+ *   rng_kind MG_RNG_PHILOX: uniform s of pixel j = Philox4x32-10 with
+ *                          counter (j, iteration, s/2, stream), key = `key`
+ *                          (statistically equivalent scale mode).
+ * params_prev_next holds pi_{t-1} on entry and pi_{t+1} on exit.
+ * exponents/target are dtype arrays [P].  "same" (diff = 0) is taken from
+ * scalars->changed == 0, the previous step's reduction. */
+typedef struct mg_render_args {
+  mg_meta_update_args update; /* meta params, prop_coef, beta_delta, first_step, ssn override */
+  int32_t spp;
+  int32_t rng_kind;
+  uint64_t key;       /* mg_stream_seed(seed, replicate) */
+  uint32_t iteration; /* Philox counter word 1 */
+  uint32_t stream;    /* Philox counter word 3 (0: main pair, 1: independent pair) */
+} mg_render_args;
+
+int mg_minirender_meta_iteration(mg_ctx* ctx, int32_t dtype, int64_t P, const mg_render_args* a,
+                                 const void* exponents, const void* target,
+                                 const double* uniforms, const void* params_now,
+                                 void* params_prev_next, void* m2_prop, void* m2_diff, void* mean,
+                                 void* var, void* alpha_prev, mg_update_scalars* scalars,
+                                 void* prop_out, void* diff_out);
+
 /* ------------------------------- device-resident run_single (A13, A14) */
 /* Per-replicate record of one coordinate plus scalars (harness.hpp:73-90;
  * full vectors are O(iterations*N) and are not recorded on the device). */

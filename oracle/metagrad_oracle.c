@@ -90,6 +90,36 @@ void mgo_rng_draws(uint64_t seed, uint64_t rep, int mode, int64_t n, void* out) 
   }
 }
 
+/* Philox4x32-10 (Salmon et al., SC'11), published algorithm; the scale-mode
+ * RNG of the device samplers (paper_2309_15676_b200/csrc/philox.cuh).
+ * ctr/out are 4 words; key is the 64-bit replicate engine seed. */
+void mgo_philox4x32_10(const uint32_t ctr[4], uint64_t key, uint32_t out[4]) {
+  uint32_t c0 = ctr[0], c1 = ctr[1], c2 = ctr[2], c3 = ctr[3];
+  uint32_t k0 = (uint32_t)key, k1 = (uint32_t)(key >> 32);
+  for (int r = 0; r < 10; ++r) {
+    const uint64_t p0 = (uint64_t)0xD2511F53u * c0, p1 = (uint64_t)0xCD9E8D57u * c2;
+    const uint32_t hi0 = (uint32_t)(p0 >> 32), lo0 = (uint32_t)p0;
+    const uint32_t hi1 = (uint32_t)(p1 >> 32), lo1 = (uint32_t)p1;
+    c0 = hi1 ^ c1 ^ k0;
+    c1 = lo1;
+    c2 = hi0 ^ c3 ^ k1;
+    c3 = lo0;
+    k0 += 0x9E3779B9u;
+    k1 += 0xBB67AE85u;
+  }
+  out[0] = c0; out[1] = c1; out[2] = c2; out[3] = c3;
+}
+
+/* uniform s of pixel j at iteration it, stream st (philox_uniform_at) */
+double mgo_philox_uniform(uint64_t key, uint32_t j, uint32_t it, uint32_t s, uint32_t st) {
+  const uint32_t ctr[4] = {j, it, s >> 1, st};
+  uint32_t o[4];
+  mgo_philox4x32_10(ctr, key, o);
+  const uint64_t a = ((uint64_t)o[0] << 21) ^ (uint64_t)(o[1] >> 11);
+  const uint64_t b = ((uint64_t)o[2] << 21) ^ (uint64_t)(o[3] >> 11);
+  return (double)((s & 1u) ? b : a) * 0x1.0p-53;
+}
+
 /* -------------------------------------------------------------- Moment2 */
 
 /* moment2.hpp:30-39: count++; decay_pow *= decay; m2 += (w/w_sum)*(x^2 - m2) */

@@ -37,6 +37,11 @@ double mgo_uniform_pos(mgo_mt64* g);
 /* same modes as ref_rng_draws (oracle/ref/ref_capi.cpp) */
 void mgo_rng_draws(uint64_t seed, uint64_t rep, int mode, int64_t n, void* out);
 
+/* Philox4x32-10 and the samplers' uniform mapping (scale mode, not in the
+ * reference; see paper_2309_15676_b200/csrc/philox.cuh) */
+void mgo_philox4x32_10(const uint32_t ctr[4], uint64_t key, uint32_t out[4]);
+double mgo_philox_uniform(uint64_t key, uint32_t j, uint32_t it, uint32_t s, uint32_t st);
+
 /* Moment2 (moment2.hpp:21-50) */
 void mgo_moment2_step(int64_t n, double decay, double* decay_pow, int64_t* count, double* m2,
                       const double* x);

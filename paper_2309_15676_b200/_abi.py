@@ -73,6 +73,11 @@ class MetaExtras(C.Structure):
                 ("target", C.c_void_p), ("delta_out", C.c_void_p)]
 
 
+class RenderArgs(C.Structure):
+    _fields_ = [("update", MetaUpdateArgs), ("spp", C.c_int32), ("rng_kind", C.c_int32),
+                ("key", C.c_uint64), ("iteration", C.c_uint32), ("stream", C.c_uint32)]
+
+
 class RunRecordC(C.Structure):
     _fields_ = [("iterations_run", C.c_int32), ("status", C.c_int32),
                 ("draws_used", C.c_int64), ("evals_used", C.c_int64)]

@@ -88,6 +88,8 @@ def load():
         "mg_exprate_sample_pair": (C.c_int, [_vp, C.c_int32, C.c_double, C.c_int32] + [_vp] * 6),
         "mg_multnoise_sample_pair": (C.c_int, [_vp, C.c_int32, C.c_int32, C.c_double,
                                                C.c_int32] + [_vp] * 7),
+        "mg_minirender_meta_iteration": (C.c_int, [_vp, C.c_int32, C.c_int64, P(_abi.RenderArgs)] +
+                                         [_vp] * 10 + [_vp, _vp, _vp]),
         "mg_run_replicates": (C.c_int, [_vp, P(_abi.ExperimentConfigC), C.c_int32, C.c_int32,
                                         _vp, P(_abi.RunSeriesC), _vp]),
     }

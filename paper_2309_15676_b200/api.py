@@ -34,7 +34,7 @@ from ._lib import DomainError, InvalidArgument, LogicError, MgError, check, load
 
 __all__ = ["Context", "Rng", "Moment2", "GradientSamplePair", "MetaEstimator", "Adam",
            "MiniRenderProblem", "ExpRateProblem", "MultNoiseQuadratic", "FusedMetaUpdate",
-           "FusedAdamUpdate", "ExperimentConfig", "RunRecord", "AggregateReport", "run_single",
+           "FusedAdamUpdate", "MiniRenderRun", "ExperimentConfig", "RunRecord", "AggregateReport", "run_single",
            "run_experiment", "InvalidArgument", "LogicError", "DomainError", "mix64"]
 
 
@@ -493,6 +493,77 @@ class FusedAdamUpdate:
                                     0.0 if self.project_lo is None else self.project_lo,
                                     _p(grad), _p(self.m), _p(self.v), _p(params_in),
                                     _p(params_out), _p(target), _p(self.scalars_buf)))
+
+
+class MiniRenderRun:
+    """One mini-render optimisation run at scale, each iteration ONE fused
+    kernel (mg_minirender_meta_iteration): sample_pair + Moment2 x2 +
+    MetaEstimator + projected update, the pair never leaving registers.
+
+    rng="mt64": the replicate's exact std::mt19937_64 stream (Rng::stream(seed,
+    replicate), pixel-major draws, problems.cpp:201-202) — bit-compatible with
+    the reference, but the stream is sequential (one CTA draws P*spp values
+    per iteration).  rng="philox": counter-based, every pixel draws its own
+    uniforms in-kernel (statistically equivalent; the scale mode)."""
+
+    def __init__(self, pixel_count: int, spp: int, gen_seed: int = 1234, albedo_init: float = 0.1,
+                 exponent_max: float = 4.0, lr: float = 0.01, beta_f: float = 0.9,
+                 beta_delta: float = 0.5, eps_step: float = 1e-8, eps_alpha: float = 1e-30,
+                 clip: bool = True, seed: int = 0, replicate: int = 0, rng: str = "philox",
+                 dtype=torch.float32, ctx=None):
+        self.ctx = ctx or Context.default()
+        self.problem = MiniRenderProblem(pixel_count, spp, gen_seed, albedo_init, exponent_max,
+                                         ctx=self.ctx)
+        self.P, self.spp, self.dtype = pixel_count, spp, dtype
+        self.b = self.problem.exponents.to(dtype).contiguous()
+        self.T = self.problem.target.to(dtype).contiguous()
+        self.params = torch.full((pixel_count,), albedo_init, dtype=dtype, device="cuda")
+        self.prev = self.params.clone()
+        mk = lambda: torch.empty(pixel_count, dtype=dtype, device="cuda")  # noqa: E731
+        self.m2_prop, self.m2_diff, self.mean, self.var, self.alpha_prev = (mk() for _ in range(5))
+        self.scalars_buf = torch.zeros(C.sizeof(_abi.UpdateScalars) // 8, dtype=torch.float64,
+                                       device="cuda")
+        check(load().mg_scalars_write(self.ctx.h, _p(self.scalars_buf),
+                                      C.byref(_abi.fresh_scalars())))
+        self.meta = _abi.MetaParams(lr, eps_step, eps_alpha, int(clip))
+        self.beta_f, self.beta_delta = beta_f, beta_delta
+        self.rng_kind = {"mt64": _abi.MG_RNG_MT64, "philox": _abi.MG_RNG_PHILOX}[rng]
+        self.key = int(load().mg_stream_seed(seed, replicate))
+        if self.rng_kind == _abi.MG_RNG_MT64:
+            self.rng = Rng.stream(seed, replicate, ctx=self.ctx)
+            self.u = torch.empty(pixel_count * spp, dtype=torch.float64, device="cuda")
+        else:
+            self.rng, self.u = None, None
+        self.t = 0
+        self.beta_f_pow = 1.0
+
+    def draws_per_sample(self) -> int:
+        return self.P * self.spp
+
+    def step(self, prop_out=None, diff_out=None):
+        self.t += 1
+        self.beta_f_pow *= self.beta_f
+        upd = _abi.MetaUpdateArgs(meta=self.meta,
+                                  prop_coef=(1.0 - self.beta_f) / (1.0 - self.beta_f_pow),
+                                  beta_delta=self.beta_delta, first_step=int(self.t == 1),
+                                  diff_norm=_abi.MG_DIFF_NORM_GLOBAL, project=1)
+        a = _abi.RenderArgs(update=upd, spp=self.spp, rng_kind=self.rng_kind, key=self.key,
+                            iteration=self.t - 1, stream=0)
+        L = load()
+        if self.rng is not None:
+            check(L.mg_mt64_draw(self.ctx.h, self.rng.h, self.P * self.spp, 1, _p(self.u)))
+        check(L.mg_minirender_meta_iteration(
+            self.ctx.h, _dtype_code(self.params), self.P, C.byref(a), _p(self.b), _p(self.T),
+            _p(self.u), _p(self.params), _p(self.prev), _p(self.m2_prop), _p(self.m2_diff),
+            _p(self.mean), _p(self.var), _p(self.alpha_prev), _p(self.scalars_buf),
+            _p(prop_out), _p(diff_out)))
+        # prev now holds pi_{t+1}: swap roles
+        self.params, self.prev = self.prev, self.params
+
+    def scalars(self) -> _abi.UpdateScalars:
+        out = _abi.UpdateScalars()
+        check(load().mg_scalars_read(self.ctx.h, _p(self.scalars_buf), C.byref(out)))
+        return out
 
 
 # ------------------------------------------------------------- harness

@@ -52,6 +52,34 @@ __device__ __forceinline__ void minirender_terms<float>(double b, const double* 
   mean_basis = sum / n;
 }
 
+// Same terms with the uniforms supplied by a functor u(s) (fused kernels).
+template <class T, class U>
+__device__ __forceinline__ void minirender_terms_fn(double b, int spp, U u, T& cross,
+                                                    T& mean_basis) {
+  if constexpr (sizeof(T) == 8) {
+    const double n = double(spp);
+    double sum = 0.0, sum_sq = 0.0;
+    for (int s = 0; s < spp; ++s) {
+      const double basis = (b + 1.0) * pow(u(s), b);
+      sum += basis;
+      sum_sq += basis * basis;
+    }
+    cross = (sum * sum - sum_sq) / (n * (n - 1.0));
+    mean_basis = sum / n;
+  } else {
+    const float n = float(spp);
+    const float bf = float(b);
+    float sum = 0.f, pairs = 0.f;
+    for (int s = 0; s < spp; ++s) {
+      const float basis = (bf + 1.f) * powf(float(u(s)), bf);
+      pairs += basis * sum;
+      sum += basis;
+    }
+    cross = (2.f * pairs) / (n * (n - 1.f));
+    mean_basis = sum / n;
+  }
+}
+
 // ExpRateProblem draws (problems.cpp:58-63); u are uniform_pos() values.
 __device__ __forceinline__ void exprate_sums(const double* __restrict__ u, int n, double& sum_c,
                                              double& sum_c_sq) {

@@ -74,10 +74,25 @@ class Oracle:
         L.mgo_run_single_series.argtypes = [C.POINTER(_abi.ExperimentConfigC), C.c_int32,
                                             C.POINTER(_abi.RunRecordC),
                                             C.POINTER(_abi.RunSeriesC), C.c_int32, C.c_void_p]
+        L.mgo_philox4x32_10.argtypes = [C.POINTER(C.c_uint32 * 4), C.c_uint64,
+                                        C.POINTER(C.c_uint32 * 4)]
+        L.mgo_philox_uniform.restype = C.c_double
+        L.mgo_philox_uniform.argtypes = [C.c_uint64, C.c_uint32, C.c_uint32, C.c_uint32,
+                                         C.c_uint32]
         # sample-pair helpers take an mgo_mt64*; we re-create streams per call
         self._mt_size = 312 * 8 + 8
 
     # ------------------------------------------------------------ rng
+    def philox(self, ctr, key):
+        c = (C.c_uint32 * 4)(*ctr)
+        o = (C.c_uint32 * 4)()
+        self.lib.mgo_philox4x32_10(C.byref(c), key, C.byref(o))
+        return list(o)
+
+    def philox_uniforms(self, key, P, spp, it, stream=0):
+        f = self.lib.mgo_philox_uniform
+        return np.array([f(key, j, it, s, stream) for j in range(P) for s in range(spp)])
+
     def mix64(self, x):
         return self.lib.mgo_mix64(x)
 

@@ -175,3 +175,15 @@ def test_noiseless_recurrence_hand_values(oracle):
     assert rec["ssn"][1] == 1.0
     assert rec["alpha"][1, 0] == pytest.approx(alpha, rel=1e-14)
     assert rec["mean_est"][1, 0] == pytest.approx(1.0, rel=1e-14)
+
+
+def test_philox4x32_10_known_answers(oracle):
+    """Random123 published known-answer vectors for philox4x32-10."""
+    assert oracle.philox([0, 0, 0, 0], 0) == [0x6627e8d5, 0xe169c58d, 0xbc57ac4c, 0x9b00dbd8]
+    assert oracle.philox([0xffffffff] * 4, 0xffffffffffffffff) == [
+        0x408f276d, 0x41c83b0e, 0xa20bc7c6, 0x6d5451fd]
+    assert oracle.philox([0x243f6a88, 0x85a308d3, 0x13198a2e, 0x03707344],
+                         (0x299f31d0 << 32) | 0xa4093822) == [
+        0xd16cfe09, 0x94fdcceb, 0x5001e420, 0x24126ea1]
+    u = oracle.philox_uniforms(12345, 4, 3, 7)
+    assert u.shape == (12,) and (u >= 0).all() and (u < 1).all()
