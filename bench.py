@@ -102,6 +102,19 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.samples)}
 
 
+def ncu_traffic(n, dtype):
+    """DRAM bytes per launch of the fused update from the committed ncu
+    capture (profiles/r01_meta_update_traffic.json: dram__bytes_read.sum +
+    dram__bytes_write.sum at 2^28 fp32), scaled to n; None if not captured
+    for this dtype."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "r01_meta_update_traffic.json")) as f:
+            d = json.load(f)
+        return d["bytes_per_param"] * n if dtype == "f32" else None
+    except Exception:
+        return None
+
+
 def measured_peak():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -286,7 +299,8 @@ def run_ours(args):
                        "beta_f": 0.9, "beta_delta": 0.5, "lr": 0.01,
                        "kernel": "register-streaming" if args.no_tma else "tma-bulk-pipeline"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": None, "peak_kind": peak_kind,
+                         "frac": achieved / peak, "traffic": ncu_traffic(n, args.dtype),
+                         "peak_kind": peak_kind,
                          "kernel_ms": k_ms, "algorithmic_bytes": algo_bytes},
             "e2e": {"value": e2e_val, "unit": UNIT, "h2d_bytes_per_step": 2 * esz * n,
                     "d2h_bytes_per_step": 64, "steps": e2e_steps},

@@ -680,36 +680,32 @@ class AggregateReport:
     records: List[RunRecord]
 
 
-def _quantile(xs: np.ndarray, p: float) -> float:
-    """stats.hpp:45-53 (linear interpolation on the sorted sample)."""
-    if xs.size == 0:
-        return math.nan
-    s = np.sort(xs)
-    pos = p * (s.size - 1)
-    lo = int(pos)
-    if lo + 1 >= s.size:
-        return float(s[-1])
-    frac = pos - lo
-    return float(s[lo] * (1.0 - frac) + s[lo + 1] * frac)
+def _seq_sum(x: np.ndarray, axis: int = 0) -> np.ndarray:
+    """Sequential (index-order) sum along axis: the last element of a prefix
+    sum, which numpy evaluates left to right — identical to stats.hpp's
+    `for (double x : xs) s += x` (np.sum would sum pairwise)."""
+    if x.shape[axis] == 0:
+        return np.zeros(np.delete(x.shape, axis))
+    return np.take(np.cumsum(x, axis=axis), -1, axis=axis)
 
 
-def _mean_of(xs):  # stats.hpp:55-60 (sequential sum)
-    if xs.size == 0:
-        return math.nan
-    s = 0.0
-    for x in xs:
-        s += float(x)
-    return s / xs.size
+def _column_stats(vals: np.ndarray):
+    """mean_of / variance_of / quantile (stats.hpp:45-68) of one sample."""
+    n = vals.size
+    if n == 0:
+        return math.nan, 0.0, math.nan, math.nan, math.nan
+    mean = float(_seq_sum(vals)) / n
+    var = float(_seq_sum((vals - mean) * (vals - mean))) / (n - 1) if n >= 2 else 0.0
+    s = np.sort(vals)
 
-
-def _variance_of(xs):  # stats.hpp:62-68
-    if xs.size < 2:
-        return 0.0
-    m = _mean_of(xs)
-    s = 0.0
-    for x in xs:
-        s += (float(x) - m) * (float(x) - m)
-    return s / (xs.size - 1)
+    def q(p):
+        pos = p * (n - 1)
+        lo = int(pos)
+        if lo + 1 >= n:
+            return float(s[-1])
+        frac = pos - lo
+        return float(s[lo] * (1.0 - frac) + s[lo + 1] * frac)
+    return mean, var, q(0.5), q(0.25), q(0.75)
 
 
 SERIES_ORDER = ["param_err", "loss", "prop", "diff", "grad_est", "est_var", "alpha", "delta",
@@ -720,18 +716,15 @@ def aggregate(cfg: ExperimentConfig, records: List[RunRecord]) -> AggregateRepor
     """Per-iteration reduction in replicate order (harness.cpp:274-302)."""
     it = cfg.iterations
     names = [n for n in SERIES_ORDER if cfg.optimizer == "meta" or n != "alpha"]
-    active = np.array([sum(1 for r in records if r.iterations_run > i) for i in range(it)])
+    runs = np.array([r.iterations_run for r in records])
+    active = np.array([int(np.sum(runs > i)) for i in range(it)])
     stats = {}
     for n in names:
-        cols = np.stack([r.series[n] for r in records])  # [R][it]
+        cols = np.stack([r.series[n] for r in records])  # [R][it], replicate order
         st = SeriesStats(*(np.empty(it) for _ in range(5)))
         for i in range(it):
-            vals = np.array([cols[k, i] for k, r in enumerate(records) if r.iterations_run > i])
-            st.mean[i] = _mean_of(vals)
-            st.variance[i] = _variance_of(vals)
-            st.median[i] = _quantile(vals, 0.5)
-            st.q25[i] = _quantile(vals, 0.25)
-            st.q75[i] = _quantile(vals, 0.75)
+            vals = cols[runs > i, i]
+            st.mean[i], st.variance[i], st.median[i], st.q25[i], st.q75[i] = _column_stats(vals)
         stats[n] = st
     div = sum(1 for r in records if r.status == "diverged")
     return AggregateReport(cfg, names, stats, active, div, records)

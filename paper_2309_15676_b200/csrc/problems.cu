@@ -73,7 +73,7 @@ __global__ void minirender_pair_kernel(int R, int P, int spp, const double* __re
                                        const T* __restrict__ prev, T* __restrict__ prop,
                                        T* __restrict__ diff, double* __restrict__ ssn,
                                        const int* __restrict__ changed) {
-  const int r = blockIdx.y;
+  for (int r = blockIdx.y; r < R; r += gridDim.y) {
   const bool same = changed[r] == 0;
   for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < P; j += gridDim.x * blockDim.x) {
     const size_t at = size_t(r) * P + j;
@@ -84,6 +84,7 @@ __global__ void minirender_pair_kernel(int R, int P, int spp, const double* __re
     diff[at] = same ? T(0) : (T(2) * (a - prev[at])) * cross;  // :206-213
   }
   if (same && blockIdx.x == 0 && threadIdx.x == 0) ssn[r] = 0.0;  // :208
+  }
 }
 
 // problems.cpp:54-76 (dim 1): one thread per replicate, sequential sums.
@@ -186,7 +187,8 @@ int mg_minirender_sample_pair(mg_ctx* ctx, int32_t dtype, int32_t R, int32_t P, 
   MG_CUDA_TRY(cudaMallocAsync(&changed, sizeof(int) * size_t(R), ctx->stream));
   int st = mt64_draw(ctx, g, int64_t(P) * spp, 1, u);  // problems.cpp:201-202
   if (!st) {
-    const dim3 grid((P + kThreads - 1) / kThreads < 1024 ? (P + kThreads - 1) / kThreads : 1024, R);
+    const dim3 grid((P + kThreads - 1) / kThreads < 1024 ? (P + kThreads - 1) / kThreads : 1024,
+                    R < 65535 ? R : 65535);
     if (dtype == MG_F64) {
       pair_norm_kernel<double><<<R, kThreads, 0, ctx->stream>>>(R, P, (const double*)now,
                                                                 (const double*)prev, ssn_out,

@@ -80,6 +80,51 @@ __device__ __forceinline__ void minirender_terms_fn(double b, int spp, U u, T& c
   }
 }
 
+// fp32 fast-mode u^b for u in [0,1), b >= 0: exp2(b * log2(u)) on the SFU
+// (MUFU.LG2 / MUFU.EX2).  |log2 u| <= 53 and b <= exponent_max keep the
+// relative error ~1e-6 (tolerance 1e-4); pow(u, 0) = 1 and
+// pow(0, b>0) = 0 as in libm.
+__device__ __forceinline__ float fast_powf01(float u, float b) {
+  if (b == 0.f) return 1.f;
+  if (u == 0.f) return 0.f;
+  return exp2f(b * __log2f(u));
+}
+
+// Same terms from a register array of up to MAXS uniforms (spp <= MAXS),
+// fully unrolled so the array stays in registers.
+template <class T, int MAXS>
+__device__ __forceinline__ void minirender_terms_arr(double b, int spp, const double (&u)[MAXS],
+                                                     T& cross, T& mean_basis) {
+  if constexpr (sizeof(T) == 8) {
+    const double n = double(spp);
+    double sum = 0.0, sum_sq = 0.0;
+#pragma unroll
+    for (int s = 0; s < MAXS; ++s) {
+      if (s < spp) {
+        const double basis = (b + 1.0) * pow(u[s], b);
+        sum += basis;
+        sum_sq += basis * basis;
+      }
+    }
+    cross = (sum * sum - sum_sq) / (n * (n - 1.0));
+    mean_basis = sum / n;
+  } else {
+    const float n = float(spp);
+    const float bf = float(b);
+    float sum = 0.f, pairs = 0.f;
+#pragma unroll
+    for (int s = 0; s < MAXS; ++s) {
+      if (s < spp) {
+        const float basis = (bf + 1.f) * fast_powf01(float(u[s]), bf);
+        pairs += basis * sum;
+        sum += basis;
+      }
+    }
+    cross = (2.f * pairs) / (n * (n - 1.f));
+    mean_basis = sum / n;
+  }
+}
+
 // ExpRateProblem draws (problems.cpp:58-63); u are uniform_pos() values.
 __device__ __forceinline__ void exprate_sums(const double* __restrict__ u, int n, double& sum_c,
                                              double& sum_c_sq) {

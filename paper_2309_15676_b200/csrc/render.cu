@@ -19,6 +19,7 @@
 #include "problems.cuh"
 
 namespace mg {
+bool g_render_vec = true;  // mg_set_option("render_vec", 0) forces one pixel per thread
 namespace {
 
 constexpr int kThreads = 256;
@@ -31,8 +32,61 @@ struct RenderK {
   uint32_t iteration, stream;
 };
 
-template <class T, bool FIRST>
-__global__ void __launch_bounds__(kThreads)
+// Uniforms of one pixel into u[0..spp): Philox in pairs (one 4x32 block
+// gives two 53-bit doubles) or the mt19937_64 buffer (pixel-major).
+template <int MAXS>
+__device__ __forceinline__ void pixel_uniforms(const RenderK& k, int64_t j,
+                                               const double* __restrict__ uniforms, double* u) {
+  if (k.philox) {
+#pragma unroll
+    for (int q = 0; q < MAXS; q += 2) {
+      if (q < k.spp) {
+        const Philox4 r = philox4x32_10(Philox4{{uint32_t(j), k.iteration, uint32_t(q >> 1),
+                                                 k.stream}},
+                                        uint32_t(k.key), uint32_t(k.key >> 32));
+        philox_uniform2(r, u[q], u[q + 1 < MAXS ? q + 1 : q]);
+      }
+    }
+  } else {
+    const double* src = uniforms + j * k.spp;  // problems.cpp:201-202
+#pragma unroll
+    for (int q = 0; q < MAXS; ++q)
+      if (q < k.spp) u[q] = src[q];
+  }
+}
+
+// One pixel: sample pair (problems.cpp:205-213) + fused meta update.
+template <class T, bool FIRST, int MAXS>
+__device__ __forceinline__ void render_pixel(const RenderK& k, const StepScal& s, bool same,
+                                             int64_t j, const double* __restrict__ uniforms,
+                                             T bj, T target, T a, T a_prev, T& m2p, T& m2d,
+                                             T& mean, T& var, T& ap, T& pout, T& prop, T& diff,
+                                             Acc& acc) {
+  T cross, mb;
+  if (k.spp <= MAXS) {
+    double u[MAXS];
+    pixel_uniforms<MAXS>(k, j, uniforms, u);
+    minirender_terms_arr<T, MAXS>(double(bj), k.spp, u, cross, mb);
+  } else if (k.philox) {
+    minirender_terms_fn<T>(double(bj), k.spp,
+                           [&](int q) {
+                             return philox_uniform_at(k.key, uint32_t(j), k.iteration,
+                                                      uint32_t(q), k.stream);
+                           },
+                           cross, mb);
+  } else {
+    const double* u = uniforms + j * k.spp;
+    minirender_terms_fn<T>(double(bj), k.spp, [&](int q) { return u[q]; }, cross, mb);
+  }
+  prop = (T(2) * a) * cross - (T(2) * target) * mb;      // problems.cpp:205
+  diff = same ? T(0) : (T(2) * (a - a_prev)) * cross;   // problems.cpp:206-213
+  T dl;
+  meta_elem<T, FIRST>(k.meta, s, prop, diff, prop, diff, m2p, m2d, mean, var, ap, a, a_prev,
+                      target, true, pout, dl, acc);
+}
+
+template <class T, bool FIRST, bool VEC>
+__global__ void __launch_bounds__(kThreads, sizeof(T) == 4 ? 3 : 2)
     minirender_meta_kernel(int64_t P, RenderK k, const T* __restrict__ b,
                            const T* __restrict__ tgt, const double* __restrict__ uniforms,
                            const T* __restrict__ pnow, T* __restrict__ pprev_next,
@@ -40,44 +94,59 @@ __global__ void __launch_bounds__(kThreads)
                            T* __restrict__ var, T* __restrict__ ap, T* __restrict__ prop_out,
                            T* __restrict__ diff_out, mg_update_scalars* sc,
                            ReducePartials* partials, unsigned int* counter) {
+  constexpr int MAXS = 4;
   const StepScal s = load_step_scalars(k.meta, sc);
   const bool same = __ldcg(&sc->changed) == 0.0;  // (params == prev).all(), problems.cpp:206
   Acc acc;
-  for (int64_t j = int64_t(blockIdx.x) * kThreads + threadIdx.x; j < P;
-       j += int64_t(gridDim.x) * kThreads) {
-    T cross, mb;
-    if (k.philox) {
-      minirender_terms_fn<T>(double(b[j]), k.spp,
-                             [&](int q) {
-                               return philox_uniform_at(k.key, uint32_t(j), k.iteration,
-                                                        uint32_t(q), k.stream);
-                             },
-                             cross, mb);
-    } else {
-      const double* u = uniforms + j * k.spp;  // pixel-major (problems.cpp:201-202)
-      minirender_terms_fn<T>(double(b[j]), k.spp, [&](int q) { return u[q]; }, cross, mb);
+  const int64_t tid = int64_t(blockIdx.x) * kThreads + threadIdx.x;
+  const int64_t stride = int64_t(gridDim.x) * kThreads;
+  constexpr int W = VEC ? VecOf<T>::width : 1;
+  const int64_t items = VEC ? P / W : 0;
+  if constexpr (VEC) {
+    for (int64_t it = tid; it < items; it += stride) {
+      const int64_t base = it * W;
+      const Pack<T> B = ld_stream(b + base), TG = ld_stream(tgt + base);
+      const Pack<T> A = ld_plain(pnow + base), AQ = ld_plain(pprev_next + base);
+      Pack<T> M2P{}, M2D{}, ME{}, VA{}, AL{}, PO, PR, DF;
+      if (!FIRST) {
+        M2P = ld_plain(m2p + base);
+        ME = ld_plain(mean + base);
+        VA = ld_plain(var + base);
+        AL = ld_plain(ap + base);
+      }
+      if (s.cnt0 > 0) M2D = ld_plain(m2d + base);
+#pragma unroll
+      for (int w = 0; w < W; ++w)
+        render_pixel<T, FIRST, MAXS>(k, s, same, base + w, uniforms, B.v[w], TG.v[w], A.v[w],
+                                     AQ.v[w], M2P.v[w], M2D.v[w], ME.v[w], VA.v[w], AL.v[w],
+                                     PO.v[w], PR.v[w], DF.v[w], acc);
+      st_plain(m2p + base, M2P);
+      if (s.active) st_plain(m2d + base, M2D);
+      st_plain(mean + base, ME);
+      st_plain(var + base, VA);
+      st_plain(ap + base, AL);
+      st_plain(pprev_next + base, PO);
+      if (prop_out) st_plain(prop_out + base, PR);
+      if (diff_out) st_plain(diff_out + base, DF);
     }
-    const T a = pnow[j];
-    const T a_prev = pprev_next[j];
-    const T target = tgt[j];
-    const T prop = (T(2) * a) * cross - (T(2) * target) * mb;          // :205
-    const T diff = same ? T(0) : (T(2) * (a - a_prev)) * cross;       // :206-213
-    if (prop_out) prop_out[j] = prop;
-    if (diff_out) diff_out[j] = diff;
+  }
+  for (int64_t j = items * W + tid; j < P; j += stride) {
     T M2P = FIRST ? T(0) : m2p[j];
     T M2D = s.cnt0 > 0 ? m2d[j] : T(0);
     T ME = FIRST ? T(0) : mean[j];
     T VA = FIRST ? T(0) : var[j];
-    T AP = FIRST ? T(0) : ap[j];
-    T PO, DL;
-    meta_elem<T, FIRST>(k.meta, s, prop, diff, prop, diff, M2P, M2D, ME, VA, AP, a, a_prev,
-                        target, true, PO, DL, acc);
+    T AL = FIRST ? T(0) : ap[j];
+    T PO, PR, DF;
+    render_pixel<T, FIRST, MAXS>(k, s, same, j, uniforms, b[j], tgt[j], pnow[j], pprev_next[j],
+                                 M2P, M2D, ME, VA, AL, PO, PR, DF, acc);
     m2p[j] = M2P;
     if (s.active) m2d[j] = M2D;
     mean[j] = ME;
     var[j] = VA;
-    ap[j] = AP;
+    ap[j] = AL;
     pprev_next[j] = PO;
+    if (prop_out) prop_out[j] = PR;
+    if (diff_out) diff_out[j] = DF;
   }
   grid_reduce4<kThreads>(acc.partials(), partials, counter, [&](const ReducePartials& t) {
     sc->ssn = t.ssn;
@@ -94,13 +163,23 @@ template <class T>
 int launch(mg_ctx* ctx, int64_t P, const RenderK& k, bool first, const void* b, const void* t,
            const double* u, const void* pnow, void* pprev, void* m2p, void* m2d, void* mean,
            void* var, void* ap, void* prop_out, void* diff_out, mg_update_scalars* sc) {
-  const int grid = grid_for(ctx, P, kThreads, 8);
+  // fp32: 4 pixels per thread (16-byte packs, ILP across 4 Philox/pow
+  // chains); fp64: one pixel per thread (the packed fp64 body needs 155 regs)
+  const bool vec = g_render_vec && sizeof(T) == 4 && aligned16(b) && aligned16(t) && aligned16(pnow) && aligned16(pprev) &&
+                   aligned16(m2p) && aligned16(m2d) && aligned16(mean) && aligned16(var) &&
+                   aligned16(ap) && (!prop_out || aligned16(prop_out)) &&
+                   (!diff_out || aligned16(diff_out));
+  const int64_t items = vec ? (P + VecOf<T>::width - 1) / VecOf<T>::width : P;
+  const int grid = grid_for(ctx, items, kThreads, 8);
   auto run = [&](auto kernel) {
     kernel<<<grid, kThreads, 0, ctx->stream>>>(
         P, k, (const T*)b, (const T*)t, u, (const T*)pnow, (T*)pprev, (T*)m2p, (T*)m2d, (T*)mean,
         (T*)var, (T*)ap, (T*)prop_out, (T*)diff_out, sc, ctx->partials, ctx->counter);
   };
-  first ? run(minirender_meta_kernel<T, true>) : run(minirender_meta_kernel<T, false>);
+  if (first)
+    vec ? run(minirender_meta_kernel<T, true, true>) : run(minirender_meta_kernel<T, true, false>);
+  else
+    vec ? run(minirender_meta_kernel<T, false, true>) : run(minirender_meta_kernel<T, false, false>);
   MG_LAUNCH_CHECK(ctx);
   return MG_OK;
 }

@@ -26,6 +26,7 @@
 namespace mg {
 // Test/benchmark switch: force the register-streaming kernel (mg_set_option).
 bool g_disable_tma = false;
+extern bool g_render_vec;
 // -1: per-dtype default measured on B200 (tools/sweep_update_variants.py):
 // fp32 -> variant 4 (3 CTAs/SM x 256 thr, 2 stages; the fp32 body is
 // issue-heavy, more warps hide it), fp64 -> variant 0 (1 CTA/SM, 4 stages).
@@ -513,6 +514,10 @@ int mg_set_option(const char* name, int64_t value) {
   if (!name) return fail(MG_EINVAL, "mg_set_option: null name");
   if (std::string(name) == "disable_tma") {
     g_disable_tma = value != 0;
+    return MG_OK;
+  }
+  if (std::string(name) == "render_vec") {
+    g_render_vec = value != 0;
     return MG_OK;
   }
   if (std::string(name) == "tma_variant") {
