@@ -302,6 +302,10 @@ int mg_multnoise_sample_pair(mg_ctx* ctx, int32_t replicates, int32_t dim, doubl
  *                          counter (j, iteration, s/2, stream), key = `key`
  *                          (statistically equivalent scale mode).
  * params_prev_next holds pi_{t-1} on entry and pi_{t+1} on exit.
+ * Pixel sharding: a rank owning pixels [lo, lo+P) passes pixel_offset = lo
+ * (Philox counters use the global index) and, in mt64 mode, the slice
+ * uniforms + lo*spp of the full iteration stream; then all-reduces the
+ * first 4 doubles of *scalars (SUM) before the next iteration.
  * exponents/target are dtype arrays [P].  "same" (diff = 0) is taken from
  * scalars->changed == 0, the previous step's reduction. */
 typedef struct mg_render_args {
@@ -311,6 +315,8 @@ typedef struct mg_render_args {
   uint64_t key;       /* mg_stream_seed(seed, replicate) */
   uint32_t iteration; /* Philox counter word 1 */
   uint32_t stream;    /* Philox counter word 3 (0: main pair, 1: independent pair) */
+  uint32_t pixel_offset; /* global index of local pixel 0 (pixel-sharded runs) */
+  uint32_t reserved;
 } mg_render_args;
 
 int mg_minirender_meta_iteration(mg_ctx* ctx, int32_t dtype, int64_t P, const mg_render_args* a,

@@ -510,14 +510,19 @@ class MiniRenderRun:
                  exponent_max: float = 4.0, lr: float = 0.01, beta_f: float = 0.9,
                  beta_delta: float = 0.5, eps_step: float = 1e-8, eps_alpha: float = 1e-30,
                  clip: bool = True, seed: int = 0, replicate: int = 0, rng: str = "philox",
-                 dtype=torch.float32, ctx=None):
+                 dtype=torch.float32, pixel_range=None, ctx=None):
         self.ctx = ctx or Context.default()
         self.problem = MiniRenderProblem(pixel_count, spp, gen_seed, albedo_init, exponent_max,
                                          ctx=self.ctx)
-        self.P, self.spp, self.dtype = pixel_count, spp, dtype
-        self.b = self.problem.exponents.to(dtype).contiguous()
-        self.T = self.problem.target.to(dtype).contiguous()
-        self.params = torch.full((pixel_count,), albedo_init, dtype=dtype, device="cuda")
+        lo, hi = pixel_range if pixel_range is not None else (0, pixel_count)
+        if not 0 <= lo < hi <= pixel_count:
+            raise InvalidArgument(_abi.MG_EINVAL, "MiniRenderRun: bad pixel_range")
+        self.lo, self.hi, self.P_total = lo, hi, pixel_count
+        self.P, self.spp, self.dtype = hi - lo, spp, dtype
+        self.b = self.problem.exponents[lo:hi].to(dtype).contiguous()
+        self.T = self.problem.target[lo:hi].to(dtype).contiguous()
+        self.params = torch.full((self.P,), albedo_init, dtype=dtype, device="cuda")
+        pixel_count = self.P
         self.prev = self.params.clone()
         mk = lambda: torch.empty(pixel_count, dtype=dtype, device="cuda")  # noqa: E731
         self.m2_prop, self.m2_diff, self.mean, self.var, self.alpha_prev = (mk() for _ in range(5))
@@ -530,8 +535,9 @@ class MiniRenderRun:
         self.rng_kind = {"mt64": _abi.MG_RNG_MT64, "philox": _abi.MG_RNG_PHILOX}[rng]
         self.key = int(load().mg_stream_seed(seed, replicate))
         if self.rng_kind == _abi.MG_RNG_MT64:
+            # the replicate's stream covers ALL pixels; a shard reads its slice
             self.rng = Rng.stream(seed, replicate, ctx=self.ctx)
-            self.u = torch.empty(pixel_count * spp, dtype=torch.float64, device="cuda")
+            self.u = torch.empty(self.P_total * spp, dtype=torch.float64, device="cuda")
         else:
             self.rng, self.u = None, None
         self.t = 0
@@ -548,13 +554,15 @@ class MiniRenderRun:
                                   beta_delta=self.beta_delta, first_step=int(self.t == 1),
                                   diff_norm=_abi.MG_DIFF_NORM_GLOBAL, project=1)
         a = _abi.RenderArgs(update=upd, spp=self.spp, rng_kind=self.rng_kind, key=self.key,
-                            iteration=self.t - 1, stream=0)
+                            iteration=self.t - 1, stream=0, pixel_offset=self.lo)
         L = load()
+        u = None
         if self.rng is not None:
-            check(L.mg_mt64_draw(self.ctx.h, self.rng.h, self.P * self.spp, 1, _p(self.u)))
+            check(L.mg_mt64_draw(self.ctx.h, self.rng.h, self.P_total * self.spp, 1, _p(self.u)))
+            u = C.c_void_p(self.u.data_ptr() + 8 * self.lo * self.spp)
         check(L.mg_minirender_meta_iteration(
             self.ctx.h, _dtype_code(self.params), self.P, C.byref(a), _p(self.b), _p(self.T),
-            _p(self.u), _p(self.params), _p(self.prev), _p(self.m2_prop), _p(self.m2_diff),
+            u, _p(self.params), _p(self.prev), _p(self.m2_prop), _p(self.m2_diff),
             _p(self.mean), _p(self.var), _p(self.alpha_prev), _p(self.scalars_buf),
             _p(prop_out), _p(diff_out)))
         # prev now holds pi_{t+1}: swap roles

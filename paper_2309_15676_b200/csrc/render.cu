@@ -29,7 +29,7 @@ struct RenderK {
   int spp;
   int philox;  // 0: uniforms buffer (mt19937_64 stream), 1: Philox counter
   uint64_t key;
-  uint32_t iteration, stream;
+  uint32_t iteration, stream, pixel_offset;
 };
 
 // Uniforms of one pixel into u[0..spp): Philox in pairs (one 4x32 block
@@ -41,7 +41,8 @@ __device__ __forceinline__ void pixel_uniforms(const RenderK& k, int64_t j,
 #pragma unroll
     for (int q = 0; q < MAXS; q += 2) {
       if (q < k.spp) {
-        const Philox4 r = philox4x32_10(Philox4{{uint32_t(j), k.iteration, uint32_t(q >> 1),
+        const Philox4 r = philox4x32_10(Philox4{{uint32_t(j) + k.pixel_offset, k.iteration,
+                                                 uint32_t(q >> 1),
                                                  k.stream}},
                                         uint32_t(k.key), uint32_t(k.key >> 32));
         philox_uniform2(r, u[q], u[q + 1 < MAXS ? q + 1 : q]);
@@ -70,7 +71,8 @@ __device__ __forceinline__ void render_pixel(const RenderK& k, const StepScal& s
   } else if (k.philox) {
     minirender_terms_fn<T>(double(bj), k.spp,
                            [&](int q) {
-                             return philox_uniform_at(k.key, uint32_t(j), k.iteration,
+                             return philox_uniform_at(k.key, uint32_t(j) + k.pixel_offset,
+                                                      k.iteration,
                                                       uint32_t(q), k.stream);
                            },
                            cross, mb);
@@ -223,6 +225,7 @@ extern "C" int mg_minirender_meta_iteration(mg_ctx* ctx, int32_t dtype, int64_t 
   k.key = a->key;
   k.iteration = a->iteration;
   k.stream = a->stream;
+  k.pixel_offset = a->pixel_offset;
   const bool first = a->update.first_step != 0;
   if (dtype == MG_F32)
     return launch<float>(ctx, P, k, first, exponents, target, uniforms, params_now,

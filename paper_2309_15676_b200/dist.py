@@ -77,3 +77,62 @@ def run_experiment_sharded(cfg, run_fn: Callable[[object, int, int], Sequence], 
     if aggregate_fn is None:
         from .api import aggregate as aggregate_fn
     return aggregate_fn(cfg, records)
+
+
+def _reduce_scatter_sum(full, shard_out, group=None):
+    """SUM-reduce `full` over ranks and keep this rank's contiguous slice
+    (NCCL reduce_scatter_tensor; gloo has no reduce-scatter, so all-reduce
+    + slice there — same result)."""
+    import torch.distributed as dist
+    if full.is_cuda:
+        dist.reduce_scatter_tensor(shard_out, full, op=dist.ReduceOp.SUM, group=group)
+    else:
+        buf = full.clone()
+        dist.all_reduce(buf, op=dist.ReduceOp.SUM, group=group)
+        rank = dist.get_rank(group)
+        n = shard_out.numel()
+        shard_out.copy_(buf[rank * n:(rank + 1) * n])
+
+
+class SharedParamStep:
+    """One iteration of a shared-parameter problem sharded by image tiles
+    (SURVEY.md §8(e), configs 4/5): every rank renders its tiles and produces
+    FULL-length partial gradient samples (prop, diff) for the one shared
+    parameter vector; the partials are SUM-reduce-scattered so each rank
+    owns the summed pair for its parameter shard, the fused meta update runs
+    on that shard only (state is sharded too: 1/G of the optimiser memory
+    per GPU), the new parameters are all-gathered, and the 4 reducible
+    scalars all-reduced.  Parameter count must be divisible by world*align.
+
+    updater: FusedMetaUpdate-like object over n/world parameters."""
+
+    def __init__(self, updater, n: int, group=None):
+        import torch.distributed as dist
+        self.updater = updater
+        self.group = group
+        self.world = dist.get_world_size(group) if dist.is_initialized() else 1
+        self.rank = dist.get_rank(group) if dist.is_initialized() else 0
+        if n % self.world:
+            raise ValueError("shared parameter count must divide evenly across ranks")
+        self.n, self.shard = n, n // self.world
+
+    def __call__(self, prop_partial, diff_partial, params_full, params_full_out):
+        import torch
+        import torch.distributed as dist
+        lo = self.rank * self.shard
+        prop = torch.empty(self.shard, dtype=prop_partial.dtype, device=prop_partial.device)
+        diff = torch.empty_like(prop)
+        pair = torch.cat([prop_partial.view(self.world, self.shard),
+                          diff_partial.view(self.world, self.shard)], dim=1).reshape(-1)
+        pair_shard = torch.empty(2 * self.shard, dtype=pair.dtype, device=pair.device)
+        _reduce_scatter_sum(pair, pair_shard, self.group)          # one collective for both
+        prop.copy_(pair_shard[:self.shard])
+        diff.copy_(pair_shard[self.shard:])
+        p_in = params_full[lo:lo + self.shard].contiguous()
+        p_out = torch.empty_like(p_in)
+        self.updater.step(prop, diff, p_in, p_out)
+        if self.world > 1:
+            dist.all_reduce(self.updater.scalars_buf[:4], op=dist.ReduceOp.SUM, group=self.group)
+            dist.all_gather_into_tensor(params_full_out, p_out, group=self.group)
+        else:
+            params_full_out.copy_(p_out)

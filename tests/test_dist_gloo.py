@@ -171,3 +171,49 @@ def test_replicate_sharded_experiment_is_world_size_invariant(tmp_path):
     want = np.stack([rep.stats[nm].median for nm in rep.series_names] +
                     [rep.stats[nm].mean for nm in rep.series_names])
     assert np.array_equal(got, want, equal_nan=True)
+
+
+class OracleShardUpdater(OracleUpdater):
+    """OracleUpdater with the FusedMetaUpdate.step(prop, diff, p_in, p_out) shape."""
+
+    def step(self, prop, diff, p_in, p_out):
+        super().step(prop.numpy(), diff.numpy(), p_in.numpy())
+        p_out.copy_(torch.from_numpy(self.out))
+
+
+def _shared_worker(rank, world, port, n, steps, result_path):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from oracle_bind import Oracle
+    rs = np.random.RandomState(100 + rank)  # each rank renders different tiles
+    step = mgdist.SharedParamStep(OracleShardUpdater(Oracle(), n // world), n)
+    params = torch.full((n,), 0.2, dtype=torch.float64)
+    out = torch.empty_like(params)
+    for t in range(steps):
+        prop = torch.from_numpy(rs.standard_normal(n))
+        diff = torch.zeros(n, dtype=torch.float64) if t == 0 else \
+            torch.from_numpy(0.1 * rs.standard_normal(n))
+        step(prop, diff, params, out)
+        params, out = out, params
+    if rank == 0:
+        np.save(result_path, params.numpy())
+    dist.destroy_process_group()
+
+
+def test_shared_parameter_reduce_scatter_update(oracle, tmp_path):
+    """Tile-sharded shared parameters: reduce-scatter of the partial sample
+    pairs + sharded fused update + all-gather == the single-process update on
+    the summed pairs."""
+    n, steps, world = 4096, 8, 2
+    out = str(tmp_path / "shared.npy")
+    mp.spawn(_shared_worker, args=(world, free_port(), n, steps, out), nprocs=world, join=True)
+    got = np.load(out)
+    rss = [np.random.RandomState(100 + r) for r in range(world)]
+    up = OracleUpdater(oracle, n)
+    p = np.full(n, 0.2)
+    for t in range(steps):
+        props = [r.standard_normal(n) for r in rss]
+        diffs = [np.zeros(n) if t == 0 else 0.1 * r.standard_normal(n) for r in rss]
+        up.step(props[0] + props[1], diffs[0] + diffs[1], p)
+        p = up.out
+    np.testing.assert_allclose(got, p, rtol=1e-12, atol=1e-15)

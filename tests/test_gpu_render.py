@@ -106,3 +106,28 @@ def test_philox_estimator_is_unbiased(api):
     x = host(prop)
     z = abs(x.mean() - 2 * (0.7 - 0.5)) / (x.std(ddof=1) / np.sqrt(P))
     assert z < 4.0, z
+
+
+@pytest.mark.parametrize("rng", ["philox", "mt64"])
+def test_pixel_sharded_run_matches_unsharded(api, rng):
+    """Two pixel shards of ONE run, executed one after the other on this GPU
+    with the 4 reducible scalars summed between iterations (what ShardedStep's
+    NCCL all-reduce does across GPUs), reproduce the unsharded run: the
+    per-pixel draws are addressed by global pixel index (Philox) or sliced
+    from the replicate's full stream (mt64), so only the step-norm summation
+    order differs."""
+    P, spp, cut = 5003, 3, 2048
+    kw = dict(gen_seed=5, lr=0.02, seed=4, replicate=1, rng=rng, dtype=torch.float64)
+    full = api.MiniRenderRun(P, spp, **kw)
+    shards = [api.MiniRenderRun(P, spp, pixel_range=(0, cut), **kw),
+              api.MiniRenderRun(P, spp, pixel_range=(cut, P), **kw)]
+    for _ in range(12):
+        full.step()
+        for s in shards:
+            s.step()
+        tot = shards[0].scalars_buf[:4] + shards[1].scalars_buf[:4]
+        for s in shards:
+            s.scalars_buf[:4] = tot
+    got = np.concatenate([host(s.params) for s in shards])
+    np.testing.assert_allclose(got, host(full.params), rtol=1e-12, atol=1e-15)
+    assert full.scalars().loss == pytest.approx(float(tot[2]), rel=1e-12)
