@@ -14,6 +14,7 @@
 #include <chrono>
 #include <cmath>
 #include <cstdint>
+#include <cstdio>
 #include <cstring>
 #include <limits>
 #include <sstream>
@@ -302,7 +303,17 @@ int ref_run_experiment(const char* cfg_text, const char* csv_path, double* out_s
     const AggregateReport rep = run_experiment(cfg);
     *out_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
     if (out_diverged) *out_diverged = rep.diverged_count;
-    if (csv_path && *csv_path) write_aggregate_csv(rep, std::string(csv_path));
+    if (csv_path && *csv_path) {
+      // harness.cpp:311-334 into a string, then plain stdio (std::ofstream
+      // crashes when numpy's bundled runtime is loaded in the same process)
+      std::ostringstream os;
+      write_aggregate_csv(rep, os);
+      const std::string text = os.str();
+      FILE* f = std::fopen(csv_path, "wb");
+      if (!f) throw std::runtime_error(std::string("cannot open output file: ") + csv_path);
+      std::fwrite(text.data(), 1, text.size(), f);
+      std::fclose(f);
+    }
   });
 }
 
@@ -359,6 +370,14 @@ int ref_meta_update_bench(std::int64_t n, int steps, int threads, int pool, cons
     std::sort(times.begin(), times.end());
     *out_sec_per_step = times[times.size() / 2];
   });
+}
+
+// harness.cpp:305-309 (shortest round-trip std::to_chars)
+int ref_format_double(double v, char* out, int cap) {
+  const std::string s = format_double(v);
+  if (int(s.size()) + 1 > cap) return 1;
+  std::memcpy(out, s.c_str(), s.size() + 1);
+  return 0;
 }
 
 // validation.cpp:262-299

@@ -1,0 +1,94 @@
+"""F3: the reference's CSV writer restated on the host — format_double
+against the reference's own std::to_chars (oracle/_ref), and whole CSVs
+byte-identical for runs whose trajectories are bit-exact."""
+import ctypes as C
+import os
+import struct
+
+import numpy as np
+import pytest
+
+from paper_2309_15676_b200 import report
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def ref_fmt():
+    from oracle_bind import REF_SO, ref_available
+    if not ref_available():
+        pytest.skip("oracle/_ref not built")
+    L = C.CDLL(REF_SO)
+    L.ref_format_double.argtypes = [C.c_double, C.c_char_p, C.c_int]
+
+    def f(v):
+        buf = C.create_string_buffer(64)
+        assert L.ref_format_double(v, buf, 64) == 0
+        return buf.value.decode()
+    return f
+
+
+REF_EXE = os.path.join(ROOT, "oracle", "_ref", "run_experiment")
+
+
+def ref_csv_golden(kw, path):
+    """The reference's own run_experiment + CSV writer, in a separate process
+    (its iostreams crash when numpy's bundled runtime shares the process)."""
+    import subprocess
+    from paper_2309_15676_b200 import _abi
+    if not os.path.exists(REF_EXE):
+        pytest.skip("oracle/_ref not built")
+    subprocess.run([REF_EXE, _abi.config_text(**kw), path], check=True, capture_output=True)
+
+
+def test_format_double_matches_std_to_chars():
+    f = ref_fmt()
+    rs = np.random.RandomState(0)
+    vals = [0.0, -0.0, 1.0, -1.0, 0.1, 1e-5, 1e-4, 123456.0, 1e15, 1e16, 1e21, 1e22, 1e23,
+            2.5e-300, 5e-324, 1.7976931348623157e308, float("inf"), float("-inf"), 0.5, 100.0,
+            1234567.0, 0.001, 12.5, 1e100, 3.0e-7, 65536.0, 2.0 ** 53, 2.0 ** 60]
+    vals += list(rs.standard_normal(3000))
+    vals += list(np.exp(rs.uniform(-700, 700, 3000)))
+    vals += [struct.unpack("<d", struct.pack("<Q", int(x)))[0]
+             for x in rs.randint(0, 2 ** 62, 3000, dtype=np.int64)]
+    vals += [float(k) for k in range(-50, 50)] + [k / 8 for k in range(-100, 100)]
+    bad = [(v, report.format_double(v), f(v)) for v in vals
+           if not np.isnan(v) and report.format_double(v) != f(v)]
+    assert not bad, bad[:10]
+
+
+def test_csv_bytes_match_reference_oracle(tmp_path):
+    """Aggregate CSV of oracle records (bit-exact with the reference for
+    mult-noise) written by report.write_aggregate_csv == the reference's own
+    writer, byte for byte."""
+    from test_dist_gloo import _oracle_run_fn
+    from paper_2309_15676_b200 import _abi
+    from paper_2309_15676_b200.api import ExperimentConfig, aggregate
+    kw = dict(problem="mult-noise", dim=2, iterations=25, replicates=6, seed=5)
+    ref_csv = str(tmp_path / "ref.csv")
+    ref_csv_golden(dict(kw, threads=1), ref_csv)
+    cfg = ExperimentConfig(**kw)
+    rep = aggregate(cfg, _oracle_run_fn(cfg, 0, 6))
+    ours = str(tmp_path / "ours.csv")
+    report.write_aggregate_csv(rep, ours)
+    assert open(ours, "rb").read() == open(ref_csv, "rb").read()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("kw", [
+    dict(problem="mult-noise", dim=2, iterations=25, replicates=6, seed=5),
+    dict(problem="mult-noise", dim=1, sigma=1.0, samples_per_iter=4, trajectory="scripted-exp",
+         traj_rate=0.05, iterations=40, replicates=50, seed=606),
+    dict(problem="mult-noise", dim=3, iterations=30, replicates=9, seed=8, optimizer="adam",
+         lr=0.05),
+])
+def test_device_run_csv_is_byte_identical_to_reference(tmp_path, kw):
+    """End to end: the device runner's report, written in the reference's
+    format, equals the reference harness's CSV byte for byte (problems whose
+    arithmetic has no transcendental functions are bit-exact on the device)."""
+    from paper_2309_15676_b200 import api
+    ref_csv = str(tmp_path / "ref.csv")
+    ref_csv_golden(dict(kw, threads=1), ref_csv)
+    rep = api.run_experiment(api.ExperimentConfig(**kw))
+    ours = str(tmp_path / "ours.csv")
+    report.write_aggregate_csv(rep, ours)
+    assert open(ours, "rb").read() == open(ref_csv, "rb").read()
