@@ -378,6 +378,24 @@ def extras(args, ctx):
         "frac": 60 * P / (ms / 1e3) / 1e9 / peak, "loss": run.scalars().loss}
     del run
     torch.cuda.empty_cache()
+    # same, with the reference's exact mt19937_64 stream: 591 engines on ONE
+    # stream (GF(2) jump-ahead), bit-identical draws to the sequential stream
+    run = api.MiniRenderRun(P, spp, gen_seed=1, lr=0.01, rng="mt64", dtype=torch.float32, ctx=ctx)
+    for _ in range(2):
+        run.step()
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record(ctx.stream)
+    for _ in range(10):
+        run.step()
+    b.record(ctx.stream)
+    torch.cuda.synchronize()
+    ms = a.elapsed_time(b) / 10
+    out["minirender_fused_mt64_exact_f32"] = {
+        "pixels": P, "spp": spp, "engines": run.rng.n, "ms_per_iteration": ms,
+        "pairs_per_s": P * spp / (ms / 1e3)}
+    del run
+    torch.cuda.empty_cache()
     # mini-render stand-in for configs[0] (P=4096, spp=2, 200 iterations)
     cfg = api.ExperimentConfig(problem="mini-render", pixel_count=4096, spp=2, iterations=200,
                                seed=0, problem_seed=1, lr=0.01, replicates=148)

@@ -141,6 +141,24 @@ int mg_mt64_destroy(mg_mt64* g);
  * 2 = uniform_pos() double (rng.hpp:31). */
 int mg_mt64_draw(mg_ctx* ctx, mg_mt64* g, int64_t n, int32_t kind, void* out);
 
+/* GF(2) jump-ahead (Haramoto et al. 2008): advance every stream of g by
+ * `distance` draws in O(19937) work, so many engines can produce disjoint
+ * segments of ONE replicate's stream bit-exactly.  Streams must sit at a
+ * 312-draw block boundary (freshly created, or having drawn a multiple of
+ * 312 since) — MG_EINVAL otherwise.  Synchronises the stream. */
+int mg_mt64_jump(mg_ctx* ctx, mg_mt64* g, uint64_t distance);
+/* `segments` engines positioned at draws c*segment_len (c = 0..segments-1)
+ * of the single stream seeded with engine_seed.  With segment_len a multiple
+ * of 312, drawing segment_len from every engine yields draws
+ * [0, segments*segment_len) of the stream in [engine][draw] order; jumping
+ * all by (D - segment_len) then positions them for the next D-draw block. */
+int mg_mt64_split(mg_ctx* ctx, uint64_t engine_seed, int32_t segments, uint64_t segment_len,
+                  mg_mt64** out);
+/* Host helper: g(x) = x^distance mod phi(x) as 312 little-endian words and
+ * its degree (phi = characteristic polynomial of mt19937_64, recovered once
+ * with Berlekamp-Massey).  No device needed. */
+int mg_mt64_jump_polynomial(uint64_t distance, uint64_t* out_words, int32_t* out_deg);
+
 /* ------------------------------------- fused estimator kernels (A8-A12) */
 /* Host-owned scalar state of one Moment2 (moment2.hpp:45-47).  The device
  * only ever sees the per-step coefficient w/w_sum computed from it in fp64,

@@ -90,6 +90,26 @@ void mgo_rng_draws(uint64_t seed, uint64_t rep, int mode, int64_t n, void* out) 
   }
 }
 
+/* GF(2) jump-ahead (Haramoto et al. 2008) restated bit by bit: for a
+ * generator at a block boundary (idx == 312, window W = mt[0..311]),
+ * R = g(A) W with Horner's rule, A = one output step of the window
+ * (x_new = W[156] ^ mag(W[0], W[1]), shift).  poly: 312 words, bit i = g_i. */
+void mgo_mt64_jump(mgo_mt64* g, const uint64_t* poly, int deg) {
+  uint64_t W[MT_N], R[MT_N];
+  memcpy(W, g->mt, sizeof(W));
+  memset(R, 0, sizeof(R));
+  int s = 0;
+  for (int i = deg; i >= 0; --i) {
+    const uint64_t y = (R[s] & MT_UPPER) | (R[(s + 1) % MT_N] & MT_LOWER);
+    R[s] = R[(s + MT_M) % MT_N] ^ (y >> 1) ^ ((y & 1ULL) ? MT_A : 0ULL);
+    s = (s + 1) % MT_N;
+    if ((poly[i >> 6] >> (i & 63)) & 1ULL)
+      for (int c = 0; c < MT_N; ++c) R[(s + c) % MT_N] ^= W[c];
+  }
+  for (int c = 0; c < MT_N; ++c) g->mt[c] = R[(s + c) % MT_N];
+  g->idx = MT_N;
+}
+
 /* Philox4x32-10 (Salmon et al., SC'11), published algorithm; the scale-mode
  * RNG of the device samplers (paper_2309_15676_b200/csrc/philox.cuh).
  * ctr/out are 4 words; key is the 64-bit replicate engine seed. */

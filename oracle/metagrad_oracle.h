@@ -37,6 +37,9 @@ double mgo_uniform_pos(mgo_mt64* g);
 /* same modes as ref_rng_draws (oracle/ref/ref_capi.cpp) */
 void mgo_rng_draws(uint64_t seed, uint64_t rep, int mode, int64_t n, void* out);
 
+/* GF(2) jump-ahead of a block-boundary engine by g(A) (poly: 312 words) */
+void mgo_mt64_jump(mgo_mt64* g, const uint64_t* poly, int deg);
+
 /* Philox4x32-10 and the samplers' uniform mapping (scale mode, not in the
  * reference; see paper_2309_15676_b200/csrc/philox.cuh) */
 void mgo_philox4x32_10(const uint32_t ctr[4], uint64_t key, uint32_t out[4]);

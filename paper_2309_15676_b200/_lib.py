@@ -71,6 +71,9 @@ def load():
         "mg_mt64_create": (C.c_int, [_vp, C.c_int32, _vp, P(_vp)]),
         "mg_mt64_destroy": (C.c_int, [_vp]),
         "mg_mt64_draw": (C.c_int, [_vp, _vp, C.c_int64, C.c_int32, _vp]),
+        "mg_mt64_jump": (C.c_int, [_vp, _vp, C.c_uint64]),
+        "mg_mt64_split": (C.c_int, [_vp, C.c_uint64, C.c_int32, C.c_uint64, P(_vp)]),
+        "mg_mt64_jump_polynomial": (C.c_int, [C.c_uint64, _vp, P(C.c_int32)]),
         "mg_moment2_step": (C.c_int, [_vp, C.c_int32, C.c_int64, P(_abi.Moment2Scalars), _vp,
                                       _vp]),
         "mg_meta_step": (C.c_int, [_vp, C.c_int32, C.c_int64, P(_abi.MetaParams), C.c_int32] +

@@ -122,6 +122,22 @@ class Rng:
         return cls([load().mg_stream_seed(base_seed, replicate)], ctx)
 
     @classmethod
+    def split(cls, engine_seed: int, segments: int, segment_len: int, ctx=None) -> "Rng":
+        """`segments` engines at draws c*segment_len of ONE stream seeded with
+        engine_seed (GF(2) jump-ahead; mg_mt64_split)."""
+        self = cls.__new__(cls)
+        self.ctx = ctx or Context.default()
+        self.n = segments
+        h = C.c_void_p()
+        check(load().mg_mt64_split(self.ctx.h, engine_seed, segments, segment_len, C.byref(h)))
+        self.h = h
+        return self
+
+    def jump(self, distance: int):
+        """Advance every engine by `distance` draws (mg_mt64_jump)."""
+        check(load().mg_mt64_jump(self.ctx.h, self.h, distance))
+
+    @classmethod
     def streams(cls, base_seed: int, replicates, ctx=None) -> "Rng":
         L = load()
         return cls([L.mg_stream_seed(base_seed, int(r)) for r in replicates], ctx)
@@ -510,7 +526,7 @@ class MiniRenderRun:
                  exponent_max: float = 4.0, lr: float = 0.01, beta_f: float = 0.9,
                  beta_delta: float = 0.5, eps_step: float = 1e-8, eps_alpha: float = 1e-30,
                  clip: bool = True, seed: int = 0, replicate: int = 0, rng: str = "philox",
-                 dtype=torch.float32, pixel_range=None, ctx=None):
+                 dtype=torch.float32, pixel_range=None, mt64_segments=None, ctx=None):
         self.ctx = ctx or Context.default()
         self.problem = MiniRenderProblem(pixel_count, spp, gen_seed, albedo_init, exponent_max,
                                          ctx=self.ctx)
@@ -535,9 +551,25 @@ class MiniRenderRun:
         self.rng_kind = {"mt64": _abi.MG_RNG_MT64, "philox": _abi.MG_RNG_PHILOX}[rng]
         self.key = int(load().mg_stream_seed(seed, replicate))
         if self.rng_kind == _abi.MG_RNG_MT64:
-            # the replicate's stream covers ALL pixels; a shard reads its slice
-            self.rng = Rng.stream(seed, replicate, ctx=self.ctx)
-            self.u = torch.empty(self.P_total * spp, dtype=torch.float64, device="cuda")
+            # the replicate's stream covers ALL pixels; a shard reads its slice.
+            # D = P*spp draws per iteration come from G engines positioned
+            # L = 312*k draws apart on the SAME stream (jump-ahead), each
+            # drawing L per iteration, then jumping D - L: bit-identical to
+            # the sequential stream, generated in parallel.
+            D = self.P_total * spp
+            self.D = D
+            if D >= 312 and mt64_segments != 1:
+                gmax = mt64_segments or 592
+                L = 312 * (-(-(-(-D // gmax)) // 312))
+                G = -(-D // L)
+                self.rng = Rng.split(int(load().mg_stream_seed(seed, replicate)), G, L,
+                                     ctx=self.ctx)
+                self.seg_len = L
+            else:
+                self.rng = Rng.stream(seed, replicate, ctx=self.ctx)
+                self.seg_len = None
+            rows = self.rng.n * (self.seg_len or D)
+            self.u = torch.empty(rows, dtype=torch.float64, device="cuda")
         else:
             self.rng, self.u = None, None
         self.t = 0
@@ -558,13 +590,18 @@ class MiniRenderRun:
         L = load()
         u = None
         if self.rng is not None:
-            check(L.mg_mt64_draw(self.ctx.h, self.rng.h, self.P_total * self.spp, 1, _p(self.u)))
+            if self.seg_len:
+                check(L.mg_mt64_draw(self.ctx.h, self.rng.h, self.seg_len, 1, _p(self.u)))
+            else:
+                check(L.mg_mt64_draw(self.ctx.h, self.rng.h, self.D, 1, _p(self.u)))
             u = C.c_void_p(self.u.data_ptr() + 8 * self.lo * self.spp)
         check(L.mg_minirender_meta_iteration(
             self.ctx.h, _dtype_code(self.params), self.P, C.byref(a), _p(self.b), _p(self.T),
             u, _p(self.params), _p(self.prev), _p(self.m2_prop), _p(self.m2_diff),
             _p(self.mean), _p(self.var), _p(self.alpha_prev), _p(self.scalars_buf),
             _p(prop_out), _p(diff_out)))
+        if self.rng is not None and self.seg_len:
+            self.rng.jump(self.D - self.seg_len)  # engines to the next iteration's block
         # prev now holds pi_{t+1}: swap roles
         self.params, self.prev = self.prev, self.params
 

@@ -4,6 +4,10 @@
 #include "mg_common.cuh"
 #include "mt64.cuh"
 #include "mt64_state.h"
+#include "mt64_jump.h"
+
+#include <map>
+#include <mutex>
 
 namespace mg {
 namespace {
@@ -39,7 +43,153 @@ __global__ void __launch_bounds__(kDrawThreads)
   mt_block_store(e, state + size_t(r) * kMtN, idx + r);
 }
 
+// GF(2) jump-ahead of every stream (Haramoto et al. 2008, see
+// mt64_jump.cu): R = g(A) W by Horner's rule in base 16, one warp per
+// stream.  W is the state window (x_t .. x_{t+311}) = the stored buffer of a
+// stream sitting at a block boundary (idx == 312).  Streams with mask[r]==0
+// (when a mask is given) are left untouched.
+constexpr int kJumpThreads = 32;
+constexpr size_t kJumpSmem = sizeof(uint64_t) * (16 * kMtN + kMtN + kMtN + 3 + kMtN);
+
+__global__ void __launch_bounds__(kJumpThreads)
+    mt_jump_kernel(int streams, uint64_t* __restrict__ state, const int* __restrict__ idx,
+                   const uint64_t* __restrict__ g, int deg, const uint8_t* __restrict__ mask,
+                   int* __restrict__ bad) {
+  extern __shared__ uint64_t sm[];
+  uint64_t* T = sm;                  // [16][312]: T[m] = sum_{j in m} A^j W
+  uint64_t* R = sm + 16 * kMtN;      // circular window, start s
+  uint64_t* E = R + kMtN;            // W followed by 3 new words
+  uint64_t* G = E + kMtN + 3;        // the jump polynomial
+  const int r = blockIdx.x;
+  const int lane = threadIdx.x;
+  if (mask && !mask[r]) return;
+  if (idx[r] != kMtN) {
+    if (lane == 0) *bad = 1;
+    return;
+  }
+  uint64_t* st = state + size_t(r) * kMtN;
+  for (int c = lane; c < kMtN; c += kJumpThreads) {
+    E[c] = st[c];
+    R[c] = 0;
+    G[c] = g[c];
+  }
+  __syncwarp();
+  if (lane < 3) {
+    // y_i = E[i+156] ^ mag(E[i], E[i+1]) for i = 0..2 (all inputs are in W)
+    E[kMtN + lane] = E[lane + kMtM] ^ mt_mag(E[lane], E[lane + 1]);
+  }
+  __syncwarp();
+  for (int c = lane; c < kMtN; c += kJumpThreads) {
+#pragma unroll
+    for (int m = 0; m < 16; ++m) {
+      uint64_t v = 0;
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+        if (m & (1 << j)) v ^= E[j + c];
+      T[m * kMtN + c] = v;
+    }
+  }
+  __syncwarp();
+  int s = 0;  // R canonical word c lives at R[(s + c) mod 312]
+  constexpr int kPer = (kMtN + kJumpThreads - 1) / kJumpThreads;  // 10 words per lane
+  const int top = deg < 0 ? -1 : deg / 4;
+  int digit_next = top >= 0 ? int((G[(4 * top) >> 6] >> ((4 * top) & 63)) & 0xFu) : 0;
+  for (int k = top; k >= 0; --k) {
+    const int digit = digit_next;
+    if (k > 0) digit_next = int((G[(4 * (k - 1)) >> 6] >> ((4 * (k - 1)) & 63)) & 0xFu);
+    // R = A^4 R: four new words from the current window (independent), then
+    // they replace the 4 words shifted out
+    uint64_t y = 0;
+    if (lane < 4) {
+      int i0 = s + lane, i1 = i0 + 1, i2 = i0 + kMtM;
+      i0 -= i0 >= kMtN ? kMtN : 0;
+      i1 -= i1 >= kMtN ? kMtN : 0;
+      i2 -= i2 >= kMtN ? kMtN : 0;
+      y = R[i2] ^ mt_mag(R[i0], R[i1]);
+    }
+    __syncwarp();
+    if (lane < 4) {
+      int w = s + lane;
+      R[w - (w >= kMtN ? kMtN : 0)] = y;
+    }
+    s += 4;
+    s -= s >= kMtN ? kMtN : 0;
+    __syncwarp();
+    if (digit) {
+      // R ^= T[digit]: all loads first (ILP), then the stores
+      const uint64_t* t = T + digit * kMtN;
+      uint64_t v[kPer];
+      int at[kPer];
+#pragma unroll
+      for (int i = 0; i < kPer; ++i) {
+        const int c = lane + i * kJumpThreads;
+        int w = s + c;
+        w -= w >= kMtN ? kMtN : 0;
+        at[i] = w;
+        v[i] = c < kMtN ? (R[w < kMtN ? w : 0] ^ t[c < kMtN ? c : 0]) : 0;
+      }
+#pragma unroll
+      for (int i = 0; i < kPer; ++i)
+        if (lane + i * kJumpThreads < kMtN) R[at[i]] = v[i];
+    }
+    __syncwarp();
+  }
+  for (int c = lane; c < kMtN; c += kJumpThreads) st[c] = R[(s + c) % kMtN];
+}
+
 }  // namespace
+
+// Host cache of jump polynomials (computing one costs ~0.1 s).
+struct JumpPoly {
+  uint64_t* dev = nullptr;
+  int deg = -1;
+};
+
+static int get_jump_poly(uint64_t distance, JumpPoly* out) {
+  static std::mutex mu;
+  static std::map<uint64_t, JumpPoly> cache;
+  std::lock_guard<std::mutex> lock(mu);
+  auto it = cache.find(distance);
+  if (it != cache.end()) {
+    *out = it->second;
+    return MG_OK;
+  }
+  std::vector<uint64_t> w(kMtJumpWords);
+  int deg = -1;
+  if (!mt64_jump_polynomial(distance, w.data(), &deg))
+    return fail(MG_ELOGIC, "mt19937_64 characteristic polynomial: unexpected degree");
+  JumpPoly jp;
+  jp.deg = deg;
+  MG_CUDA_TRY(cudaMalloc(&jp.dev, sizeof(uint64_t) * kMtJumpWords));
+  MG_CUDA_TRY(cudaMemcpy(jp.dev, w.data(), sizeof(uint64_t) * kMtJumpWords,
+                         cudaMemcpyHostToDevice));
+  cache[distance] = jp;
+  *out = jp;
+  return MG_OK;
+}
+
+int mt64_jump(mg_ctx* ctx, mg_mt64* g, uint64_t distance, const uint8_t* dev_mask) {
+  if (!ctx || !g) return fail(MG_EINVAL, "mg_mt64_jump: null argument");
+  if (distance == 0) return MG_OK;
+  JumpPoly jp;
+  int st = get_jump_poly(distance, &jp);
+  if (st) return st;
+  static bool attr_set = false;
+  if (!attr_set) {
+    MG_CUDA_TRY(cudaFuncSetAttribute(mt_jump_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     int(kJumpSmem)));
+    attr_set = true;
+  }
+  // All streams of a batch draw the same counts, so their block position is
+  // tracked on the host (no device round trip); the kernel re-checks.
+  if (g->host_idx != kMtN)
+    return fail(MG_EINVAL, "mg_mt64_jump: the streams are not at a 312-draw block boundary "
+                           "(draw multiples of 312 between jumps)");
+  mt_jump_kernel<<<g->streams, kJumpThreads, kJumpSmem, ctx->stream>>>(
+      g->streams, g->state, g->idx, jp.dev, jp.deg, dev_mask, ctx->flag);
+  MG_LAUNCH_CHECK(ctx);
+  return MG_OK;
+}
 
 int mt64_create(mg_ctx* ctx, int32_t streams, const uint64_t* host_seeds, mg_mt64** out) {
   if (!ctx || !out || !host_seeds || streams < 1) return fail(MG_EINVAL, "mg_mt64_create: bad args");
@@ -81,6 +231,7 @@ int mt64_draw(mg_ctx* ctx, mg_mt64* g, int64_t n, int32_t kind, void* out) {
   if (!ctx || !g || !out || n < 0 || kind < 0 || kind > 2)
     return fail(MG_EINVAL, "mg_mt64_draw: bad args");
   if (n == 0) return MG_OK;
+  g->host_idx = int((int64_t(g->host_idx) + n - 1) % kMtN) + 1;  // position after n draws
   mt_draw_kernel<<<g->streams, kDrawThreads, 0, ctx->stream>>>(n, kind, g->state, g->idx, out);
   MG_LAUNCH_CHECK(ctx);
   return MG_OK;
@@ -89,6 +240,39 @@ int mt64_draw(mg_ctx* ctx, mg_mt64* g, int64_t n, int32_t kind, void* out) {
 }  // namespace mg
 
 extern "C" {
+
+int mg_mt64_jump(mg_ctx* ctx, mg_mt64* g, uint64_t distance) {
+  return mg::mt64_jump(ctx, g, distance, nullptr);
+}
+
+// `segments` engines on ONE stream: engine c starts c*segment_len draws
+// into the stream seeded with engine_seed (binary decomposition of c into
+// jumps by 2^i * segment_len, masked per engine).
+int mg_mt64_split(mg_ctx* ctx, uint64_t engine_seed, int32_t segments, uint64_t segment_len,
+                  mg_mt64** out) {
+  using namespace mg;
+  if (!ctx || !out || segments < 1) return fail(MG_EINVAL, "mg_mt64_split: bad arguments");
+  std::vector<uint64_t> seeds(size_t(segments), engine_seed);
+  mg_mt64* g = nullptr;
+  int st = mt64_create(ctx, segments, seeds.data(), &g);
+  if (st) return st;
+  uint8_t* dmask = nullptr;
+  MG_CUDA_TRY(cudaMalloc(&dmask, size_t(segments)));
+  std::vector<uint8_t> mask(static_cast<size_t>(segments));
+  for (int bit = 0; bit < 31 && (int64_t(1) << bit) < segments; ++bit) {
+    for (int c = 0; c < segments; ++c) mask[size_t(c)] = uint8_t((c >> bit) & 1);
+    cudaMemcpy(dmask, mask.data(), size_t(segments), cudaMemcpyHostToDevice);
+    st = mt64_jump(ctx, g, segment_len << bit, dmask);
+    if (st) break;
+  }
+  cudaFree(dmask);
+  if (st) {
+    mt64_destroy(g);
+    return st;
+  }
+  *out = g;
+  return MG_OK;
+}
 
 int mg_mt64_create(mg_ctx* ctx, int32_t streams, const uint64_t* host_seeds, mg_mt64** out) {
   return mg::mt64_create(ctx, streams, host_seeds, out);
