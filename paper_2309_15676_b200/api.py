@@ -558,20 +558,28 @@ class MiniRenderRun:
             # the sequential stream, generated in parallel.
             D = self.P_total * spp
             self.D = D
-            if D >= 312 and mt64_segments != 1:
+            # one engine draws ~3e5 values in the time a jump takes (~1 ms,
+            # latency-bound), so split only large per-iteration blocks; the
+            # engines then tile K iterations' worth of the stream (K*D draws,
+            # <= ~2 GB of uniforms) so each engine jumps once per K iterations.
+            auto = mt64_segments is None and D >= (1 << 20)
+            if D >= 312 and (auto or (mt64_segments or 1) > 1):
                 gmax = mt64_segments or 592
-                L = 312 * (-(-(-(-D // gmax)) // 312))
-                G = -(-D // L)
+                K = max(1, min(16, (1 << 28) // D))
+                block = K * D
+                L = 312 * (-(-(-(-block // gmax)) // 312))
+                G = -(-block // L)
                 self.rng = Rng.split(int(load().mg_stream_seed(seed, replicate)), G, L,
                                      ctx=self.ctx)
-                self.seg_len = L
+                self.seg_len, self.block_iters = L, K
             else:
                 self.rng = Rng.stream(seed, replicate, ctx=self.ctx)
-                self.seg_len = None
-            rows = self.rng.n * (self.seg_len or D)
+                self.seg_len, self.block_iters = None, 1
+            rows = self.rng.n * self.seg_len if self.seg_len else D
             self.u = torch.empty(rows, dtype=torch.float64, device="cuda")
         else:
             self.rng, self.u = None, None
+            self.seg_len, self.block_iters = None, 1
         self.t = 0
         self.beta_f_pow = 1.0
 
@@ -590,18 +598,19 @@ class MiniRenderRun:
         L = load()
         u = None
         if self.rng is not None:
+            k = (self.t - 1) % self.block_iters
             if self.seg_len:
-                check(L.mg_mt64_draw(self.ctx.h, self.rng.h, self.seg_len, 1, _p(self.u)))
+                if k == 0:  # draws for the next K iterations, then jump past them
+                    check(L.mg_mt64_draw(self.ctx.h, self.rng.h, self.seg_len, 1, _p(self.u)))
+                    self.rng.jump(self.block_iters * self.D - self.seg_len)
             else:
                 check(L.mg_mt64_draw(self.ctx.h, self.rng.h, self.D, 1, _p(self.u)))
-            u = C.c_void_p(self.u.data_ptr() + 8 * self.lo * self.spp)
+            u = C.c_void_p(self.u.data_ptr() + 8 * (k * self.D + self.lo * self.spp))
         check(L.mg_minirender_meta_iteration(
             self.ctx.h, _dtype_code(self.params), self.P, C.byref(a), _p(self.b), _p(self.T),
             u, _p(self.params), _p(self.prev), _p(self.m2_prop), _p(self.m2_diff),
             _p(self.mean), _p(self.var), _p(self.alpha_prev), _p(self.scalars_buf),
             _p(prop_out), _p(diff_out)))
-        if self.rng is not None and self.seg_len:
-            self.rng.jump(self.D - self.seg_len)  # engines to the next iteration's block
         # prev now holds pi_{t+1}: swap roles
         self.params, self.prev = self.prev, self.params
 
