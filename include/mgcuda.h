@@ -334,7 +334,8 @@ typedef struct mg_render_args {
   uint32_t iteration; /* Philox counter word 1 */
   uint32_t stream;    /* Philox counter word 3 (0: main pair, 1: independent pair) */
   uint32_t pixel_offset; /* global index of local pixel 0 (pixel-sharded runs) */
-  uint32_t reserved;
+  int32_t record_plus1;  /* 0: prop_out/diff_out (if given) are full [P] arrays;
+                            k+1: they are single values and receive local pixel k */
 } mg_render_args;
 
 int mg_minirender_meta_iteration(mg_ctx* ctx, int32_t dtype, int64_t P, const mg_render_args* a,

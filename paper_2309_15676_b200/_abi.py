@@ -76,7 +76,7 @@ class MetaExtras(C.Structure):
 class RenderArgs(C.Structure):
     _fields_ = [("update", MetaUpdateArgs), ("spp", C.c_int32), ("rng_kind", C.c_int32),
                 ("key", C.c_uint64), ("iteration", C.c_uint32), ("stream", C.c_uint32),
-                ("pixel_offset", C.c_uint32), ("reserved", C.c_uint32)]
+                ("pixel_offset", C.c_uint32), ("record_plus1", C.c_int32)]
 
 
 class RunRecordC(C.Structure):

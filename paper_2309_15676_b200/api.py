@@ -586,7 +586,10 @@ class MiniRenderRun:
     def draws_per_sample(self) -> int:
         return self.P * self.spp
 
-    def step(self, prop_out=None, diff_out=None):
+    def step(self, prop_out=None, diff_out=None, record: Optional[int] = None):
+        """One iteration.  prop_out/diff_out receive this iteration's sample
+        pair: full [P] tensors, or (record=k) one-element tensors receiving
+        local pixel k only."""
         self.t += 1
         self.beta_f_pow *= self.beta_f
         upd = _abi.MetaUpdateArgs(meta=self.meta,
@@ -594,7 +597,8 @@ class MiniRenderRun:
                                   beta_delta=self.beta_delta, first_step=int(self.t == 1),
                                   diff_norm=_abi.MG_DIFF_NORM_GLOBAL, project=1)
         a = _abi.RenderArgs(update=upd, spp=self.spp, rng_kind=self.rng_kind, key=self.key,
-                            iteration=self.t - 1, stream=0, pixel_offset=self.lo)
+                            iteration=self.t - 1, stream=0, pixel_offset=self.lo,
+                            record_plus1=0 if record is None else record + 1)
         L = load()
         u = None
         if self.rng is not None:
@@ -689,7 +693,74 @@ class RunRecord:
     final_params: np.ndarray
 
 
+SCALED_MIN_PIXELS = 1 << 16
+
+
+def _scaled_eligible(cfg: ExperimentConfig) -> bool:
+    """Large mini-render replicates run on the whole GPU (fused iteration
+    kernel + jump-ahead mt64 engines) instead of one CTA of the runner."""
+    return (cfg.problem == "mini-render" and cfg.optimizer == "meta" and
+            cfg.pixel_count >= SCALED_MIN_PIXELS and cfg.trajectory == "optimise" and
+            cfg.diff_norm == "global" and not cfg.independent_variance_samples and
+            cfg.rng == "mt64")
+
+
+def _run_minirender_scaled(cfg: ExperimentConfig, replicate: int, ctx=None) -> "RunRecord":
+    """harness.cpp:90-200 for one large mini-render replicate: each iteration
+    is one fused kernel; the extractor series of coordinate `coord` and the
+    scalars are gathered on the device (no per-iteration host sync) and read
+    back once.  Divergence (non-finite params, harness.cpp:116) truncates."""
+    ctx = ctx or Context.default()
+    dt = torch.float64 if cfg.dtype == "f64" else torch.float32
+    run = MiniRenderRun(cfg.pixel_count, cfg.spp, gen_seed=cfg.problem_seed,
+                        albedo_init=cfg.albedo_init, exponent_max=cfg.exponent_max, lr=cfg.lr,
+                        beta_f=cfg.beta_f, beta_delta=cfg.beta_delta, eps_step=cfg.eps_step,
+                        eps_alpha=cfg.eps_alpha, clip=not cfg.no_alpha_clip, seed=cfg.seed,
+                        replicate=replicate, rng="mt64", dtype=dt, ctx=ctx)
+    it, c = cfg.iterations, cfg.coord
+    T = run.problem.target  # fp64 truth
+    ser = torch.full((11, it), float("nan"), dtype=torch.float64, device="cuda")
+    pr = torch.empty(1, dtype=dt, device="cuda")
+    df = torch.empty(1, dtype=dt, device="cuda")
+    loss0 = ((run.params.double() - T) ** 2).sum()
+    n, status, finals = it, "completed", None
+    D = cfg.pixel_count * cfg.spp
+    draws = evals = 0
+    changed_prev = 0.0  # params == prev before the first step (no diff)
+    for i in range(it):
+        p_i = run.params[c].double().clone()
+        loss_i = loss0 if i == 0 else run.scalars_buf[2].clone()  # step i overwrites it
+        run.step(prop_out=pr, diff_out=df, record=c)
+        m, v = run.mean[c].double(), run.var[c].double()
+        delta = (-cfg.lr * m) / (torch.sqrt(v) + cfg.eps_step)  # meta.hpp:112
+        ser[:, i] = torch.stack([torch.sqrt(loss_i), loss_i, pr[0].double(), df[0].double(), m, v,
+                                 run.alpha_prev[c].double(), delta, 2.0 * (p_i - T[c]),
+                                 run.scalars_buf[6], p_i])
+        draws += D
+        evals += D * (2 if changed_prev > 0 else 1)  # harness.cpp:129-131
+        sc = run.scalars()
+        changed_prev = sc.changed
+        if sc.nonfinite > 0:  # params of iteration i+1 non-finite: harness.cpp:116-119
+            n, status = i + 1, ("diverged" if i + 1 < it else "completed")
+            finals = run.prev  # params of iteration i (the last recorded)
+            if i + 1 < it:
+                break
+    if finals is None:
+        finals = run.prev
+    ser_h = ser.cpu().numpy()
+    ser_h[:, n:] = np.nan
+    finals = finals.double().cpu().numpy()
+    rec = RunRecord(status, n, draws, evals,
+                    {nm: ser_h[k] for k, nm in enumerate(_abi.SERIES_NAMES)}, finals)
+    if status != "diverged" and cfg.converge_threshold > 0.0 and n > 0:
+        if ser_h[0][n - 1] < cfg.converge_threshold:  # harness.cpp:191-198
+            rec.status = "converged"
+    return rec
+
+
 def _run_device(cfg: ExperimentConfig, rep_begin: int, rep_count: int, ctx=None):
+    if _scaled_eligible(cfg):
+        return [_run_minirender_scaled(cfg, r, ctx) for r in range(rep_begin, rep_begin + rep_count)]
     ctx = ctx or Context.default()
     c = cfg.to_c()
     it = cfg.iterations

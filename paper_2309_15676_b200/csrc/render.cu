@@ -30,6 +30,7 @@ struct RenderK {
   int philox;  // 0: uniforms buffer (mt19937_64 stream), 1: Philox counter
   uint64_t key;
   uint32_t iteration, stream, pixel_offset;
+  int64_t record;  // -1: full prop/diff outputs, else only this local pixel
 };
 
 // Uniforms of one pixel into u[0..spp): Philox in pairs (one 4x32 block
@@ -128,8 +129,17 @@ __global__ void __launch_bounds__(kThreads, sizeof(T) == 4 ? 3 : 2)
       st_plain(var + base, VA);
       st_plain(ap + base, AL);
       st_plain(pprev_next + base, PO);
-      if (prop_out) st_plain(prop_out + base, PR);
-      if (diff_out) st_plain(diff_out + base, DF);
+      if (k.record < 0) {
+        if (prop_out) st_plain(prop_out + base, PR);
+        if (diff_out) st_plain(diff_out + base, DF);
+      } else if (k.record >= base && k.record < base + W) {
+#pragma unroll
+        for (int w = 0; w < W; ++w)
+          if (base + w == k.record) {
+            if (prop_out) prop_out[0] = PR.v[w];
+            if (diff_out) diff_out[0] = DF.v[w];
+          }
+      }
     }
   }
   for (int64_t j = items * W + tid; j < P; j += stride) {
@@ -147,8 +157,13 @@ __global__ void __launch_bounds__(kThreads, sizeof(T) == 4 ? 3 : 2)
     var[j] = VA;
     ap[j] = AL;
     pprev_next[j] = PO;
-    if (prop_out) prop_out[j] = PR;
-    if (diff_out) diff_out[j] = DF;
+    if (k.record < 0) {
+      if (prop_out) prop_out[j] = PR;
+      if (diff_out) diff_out[j] = DF;
+    } else if (j == k.record) {
+      if (prop_out) prop_out[0] = PR;
+      if (diff_out) diff_out[0] = DF;
+    }
   }
   grid_reduce4<kThreads>(acc.partials(), partials, counter, [&](const ReducePartials& t) {
     sc->ssn = t.ssn;
@@ -169,8 +184,8 @@ int launch(mg_ctx* ctx, int64_t P, const RenderK& k, bool first, const void* b, 
   // chains); fp64: one pixel per thread (the packed fp64 body needs 155 regs)
   const bool vec = g_render_vec && sizeof(T) == 4 && aligned16(b) && aligned16(t) && aligned16(pnow) && aligned16(pprev) &&
                    aligned16(m2p) && aligned16(m2d) && aligned16(mean) && aligned16(var) &&
-                   aligned16(ap) && (!prop_out || aligned16(prop_out)) &&
-                   (!diff_out || aligned16(diff_out));
+                   aligned16(ap) && (k.record >= 0 || !prop_out || aligned16(prop_out)) &&
+                   (k.record >= 0 || !diff_out || aligned16(diff_out));
   const int64_t items = vec ? (P + VecOf<T>::width - 1) / VecOf<T>::width : P;
   const int grid = grid_for(ctx, items, kThreads, 8);
   auto run = [&](auto kernel) {
@@ -226,6 +241,8 @@ extern "C" int mg_minirender_meta_iteration(mg_ctx* ctx, int32_t dtype, int64_t 
   k.iteration = a->iteration;
   k.stream = a->stream;
   k.pixel_offset = a->pixel_offset;
+  k.record = a->record_plus1 > 0 ? int64_t(a->record_plus1) - 1 : -1;
+  if (k.record >= P) return fail(MG_EINVAL, "mg_minirender_meta_iteration: record index out of range");
   const bool first = a->update.first_step != 0;
   if (dtype == MG_F32)
     return launch<float>(ctx, P, k, first, exponents, target, uniforms, params_now,

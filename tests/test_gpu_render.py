@@ -131,3 +131,24 @@ def test_pixel_sharded_run_matches_unsharded(api, rng):
     got = np.concatenate([host(s.params) for s in shards])
     np.testing.assert_allclose(got, host(full.params), rtol=1e-12, atol=1e-15)
     assert full.scalars().loss == pytest.approx(float(tot[2]), rel=1e-12)
+
+
+@pytest.mark.parametrize("dt,rtol", [("f64", 1e-9), ("f32", 1e-4)])
+def test_scaled_run_single_matches_reference_series(api, oracle, dt, rtol):
+    """run_single of a large mini-render replicate dispatches to the fused
+    whole-GPU iteration (exact mt64 stream) and reproduces the reference's
+    extractor series and counters."""
+    P = api.SCALED_MIN_PIXELS + 1000
+    kw = dict(problem="mini-render", pixel_count=P, spp=2, iterations=15, seed=2,
+              problem_seed=9, lr=0.02, coord=777)
+    cfg = api.ExperimentConfig(dtype=dt, **kw)
+    assert api._scaled_eligible(cfg)
+    rec = api.run_single(cfg, 1)
+    ser, recs, finals = oracle.run_series(_abi.config_from(**kw), 2)
+    assert (rec.iterations_run, rec.draws_used, rec.evals_used) == recs[1][0:1] + recs[1][2:4]
+    for name in ("loss", "param_err", "prop", "diff", "grad_est", "est_var", "alpha", "delta",
+                 "true_grad", "step_sq_norm", "param"):
+        ref = ser[name][1]
+        scale = np.max(np.abs(ref)) + 1e-300
+        np.testing.assert_allclose(rec.series[name], ref, rtol=rtol, atol=rtol * scale,
+                                   err_msg=name)
