@@ -264,6 +264,23 @@ int mg_meta_update(mg_ctx* ctx, int32_t dtype, int64_t n, const mg_meta_update_a
                    void* var, void* alpha_prev, const void* params_in, void* params_out,
                    mg_update_scalars* scalars, const mg_meta_extras* x);
 
+/* Tile-sharded SHARED parameters (configs 4/5 shape), one rank's step as one
+ * kernel over peer memory: for the parameter shard [shard_lo, shard_lo +
+ * shard_n) it sums the world ranks' partial sample pairs prop_parts[q],
+ * diff_parts[q] (device pointers to full-length vectors, local or NVLink
+ * peer, summed in rank order 0..world-1), runs the fused meta update on its
+ * shard state (m2_prop.. alpha_prev, target: shard-length), and stores the
+ * new parameters into params_out[q] + shard_lo for every rank q
+ * (all-gather).  params_in is this rank's full current parameter vector.
+ * world <= 8.  The caller fences the ranks around the call (e.g. a
+ * symmetric-memory barrier) and all-reduces the first 4 scalars. */
+int mg_shared_meta_update(mg_ctx* ctx, int32_t dtype, int64_t shard_n, int64_t shard_lo,
+                          int32_t world, const mg_meta_update_args* a,
+                          const void* const* prop_parts, const void* const* diff_parts,
+                          void* const* params_out, const void* params_in, void* m2_prop,
+                          void* m2_diff, void* mean, void* var, void* alpha_prev,
+                          const void* target, mg_update_scalars* scalars);
+
 /* Fused Adam baseline iteration (adam.hpp:23-37 + harness.cpp:165-166,
  * 182-188): m, v updated, params_out = project(params_in + delta), with the
  * same ssn/loss reductions into scalars. */

@@ -256,6 +256,67 @@ __global__ void __launch_bounds__(kTmaThreads, kMinBlocks)
   });
 }
 
+// ------------------------------------- shared-parameter fused step (peers)
+// One rank's part of a tile-sharded shared-parameter iteration (SURVEY.md
+// §8(e), configs 4/5 shape) as ONE kernel over NVLink peer memory: for its
+// parameter shard it sums the ranks' partial sample pairs straight out of
+// their buffers (reduce-scatter, rank order 0..G-1: deterministic), runs the
+// fused meta update, and stores the new parameters into every rank's
+// parameter buffer (all-gather by peer stores).  No staging copies; the only
+// other collective is the 4-double scalar all-reduce.
+constexpr int kMaxPeers = 8;
+template <class T>
+struct PeerPtrs {
+  const T* prop[kMaxPeers];
+  const T* diff[kMaxPeers];
+  T* params_out[kMaxPeers];
+};
+
+template <class T, bool FIRST>
+__global__ void __launch_bounds__(kThreads)
+    shared_meta_update_kernel(int64_t n, int64_t lo, int world, MetaK k, PeerPtrs<T> pp,
+                              const T* __restrict__ pin, T* __restrict__ m2p,
+                              T* __restrict__ m2d, T* __restrict__ mean, T* __restrict__ var,
+                              T* __restrict__ ap, const T* __restrict__ target,
+                              mg_update_scalars* sc, ReducePartials* partials,
+                              unsigned int* counter) {
+  const StepScal s = load_step_scalars(k, sc);
+  const bool has_target = target != nullptr;
+  Acc acc;
+  for (int64_t i = int64_t(blockIdx.x) * kThreads + threadIdx.x; i < n;
+       i += int64_t(gridDim.x) * kThreads) {
+    const int64_t g = lo + i;
+    T prop = pp.prop[0][g], diff = pp.diff[0][g];
+    for (int q = 1; q < world; ++q) {  // reduce-scatter from the peers, fixed order
+      prop = prop + pp.prop[q][g];
+      diff = diff + pp.diff[q][g];
+    }
+    T M2P = FIRST ? T(0) : m2p[i];
+    T M2D = s.cnt0 > 0 ? m2d[i] : T(0);
+    T ME = FIRST ? T(0) : mean[i];
+    T VA = FIRST ? T(0) : var[i];
+    T AP = FIRST ? T(0) : ap[i];
+    T PO, DL;
+    meta_elem<T, FIRST>(k, s, prop, diff, prop, diff, M2P, M2D, ME, VA, AP, pin[g], T(0),
+                        has_target ? target[i] : T(0), has_target, PO, DL, acc);
+    m2p[i] = M2P;
+    if (s.active) m2d[i] = M2D;
+    mean[i] = ME;
+    var[i] = VA;
+    ap[i] = AP;
+    for (int q = 0; q < world; ++q) pp.params_out[q][g] = PO;  // all-gather by peer stores
+  }
+  grid_reduce4<kThreads>(acc.partials(), partials, counter, [&](const ReducePartials& t) {
+    sc->ssn = t.ssn;
+    sc->changed = t.changed;
+    sc->loss = has_target ? t.loss : nan("");
+    sc->nonfinite = t.nonfinite;
+    sc->diff_count = s.cnt;
+    sc->diff_decay_pow = s.dpow;
+    sc->ssn_used = s.ssn;
+  });
+}
+
 // ------------------------------------------------------------------- Adam
 struct AdamK {
   double beta1, beta2, c1, c2, d1, d2, lr, eps, proj_lo;
@@ -561,6 +622,50 @@ int mg_meta_update(mg_ctx* ctx, int32_t dtype, int64_t n, const mg_meta_update_a
     return launch_meta_update<double>(ctx, n, k, q, a->first_step != 0, scalars);
   }
   return fail(MG_EINVAL, "mg_meta_update: unknown dtype");
+}
+
+int mg_shared_meta_update(mg_ctx* ctx, int32_t dtype, int64_t shard_n, int64_t shard_lo,
+                          int32_t world, const mg_meta_update_args* a,
+                          const void* const* prop_parts, const void* const* diff_parts,
+                          void* const* params_out, const void* params_in, void* m2_prop,
+                          void* m2_diff, void* mean, void* var, void* alpha_prev,
+                          const void* target, mg_update_scalars* scalars) {
+  if (!ctx || !a || !scalars || !prop_parts || !diff_parts || !params_out || !params_in)
+    return fail(MG_EINVAL, "mg_shared_meta_update: null argument");
+  if (world < 1 || world > kMaxPeers)
+    return fail(MG_EINVAL, "mg_shared_meta_update: world must be 1..8");
+  if (shard_n < 0 || shard_lo < 0) return fail(MG_EINVAL, "mg_shared_meta_update: bad shard");
+  if (a->diff_norm != MG_DIFF_NORM_GLOBAL)
+    return fail(MG_EUNSUPPORTED, "mg_shared_meta_update: global diff norm only");
+  if (shard_n == 0) return MG_OK;
+  const MetaK k = make_meta_k(a);
+  const bool first = a->first_step != 0;
+  const int grid = grid_for(ctx, shard_n, kThreads, 8);
+  auto go = [&](auto tag) {
+    using T = decltype(tag);
+    PeerPtrs<T> pp{};
+    for (int q = 0; q < world; ++q) {
+      pp.prop[q] = static_cast<const T*>(prop_parts[q]);
+      pp.diff[q] = static_cast<const T*>(diff_parts[q]);
+      pp.params_out[q] = static_cast<T*>(params_out[q]);
+    }
+    auto kern = first ? shared_meta_update_kernel<T, true> : shared_meta_update_kernel<T, false>;
+    kern<<<grid, kThreads, 0, ctx->stream>>>(shard_n, shard_lo, world, k, pp,
+                                             static_cast<const T*>(params_in),
+                                             static_cast<T*>(m2_prop), static_cast<T*>(m2_diff),
+                                             static_cast<T*>(mean), static_cast<T*>(var),
+                                             static_cast<T*>(alpha_prev),
+                                             static_cast<const T*>(target), scalars,
+                                             ctx->partials, ctx->counter);
+  };
+  if (dtype == MG_F32)
+    go(float{});
+  else if (dtype == MG_F64)
+    go(double{});
+  else
+    return fail(MG_EINVAL, "mg_shared_meta_update: unknown dtype");
+  MG_LAUNCH_CHECK(ctx);
+  return MG_OK;
 }
 
 int mg_adam_update(mg_ctx* ctx, int32_t dtype, int64_t n, mg_adam_scalars* s, int32_t project,

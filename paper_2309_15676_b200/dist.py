@@ -136,3 +136,89 @@ class SharedParamStep:
             dist.all_gather_into_tensor(params_full_out, p_out, group=self.group)
         else:
             params_full_out.copy_(p_out)
+
+
+class SharedParamStepP2P:
+    """SharedParamStep as ONE kernel over NVLink peer memory per rank
+    (mg_shared_meta_update): the partial sample pairs and both parameter
+    ping-pong buffers live in torch symmetric memory, so each rank reduces its
+    shard straight out of the peers' buffers (rank order, deterministic) and
+    stores the updated shard into every peer's parameter buffer — no NCCL
+    reduce-scatter/all-gather, no staging copies.  Two symmetric-memory
+    barriers fence the step; the 4 scalars are all-reduced with NCCL.
+
+    Tested with emulated ranks on one GPU (tests/test_gpu_parity.py::
+    test_shared_param_peer_kernel_emulated_ranks); this round's environment
+    has a single GPU, so the symmetric-memory plumbing itself is not
+    exercised on >1 GPU yet."""
+
+    def __init__(self, n: int, dtype=None, group=None, lr=0.01, beta_f=0.9, beta_delta=0.5,
+                 eps_step=1e-8, eps_alpha=1e-30, clip=True, project_lo=None, init=0.0):
+        import ctypes as C
+
+        import torch
+        import torch.distributed as dist
+        import torch.distributed._symmetric_memory as symm_mem
+
+        from . import _abi
+        from .api import Context
+
+        dtype = dtype or torch.float32
+        self.C, self._abi, self.torch, self.dist = C, _abi, torch, dist
+        self.group = group or dist.group.WORLD
+        self.world = dist.get_world_size(self.group)
+        self.rank = dist.get_rank(self.group)
+        if n % self.world:
+            raise ValueError("shared parameter count must divide evenly across ranks")
+        self.n, self.S, self.dtype = n, n // self.world, dtype
+        dev = torch.device("cuda", torch.cuda.current_device())
+        self.ctx = Context.default()
+
+        def symm(fill=None):
+            t = symm_mem.empty(n, dtype=dtype, device=dev)
+            if fill is not None:
+                t.fill_(fill)
+            h = symm_mem.rendezvous(t, self.group)
+            assert t.data_ptr() == h.buffer_ptrs[self.rank], "tensor not at allocation base"
+            return t, h
+
+        self.prop, self.h_prop = symm()
+        self.diff, self.h_diff = symm()
+        self.params, self.h_params = symm(init)
+        self.params_next, self.h_next = symm(init)
+        mk = lambda: torch.empty(self.S, dtype=dtype, device=dev)  # noqa: E731
+        self.state = [mk() for _ in range(5)]
+        self.scalars_buf = torch.zeros(8, dtype=torch.float64, device=dev)
+        from ._lib import check, load
+        self._check, self._L = check, load()
+        self._check(self._L.mg_scalars_write(self.ctx.h, C.c_void_p(self.scalars_buf.data_ptr()),
+                                             C.byref(_abi.fresh_scalars())))
+        self.meta = _abi.MetaParams(lr, eps_step, eps_alpha, int(clip))
+        self.beta_f, self.beta_delta, self.project_lo = beta_f, beta_delta, project_lo
+        self.t, self.bp = 0, 1.0
+
+    def __call__(self, target_shard=None):
+        """One iteration; the caller has written this rank's partial pair into
+        self.prop / self.diff (e.g. rendered straight into them)."""
+        C, _abi = self.C, self._abi
+        self.t += 1
+        self.bp *= self.beta_f
+        a = _abi.MetaUpdateArgs(meta=self.meta, prop_coef=(1.0 - self.beta_f) / (1.0 - self.bp),
+                                beta_delta=self.beta_delta, first_step=int(self.t == 1),
+                                project=int(self.project_lo is not None),
+                                proj_lo=self.project_lo or 0.0)
+        arr = lambda ptrs: (C.c_void_p * self.world)(*ptrs)  # noqa: E731
+        self.h_prop.barrier()                      # every rank's partials are written
+        self._check(self._L.mg_shared_meta_update(
+            self.ctx.h, _abi.MG_F32 if self.dtype == self.torch.float32 else _abi.MG_F64,
+            self.S, self.rank * self.S, self.world, C.byref(a), arr(self.h_prop.buffer_ptrs),
+            arr(self.h_diff.buffer_ptrs), arr(self.h_next.buffer_ptrs),
+            C.c_void_p(self.params.data_ptr()),
+            *[C.c_void_p(x.data_ptr()) for x in self.state],
+            None if target_shard is None else C.c_void_p(target_shard.data_ptr()),
+            C.c_void_p(self.scalars_buf.data_ptr())))
+        self.h_next.barrier()                      # every shard stored everywhere
+        if self.world > 1:
+            self.dist.all_reduce(self.scalars_buf[:4], op=self.dist.ReduceOp.SUM, group=self.group)
+        self.params, self.params_next = self.params_next, self.params
+        self.h_params, self.h_next = self.h_next, self.h_params

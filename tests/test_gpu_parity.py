@@ -448,3 +448,61 @@ def test_tma_pipeline_matches_register_kernel(api, dt):
     for f in ("ssn", "changed", "nonfinite", "diff_count", "diff_decay_pow"):
         assert getattr(a[6], f) == getattr(b[6], f), f
     np.testing.assert_allclose(a[6].loss, b[6].loss, rtol=1e-12)
+
+
+@pytest.mark.parametrize("world", [1, 3])
+def test_shared_param_peer_kernel_emulated_ranks(api, oracle, world):
+    """mg_shared_meta_update, the tile-sharded shared-parameter step as one
+    kernel over peer memory, with `world` ranks emulated on this GPU (each
+    rank's buffers distinct, one launch per rank, no launch waits on another;
+    the scalar all-reduce done by summation between iterations).  Every
+    rank's parameter copy equals the oracle run on the summed sample pairs,
+    bit for bit (same step norm handed to both)."""
+    import ctypes as C
+    from paper_2309_15676_b200 import _lib
+    L = _lib.load()
+    ctx = api.Context.default()
+    S, steps = 4099, 5
+    n = S * world
+    rs = np.random.RandomState(world)
+    dev = lambda a: torch.tensor(a, dtype=torch.float64, device="cuda")  # noqa: E731
+    p = lambda t: C.c_void_p(t.data_ptr())  # noqa: E731
+    pin = [dev(np.full(n, 0.3)) for _ in range(world)]
+    pout = [torch.empty(n, dtype=torch.float64, device="cuda") for _ in range(world)]
+    st = [[torch.empty(S, dtype=torch.float64, device="cuda") for _ in range(5)]
+          for _ in range(world)]
+    target = rs.uniform(0, 1, n)
+    sc = [torch.zeros(8, dtype=torch.float64, device="cuda") for _ in range(world)]
+    for r in range(world):
+        L.mg_scalars_write(ctx.h, p(sc[r]), C.byref(_abi.fresh_scalars()))
+    ost = oracle_state(n)
+    osc = _abi.fresh_scalars()
+    p_host = np.full(n, 0.3)
+    bp = 1.0
+    for t in range(steps):
+        props = [rs.standard_normal(n) for _ in range(world)]
+        diffs = [np.zeros(n) if t == 0 else 0.1 * rs.standard_normal(n) for _ in range(world)]
+        dprops, ddiffs = [dev(x) for x in props], [dev(x) for x in diffs]
+        bp *= 0.9
+        a = _abi.MetaUpdateArgs(meta=_abi.MetaParams(0.01, 1e-8, 1e-30, 1),
+                                prop_coef=(1 - 0.9) / (1 - bp), beta_delta=0.5,
+                                first_step=int(t == 0), project=1, ssn_from_host=1,
+                                ssn_host=osc.ssn)
+        tot_p, tot_d = props[0].copy(), diffs[0].copy()
+        for q in range(1, world):
+            tot_p, tot_d = tot_p + props[q], tot_d + diffs[q]
+        p_host, _, rc = oracle.meta_update(a, ost, tot_p, tot_d, p_host, osc, target=target)
+        arr = lambda ts: (C.c_void_p * world)(*[t_.data_ptr() for t_ in ts])  # noqa: E731
+        for r in range(world):
+            lo = r * S
+            assert L.mg_shared_meta_update(
+                ctx.h, _abi.MG_F64, S, lo, world, C.byref(a), arr(dprops), arr(ddiffs),
+                arr(pout), p(pin[r]), *[p(x) for x in st[r]], p(dev(target[lo:lo + S])),
+                p(sc[r])) == 0
+        tot = sum(x[:4] for x in sc)
+        for r in range(world):
+            sc[r][:4] = tot
+        for r in range(world):
+            assert bits_equal(host(pout[r]), p_host), (t, r)
+        np.testing.assert_allclose(float(tot[0]), osc.ssn, rtol=1e-12)
+        pin, pout = pout, pin
