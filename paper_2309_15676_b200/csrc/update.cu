@@ -27,9 +27,10 @@ namespace mg {
 // Test/benchmark switch: force the register-streaming kernel (mg_set_option).
 bool g_disable_tma = false;
 extern bool g_render_vec;
-// -1: per-dtype default measured on B200 (tools/sweep_update_variants.py):
-// fp32 -> variant 4 (3 CTAs/SM x 256 thr, 2 stages; the fp32 body is
-// issue-heavy, more warps hide it), fp64 -> variant 0 (1 CTA/SM, 4 stages).
+// -1: per-dtype default measured on B200 (tools/sweep_update_variants.py,
+// profiles/r01_sweep_update_variants_*): fp32 -> variant 6 (2 CTAs/SM x 192
+// threads, 4 stages of 3 KB tiles: the fp32 body is issue-heavy, so it wants
+// both warps and depth), fp64 -> variant 0 (1 CTA/SM x 256 thr, 4 stages).
 int g_tma_variant = -1;
 namespace {
 
@@ -134,9 +135,14 @@ __host__ __device__ constexpr TmaVariant tma_variant(int i) {
        : i == 1 ? TmaVariant{256, 3, 2}
        : i == 2 ? TmaVariant{512, 3, 1}
        : i == 3 ? TmaVariant{128, 3, 4}
-                : TmaVariant{256, 2, 3};
+       : i == 4 ? TmaVariant{256, 2, 3}
+       : i == 5 ? TmaVariant{160, 5, 2}
+       : i == 6 ? TmaVariant{192, 4, 2}
+       : i == 7 ? TmaVariant{224, 3, 2}
+       : i == 8 ? TmaVariant{96, 4, 4}
+                : TmaVariant{192, 3, 2};
 }
-constexpr int kNumTmaVariants = 5;
+constexpr int kNumTmaVariants = 10;
 
 template <class T, int THREADS>
 __host__ __device__ constexpr int tma_tile() { return THREADS * VecOf<T>::width; }
@@ -483,12 +489,17 @@ int launch_meta_update(mg_ctx* ctx, int64_t n, const MetaK& k, const MetaPtrs<T>
       else
         run_tma(meta_update_tma_kernel<T, false, v.threads, v.stages, v.ctas_per_sm>, vc);
     };
-    const int variant = g_tma_variant >= 0 ? g_tma_variant : (sizeof(T) == 4 ? 4 : 0);
+    const int variant = g_tma_variant >= 0 ? g_tma_variant : (sizeof(T) == 4 ? 6 : 0);
     switch (variant) {
       case 1: pick(std::integral_constant<int, 1>{}); break;
       case 2: pick(std::integral_constant<int, 2>{}); break;
       case 3: pick(std::integral_constant<int, 3>{}); break;
       case 4: pick(std::integral_constant<int, 4>{}); break;
+      case 5: pick(std::integral_constant<int, 5>{}); break;
+      case 6: pick(std::integral_constant<int, 6>{}); break;
+      case 7: pick(std::integral_constant<int, 7>{}); break;
+      case 8: pick(std::integral_constant<int, 8>{}); break;
+      case 9: pick(std::integral_constant<int, 9>{}); break;
       default: pick(std::integral_constant<int, 0>{}); break;
     }
     MG_LAUNCH_CHECK(ctx);

@@ -26,7 +26,7 @@ peak = json.load(open(os.path.join(os.path.dirname(__file__), "..", "MEASURED_PE
 bpp = 56 if a.dtype == "f32" else 112
 res = {}
 for name, opts in [("register", {"disable_tma": 1})] + [
-        (f"tma{v}", {"disable_tma": 0, "tma_variant": v}) for v in range(5)]:
+        (f"tma{v}", {"disable_tma": 0, "tma_variant": v}) for v in range(10)]:
     for k, v in opts.items():
         L.mg_set_option(k.encode(), v)
     upd = api.FusedMetaUpdate(n, dtype=dt)
