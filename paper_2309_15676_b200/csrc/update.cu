@@ -402,6 +402,96 @@ __global__ void __launch_bounds__(kThreads)
   });
 }
 
+// TMA-pipelined Adam update: grad, m, v, pi (+ target) streamed through a
+// shared-memory ring by bulk copies, m, v, pi' stored from registers.
+constexpr int kAdamArrays = 5;  // grad m v pin target
+
+template <class T, bool FIRST, int kTh, int kSt, int kMinB>
+__global__ void __launch_bounds__(kTh, kMinB)
+    adam_update_tma_kernel(int64_t n, AdamK k, const T* grad, T* m, T* v, const T* pin, T* pout,
+                           const T* target, T* delta, mg_update_scalars* sc,
+                           ReducePartials* partials, unsigned int* counter) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  __shared__ __align__(8) uint64_t full[kSt];
+  constexpr int W = VecOf<T>::width;
+  constexpr int TILE = kTh * W;
+  T* sbuf = reinterpret_cast<T*>(smem_raw);
+  const double ssn_in = __ldcg(&sc->ssn);
+  const bool has_target = target != nullptr;
+  const T* src[kAdamArrays] = {grad, m, v, pin, target};
+  const bool use[kAdamArrays] = {true, !FIRST, !FIRST, true, has_target};
+  uint32_t tx = 0;
+#pragma unroll
+  for (int a = 0; a < kAdamArrays; ++a) tx += use[a] ? uint32_t(TILE * sizeof(T)) : 0u;
+  const int64_t tiles = n / TILE;
+  const int64_t my_tiles =
+      int64_t(blockIdx.x) < tiles ? (tiles - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
+  if (threadIdx.x == 0) {
+    for (int st = 0; st < kSt; ++st) mbar_init(&full[st], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  const uint64_t pol = l2_evict_first_policy();
+  auto issue = [&](int64_t li) {
+    const int st = int(li % kSt);
+    const int64_t tile = int64_t(blockIdx.x) + li * gridDim.x;
+    mbar_arrive_expect_tx(&full[st], tx);
+#pragma unroll
+    for (int a = 0; a < kAdamArrays; ++a)
+      if (use[a])
+        bulk_g2s_hint(sbuf + (size_t(st) * kAdamArrays + a) * TILE, src[a] + tile * TILE,
+                      uint32_t(TILE * sizeof(T)), &full[st], pol);
+  };
+  if (threadIdx.x == 0)
+    for (int64_t li = 0; li < my_tiles && li < kSt; ++li) issue(li);
+  Acc acc;
+  const int e = threadIdx.x * W;
+  for (int64_t li = 0; li < my_tiles; ++li) {
+    const int st = int(li % kSt);
+    mbar_wait(&full[st], uint32_t((li / kSt) & 1));
+    const T* sb = sbuf + size_t(st) * kAdamArrays * TILE + e;
+    const Pack<T> G = ld_plain(sb);
+    Pack<T> M{}, V{}, TG{}, PO, DL;
+    if (!FIRST) {
+      M = ld_plain(sb + TILE);
+      V = ld_plain(sb + 2 * TILE);
+    }
+    const Pack<T> PI = ld_plain(sb + 3 * TILE);
+    if (has_target) TG = ld_plain(sb + 4 * TILE);
+#pragma unroll
+    for (int w = 0; w < W; ++w)
+      adam_elem<T>(k, G.v[w], M.v[w], V.v[w], PI.v[w], TG.v[w], has_target, PO.v[w], DL.v[w],
+                   acc);
+    const int64_t b = (int64_t(blockIdx.x) + li * gridDim.x) * TILE + e;
+    st_plain(m + b, M);
+    st_plain(v + b, V);
+    st_plain(pout + b, PO);
+    if (delta) st_plain(delta + b, DL);
+    __syncthreads();
+    if (threadIdx.x == 0 && li + kSt < my_tiles) {
+      fence_proxy_async_smem();
+      issue(li + kSt);
+    }
+  }
+  const int64_t tid = int64_t(blockIdx.x) * kTh + threadIdx.x;
+  for (int64_t i = tiles * TILE + tid; i < n; i += int64_t(gridDim.x) * kTh) {
+    T M = FIRST ? T(0) : m[i], V = FIRST ? T(0) : v[i], PO, DL;
+    adam_elem<T>(k, grad[i], M, V, pin[i], has_target ? target[i] : T(0), has_target, PO, DL,
+                 acc);
+    m[i] = M;
+    v[i] = V;
+    pout[i] = PO;
+    if (delta) delta[i] = DL;
+  }
+  grid_reduce4<kTh>(acc.partials(), partials, counter, [&](const ReducePartials& t) {
+    sc->ssn = t.ssn;
+    sc->changed = t.changed;
+    sc->loss = has_target ? t.loss : nan("");
+    sc->nonfinite = t.nonfinite;
+    sc->ssn_used = ssn_in;
+  });
+}
+
 // ------------------------------------------------------- standalone steps
 template <class T>
 __global__ void moment2_kernel(int64_t n, double c, bool first, T* __restrict__ m2,
@@ -525,6 +615,22 @@ int launch_adam_update(mg_ctx* ctx, int64_t n, const AdamK& k, bool first, const
   const bool vec = aligned16(grad) && aligned16(m) && aligned16(v) && aligned16(pin) &&
                    aligned16(pout) && (!target || aligned16(target)) &&
                    (!delta || aligned16(delta));
+  // TMA ring: 192 threads x 4 stages x 5 arrays x 3 KB (fp32) per CTA, 2 CTAs/SM
+  constexpr int kTh = 192, kSt = 4;
+  if (vec && !g_disable_tma && n >= int64_t(kTh) * VecOf<T>::width * ctx->sm_count) {
+    constexpr size_t smem = size_t(kSt) * kAdamArrays * kTh * VecOf<T>::width * sizeof(T);
+    auto run_tma = [&](auto kernel) {
+      cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+      const int64_t tiles = n / (int64_t(kTh) * VecOf<T>::width);
+      const int64_t want = int64_t(ctx->sm_count) * 2;
+      kernel<<<int(tiles < want ? tiles : want), kTh, smem, ctx->stream>>>(
+          n, k, grad, m, v, pin, pout, target, delta, sc, ctx->partials, ctx->counter);
+    };
+    first ? run_tma(adam_update_tma_kernel<T, true, kTh, kSt, 2>)
+          : run_tma(adam_update_tma_kernel<T, false, kTh, kSt, 2>);
+    MG_LAUNCH_CHECK(ctx);
+    return MG_OK;
+  }
   const int64_t items = vec ? (n + VecOf<T>::width - 1) / VecOf<T>::width : n;
   const int grid = grid_for(ctx, items, kThreads, 8);
   auto run = [&](auto kernel) {

@@ -506,3 +506,28 @@ def test_shared_param_peer_kernel_emulated_ranks(api, oracle, world):
             assert bits_equal(host(pout[r]), p_host), (t, r)
         np.testing.assert_allclose(float(tot[0]), osc.ssn, rtol=1e-12)
         pin, pout = pout, pin
+
+
+@pytest.mark.parametrize("dt", [torch.float32, torch.float64])
+def test_adam_tma_matches_register_kernel(api, dt):
+    from paper_2309_15676_b200 import _lib
+    L = _lib.load()
+    n = 768 * 148 * 3 + 331
+    rs = np.random.RandomState(4)
+    grads = [cu(rs.standard_normal(n), dt) for _ in range(4)]
+    target = cu(rs.uniform(0, 1, n), dt)
+    outs = []
+    for disable in (0, 1):
+        L.mg_set_option(b"disable_tma", disable)
+        try:
+            up = api.FusedAdamUpdate(n, dtype=dt, lr=0.02)
+            pa = torch.full((n,), 0.5, dtype=dt, device="cuda")
+            pb = torch.empty_like(pa)
+            for g in grads:
+                up.step(g, pa, pb, target=target)
+                pa, pb = pb, pa
+            outs.append((host(pa), host(up.m), host(up.v)))
+        finally:
+            L.mg_set_option(b"disable_tma", 0)
+    for x, y in zip(*outs):
+        assert bits_equal(x, y)
