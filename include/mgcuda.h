@@ -362,6 +362,28 @@ int mg_minirender_meta_iteration(mg_ctx* ctx, int32_t dtype, int64_t P, const mg
                                  void* var, void* alpha_prev, mg_update_scalars* scalars,
                                  void* prop_out, void* diff_out);
 
+/* ---------------------------------------------------------------------------
+ * F1 slice (BASELINE.json configs[0]): path-traced gradient
+ * samples of a textured quad under a rectangular area light, direct lighting,
+ * Lambertian BSDF, RGB texture R x R (nearest), image W x H.  Not in the
+ * reference: scene and estimators are this repo's own
+ * (DESIGN.md §F1), checked against oracle/metagrad_oracle.c mgo_quad_*.
+ * Textures/gradients are channel-major [3][R*R], images [3][H*W], dtype
+ * arrays; Le is the light's RGB radiance (host).  Philox counters
+ * (pixel, iteration, sample, stream) with key = replicate seed.
+ * ------------------------------------------------------------------------- */
+/* spp-sample mean image of texture tex (iteration word 0xffffffff). */
+int mg_quad_render(mg_ctx* ctx, int32_t dtype, int32_t W, int32_t H, int32_t R, const double* Le,
+                   int32_t spp, uint64_t key, uint32_t stream, const void* tex, void* img);
+/* One gradient sample pair: prop/diff [3][R*R] (1 FD + 2 proportional spp
+ * per pixel), loss_out (device double) = unbiased estimate of
+ * sum (I - I*)^2.  accum: device scratch of 6*R*R int64, zero on first use
+ * (left zeroed).  Deterministic (fixed-point adjoint accumulation). */
+int mg_quad_sample_pair(mg_ctx* ctx, int32_t dtype, int32_t W, int32_t H, int32_t R,
+                        const double* Le, const void* target_img, const void* now,
+                        const void* prev, uint64_t key, uint32_t iteration, uint32_t stream,
+                        void* accum, void* prop, void* diff, double* loss_out);
+
 /* ------------------------------- device-resident run_single (A13, A14) */
 /* Per-replicate record of one coordinate plus scalars (harness.hpp:73-90;
  * full vectors are O(iterations*N) and are not recorded on the device). */

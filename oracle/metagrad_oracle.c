@@ -836,3 +836,125 @@ int mgo_run_single_series(const mg_experiment_config* cfg, int32_t replicate, mg
   problem_free(&p);
   return st;
 }
+
+
+/* =====================================================================
+ * F1 slice: textured quad under a rectangular area light, direct lighting
+ * (BASELINE.json configs[0] "PR1 ref").  Not in the reference:
+ * this is the repo's own CPU restatement of its own renderer
+ * (paper_2309_15676_b200/csrc/quad.cu), the oracle for that kernel.
+ * Scene, estimators and fixed-point adjoint accumulation are specified in
+ * DESIGN.md §F1.
+ * ===================================================================== */
+
+/* pinhole at (0,0,3) looking -z; image plane z=0 */
+static const double QS_HALF = 1.2;      /* image plane half-extent at z=0  */
+static const double QS_LX0 = -0.5, QS_LX1 = 0.5, QS_LY0 = 0.8, QS_LY1 = 1.4, QS_LZ = 1.5;
+static const double QS_FIX = 1099511627776.0; /* 2^40 fixed-point scale */
+static const double QS_PI = 3.14159265358979323846;
+
+/* radiance factor K_c = Le_c / pi * G * A for one NEE sample; 0 if the
+ * camera ray misses the quad.  Writes the texel index. */
+static void qs_sample(int W, int H, int R, int px, int py, const double u[4], int* texel,
+                      double K[3], const double Le[3]) {
+  const double nx = ((px + u[0]) / W) * 2.0 - 1.0;
+  const double ny = 1.0 - ((py + u[1]) / H) * 2.0;
+  const double x = QS_HALF * nx, y = QS_HALF * ny; /* hit on z = 0 */
+  if (x < -1.0 || x > 1.0 || y < -1.0 || y > 1.0) {
+    *texel = -1;
+    K[0] = K[1] = K[2] = 0.0;
+    return;
+  }
+  int tx = (int)(((x + 1.0) * 0.5) * R), ty = (int)(((y + 1.0) * 0.5) * R);
+  if (tx > R - 1) tx = R - 1;
+  if (ty > R - 1) ty = R - 1;
+  *texel = ty * R + tx;
+  const double lx = QS_LX0 + u[2] * (QS_LX1 - QS_LX0);
+  const double ly = QS_LY0 + u[3] * (QS_LY1 - QS_LY0);
+  const double wx = lx - x, wy = ly - y, wz = QS_LZ;
+  const double d2 = (wx * wx + wy * wy) + wz * wz;
+  const double inv = 1.0 / sqrt(d2);
+  const double cz = wz * inv; /* cos at the quad (n=+z) == cos at the light (n=-z) */
+  const double area = (QS_LX1 - QS_LX0) * (QS_LY1 - QS_LY0);
+  const double G = ((cz * cz) / d2) * area;
+  for (int c = 0; c < 3; ++c) K[c] = (Le[c] / QS_PI) * G;
+}
+
+static void qs_uniforms(uint64_t key, uint32_t pixel, uint32_t it, uint32_t sid, uint32_t st,
+                        double u[4]) {
+  const uint32_t ctr[4] = {pixel, it, sid, st};
+  uint32_t o[4];
+  mgo_philox4x32_10(ctr, key, o);
+  for (int k = 0; k < 4; ++k) u[k] = (double)o[k] * 0x1.0p-32;
+}
+
+/* Expected-image stand-in: spp-sample mean image [3][H*W] of texture tex
+ * [3][R*R] (channel-major), Philox stream `st`, iteration word 0xffffffff. */
+void mgo_quad_render(int W, int H, int R, const double* tex, const double Le[3], int spp,
+                     uint64_t key, uint32_t st, double* img) {
+  for (int py = 0; py < H; ++py)
+    for (int px = 0; px < W; ++px) {
+      double acc[3] = {0.0, 0.0, 0.0};
+      const uint32_t pix = (uint32_t)(py * W + px);
+      for (int s = 0; s < spp; ++s) {
+        double u[4], K[3];
+        int t;
+        qs_uniforms(key, pix, 0xffffffffu, (uint32_t)s, st, u);
+        qs_sample(W, H, R, px, py, u, &t, K, Le);
+        if (t < 0) continue;
+        for (int c = 0; c < 3; ++c) acc[c] += tex[c * R * R + t] * K[c];
+      }
+      for (int c = 0; c < 3; ++c) img[(size_t)c * W * H + pix] = acc[c] / (double)spp;
+    }
+}
+
+static int64_t qs_fix(double v) { return (int64_t)llrint(v * QS_FIX); }
+
+/* One gradient sample pair of the quad problem:
+ *   samples A, B (proportional) and C (finite difference) per pixel;
+ *   prop[c][t] = sum_p r_A K_B [t_B] + r_B K_A [t_A],   r_X = a[t_X] K_X - I*
+ *   diff[c][t] = sum_p dI_C K_A [t_A] + dI_C K_B [t_B], dI_C = (a - a_prev)[t_C] K_C
+ * accumulated in 2^-40 fixed point (order independent), returned as double.
+ * loss_est = sum_p,c r_A r_B (unbiased for sum (I - I*)^2). */
+void mgo_quad_sample_pair(int W, int H, int R, const double Le[3], const double* target_img,
+                          const double* now, const double* prev, uint64_t key, uint32_t it,
+                          uint32_t st, double* prop, double* diff, double* loss_est) {
+  const int T = R * R;
+  int64_t* fp = (int64_t*)calloc((size_t)3 * T, sizeof(int64_t));
+  int64_t* fd = (int64_t*)calloc((size_t)3 * T, sizeof(int64_t));
+  double loss = 0.0;
+  for (int py = 0; py < H; ++py)
+    for (int px = 0; px < W; ++px) {
+      const uint32_t pix = (uint32_t)(py * W + px);
+      double uA[4], uB[4], uC[4], KA[3], KB[3], KC[3];
+      int tA, tB, tC;
+      qs_uniforms(key, pix, it, 0, st, uA);
+      qs_uniforms(key, pix, it, 1, st, uB);
+      qs_uniforms(key, pix, it, 2, st, uC);
+      qs_sample(W, H, R, px, py, uA, &tA, KA, Le);
+      qs_sample(W, H, R, px, py, uB, &tB, KB, Le);
+      qs_sample(W, H, R, px, py, uC, &tC, KC, Le);
+      for (int c = 0; c < 3; ++c) {
+        const double Is = target_img[(size_t)c * W * H + pix];
+        const double rA = (tA >= 0 ? now[c * T + tA] * KA[c] : 0.0) - Is;
+        const double rB = (tB >= 0 ? now[c * T + tB] * KB[c] : 0.0) - Is;
+        const double dI = tC >= 0 ? (now[c * T + tC] - prev[c * T + tC]) * KC[c] : 0.0;
+        loss += rA * rB;
+        if (tB >= 0) {
+          fp[c * T + tB] += qs_fix(rA * KB[c]);
+          fd[c * T + tB] += qs_fix(dI * KB[c]);
+        }
+        if (tA >= 0) {
+          fp[c * T + tA] += qs_fix(rB * KA[c]);
+          fd[c * T + tA] += qs_fix(dI * KA[c]);
+        }
+      }
+    }
+  for (int k = 0; k < 3 * T; ++k) {
+    prop[k] = (double)fp[k] / QS_FIX;
+    diff[k] = (double)fd[k] / QS_FIX;
+  }
+  *loss_est = loss;
+  free(fp);
+  free(fd);
+}

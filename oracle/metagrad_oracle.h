@@ -114,6 +114,14 @@ typedef struct mgo_full_record {
   double* true_grad;
 } mgo_full_record;
 
+/* F1 slice: textured quad + rectangular area light, direct lighting (own
+ * renderer).  tex/now/prev/prop/diff: [3][R*R]; images [3][H*W]. */
+void mgo_quad_render(int W, int H, int R, const double* tex, const double Le[3], int spp,
+                     uint64_t key, uint32_t st, double* img);
+void mgo_quad_sample_pair(int W, int H, int R, const double Le[3], const double* target_img,
+                          const double* now, const double* prev, uint64_t key, uint32_t it,
+                          uint32_t st, double* prop, double* diff, double* loss_est);
+
 int mgo_problem_dim(const mg_experiment_config* cfg);
 int mgo_run_single(const mg_experiment_config* cfg, int32_t replicate, mg_run_record* rec,
                    const mgo_full_record* out);

@@ -96,6 +96,11 @@ def load():
                                                C.c_int32] + [_vp] * 7),
         "mg_minirender_meta_iteration": (C.c_int, [_vp, C.c_int32, C.c_int64, P(_abi.RenderArgs)] +
                                          [_vp] * 10 + [_vp, _vp, _vp]),
+        "mg_quad_render": (C.c_int, [_vp, C.c_int32, C.c_int32, C.c_int32, C.c_int32, _vp,
+                                     C.c_int32, C.c_uint64, C.c_uint32, _vp, _vp]),
+        "mg_quad_sample_pair": (C.c_int, [_vp, C.c_int32, C.c_int32, C.c_int32, C.c_int32, _vp,
+                                          _vp, _vp, _vp, C.c_uint64, C.c_uint32, C.c_uint32,
+                                          _vp, _vp, _vp, _vp]),
         "mg_run_replicates": (C.c_int, [_vp, P(_abi.ExperimentConfigC), C.c_int32, C.c_int32,
                                         _vp, P(_abi.RunSeriesC), _vp]),
     }

@@ -34,7 +34,8 @@ from ._lib import DomainError, InvalidArgument, LogicError, MgError, check, load
 
 __all__ = ["Context", "Rng", "Moment2", "GradientSamplePair", "MetaEstimator", "Adam",
            "MiniRenderProblem", "ExpRateProblem", "MultNoiseQuadratic", "FusedMetaUpdate",
-           "FusedAdamUpdate", "MiniRenderRun", "ExperimentConfig", "RunRecord", "AggregateReport", "run_single",
+           "FusedAdamUpdate", "MiniRenderRun", "QuadTextureProblem", "QuadTextureRun",
+           "ExperimentConfig", "RunRecord", "AggregateReport", "run_single",
            "run_experiment", "InvalidArgument", "LogicError", "DomainError", "mix64"]
 
 
@@ -622,6 +623,109 @@ class MiniRenderRun:
         out = _abi.UpdateScalars()
         check(load().mg_scalars_read(self.ctx.h, _p(self.scalars_buf), C.byref(out)))
         return out
+
+
+# ------------------------------------------------- F1 slice: textured quad
+class QuadTextureProblem:
+    """BASELINE.json configs[0] ("PR1 ref"): W x H image of one textured quad
+    lit by one rectangular area light, direct lighting only, Lambertian BSDF;
+    the parameters are an R x R RGB albedo texture ([3][R*R], channel-major).
+    The reference has no renderer; scene and estimators are this
+    repo's own, restated in oracle/metagrad_oracle.c.
+
+    Textures: Rng(mix64(seed)).uniform() x 3R^2 (init seed 0, target seed 1,
+    as the mini-render construction draws, problems.cpp:168-172); the target
+    image is a target_spp-sample render of the target texture."""
+
+    STREAM_TARGET = 7
+
+    def __init__(self, width: int = 64, height: int = 64, tex_res: int = 32,
+                 light=(8.0, 7.0, 6.0), init_seed: int = 0, target_seed: int = 1,
+                 target_spp: int = 1024, dtype=torch.float64, ctx=None):
+        self.ctx = ctx or Context.default()
+        self.W, self.H, self.R, self.dtype = width, height, tex_res, dtype
+        self.Le = (C.c_double * 3)(*light)
+        n = 3 * tex_res * tex_res
+        L = load()
+        self.init = Rng([L.mg_mix64(init_seed)], ctx=self.ctx).uniform(n)[0].to(dtype)
+        self.target_tex = Rng([L.mg_mix64(target_seed)], ctx=self.ctx).uniform(n)[0].to(dtype)
+        self.target_img = torch.empty(3 * width * height, dtype=dtype, device="cuda")
+        check(L.mg_quad_render(self.ctx.h, _dtype_code(self.target_tex), width, height, tex_res,
+                               self.Le, target_spp, L.mg_mix64(target_seed), self.STREAM_TARGET,
+                               _p(self.target_tex), _p(self.target_img)))
+        self.accum = torch.zeros(6 * tex_res * tex_res, dtype=torch.int64, device="cuda")
+        self.loss_buf = torch.zeros(1, dtype=torch.float64, device="cuda")
+
+    def dim(self) -> int:
+        return 3 * self.R * self.R
+
+    def draws_per_sample(self) -> int:
+        """Path samples per iteration: 2 proportional + 1 finite-difference spp."""
+        return 3 * self.W * self.H
+
+    def initial_params(self):
+        return self.init.clone()
+
+    def truth_params(self):
+        return self.target_tex
+
+    def render(self, tex, spp: int, key: int, stream: int = 3):
+        img = torch.empty(3 * self.W * self.H, dtype=tex.dtype, device="cuda")
+        check(load().mg_quad_render(self.ctx.h, _dtype_code(tex), self.W, self.H, self.R,
+                                    self.Le, spp, key, stream, _p(tex.contiguous()), _p(img)))
+        return img
+
+    def sample_pair(self, now, prev, iteration: int, key: int, stream: int = 0):
+        """One gradient sample pair (prop, diff) for the L2 image loss; the
+        returned pair's step_sq_norm is left to the fused update (device)."""
+        prop, diff = torch.empty_like(now), torch.empty_like(now)
+        check(load().mg_quad_sample_pair(self.ctx.h, _dtype_code(now), self.W, self.H, self.R,
+                                         self.Le, _p(self.target_img), _p(now.contiguous()),
+                                         _p(prev.contiguous()), key, iteration, stream,
+                                         _p(self.accum), _p(prop), _p(diff), _p(self.loss_buf)))
+        return GradientSamplePair(prop, diff)
+
+
+class QuadTextureRun:
+    """configs[0] optimisation loop on the device: per iteration one
+    gradient-sample-pair launch (render + adjoint scatter) and one fused
+    update (meta-estimator, or the Adam baseline), projection max(p, 0)."""
+
+    def __init__(self, problem: QuadTextureProblem, optimizer: str = "meta", lr: float = 0.01,
+                 seed: int = 0, replicate: int = 0, **kw):
+        self.p = problem
+        self.params = problem.initial_params()
+        self.prev = self.params.clone()
+        self.key = int(load().mg_stream_seed(seed, replicate))
+        n = problem.dim()
+        if optimizer == "meta":
+            self.upd = FusedMetaUpdate(n, dtype=problem.dtype, lr=lr, project_lo=0.0,
+                                       ctx=problem.ctx, **kw)
+        elif optimizer == "adam":
+            self.upd = FusedAdamUpdate(n, dtype=problem.dtype, lr=lr, project_lo=0.0,
+                                       ctx=problem.ctx, **kw)
+        else:
+            raise InvalidArgument(_abi.MG_EINVAL, "optimizer must be meta or adam")
+        self.optimizer = optimizer
+        self.t = 0
+
+    def step(self):
+        pair = self.p.sample_pair(self.params, self.prev if self.optimizer == "meta" else
+                                  self.params, self.t, self.key)
+        new = self.prev  # ping-pong: pi_{t-1} buffer receives pi_{t+1}
+        if self.optimizer == "meta":
+            self.upd.step(pair.prop, pair.diff, self.params, new)
+        else:
+            self.upd.step(pair.prop, self.params, new)
+        self.prev, self.params = self.params, new
+        self.t += 1
+        return pair
+
+    def loss_estimate(self) -> float:
+        return float(self.p.loss_buf[0])
+
+    def texture_error(self) -> float:
+        return float(torch.linalg.vector_norm((self.params - self.p.target_tex).double()))
 
 
 # ------------------------------------------------------------- harness

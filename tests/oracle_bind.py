@@ -220,6 +220,26 @@ class Oracle:
                     _ptr(prop), _ptr(diff))
         return prop, diff, ssn
 
+    # ------------------------------------------------------ F1 quad slice
+    def quad_render(self, W, H, R, tex, Le, spp, key, stream):
+        f = self.lib.mgo_quad_render
+        f.argtypes = [C.c_int, C.c_int, C.c_int, C.c_void_p, C.c_void_p, C.c_int, C.c_uint64,
+                      C.c_uint32, C.c_void_p]
+        img = np.empty(3 * W * H)
+        le = _f64(Le)
+        f(W, H, R, _ptr(_f64(tex)), _ptr(le), spp, key, stream, _ptr(img))
+        return img
+
+    def quad_sample_pair(self, W, H, R, Le, target_img, now, prev, key, it, stream=0):
+        f = self.lib.mgo_quad_sample_pair
+        f.argtypes = [C.c_int, C.c_int, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
+                      C.c_uint64, C.c_uint32, C.c_uint32, C.c_void_p, C.c_void_p, _dp]
+        n = 3 * R * R
+        prop, diff, loss = np.empty(n), np.empty(n), C.c_double()
+        f(W, H, R, _ptr(_f64(Le)), _ptr(_f64(target_img)), _ptr(_f64(now)), _ptr(_f64(prev)),
+          key, it, stream, _ptr(prop), _ptr(diff), C.byref(loss))
+        return prop, diff, loss.value
+
     # ----------------------------------------------------------- harness
     def run_single(self, cfg, replicate):
         dim = self.lib.mgo_problem_dim(C.byref(cfg))

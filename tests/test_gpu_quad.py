@@ -1,0 +1,129 @@
+"""F1 slice: path-traced gradient samples of the textured
+quad (BASELINE.json configs[0]) against the repo's own CPU oracle
+(oracle/metagrad_oracle.c mgo_quad_*; the reference has no renderer).
+
+  * fp64: render and gradient sample pairs BIT-EXACT (only IEEE + - * / sqrt,
+    Philox-addressed samples, fixed-point adjoint accumulation);
+  * fp32: <= 1e-5 of the gradient scale;
+  * the finite-difference sample is unbiased for the change of the
+    proportional sample's expectation (z-test over 4000 iterations);
+  * the meta-estimator and Adam both fit the target texture.
+"""
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+LE = (8.0, 7.0, 6.0)
+
+
+@pytest.fixture(scope="module")
+def api():
+    from paper_2309_15676_b200 import api as a
+    return a
+
+
+def host(t):
+    return t.detach().double().cpu().numpy()
+
+
+def bits_equal(a, b):
+    a, b = np.asarray(a, dtype=np.float64), np.asarray(b, dtype=np.float64)
+    return a.shape == b.shape and np.array_equal(a.view(np.uint64), b.view(np.uint64))
+
+
+def test_quad_render_and_target_bit_exact(api, oracle):
+    prob = api.QuadTextureProblem(64, 64, 32, LE, target_spp=64)
+    from paper_2309_15676_b200 import _lib
+    key = _lib.load().mg_mix64(1)
+    ref = oracle.quad_render(64, 64, 32, host(prob.target_tex), LE, 64, key, 7)
+    assert bits_equal(host(prob.target_img), ref)
+    assert (ref >= 0).all() and ref.max() > 0.05
+
+
+@pytest.mark.parametrize("W,H,R", [(64, 64, 32), (96, 80, 16), (256, 256, 64)])
+def test_quad_sample_pair_bit_exact_fp64(api, oracle, W, H, R):
+    prob = api.QuadTextureProblem(W, H, R, LE, target_spp=16)
+    rs = np.random.RandomState(R)
+    now = rs.uniform(0, 1, 3 * R * R)
+    prev = now - 0.01 * rs.uniform(0, 1, now.size)
+    tnow = torch.tensor(now, device="cuda")
+    tprev = torch.tensor(prev, device="cuda")
+    for it in (0, 5):
+        pair = prob.sample_pair(tnow, tprev, it, key=12345)
+        p, d, loss = oracle.quad_sample_pair(W, H, R, LE, host(prob.target_img), now, prev,
+                                             12345, it)
+        assert bits_equal(host(pair.prop), p), it
+        assert bits_equal(host(pair.diff), d), it
+        assert float(prob.loss_buf[0]) == pytest.approx(loss, rel=1e-12)
+    same = prob.sample_pair(tnow, tnow, 3, key=1)
+    assert (host(same.diff) == 0).all()
+
+
+def test_quad_sample_pair_fp32(api, oracle):
+    W, H, R = 64, 64, 32
+    prob = api.QuadTextureProblem(W, H, R, LE, target_spp=16, dtype=torch.float32)
+    rs = np.random.RandomState(0)
+    now = rs.uniform(0, 1, 3 * R * R).astype(np.float32)
+    prev = (now - 0.01 * rs.uniform(0, 1, now.size)).astype(np.float32)
+    pair = prob.sample_pair(torch.tensor(now, device="cuda"), torch.tensor(prev, device="cuda"),
+                            2, key=99)
+    p, d, _ = oracle.quad_sample_pair(W, H, R, LE, host(prob.target_img), now, prev, 99, 2)
+    scale = np.abs(p).max()
+    assert np.abs(host(pair.prop) - p).max() < 1e-5 * scale
+    assert np.abs(host(pair.diff) - d).max() < 1e-5 * max(np.abs(d).max(), 1e-30) + 1e-9
+
+
+def test_quad_fd_sample_is_unbiased(api):
+    """E[diff(theta_t, theta_{t-1})] = E[prop(theta_t)] - E[prop(theta_{t-1})]:
+    the common-random-number difference estimates the gradient change."""
+    W, H, R, K = 32, 32, 8, 4000
+    prob = api.QuadTextureProblem(W, H, R, LE, target_spp=256)
+    rs = np.random.RandomState(3)
+    a = torch.tensor(rs.uniform(0.2, 0.8, 3 * R * R), device="cuda")
+    b = a - torch.tensor(0.05 * rs.uniform(0.5, 1.0, 3 * R * R), device="cuda")
+    d_sum = torch.zeros_like(a)
+    d_sq = torch.zeros_like(a)
+    pa = torch.zeros_like(a)
+    pa_sq = torch.zeros_like(a)
+    pb = torch.zeros_like(a)
+    pb_sq = torch.zeros_like(a)
+    for it in range(K):
+        x = prob.sample_pair(a, b, it, key=5)
+        d_sum += x.diff
+        d_sq += x.diff ** 2
+        ya = prob.sample_pair(a, a, it, key=6).prop  # independent draws
+        yb = prob.sample_pair(b, b, it, key=7).prop
+        pa += ya
+        pa_sq += ya ** 2
+        pb += yb
+        pb_sq += yb ** 2
+    mean = lambda s: host(s) / K  # noqa: E731
+    var = lambda s, q: (host(q) / K - (host(s) / K) ** 2) / K  # noqa: E731 (variance of the mean)
+    md = mean(d_sum)
+    me = mean(pa) - mean(pb)
+    se = np.sqrt(var(d_sum, d_sq) + var(pa, pa_sq) + var(pb, pb_sq)) + 1e-300
+    z = np.abs(md - me) / se
+    assert np.mean(z > 3.0) < 0.02, np.mean(z > 3.0)
+    assert z.max() < 6.0, z.max()
+    # and the FD sample has far lower variance than the difference of props
+    assert np.median(var(d_sum, d_sq) / (var(pa, pa_sq) + var(pb, pb_sq))) < 0.2
+
+
+@pytest.mark.parametrize("opt,lr", [("meta", 0.01), ("adam", 0.01)])
+def test_quad_config1_optimisation_fits_target(api, opt, lr, record_property):
+    """configs[0]: 64x64, 32x32 RGB texture from seed 0 towards seed 1, 200
+    iterations, lr 0.01 — the texture error must drop."""
+    prob = api.QuadTextureProblem(64, 64, 32, LE, target_spp=1024)
+    run = api.QuadTextureRun(prob, optimizer=opt, lr=lr, seed=0)
+    e0 = run.texture_error()
+    losses = []
+    for _ in range(200):
+        run.step()
+        losses.append(run.loss_estimate())
+    e1 = run.texture_error()
+    record_property("texture_error", [e0, e1])
+    record_property("loss_first_last", [losses[0], float(np.mean(losses[-20:]))])
+    assert e1 < 0.6 * e0
+    assert np.mean(losses[-20:]) < 0.2 * losses[0]

@@ -187,3 +187,28 @@ def test_philox4x32_10_known_answers(oracle):
         0xd16cfe09, 0x94fdcceb, 0x5001e420, 0x24126ea1]
     u = oracle.philox_uniforms(12345, 4, 3, 7)
     assert u.shape == (12,) and (u >= 0).all() and (u < 1).all()
+
+
+# ------------------------------------------------ F1 slice (own renderer)
+def test_quad_oracle_properties(oracle):
+    """The F1 oracle (mgo_quad_*; the reference has no renderer): identical
+    textures give an exactly zero FD sample; the gradient sample is affine
+    in the texture (Lambertian direct lighting is linear in the albedo);
+    renders are deterministic in (key, stream)."""
+    W, H, R, Le = 32, 32, 8, (8.0, 7.0, 6.0)
+    rs = np.random.RandomState(0)
+    tex = rs.uniform(0, 1, 3 * R * R)
+    img = oracle.quad_render(W, H, R, tex, Le, 8, 11, 7)
+    assert np.array_equal(img, oracle.quad_render(W, H, R, tex, Le, 8, 11, 7))
+    assert img.max() > 0 and (img >= 0).all()
+    p0, d0, _ = oracle.quad_sample_pair(W, H, R, Le, img, tex, tex, 3, 0)
+    assert (d0 == 0).all()
+    # affine: prop(a + s*e) - prop(a) is linear in s
+    e = rs.uniform(-1, 1, tex.size)
+    p1, _, _ = oracle.quad_sample_pair(W, H, R, Le, img, tex + 0.1 * e, tex + 0.1 * e, 3, 0)
+    p2, _, _ = oracle.quad_sample_pair(W, H, R, Le, img, tex + 0.2 * e, tex + 0.2 * e, 3, 0)
+    np.testing.assert_allclose(p2 - p0, 2 * (p1 - p0), atol=1e-9)
+    # FD sample == linear response to the texture step on shared draws
+    _, d1, _ = oracle.quad_sample_pair(W, H, R, Le, img, tex + 0.1 * e, tex, 3, 0)
+    _, d2, _ = oracle.quad_sample_pair(W, H, R, Le, img, tex + 0.2 * e, tex, 3, 0)
+    np.testing.assert_allclose(d2, 2 * d1, atol=1e-9)
