@@ -396,6 +396,27 @@ def extras(args, ctx):
         "pairs_per_s": P * spp / (ms / 1e3)}
     del run
     torch.cuda.empty_cache()
+    # F1 slice, BASELINE configs[0]: 64x64 textured quad, 32x32 RGB texture,
+    # 1 FD + 2 proportional spp, 200 meta iterations (render+scatter, update)
+    for W, R, iters in ((64, 32, 200), (1024, 512, 50)):
+        prob = api.QuadTextureProblem(W, W, R, target_spp=64, dtype=torch.float32, ctx=ctx)
+        qrun = api.QuadTextureRun(prob, optimizer="meta", lr=0.01)
+        for _ in range(3):
+            qrun.step()
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(ctx.stream)
+        for _ in range(iters):
+            qrun.step()
+        b.record(ctx.stream)
+        torch.cuda.synchronize()
+        ms = a.elapsed_time(b) / iters
+        out[f"quad_texture_{W}px_{R}tex_f32"] = {
+            "iterations": iters, "ms_per_iteration": ms, "iterations_per_s": 1e3 / ms,
+            "path_samples_per_s": prob.draws_per_sample() / (ms / 1e3),
+            "texture_params": prob.dim()}
+        del prob, qrun
+    torch.cuda.empty_cache()
     # mini-render stand-in for configs[0] (P=4096, spp=2, 200 iterations)
     cfg = api.ExperimentConfig(problem="mini-render", pixel_count=4096, spp=2, iterations=200,
                                seed=0, problem_seed=1, lr=0.01, replicates=148)
