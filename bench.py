@@ -417,6 +417,24 @@ def extras(args, ctx):
             "texture_params": prob.dim()}
         del prob, qrun
     torch.cuda.empty_cache()
+    # F1 slice 2, BASELINE configs[2]: 256x256 helix of 64 spheres, depth-4
+    # path tracing with NEE, 5 principled-BSDF parameters, 1 FD + 2 prop spp
+    for dtn, dt in (("f32", torch.float32), ("f64", torch.float64)):
+        hprob = api.HelixProblem(256, 256, target_spp=16, dtype=dt, ctx=ctx)
+        hrun = api.HelixRun(hprob, optimizer="meta", lr=0.01)
+        for _ in range(2):
+            hrun.step()
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(ctx.stream)
+        for _ in range(10):
+            hrun.step()
+        b.record(ctx.stream)
+        torch.cuda.synchronize()
+        ms = a.elapsed_time(b) / 10
+        out[f"helix_256px_{dtn}"] = {"ms_per_iteration": ms, "iterations_per_s": 1e3 / ms,
+                                     "paths_per_s": hprob.draws_per_sample() / (ms / 1e3)}
+        del hprob, hrun
     # mini-render stand-in for configs[0] (P=4096, spp=2, 200 iterations)
     cfg = api.ExperimentConfig(problem="mini-render", pixel_count=4096, spp=2, iterations=200,
                                seed=0, problem_seed=1, lr=0.01, replicates=148)

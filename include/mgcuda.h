@@ -236,10 +236,12 @@ typedef struct mg_meta_update_args {
   double beta_delta;     /* decay of the decoupled diff EMA (harness.hpp:28) */
   int32_t first_step;    /* lazy init of Moment2 / MetaEstimator state (moment2.hpp:31, meta.hpp:92-96) */
   int32_t diff_norm;     /* mg_diff_norm_kind (harness.cpp:146-158) */
-  int32_t project;       /* 1: p = max(p, proj_lo) (problems.cpp:228 uses 0.0) */
+  int32_t project;       /* 1: p = max(p, proj_lo) (problems.cpp:228 uses 0.0);
+                            2: p = min(max(p, proj_lo), proj_hi) */
   int32_t ssn_from_host; /* 1: step_sq_norm = ssn_host instead of scalars->ssn */
   double proj_lo;
   double ssn_host;
+  double proj_hi;
 } mg_meta_update_args;
 
 /* Optional side inputs/outputs of the fused update.  Any may be NULL. */
@@ -383,6 +385,27 @@ int mg_quad_sample_pair(mg_ctx* ctx, int32_t dtype, int32_t W, int32_t H, int32_
                         const double* Le, const void* target_img, const void* now,
                         const void* prev, uint64_t key, uint32_t iteration, uint32_t stream,
                         void* accum, void* prop, void* diff, double* loss_out);
+
+/* F1 slice 2 (BASELINE.json configs[2]): helix of spheres on a diffuse ground
+ * plane, rectangular area light (y=4, x,z in [-1,1]) + constant environment,
+ * depth-4 path tracing with NEE, principled BSDF with 5 global parameters
+ * theta = (base r, g, b, metalness, roughness).
+ * spheres: device fp64 [nsph][4] (center, radius), nsph <= 256; Le/env/ground
+ * host fp64 RGB triples; theta/now/prev DEVICE dtype 5-vectors (read by the
+ * kernel: no host round trip per iteration); images [3][H*W] dtype. */
+int mg_helix_render(mg_ctx* ctx, int32_t dtype, int32_t W, int32_t H, int32_t nsph,
+                    const double* spheres, const double* Le, const double* env,
+                    const double* ground, const void* theta, int32_t spp, uint64_t key,
+                    void* img);
+/* One gradient sample pair for theta: prop/diff are dtype [5] (device),
+ * loss_out device double, accum device scratch of 10 int64 (zero, left zero).
+ * Paths A, B (proportional) and C (finite difference, A and C evaluated at
+ * theta_now and theta_prev on the same path). */
+int mg_helix_sample_pair(mg_ctx* ctx, int32_t dtype, int32_t W, int32_t H, int32_t nsph,
+                         const double* spheres, const double* Le, const double* env,
+                         const double* ground, const void* target_img, const void* now,
+                         const void* prev, uint64_t key, uint32_t iteration, void* accum,
+                         void* prop, void* diff, double* loss_out);
 
 /* ------------------------------- device-resident run_single (A13, A14) */
 /* Per-replicate record of one coordinate plus scalars (harness.hpp:73-90;

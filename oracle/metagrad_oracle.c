@@ -304,6 +304,7 @@ int mgo_meta_update(int64_t n, const mg_meta_update_args* a, const double* prop,
     if (delta_out) delta_out[i] = delta;
     double p = params_in[i] + delta;
     if (a->project) p = (p < a->proj_lo) ? a->proj_lo : p; /* std::max(p, lo) */
+    if (a->project == 2) p = (a->proj_hi < p) ? a->proj_hi : p;
     params_out[i] = p;
   }
   sc->ssn_used = ssn;
@@ -957,4 +958,329 @@ void mgo_quad_sample_pair(int W, int H, int R, const double Le[3], const double*
   *loss_est = loss;
   free(fp);
   free(fd);
+}
+
+
+/* =====================================================================
+ * F1 slice 2: helix of spheres (BASELINE.json configs[2]), own renderer.
+ * Multi-bounce path tracing (max 4 vertices) with next-event estimation to a
+ * rectangular area light, constant environment, diffuse ground plane and a
+ * principled-style BSDF (Lambert diffuse + GGX/Schlick/Smith specular) whose
+ * 5 global parameters (base RGB, metalness, roughness) are optimised.
+ * Directions are sampled independently of the parameters (cosine-weighted,
+ * Malley's method with Philox-addressed rejection candidates), so the
+ * parameter derivative is forward-mode along the path and the finite
+ * difference shares the complete path.  DESIGN.md §F1b.
+ * ===================================================================== */
+
+#define HX_MAXV 4
+#define HX_NP 5
+static const double HX_EPS = 1e-4;
+static const double HX_TANH = 0.35;
+static const double HX_LY = 4.0;     /* light plane y, x,z in [-1,1], facing -y */
+static const double HX_LA = 4.0;     /* light area */
+
+typedef struct hx_scene {
+  int W, H, nsph;
+  const double* sph; /* [nsph][4]: cx cy cz r */
+  double Le[3], env[3], ground[3];
+} hx_scene;
+
+static inline double hx_dot(const double a[3], const double b[3]) {
+  return (a[0] * b[0] + a[1] * b[1]) + a[2] * b[2];
+}
+
+/* closest hit: 0 none, 1 sphere (index *k), 2 ground, 3 light (camera only) */
+static int hx_intersect(const hx_scene* S, const double o[3], const double d[3], int want_light,
+                        double tmax, double* t_out, int* k_out) {
+  double best = tmax;
+  int kind = 0, kb = -1;
+  for (int k = 0; k < S->nsph; ++k) {
+    const double* c = S->sph + 4 * k;
+    const double oc[3] = {o[0] - c[0], o[1] - c[1], o[2] - c[2]};
+    const double b = hx_dot(oc, d);
+    const double cc = hx_dot(oc, oc) - c[3] * c[3];
+    const double disc = b * b - cc;
+    if (disc < 0.0) continue;
+    const double sq = sqrt(disc);
+    double t = -b - sq;
+    if (t < HX_EPS) t = -b + sq;
+    if (t < HX_EPS || t >= best) continue;
+    best = t;
+    kind = 1;
+    kb = k;
+  }
+  if (d[1] < 0.0) {
+    const double t = -o[1] / d[1];
+    if (t >= HX_EPS && t < best) {
+      best = t;
+      kind = 2;
+    }
+  }
+  if (want_light && d[1] > 0.0) {
+    const double t = (HX_LY - o[1]) / d[1];
+    if (t >= HX_EPS && t < best) {
+      const double x = o[0] + t * d[0], z = o[2] + t * d[2];
+      if (x >= -1.0 && x <= 1.0 && z >= -1.0 && z <= 1.0) {
+        best = t;
+        kind = 3;
+      }
+    }
+  }
+  *t_out = best;
+  *k_out = kb;
+  return kind;
+}
+
+/* principled BSDF value f[3] and df[3][5] (d/d base_r, base_g, base_b,
+ * metal, rough) for unit n, wi, wo with n.wi > 0, n.wo > 0 */
+static void hx_bsdf(const double th[HX_NP], const double n[3], const double wi[3],
+                    const double wo[3], double f[3], double df[3][HX_NP]) {
+  const double metal = th[3], rough = th[4];
+  const double alpha = 0.05 + 0.95 * (rough * rough);
+  const double a2 = alpha * alpha;
+  double h[3] = {wi[0] + wo[0], wi[1] + wo[1], wi[2] + wo[2]};
+  const double hl = sqrt(hx_dot(h, h));
+  h[0] /= hl; h[1] /= hl; h[2] /= hl;
+  const double nh = hx_dot(n, h), ni = hx_dot(n, wi), no = hx_dot(n, wo), ih = hx_dot(wi, h);
+  const double den = nh * nh * (a2 - 1.0) + 1.0;
+  const double D = a2 / (QS_PI * (den * den));
+  const double dD_da2 = (den - 2.0 * a2 * (nh * nh)) / (QS_PI * ((den * den) * den));
+  const double si = sqrt(a2 + (1.0 - a2) * (ni * ni));
+  const double so = sqrt(a2 + (1.0 - a2) * (no * no));
+  const double G1i = (2.0 * ni) / (ni + si), G1o = (2.0 * no) / (no + so);
+  const double dG1i = ((-2.0 * ni) / ((ni + si) * (ni + si))) * ((1.0 - ni * ni) / (2.0 * si));
+  const double dG1o = ((-2.0 * no) / ((no + so) * (no + so))) * ((1.0 - no * no) / (2.0 * so));
+  const double G = G1i * G1o;
+  const double dG_da2 = dG1i * G1o + G1i * dG1o;
+  const double q = 1.0 - ih;
+  const double q5 = ((q * q) * (q * q)) * q;
+  const double denom = 4.0 * ni * no;
+  const double DG = (D * G) / denom;
+  const double dDG_drough = (((dD_da2 * G + D * dG_da2) / denom) * (2.0 * alpha)) * (1.9 * rough);
+  for (int c = 0; c < 3; ++c) {
+    const double base = th[c];
+    const double F0 = 0.04 * (1.0 - metal) + base * metal;
+    const double F = F0 + (1.0 - F0) * q5;
+    f[c] = ((1.0 - metal) * base) / QS_PI + DG * F;
+    for (int k = 0; k < HX_NP; ++k) df[c][k] = 0.0;
+    df[c][c] = (1.0 - metal) / QS_PI + DG * (metal * (1.0 - q5));
+    df[c][3] = (-base) / QS_PI + DG * ((base - 0.04) * (1.0 - q5));
+    df[c][4] = dDG_drough * F;
+  }
+}
+
+/* Duff et al. orthonormal basis */
+static void hx_onb(const double n[3], double T[3], double B[3]) {
+  const double sign = copysign(1.0, n[2]);
+  const double a = -1.0 / (sign + n[2]);
+  const double b = n[0] * n[1] * a;
+  T[0] = 1.0 + sign * (n[0] * n[0]) * a; T[1] = sign * b; T[2] = -sign * n[0];
+  B[0] = b; B[1] = sign + (n[1] * n[1]) * a; B[2] = -n[1];
+}
+
+static void hx_rng(uint64_t key, uint32_t pix, uint32_t it, uint32_t path, uint32_t slot,
+                   double u[4]) {
+  const uint32_t ctr[4] = {pix, it, path, slot};
+  uint32_t o[4];
+  mgo_philox4x32_10(ctr, key, o);
+  for (int k = 0; k < 4; ++k) u[k] = (double)o[k] * 0x1.0p-32;
+}
+
+/* one path for up to two parameter sets; L[s][3], dL[s][3][5] */
+static void hx_path(const hx_scene* S, const double th[2][HX_NP], int nsets, int px, int py,
+                    uint64_t key, uint32_t it, uint32_t path, double L[2][3],
+                    double dL[2][3][HX_NP]) {
+  const uint32_t pix = (uint32_t)(py * S->W + px);
+  double u[4];
+  hx_rng(key, pix, it, path, 0u, u);
+  const double sx = ((px + u[0]) / S->W) * 2.0 - 1.0;
+  const double sy = 1.0 - ((py + u[1]) / S->H) * 2.0;
+  double o[3] = {0.0, 1.0, 6.0};
+  double d[3] = {sx * HX_TANH * ((double)S->W / (double)S->H), sy * HX_TANH, -1.0};
+  double dl = sqrt(hx_dot(d, d));
+  d[0] /= dl; d[1] /= dl; d[2] /= dl;
+  double beta[2][3], dbeta[2][3][HX_NP];
+  for (int s = 0; s < 2; ++s)
+    for (int c = 0; c < 3; ++c) {
+      beta[s][c] = 1.0; L[s][c] = 0.0;
+      for (int k = 0; k < HX_NP; ++k) { dbeta[s][c][k] = 0.0; dL[s][c][k] = 0.0; }
+    }
+  for (int v = 0; v < HX_MAXV; ++v) {
+    double t;
+    int k;
+    const int kind = hx_intersect(S, o, d, v == 0, 1e30, &t, &k);
+    if (kind == 0) { /* escaped: environment */
+      for (int s = 0; s < nsets; ++s)
+        for (int c = 0; c < 3; ++c) {
+          L[s][c] += beta[s][c] * S->env[c];
+          for (int j = 0; j < HX_NP; ++j) dL[s][c][j] += dbeta[s][c][j] * S->env[c];
+        }
+      return;
+    }
+    if (kind == 3) { /* camera ray sees the light */
+      for (int s = 0; s < nsets; ++s)
+        for (int c = 0; c < 3; ++c) L[s][c] += S->Le[c];
+      return;
+    }
+    const double x[3] = {o[0] + t * d[0], o[1] + t * d[1], o[2] + t * d[2]};
+    double n[3];
+    if (kind == 1) {
+      const double* c = S->sph + 4 * k;
+      n[0] = (x[0] - c[0]) / c[3]; n[1] = (x[1] - c[1]) / c[3]; n[2] = (x[2] - c[2]) / c[3];
+    } else {
+      n[0] = 0.0; n[1] = 1.0; n[2] = 0.0;
+    }
+    const double wo[3] = {-d[0], -d[1], -d[2]};
+    hx_rng(key, pix, it, path, (uint32_t)(v * 256 + 1), u);
+    /* next-event estimation */
+    const double ly[3] = {-1.0 + 2.0 * u[0], HX_LY, -1.0 + 2.0 * u[1]};
+    double w[3] = {ly[0] - x[0], ly[1] - x[1], ly[2] - x[2]};
+    const double d2 = hx_dot(w, w);
+    const double wl = sqrt(d2);
+    w[0] /= wl; w[1] /= wl; w[2] /= wl;
+    const double cx = hx_dot(n, w), cl = w[1];
+    if (cx > 0.0 && cl > 0.0 && hx_dot(n, wo) > 0.0) {
+      double ts;
+      int ks;
+      if (hx_intersect(S, x, w, 0, wl - HX_EPS, &ts, &ks) == 0) {
+        const double gl = ((cx * cl) / d2) * HX_LA;
+        for (int s = 0; s < nsets; ++s) {
+          double f[3], df[3][HX_NP];
+          if (kind == 1) {
+            hx_bsdf(th[s], n, w, wo, f, df);
+          } else {
+            for (int c = 0; c < 3; ++c) {
+              f[c] = S->ground[c] / QS_PI;
+              for (int j = 0; j < HX_NP; ++j) df[c][j] = 0.0;
+            }
+          }
+          for (int c = 0; c < 3; ++c) {
+            const double g = gl * S->Le[c];
+            L[s][c] += beta[s][c] * (f[c] * g);
+            for (int j = 0; j < HX_NP; ++j)
+              dL[s][c][j] += dbeta[s][c][j] * (f[c] * g) + beta[s][c] * (df[c][j] * g);
+          }
+        }
+      }
+    }
+    if (v == HX_MAXV - 1 || hx_dot(n, wo) <= 0.0) return;
+    /* cosine-weighted bounce: Malley, rejection in the unit disk */
+    double dx = 0.0, dy = 0.0;
+    int got = 0;
+    for (uint32_t j = 0; !got && j < 64; ++j) {
+      double c4[4];
+      if (j == 0) {
+        c4[0] = u[2]; c4[1] = u[3]; c4[2] = 2.0; c4[3] = 2.0;
+      } else {
+        hx_rng(key, pix, it, path, (uint32_t)(v * 256 + 1 + j), c4);
+      }
+      for (int m = 0; m < 4 && !got; m += 2) {
+        const double a = 2.0 * c4[m] - 1.0, b = 2.0 * c4[m + 1] - 1.0;
+        if (c4[m] <= 1.0 && a * a + b * b < 1.0) { dx = a; dy = b; got = 1; }
+      }
+    }
+    const double dz = sqrt(fmax(0.0, 1.0 - (dx * dx + dy * dy)));
+    double T[3], Bv[3];
+    hx_onb(n, T, Bv);
+    const double wi[3] = {(dx * T[0] + dy * Bv[0]) + dz * n[0], (dx * T[1] + dy * Bv[1]) + dz * n[1],
+                          (dx * T[2] + dy * Bv[2]) + dz * n[2]};
+    if (dz <= 0.0) return;
+    for (int s = 0; s < nsets; ++s) {
+      double f[3], df[3][HX_NP];
+      if (kind == 1) {
+        hx_bsdf(th[s], n, wi, wo, f, df);
+      } else {
+        for (int c = 0; c < 3; ++c) {
+          f[c] = S->ground[c] / QS_PI;
+          for (int j = 0; j < HX_NP; ++j) df[c][j] = 0.0;
+        }
+      }
+      for (int c = 0; c < 3; ++c) {
+        const double wgt = f[c] * QS_PI; /* f cos / (cos / pi) */
+        for (int j = 0; j < HX_NP; ++j)
+          dbeta[s][c][j] = dbeta[s][c][j] * wgt + beta[s][c] * (df[c][j] * QS_PI);
+        beta[s][c] = beta[s][c] * wgt;
+      }
+    }
+    o[0] = x[0]; o[1] = x[1]; o[2] = x[2];
+    d[0] = wi[0]; d[1] = wi[1]; d[2] = wi[2];
+  }
+}
+
+void mgo_helix_render(int W, int H, int nsph, const double* sph, const double Le[3],
+                      const double env[3], const double ground[3], const double th[HX_NP],
+                      int spp, uint64_t key, double* img) {
+  hx_scene S = {W, H, nsph, sph, {Le[0], Le[1], Le[2]}, {env[0], env[1], env[2]},
+                {ground[0], ground[1], ground[2]}};
+  double t2[2][HX_NP];
+  for (int k = 0; k < HX_NP; ++k) t2[0][k] = t2[1][k] = th[k];
+  for (int py = 0; py < H; ++py)
+    for (int px = 0; px < W; ++px) {
+      double acc[3] = {0.0, 0.0, 0.0};
+      for (int s = 0; s < spp; ++s) {
+        double L[2][3], dL[2][3][HX_NP];
+        hx_path(&S, (const double(*)[HX_NP])t2, 1, px, py, key, 0xffffffffu, (uint32_t)s, L, dL);
+        for (int c = 0; c < 3; ++c) acc[c] += L[0][c];
+      }
+      for (int c = 0; c < 3; ++c) img[(size_t)c * W * H + (size_t)py * W + px] = acc[c] / spp;
+    }
+}
+
+/* gradient sample pair for the 5 global parameters:
+ *   prop = sum_p,c r_A dI_B + r_B dI_A             (paths A, B at theta_t)
+ *   diff = sum_p,c [r_C dI_A + r_A dI_C](theta_t) - [same](theta_{t-1})
+ * fixed-point 2^-40 accumulation (order independent). */
+void mgo_helix_sample_pair(int W, int H, int nsph, const double* sph, const double Le[3],
+                           const double env[3], const double ground[3], const double* target_img,
+                           const double now[HX_NP], const double prev[HX_NP], uint64_t key,
+                           uint32_t it, double prop[HX_NP], double diff[HX_NP],
+                           double* loss_est) {
+  hx_scene S = {W, H, nsph, sph, {Le[0], Le[1], Le[2]}, {env[0], env[1], env[2]},
+                {ground[0], ground[1], ground[2]}};
+  double th[2][HX_NP];
+  for (int k = 0; k < HX_NP; ++k) { th[0][k] = now[k]; th[1][k] = prev[k]; }
+  int64_t fp[HX_NP] = {0}, fd[HX_NP] = {0};
+  double loss = 0.0;
+  for (int py = 0; py < H; ++py)
+    for (int px = 0; px < W; ++px) {
+      double LA[2][3], dA[2][3][HX_NP], LB[2][3], dB[2][3][HX_NP], LC[2][3], dC[2][3][HX_NP];
+      hx_path(&S, (const double(*)[HX_NP])th, 2, px, py, key, it, 0u, LA, dA);
+      hx_path(&S, (const double(*)[HX_NP])th, 1, px, py, key, it, 1u, LB, dB);
+      hx_path(&S, (const double(*)[HX_NP])th, 2, px, py, key, it, 2u, LC, dC);
+      const size_t pix = (size_t)py * W + px;
+      for (int c = 0; c < 3; ++c) {
+        const double Is = target_img[(size_t)c * W * H + pix];
+        const double rA = LA[0][c] - Is, rB = LB[0][c] - Is, rC = LC[0][c] - Is;
+        const double rA1 = LA[1][c] - Is, rC1 = LC[1][c] - Is;
+        loss += rA * rB;
+        for (int j = 0; j < HX_NP; ++j) {
+          fp[j] += qs_fix(rA * dB[0][c][j]);
+          fp[j] += qs_fix(rB * dA[0][c][j]);
+          fd[j] += qs_fix((rC * dA[0][c][j] + rA * dC[0][c][j]) -
+                          (rC1 * dA[1][c][j] + rA1 * dC[1][c][j]));
+        }
+      }
+    }
+  for (int j = 0; j < HX_NP; ++j) {
+    prop[j] = (double)fp[j] / QS_FIX;
+    diff[j] = (double)fd[j] / QS_FIX;
+  }
+  *loss_est = loss;
+}
+
+/* one path's radiance L[3] and dL/dtheta [3][5] (derivative checks) */
+void mgo_helix_path(int W, int H, int nsph, const double* sph, const double Le[3],
+                    const double env[3], const double ground[3], const double th[HX_NP], int px,
+                    int py, uint64_t key, uint32_t it, uint32_t path, double L[3],
+                    double dL[3 * HX_NP]) {
+  hx_scene S = {W, H, nsph, sph, {Le[0], Le[1], Le[2]}, {env[0], env[1], env[2]},
+                {ground[0], ground[1], ground[2]}};
+  double t2[2][HX_NP], L2[2][3], dL2[2][3][HX_NP];
+  for (int k = 0; k < HX_NP; ++k) t2[0][k] = t2[1][k] = th[k];
+  hx_path(&S, (const double(*)[HX_NP])t2, 1, px, py, key, it, path, L2, dL2);
+  for (int c = 0; c < 3; ++c) {
+    L[c] = L2[0][c];
+    for (int k = 0; k < HX_NP; ++k) dL[c * HX_NP + k] = dL2[0][c][k];
+  }
 }

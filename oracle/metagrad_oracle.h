@@ -122,6 +122,17 @@ void mgo_quad_sample_pair(int W, int H, int R, const double Le[3], const double*
                           const double* now, const double* prev, uint64_t key, uint32_t it,
                           uint32_t st, double* prop, double* diff, double* loss_est);
 
+/* F1 slice 2: helix of spheres, multi-bounce NEE, principled BSDF with 5
+ * global parameters (base RGB, metal, rough) (own renderer).
+ * sph: [nsph][4] (center, radius); images [3][H*W]. */
+void mgo_helix_render(int W, int H, int nsph, const double* sph, const double Le[3],
+                      const double env[3], const double ground[3], const double th[5], int spp,
+                      uint64_t key, double* img);
+void mgo_helix_sample_pair(int W, int H, int nsph, const double* sph, const double Le[3],
+                           const double env[3], const double ground[3], const double* target_img,
+                           const double now[5], const double prev[5], uint64_t key, uint32_t it,
+                           double prop[5], double diff[5], double* loss_est);
+
 int mgo_problem_dim(const mg_experiment_config* cfg);
 int mgo_run_single(const mg_experiment_config* cfg, int32_t replicate, mg_run_record* rec,
                    const mgo_full_record* out);

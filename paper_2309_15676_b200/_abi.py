@@ -65,7 +65,8 @@ class UpdateScalars(C.Structure):
 class MetaUpdateArgs(C.Structure):
     _fields_ = [("meta", MetaParams), ("prop_coef", C.c_double), ("beta_delta", C.c_double),
                 ("first_step", C.c_int32), ("diff_norm", C.c_int32), ("project", C.c_int32),
-                ("ssn_from_host", C.c_int32), ("proj_lo", C.c_double), ("ssn_host", C.c_double)]
+                ("ssn_from_host", C.c_int32), ("proj_lo", C.c_double), ("ssn_host", C.c_double),
+                ("proj_hi", C.c_double)]
 
 
 class MetaExtras(C.Structure):

@@ -35,6 +35,7 @@ from ._lib import DomainError, InvalidArgument, LogicError, MgError, check, load
 __all__ = ["Context", "Rng", "Moment2", "GradientSamplePair", "MetaEstimator", "Adam",
            "MiniRenderProblem", "ExpRateProblem", "MultNoiseQuadratic", "FusedMetaUpdate",
            "FusedAdamUpdate", "MiniRenderRun", "QuadTextureProblem", "QuadTextureRun",
+           "HelixProblem", "HelixRun", "helix_spheres",
            "ExperimentConfig", "RunRecord", "AggregateReport", "run_single",
            "run_experiment", "InvalidArgument", "LogicError", "DomainError", "mix64"]
 
@@ -441,12 +442,13 @@ class FusedMetaUpdate:
     def __init__(self, n: int, dtype=torch.float32, lr: float = 0.01, beta_f: float = 0.9,
                  beta_delta: float = 0.5, eps_step: float = 1e-8, eps_alpha: float = 1e-30,
                  clip: bool = True, project_lo: Optional[float] = None,
-                 diff_norm: str = "global", ctx=None, device="cuda"):
+                 diff_norm: str = "global", ctx=None, device="cuda",
+                 project_hi: Optional[float] = None):
         self.ctx = ctx or Context.default()
         self.n, self.dtype = n, dtype
         self.beta_f, self.beta_delta = beta_f, beta_delta
         self.meta = _abi.MetaParams(lr, eps_step, eps_alpha, int(clip))
-        self.project_lo = project_lo
+        self.project_lo, self.project_hi = project_lo, project_hi
         self.diff_norm = _abi.DIFF_NORMS[diff_norm]
         mk = lambda: torch.empty(n, dtype=dtype, device=device)  # noqa: E731
         self.m2_prop, self.m2_diff, self.mean, self.var, self.alpha_prev = (mk() for _ in range(5))
@@ -473,10 +475,11 @@ class FusedMetaUpdate:
         return _abi.MetaUpdateArgs(
             meta=self.meta, prop_coef=c_prop, beta_delta=self.beta_delta,
             first_step=int(self.t == 1), diff_norm=self.diff_norm,
-            project=int(self.project_lo is not None),
+            project=(2 if self.project_hi is not None else int(self.project_lo is not None)),
             ssn_from_host=int(ssn_host is not None),
             proj_lo=0.0 if self.project_lo is None else self.project_lo,
-            ssn_host=0.0 if ssn_host is None else ssn_host)
+            ssn_host=0.0 if ssn_host is None else ssn_host,
+            proj_hi=0.0 if self.project_hi is None else self.project_hi)
 
     def step(self, prop, diff, params_in, params_out, target=None, vprop=None, vdiff=None,
              params_prev=None, delta_out=None, ssn_host=None):
@@ -726,6 +729,84 @@ class QuadTextureRun:
 
     def texture_error(self) -> float:
         return float(torch.linalg.vector_norm((self.params - self.p.target_tex).double()))
+
+
+def helix_spheres(n: int = 64, radius: float = 0.1, turns: float = 4.0, helix_radius: float = 1.0,
+                  y0: float = 0.3, y1: float = 2.3) -> np.ndarray:
+    """configs[2] geometry: n spheres evenly along a helix (host libm
+    cos/sin, computed once and shared by the device and the oracle)."""
+    out = np.empty((n, 4))
+    for k in range(n):
+        phi = 2.0 * math.pi * turns * k / n
+        out[k] = (helix_radius * math.cos(phi), y0 + (y1 - y0) * k / max(n - 1, 1),
+                  helix_radius * math.sin(phi), radius)
+    return out
+
+
+class HelixProblem:
+    """BASELINE.json configs[2]: a W x H render of a procedural helix of 64
+    spheres (radius 0.1, 4 turns) on a diffuse ground plane under one area
+    light plus a constant environment, depth-4 path tracing with NEE; the
+    spheres' principled BSDF has 5 global parameters theta = (base r, g, b,
+    metalness, roughness), initialised U(0,1) from seed 0 against seeded
+    target values (seed 1).  Own renderer (oracle
+    mgo_helix_*)."""
+
+    def __init__(self, width: int = 256, height: int = 256, light=(10.0, 10.0, 10.0),
+                 env=(0.2, 0.2, 0.2), ground=(0.5, 0.5, 0.5), init_seed: int = 0,
+                 target_seed: int = 1, target_spp: int = 64, dtype=torch.float64, ctx=None):
+        self.ctx = ctx or Context.default()
+        self.W, self.H, self.dtype = width, height, dtype
+        self.spheres_host = helix_spheres()
+        self.spheres = torch.tensor(self.spheres_host, dtype=torch.float64, device="cuda")
+        self.Le = (C.c_double * 3)(*light)
+        self.env = (C.c_double * 3)(*env)
+        self.ground = (C.c_double * 3)(*ground)
+        L = load()
+        self.init = Rng([L.mg_mix64(init_seed)], ctx=self.ctx).uniform(5)[0].to(dtype)
+        tt = Rng([L.mg_mix64(target_seed)], ctx=self.ctx).uniform(5)[0]
+        tt[4] = 0.3 + 0.7 * tt[4]  # target roughness in [0.3, 1] (well-conditioned highlights)
+        self.target_theta = tt.to(dtype)
+        self.target_img = self.render(self.target_theta, target_spp, int(L.mg_mix64(target_seed)))
+        self.accum = torch.zeros(10, dtype=torch.int64, device="cuda")
+        self.loss_buf = torch.zeros(1, dtype=torch.float64, device="cuda")
+
+    def dim(self) -> int:
+        return 5
+
+    def draws_per_sample(self) -> int:
+        """Paths per iteration: 2 proportional + 1 finite-difference spp."""
+        return 3 * self.W * self.H
+
+    def initial_params(self):
+        return self.init.clone()
+
+    def render(self, theta, spp: int, key: int):
+        img = torch.empty(3 * self.W * self.H, dtype=theta.dtype, device="cuda")
+        check(load().mg_helix_render(self.ctx.h, _dtype_code(theta), self.W, self.H,
+                                     self.spheres.shape[0], _p(self.spheres), self.Le, self.env,
+                                     self.ground, _p(theta.contiguous()), spp, key, _p(img)))
+        return img
+
+    def sample_pair(self, now, prev, iteration: int, key: int):
+        prop, diff = torch.empty_like(now), torch.empty_like(now)
+        check(load().mg_helix_sample_pair(
+            self.ctx.h, _dtype_code(now), self.W, self.H, self.spheres.shape[0], _p(self.spheres),
+            self.Le, self.env, self.ground, _p(self.target_img), _p(now.contiguous()),
+            _p(prev.contiguous()), key, iteration, _p(self.accum), _p(prop), _p(diff),
+            _p(self.loss_buf)))
+        return GradientSamplePair(prop, diff)
+
+
+class HelixRun(QuadTextureRun):
+    """configs[2] optimisation loop (same structure as QuadTextureRun); the 5
+    parameters (colours, metalness, roughness) are projected to [0, 1]."""
+
+    def __init__(self, problem, optimizer: str = "meta", lr: float = 0.01, seed: int = 0,
+                 replicate: int = 0, **kw):
+        if optimizer == "meta":
+            kw.setdefault("project_hi", 1.0)
+        super().__init__(problem, optimizer, lr, seed, replicate, **kw)
 
 
 # ------------------------------------------------------------- harness

@@ -12,7 +12,7 @@
 namespace mg {
 
 struct MetaK {
-  double lr, eps_step, eps_alpha, prop_coef, beta_delta, proj_lo, ssn_host;
+  double lr, eps_step, eps_alpha, prop_coef, beta_delta, proj_lo, ssn_host, proj_hi;
   int clip, diff_norm, project, ssn_from_host;
 };
 
@@ -103,6 +103,7 @@ __device__ __forceinline__ void meta_elem(const MetaK& k, const StepScal& s, T p
   // params += delta; project (harness.cpp:186-187, problems.cpp:228)
   T p = pin + delta;
   if (k.project) p = std_max(p, T(k.proj_lo));
+  if (k.project == 2) p = std_min(p, T(k.proj_hi));
   pout = p;
   // fused reductions (problems.cpp:206,214,225; harness.cpp:116)
   const double d = double(p - pin);

@@ -233,6 +233,7 @@ extern "C" int mg_minirender_meta_iteration(mg_ctx* ctx, int32_t dtype, int64_t 
   k.meta.diff_norm = MG_DIFF_NORM_GLOBAL;
   k.meta.project = 1;  // problems.cpp:228: params = params.max(0.0)
   k.meta.proj_lo = 0.0;
+  k.meta.proj_hi = 0.0;
   k.meta.ssn_from_host = a->update.ssn_from_host;
   k.meta.ssn_host = a->update.ssn_host;
   k.spp = a->spp;

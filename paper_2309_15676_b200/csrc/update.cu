@@ -656,6 +656,7 @@ MetaK make_meta_k(const mg_meta_update_args* a) {
   k.diff_norm = a->diff_norm;
   k.project = a->project;
   k.proj_lo = a->proj_lo;
+  k.proj_hi = a->proj_hi;
   k.ssn_from_host = a->ssn_from_host;
   k.ssn_host = a->ssn_host;
   return k;

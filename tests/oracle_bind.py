@@ -240,6 +240,27 @@ class Oracle:
           key, it, stream, _ptr(prop), _ptr(diff), C.byref(loss))
         return prop, diff, loss.value
 
+    def helix_render(self, W, H, sph, Le, env, ground, theta, spp, key):
+        f = self.lib.mgo_helix_render
+        f.argtypes = [C.c_int, C.c_int, C.c_int] + [C.c_void_p] * 5 + [C.c_int, C.c_uint64,
+                                                                      C.c_void_p]
+        img = np.empty(3 * W * H)
+        sph = _f64(sph)
+        f(W, H, sph.shape[0], _ptr(sph), _ptr(_f64(Le)), _ptr(_f64(env)), _ptr(_f64(ground)),
+          _ptr(_f64(theta)), spp, key, _ptr(img))
+        return img
+
+    def helix_sample_pair(self, W, H, sph, Le, env, ground, target_img, now, prev, key, it):
+        f = self.lib.mgo_helix_sample_pair
+        f.argtypes = [C.c_int, C.c_int, C.c_int] + [C.c_void_p] * 7 + [C.c_uint64, C.c_uint32,
+                                                                      C.c_void_p, C.c_void_p, _dp]
+        prop, diff, loss = np.empty(5), np.empty(5), C.c_double()
+        sph = _f64(sph)
+        f(W, H, sph.shape[0], _ptr(sph), _ptr(_f64(Le)), _ptr(_f64(env)), _ptr(_f64(ground)),
+          _ptr(_f64(target_img)), _ptr(_f64(now)), _ptr(_f64(prev)), key, it, _ptr(prop),
+          _ptr(diff), C.byref(loss))
+        return prop, diff, loss.value
+
     # ----------------------------------------------------------- harness
     def run_single(self, cfg, replicate):
         dim = self.lib.mgo_problem_dim(C.byref(cfg))
