@@ -380,11 +380,14 @@ int mg_quad_render(mg_ctx* ctx, int32_t dtype, int32_t W, int32_t H, int32_t R, 
 /* One gradient sample pair: prop/diff [3][R*R] (1 FD + 2 proportional spp
  * per pixel), loss_out (device double) = unbiased estimate of
  * sum (I - I*)^2.  accum: device scratch of 6*R*R int64, zero on first use
- * (left zeroed).  Deterministic (fixed-point adjoint accumulation). */
+ * (left zeroed).  Deterministic (fixed-point adjoint accumulation).
+ * Tile sharding: only image rows [row0, row1) contribute (0, H for all);
+ * the partial pairs of disjoint tiles sum EXACTLY to the full pair. */
 int mg_quad_sample_pair(mg_ctx* ctx, int32_t dtype, int32_t W, int32_t H, int32_t R,
                         const double* Le, const void* target_img, const void* now,
                         const void* prev, uint64_t key, uint32_t iteration, uint32_t stream,
-                        void* accum, void* prop, void* diff, double* loss_out);
+                        int32_t row0, int32_t row1, void* accum, void* prop, void* diff,
+                        double* loss_out);
 
 /* F1 slice 2 (BASELINE.json configs[2]): helix of spheres on a diffuse ground
  * plane, rectangular area light (y=4, x,z in [-1,1]) + constant environment,
@@ -404,8 +407,8 @@ int mg_helix_render(mg_ctx* ctx, int32_t dtype, int32_t W, int32_t H, int32_t ns
 int mg_helix_sample_pair(mg_ctx* ctx, int32_t dtype, int32_t W, int32_t H, int32_t nsph,
                          const double* spheres, const double* Le, const double* env,
                          const double* ground, const void* target_img, const void* now,
-                         const void* prev, uint64_t key, uint32_t iteration, void* accum,
-                         void* prop, void* diff, double* loss_out);
+                         const void* prev, uint64_t key, uint32_t iteration, int32_t row0,
+                         int32_t row1, void* accum, void* prop, void* diff, double* loss_out);
 
 /* ------------------------------- device-resident run_single (A13, A14) */
 /* Per-replicate record of one coordinate plus scalars (harness.hpp:73-90;
@@ -442,6 +445,25 @@ typedef struct mg_run_series {
 int mg_run_replicates(mg_ctx* ctx, const mg_experiment_config* cfg, int32_t rep_begin,
                       int32_t rep_count, mg_run_record* records, const mg_run_series* series,
                       double* final_params);
+
+/* ---------------------------------- across-replicate aggregation (F2) */
+/* Per-iteration statistics across replicates (harness.cpp:274-302,
+ * stats.hpp:44-68), on the device.  series: device fp64 [S][R][T] (entry
+ * [s][r][i] read only while i < iterations_run[r]); iterations_run: device
+ * int32 [R].  Outputs (device): stats [S][5][T] = mean, variance (n-1),
+ * median, q25, q75 of the active replicates — sums in replicate order, so
+ * bit-identical to the reference; NaN sorts last — and optionally active[T]
+ * (number of replicates with iterations_run > i).  R <= 8192. */
+int mg_aggregate_series(mg_ctx* ctx, int32_t S, int32_t R, int32_t T, const double* series,
+                        const int32_t* iterations_run, double* stats, int32_t* active);
+
+/* run_experiment's replicate run + aggregation without the series leaving
+ * the device: records[rep_count] as mg_run_replicates; stats: HOST fp64
+ * [11][5][iterations] in mg_run_series field order; active: HOST int32
+ * [iterations] or NULL. */
+int mg_run_experiment_stats(mg_ctx* ctx, const mg_experiment_config* cfg, int32_t rep_begin,
+                            int32_t rep_count, mg_run_record* records, double* stats,
+                            int32_t* active);
 
 #ifdef __cplusplus
 }  /* extern "C" */

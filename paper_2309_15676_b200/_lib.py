@@ -100,14 +100,18 @@ def load():
                                      C.c_int32, C.c_uint64, C.c_uint32, _vp, _vp]),
         "mg_quad_sample_pair": (C.c_int, [_vp, C.c_int32, C.c_int32, C.c_int32, C.c_int32, _vp,
                                           _vp, _vp, _vp, C.c_uint64, C.c_uint32, C.c_uint32,
-                                          _vp, _vp, _vp, _vp]),
+                                          C.c_int32, C.c_int32, _vp, _vp, _vp, _vp]),
         "mg_helix_render": (C.c_int, [_vp, C.c_int32, C.c_int32, C.c_int32, C.c_int32, _vp, _vp,
                                       _vp, _vp, _vp, C.c_int32, C.c_uint64, _vp]),
         "mg_helix_sample_pair": (C.c_int, [_vp, C.c_int32, C.c_int32, C.c_int32, C.c_int32, _vp,
                                            _vp, _vp, _vp, _vp, _vp, _vp, C.c_uint64, C.c_uint32,
-                                           _vp, _vp, _vp, _vp]),
+                                           C.c_int32, C.c_int32, _vp, _vp, _vp, _vp]),
         "mg_run_replicates": (C.c_int, [_vp, P(_abi.ExperimentConfigC), C.c_int32, C.c_int32,
                                         _vp, P(_abi.RunSeriesC), _vp]),
+        "mg_aggregate_series": (C.c_int, [_vp, C.c_int32, C.c_int32, C.c_int32, _vp, _vp, _vp,
+                                          _vp]),
+        "mg_run_experiment_stats": (C.c_int, [_vp, P(_abi.ExperimentConfigC), C.c_int32,
+                                              C.c_int32, _vp, _vp, _vp]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)

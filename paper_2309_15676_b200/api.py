@@ -678,13 +678,16 @@ class QuadTextureProblem:
                                     self.Le, spp, key, stream, _p(tex.contiguous()), _p(img)))
         return img
 
-    def sample_pair(self, now, prev, iteration: int, key: int, stream: int = 0):
+    def sample_pair(self, now, prev, iteration: int, key: int, stream: int = 0, rows=None):
         """One gradient sample pair (prop, diff) for the L2 image loss; the
-        returned pair's step_sq_norm is left to the fused update (device)."""
+        returned pair's step_sq_norm is left to the fused update (device).
+        rows=(r0, r1) restricts it to an image tile (partials of disjoint
+        tiles sum exactly to the full pair)."""
+        r0, r1 = rows if rows is not None else (0, self.H)
         prop, diff = torch.empty_like(now), torch.empty_like(now)
         check(load().mg_quad_sample_pair(self.ctx.h, _dtype_code(now), self.W, self.H, self.R,
                                          self.Le, _p(self.target_img), _p(now.contiguous()),
-                                         _p(prev.contiguous()), key, iteration, stream,
+                                         _p(prev.contiguous()), key, iteration, stream, r0, r1,
                                          _p(self.accum), _p(prop), _p(diff), _p(self.loss_buf)))
         return GradientSamplePair(prop, diff)
 
@@ -788,12 +791,13 @@ class HelixProblem:
                                      self.ground, _p(theta.contiguous()), spp, key, _p(img)))
         return img
 
-    def sample_pair(self, now, prev, iteration: int, key: int):
+    def sample_pair(self, now, prev, iteration: int, key: int, rows=None):
+        r0, r1 = rows if rows is not None else (0, self.H)
         prop, diff = torch.empty_like(now), torch.empty_like(now)
         check(load().mg_helix_sample_pair(
             self.ctx.h, _dtype_code(now), self.W, self.H, self.spheres.shape[0], _p(self.spheres),
             self.Le, self.env, self.ground, _p(self.target_img), _p(now.contiguous()),
-            _p(prev.contiguous()), key, iteration, _p(self.accum), _p(prop), _p(diff),
+            _p(prev.contiguous()), key, iteration, r0, r1, _p(self.accum), _p(prop), _p(diff),
             _p(self.loss_buf)))
         return GradientSamplePair(prop, diff)
 
@@ -1040,13 +1044,59 @@ def aggregate(cfg: ExperimentConfig, records: List[RunRecord]) -> AggregateRepor
     return AggregateReport(cfg, names, stats, active, div, records)
 
 
+def aggregate_series_device(series, iterations_run, ctx=None):
+    """F2: across-replicate statistics on the device (harness.cpp:274-302).
+    series: CUDA fp64 [S][R][T]; iterations_run: CUDA int32 [R].  Returns
+    (stats [S][5][T] = mean, variance, median, q25, q75; active [T]),
+    bit-identical to `aggregate` (sequential sums in replicate order)."""
+    import torch
+    if series.dim() != 3 or series.dtype != torch.float64 or not series.is_cuda:
+        raise InvalidArgument(_abi.MG_EINVAL, "series must be a CUDA fp64 [S][R][T] tensor")
+    ctx = ctx or Context.default()
+    S, R, T = series.shape
+    runs = iterations_run.to(device=series.device, dtype=torch.int32).contiguous()
+    if runs.numel() != R:
+        raise InvalidArgument(_abi.MG_EINVAL, "iterations_run must hold one entry per replicate")
+    stats = torch.empty((S, 5, T), dtype=torch.float64, device=series.device)
+    active = torch.empty(T, dtype=torch.int32, device=series.device)
+    check(load().mg_aggregate_series(ctx.h, S, R, T, _p(series.contiguous()), _p(runs), _p(stats),
+                                     _p(active)))
+    return stats, active
+
+
+def _run_experiment_device_stats(cfg: ExperimentConfig, rep_begin: int, rep_count: int,
+                                 ctx=None) -> AggregateReport:
+    ctx = ctx or Context.default()
+    c = cfg.to_c()
+    it = cfg.iterations
+    recs = (_abi.RunRecordC * rep_count)()
+    stats = np.empty((len(_abi.SERIES_NAMES), 5, it))
+    active = np.empty(it, dtype=np.int32)
+    check(load().mg_run_experiment_stats(ctx.h, C.byref(c), rep_begin, rep_count,
+                                         C.cast(recs, C.c_void_p),
+                                         stats.ctypes.data_as(C.c_void_p),
+                                         active.ctypes.data_as(C.c_void_p)))
+    records = [RunRecord(STATUS[r.status], r.iterations_run, r.draws_used, r.evals_used, {}, None)
+               for r in recs]
+    names = [n for n in SERIES_ORDER if cfg.optimizer == "meta" or n != "alpha"]
+    st = {n: SeriesStats(*(stats[_abi.SERIES_NAMES.index(n), q].copy() for q in range(5)))
+          for n in names}
+    div = sum(1 for r in records if r.status == "diverged")
+    return AggregateReport(cfg, names, st, active.astype(np.int64), div, records)
+
+
 def run_experiment(cfg: ExperimentConfig, ctx=None, rep_begin: int = 0,
-                   rep_count: Optional[int] = None) -> AggregateReport:
+                   rep_count: Optional[int] = None,
+                   device_aggregate: bool = False) -> AggregateReport:
     """harness.cpp:249-302: all replicates as one device launch (the thread
-    pool becomes the grid); reduction in replicate order on the host."""
+    pool becomes the grid); reduction in replicate order on the host, or on
+    the device with device_aggregate=True (F2: only the statistics leave the
+    GPU; records then carry no per-iteration series)."""
     cfg.validate()
     if cfg.coord >= cfg.problem_dim():
         raise InvalidArgument(_abi.MG_EINVAL, "coord exceeds problem dimension")
     n = cfg.replicates if rep_count is None else rep_count
+    if device_aggregate and not _scaled_eligible(cfg):
+        return _run_experiment_device_stats(cfg, rep_begin, n, ctx)
     recs = _run_device(cfg, rep_begin, n, ctx)
     return aggregate(cfg, recs)

@@ -35,6 +35,7 @@ constexpr double kFixH = 1099511627776.0;  // 2^40
 
 struct HelixK {
   int W, H, nsph;
+  int row0, row1;  // image rows [row0, row1) of this tile (sample pairs)
   double Le[3], env[3], ground[3];
   uint64_t key;
   uint32_t iteration;
@@ -364,7 +365,7 @@ __global__ void __launch_bounds__(kHThreads)
   const int npix = q.W * q.H;
   long long fp[kNP] = {0, 0, 0, 0, 0}, fd[kNP] = {0, 0, 0, 0, 0};
   double loss = 0.0;
-  for (int pix = blockIdx.x * kHThreads + threadIdx.x; pix < npix;
+  for (int pix = q.row0 * q.W + blockIdx.x * kHThreads + threadIdx.x; pix < q.row1 * q.W;
        pix += gridDim.x * kHThreads) {
     const int px = pix % q.W, py = pix / q.W;
     T LA[2][3], dA[2][3][kNP], LB[1][3], dB[1][3][kNP], LC[2][3], dC[2][3][kNP];
@@ -427,6 +428,8 @@ HelixK make_helix(int W, int H, int nsph, const double* Le, const double* env, c
   q.W = W;
   q.H = H;
   q.nsph = nsph;
+  q.row0 = 0;
+  q.row1 = H;
   for (int c = 0; c < 3; ++c) {
     q.Le[c] = Le[c];
     q.env[c] = env[c];
@@ -469,15 +472,18 @@ int mg_helix_render(mg_ctx* ctx, int32_t dtype, int32_t W, int32_t H, int32_t ns
 int mg_helix_sample_pair(mg_ctx* ctx, int32_t dtype, int32_t W, int32_t H, int32_t nsph,
                          const double* spheres, const double* Le, const double* env,
                          const double* ground, const void* target_img, const void* now,
-                         const void* prev, uint64_t key, uint32_t iteration, void* accum,
-                         void* prop, void* diff, double* loss_out) {
+                         const void* prev, uint64_t key, uint32_t iteration, int32_t row0,
+                         int32_t row1, void* accum, void* prop, void* diff, double* loss_out) {
   if (!ctx || !spheres || !Le || !env || !ground || !target_img || !now || !prev || !accum ||
       !prop || !diff || !loss_out)
     return fail(MG_EINVAL, "mg_helix_sample_pair: null argument");
   if (W < 1 || H < 1 || nsph < 0 || nsph > kMaxSph)
     return fail(MG_EINVAL, "mg_helix_sample_pair: bad sizes (nsph <= 256)");
-  const HelixK q = make_helix(W, H, nsph, Le, env, ground, key, iteration);
-  const int grid = grid_for(ctx, int64_t(W) * H, kHThreads, 8);
+  if (row0 < 0 || row1 > H || row0 > row1) return fail(MG_EINVAL, "mg_helix_sample_pair: bad rows");
+  HelixK q = make_helix(W, H, nsph, Le, env, ground, key, iteration);
+  q.row0 = row0;
+  q.row1 = row1;
+  const int grid = grid_for(ctx, int64_t(W) * (row1 - row0) + 1, kHThreads, 8);
   if (dtype == MG_F64) {
     helix_pair_kernel<double><<<grid, kHThreads, 0, ctx->stream>>>(
         q, spheres, (const double*)now, (const double*)prev, (const double*)target_img,

@@ -32,6 +32,11 @@ int cuda_fail(cudaError_t e, const char* what);
     if (mg_e_ != cudaSuccess) return ::mg::cuda_fail(mg_e_, "kernel launch"); \
   } while (0)
 
+// across-replicate aggregation (aggregate.cu); runs[r * runs_stride] are the
+// replicates' iterations_run
+int launch_aggregate(mg_ctx* ctx, int S, int R, int T, const double* series, const int32_t* runs,
+                     int runs_stride, double* stats, int32_t* active);
+
 // ----------------------------------------------------------------- context
 // Reduction epilogue workspace: per-block partials + arrival counter.
 constexpr int kMaxReduceBlocks = 148 * 16;

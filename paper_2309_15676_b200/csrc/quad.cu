@@ -28,6 +28,7 @@ constexpr double kPi = 3.14159265358979323846;
 
 struct QuadK {
   int W, H, R;
+  int row0, row1;  // image rows [row0, row1) of this tile
   double Le[3];
   uint64_t key;
   uint32_t iteration, stream;
@@ -98,13 +99,15 @@ __global__ void __launch_bounds__(kQThreads)
   extern __shared__ unsigned long long acc_s[];
   const int npix = q.W * q.H;
   const int T_ = q.R * q.R;
+  const int pix0 = q.row0 * q.W, pix1 = q.row1 * q.W;
   unsigned long long* acc = SHARED ? acc_s : acc_g;
   if (SHARED) {
     for (int k = threadIdx.x; k < 6 * T_; k += kQThreads) acc_s[k] = 0ull;
     __syncthreads();
   }
   double loss = 0.0;
-  for (int pix = blockIdx.x * kQThreads + threadIdx.x; pix < npix; pix += gridDim.x * kQThreads) {
+  for (int pix = pix0 + blockIdx.x * kQThreads + threadIdx.x; pix < pix1;
+       pix += gridDim.x * kQThreads) {
     const int px = pix % q.W, py = pix / q.W;
     double uA[4], uB[4], uC[4], KA[3], KB[3], KC[3];
     quad_uniforms(q.key, uint32_t(pix), q.iteration, 0u, q.stream, uA);
@@ -158,6 +161,8 @@ QuadK make_quad(int W, int H, int R, const double* Le, uint64_t key, uint32_t it
   q.W = W;
   q.H = H;
   q.R = R;
+  q.row0 = 0;
+  q.row1 = H;
   for (int c = 0; c < 3; ++c) q.Le[c] = Le[c];
   q.key = key;
   q.iteration = it;
@@ -193,15 +198,19 @@ int mg_quad_render(mg_ctx* ctx, int32_t dtype, int32_t W, int32_t H, int32_t R, 
 int mg_quad_sample_pair(mg_ctx* ctx, int32_t dtype, int32_t W, int32_t H, int32_t R,
                         const double* Le, const void* target_img, const void* now,
                         const void* prev, uint64_t key, uint32_t iteration, uint32_t stream,
-                        void* accum, void* prop, void* diff, double* loss_out) {
+                        int32_t row0, int32_t row1, void* accum, void* prop, void* diff,
+                        double* loss_out) {
   if (!ctx || !Le || !target_img || !now || !prev || !accum || !prop || !diff || !loss_out)
     return fail(MG_EINVAL, "mg_quad_sample_pair: null argument");
   if (W < 1 || H < 1 || R < 1) return fail(MG_EINVAL, "mg_quad_sample_pair: bad sizes");
-  const QuadK q = make_quad(W, H, R, Le, key, iteration, stream);
+  if (row0 < 0 || row1 > H || row0 > row1) return fail(MG_EINVAL, "mg_quad_sample_pair: bad rows");
+  QuadK q = make_quad(W, H, R, Le, key, iteration, stream);
+  q.row0 = row0;
+  q.row1 = row1;
   const int T_ = R * R;
   const size_t smem = sizeof(unsigned long long) * 6 * size_t(T_);
   const bool shared = smem <= 96 * 1024;
-  const int grid = grid_for(ctx, int64_t(W) * H, kQThreads, shared ? 2 : 8);
+  const int grid = grid_for(ctx, int64_t(W) * (row1 - row0) + 1, kQThreads, shared ? 2 : 8);
   auto go = [&](auto tag) {
     using T = decltype(tag);
     if (shared) {

@@ -401,8 +401,12 @@ void schedule_table(const mg_experiment_config* c, const std::vector<double>& fr
 }
 
 template <class T>
+// stats/active non-null: every series is kept on the device and reduced
+// there (aggregate.cu); only the [kNumSeries][5][iterations] statistics and
+// active counts come back (`series` is ignored).
 int run_replicates(mg_ctx* ctx, const mg_experiment_config* cfg, int rep_begin, int R,
-                   mg_run_record* records, const mg_run_series* series, double* final_params) {
+                   mg_run_record* records, const mg_run_series* series, double* final_params,
+                   double* stats = nullptr, int32_t* active = nullptr) {
   const int d = problem_dim(cfg);
   const int iters = cfg->iterations;
   std::vector<double> truth(d, 0.0), init(d, 0.0);
@@ -506,8 +510,21 @@ int run_replicates(mg_ctx* ctx, const mg_experiment_config* cfg, int rep_begin, 
     return fail(MG_ENOMEM, "run: allocation failed");
   }
   const size_t ser_bytes = sizeof(double) * size_t(R) * iters;
-  void* const* host_series = series ? reinterpret_cast<void* const*>(series) : nullptr;
-  for (int i = 0; i < kNumSeries; ++i) {
+  void* const* host_series = series && !stats ? reinterpret_cast<void* const*>(series) : nullptr;
+  double* dstats = nullptr;
+  int32_t* dactive = nullptr;
+  if (stats) {
+    double* base = (double*)dalloc(ser_bytes * kNumSeries);
+    dstats = (double*)dalloc(sizeof(double) * 5 * kNumSeries * size_t(iters));
+    dactive = (int32_t*)dalloc(sizeof(int32_t) * size_t(iters));
+    if (!base || !dstats || !dactive) {
+      cleanup();
+      return fail(MG_ENOMEM, "run: allocation failed");
+    }
+    cudaMemsetAsync(base, 0xff, ser_bytes * kNumSeries, s);
+    for (int i = 0; i < kNumSeries; ++i) k.series[i] = base + size_t(i) * R * iters;
+  }
+  for (int i = 0; i < kNumSeries && !stats; ++i) {
     k.series[i] = nullptr;
     if (host_series && host_series[i]) {
       k.series[i] = (double*)dalloc(ser_bytes);
@@ -533,8 +550,22 @@ int run_replicates(mg_ctx* ctx, const mg_experiment_config* cfg, int rep_begin, 
     cleanup();
     return cuda_fail(e, "run_kernel");
   }
+  if (stats) {
+    static_assert(sizeof(mg_run_record) % sizeof(int32_t) == 0, "record stride");
+    const int st = launch_aggregate(ctx, kNumSeries, R, iters, k.series[0],
+                                    &k.recs[0].iterations_run,
+                                    int(sizeof(mg_run_record) / sizeof(int32_t)), dstats, dactive);
+    if (st) {
+      cleanup();
+      return st;
+    }
+    cudaMemcpyAsync(stats, dstats, sizeof(double) * 5 * kNumSeries * size_t(iters),
+                    cudaMemcpyDeviceToHost, s);
+    if (active)
+      cudaMemcpyAsync(active, dactive, sizeof(int32_t) * size_t(iters), cudaMemcpyDeviceToHost, s);
+  }
   cudaMemcpyAsync(records, k.recs, sizeof(mg_run_record) * R, cudaMemcpyDeviceToHost, s);
-  for (int i = 0; i < kNumSeries; ++i)
+  for (int i = 0; i < kNumSeries && host_series; ++i)
     if (k.series[i]) cudaMemcpyAsync(host_series[i], k.series[i], ser_bytes, cudaMemcpyDeviceToHost, s);
   if (final_params)
     cudaMemcpyAsync(final_params, k.final_params, sizeof(double) * size_t(R) * d,
@@ -549,6 +580,24 @@ int run_replicates(mg_ctx* ctx, const mg_experiment_config* cfg, int rep_begin, 
 }  // namespace mg
 
 using namespace mg;
+
+extern "C" int mg_run_experiment_stats(mg_ctx* ctx, const mg_experiment_config* cfg,
+                                       int32_t rep_begin, int32_t rep_count,
+                                       mg_run_record* records, double* stats, int32_t* active) {
+  if (!ctx || !cfg || !records || !stats)
+    return fail(MG_EINVAL, "mg_run_experiment_stats: null argument");
+  int st = mg_config_validate(cfg);
+  if (st) return st;
+  if (rep_count < 1 || rep_begin < 0)
+    return fail(MG_EINVAL, "mg_run_experiment_stats: bad replicate range");
+  if (cfg->rng != MG_RNG_MT64)
+    return fail(MG_EUNSUPPORTED, "mg_run_experiment_stats: only the bit-exact mt64 streams are supported");
+  if (cfg->dtype == MG_F64)
+    return run_replicates<double>(ctx, cfg, rep_begin, rep_count, records, nullptr, nullptr, stats,
+                                  active);
+  return run_replicates<float>(ctx, cfg, rep_begin, rep_count, records, nullptr, nullptr, stats,
+                               active);
+}
 
 extern "C" int mg_run_replicates(mg_ctx* ctx, const mg_experiment_config* cfg, int32_t rep_begin,
                                  int32_t rep_count, mg_run_record* records,

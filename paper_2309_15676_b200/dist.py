@@ -40,6 +40,15 @@ def replicate_range(replicates: int, rank: int, world: int) -> Tuple[int, int]:
     return replicates * rank // world, replicates * (rank + 1) // world
 
 
+def tile_rows(height: int, rank: int, world: int) -> Tuple[int, int]:
+    """Image rows [r0, r1) this rank renders for a shared-parameter problem
+    (the `rows=` argument of QuadTextureProblem/HelixProblem.sample_pair).
+    The renderers accumulate adjoints in 2^-40 fixed point, so the partial
+    pairs of disjoint tiles sum EXACTLY to the unsharded pair: the summed
+    gradient (and hence the whole run) is independent of the world size."""
+    return replicate_range(height, rank, world)
+
+
 class ShardedStep:
     """One iteration of a parameter-sharded run: local fused update, then one
     SUM all-reduce of the 4 reducible scalars (in place, on the scalars'

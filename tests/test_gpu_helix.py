@@ -89,3 +89,17 @@ def test_helix_optimisation_fits_target(api, record_property):
     record_property("theta_error", [e0, e1])
     print("helix theta error", e0, "->", e1, host(run.params), host(prob.target_theta))
     assert e1 < 0.7 * e0, (e0, e1, host(run.params), host(prob.target_theta))
+
+
+def test_helix_tile_sharded_gradients_sum_exactly(api):
+    prob = api.HelixProblem(40, 40, target_spp=4)
+    a = torch.tensor([0.6, 0.35, 0.2, 0.3, 0.45], device="cuda", dtype=torch.float64)
+    b = a - 0.01
+    full = prob.sample_pair(a, b, 2, key=9)
+    full = (full.prop.clone(), full.diff.clone())
+    sp, sd = torch.zeros_like(a), torch.zeros_like(a)
+    for r0, r1 in ((0, 13), (13, 29), (29, 40)):
+        part = prob.sample_pair(a, b, 2, key=9, rows=(r0, r1))
+        sp += part.prop
+        sd += part.diff
+    assert torch.equal(sp, full[0]) and torch.equal(sd, full[1])

@@ -127,3 +127,27 @@ def test_quad_config1_optimisation_fits_target(api, opt, lr, record_property):
     record_property("loss_first_last", [losses[0], float(np.mean(losses[-20:]))])
     assert e1 < 0.6 * e0
     assert np.mean(losses[-20:]) < 0.2 * losses[0]
+
+
+@pytest.mark.parametrize("tiles", [2, 3])
+def test_tile_sharded_gradients_sum_exactly(api, tiles):
+    """Image tiles shard across GPUs: the partial gradient
+    pairs of disjoint row tiles — computed as separate launches here, one
+    per emulated rank — sum EXACTLY (fixed-point accumulation) to the
+    unsharded pair, so the all-reduce/reduce-scatter of the partials gives
+    a result independent of the rank count."""
+    W, H, R = 64, 64, 32
+    prob = api.QuadTextureProblem(W, H, R, LE, target_spp=16)
+    rs = np.random.RandomState(1)
+    now = torch.tensor(rs.uniform(0, 1, 3 * R * R), device="cuda")
+    prev = now - 0.01
+    full = prob.sample_pair(now, prev, 4, key=3)
+    full = (full.prop.clone(), full.diff.clone())
+    from paper_2309_15676_b200.dist import tile_rows
+    sp = torch.zeros_like(now)
+    sd = torch.zeros_like(now)
+    for r in range(tiles):
+        part = prob.sample_pair(now, prev, 4, key=3, rows=tile_rows(H, r, tiles))
+        sp += part.prop
+        sd += part.diff
+    assert torch.equal(sp, full[0]) and torch.equal(sd, full[1])

@@ -81,14 +81,15 @@ def test_csv_bytes_match_reference_oracle(tmp_path):
     dict(problem="mult-noise", dim=3, iterations=30, replicates=9, seed=8, optimizer="adam",
          lr=0.05),
 ])
-def test_device_run_csv_is_byte_identical_to_reference(tmp_path, kw):
+@pytest.mark.parametrize("device_aggregate", [False, True])
+def test_device_run_csv_is_byte_identical_to_reference(tmp_path, kw, device_aggregate):
     """End to end: the device runner's report, written in the reference's
     format, equals the reference harness's CSV byte for byte (problems whose
     arithmetic has no transcendental functions are bit-exact on the device)."""
     from paper_2309_15676_b200 import api
     ref_csv = str(tmp_path / "ref.csv")
     ref_csv_golden(dict(kw, threads=1), ref_csv)
-    rep = api.run_experiment(api.ExperimentConfig(**kw))
+    rep = api.run_experiment(api.ExperimentConfig(**kw), device_aggregate=device_aggregate)
     ours = str(tmp_path / "ours.csv")
     report.write_aggregate_csv(rep, ours)
     assert open(ours, "rb").read() == open(ref_csv, "rb").read()
