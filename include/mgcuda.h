@@ -123,6 +123,12 @@ int mg_free(mg_ctx* ctx, void* p);
 int mg_copy_to_device(mg_ctx* ctx, void* dst, const void* src, size_t bytes);
 int mg_copy_to_host(mg_ctx* ctx, void* dst, const void* src, size_t bytes);
 int mg_copy_device(mg_ctx* ctx, void* dst, const void* src, size_t bytes);
+/* Page-locked host staging memory (cudaMallocHost) and a stream-ordered
+ * copy in any direction (cudaMemcpyDefault; asynchronous w.r.t. the host
+ * when the host side is page-locked — pair with mg_ctx_synchronize). */
+int mg_host_malloc(size_t bytes, void** out);
+int mg_host_free(void* p);
+int mg_copy_async(mg_ctx* ctx, void* dst, const void* src, size_t bytes);
 int mg_fill(mg_ctx* ctx, int32_t dtype, int64_t n, void* dst, double value);
 
 /* -------------------------------------------------- RNG streams (row A1) */
@@ -189,6 +195,18 @@ typedef struct mg_meta_params {
 int mg_meta_step(mg_ctx* ctx, int32_t dtype, int64_t n, const mg_meta_params* p,
                  int32_t first_call, void* mean, void* var, void* alpha_prev, const void* prop,
                  const void* diff, const void* var_prop, const void* var_diff, void* delta);
+
+/* compute_alpha (meta.hpp:38-47), the standalone clipped weight:
+ * out = min(vp / (((vp + var_meta) + var_diff) + eps_alpha), 1 / (2 - alpha_prev)).
+ * A negative variance input -> MG_ELOGIC (synchronises the stream). */
+int mg_compute_alpha(mg_ctx* ctx, int32_t dtype, int64_t n, const void* var_prop,
+                     const void* var_meta, const void* var_diff, const void* alpha_prev,
+                     double eps_alpha, void* out);
+
+/* out = x * s (op 0: rescale_diff_variance, meta.hpp:51-53) or
+ * out = x / s (op 1: Adam::m_hat / v_hat bias correction, adam.hpp:43-44). */
+int mg_scalar_op(mg_ctx* ctx, int32_t dtype, int64_t n, const void* x, double s, int32_t op,
+                 void* out);
 
 /* Adam::step (adam.hpp:23-37).  b1pow/b2pow/t live on the host like the
  * reference's members (adam.hpp:47-48) and are advanced by this call. */

@@ -108,6 +108,12 @@ def load():
                                            C.c_int32, C.c_int32, _vp, _vp, _vp, _vp]),
         "mg_run_replicates": (C.c_int, [_vp, P(_abi.ExperimentConfigC), C.c_int32, C.c_int32,
                                         _vp, P(_abi.RunSeriesC), _vp]),
+        "mg_host_malloc": (C.c_int, [C.c_size_t, _vp]),
+        "mg_host_free": (C.c_int, [_vp]),
+        "mg_copy_async": (C.c_int, [_vp, _vp, _vp, C.c_size_t]),
+        "mg_compute_alpha": (C.c_int, [_vp, C.c_int32, C.c_int64, _vp, _vp, _vp, _vp, C.c_double,
+                                       _vp]),
+        "mg_scalar_op": (C.c_int, [_vp, C.c_int32, C.c_int64, _vp, C.c_double, C.c_int32, _vp]),
         "mg_aggregate_series": (C.c_int, [_vp, C.c_int32, C.c_int32, C.c_int32, _vp, _vp, _vp,
                                           _vp]),
         "mg_run_experiment_stats": (C.c_int, [_vp, P(_abi.ExperimentConfigC), C.c_int32,

@@ -229,6 +229,25 @@ int mg_copy_device(mg_ctx* ctx, void* dst, const void* src, size_t bytes) {
   return MG_OK;
 }
 
+int mg_host_malloc(size_t bytes, void** out) {
+  if (!out) return fail(MG_EINVAL, "mg_host_malloc: null argument");
+  *out = nullptr;
+  if (bytes == 0) return MG_OK;
+  MG_CUDA_TRY(cudaMallocHost(out, bytes));
+  return MG_OK;
+}
+
+int mg_host_free(void* p) {
+  if (p) MG_CUDA_TRY(cudaFreeHost(p));
+  return MG_OK;
+}
+
+int mg_copy_async(mg_ctx* ctx, void* dst, const void* src, size_t bytes) {
+  if (!ctx || (bytes && (!dst || !src))) return fail(MG_EINVAL, "mg_copy_async: null argument");
+  if (bytes) MG_CUDA_TRY(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, ctx->stream));
+  return MG_OK;
+}
+
 uint64_t mg_mix64(uint64_t x) {
   // rng.hpp:9-14
   x += 0x9e3779b97f4a7c15ULL;

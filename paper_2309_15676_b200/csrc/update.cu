@@ -536,6 +536,29 @@ __global__ void meta_step_kernel(int64_t n, MetaK k, bool first, T* __restrict__
   }
 }
 
+// compute_alpha (meta.hpp:38-47): the standalone weight with var_meta and
+// var_diff kept apart, summed left to right as in the reference expression.
+template <class T>
+__global__ void compute_alpha_kernel(int64_t n, double eps_alpha, const T* __restrict__ vp,
+                                     const T* __restrict__ vm, const T* __restrict__ vd,
+                                     const T* __restrict__ ap, T* __restrict__ out) {
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += int64_t(gridDim.x) * blockDim.x) {
+    const T raw = vp[i] / (((vp[i] + vm[i]) + vd[i]) + T(eps_alpha));
+    out[i] = std_min(raw, T(1) / (T(2) - ap[i]));
+  }
+}
+
+// out = x * s (rescale_diff_variance, meta.hpp:51-53) or x / s (the bias
+// corrections of Adam::m_hat / v_hat, adam.hpp:43-44).
+template <class T>
+__global__ void scalar_op_kernel(int64_t n, double s, int op, const T* __restrict__ x,
+                                 T* __restrict__ out) {
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += int64_t(gridDim.x) * blockDim.x)
+    out[i] = op == 0 ? x[i] * T(s) : x[i] / T(s);
+}
+
 template <class T>
 __global__ void adam_step_kernel(int64_t n, AdamK k, bool first, T* __restrict__ m,
                                  T* __restrict__ v, const T* __restrict__ g,
@@ -885,6 +908,63 @@ int mg_adam_step(mg_ctx* ctx, int32_t dtype, int64_t n, mg_adam_scalars* s, void
                                                             (const double*)grad, (double*)delta);
   else
     return fail(MG_EINVAL, "mg_adam_step: unknown dtype");
+  MG_LAUNCH_CHECK(ctx);
+  return MG_OK;
+}
+
+int mg_compute_alpha(mg_ctx* ctx, int32_t dtype, int64_t n, const void* var_prop,
+                     const void* var_meta, const void* var_diff, const void* alpha_prev,
+                     double eps_alpha, void* out) {
+  if (!ctx) return fail(MG_EINVAL, "mg_compute_alpha: null argument");
+  if (n < 0) return fail(MG_EINVAL, "compute_alpha: dimension mismatch");
+  if (n == 0) return MG_OK;
+  if (!var_prop || !var_meta || !var_diff || !alpha_prev || !out)
+    return fail(MG_EINVAL, "mg_compute_alpha: null argument");
+  if (dtype != MG_F32 && dtype != MG_F64) return fail(MG_EINVAL, "mg_compute_alpha: unknown dtype");
+  const int grid = grid_for(ctx, n, 256, 8);
+  MG_CUDA_TRY(cudaMemsetAsync(ctx->flag, 0, sizeof(int), ctx->stream));
+  if (dtype == MG_F32) {
+    negvar_check_kernel<float><<<grid, 256, 0, ctx->stream>>>(n, (const float*)var_prop,
+                                                              (const float*)var_meta, ctx->flag);
+    negvar_check_kernel<float><<<grid, 256, 0, ctx->stream>>>(n, (const float*)var_diff,
+                                                              (const float*)var_diff, ctx->flag);
+  } else {
+    negvar_check_kernel<double><<<grid, 256, 0, ctx->stream>>>(n, (const double*)var_prop,
+                                                               (const double*)var_meta, ctx->flag);
+    negvar_check_kernel<double><<<grid, 256, 0, ctx->stream>>>(n, (const double*)var_diff,
+                                                               (const double*)var_diff, ctx->flag);
+  }
+  MG_LAUNCH_CHECK(ctx);
+  ctx->launches++;
+  int flag = 0;
+  MG_CUDA_TRY(cudaMemcpyAsync(&flag, ctx->flag, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+  MG_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+  if (flag) return fail(MG_ELOGIC, "compute_alpha: negative variance input");
+  if (dtype == MG_F32)
+    compute_alpha_kernel<float><<<grid, 256, 0, ctx->stream>>>(
+        n, eps_alpha, (const float*)var_prop, (const float*)var_meta, (const float*)var_diff,
+        (const float*)alpha_prev, (float*)out);
+  else
+    compute_alpha_kernel<double><<<grid, 256, 0, ctx->stream>>>(
+        n, eps_alpha, (const double*)var_prop, (const double*)var_meta, (const double*)var_diff,
+        (const double*)alpha_prev, (double*)out);
+  MG_LAUNCH_CHECK(ctx);
+  return MG_OK;
+}
+
+int mg_scalar_op(mg_ctx* ctx, int32_t dtype, int64_t n, const void* x, double s, int32_t op,
+                 void* out) {
+  if (!ctx || (n > 0 && (!x || !out))) return fail(MG_EINVAL, "mg_scalar_op: null argument");
+  if (op != 0 && op != 1) return fail(MG_EINVAL, "mg_scalar_op: op must be 0 (mul) or 1 (div)");
+  if (n <= 0) return n < 0 ? fail(MG_EINVAL, "mg_scalar_op: negative size") : MG_OK;
+  const int grid = grid_for(ctx, n, 256, 8);
+  if (dtype == MG_F32)
+    scalar_op_kernel<float><<<grid, 256, 0, ctx->stream>>>(n, s, op, (const float*)x, (float*)out);
+  else if (dtype == MG_F64)
+    scalar_op_kernel<double><<<grid, 256, 0, ctx->stream>>>(n, s, op, (const double*)x,
+                                                            (double*)out);
+  else
+    return fail(MG_EINVAL, "mg_scalar_op: unknown dtype");
   MG_LAUNCH_CHECK(ctx);
   return MG_OK;
 }
