@@ -37,6 +37,11 @@ inline void check(int status) {
   }
 }
 
+// Argument validation with the reference's exception type and message.
+inline void require(bool ok, const char* what) {
+  if (!ok) throw std::invalid_argument(what);
+}
+
 // Per host thread: one context (device + private stream) and the staging
 // blocks.  The reference runs one replicate per std::thread
 // (harness.cpp:263-271); a libmgcuda context is single-threaded.
