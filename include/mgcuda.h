@@ -464,6 +464,15 @@ int mg_run_replicates(mg_ctx* ctx, const mg_experiment_config* cfg, int32_t rep_
                       int32_t rep_count, mg_run_record* records, const mg_run_series* series,
                       double* final_params);
 
+/* mg_run_replicates that also returns every RunRecord vector
+ * (harness.hpp:79-88, recorded at harness.cpp:170-179): full is a HOST fp64
+ * array [rep_count][iterations][8][dim] holding, per iteration, params,
+ * prop, diff, mean_est, var_est, alpha (NaN for Adam), delta, true_grad;
+ * NaN past iterations_run.  Feeds write_replicate_csv (harness.cpp:344-365). */
+int mg_run_replicates_full(mg_ctx* ctx, const mg_experiment_config* cfg, int32_t rep_begin,
+                           int32_t rep_count, mg_run_record* records, const mg_run_series* series,
+                           double* final_params, double* full);
+
 /* ---------------------------------- across-replicate aggregation (F2) */
 /* Per-iteration statistics across replicates (harness.cpp:274-302,
  * stats.hpp:44-68), on the device.  series: device fp64 [S][R][T] (entry

@@ -23,6 +23,8 @@
 #include <thread>
 #include <vector>
 
+#include <json.hpp>
+
 #include "metagrad/adam.hpp"
 #include "metagrad/harness.hpp"
 #include "metagrad/meta.hpp"
@@ -295,6 +297,37 @@ int ref_run_single(const char* cfg_text, int replicate, int* out_iters, int* out
 
 // harness.cpp:249-302 (+ writers :311-342).  Returns the wall time in
 // seconds of run_experiment; writes the aggregate CSV to csv_path if given.
+static void write_text(const char* path, const std::string& text) {
+  FILE* f = std::fopen(path, "wb");
+  if (!f) throw std::runtime_error(std::string("cannot open output file: ") + path);
+  std::fwrite(text.data(), 1, text.size(), f);
+  std::fclose(f);
+}
+
+// run_experiment + every writer of harness.cpp:305-427: the aggregate CSV,
+// summary_json, and write_replicate_csv of replicate `rep_index` (paths may
+// be NULL/empty to skip).  Golden for tests/test_report_format.py.
+int ref_run_experiment_outputs(const char* cfg_text, const char* csv_path, const char* json_path,
+                               const char* rep_csv_path, int rep_index) {
+  return guarded([&] {
+    const ExperimentConfig cfg = parse_config(cfg_text);
+    const AggregateReport rep = run_experiment(cfg);
+    if (csv_path && *csv_path) {
+      std::ostringstream os;
+      write_aggregate_csv(rep, os);
+      write_text(csv_path, os.str());
+    }
+    if (json_path && *json_path) write_text(json_path, summary_json(rep));
+    if (rep_csv_path && *rep_csv_path) {
+      if (rep_index < 0 || rep_index >= int(rep.records.size()))
+        throw std::invalid_argument("replicate index out of range");
+      std::ostringstream os;
+      write_replicate_csv(rep.records[size_t(rep_index)], os);
+      write_text(rep_csv_path, os.str());
+    }
+  });
+}
+
 int ref_run_experiment(const char* cfg_text, const char* csv_path, double* out_seconds,
                        int* out_diverged) {
   return guarded([&] {
@@ -375,6 +408,15 @@ int ref_meta_update_bench(std::int64_t n, int steps, int threads, int pool, cons
 // harness.cpp:305-309 (shortest round-trip std::to_chars)
 int ref_format_double(double v, char* out, int cap) {
   const std::string s = format_double(v);
+  if (int(s.size()) + 1 > cap) return 1;
+  std::memcpy(out, s.c_str(), s.size() + 1);
+  return 0;
+}
+
+// A double as the reference's summary_json emits it (nlohmann::json dump,
+// harness.cpp:367-427) — pins report.json_double.
+int ref_json_double(double v, char* out, int cap) {
+  const std::string s = nlohmann::ordered_json(v).dump();
   if (int(s.size()) + 1 > cap) return 1;
   std::memcpy(out, s.c_str(), s.size() + 1);
   return 0;

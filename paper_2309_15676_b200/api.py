@@ -880,6 +880,9 @@ class RunRecord:
     evals_used: int
     series: Dict[str, np.ndarray]
     final_params: np.ndarray
+    # full per-iteration vectors (harness.hpp:79-88), [iterations_run][dim]
+    # each, when requested (run_single(..., full=True)); alpha is None for Adam
+    vectors: Optional[Dict[str, Optional[np.ndarray]]] = None
 
 
 SCALED_MIN_PIXELS = 1 << 16
@@ -947,32 +950,52 @@ def _run_minirender_scaled(cfg: ExperimentConfig, replicate: int, ctx=None) -> "
     return rec
 
 
-def _run_device(cfg: ExperimentConfig, rep_begin: int, rep_count: int, ctx=None):
-    if _scaled_eligible(cfg):
+def _run_device(cfg: ExperimentConfig, rep_begin: int, rep_count: int, ctx=None,
+                full: bool = False):
+    if _scaled_eligible(cfg) and not full:
         return [_run_minirender_scaled(cfg, r, ctx) for r in range(rep_begin, rep_begin + rep_count)]
     ctx = ctx or Context.default()
     c = cfg.to_c()
     it = cfg.iterations
+    dim = cfg.problem_dim()
     bufs = {n: np.full((rep_count, it), np.nan) for n in _abi.SERIES_NAMES}
     ser = _abi.RunSeriesC(*[b.ctypes.data_as(C.c_void_p) for b in bufs.values()])
     recs = (_abi.RunRecordC * rep_count)()
-    finals = np.empty((rep_count, cfg.problem_dim()))
-    check(load().mg_run_replicates(ctx.h, C.byref(c), rep_begin, rep_count, C.cast(recs, C.c_void_p),
-                                   C.byref(ser), finals.ctypes.data_as(C.c_void_p)))
+    finals = np.empty((rep_count, dim))
+    if full:
+        vecs = np.empty((rep_count, it, 8, dim))
+        check(load().mg_run_replicates_full(ctx.h, C.byref(c), rep_begin, rep_count,
+                                            C.cast(recs, C.c_void_p), C.byref(ser),
+                                            finals.ctypes.data_as(C.c_void_p),
+                                            vecs.ctypes.data_as(C.c_void_p)))
+    else:
+        check(load().mg_run_replicates(ctx.h, C.byref(c), rep_begin, rep_count,
+                                       C.cast(recs, C.c_void_p), C.byref(ser),
+                                       finals.ctypes.data_as(C.c_void_p)))
     out = []
     for r in range(rep_count):
         rec = recs[r]
+        vectors = None
+        if full:
+            from .report import REPLICATE_VECTORS
+            n_run = rec.iterations_run
+            vectors = {n: vecs[r, :n_run, k].copy() for k, n in enumerate(REPLICATE_VECTORS)}
+            if cfg.optimizer != "meta":
+                vectors["alpha"] = None
         out.append(RunRecord(STATUS[rec.status], rec.iterations_run, rec.draws_used,
-                             rec.evals_used, {n: bufs[n][r] for n in bufs}, finals[r]))
+                             rec.evals_used, {n: bufs[n][r] for n in bufs}, finals[r], vectors))
     return out
 
 
-def run_single(cfg: ExperimentConfig, replicate_index: int, ctx=None) -> RunRecord:
-    """harness.cpp:90-200 on the device."""
+def run_single(cfg: ExperimentConfig, replicate_index: int, ctx=None,
+               full: bool = False) -> RunRecord:
+    """harness.cpp:90-200 on the device.  full=True also returns every
+    per-iteration vector of the reference's RunRecord (record.vectors),
+    e.g. for report.write_replicate_csv."""
     cfg.validate()
     if cfg.coord >= cfg.problem_dim():
         raise InvalidArgument(_abi.MG_EINVAL, "coord exceeds problem dimension")
-    return _run_device(cfg, replicate_index, 1, ctx)[0]
+    return _run_device(cfg, replicate_index, 1, ctx, full=full)[0]
 
 
 @dataclasses.dataclass

@@ -45,6 +45,9 @@ struct RunK {
   mg_run_record* recs;
   double* series[kNumSeries];  // [R][iterations] each, or null
   double* final_params;        // [R][dim] or null
+  // full per-iteration vectors (harness.hpp:79-88), [R][iterations][8][dim]:
+  // params, prop, diff, mean_est, var_est, alpha, delta, true_grad; or null
+  double* full;
 };
 
 // Up to three independent sums over j in [0, n) of f(j) (returns in
@@ -331,6 +334,27 @@ __global__ void __launch_bounds__(kThreads) run_kernel(RunK<T> k) {
       for (int s = 0; s < kNumSeries; ++s)
         if (k.series[s]) k.series[s][at] = vals[s];
     }
+    if (k.full) {  // RunRecord vectors, harness.cpp:170-179
+      double* fr = k.full + (size_t(r) * iters + i) * 8 * size_t(d);
+      for (int j = threadIdx.x; j < d; j += kThreads) {
+        const double x = double(params[j]);
+        double tgj;
+        if (c.problem == MG_EXP_RATE)
+          tgj = (2.0 * (1.0 / x - c.target_mean)) * (-1.0 / (x * x));
+        else if (c.problem == MG_MULT_NOISE)
+          tgj = x - k.truth[j];
+        else
+          tgj = 2.0 * (x - k.truth[j]);
+        fr[j] = x;
+        fr[size_t(d) + j] = double(prop[j]);
+        fr[2 * size_t(d) + j] = double(diff[j]);
+        fr[3 * size_t(d) + j] = double(mest[j]);
+        fr[4 * size_t(d) + j] = double(vest[j]);
+        fr[5 * size_t(d) + j] = use_meta ? double(ap[j]) : nan("");
+        fr[6 * size_t(d) + j] = double(delta[j]);
+        fr[7 * size_t(d) + j] = tgj;
+      }
+    }
     iters_run = i + 1;
     // prev = params; params += delta; project (harness.cpp:182-188)
     for (int j = threadIdx.x; j < d; j += kThreads) {
@@ -406,7 +430,7 @@ template <class T>
 // active counts come back (`series` is ignored).
 int run_replicates(mg_ctx* ctx, const mg_experiment_config* cfg, int rep_begin, int R,
                    mg_run_record* records, const mg_run_series* series, double* final_params,
-                   double* stats = nullptr, int32_t* active = nullptr) {
+                   double* stats = nullptr, int32_t* active = nullptr, double* full = nullptr) {
   const int d = problem_dim(cfg);
   const int iters = cfg->iterations;
   std::vector<double> truth(d, 0.0), init(d, 0.0);
@@ -543,6 +567,15 @@ int run_replicates(mg_ctx* ctx, const mg_experiment_config* cfg, int rep_begin, 
       return fail(MG_ENOMEM, "run: allocation failed");
     }
   }
+  const size_t full_bytes = sizeof(double) * size_t(R) * iters * 8 * size_t(d);
+  if (full) {
+    k.full = (double*)dalloc(full_bytes);
+    if (!k.full) {
+      cleanup();
+      return fail(MG_ENOMEM, "run: allocation failed (full records)");
+    }
+    cudaMemsetAsync(k.full, 0xff, full_bytes, s);  // NaN past iterations_run
+  }
   run_kernel<T><<<R, kThreads, 0, s>>>(k);
   ctx->launches++;
   cudaError_t e = cudaGetLastError();
@@ -567,6 +600,7 @@ int run_replicates(mg_ctx* ctx, const mg_experiment_config* cfg, int rep_begin, 
   cudaMemcpyAsync(records, k.recs, sizeof(mg_run_record) * R, cudaMemcpyDeviceToHost, s);
   for (int i = 0; i < kNumSeries && host_series; ++i)
     if (k.series[i]) cudaMemcpyAsync(host_series[i], k.series[i], ser_bytes, cudaMemcpyDeviceToHost, s);
+  if (full) cudaMemcpyAsync(full, k.full, full_bytes, cudaMemcpyDeviceToHost, s);
   if (final_params)
     cudaMemcpyAsync(final_params, k.final_params, sizeof(double) * size_t(R) * d,
                     cudaMemcpyDeviceToHost, s);
@@ -580,6 +614,25 @@ int run_replicates(mg_ctx* ctx, const mg_experiment_config* cfg, int rep_begin, 
 }  // namespace mg
 
 using namespace mg;
+
+extern "C" int mg_run_replicates_full(mg_ctx* ctx, const mg_experiment_config* cfg,
+                                      int32_t rep_begin, int32_t rep_count,
+                                      mg_run_record* records, const mg_run_series* series,
+                                      double* final_params, double* full) {
+  if (!ctx || !cfg || !records || !full)
+    return fail(MG_EINVAL, "mg_run_replicates_full: null argument");
+  int st = mg_config_validate(cfg);
+  if (st) return st;
+  if (rep_count < 1 || rep_begin < 0)
+    return fail(MG_EINVAL, "mg_run_replicates_full: bad replicate range");
+  if (cfg->rng != MG_RNG_MT64)
+    return fail(MG_EUNSUPPORTED, "mg_run_replicates_full: only the bit-exact mt64 streams are supported");
+  if (cfg->dtype == MG_F64)
+    return run_replicates<double>(ctx, cfg, rep_begin, rep_count, records, series, final_params,
+                                  nullptr, nullptr, full);
+  return run_replicates<float>(ctx, cfg, rep_begin, rep_count, records, series, final_params,
+                               nullptr, nullptr, full);
+}
 
 extern "C" int mg_run_experiment_stats(mg_ctx* ctx, const mg_experiment_config* cfg,
                                        int32_t rep_begin, int32_t rep_count,
