@@ -52,7 +52,9 @@ struct ThreadState {
   void* dev = nullptr;   // device staging block
   void* host = nullptr;  // page-locked host staging block
   size_t cap = 0;        // doubles in each block
+  mg_mt64* engine = nullptr;  // one device mt19937_64 (problems.hpp adapters)
   ~ThreadState() {
+    if (engine) mg_mt64_destroy(engine);
     if (ctx) {
       if (dev) mg_free(ctx, dev);
       mg_ctx_synchronize(ctx);

@@ -147,6 +147,14 @@ int mg_mt64_destroy(mg_mt64* g);
  * 2 = uniform_pos() double (rng.hpp:31). */
 int mg_mt64_draw(mg_ctx* ctx, mg_mt64* g, int64_t n, int32_t kind, void* out);
 
+/* Engine state of stream `stream` in std::mt19937_64's own layout (the 312
+ * state words and the position 0..312, as its operator<< writes them), so
+ * a host engine (the reference's Rng, rng.hpp:36) can continue on the
+ * device and resume on the host bit-exactly. */
+int mg_mt64_set_state(mg_ctx* ctx, mg_mt64* g, int32_t stream, const uint64_t* words,
+                      int32_t idx);
+int mg_mt64_get_state(mg_ctx* ctx, mg_mt64* g, int32_t stream, uint64_t* words, int32_t* idx);
+
 /* GF(2) jump-ahead (Haramoto et al. 2008): advance every stream of g by
  * `distance` draws in O(19937) work, so many engines can produce disjoint
  * segments of ONE replicate's stream bit-exactly.  Streams must sit at a

@@ -110,6 +110,8 @@ def load():
                                         _vp, P(_abi.RunSeriesC), _vp]),
         "mg_run_replicates_full": (C.c_int, [_vp, P(_abi.ExperimentConfigC), C.c_int32,
                                              C.c_int32, _vp, P(_abi.RunSeriesC), _vp, _vp]),
+        "mg_mt64_set_state": (C.c_int, [_vp, _vp, C.c_int32, _vp, C.c_int32]),
+        "mg_mt64_get_state": (C.c_int, [_vp, _vp, C.c_int32, _vp, _vp]),
         "mg_host_malloc": (C.c_int, [C.c_size_t, _vp]),
         "mg_host_free": (C.c_int, [_vp]),
         "mg_copy_async": (C.c_int, [_vp, _vp, _vp, C.c_size_t]),

@@ -287,4 +287,36 @@ int mg_mt64_draw(mg_ctx* ctx, mg_mt64* g, int64_t n, int32_t kind, void* out) {
   return mg::mt64_draw(ctx, g, n, kind, out);
 }
 
+// The engine state in libstdc++'s std::mt19937_64 layout (_M_x[312], _M_p;
+// random.h:1620-1627, serialised by its operator<< / operator>>), so a host
+// engine can hand its position to the device and take it back.
+int mg_mt64_set_state(mg_ctx* ctx, mg_mt64* g, int32_t stream, const uint64_t* words,
+                      int32_t idx) {
+  using namespace mg;
+  if (!ctx || !g || !words) return fail(MG_EINVAL, "mg_mt64_set_state: null argument");
+  if (stream < 0 || stream >= g->streams) return fail(MG_EINVAL, "mg_mt64_set_state: bad stream");
+  if (idx < 0 || idx > kMtN) return fail(MG_EINVAL, "mg_mt64_set_state: index must lie in [0, 312]");
+  MG_CUDA_TRY(cudaMemcpyAsync(g->state + size_t(stream) * kMtN, words, sizeof(uint64_t) * kMtN,
+                              cudaMemcpyHostToDevice, ctx->stream));
+  MG_CUDA_TRY(cudaMemcpyAsync(g->idx + stream, &idx, sizeof(int), cudaMemcpyHostToDevice,
+                              ctx->stream));
+  MG_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+  g->host_idx = idx;
+  return MG_OK;
+}
+
+int mg_mt64_get_state(mg_ctx* ctx, mg_mt64* g, int32_t stream, uint64_t* words, int32_t* idx) {
+  using namespace mg;
+  if (!ctx || !g || !words || !idx) return fail(MG_EINVAL, "mg_mt64_get_state: null argument");
+  if (stream < 0 || stream >= g->streams) return fail(MG_EINVAL, "mg_mt64_get_state: bad stream");
+  int i = 0;
+  MG_CUDA_TRY(cudaMemcpyAsync(words, g->state + size_t(stream) * kMtN, sizeof(uint64_t) * kMtN,
+                              cudaMemcpyDeviceToHost, ctx->stream));
+  MG_CUDA_TRY(cudaMemcpyAsync(&i, g->idx + stream, sizeof(int), cudaMemcpyDeviceToHost,
+                              ctx->stream));
+  MG_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+  *idx = i;
+  return MG_OK;
+}
+
 }  // extern "C"

@@ -41,3 +41,12 @@ def test_reference_validation_suite_on_gpu_estimators():
 def test_reference_acceptance_on_gpu_estimators(criterion):
     rc, out = _run(["acceptance", criterion], timeout=1500)
     assert rc == 0, out[-3000:]
+
+
+def test_gpu_problem_adapters_match_reference_samplers():
+    """metagrad_gpu::{MiniRenderProblem, ExpRateProblem, MultNoiseQuadratic}
+    (device sample_pair behind the reference's Problem interface) vs the
+    reference's CPU samplers on twin Rngs (tests/cpp/dropin/test_gpu_problems.cpp)."""
+    rc, out = _run(["test_gpu_problems"])
+    assert rc == 0, out[-3000:]
+    assert "0 failed" in out, out[-3000:]
