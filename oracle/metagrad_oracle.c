@@ -1284,3 +1284,318 @@ void mgo_helix_path(int W, int H, int nsph, const double* sph, const double Le[3
     for (int k = 0; k < HX_NP; ++k) dL[c * HX_NP + k] = dL2[0][c][k];
   }
 }
+
+
+/* =====================================================================
+ * F1 slice 3: textured triangle-mesh scene (BASELINE.json configs[3]),
+ * own renderer.  Objects are triangle meshes (quad, tessellated sphere,
+ * seeded displaced sphere), each with its own R x R RGB albedo + roughness
+ * texture (nearest texel of the interpolated uv): the parameter vector is
+ * [object][channel: base r, g, b, roughness][R*R].  Paths of up to `maxv`
+ * vertices with NEE to a rectangular area light (not visible to camera
+ * rays) and a constant environment collected by escaping rays.  BSDF: the
+ * helix slice's principled BSDF with metalness 0.  Directions are sampled
+ * independently of the parameters, so one geometric trace serves both
+ * parameter sets of the finite difference.  Parameter gradients are
+ * reverse-mode: per vertex the NEE weight, the bounce factor's reciprocal
+ * and the roughness derivatives are stored; suffix radiance is accumulated
+ * backwards; every (vertex, parameter) contribution is quantised to 2^-40
+ * and summed as an integer (order independent).  This oracle intersects by
+ * brute force over all triangles (the device uses a BVH; equal results
+ * because the closest hit breaks ties on the lower triangle index and the
+ * BVH culling is conservative).  DESIGN.md §12.
+ * ===================================================================== */
+
+#define MS_MAXV 8
+#define MS_REC 18  /* per-triangle record: v0 e1 e2 n(unit) uv0 duv1 duv2 */
+static const double MS_TMIN = 1e-9;
+static const double MS_OFF = 1e-6;
+
+typedef struct ms_scene {
+  int W, H, T, R;
+  const double* tri;
+  const int32_t* obj;
+  const double* view; /* cam fwd right up(3 each) tanh ly lx0 lx1 lz0 lz1 Le(3) env(3) maxv */
+} ms_scene;
+
+static inline void ms_cross(const double a[3], const double b[3], double r[3]) {
+  r[0] = a[1] * b[2] - a[2] * b[1];
+  r[1] = a[2] * b[0] - a[0] * b[2];
+  r[2] = a[0] * b[1] - a[1] * b[0];
+}
+
+/* Moller-Trumbore; 1 on a hit with t > MS_TMIN */
+static int ms_tri_hit(const double* r, const double o[3], const double d[3], double* t, double* u,
+                      double* v) {
+  const double* v0 = r;
+  const double* e1 = r + 3;
+  const double* e2 = r + 6;
+  double p[3], q[3], s[3];
+  ms_cross(d, e2, p);
+  const double det = hx_dot(e1, p);
+  if (det == 0.0) return 0;
+  const double inv = 1.0 / det;
+  s[0] = o[0] - v0[0]; s[1] = o[1] - v0[1]; s[2] = o[2] - v0[2];
+  const double uu = hx_dot(s, p) * inv;
+  if (uu < 0.0 || uu > 1.0) return 0;
+  ms_cross(s, e1, q);
+  const double vv = hx_dot(d, q) * inv;
+  if (vv < 0.0 || uu + vv > 1.0) return 0;
+  const double tt = hx_dot(e2, q) * inv;
+  if (!(tt > MS_TMIN)) return 0;
+  *t = tt; *u = uu; *v = vv;
+  return 1;
+}
+
+int mgo_mesh_closest_hit(int T, const double* tri, const double o[3], const double d[3],
+                         double* t_out, double* u_out, double* v_out) {
+  double best = INFINITY, bu = 0.0, bv = 0.0;
+  int bk = -1;
+  for (int k = 0; k < T; ++k) {
+    double t, u, v;
+    if (ms_tri_hit(tri + (size_t)MS_REC * k, o, d, &t, &u, &v) && t < best) {
+      best = t; bu = u; bv = v; bk = k;
+    }
+  }
+  *t_out = best; *u_out = bu; *v_out = bv;
+  return bk;
+}
+
+static int ms_occluded(const ms_scene* S, const double o[3], const double d[3], double tmax) {
+  for (int k = 0; k < S->T; ++k) {
+    double t, u, v;
+    if (ms_tri_hit(S->tri + (size_t)MS_REC * k, o, d, &t, &u, &v) && t < tmax) return 1;
+  }
+  return 0;
+}
+
+/* BSDF with metalness 0: f_c = base_c / pi + S (S = DG F, channel
+ * independent); dS/drough.  Same expressions as hx_bsdf. */
+static void ms_bsdf(const double base[3], double rough, const double n[3], const double wi[3],
+                    const double wo[3], double f[3], double* dS) {
+  const double th[HX_NP] = {base[0], base[1], base[2], 0.0, rough};
+  double df[3][HX_NP];
+  hx_bsdf(th, n, wi, wo, f, df);
+  *dS = df[0][4];
+}
+
+typedef struct ms_vert {
+  int64_t base;             /* parameter index of (object, channel 0, texel) */
+  double A[2][3];           /* beta * Le * G (NEE weight), 0 without NEE */
+  double dSn[2];            /* dS/drough at the NEE direction */
+  double invfb[2][3];       /* 1 / f(bounce), 0 without a bounce or f == 0 */
+  double dSb[2];            /* dS/drough at the bounce direction */
+  double C[2][3];           /* NEE contribution */
+} ms_vert;
+
+/* One path for nsets parameter sets; L[s][3]; vertices (if vout) and the
+ * number of vertices; E[s][3] = environment collected after the last one. */
+static int ms_path(const ms_scene* S, const double* const th[2], int nsets, int px, int py,
+                   uint64_t key, uint32_t it, uint32_t path, double L[2][3], ms_vert* vout,
+                   double E[2][3]) {
+  const double* V = S->view;
+  const int maxv = (int)V[24];
+  const int64_t R2 = (int64_t)S->R * S->R;
+  const uint32_t pix = (uint32_t)(py * S->W + px);
+  double u[4];
+  hx_rng(key, pix, it, path, 0u, u);
+  const double sx = ((px + u[0]) / S->W) * 2.0 - 1.0;
+  const double sy = 1.0 - ((py + u[1]) / S->H) * 2.0;
+  const double ax = sx * (V[12] * ((double)S->W / (double)S->H)), ay = sy * V[12];
+  double o[3] = {V[0], V[1], V[2]};
+  double d[3];
+  for (int i = 0; i < 3; ++i) d[i] = (V[3 + i] + ax * V[6 + i]) + ay * V[9 + i];
+  const double dl = sqrt(hx_dot(d, d));
+  d[0] /= dl; d[1] /= dl; d[2] /= dl;
+  double beta[2][3];
+  for (int s = 0; s < 2; ++s)
+    for (int c = 0; c < 3; ++c) { beta[s][c] = 1.0; L[s][c] = 0.0; E[s][c] = 0.0; }
+  const double la = (V[15] - V[14]) * (V[17] - V[16]);
+  int nv = 0;
+  for (int v = 0; v < maxv; ++v) {
+    double t, bu, bv;
+    const int k = mgo_mesh_closest_hit(S->T, S->tri, o, d, &t, &bu, &bv);
+    if (k < 0) { /* escaped: environment */
+      for (int s = 0; s < nsets; ++s)
+        for (int c = 0; c < 3; ++c) {
+          E[s][c] = beta[s][c] * V[21 + c];
+          L[s][c] += E[s][c];
+        }
+      return nv;
+    }
+    const double* r = S->tri + (size_t)MS_REC * k;
+    const double x[3] = {o[0] + t * d[0], o[1] + t * d[1], o[2] + t * d[2]};
+    double n[3] = {r[9], r[10], r[11]};
+    if (hx_dot(n, d) > 0.0) { n[0] = -n[0]; n[1] = -n[1]; n[2] = -n[2]; }
+    const double U = (r[12] + bu * r[14]) + bv * r[16];
+    const double W_ = (r[13] + bu * r[15]) + bv * r[17];
+    int tx = (int)(U * S->R), ty = (int)(W_ * S->R);
+    tx = tx < 0 ? 0 : (tx > S->R - 1 ? S->R - 1 : tx);
+    ty = ty < 0 ? 0 : (ty > S->R - 1 ? S->R - 1 : ty);
+    const int64_t pbase = (int64_t)S->obj[k] * 4 * R2 + (int64_t)ty * S->R + tx;
+    ms_vert* mv = vout ? &vout[nv] : NULL;
+    ms_vert tmp;
+    if (!mv) mv = &tmp;
+    mv->base = pbase;
+    for (int s = 0; s < 2; ++s) {
+      mv->dSn[s] = 0.0; mv->dSb[s] = 0.0;
+      for (int c = 0; c < 3; ++c) { mv->A[s][c] = 0.0; mv->invfb[s][c] = 0.0; mv->C[s][c] = 0.0; }
+    }
+    ++nv;
+    double base[2][3], rough[2];
+    for (int s = 0; s < nsets; ++s) {
+      for (int c = 0; c < 3; ++c) base[s][c] = th[s][pbase + c * R2];
+      rough[s] = th[s][pbase + 3 * R2];
+    }
+    const double wo[3] = {-d[0], -d[1], -d[2]};
+    const double xo[3] = {x[0] + MS_OFF * n[0], x[1] + MS_OFF * n[1], x[2] + MS_OFF * n[2]};
+    hx_rng(key, pix, it, path, (uint32_t)(v * 256 + 1), u);
+    /* next-event estimation */
+    const double lp[3] = {V[14] + u[0] * (V[15] - V[14]), V[13], V[16] + u[1] * (V[17] - V[16])};
+    double w[3] = {lp[0] - x[0], lp[1] - x[1], lp[2] - x[2]};
+    const double d2 = hx_dot(w, w);
+    const double wl = sqrt(d2);
+    w[0] /= wl; w[1] /= wl; w[2] /= wl;
+    const double cx = hx_dot(n, w), cl = w[1];
+    if (cx > 0.0 && cl > 0.0 && hx_dot(n, wo) > 0.0 && !ms_occluded(S, xo, w, wl - MS_OFF)) {
+      const double gl = ((cx * cl) / d2) * la;
+      for (int s = 0; s < nsets; ++s) {
+        double f[3], dS;
+        ms_bsdf(base[s], rough[s], n, w, wo, f, &dS);
+        mv->dSn[s] = dS;
+        for (int c = 0; c < 3; ++c) {
+          const double A = beta[s][c] * (gl * V[18 + c]);
+          mv->A[s][c] = A;
+          mv->C[s][c] = A * f[c];
+          L[s][c] += mv->C[s][c];
+        }
+      }
+    }
+    if (v == maxv - 1 || hx_dot(n, wo) <= 0.0) return nv;
+    double dx = 0.0, dy = 0.0;
+    int got = 0;
+    for (uint32_t j = 0; !got && j < 64; ++j) {
+      double c4[4];
+      if (j == 0) {
+        c4[0] = u[2]; c4[1] = u[3]; c4[2] = 2.0; c4[3] = 2.0;
+      } else {
+        hx_rng(key, pix, it, path, (uint32_t)(v * 256 + 1 + j), c4);
+      }
+      for (int m = 0; m < 4 && !got; m += 2) {
+        const double a = 2.0 * c4[m] - 1.0, b = 2.0 * c4[m + 1] - 1.0;
+        if (c4[m] <= 1.0 && a * a + b * b < 1.0) { dx = a; dy = b; got = 1; }
+      }
+    }
+    const double dz = sqrt(fmax(0.0, 1.0 - (dx * dx + dy * dy)));
+    if (dz <= 0.0) return nv;
+    double Tb[3], Bb[3];
+    hx_onb(n, Tb, Bb);
+    const double wi[3] = {(dx * Tb[0] + dy * Bb[0]) + dz * n[0],
+                          (dx * Tb[1] + dy * Bb[1]) + dz * n[1],
+                          (dx * Tb[2] + dy * Bb[2]) + dz * n[2]};
+    for (int s = 0; s < nsets; ++s) {
+      double f[3], dS;
+      ms_bsdf(base[s], rough[s], n, wi, wo, f, &dS);
+      mv->dSb[s] = dS;
+      for (int c = 0; c < 3; ++c) {
+        mv->invfb[s][c] = f[c] != 0.0 ? 1.0 / f[c] : 0.0;
+        beta[s][c] = beta[s][c] * (f[c] * QS_PI);
+      }
+    }
+    o[0] = xo[0]; o[1] = xo[1]; o[2] = xo[2];
+    d[0] = wi[0]; d[1] = wi[1]; d[2] = wi[2];
+  }
+  return nv;
+}
+
+/* adjoint of one stored path for set s with channel weights w[3] */
+static void ms_scatter(const ms_vert* vs, int nv, const double E[3], int s, const double w[3],
+                       int64_t R2, int64_t* acc) {
+  double Q[3] = {E[0], E[1], E[2]};
+  for (int v = nv - 1; v >= 0; --v) {
+    const ms_vert* m = &vs[v];
+    double gr = 0.0;
+    for (int c = 0; c < 3; ++c) {
+      const double gb = w[c] * ((m->A[s][c] / QS_PI) + Q[c] * (m->invfb[s][c] / QS_PI));
+      acc[m->base + c * R2] += qs_fix(gb);
+      gr += w[c] * (m->A[s][c] * m->dSn[s] + Q[c] * (m->invfb[s][c] * m->dSb[s]));
+    }
+    acc[m->base + 3 * R2] += qs_fix(gr);
+    for (int c = 0; c < 3; ++c) Q[c] = Q[c] + m->C[s][c];
+  }
+}
+
+void mgo_mesh_render(int W, int H, int T, const double* tri, const int32_t* obj, int R,
+                     const double* view, const double* theta, int spp, uint64_t key,
+                     double* img) {
+  ms_scene S = {W, H, T, R, tri, obj, view};
+  const double* th[2] = {theta, theta};
+  for (int py = 0; py < H; ++py)
+    for (int px = 0; px < W; ++px) {
+      double acc[3] = {0.0, 0.0, 0.0};
+      for (int s = 0; s < spp; ++s) {
+        double L[2][3], E[2][3];
+        ms_path(&S, th, 1, px, py, key, 0xffffffffu, (uint32_t)s, L, NULL, E);
+        for (int c = 0; c < 3; ++c) acc[c] += L[0][c];
+      }
+      for (int c = 0; c < 3; ++c) img[(size_t)c * W * H + (size_t)py * W + px] = acc[c] / spp;
+    }
+}
+
+/* gradient sample pair over the texture parameters, image rows [row0, row1):
+ *   prop = sum_c r_A,c dI_B,c + r_B,c dI_A,c                     (theta_t)
+ *   diff = sum_c 2 r_C,c dI_A,c (theta_t) - 2 r_C,c dI_A,c (theta_{t-1})
+ * with r_X = I_X(theta_t) - I* (r_C at its own theta for the two terms);
+ * loss_est = sum r_A r_B.  prop/diff have nobj*4*R*R entries. */
+void mgo_mesh_sample_pair(int W, int H, int T, const double* tri, const int32_t* obj, int nobj,
+                          int R, const double* view, const double* target_img, const double* now,
+                          const double* prev, uint64_t key, uint32_t it, int row0, int row1,
+                          double* prop, double* diff, double* loss_est) {
+  ms_scene S = {W, H, T, R, tri, obj, view};
+  const int64_t R2 = (int64_t)R * R, np = (int64_t)nobj * 4 * R2;
+  int64_t* fp = (int64_t*)calloc((size_t)np, sizeof(int64_t));
+  int64_t* fd = (int64_t*)calloc((size_t)np, sizeof(int64_t));
+  const double* th[2] = {now, prev};
+  ms_vert va[MS_MAXV], vb[MS_MAXV];
+  double loss = 0.0;
+  for (int py = row0; py < row1; ++py)
+    for (int px = 0; px < W; ++px) {
+      double LA[2][3], EA[2][3], LB[2][3], EB[2][3], LC[2][3], EC[2][3];
+      const int na = ms_path(&S, th, 2, px, py, key, it, 0u, LA, va, EA);
+      const int nb = ms_path(&S, th, 1, px, py, key, it, 1u, LB, vb, EB);
+      ms_path(&S, th, 2, px, py, key, it, 2u, LC, NULL, EC);
+      const size_t pix = (size_t)py * W + px;
+      double rA[3], rB[3], wC0[3], wC1[3];
+      for (int c = 0; c < 3; ++c) {
+        const double Is = target_img[(size_t)c * W * H + pix];
+        rA[c] = LA[0][c] - Is;
+        rB[c] = LB[0][c] - Is;
+        wC0[c] = 2.0 * (LC[0][c] - Is);
+        wC1[c] = -2.0 * (LC[1][c] - Is);
+        loss += rA[c] * rB[c];
+      }
+      ms_scatter(va, na, EA[0], 0, rB, R2, fp);
+      ms_scatter(vb, nb, EB[0], 0, rA, R2, fp);
+      ms_scatter(va, na, EA[0], 0, wC0, R2, fd);
+      ms_scatter(va, na, EA[1], 1, wC1, R2, fd);
+    }
+  for (int64_t k = 0; k < np; ++k) {
+    prop[k] = (double)fp[k] / QS_FIX;
+    diff[k] = (double)fd[k] / QS_FIX;
+  }
+  free(fp);
+  free(fd);
+  *loss_est = loss;
+}
+
+/* one path's radiance (set 0) and its vertex count, for derivative checks */
+int mgo_mesh_path_radiance(int W, int H, int T, const double* tri, const int32_t* obj, int R,
+                           const double* view, const double* theta, int px, int py, uint64_t key,
+                           uint32_t it, uint32_t path, double L_out[3]) {
+  ms_scene S = {W, H, T, R, tri, obj, view};
+  const double* th[2] = {theta, theta};
+  double L[2][3], E[2][3];
+  const int nv = ms_path(&S, th, 1, px, py, key, it, path, L, NULL, E);
+  for (int c = 0; c < 3; ++c) L_out[c] = L[0][c];
+  return nv;
+}

@@ -145,3 +145,19 @@ int mgo_run_single_series(const mg_experiment_config* cfg, int32_t replicate, mg
 #endif
 
 #endif
+
+/* F1 slice 3: textured triangle-mesh scene (configs[3]); brute-force
+ * intersection; triangle records [T][18] = v0 e1 e2 n uv0 duv1 duv2;
+ * view[25] = cam fwd right up tan_half_fov light_y x0 x1 z0 z1 Le[3] env[3]
+ * max_vertices; parameters [nobj][4][R*R] (base r,g,b, roughness). */
+int mgo_mesh_closest_hit(int T, const double* tri, const double o[3], const double d[3],
+                         double* t_out, double* u_out, double* v_out);
+void mgo_mesh_render(int W, int H, int T, const double* tri, const int32_t* obj, int R,
+                     const double* view, const double* theta, int spp, uint64_t key, double* img);
+void mgo_mesh_sample_pair(int W, int H, int T, const double* tri, const int32_t* obj, int nobj,
+                          int R, const double* view, const double* target_img, const double* now,
+                          const double* prev, uint64_t key, uint32_t it, int row0, int row1,
+                          double* prop, double* diff, double* loss_est);
+int mgo_mesh_path_radiance(int W, int H, int T, const double* tri, const int32_t* obj, int R,
+                           const double* view, const double* theta, int px, int py, uint64_t key,
+                           uint32_t it, uint32_t path, double L_out[3]);

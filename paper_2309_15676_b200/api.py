@@ -35,7 +35,8 @@ from ._lib import DomainError, InvalidArgument, LogicError, MgError, check, load
 __all__ = ["Context", "Rng", "Moment2", "GradientSamplePair", "MetaEstimator", "Adam",
            "MiniRenderProblem", "ExpRateProblem", "MultNoiseQuadratic", "FusedMetaUpdate",
            "FusedAdamUpdate", "MiniRenderRun", "QuadTextureProblem", "QuadTextureRun",
-           "HelixProblem", "HelixRun", "helix_spheres",
+           "HelixProblem", "HelixRun", "helix_spheres", "MeshScene", "MeshTextureProblem",
+           "MeshTextureRun", "mesh_scene_geometry", "mesh_scene_view", "smooth_noise_textures",
            "ExperimentConfig", "RunRecord", "AggregateReport", "run_single",
            "run_experiment", "InvalidArgument", "LogicError", "DomainError", "mix64"]
 
@@ -805,6 +806,206 @@ class HelixProblem:
 class HelixRun(QuadTextureRun):
     """configs[2] optimisation loop (same structure as QuadTextureRun); the 5
     parameters (colours, metalness, roughness) are projected to [0, 1]."""
+
+    def __init__(self, problem, optimizer: str = "meta", lr: float = 0.01, seed: int = 0,
+                 replicate: int = 0, **kw):
+        if optimizer == "meta":
+            kw.setdefault("project_hi", 1.0)
+        super().__init__(problem, optimizer, lr, seed, replicate, **kw)
+
+
+# ------------------------------------- F1 slice 3: textured mesh scene
+MESH_VIEW_LAYOUT = ("cam[3] fwd[3] right[3] up[3] tan_half_fov light_y light_x0 light_x1 "
+                    "light_z0 light_z1 Le[3] env[3] max_vertices")
+
+
+def _sphere_triangles(center, radius_fn, n_theta: int, n_phi: int):
+    """UV-sphere tessellation: (v0, v1, v2, uv0, uv1, uv2) lists; single
+    triangles at the poles (no degenerate ones).  uv = (phi/2pi, theta/pi)."""
+    th = np.pi * np.arange(n_theta + 1) / n_theta
+    ph = 2.0 * np.pi * np.arange(n_phi + 1) / n_phi
+    T_, P_ = np.meshgrid(th, ph, indexing="ij")
+    rad = radius_fn(T_, P_)
+    pos = np.stack([center[0] + rad * np.sin(T_) * np.cos(P_), center[1] + rad * np.cos(T_),
+                    center[2] + rad * np.sin(T_) * np.sin(P_)], axis=-1)
+    uv = np.stack([P_ / (2.0 * np.pi), T_ / np.pi], axis=-1)
+    tris = []
+    for i in range(n_theta):
+        for j in range(n_phi):
+            a, b, c, d = (i, j), (i, j + 1), (i + 1, j), (i + 1, j + 1)
+            if i != 0:
+                tris.append((a, b, d))
+            if i != n_theta - 1:
+                tris.append((a, d, c))
+    v = np.array([[pos[k] for k in t] for t in tris])
+    w = np.array([[uv[k] for k in t] for t in tris])
+    return v, w
+
+
+def mesh_scene_geometry(sphere_res=(24, 48), displaced_res=(100, 100), seed: int = 3,
+                        displacement: float = 0.12):
+    """BASELINE.json configs[3] geometry (seed-generated):
+    object 0 a ground quad (y = 0, x, z in [-2.5, 2.5]), object 1 a sphere
+    (centre (-0.9, 0.5, 0), radius 0.5), object 2 a seeded displaced sphere
+    (centre (0.8, 0.55, 0.1), radius 0.5 (1 + displacement * noise),
+    ~2 * n_theta * n_phi triangles: 19.8k at the default 100 x 100).
+    Returns (records [T][18] fp64, object ids [T] int32, nobj)."""
+    quad_v = np.array([[[-2.5, 0.0, -2.5], [2.5, 0.0, -2.5], [2.5, 0.0, 2.5]],
+                       [[-2.5, 0.0, -2.5], [2.5, 0.0, 2.5], [-2.5, 0.0, 2.5]]])
+    quad_w = (quad_v[:, :, [0, 2]] + 2.5) / 5.0
+    sph_v, sph_w = _sphere_triangles((-0.9, 0.5, 0.0), lambda t, p: 0.5 + 0.0 * t, *sphere_res)
+    rs = np.random.RandomState(seed)
+    waves = [(rs.uniform(-1, 1), rs.randint(1, 6), rs.randint(1, 7), rs.uniform(0, 2 * np.pi))
+             for _ in range(6)]
+
+    def disp(t, p):
+        noise = sum(a * np.sin(m * t) * np.cos(g * p + q) for a, m, g, q in waves) / len(waves)
+        return 0.5 * (1.0 + displacement * noise * 2.0)
+    dsp_v, dsp_w = _sphere_triangles((0.8, 0.55, 0.1), disp, *displaced_res)
+    V = np.concatenate([quad_v, sph_v, dsp_v])
+    Wuv = np.concatenate([quad_w, sph_w, dsp_w])
+    obj = np.concatenate([np.zeros(len(quad_v)), np.ones(len(sph_v)),
+                          np.full(len(dsp_v), 2)]).astype(np.int32)
+    e1 = V[:, 1] - V[:, 0]
+    e2 = V[:, 2] - V[:, 0]
+    n = np.cross(e1, e2)
+    n = n / np.linalg.norm(n, axis=1, keepdims=True)
+    rec = np.concatenate([V[:, 0], e1, e2, n, Wuv[:, 0], Wuv[:, 1] - Wuv[:, 0],
+                          Wuv[:, 2] - Wuv[:, 0]], axis=1)
+    return np.ascontiguousarray(rec), obj, 3
+
+
+def mesh_scene_view(max_vertices: int = 6, light=(6.0, 6.0, 6.0), env=(0.25, 0.3, 0.35),
+                    cam=(0.0, 1.6, 4.5), look_at=(0.0, 0.45, 0.0), tan_half_fov: float = 0.45):
+    """view[25] (layout MESH_VIEW_LAYOUT): pinhole camera, rectangular light
+    at y = 3 over x, z in [-1, 1] facing down, constant environment."""
+    cam = np.asarray(cam, dtype=np.float64)
+    fwd = np.asarray(look_at, dtype=np.float64) - cam
+    fwd /= np.linalg.norm(fwd)
+    right = np.cross(fwd, [0.0, 1.0, 0.0])
+    right /= np.linalg.norm(right)
+    up = np.cross(right, fwd)
+    return np.concatenate([cam, fwd, right, up, [tan_half_fov, 3.0, -1.0, 1.0, -1.0, 1.0],
+                           light, env, [float(max_vertices)]]).astype(np.float64)
+
+
+def smooth_noise_textures(nobj: int, R: int, seed: int, grid: int = 6,
+                          base_range=(0.15, 0.85), rough_range=(0.25, 0.9)) -> np.ndarray:
+    """Seeded smooth-noise textures [nobj][4][R*R] (bilinear upsampling of a
+    grid x grid lattice of uniforms): base colour and roughness."""
+    rs = np.random.RandomState(seed)
+    x = (np.arange(R) + 0.5) / R * (grid - 1)
+    i0 = np.minimum(x.astype(int), grid - 2)
+    f = x - i0
+    out = np.empty((nobj, 4, R * R))
+    for o in range(nobj):
+        for c in range(4):
+            g = rs.uniform(0, 1, (grid, grid))
+            rows = g[i0] * (1 - f)[:, None] + g[i0 + 1] * f[:, None]
+            img = rows[:, i0] * (1 - f)[None, :] + rows[:, i0 + 1] * f[None, :]
+            lo, hi = base_range if c < 3 else rough_range
+            out[o, c] = (lo + (hi - lo) * img).reshape(-1)
+    return out
+
+
+class MeshScene:
+    """A triangle scene on the device (BVH built on the host, mg_meshscene_*)."""
+
+    def __init__(self, records: np.ndarray, obj: np.ndarray, nobj: int, tex_res: int, view,
+                 ctx=None):
+        self.ctx = ctx or Context.default()
+        self.records = np.ascontiguousarray(records, dtype=np.float64)
+        self.obj = np.ascontiguousarray(obj, dtype=np.int32)
+        self.nobj, self.R = nobj, tex_res
+        self.view = np.ascontiguousarray(view, dtype=np.float64)
+        h = C.c_void_p()
+        check(load().mg_meshscene_create(self.ctx.h, self.records.shape[0],
+                                         self.records.ctypes.data_as(C.c_void_p),
+                                         self.obj.ctypes.data_as(C.c_void_p), nobj, tex_res,
+                                         C.byref(h)))
+        self.h = h
+
+    def info(self):
+        nodes, depth, params = C.c_int32(), C.c_int32(), C.c_int64()
+        check(load().mg_meshscene_info(self.h, C.byref(nodes), C.byref(depth), C.byref(params)))
+        return {"nodes": nodes.value, "depth": depth.value, "params": params.value,
+                "triangles": self.records.shape[0]}
+
+    def params(self) -> int:
+        return self.nobj * 4 * self.R * self.R
+
+    def intersect(self, rays: torch.Tensor):
+        """rays: CUDA fp64 [n][6] -> (t [n], triangle [n])"""
+        n = rays.shape[0]
+        t = torch.empty(n, dtype=torch.float64, device=rays.device)
+        k = torch.empty(n, dtype=torch.int32, device=rays.device)
+        check(load().mg_meshscene_intersect(self.ctx.h, self.h, n, _p(rays.contiguous()), _p(t),
+                                            _p(k)))
+        return t, k
+
+    def render(self, theta, W: int, H: int, spp: int, key: int):
+        img = torch.empty(3 * W * H, dtype=theta.dtype, device="cuda")
+        check(load().mg_meshscene_render(self.ctx.h, self.h, _dtype_code(theta), W, H,
+                                         self.view.ctypes.data_as(C.c_void_p), spp, key,
+                                         _p(theta.contiguous()), _p(img)))
+        return img
+
+    def __del__(self):
+        try:
+            if getattr(self, "h", None):
+                load().mg_meshscene_destroy(self.h)
+        except Exception:
+            pass
+
+
+class MeshTextureProblem:
+    """BASELINE.json configs[3]: W x H render of the 3-object mesh scene,
+    each object with an R x R RGB albedo + roughness texture (3 * 4 * R^2
+    parameters, ~3.1M at R = 512), targets seeded smooth noise (seed 1),
+    initialised to base 0.5 / roughness 0.5, depth-6 NEE path tracing,
+    1 FD + 2 proportional spp (paths A, B, C).  Own renderer (DESIGN.md §12,
+    oracle mgo_mesh_*)."""
+
+    def __init__(self, width: int = 512, height: int = 512, tex_res: int = 512,
+                 sphere_res=(24, 48), displaced_res=(100, 100), max_vertices: int = 6,
+                 target_seed: int = 1, target_spp: int = 16, dtype=torch.float32, ctx=None):
+        self.ctx = ctx or Context.default()
+        self.W, self.H, self.R, self.dtype = width, height, tex_res, dtype
+        rec, obj, nobj = mesh_scene_geometry(sphere_res, displaced_res)
+        self.scene = MeshScene(rec, obj, nobj, tex_res, mesh_scene_view(max_vertices), self.ctx)
+        n = self.scene.params()
+        self.target_tex = torch.tensor(smooth_noise_textures(nobj, tex_res, target_seed).reshape(-1),
+                                       device="cuda").to(dtype)
+        init = np.full((nobj, 4, tex_res * tex_res), 0.5)
+        self.init = torch.tensor(init.reshape(-1), device="cuda").to(dtype)
+        self.target_img = self.scene.render(self.target_tex, width, height, target_spp,
+                                            int(load().mg_mix64(target_seed)))
+        self.accum = torch.zeros(2 * n, dtype=torch.int64, device="cuda")
+        self.loss_buf = torch.zeros(1, dtype=torch.float64, device="cuda")
+
+    def dim(self) -> int:
+        return self.scene.params()
+
+    def draws_per_sample(self) -> int:
+        return 3 * self.W * self.H
+
+    def initial_params(self):
+        return self.init.clone()
+
+    def sample_pair(self, now, prev, iteration: int, key: int, rows=None):
+        r0, r1 = rows if rows is not None else (0, self.H)
+        prop, diff = torch.empty_like(now), torch.empty_like(now)
+        check(load().mg_meshscene_sample_pair(
+            self.ctx.h, self.scene.h, _dtype_code(now), self.W, self.H,
+            self.scene.view.ctypes.data_as(C.c_void_p), _p(self.target_img), _p(now.contiguous()),
+            _p(prev.contiguous()), key, iteration, r0, r1, _p(self.accum), _p(prop), _p(diff),
+            _p(self.loss_buf)))
+        return GradientSamplePair(prop, diff)
+
+
+class MeshTextureRun(QuadTextureRun):
+    """configs[3] optimisation loop: sample pair + fused update per
+    iteration; texture values projected to [0, 1] (meta)."""
 
     def __init__(self, problem, optimizer: str = "meta", lr: float = 0.01, seed: int = 0,
                  replicate: int = 0, **kw):

@@ -1,0 +1,916 @@
+// F1 slice 3 (BASELINE.json configs[3]): gradient samples for texture
+// optimisation on a triangle-mesh scene — quad, tessellated sphere and a
+// seeded displaced-sphere mesh, each with its own R x R RGB albedo +
+// roughness texture — path traced to depth 6 with next-event estimation.
+// Scene, estimators and the CPU oracle: DESIGN.md §12 and
+// oracle/metagrad_oracle.c mgo_mesh_* (the reference has no renderer).
+//
+// * BVH: binned-SAH build on the host, nodes relabelled breadth-first so
+//   the top levels are one contiguous block that every CTA stages in shared
+//   memory; boxes are fp32, rounded outwards and padded, so the fp32 slab
+//   test never culls a triangle the fp64 Moller-Trumbore test would hit —
+//   the closest hit (ties -> lower original triangle index) equals the
+//   oracle's brute-force answer bit for bit.
+// * One thread per pixel traces paths A (both parameter sets: shared
+//   geometry, two BSDF evaluations), B and C; sampling is independent of
+//   the parameters.  Path A's per-vertex adjoint data is stored, suffix
+//   radiance accumulated backwards, and every (vertex, parameter)
+//   contribution is added as a 2^-40 fixed-point int64 atomic into the
+//   texture's prop / diff accumulators (order independent, deterministic).
+//   Path B is traced twice (radiance first, then with storage) so that only
+//   one path's vertex data is live at a time.
+#include <math.h>
+#include <stdint.h>
+
+#include <algorithm>
+#include <climits>
+#include <vector>
+
+#include "mg_common.cuh"
+#include "philox.cuh"
+
+struct mg_mesh_scene {
+  int T = 0, nobj = 0, R = 0, nnodes = 0, depth = 0;
+  double* tri = nullptr;   // [T][18] in BVH order
+  int* orig = nullptr;     // [T] original triangle index
+  int* obj = nullptr;      // [T] object id (BVH order)
+  float4* nodes = nullptr; // [2 * nnodes]: (lo.xyz, a) (hi.xyz, b)
+};
+
+namespace mg {
+namespace {
+
+constexpr int kMThreads = 128;
+constexpr int kMaxV = 8;
+constexpr int kRec = 18;
+constexpr int kSmemNodes = 512;  // top BVH levels staged in shared memory (16 KB)
+constexpr double kTMin = 1e-9, kOff = 1e-6;
+constexpr double kPiM = 3.14159265358979323846;
+constexpr double kFixM = 1099511627776.0;  // 2^40
+
+// ------------------------------------------------------------ host BVH
+struct TmpNode {
+  double lo[3], hi[3];
+  int left = -1, right = -1, first = 0, count = 0;
+};
+
+struct Builder {
+  const double* tri;
+  std::vector<double> blo, bhi, cen;  // [T][3]
+  std::vector<int> idx;
+  std::vector<TmpNode> nodes;
+  int max_depth = 0;
+
+  void bounds(int b, int e, double lo[3], double hi[3], bool centroids) const {
+    for (int k = 0; k < 3; ++k) {
+      lo[k] = INFINITY;
+      hi[k] = -INFINITY;
+    }
+    for (int i = b; i < e; ++i) {
+      const int t = idx[size_t(i)];
+      for (int k = 0; k < 3; ++k) {
+        const double l = centroids ? cen[size_t(3 * t + k)] : blo[size_t(3 * t + k)];
+        const double h = centroids ? cen[size_t(3 * t + k)] : bhi[size_t(3 * t + k)];
+        lo[k] = std::min(lo[k], l);
+        hi[k] = std::max(hi[k], h);
+      }
+    }
+  }
+  static double area(const double lo[3], const double hi[3]) {
+    const double x = hi[0] - lo[0], y = hi[1] - lo[1], z = hi[2] - lo[2];
+    return (x < 0 || y < 0 || z < 0) ? 0.0 : 2.0 * (x * y + y * z + z * x);
+  }
+
+  int build(int b, int e, int depth) {
+    max_depth = std::max(max_depth, depth);
+    const int id = int(nodes.size());
+    nodes.emplace_back();
+    TmpNode nd;
+    bounds(b, e, nd.lo, nd.hi, false);
+    const int n = e - b;
+    auto make_leaf = [&]() {
+      nd.first = b;
+      nd.count = n;
+      nodes[size_t(id)] = nd;
+      return id;
+    };
+    if (n <= 4 || depth >= 60) return make_leaf();
+    double clo[3], chi[3];
+    bounds(b, e, clo, chi, true);
+    int axis = 0;
+    for (int k = 1; k < 3; ++k)
+      if (chi[k] - clo[k] > chi[axis] - clo[axis]) axis = k;
+    const double ext = chi[axis] - clo[axis];
+    int mid = -1;
+    if (ext > 0.0) {
+      constexpr int kBins = 16;
+      int cnt[kBins] = {0};
+      double bl[kBins][3], bh[kBins][3];
+      for (int i = 0; i < kBins; ++i)
+        for (int k = 0; k < 3; ++k) {
+          bl[i][k] = INFINITY;
+          bh[i][k] = -INFINITY;
+        }
+      auto bin_of = [&](int t) {
+        int q = int(((cen[size_t(3 * t + axis)] - clo[axis]) / ext) * kBins);
+        return q < 0 ? 0 : (q >= kBins ? kBins - 1 : q);
+      };
+      for (int i = b; i < e; ++i) {
+        const int t = idx[size_t(i)], q = bin_of(t);
+        cnt[q]++;
+        for (int k = 0; k < 3; ++k) {
+          bl[q][k] = std::min(bl[q][k], blo[size_t(3 * t + k)]);
+          bh[q][k] = std::max(bh[q][k], bhi[size_t(3 * t + k)]);
+        }
+      }
+      double best = INFINITY;
+      int best_split = -1;
+      for (int s = 1; s < kBins; ++s) {
+        double l0[3] = {INFINITY, INFINITY, INFINITY}, h0[3] = {-INFINITY, -INFINITY, -INFINITY};
+        double l1[3] = {INFINITY, INFINITY, INFINITY}, h1[3] = {-INFINITY, -INFINITY, -INFINITY};
+        int n0 = 0, n1 = 0;
+        for (int q = 0; q < kBins; ++q) {
+          double* L = q < s ? l0 : l1;
+          double* H = q < s ? h0 : h1;
+          (q < s ? n0 : n1) += cnt[q];
+          for (int k = 0; k < 3; ++k) {
+            L[k] = std::min(L[k], bl[q][k]);
+            H[k] = std::max(H[k], bh[q][k]);
+          }
+        }
+        if (!n0 || !n1) continue;
+        const double c = area(l0, h0) * n0 + area(l1, h1) * n1;
+        if (c < best) {
+          best = c;
+          best_split = s;
+        }
+      }
+      if (best_split > 0) {
+        auto it = std::partition(idx.begin() + b, idx.begin() + e,
+                                 [&](int t) { return bin_of(t) < best_split; });
+        mid = int(it - idx.begin());
+      }
+    }
+    if (mid <= b || mid >= e) {  // degenerate: median split on the axis
+      mid = (b + e) / 2;
+      std::nth_element(idx.begin() + b, idx.begin() + mid, idx.begin() + e, [&](int x, int y) {
+        const double cx = cen[size_t(3 * x + axis)], cy = cen[size_t(3 * y + axis)];
+        return cx < cy || (cx == cy && x < y);
+      });
+    }
+    const int l = build(b, mid, depth + 1);
+    const int r = build(mid, e, depth + 1);
+    nd.left = l;
+    nd.right = r;
+    nodes[size_t(id)] = nd;
+    return id;
+  }
+};
+
+// ------------------------------------------------------------ device
+struct MeshDev {
+  const double* __restrict__ tri;
+  const int* __restrict__ orig;
+  const int* __restrict__ obj;
+  const float4* __restrict__ nodes;
+  int nnodes;
+};
+
+struct MeshK {
+  int W, H, R, nobj;
+  int row0, row1;
+  double view[25];
+  uint64_t key;
+  uint32_t iteration;
+};
+
+__device__ __forceinline__ double dot3d(const double a[3], const double b[3]) {
+  return (a[0] * b[0] + a[1] * b[1]) + a[2] * b[2];
+}
+
+__device__ __forceinline__ void cross3d(const double a[3], const double b[3], double r[3]) {
+  r[0] = a[1] * b[2] - a[2] * b[1];
+  r[1] = a[2] * b[0] - a[0] * b[2];
+  r[2] = a[0] * b[1] - a[1] * b[0];
+}
+
+// Moller-Trumbore in fp64, same operation order as the oracle (ms_tri_hit)
+__device__ __forceinline__ bool tri_hit(const double* __restrict__ r, const double o[3],
+                                        const double d[3], double& t, double& u, double& v) {
+  const double v0[3] = {r[0], r[1], r[2]}, e1[3] = {r[3], r[4], r[5]}, e2[3] = {r[6], r[7], r[8]};
+  double p[3], q[3], s[3];
+  cross3d(d, e2, p);
+  const double det = dot3d(e1, p);
+  if (det == 0.0) return false;
+  const double inv = 1.0 / det;
+  s[0] = o[0] - v0[0];
+  s[1] = o[1] - v0[1];
+  s[2] = o[2] - v0[2];
+  const double uu = dot3d(s, p) * inv;
+  if (uu < 0.0 || uu > 1.0) return false;
+  cross3d(s, e1, q);
+  const double vv = dot3d(d, q) * inv;
+  if (vv < 0.0 || uu + vv > 1.0) return false;
+  const double tt = dot3d(e2, q) * inv;
+  if (!(tt > kTMin)) return false;
+  t = tt;
+  u = uu;
+  v = vv;
+  return true;
+}
+
+__device__ __forceinline__ void load_node(const MeshDev& m, const float4* sn, int i, float4& a,
+                                          float4& b) {
+  if (i < kSmemNodes) {
+    a = sn[2 * i];
+    b = sn[2 * i + 1];
+  } else {
+    a = __ldg(&m.nodes[2 * i]);
+    b = __ldg(&m.nodes[2 * i + 1]);
+  }
+}
+
+__device__ __forceinline__ bool slab(const float4& a, const float4& b, const float o[3],
+                                     const float inv[3], float tmax, float& tnear) {
+  const float tx0 = (a.x - o[0]) * inv[0], tx1 = (b.x - o[0]) * inv[0];
+  const float ty0 = (a.y - o[1]) * inv[1], ty1 = (b.y - o[1]) * inv[1];
+  const float tz0 = (a.z - o[2]) * inv[2], tz1 = (b.z - o[2]) * inv[2];
+  const float tn = fmaxf(fmaxf(fminf(tx0, tx1), fminf(ty0, ty1)), fmaxf(fminf(tz0, tz1), 0.0f));
+  const float tf = fminf(fminf(fmaxf(tx0, tx1), fmaxf(ty0, ty1)), fminf(fmaxf(tz0, tz1), tmax));
+  tnear = tn;
+  return tn <= tf;
+}
+
+// ANY: any hit with t < tmax (shadow rays).  Otherwise the closest hit with
+// t < tmax; ties on t resolve to the lower original triangle index, so the
+// answer is the oracle's brute-force scan.  Returns the BVH slot or -1.
+template <bool ANY>
+__device__ int trace(const MeshDev& m, const float4* sn, const double o[3], const double d[3],
+                     double tmax, double& t_out, double& u_out, double& v_out) {
+  float of[3], inv[3];
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    of[k] = float(o[k]);
+    const float dk = float(d[k]);
+    inv[k] = 1.0f / (fabsf(dk) > 1e-20f ? dk : copysignf(1e-20f, dk));
+  }
+  int stack[64];
+  int sp = 0, node = 0;
+  double best = tmax, bu = 0.0, bv = 0.0;
+  int bslot = -1, bid = INT_MAX;
+  float bestf = __double2float_ru(best);
+  float4 na, nb;
+  load_node(m, sn, 0, na, nb);
+  float tn;
+  if (!slab(na, nb, of, inv, bestf, tn)) return -1;
+  for (;;) {
+    load_node(m, sn, node, na, nb);
+    const int a = __float_as_int(na.w), b = __float_as_int(nb.w);
+    if (b < 0) {  // leaf: triangles [a, a - b)
+      for (int s = a; s < a - b; ++s) {
+        double t, u, v;
+        if (!tri_hit(m.tri + size_t(kRec) * s, o, d, t, u, v) || !(t <= best)) continue;
+        if (ANY) {
+          if (t < tmax) return s;
+          continue;
+        }
+        const int id = __ldg(&m.orig[s]);
+        if (t < best || id < bid) {
+          best = t;
+          bu = u;
+          bv = v;
+          bslot = s;
+          bid = id;
+          bestf = __double2float_ru(best);
+        }
+      }
+    } else {
+      float4 la, lb, ra, rb;
+      load_node(m, sn, a, la, lb);
+      load_node(m, sn, b, ra, rb);
+      float t0, t1;
+      const bool h0 = slab(la, lb, of, inv, bestf, t0);
+      const bool h1 = slab(ra, rb, of, inv, bestf, t1);
+      if (h0 && h1) {
+        const bool first0 = t0 <= t1;
+        stack[sp++] = first0 ? b : a;
+        node = first0 ? a : b;
+        continue;
+      }
+      if (h0) {
+        node = a;
+        continue;
+      }
+      if (h1) {
+        node = b;
+        continue;
+      }
+    }
+    if (sp == 0) break;
+    node = stack[--sp];
+  }
+  t_out = best;
+  u_out = bu;
+  v_out = bv;
+  return bslot;
+}
+
+__device__ __forceinline__ void prng(uint64_t key, uint32_t pix, uint32_t it, uint32_t path,
+                                     uint32_t slot, double u[4]) {
+  const Philox4 r =
+      philox4x32_10(Philox4{{pix, it, path, slot}}, uint32_t(key), uint32_t(key >> 32));
+#pragma unroll
+  for (int k = 0; k < 4; ++k) u[k] = double(r.x[k]) * 0x1.0p-32;
+}
+
+// principled BSDF with metalness 0 (the helix slice's expressions with
+// metal = 0): f_c = base_c / pi + DG F, and dS/drough = dDG/drough F
+template <class T>
+__device__ __forceinline__ void bsdf_m0(const T base[3], T rough, const T n[3], const T wi[3],
+                                        const T wo[3], T f[3], T& dS) {
+  const T alpha = T(0.05) + T(0.95) * (rough * rough);
+  const T a2 = alpha * alpha;
+  T h[3] = {wi[0] + wo[0], wi[1] + wo[1], wi[2] + wo[2]};
+  const T hl = sqrt((h[0] * h[0] + h[1] * h[1]) + h[2] * h[2]);
+  h[0] /= hl;
+  h[1] /= hl;
+  h[2] /= hl;
+  auto dt = [](const T* a, const T* b) { return (a[0] * b[0] + a[1] * b[1]) + a[2] * b[2]; };
+  const T nh = dt(n, h), ni = dt(n, wi), no = dt(n, wo), ih = dt(wi, h);
+  const T den = nh * nh * (a2 - T(1)) + T(1);
+  const T D = a2 / (T(kPiM) * (den * den));
+  const T dD_da2 = (den - T(2) * a2 * (nh * nh)) / (T(kPiM) * ((den * den) * den));
+  const T si = sqrt(a2 + (T(1) - a2) * (ni * ni));
+  const T so = sqrt(a2 + (T(1) - a2) * (no * no));
+  const T G1i = (T(2) * ni) / (ni + si), G1o = (T(2) * no) / (no + so);
+  const T dG1i = ((T(-2) * ni) / ((ni + si) * (ni + si))) * ((T(1) - ni * ni) / (T(2) * si));
+  const T dG1o = ((T(-2) * no) / ((no + so) * (no + so))) * ((T(1) - no * no) / (T(2) * so));
+  const T G = G1i * G1o;
+  const T dG_da2 = dG1i * G1o + G1i * dG1o;
+  const T q = T(1) - ih;
+  const T q5 = ((q * q) * (q * q)) * q;
+  const T denom = T(4) * ni * no;
+  const T DG = (D * G) / denom;
+  const T dDG_drough = (((dD_da2 * G + D * dG_da2) / denom) * (T(2) * alpha)) * (T(1.9) * rough);
+  const T F0 = T(0.04);
+  const T F = F0 + (T(1) - F0) * q5;
+#pragma unroll
+  for (int c = 0; c < 3; ++c) f[c] = base[c] / T(kPiM) + DG * F;
+  dS = dDG_drough * F;
+}
+
+template <class T, int NS>
+struct PathStore {
+  int base[kMaxV];
+  T A[NS][kMaxV][3];
+  T dSn[NS][kMaxV];
+  T invfb[NS][kMaxV][3];
+  T dSb[NS][kMaxV];
+  T C[NS][kMaxV][3];
+};
+
+struct NoStore {};
+
+// One path for NS parameter sets (th[0] = theta_t, th[1] = theta_{t-1});
+// radiance L[s][c], environment after the last vertex E[s][c]; per-vertex
+// adjoint data into *st when STORE.  Returns the number of vertices.
+template <class T, int NS, bool STORE, class Store>
+__device__ int mesh_path(const MeshK& q, const MeshDev& m, const float4* sn, const T* const th[2],
+                         int px, int py, uint32_t it, uint32_t path, T L[NS][3], T E[NS][3],
+                         Store* st) {
+  const double* V = q.view;
+  const int maxv = int(V[24]);
+  const int R2 = q.R * q.R;
+  const uint32_t pix = uint32_t(py * q.W + px);
+  double u[4];
+  prng(q.key, pix, it, path, 0u, u);
+  const double sx = ((double(px) + u[0]) / double(q.W)) * 2.0 - 1.0;
+  const double sy = 1.0 - ((double(py) + u[1]) / double(q.H)) * 2.0;
+  const double ax = sx * (V[12] * (double(q.W) / double(q.H))), ay = sy * V[12];
+  double o[3] = {V[0], V[1], V[2]};
+  double d[3];
+#pragma unroll
+  for (int i = 0; i < 3; ++i) d[i] = (V[3 + i] + ax * V[6 + i]) + ay * V[9 + i];
+  const double dl = sqrt(dot3d(d, d));
+  d[0] /= dl;
+  d[1] /= dl;
+  d[2] /= dl;
+  T beta[NS][3];
+#pragma unroll
+  for (int s = 0; s < NS; ++s)
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      beta[s][c] = T(1);
+      L[s][c] = T(0);
+      E[s][c] = T(0);
+    }
+  const double la = (V[15] - V[14]) * (V[17] - V[16]);
+  int nv = 0;
+  for (int v = 0; v < maxv && v < kMaxV; ++v) {
+    double t = INFINITY, bu, bv;
+    const int slot = trace<false>(m, sn, o, d, INFINITY, t, bu, bv);
+    if (slot < 0) {
+#pragma unroll
+      for (int s = 0; s < NS; ++s)
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+          E[s][c] = beta[s][c] * T(V[21 + c]);
+          L[s][c] += E[s][c];
+        }
+      return nv;
+    }
+    const double* r = m.tri + size_t(kRec) * slot;
+    const double x[3] = {o[0] + t * d[0], o[1] + t * d[1], o[2] + t * d[2]};
+    double n[3] = {r[9], r[10], r[11]};
+    if (dot3d(n, d) > 0.0) {
+      n[0] = -n[0];
+      n[1] = -n[1];
+      n[2] = -n[2];
+    }
+    const double U = (r[12] + bu * r[14]) + bv * r[16];
+    const double W_ = (r[13] + bu * r[15]) + bv * r[17];
+    int tx = int(U * q.R), ty = int(W_ * q.R);
+    tx = tx < 0 ? 0 : (tx > q.R - 1 ? q.R - 1 : tx);
+    ty = ty < 0 ? 0 : (ty > q.R - 1 ? q.R - 1 : ty);
+    const int pbase = __ldg(&m.obj[slot]) * 4 * R2 + ty * q.R + tx;
+    if constexpr (STORE) {
+      st->base[nv] = pbase;
+#pragma unroll
+      for (int s = 0; s < NS; ++s) {
+        st->dSn[s][nv] = T(0);
+        st->dSb[s][nv] = T(0);
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+          st->A[s][nv][c] = T(0);
+          st->invfb[s][nv][c] = T(0);
+          st->C[s][nv][c] = T(0);
+        }
+      }
+    }
+    const int vi = nv;
+    ++nv;
+    T base[NS][3], rough[NS];
+#pragma unroll
+    for (int s = 0; s < NS; ++s) {
+#pragma unroll
+      for (int c = 0; c < 3; ++c) base[s][c] = th[s][pbase + c * R2];
+      rough[s] = th[s][pbase + 3 * R2];
+    }
+    const double wo[3] = {-d[0], -d[1], -d[2]};
+    const double xo[3] = {x[0] + kOff * n[0], x[1] + kOff * n[1], x[2] + kOff * n[2]};
+    prng(q.key, pix, it, path, uint32_t(v * 256 + 1), u);
+    const double lp[3] = {V[14] + u[0] * (V[15] - V[14]), V[13], V[16] + u[1] * (V[17] - V[16])};
+    double w[3] = {lp[0] - x[0], lp[1] - x[1], lp[2] - x[2]};
+    const double d2 = dot3d(w, w);
+    const double wl = sqrt(d2);
+    w[0] /= wl;
+    w[1] /= wl;
+    w[2] /= wl;
+    const double cx = dot3d(n, w), cl = w[1];
+    const T nT[3] = {T(n[0]), T(n[1]), T(n[2])}, woT[3] = {T(wo[0]), T(wo[1]), T(wo[2])};
+    if (cx > 0.0 && cl > 0.0 && dot3d(n, wo) > 0.0) {
+      double ts, tu, tv;
+      if (trace<true>(m, sn, xo, w, wl - kOff, ts, tu, tv) < 0) {
+        const double gl = ((cx * cl) / d2) * la;
+        const T wT[3] = {T(w[0]), T(w[1]), T(w[2])};
+#pragma unroll
+        for (int s = 0; s < NS; ++s) {
+          T f[3], dS;
+          bsdf_m0<T>(base[s], rough[s], nT, wT, woT, f, dS);
+          if constexpr (STORE) st->dSn[s][vi] = dS;
+#pragma unroll
+          for (int c = 0; c < 3; ++c) {
+            const T A = beta[s][c] * T(gl * V[18 + c]);
+            const T Cc = A * f[c];
+            if constexpr (STORE) {
+              st->A[s][vi][c] = A;
+              st->C[s][vi][c] = Cc;
+            }
+            L[s][c] += Cc;
+          }
+        }
+      }
+    }
+    if (v == maxv - 1 || dot3d(n, wo) <= 0.0) return nv;
+    double dx = 0.0, dy = 0.0;
+    bool got = false;
+    for (uint32_t j = 0; !got && j < 64; ++j) {
+      double c4[4];
+      if (j == 0) {
+        c4[0] = u[2];
+        c4[1] = u[3];
+        c4[2] = 2.0;
+        c4[3] = 2.0;
+      } else {
+        prng(q.key, pix, it, path, uint32_t(v * 256 + 1) + j, c4);
+      }
+#pragma unroll
+      for (int mm = 0; mm < 4; mm += 2) {
+        if (got) break;
+        const double a = 2.0 * c4[mm] - 1.0, b = 2.0 * c4[mm + 1] - 1.0;
+        if (c4[mm] <= 1.0 && a * a + b * b < 1.0) {
+          dx = a;
+          dy = b;
+          got = true;
+        }
+      }
+    }
+    const double dz = sqrt(fmax(0.0, 1.0 - (dx * dx + dy * dy)));
+    if (dz <= 0.0) return nv;
+    // Duff et al. orthonormal basis (oracle hx_onb)
+    const double sign = copysign(1.0, n[2]);
+    const double aa = -1.0 / (sign + n[2]);
+    const double bb = n[0] * n[1] * aa;
+    const double Tb[3] = {1.0 + sign * (n[0] * n[0]) * aa, sign * bb, -sign * n[0]};
+    const double Bb[3] = {bb, sign + (n[1] * n[1]) * aa, -n[1]};
+    const double wi[3] = {(dx * Tb[0] + dy * Bb[0]) + dz * n[0],
+                          (dx * Tb[1] + dy * Bb[1]) + dz * n[1],
+                          (dx * Tb[2] + dy * Bb[2]) + dz * n[2]};
+    const T wiT[3] = {T(wi[0]), T(wi[1]), T(wi[2])};
+#pragma unroll
+    for (int s = 0; s < NS; ++s) {
+      T f[3], dS;
+      bsdf_m0<T>(base[s], rough[s], nT, wiT, woT, f, dS);
+      if constexpr (STORE) st->dSb[s][vi] = dS;
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        if constexpr (STORE) st->invfb[s][vi][c] = f[c] != T(0) ? T(1) / f[c] : T(0);
+        beta[s][c] = beta[s][c] * (f[c] * T(kPiM));
+      }
+    }
+    o[0] = xo[0];
+    o[1] = xo[1];
+    o[2] = xo[2];
+    d[0] = wi[0];
+    d[1] = wi[1];
+    d[2] = wi[2];
+  }
+  return nv;
+}
+
+__device__ __forceinline__ unsigned long long fixq(double v) {
+  return (unsigned long long)llrint(v * kFixM);
+}
+
+// adjoint of a stored path, set s, channel weights w (oracle ms_scatter)
+template <class T, int NS>
+__device__ void scatter(const PathStore<T, NS>& st, int nv, const T E[3], int s, const T w[3],
+                        int R2, unsigned long long* __restrict__ acc) {
+  T Q[3] = {E[0], E[1], E[2]};
+  for (int v = nv - 1; v >= 0; --v) {
+    T gr = T(0);
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      const T gb = w[c] * ((st.A[s][v][c] / T(kPiM)) + Q[c] * (st.invfb[s][v][c] / T(kPiM)));
+      atomicAdd(&acc[st.base[v] + c * R2], fixq(double(gb)));
+      gr += w[c] * (st.A[s][v][c] * st.dSn[s][v] + Q[c] * (st.invfb[s][v][c] * st.dSb[s][v]));
+    }
+    atomicAdd(&acc[st.base[v] + 3 * R2], fixq(double(gr)));
+#pragma unroll
+    for (int c = 0; c < 3; ++c) Q[c] = Q[c] + st.C[s][v][c];
+  }
+}
+
+__device__ __forceinline__ void stage_nodes(const MeshDev& m, float4* sn) {
+  const int n = 2 * (m.nnodes < kSmemNodes ? m.nnodes : kSmemNodes);
+  for (int i = threadIdx.x; i < n; i += blockDim.x) sn[i] = m.nodes[i];
+  __syncthreads();
+}
+
+template <class T>
+__global__ void __launch_bounds__(kMThreads)
+    mesh_render_kernel(MeshK q, MeshDev m, int spp, const T* __restrict__ theta,
+                       T* __restrict__ img) {
+  __shared__ float4 sn[2 * kSmemNodes];
+  stage_nodes(m, sn);
+  const int npix = q.W * q.H;
+  const T* th[2] = {theta, theta};
+  for (int pix = blockIdx.x * kMThreads + threadIdx.x; pix < npix; pix += gridDim.x * kMThreads) {
+    const int px = pix % q.W, py = pix / q.W;
+    double acc[3] = {0.0, 0.0, 0.0};
+    for (int s = 0; s < spp; ++s) {
+      T L[1][3], E[1][3];
+      mesh_path<T, 1, false, NoStore>(q, m, sn, th, px, py, 0xffffffffu, uint32_t(s), L, E,
+                                      nullptr);
+#pragma unroll
+      for (int c = 0; c < 3; ++c) acc[c] += double(L[0][c]);
+    }
+#pragma unroll
+    for (int c = 0; c < 3; ++c) img[size_t(c) * npix + pix] = T(acc[c] / double(spp));
+  }
+}
+
+template <class T>
+__global__ void __launch_bounds__(kMThreads)
+    mesh_pair_kernel(MeshK q, MeshDev m, const T* __restrict__ target_img,
+                     const T* __restrict__ now, const T* __restrict__ prev,
+                     unsigned long long* __restrict__ acc, long long np,
+                     ReducePartials* partials, unsigned int* counter, double* loss_out) {
+  __shared__ float4 sn[2 * kSmemNodes];
+  stage_nodes(m, sn);
+  const int npix = q.W * q.H;
+  const int R2 = q.R * q.R;
+  const T* th[2] = {now, prev};
+  const int pix0 = q.row0 * q.W, pix1 = q.row1 * q.W;
+  double loss = 0.0;
+  for (int pix = pix0 + blockIdx.x * kMThreads + threadIdx.x; pix < pix1;
+       pix += gridDim.x * kMThreads) {
+    const int px = pix % q.W, py = pix / q.W;
+    T LB[1][3], EB[1][3], LC[2][3], EC[2][3], LA[2][3], EA[2][3];
+    mesh_path<T, 1, false, NoStore>(q, m, sn, th, px, py, q.iteration, 1u, LB, EB, nullptr);
+    mesh_path<T, 2, false, NoStore>(q, m, sn, th, px, py, q.iteration, 2u, LC, EC, nullptr);
+    T rA[3], rB[3], wC0[3], wC1[3];
+    {
+      PathStore<T, 2> st;
+      const int na =
+          mesh_path<T, 2, true>(q, m, sn, th, px, py, q.iteration, 0u, LA, EA, &st);
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        const T Is = target_img[size_t(c) * npix + pix];
+        rA[c] = LA[0][c] - Is;
+        rB[c] = LB[0][c] - Is;
+        wC0[c] = T(2) * (LC[0][c] - Is);
+        wC1[c] = T(-2) * (LC[1][c] - Is);
+        loss += double(rA[c] * rB[c]);
+      }
+      scatter<T, 2>(st, na, EA[0], 0, rB, R2, acc);
+      scatter<T, 2>(st, na, EA[0], 0, wC0, R2, acc + np);
+      scatter<T, 2>(st, na, EA[1], 1, wC1, R2, acc + np);
+    }
+    {
+      PathStore<T, 1> st;
+      const int nb =
+          mesh_path<T, 1, true>(q, m, sn, th, px, py, q.iteration, 1u, LB, EB, &st);
+      scatter<T, 1>(st, nb, EB[0], 0, rA, R2, acc);
+    }
+  }
+  Acc a;
+  a.ssn = loss;
+  grid_reduce4<kMThreads>(a.partials(), partials, counter,
+                          [&](const ReducePartials& t) { *loss_out = t.ssn; });
+}
+
+template <class T>
+__global__ void mesh_finalize_kernel(long long n, unsigned long long* __restrict__ acc,
+                                     T* __restrict__ prop, T* __restrict__ diff) {
+  for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < n;
+       k += (long long)gridDim.x * blockDim.x) {
+    prop[k] = T(double((long long)acc[k]) / kFixM);
+    diff[k] = T(double((long long)acc[n + k]) / kFixM);
+    acc[k] = 0ull;
+    acc[n + k] = 0ull;
+  }
+}
+
+__global__ void mesh_intersect_kernel(MeshDev m, int n, const double* __restrict__ rays,
+                                      double* __restrict__ t_out, int* __restrict__ tri_out) {
+  __shared__ float4 sn[2 * kSmemNodes];
+  stage_nodes(m, sn);
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const double o[3] = {rays[6 * i], rays[6 * i + 1], rays[6 * i + 2]};
+    const double d[3] = {rays[6 * i + 3], rays[6 * i + 4], rays[6 * i + 5]};
+    double t = INFINITY, u, v;
+    const int s = trace<false>(m, sn, o, d, INFINITY, t, u, v);
+    t_out[i] = s < 0 ? INFINITY : t;
+    tri_out[i] = s < 0 ? -1 : m.orig[s];
+  }
+}
+
+MeshDev dev_of(const mg_mesh_scene* s) {
+  MeshDev m;
+  m.tri = s->tri;
+  m.orig = s->orig;
+  m.obj = s->obj;
+  m.nodes = s->nodes;
+  m.nnodes = s->nnodes;
+  return m;
+}
+
+MeshK make_k(const mg_mesh_scene* s, int W, int H, const double* view, uint64_t key,
+             uint32_t it) {
+  MeshK q;
+  q.W = W;
+  q.H = H;
+  q.R = s->R;
+  q.nobj = s->nobj;
+  q.row0 = 0;
+  q.row1 = H;
+  for (int i = 0; i < 25; ++i) q.view[i] = view[i];
+  q.key = key;
+  q.iteration = it;
+  return q;
+}
+
+}  // namespace
+}  // namespace mg
+
+using namespace mg;
+
+extern "C" {
+
+int mg_meshscene_create(mg_ctx* ctx, int32_t tri_count, const double* tri, const int32_t* obj,
+                        int32_t nobj, int32_t tex_res, mg_mesh_scene** out) {
+  if (!ctx || !tri || !obj || !out) return fail(MG_EINVAL, "mg_meshscene_create: null argument");
+  if (tri_count < 1 || nobj < 1 || tex_res < 1)
+    return fail(MG_EINVAL, "mg_meshscene_create: bad sizes");
+  if (int64_t(nobj) * 4 * tex_res * tex_res > 0x7fffffffLL)
+    return fail(MG_EINVAL, "mg_meshscene_create: parameter count exceeds 2^31");
+  for (int k = 0; k < tri_count; ++k)
+    if (obj[k] < 0 || obj[k] >= nobj) return fail(MG_EINVAL, "mg_meshscene_create: bad object id");
+  Builder B;
+  B.tri = tri;
+  const size_t T = size_t(tri_count);
+  B.blo.resize(3 * T);
+  B.bhi.resize(3 * T);
+  B.cen.resize(3 * T);
+  B.idx.resize(T);
+  double slo[3] = {INFINITY, INFINITY, INFINITY}, shi[3] = {-INFINITY, -INFINITY, -INFINITY};
+  for (size_t k = 0; k < T; ++k) {
+    const double* r = tri + kRec * k;
+    for (int a = 0; a < 3; ++a) {
+      const double p0 = r[a], p1 = r[a] + r[3 + a], p2 = r[a] + r[6 + a];
+      const double lo = std::min(p0, std::min(p1, p2)), hi = std::max(p0, std::max(p1, p2));
+      B.blo[3 * k + a] = lo;
+      B.bhi[3 * k + a] = hi;
+      B.cen[3 * k + a] = 0.5 * (lo + hi);
+      slo[a] = std::min(slo[a], lo);
+      shi[a] = std::max(shi[a], hi);
+    }
+    B.idx[k] = int(k);
+  }
+  B.nodes.reserve(2 * T);
+  B.build(0, tri_count, 0);
+  // breadth-first relabelling: the top levels become nodes [0, kSmemNodes)
+  const int nn = int(B.nodes.size());
+  std::vector<int> order, label(size_t(nn), -1);
+  order.reserve(size_t(nn));
+  order.push_back(0);
+  label[0] = 0;
+  for (size_t h = 0; h < order.size(); ++h) {
+    const TmpNode& nd = B.nodes[size_t(order[h])];
+    if (nd.left >= 0) {
+      label[size_t(nd.left)] = int(order.size());
+      order.push_back(nd.left);
+      label[size_t(nd.right)] = int(order.size());
+      order.push_back(nd.right);
+    }
+  }
+  const double diag = sqrt((shi[0] - slo[0]) * (shi[0] - slo[0]) +
+                           (shi[1] - slo[1]) * (shi[1] - slo[1]) +
+                           (shi[2] - slo[2]) * (shi[2] - slo[2]));
+  const float pad = float(1e-5 * diag + 1e-7);
+  std::vector<float4> nodes(2 * size_t(nn));
+  for (int i = 0; i < nn; ++i) {
+    const TmpNode& nd = B.nodes[size_t(order[size_t(i)])];
+    float lo[3], hi[3];
+    for (int a = 0; a < 3; ++a) {
+      lo[a] = nextafterf(float(nd.lo[a]), -INFINITY) - pad;
+      hi[a] = nextafterf(float(nd.hi[a]), INFINITY) + pad;
+    }
+    const int a = nd.left >= 0 ? label[size_t(nd.left)] : nd.first;
+    const int b = nd.left >= 0 ? label[size_t(nd.right)] : -nd.count;
+    int ai, bi;
+    memcpy(&ai, &a, 4);
+    memcpy(&bi, &b, 4);
+    float af, bf;
+    memcpy(&af, &ai, 4);
+    memcpy(&bf, &bi, 4);
+    nodes[2 * size_t(i)] = make_float4(lo[0], lo[1], lo[2], af);
+    nodes[2 * size_t(i) + 1] = make_float4(hi[0], hi[1], hi[2], bf);
+  }
+  std::vector<double> stri(kRec * T);
+  std::vector<int> sorig(T), sobj(T);
+  for (size_t s = 0; s < T; ++s) {
+    const int k = B.idx[s];
+    memcpy(&stri[kRec * s], tri + kRec * size_t(k), sizeof(double) * kRec);
+    sorig[s] = k;
+    sobj[s] = obj[k];
+  }
+  mg_mesh_scene* sc = new mg_mesh_scene();
+  sc->T = tri_count;
+  sc->nobj = nobj;
+  sc->R = tex_res;
+  sc->nnodes = nn;
+  sc->depth = B.max_depth;
+  cudaError_t e = cudaMalloc(&sc->tri, sizeof(double) * stri.size());
+  if (e == cudaSuccess) e = cudaMalloc(&sc->orig, sizeof(int) * T);
+  if (e == cudaSuccess) e = cudaMalloc(&sc->obj, sizeof(int) * T);
+  if (e == cudaSuccess) e = cudaMalloc(&sc->nodes, sizeof(float4) * nodes.size());
+  if (e == cudaSuccess)
+    e = cudaMemcpy(sc->tri, stri.data(), sizeof(double) * stri.size(), cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = cudaMemcpy(sc->orig, sorig.data(), sizeof(int) * T, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = cudaMemcpy(sc->obj, sobj.data(), sizeof(int) * T, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess)
+    e = cudaMemcpy(sc->nodes, nodes.data(), sizeof(float4) * nodes.size(), cudaMemcpyHostToDevice);
+  if (e != cudaSuccess) {
+    cudaFree(sc->tri);
+    cudaFree(sc->orig);
+    cudaFree(sc->obj);
+    cudaFree(sc->nodes);
+    delete sc;
+    return cuda_fail(e, "mg_meshscene_create");
+  }
+  *out = sc;
+  return MG_OK;
+}
+
+int mg_meshscene_destroy(mg_mesh_scene* s) {
+  if (!s) return MG_OK;
+  cudaFree(s->tri);
+  cudaFree(s->orig);
+  cudaFree(s->obj);
+  cudaFree(s->nodes);
+  delete s;
+  return MG_OK;
+}
+
+int mg_meshscene_info(const mg_mesh_scene* s, int32_t* nodes, int32_t* depth, int64_t* params) {
+  if (!s) return fail(MG_EINVAL, "mg_meshscene_info: null scene");
+  if (nodes) *nodes = s->nnodes;
+  if (depth) *depth = s->depth;
+  if (params) *params = int64_t(s->nobj) * 4 * s->R * s->R;
+  return MG_OK;
+}
+
+int mg_meshscene_intersect(mg_ctx* ctx, const mg_mesh_scene* s, int32_t n, const double* rays,
+                           double* t_out, int32_t* tri_out) {
+  if (!ctx || !s || (n > 0 && (!rays || !t_out || !tri_out)))
+    return fail(MG_EINVAL, "mg_meshscene_intersect: null argument");
+  if (n <= 0) return MG_OK;
+  const int grid = grid_for(ctx, n, kMThreads, 8);
+  mesh_intersect_kernel<<<grid, kMThreads, 0, ctx->stream>>>(dev_of(s), n, rays, t_out, tri_out);
+  MG_LAUNCH_CHECK(ctx);
+  return MG_OK;
+}
+
+static int check_view(const double* view) {
+  if (!view) return fail(MG_EINVAL, "mesh scene: null view");
+  const int maxv = int(view[24]);
+  if (maxv < 1 || maxv > kMaxV) return fail(MG_EINVAL, "mesh scene: max_vertices must lie in [1, 8]");
+  return MG_OK;
+}
+
+int mg_meshscene_render(mg_ctx* ctx, const mg_mesh_scene* s, int32_t dtype, int32_t W, int32_t H,
+                        const double* view, int32_t spp, uint64_t key, const void* theta,
+                        void* img) {
+  if (!ctx || !s || !theta || !img) return fail(MG_EINVAL, "mg_meshscene_render: null argument");
+  if (W < 1 || H < 1 || spp < 1) return fail(MG_EINVAL, "mg_meshscene_render: bad sizes");
+  int st = check_view(view);
+  if (st) return st;
+  const MeshK q = make_k(s, W, H, view, key, 0xffffffffu);
+  const int grid = grid_for(ctx, int64_t(W) * H, kMThreads, 4);
+  if (dtype == MG_F64)
+    mesh_render_kernel<double><<<grid, kMThreads, 0, ctx->stream>>>(q, dev_of(s), spp,
+                                                                    (const double*)theta,
+                                                                    (double*)img);
+  else if (dtype == MG_F32)
+    mesh_render_kernel<float><<<grid, kMThreads, 0, ctx->stream>>>(q, dev_of(s), spp,
+                                                                   (const float*)theta,
+                                                                   (float*)img);
+  else
+    return fail(MG_EINVAL, "mg_meshscene_render: unknown dtype");
+  MG_LAUNCH_CHECK(ctx);
+  return MG_OK;
+}
+
+int mg_meshscene_sample_pair(mg_ctx* ctx, const mg_mesh_scene* s, int32_t dtype, int32_t W,
+                             int32_t H, const double* view, const void* target_img,
+                             const void* now, const void* prev, uint64_t key, uint32_t iteration,
+                             int32_t row0, int32_t row1, void* accum, void* prop, void* diff,
+                             double* loss_out) {
+  if (!ctx || !s || !target_img || !now || !prev || !accum || !prop || !diff || !loss_out)
+    return fail(MG_EINVAL, "mg_meshscene_sample_pair: null argument");
+  if (W < 1 || H < 1) return fail(MG_EINVAL, "mg_meshscene_sample_pair: bad sizes");
+  if (row0 < 0 || row1 > H || row0 > row1)
+    return fail(MG_EINVAL, "mg_meshscene_sample_pair: bad rows");
+  int st = check_view(view);
+  if (st) return st;
+  MeshK q = make_k(s, W, H, view, key, iteration);
+  q.row0 = row0;
+  q.row1 = row1;
+  const long long np = (long long)s->nobj * 4 * s->R * s->R;
+  const int grid = grid_for(ctx, int64_t(W) * (row1 - row0) + 1, kMThreads, 4);
+  unsigned long long* acc = (unsigned long long*)accum;
+  if (dtype == MG_F64)
+    mesh_pair_kernel<double><<<grid, kMThreads, 0, ctx->stream>>>(
+        q, dev_of(s), (const double*)target_img, (const double*)now, (const double*)prev, acc, np,
+        ctx->partials, ctx->counter, loss_out);
+  else if (dtype == MG_F32)
+    mesh_pair_kernel<float><<<grid, kMThreads, 0, ctx->stream>>>(
+        q, dev_of(s), (const float*)target_img, (const float*)now, (const float*)prev, acc, np,
+        ctx->partials, ctx->counter, loss_out);
+  else
+    return fail(MG_EINVAL, "mg_meshscene_sample_pair: unknown dtype");
+  MG_LAUNCH_CHECK(ctx);
+  const int fgrid = grid_for(ctx, np, 256, 8);
+  if (dtype == MG_F64)
+    mesh_finalize_kernel<double><<<fgrid, 256, 0, ctx->stream>>>(np, acc, (double*)prop,
+                                                                 (double*)diff);
+  else
+    mesh_finalize_kernel<float><<<fgrid, 256, 0, ctx->stream>>>(np, acc, (float*)prop,
+                                                                (float*)diff);
+  MG_LAUNCH_CHECK(ctx);
+  return MG_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,150 @@
+"""F1 slice 3 (configs[3], textured triangle-mesh scene) on the B200 against
+the CPU oracle (mgo_mesh_*): BVH closest hits equal brute force; renders
+and gradient sample pairs bit-exact in fp64; fp32 within tolerance; image
+tiles sum exactly; the optimisation fits the target textures."""
+import numpy as np
+import pytest
+import torch
+
+from oracle_bind import Oracle
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def api():
+    from paper_2309_15676_b200 import api
+    return api
+
+
+@pytest.fixture(scope="module")
+def oracle():
+    return Oracle()
+
+
+def _rays(n, seed):
+    rs = np.random.RandomState(seed)
+    o = np.stack([rs.uniform(-2, 2, n), rs.uniform(0.05, 2.5, n), rs.uniform(-2, 3, n)], 1)
+    d = rs.standard_normal((n, 3))
+    d /= np.linalg.norm(d, axis=1, keepdims=True)
+    # half of the rays aimed at the objects
+    tgt = np.stack([rs.uniform(-1.4, 1.4, n), rs.uniform(0.0, 1.1, n), rs.uniform(-0.5, 0.6, n)], 1)
+    aim = tgt - o
+    aim /= np.linalg.norm(aim, axis=1, keepdims=True)
+    d[: n // 2] = aim[: n // 2]
+    return np.concatenate([o, d], 1)
+
+
+@pytest.mark.parametrize("res", [((6, 8), (8, 10)), ((24, 48), (100, 100))])
+def test_bvh_closest_hit_equals_brute_force(api, oracle, res):
+    rec, obj, nobj = api.mesh_scene_geometry(*res)
+    sc = api.MeshScene(rec, obj, nobj, 4, api.mesh_scene_view())
+    info = sc.info()
+    assert info["triangles"] == rec.shape[0] and info["nodes"] >= 1
+    n = 1500
+    rays = _rays(n, 3)
+    t, k = sc.intersect(torch.tensor(rays, device="cuda"))
+    t, k = t.cpu().numpy(), k.cpu().numpy()
+    hits = 0
+    for i in range(n):
+        kk, tt = oracle.mesh_closest_hit(rec, rays[i, :3], rays[i, 3:])
+        assert kk == k[i], (i, kk, k[i])
+        if kk >= 0:
+            hits += 1
+            assert tt == t[i]
+        else:
+            assert np.isinf(t[i])
+    assert hits > n // 3
+
+
+def _small(api, R=4, maxv=4):
+    rec, obj, nobj = api.mesh_scene_geometry((6, 8), (8, 10))
+    view = api.mesh_scene_view(max_vertices=maxv)
+    return rec, obj, nobj, view, api.MeshScene(rec, obj, nobj, R, view)
+
+
+def test_render_bit_exact_vs_oracle(api, oracle):
+    R = 4
+    rec, obj, nobj, view, sc = _small(api, R)
+    rs = np.random.RandomState(0)
+    theta = rs.uniform(0.1, 0.9, nobj * 4 * R * R)
+    W, H = 12, 9
+    img = sc.render(torch.tensor(theta, device="cuda"), W, H, 3, 99).cpu().numpy()
+    want = oracle.mesh_render(W, H, rec, obj, R, view, theta, 3, 99)
+    assert np.array_equal(img, want)
+
+
+@pytest.mark.parametrize("maxv", [1, 4, 6])
+def test_sample_pair_bit_exact_vs_oracle(api, oracle, maxv):
+    R = 4
+    rec, obj, nobj, view, sc = _small(api, R, maxv)
+    n = nobj * 4 * R * R
+    rs = np.random.RandomState(maxv)
+    now = rs.uniform(0.1, 0.9, n)
+    prev = np.clip(now + rs.uniform(-0.02, 0.02, n), 0, 1)
+    W, H = 10, 8
+    target = rs.uniform(0.0, 0.6, 3 * W * H)
+    prob_accum = torch.zeros(2 * n, dtype=torch.int64, device="cuda")
+    prop = torch.empty(n, dtype=torch.float64, device="cuda")
+    diff = torch.empty_like(prop)
+    loss = torch.zeros(1, dtype=torch.float64, device="cuda")
+    import ctypes as C
+    from paper_2309_15676_b200._lib import check, load
+    from paper_2309_15676_b200.api import _p
+    tgt = torch.tensor(target, device="cuda")
+    tn, tp = torch.tensor(now, device="cuda"), torch.tensor(prev, device="cuda")
+    check(load().mg_meshscene_sample_pair(sc.ctx.h, sc.h, 1, W, H,
+                                          sc.view.ctypes.data_as(C.c_void_p), _p(tgt), _p(tn),
+                                          _p(tp), 1234, 7, 0, H, _p(prob_accum), _p(prop),
+                                          _p(diff), _p(loss)))
+    wp, wd, wl = oracle.mesh_sample_pair(W, H, rec, obj, nobj, R, view, target, now, prev, 1234, 7)
+    assert np.array_equal(prop.cpu().numpy(), wp)
+    assert np.array_equal(diff.cpu().numpy(), wd)
+    assert abs(float(loss[0]) - wl) <= 1e-12 * max(1.0, abs(wl))
+    assert int(torch.count_nonzero(prob_accum)) == 0   # scratch left zeroed
+    assert np.count_nonzero(wp) > 10
+
+
+def test_problem_tiles_sum_exactly_and_f32_tracks_f64(api):
+    prob = api.MeshTextureProblem(24, 20, 8, (8, 12), (12, 16), max_vertices=5, target_spp=4,
+                                  dtype=torch.float64)
+    n = prob.dim()
+    rs = np.random.RandomState(2)
+    now = torch.tensor(rs.uniform(0.2, 0.8, n), device="cuda")
+    prev = (now - 0.01).clamp(0, 1)
+    full = prob.sample_pair(now, prev, 3, key=11)
+    full = (full.prop.clone(), full.diff.clone())
+    sp, sd = torch.zeros_like(now), torch.zeros_like(now)
+    from paper_2309_15676_b200.dist import tile_rows
+    for r in range(3):
+        part = prob.sample_pair(now, prev, 3, key=11, rows=tile_rows(prob.H, r, 3))
+        sp += part.prop
+        sd += part.diff
+    assert torch.equal(sp, full[0]) and torch.equal(sd, full[1])
+    # fp32 evaluation of the same pair (geometry stays fp64): relative to the
+    # gradient scale, and the fraction of parameters that differ noticeably
+    prob32 = api.MeshTextureProblem(24, 20, 8, (8, 12), (12, 16), max_vertices=5, target_spp=4,
+                                    dtype=torch.float32)
+    prob32.target_img = prob.target_img.float()
+    p32 = prob32.sample_pair(now.float(), prev.float(), 3, key=11)
+    scale = float(full[0].abs().max())
+    err = (p32.prop.double() - full[0]).abs()
+    assert float(err.max()) <= 1e-3 * scale
+    assert float((err > 1e-5 * scale).double().mean()) < 0.01
+
+
+def test_texture_optimisation_fits_the_image(api):
+    """The image loss (unbiased per-iteration estimate sum r_A r_B, averaged
+    over iterations) falls by > 5x within 200 meta iterations.  (Texel
+    errors are not a good measure here: texels seen only through indirect
+    bounces, and roughness under diffuse-dominated shading, are weakly
+    identifiable, so normalised steps let them wander while the image fits.)"""
+    prob = api.MeshTextureProblem(48, 40, 16, (12, 24), (24, 32), max_vertices=4, target_spp=16,
+                                  dtype=torch.float32)
+    run = api.MeshTextureRun(prob, "meta", lr=0.005)
+    losses = []
+    for i in range(200):
+        run.step()
+        losses.append(run.loss_estimate())
+    first, last = float(np.mean(losses[:3])), float(np.mean(losses[-40:]))
+    assert last < 0.2 * first, (first, last)
