@@ -435,6 +435,47 @@ def extras(args, ctx):
         out[f"helix_256px_{dtn}"] = {"ms_per_iteration": ms, "iterations_per_s": 1e3 / ms,
                                      "paths_per_s": hprob.draws_per_sample() / (ms / 1e3)}
         del hprob, hrun
+    # F1 slice 3, BASELINE configs[3]: 512x512 image of the 3-object mesh
+    # scene (22k triangles, BVH), 3 x 512^2 RGB+roughness textures (3.1M
+    # parameters), depth 6 with NEE, 1 FD + 2 prop spp; sample pair + update
+    mprob = api.MeshTextureProblem(512, 512, 512, max_vertices=6, target_spp=4,
+                                   dtype=torch.float32, ctx=ctx)
+    mrun = api.MeshTextureRun(mprob, optimizer="meta", lr=0.005)
+    for _ in range(2):
+        mrun.step()
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record(ctx.stream)
+    for _ in range(5):
+        mrun.step()
+    b.record(ctx.stream)
+    torch.cuda.synchronize()
+    ms = a.elapsed_time(b) / 5
+    out["mesh_texture_512px_f32"] = {"ms_per_iteration": ms, "iterations_per_s": 1e3 / ms,
+                                     "paths_per_s": mprob.draws_per_sample() / (ms / 1e3),
+                                     "texture_params": mprob.dim(), **mprob.scene.info()}
+    # BVH closest-hit throughput on the same scene (random rays at the objects)
+    nr = 1 << 22
+    g = torch.Generator(device="cuda").manual_seed(0)
+    org = torch.stack([torch.rand(nr, device="cuda", generator=g, dtype=torch.float64) * 4 - 2,
+                       torch.rand(nr, device="cuda", generator=g, dtype=torch.float64) * 2 + 0.1,
+                       torch.full((nr,), 4.0, device="cuda", dtype=torch.float64)], 1)
+    tgt = torch.stack([torch.rand(nr, device="cuda", generator=g, dtype=torch.float64) * 3 - 1.5,
+                       torch.rand(nr, device="cuda", generator=g, dtype=torch.float64) * 1.1,
+                       torch.zeros(nr, device="cuda", dtype=torch.float64)], 1)
+    dirs = tgt - org
+    dirs /= torch.linalg.vector_norm(dirs, dim=1, keepdim=True)
+    rays = torch.cat([org, dirs], 1).contiguous()
+    mprob.scene.intersect(rays)
+    torch.cuda.synchronize()
+    a.record(ctx.stream)
+    mprob.scene.intersect(rays)
+    b.record(ctx.stream)
+    torch.cuda.synchronize()
+    out["mesh_bvh_closest_hit"] = {"rays": nr, "ms": a.elapsed_time(b),
+                                   "rays_per_s": nr / (a.elapsed_time(b) / 1e3)}
+    del mprob, mrun, rays, org, tgt, dirs
+    torch.cuda.empty_cache()
     # mini-render stand-in for configs[0] (P=4096, spp=2, 200 iterations)
     cfg = api.ExperimentConfig(problem="mini-render", pixel_count=4096, spp=2, iterations=200,
                                seed=0, problem_seed=1, lr=0.01, replicates=148)
