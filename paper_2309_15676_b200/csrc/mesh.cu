@@ -35,6 +35,7 @@ struct mg_mesh_scene {
   int* orig = nullptr;     // [T] original triangle index
   int* obj = nullptr;      // [T] object id (BVH order)
   float4* nodes = nullptr; // [2 * nnodes]: (lo.xyz, a) (hi.xyz, b)
+  unsigned int* work = nullptr;  // pixel work counter of the pair kernel
 };
 
 namespace mg {
@@ -245,7 +246,7 @@ __device__ __forceinline__ bool slab(const float4& a, const float4& b, const flo
 // t < tmax; ties on t resolve to the lower original triangle index, so the
 // answer is the oracle's brute-force scan.  Returns the BVH slot or -1.
 template <bool ANY>
-__device__ int trace(const MeshDev& m, const float4* sn, const double o[3], const double d[3],
+__device__ __noinline__ int trace(const MeshDev& m, const float4* sn, const double o[3], const double d[3],
                      double tmax, double& t_out, double& u_out, double& v_out) {
   float of[3], inv[3];
 #pragma unroll
@@ -375,7 +376,7 @@ struct NoStore {};
 // radiance L[s][c], environment after the last vertex E[s][c]; per-vertex
 // adjoint data into *st when STORE.  Returns the number of vertices.
 template <class T, int NS, bool STORE, class Store>
-__device__ int mesh_path(const MeshK& q, const MeshDev& m, const float4* sn, const T* const th[2],
+__device__ __noinline__ int mesh_path(const MeshK& q, const MeshDev& m, const float4* sn, const T* const th[2],
                          int px, int py, uint32_t it, uint32_t path, T L[NS][3], T E[NS][3],
                          Store* st) {
   const double* V = q.view;
@@ -554,7 +555,7 @@ __device__ __forceinline__ unsigned long long fixq(double v) {
 
 // adjoint of a stored path, set s, channel weights w (oracle ms_scatter)
 template <class T, int NS>
-__device__ void scatter(const PathStore<T, NS>& st, int nv, const T E[3], int s, const T w[3],
+__device__ __noinline__ void scatter(const PathStore<T, NS>& st, int nv, const T E[3], int s, const T w[3],
                         int R2, unsigned long long* __restrict__ acc) {
   T Q[3] = {E[0], E[1], E[2]};
   for (int v = nv - 1; v >= 0; --v) {
@@ -600,11 +601,20 @@ __global__ void __launch_bounds__(kMThreads)
   }
 }
 
+// Pixels are handed out 32 at a time from a global counter (one atomic
+// per warp), so warps that drew short paths take more pixels and the CTAs
+// finish together (the path length varies 1..maxv per pixel).
+__device__ __forceinline__ int next_pixels(unsigned int* work) {
+  int base = 0;
+  if ((threadIdx.x & 31) == 0) base = int(atomicAdd(work, 32u));
+  return __shfl_sync(0xffffffffu, base, 0);
+}
+
 template <class T>
 __global__ void __launch_bounds__(kMThreads)
     mesh_pair_kernel(MeshK q, MeshDev m, const T* __restrict__ target_img,
                      const T* __restrict__ now, const T* __restrict__ prev,
-                     unsigned long long* __restrict__ acc, long long np,
+                     unsigned long long* __restrict__ acc, long long np, unsigned int* work,
                      ReducePartials* partials, unsigned int* counter, double* loss_out) {
   __shared__ float4 sn[2 * kSmemNodes];
   stage_nodes(m, sn);
@@ -613,8 +623,9 @@ __global__ void __launch_bounds__(kMThreads)
   const T* th[2] = {now, prev};
   const int pix0 = q.row0 * q.W, pix1 = q.row1 * q.W;
   double loss = 0.0;
-  for (int pix = pix0 + blockIdx.x * kMThreads + threadIdx.x; pix < pix1;
-       pix += gridDim.x * kMThreads) {
+  for (int wbase = next_pixels(work); pix0 + wbase < pix1; wbase = next_pixels(work)) {
+    const int pix = pix0 + wbase + int(threadIdx.x & 31);
+    if (pix >= pix1) continue;
     const int px = pix % q.W, py = pix / q.W;
     T LB[1][3], EB[1][3], LC[2][3], EC[2][3], LA[2][3], EA[2][3];
     mesh_path<T, 1, false, NoStore>(q, m, sn, th, px, py, q.iteration, 1u, LB, EB, nullptr);
@@ -796,6 +807,7 @@ int mg_meshscene_create(mg_ctx* ctx, int32_t tri_count, const double* tri, const
   if (e == cudaSuccess) e = cudaMalloc(&sc->orig, sizeof(int) * T);
   if (e == cudaSuccess) e = cudaMalloc(&sc->obj, sizeof(int) * T);
   if (e == cudaSuccess) e = cudaMalloc(&sc->nodes, sizeof(float4) * nodes.size());
+  if (e == cudaSuccess) e = cudaMalloc(&sc->work, sizeof(unsigned int));
   if (e == cudaSuccess)
     e = cudaMemcpy(sc->tri, stri.data(), sizeof(double) * stri.size(), cudaMemcpyHostToDevice);
   if (e == cudaSuccess) e = cudaMemcpy(sc->orig, sorig.data(), sizeof(int) * T, cudaMemcpyHostToDevice);
@@ -807,6 +819,7 @@ int mg_meshscene_create(mg_ctx* ctx, int32_t tri_count, const double* tri, const
     cudaFree(sc->orig);
     cudaFree(sc->obj);
     cudaFree(sc->nodes);
+    cudaFree(sc->work);
     delete sc;
     return cuda_fail(e, "mg_meshscene_create");
   }
@@ -820,6 +833,7 @@ int mg_meshscene_destroy(mg_mesh_scene* s) {
   cudaFree(s->orig);
   cudaFree(s->obj);
   cudaFree(s->nodes);
+  cudaFree(s->work);
   delete s;
   return MG_OK;
 }
@@ -891,14 +905,15 @@ int mg_meshscene_sample_pair(mg_ctx* ctx, const mg_mesh_scene* s, int32_t dtype,
   const long long np = (long long)s->nobj * 4 * s->R * s->R;
   const int grid = grid_for(ctx, int64_t(W) * (row1 - row0) + 1, kMThreads, 4);
   unsigned long long* acc = (unsigned long long*)accum;
+  MG_CUDA_TRY(cudaMemsetAsync(s->work, 0, sizeof(unsigned int), ctx->stream));
   if (dtype == MG_F64)
     mesh_pair_kernel<double><<<grid, kMThreads, 0, ctx->stream>>>(
         q, dev_of(s), (const double*)target_img, (const double*)now, (const double*)prev, acc, np,
-        ctx->partials, ctx->counter, loss_out);
+        s->work, ctx->partials, ctx->counter, loss_out);
   else if (dtype == MG_F32)
     mesh_pair_kernel<float><<<grid, kMThreads, 0, ctx->stream>>>(
         q, dev_of(s), (const float*)target_img, (const float*)now, (const float*)prev, acc, np,
-        ctx->partials, ctx->counter, loss_out);
+        s->work, ctx->partials, ctx->counter, loss_out);
   else
     return fail(MG_EINVAL, "mg_meshscene_sample_pair: unknown dtype");
   MG_LAUNCH_CHECK(ctx);
