@@ -466,7 +466,7 @@ int mg_meshscene_render(mg_ctx* ctx, const mg_mesh_scene* s, int32_t dtype, int3
  * double) = sum r_A r_B.  accum: device scratch of 2 * params int64, zero
  * on first use (left zeroed).  Exact fixed-point accumulation: tiles sum
  * exactly to the full pair. */
-int mg_meshscene_sample_pair(mg_ctx* ctx, const mg_mesh_scene* s, int32_t dtype, int32_t W,
+int mg_meshscene_sample_pair(mg_ctx* ctx, mg_mesh_scene* s, int32_t dtype, int32_t W,
                              int32_t H, const double* view, const void* target_img,
                              const void* now, const void* prev, uint64_t key, uint32_t iteration,
                              int32_t row0, int32_t row1, void* accum, void* prop, void* diff,

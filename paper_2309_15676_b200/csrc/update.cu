@@ -27,6 +27,7 @@ namespace mg {
 // Test/benchmark switch: force the register-streaming kernel (mg_set_option).
 bool g_disable_tma = false;
 extern bool g_render_vec;
+extern bool g_mesh_megakernel;
 // -1: per-dtype default measured on B200 (tools/sweep_update_variants.py,
 // profiles/r01_sweep_update_variants_*): fp32 -> variant 6 (2 CTAs/SM x 192
 // threads, 4 stages of 3 KB tiles: the fp32 body is issue-heavy, so it wants
@@ -716,6 +717,10 @@ int mg_set_option(const char* name, int64_t value) {
   if (!name) return fail(MG_EINVAL, "mg_set_option: null name");
   if (std::string(name) == "disable_tma") {
     g_disable_tma = value != 0;
+    return MG_OK;
+  }
+  if (std::string(name) == "mesh_megakernel") {
+    g_mesh_megakernel = value != 0;
     return MG_OK;
   }
   if (std::string(name) == "render_vec") {

@@ -74,8 +74,16 @@ def test_render_bit_exact_vs_oracle(api, oracle):
     assert np.array_equal(img, want)
 
 
+@pytest.fixture(params=["wavefront", "megakernel"])
+def kernel_mode(request):
+    from paper_2309_15676_b200._lib import check, load
+    check(load().mg_set_option(b"mesh_megakernel", int(request.param == "megakernel")))
+    yield request.param
+    check(load().mg_set_option(b"mesh_megakernel", 0))
+
+
 @pytest.mark.parametrize("maxv", [1, 4, 6])
-def test_sample_pair_bit_exact_vs_oracle(api, oracle, maxv):
+def test_sample_pair_bit_exact_vs_oracle(api, oracle, maxv, kernel_mode):
     R = 4
     rec, obj, nobj, view, sc = _small(api, R, maxv)
     n = nobj * 4 * R * R
@@ -105,7 +113,7 @@ def test_sample_pair_bit_exact_vs_oracle(api, oracle, maxv):
     assert np.count_nonzero(wp) > 10
 
 
-def test_problem_tiles_sum_exactly_and_f32_tracks_f64(api):
+def test_problem_tiles_sum_exactly_and_f32_tracks_f64(api, kernel_mode):
     prob = api.MeshTextureProblem(24, 20, 8, (8, 12), (12, 16), max_vertices=5, target_spp=4,
                                   dtype=torch.float64)
     n = prob.dim()
