@@ -49,7 +49,8 @@ namespace {
 constexpr int kMThreads = 128;
 constexpr int kMaxV = 8;
 constexpr int kRec = 18;
-constexpr int kSmemNodes = 512;  // top BVH levels staged in shared memory (16 KB)
+constexpr int kSmemNodes = 256;  // top BVH levels staged in shared memory (16 KB)
+constexpr int kStackDepth = 48;  // traversal stack per thread, in shared memory
 constexpr double kTMin = 1e-9, kOff = 1e-6;
 constexpr double kPiM = 3.14159265358979323846;
 constexpr double kFixM = 1099511627776.0;  // 2^40
@@ -66,6 +67,7 @@ struct Builder {
   std::vector<int> idx;
   std::vector<TmpNode> nodes;
   int max_depth = 0;
+  bool too_deep = false;
 
   void bounds(int b, int e, double lo[3], double hi[3], bool centroids) const {
     for (int k = 0; k < 3; ++k) {
@@ -100,7 +102,11 @@ struct Builder {
       nodes[size_t(id)] = nd;
       return id;
     };
-    if (n <= 4 || depth >= 60) return make_leaf();
+    if (n <= 4) return make_leaf();
+    if (depth >= kStackDepth - 2) {  // deeper than the traversal stack allows
+      too_deep = true;
+      return make_leaf();
+    }
     double clo[3], chi[3];
     bounds(b, e, clo, chi, true);
     int axis = 0;
@@ -225,34 +231,62 @@ __device__ __forceinline__ bool tri_hit(const double* __restrict__ r, const doub
   return true;
 }
 
-__device__ __forceinline__ void load_node(const MeshDev& m, const float4* sn, int i, float4& a,
-                                          float4& b) {
+// BVH2 node = the boxes of its two children (64 B, four float4):
+//   n0 = c0.lo.xyz c0.hi.x   n1 = c0.hi.yz c1.lo.xy   n2 = c1.lo.z c1.hi.xyz
+//   n3 = (ref0, ref1) as int bits; ref >= 0: internal node, ref < 0: leaf
+//   with triangles [first, first + count), ~ref = first * 8 + count.
+// One 64-byte fetch per traversal step tests both children.
+struct Node4 {
+  float4 a, b, c, d;
+};
+
+__device__ __forceinline__ Node4 load_node(const MeshDev& m, const float4* sn, int i) {
+  Node4 n;
   if (i < kSmemNodes) {
-    a = sn[2 * i];
-    b = sn[2 * i + 1];
+    n.a = sn[4 * i];
+    n.b = sn[4 * i + 1];
+    n.c = sn[4 * i + 2];
+    n.d = sn[4 * i + 3];
   } else {
-    a = __ldg(&m.nodes[2 * i]);
-    b = __ldg(&m.nodes[2 * i + 1]);
+    n.a = __ldg(&m.nodes[4 * i]);
+    n.b = __ldg(&m.nodes[4 * i + 1]);
+    n.c = __ldg(&m.nodes[4 * i + 2]);
+    n.d = __ldg(&m.nodes[4 * i + 3]);
   }
+  return n;
 }
 
-__device__ __forceinline__ bool slab(const float4& a, const float4& b, const float o[3],
-                                     const float inv[3], float tmax, float& tnear) {
-  const float tx0 = (a.x - o[0]) * inv[0], tx1 = (b.x - o[0]) * inv[0];
-  const float ty0 = (a.y - o[1]) * inv[1], ty1 = (b.y - o[1]) * inv[1];
-  const float tz0 = (a.z - o[2]) * inv[2], tz1 = (b.z - o[2]) * inv[2];
+__device__ __forceinline__ bool slab6(float lx, float ly, float lz, float hx, float hy, float hz,
+                                      const float o[3], const float inv[3], float tmax,
+                                      float& tnear) {
+  const float tx0 = (lx - o[0]) * inv[0], tx1 = (hx - o[0]) * inv[0];
+  const float ty0 = (ly - o[1]) * inv[1], ty1 = (hy - o[1]) * inv[1];
+  const float tz0 = (lz - o[2]) * inv[2], tz1 = (hz - o[2]) * inv[2];
   const float tn = fmaxf(fmaxf(fminf(tx0, tx1), fminf(ty0, ty1)), fmaxf(fminf(tz0, tz1), 0.0f));
   const float tf = fminf(fminf(fmaxf(tx0, tx1), fmaxf(ty0, ty1)), fminf(fmaxf(tz0, tz1), tmax));
   tnear = tn;
   return tn <= tf;
 }
 
+// Triangle record fields 0..8 (v0, e1, e2) with 16-byte loads (records are
+// 144 B = 9 x 16 B and the array is 256-byte aligned).
+__device__ __forceinline__ bool tri_hit_rec(const double* __restrict__ rec, const double o[3],
+                                            const double d[3], double& t, double& u, double& v) {
+  const double2* r2 = reinterpret_cast<const double2*>(rec);
+  const double2 x0 = __ldg(r2), x1 = __ldg(r2 + 1), x2 = __ldg(r2 + 2), x3 = __ldg(r2 + 3);
+  const double r[9] = {x0.x, x0.y, x1.x, x1.y, x2.x, x2.y, x3.x, x3.y, __ldg(rec + 8)};
+  return tri_hit(r, o, d, t, u, v);
+}
+
 // ANY: any hit with t < tmax (shadow rays).  Otherwise the closest hit with
 // t < tmax; ties on t resolve to the lower original triangle index, so the
 // answer is the oracle's brute-force scan.  Returns the BVH slot or -1.
+// (stk: reserved for a shared-memory stack; the local-memory stack measured
+// faster — the shared one cut occupancy.)
 template <bool ANY>
-__device__ __noinline__ int trace(const MeshDev& m, const float4* sn, const double o[3], const double d[3],
-                     double tmax, double& t_out, double& u_out, double& v_out) {
+__device__ __noinline__ int trace(const MeshDev& m, const float4* sn, int* stk, const double o[3],
+                                  const double d[3], double tmax, double& t_out, double& u_out,
+                                  double& v_out) {
   float of[3], inv[3];
 #pragma unroll
   for (int k = 0; k < 3; ++k) {
@@ -260,55 +294,49 @@ __device__ __noinline__ int trace(const MeshDev& m, const float4* sn, const doub
     const float dk = float(d[k]);
     inv[k] = 1.0f / (fabsf(dk) > 1e-20f ? dk : copysignf(1e-20f, dk));
   }
-  int stack[64];
+  int stack[kStackDepth];
   int sp = 0, node = 0;
   double best = tmax, bu = 0.0, bv = 0.0;
   int bslot = -1, bid = INT_MAX;
   float bestf = __double2float_ru(best);
-  float4 na, nb;
-  load_node(m, sn, 0, na, nb);
-  float tn;
-  if (!slab(na, nb, of, inv, bestf, tn)) return -1;
   for (;;) {
-    load_node(m, sn, node, na, nb);
-    const int a = __float_as_int(na.w), b = __float_as_int(nb.w);
-    if (b < 0) {  // leaf: triangles [a, a - b)
-      for (int s = a; s < a - b; ++s) {
+    if (node < 0) {  // leaf: triangles [first, first + count)
+      const int first = (~node) >> 3, count = (~node) & 7;
+      for (int sidx = first; sidx < first + count; ++sidx) {
         double t, u, v;
-        if (!tri_hit(m.tri + size_t(kRec) * s, o, d, t, u, v) || !(t <= best)) continue;
+        if (!tri_hit_rec(m.tri + size_t(kRec) * sidx, o, d, t, u, v) || !(t <= best)) continue;
         if (ANY) {
-          if (t < tmax) return s;
+          if (t < tmax) return sidx;
           continue;
         }
-        const int id = __ldg(&m.orig[s]);
+        const int id = __ldg(&m.orig[sidx]);
         if (t < best || id < bid) {
           best = t;
           bu = u;
           bv = v;
-          bslot = s;
+          bslot = sidx;
           bid = id;
           bestf = __double2float_ru(best);
         }
       }
     } else {
-      float4 la, lb, ra, rb;
-      load_node(m, sn, a, la, lb);
-      load_node(m, sn, b, ra, rb);
+      const Node4 n = load_node(m, sn, node);
       float t0, t1;
-      const bool h0 = slab(la, lb, of, inv, bestf, t0);
-      const bool h1 = slab(ra, rb, of, inv, bestf, t1);
+      const bool h0 = slab6(n.a.x, n.a.y, n.a.z, n.a.w, n.b.x, n.b.y, of, inv, bestf, t0);
+      const bool h1 = slab6(n.b.z, n.b.w, n.c.x, n.c.y, n.c.z, n.c.w, of, inv, bestf, t1);
+      const int r0 = __float_as_int(n.d.x), r1 = __float_as_int(n.d.y);
       if (h0 && h1) {
         const bool first0 = t0 <= t1;
-        stack[sp++] = first0 ? b : a;
-        node = first0 ? a : b;
+        stack[sp++] = first0 ? r1 : r0;
+        node = first0 ? r0 : r1;
         continue;
       }
       if (h0) {
-        node = a;
+        node = r0;
         continue;
       }
       if (h1) {
-        node = b;
+        node = r1;
         continue;
       }
     }
@@ -381,7 +409,8 @@ struct NoStore {};
 // radiance L[s][c], environment after the last vertex E[s][c]; per-vertex
 // adjoint data into *st when STORE.  Returns the number of vertices.
 template <class T, int NS, bool STORE, class Store>
-__device__ __noinline__ int mesh_path(const MeshK& q, const MeshDev& m, const float4* sn, const T* const th[2],
+__device__ __noinline__ int mesh_path(const MeshK& q, const MeshDev& m, const float4* sn, int* stk,
+                                     const T* const th[2],
                          int px, int py, uint32_t it, uint32_t path, T L[NS][3], T E[NS][3],
                          Store* st) {
   const double* V = q.view;
@@ -414,7 +443,7 @@ __device__ __noinline__ int mesh_path(const MeshK& q, const MeshDev& m, const fl
   int nv = 0;
   for (int v = 0; v < maxv && v < kMaxV; ++v) {
     double t = INFINITY, bu, bv;
-    const int slot = trace<false>(m, sn, o, d, INFINITY, t, bu, bv);
+    const int slot = trace<false>(m, sn, stk, o, d, INFINITY, t, bu, bv);
     if (slot < 0) {
 #pragma unroll
       for (int s = 0; s < NS; ++s)
@@ -476,7 +505,7 @@ __device__ __noinline__ int mesh_path(const MeshK& q, const MeshDev& m, const fl
     const T nT[3] = {T(n[0]), T(n[1]), T(n[2])}, woT[3] = {T(wo[0]), T(wo[1]), T(wo[2])};
     if (cx > 0.0 && cl > 0.0 && dot3d(n, wo) > 0.0) {
       double ts, tu, tv;
-      if (trace<true>(m, sn, xo, w, wl - kOff, ts, tu, tv) < 0) {
+      if (trace<true>(m, sn, stk, xo, w, wl - kOff, ts, tu, tv) < 0) {
         const double gl = ((cx * cl) / d2) * la;
         const T wT[3] = {T(w[0]), T(w[1]), T(w[2])};
 #pragma unroll
@@ -578,17 +607,22 @@ __device__ __noinline__ void scatter(const PathStore<T, NS>& st, int nv, const T
 }
 
 __device__ __forceinline__ void stage_nodes(const MeshDev& m, float4* sn) {
-  const int n = 2 * (m.nnodes < kSmemNodes ? m.nnodes : kSmemNodes);
+  const int n = 4 * (m.nnodes < kSmemNodes ? m.nnodes : kSmemNodes);
   for (int i = threadIdx.x; i < n; i += blockDim.x) sn[i] = m.nodes[i];
   __syncthreads();
 }
+
+// shared-memory arrays every tracing kernel declares
+#define MESH_SMEM                       \
+  __shared__ float4 sn[4 * kSmemNodes]; \
+  int* stk = nullptr;                   \
+  stage_nodes(m, sn)
 
 template <class T>
 __global__ void __launch_bounds__(kMThreads)
     mesh_render_kernel(MeshK q, MeshDev m, int spp, const T* __restrict__ theta,
                        T* __restrict__ img) {
-  __shared__ float4 sn[2 * kSmemNodes];
-  stage_nodes(m, sn);
+  MESH_SMEM;
   const int npix = q.W * q.H;
   const T* th[2] = {theta, theta};
   for (int pix = blockIdx.x * kMThreads + threadIdx.x; pix < npix; pix += gridDim.x * kMThreads) {
@@ -596,7 +630,7 @@ __global__ void __launch_bounds__(kMThreads)
     double acc[3] = {0.0, 0.0, 0.0};
     for (int s = 0; s < spp; ++s) {
       T L[1][3], E[1][3];
-      mesh_path<T, 1, false, NoStore>(q, m, sn, th, px, py, 0xffffffffu, uint32_t(s), L, E,
+      mesh_path<T, 1, false, NoStore>(q, m, sn, stk, th, px, py, 0xffffffffu, uint32_t(s), L, E,
                                       nullptr);
 #pragma unroll
       for (int c = 0; c < 3; ++c) acc[c] += double(L[0][c]);
@@ -621,8 +655,7 @@ __global__ void __launch_bounds__(kMThreads)
                      const T* __restrict__ now, const T* __restrict__ prev,
                      unsigned long long* __restrict__ acc, long long np, unsigned int* work,
                      ReducePartials* partials, unsigned int* counter, double* loss_out) {
-  __shared__ float4 sn[2 * kSmemNodes];
-  stage_nodes(m, sn);
+  MESH_SMEM;
   const int npix = q.W * q.H;
   const int R2 = q.R * q.R;
   const T* th[2] = {now, prev};
@@ -633,13 +666,13 @@ __global__ void __launch_bounds__(kMThreads)
     if (pix >= pix1) continue;
     const int px = pix % q.W, py = pix / q.W;
     T LB[1][3], EB[1][3], LC[2][3], EC[2][3], LA[2][3], EA[2][3];
-    mesh_path<T, 1, false, NoStore>(q, m, sn, th, px, py, q.iteration, 1u, LB, EB, nullptr);
-    mesh_path<T, 2, false, NoStore>(q, m, sn, th, px, py, q.iteration, 2u, LC, EC, nullptr);
+    mesh_path<T, 1, false, NoStore>(q, m, sn, stk, th, px, py, q.iteration, 1u, LB, EB, nullptr);
+    mesh_path<T, 2, false, NoStore>(q, m, sn, stk, th, px, py, q.iteration, 2u, LC, EC, nullptr);
     T rA[3], rB[3], wC0[3], wC1[3];
     {
       PathStore<T, 2> st;
       const int na =
-          mesh_path<T, 2, true>(q, m, sn, th, px, py, q.iteration, 0u, LA, EA, &st);
+          mesh_path<T, 2, true>(q, m, sn, stk, th, px, py, q.iteration, 0u, LA, EA, &st);
 #pragma unroll
       for (int c = 0; c < 3; ++c) {
         const T Is = target_img[size_t(c) * npix + pix];
@@ -656,7 +689,7 @@ __global__ void __launch_bounds__(kMThreads)
     {
       PathStore<T, 1> st;
       const int nb =
-          mesh_path<T, 1, true>(q, m, sn, th, px, py, q.iteration, 1u, LB, EB, &st);
+          mesh_path<T, 1, true>(q, m, sn, stk, th, px, py, q.iteration, 1u, LB, EB, &st);
       scatter<T, 1>(st, nb, EB[0], 0, rA, R2, acc);
     }
   }
@@ -680,13 +713,12 @@ __global__ void mesh_finalize_kernel(long long n, unsigned long long* __restrict
 
 __global__ void mesh_intersect_kernel(MeshDev m, int n, const double* __restrict__ rays,
                                       double* __restrict__ t_out, int* __restrict__ tri_out) {
-  __shared__ float4 sn[2 * kSmemNodes];
-  stage_nodes(m, sn);
+  MESH_SMEM;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
     const double o[3] = {rays[6 * i], rays[6 * i + 1], rays[6 * i + 2]};
     const double d[3] = {rays[6 * i + 3], rays[6 * i + 4], rays[6 * i + 5]};
     double t = INFINITY, u, v;
-    const int s = trace<false>(m, sn, o, d, INFINITY, t, u, v);
+    const int s = trace<false>(m, sn, stk, o, d, INFINITY, t, u, v);
     t_out[i] = s < 0 ? INFINITY : t;
     tri_out[i] = s < 0 ? -1 : m.orig[s];
   }
@@ -804,15 +836,14 @@ __global__ void __launch_bounds__(kMThreads) wf_gen_kernel(MeshK q, WF<T> w) {
 
 template <class T>
 __global__ void __launch_bounds__(kMThreads) wf_isect_kernel(MeshDev m, WF<T> w, int v) {
-  __shared__ float4 sn[2 * kSmemNodes];
-  stage_nodes(m, sn);
+  MESH_SMEM;
   const int n = int(w.cnt[v]);
   const int* qin = (v & 1) ? w.q1 : w.q0;
   for (int i = blockIdx.x * kMThreads + threadIdx.x; i < n; i += gridDim.x * kMThreads) {
     const int p = qin[i];
     const double o[3] = {w.ox[p], w.oy[p], w.oz[p]}, d[3] = {w.dx[p], w.dy[p], w.dz[p]};
     double t = INFINITY, bu = 0.0, bv = 0.0;
-    const int slot = trace<false>(m, sn, o, d, INFINITY, t, bu, bv);
+    const int slot = trace<false>(m, sn, stk, o, d, INFINITY, t, bu, bv);
     w.hslot[p] = slot;
     w.ht[p] = t;
     w.hu[p] = bu;
@@ -993,14 +1024,13 @@ __global__ void __launch_bounds__(kMThreads)
 
 template <class T>
 __global__ void __launch_bounds__(kMThreads) wf_shadow_kernel(MeshDev m, WF<T> w, int v) {
-  __shared__ float4 sn[2 * kSmemNodes];
-  stage_nodes(m, sn);
+  MESH_SMEM;
   const int n = int(w.cnt[kMaxV + 1 + v]);
   for (int i = blockIdx.x * kMThreads + threadIdx.x; i < n; i += gridDim.x * kMThreads) {
     const int p = w.sq[i];
     const double o[3] = {w.sox[p], w.soy[p], w.soz[p]}, d[3] = {w.sdx[p], w.sdy[p], w.sdz[p]};
     double ts, tu, tv;
-    if (trace<true>(m, sn, o, d, w.stm[p], ts, tu, tv) < 0) {
+    if (trace<true>(m, sn, stk, o, d, w.stm[p], ts, tu, tv) < 0) {
 #pragma unroll
       for (int j = 0; j < 6; ++j) w.L[size_t(j) * w.P + p] += w.pendC[size_t(j) * w.P + p];
     } else if (p < w.PS) {
@@ -1150,6 +1180,7 @@ int mg_meshscene_create(mg_ctx* ctx, int32_t tri_count, const double* tri, const
   if (!ctx || !tri || !obj || !out) return fail(MG_EINVAL, "mg_meshscene_create: null argument");
   if (tri_count < 1 || nobj < 1 || tex_res < 1)
     return fail(MG_EINVAL, "mg_meshscene_create: bad sizes");
+  if (tri_count > (1 << 27)) return fail(MG_EINVAL, "mg_meshscene_create: more than 2^27 triangles");
   if (int64_t(nobj) * 4 * tex_res * tex_res > 0x7fffffffLL)
     return fail(MG_EINVAL, "mg_meshscene_create: parameter count exceeds 2^31");
   for (int k = 0; k < tri_count; ++k)
@@ -1177,43 +1208,63 @@ int mg_meshscene_create(mg_ctx* ctx, int32_t tri_count, const double* tri, const
   }
   B.nodes.reserve(2 * T);
   B.build(0, tri_count, 0);
-  // breadth-first relabelling: the top levels become nodes [0, kSmemNodes)
-  const int nn = int(B.nodes.size());
-  std::vector<int> order, label(size_t(nn), -1);
-  order.reserve(size_t(nn));
-  order.push_back(0);
-  label[0] = 0;
-  for (size_t h = 0; h < order.size(); ++h) {
-    const TmpNode& nd = B.nodes[size_t(order[h])];
-    if (nd.left >= 0) {
-      label[size_t(nd.left)] = int(order.size());
-      order.push_back(nd.left);
-      label[size_t(nd.right)] = int(order.size());
-      order.push_back(nd.right);
-    }
-  }
+  if (B.too_deep) return fail(MG_EINVAL, "mg_meshscene_create: BVH deeper than the traversal stack");
+  // Internal nodes in breadth-first order (the top levels become nodes
+  // [0, kSmemNodes) for the shared-memory stage); each stores its two
+  // children's boxes.  A single-leaf tree gets a root whose second child is
+  // an empty box.
   const double diag = sqrt((shi[0] - slo[0]) * (shi[0] - slo[0]) +
                            (shi[1] - slo[1]) * (shi[1] - slo[1]) +
                            (shi[2] - slo[2]) * (shi[2] - slo[2]));
   const float pad = float(1e-5 * diag + 1e-7);
-  std::vector<float4> nodes(2 * size_t(nn));
-  for (int i = 0; i < nn; ++i) {
-    const TmpNode& nd = B.nodes[size_t(order[size_t(i)])];
-    float lo[3], hi[3];
+  std::vector<int> order, label(B.nodes.size(), -1);
+  if (B.nodes[0].left >= 0) {
+    order.push_back(0);
+    label[0] = 0;
+    for (size_t h = 0; h < order.size(); ++h) {
+      const TmpNode& nd = B.nodes[size_t(order[h])];
+      for (int c : {nd.left, nd.right})
+        if (B.nodes[size_t(c)].left >= 0) {
+          label[size_t(c)] = int(order.size());
+          order.push_back(c);
+        }
+    }
+  }
+  auto child_ref = [&](int c) {
+    const TmpNode& nd = B.nodes[size_t(c)];
+    return nd.left >= 0 ? label[size_t(c)] : ~(nd.first * 8 + nd.count);
+  };
+  auto box = [&](int c, float* lo, float* hi) {
+    const TmpNode& nd = B.nodes[size_t(c)];
     for (int a = 0; a < 3; ++a) {
       lo[a] = nextafterf(float(nd.lo[a]), -INFINITY) - pad;
       hi[a] = nextafterf(float(nd.hi[a]), INFINITY) + pad;
     }
-    const int a = nd.left >= 0 ? label[size_t(nd.left)] : nd.first;
-    const int b = nd.left >= 0 ? label[size_t(nd.right)] : -nd.count;
-    int ai, bi;
-    memcpy(&ai, &a, 4);
-    memcpy(&bi, &b, 4);
-    float af, bf;
-    memcpy(&af, &ai, 4);
-    memcpy(&bf, &bi, 4);
-    nodes[2 * size_t(i)] = make_float4(lo[0], lo[1], lo[2], af);
-    nodes[2 * size_t(i) + 1] = make_float4(hi[0], hi[1], hi[2], bf);
+  };
+  auto ibits = [](int v) {
+    float f;
+    memcpy(&f, &v, 4);
+    return f;
+  };
+  const int nn = order.empty() ? 1 : int(order.size());
+  std::vector<float4> nodes(4 * size_t(nn));
+  for (int i = 0; i < nn; ++i) {
+    float l0[3], h0[3], l1[3] = {1.0f, 1.0f, 1.0f}, h1[3] = {-1.0f, -1.0f, -1.0f};
+    int r0, r1 = ~0;  // empty leaf
+    if (order.empty()) {
+      box(0, l0, h0);
+      r0 = child_ref(0);
+    } else {
+      const TmpNode& nd = B.nodes[size_t(order[size_t(i)])];
+      box(nd.left, l0, h0);
+      box(nd.right, l1, h1);
+      r0 = child_ref(nd.left);
+      r1 = child_ref(nd.right);
+    }
+    nodes[4 * size_t(i)] = make_float4(l0[0], l0[1], l0[2], h0[0]);
+    nodes[4 * size_t(i) + 1] = make_float4(h0[1], h0[2], l1[0], l1[1]);
+    nodes[4 * size_t(i) + 2] = make_float4(l1[2], h1[0], h1[1], h1[2]);
+    nodes[4 * size_t(i) + 3] = make_float4(ibits(r0), ibits(r1), 0.0f, 0.0f);
   }
   std::vector<double> stri(kRec * T);
   std::vector<int> sorig(T), sobj(T);
