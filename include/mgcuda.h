@@ -439,15 +439,17 @@ int mg_helix_sample_pair(mg_ctx* ctx, int32_t dtype, int32_t W, int32_t H, int32
 /* ------------------------ F1 slice 3: textured triangle-mesh scene (configs[3]) */
 /* Scene of T triangles (host fp64 records [T][18]: v0, e1 = v1 - v0,
  * e2 = v2 - v0, unit geometric normal, uv0, uv1 - uv0, uv2 - uv0; object id
- * per triangle in [0, nobj)); each object owns an R x R texture of base
- * r, g, b and roughness: parameters [nobj][4][R*R].  The BVH is built on the
- * host (binned SAH, breadth-first node order) and uploaded.
+ * per triangle in [0, nobj)); each object owns an R x R texture of
+ * `channels` parameters per texel: 4 = base r, g, b, roughness (metalness
+ * 0; configs[3]) or 5 = + metalness (configs[4]): parameters
+ * [nobj][channels][R*R].  The BVH is built on the host (binned SAH,
+ * breadth-first node order) and uploaded.
  * view[25] = camera position, forward, right, up (3 each), tan(fov_y/2),
  * light plane y, light x0, x1, z0, z1, light radiance rgb, environment rgb,
  * max path vertices (1..8).  DESIGN.md §12; oracle mgo_mesh_*. */
 typedef struct mg_mesh_scene mg_mesh_scene;
 int mg_meshscene_create(mg_ctx* ctx, int32_t tri_count, const double* tri, const int32_t* obj,
-                        int32_t nobj, int32_t tex_res, mg_mesh_scene** out);
+                        int32_t nobj, int32_t tex_res, int32_t channels, mg_mesh_scene** out);
 int mg_meshscene_destroy(mg_mesh_scene* s);
 int mg_meshscene_info(const mg_mesh_scene* s, int32_t* nodes, int32_t* depth, int64_t* params);
 /* closest hit of n rays (device fp64 [n][6] = origin, direction): t (inf on
@@ -460,17 +462,20 @@ int mg_meshscene_intersect(mg_ctx* ctx, const mg_mesh_scene* s, int32_t n, const
 int mg_meshscene_render(mg_ctx* ctx, const mg_mesh_scene* s, int32_t dtype, int32_t W, int32_t H,
                         const double* view, int32_t spp, uint64_t key, const void* theta,
                         void* img);
-/* One gradient sample pair over image rows [row0, row1): paths A (at both
- * parameter sets), B, C per pixel; prop = sum_c r_A dI_B + r_B dI_A, diff =
- * sum_c 2 r_C dI_A (theta_t) - 2 r_C dI_A (theta_{t-1}); loss_out (device
- * double) = sum r_A r_B.  accum: device scratch of 2 * params int64, zero
- * on first use (left zeroed).  Exact fixed-point accumulation: tiles sum
- * exactly to the full pair. */
+/* One gradient sample pair over image rows [row0, row1): per pixel
+ * prop_paths (n in [2, 8]) proportional paths j (path 0 = A, also evaluated
+ * at theta_{t-1}) and one FD path C:
+ *   prop = 2/(n(n-1)) sum_c sum_j (sum_{i != j} r_i) dI_j   (n = 2: r_A dI_B + r_B dI_A)
+ *   diff = sum_c 2 r_C dI_A (theta_t) - 2 r_C dI_A (theta_{t-1})
+ *   loss_out (device double) = 2/(n(n-1)) sum_c sum_{i<j} r_i r_j.
+ * accum: device scratch of 2 * params int64, zero on first use (left
+ * zeroed).  Exact fixed-point accumulation: tiles sum exactly to the full
+ * pair. */
 int mg_meshscene_sample_pair(mg_ctx* ctx, mg_mesh_scene* s, int32_t dtype, int32_t W,
                              int32_t H, const double* view, const void* target_img,
                              const void* now, const void* prev, uint64_t key, uint32_t iteration,
-                             int32_t row0, int32_t row1, void* accum, void* prop, void* diff,
-                             double* loss_out);
+                             int32_t row0, int32_t row1, int32_t prop_paths, void* accum,
+                             void* prop, void* diff, double* loss_out);
 
 /* ------------------------------- device-resident run_single (A13, A14) */
 /* Per-replicate record of one coordinate plus scalars (harness.hpp:73-90;

@@ -1313,6 +1313,7 @@ static const double MS_OFF = 1e-6;
 
 typedef struct ms_scene {
   int W, H, T, R;
+  int nch; /* texture channels: 4 = base rgb, rough (metal 0); 5 = + metal */
   const double* tri;
   const int32_t* obj;
   const double* view; /* cam fwd right up(3 each) tanh ly lx0 lx1 lz0 lz1 Le(3) env(3) maxv */
@@ -1382,11 +1383,26 @@ static void ms_bsdf(const double base[3], double rough, const double n[3], const
 typedef struct ms_vert {
   int64_t base;             /* parameter index of (object, channel 0, texel) */
   double A[2][3];           /* beta * Le * G (NEE weight), 0 without NEE */
-  double dSn[2];            /* dS/drough at the NEE direction */
+  double dSn[2];            /* dS/drough at the NEE direction (nch 4) */
   double invfb[2][3];       /* 1 / f(bounce), 0 without a bounce or f == 0 */
-  double dSb[2];            /* dS/drough at the bounce direction */
+  double dSb[2];            /* dS/drough at the bounce direction (nch 4) */
   double C[2][3];           /* NEE contribution */
+  double dfn[2][3][3];      /* nch 5: df_c / d(base_c, metal, rough), NEE direction */
+  double dfb[2][3][3];      /* nch 5: same at the bounce direction */
 } ms_vert;
+
+/* full principled BSDF (nch 5): f[3] and df[c][base_c, metal, rough] */
+static void ms_bsdf5(const double base[3], double metal, double rough, const double n[3],
+                     const double wi[3], const double wo[3], double f[3], double df3[3][3]) {
+  const double th[HX_NP] = {base[0], base[1], base[2], metal, rough};
+  double df[3][HX_NP];
+  hx_bsdf(th, n, wi, wo, f, df);
+  for (int c = 0; c < 3; ++c) {
+    df3[c][0] = df[c][c];
+    df3[c][1] = df[c][3];
+    df3[c][2] = df[c][4];
+  }
+}
 
 /* One path for nsets parameter sets; L[s][3]; vertices (if vout) and the
  * number of vertices; E[s][3] = environment collected after the last one. */
@@ -1432,20 +1448,18 @@ static int ms_path(const ms_scene* S, const double* const th[2], int nsets, int 
     int tx = (int)(U * S->R), ty = (int)(W_ * S->R);
     tx = tx < 0 ? 0 : (tx > S->R - 1 ? S->R - 1 : tx);
     ty = ty < 0 ? 0 : (ty > S->R - 1 ? S->R - 1 : ty);
-    const int64_t pbase = (int64_t)S->obj[k] * 4 * R2 + (int64_t)ty * S->R + tx;
+    const int64_t pbase = (int64_t)S->obj[k] * S->nch * R2 + (int64_t)ty * S->R + tx;
     ms_vert* mv = vout ? &vout[nv] : NULL;
     ms_vert tmp;
     if (!mv) mv = &tmp;
+    memset(mv, 0, sizeof(*mv));
     mv->base = pbase;
-    for (int s = 0; s < 2; ++s) {
-      mv->dSn[s] = 0.0; mv->dSb[s] = 0.0;
-      for (int c = 0; c < 3; ++c) { mv->A[s][c] = 0.0; mv->invfb[s][c] = 0.0; mv->C[s][c] = 0.0; }
-    }
     ++nv;
-    double base[2][3], rough[2];
+    double base[2][3], rough[2], metal[2] = {0.0, 0.0};
     for (int s = 0; s < nsets; ++s) {
       for (int c = 0; c < 3; ++c) base[s][c] = th[s][pbase + c * R2];
       rough[s] = th[s][pbase + 3 * R2];
+      if (S->nch == 5) metal[s] = th[s][pbase + 4 * R2];
     }
     const double wo[3] = {-d[0], -d[1], -d[2]};
     const double xo[3] = {x[0] + MS_OFF * n[0], x[1] + MS_OFF * n[1], x[2] + MS_OFF * n[2]};
@@ -1460,8 +1474,12 @@ static int ms_path(const ms_scene* S, const double* const th[2], int nsets, int 
     if (cx > 0.0 && cl > 0.0 && hx_dot(n, wo) > 0.0 && !ms_occluded(S, xo, w, wl - MS_OFF)) {
       const double gl = ((cx * cl) / d2) * la;
       for (int s = 0; s < nsets; ++s) {
-        double f[3], dS;
-        ms_bsdf(base[s], rough[s], n, w, wo, f, &dS);
+        double f[3], dS = 0.0;
+        if (S->nch == 5) {
+          ms_bsdf5(base[s], metal[s], rough[s], n, w, wo, f, mv->dfn[s]);
+        } else {
+          ms_bsdf(base[s], rough[s], n, w, wo, f, &dS);
+        }
         mv->dSn[s] = dS;
         for (int c = 0; c < 3; ++c) {
           const double A = beta[s][c] * (gl * V[18 + c]);
@@ -1494,8 +1512,12 @@ static int ms_path(const ms_scene* S, const double* const th[2], int nsets, int 
                           (dx * Tb[1] + dy * Bb[1]) + dz * n[1],
                           (dx * Tb[2] + dy * Bb[2]) + dz * n[2]};
     for (int s = 0; s < nsets; ++s) {
-      double f[3], dS;
-      ms_bsdf(base[s], rough[s], n, wi, wo, f, &dS);
+      double f[3], dS = 0.0;
+      if (S->nch == 5) {
+        ms_bsdf5(base[s], metal[s], rough[s], n, wi, wo, f, mv->dfb[s]);
+      } else {
+        ms_bsdf(base[s], rough[s], n, wi, wo, f, &dS);
+      }
       mv->dSb[s] = dS;
       for (int c = 0; c < 3; ++c) {
         mv->invfb[s][c] = f[c] != 0.0 ? 1.0 / f[c] : 0.0;
@@ -1510,9 +1532,23 @@ static int ms_path(const ms_scene* S, const double* const th[2], int nsets, int 
 
 /* adjoint of one stored path for set s with channel weights w[3] */
 static void ms_scatter(const ms_vert* vs, int nv, const double E[3], int s, const double w[3],
-                       int64_t R2, int64_t* acc) {
+                       int64_t R2, int64_t* acc, int nch) {
   double Q[3] = {E[0], E[1], E[2]};
-  for (int v = nv - 1; v >= 0; --v) {
+  for (int v = nv - 1; v >= 0 && nch == 5; --v) {
+    const ms_vert* m = &vs[v];
+    double gm = 0.0, gr = 0.0;
+    for (int c = 0; c < 3; ++c) {
+      const double fb = m->invfb[s][c];
+      const double gb = w[c] * (m->A[s][c] * m->dfn[s][c][0] + Q[c] * (fb * m->dfb[s][c][0]));
+      acc[m->base + c * R2] += qs_fix(gb);
+      gm += w[c] * (m->A[s][c] * m->dfn[s][c][1] + Q[c] * (fb * m->dfb[s][c][1]));
+      gr += w[c] * (m->A[s][c] * m->dfn[s][c][2] + Q[c] * (fb * m->dfb[s][c][2]));
+    }
+    acc[m->base + 3 * R2] += qs_fix(gr);
+    acc[m->base + 4 * R2] += qs_fix(gm);
+    for (int c = 0; c < 3; ++c) Q[c] = Q[c] + m->C[s][c];
+  }
+  for (int v = nv - 1; v >= 0 && nch == 4; --v) {
     const ms_vert* m = &vs[v];
     double gr = 0.0;
     for (int c = 0; c < 3; ++c) {
@@ -1525,10 +1561,10 @@ static void ms_scatter(const ms_vert* vs, int nv, const double E[3], int s, cons
   }
 }
 
-void mgo_mesh_render(int W, int H, int T, const double* tri, const int32_t* obj, int R,
-                     const double* view, const double* theta, int spp, uint64_t key,
-                     double* img) {
-  ms_scene S = {W, H, T, R, tri, obj, view};
+void mgo_meshx_render(int W, int H, int T, const double* tri, const int32_t* obj, int nch, int R,
+                      const double* view, const double* theta, int spp, uint64_t key,
+                      double* img) {
+  ms_scene S = {W, H, T, R, nch, tri, obj, view};
   const double* th[2] = {theta, theta};
   for (int py = 0; py < H; ++py)
     for (int px = 0; px < W; ++px) {
@@ -1542,60 +1578,101 @@ void mgo_mesh_render(int W, int H, int T, const double* tri, const int32_t* obj,
     }
 }
 
-/* gradient sample pair over the texture parameters, image rows [row0, row1):
- *   prop = sum_c r_A,c dI_B,c + r_B,c dI_A,c                     (theta_t)
- *   diff = sum_c 2 r_C,c dI_A,c (theta_t) - 2 r_C,c dI_A,c (theta_{t-1})
- * with r_X = I_X(theta_t) - I* (r_C at its own theta for the two terms);
- * loss_est = sum r_A r_B.  prop/diff have nobj*4*R*R entries. */
-void mgo_mesh_sample_pair(int W, int H, int T, const double* tri, const int32_t* obj, int nobj,
-                          int R, const double* view, const double* target_img, const double* now,
-                          const double* prev, uint64_t key, uint32_t it, int row0, int row1,
-                          double* prop, double* diff, double* loss_est) {
-  ms_scene S = {W, H, T, R, tri, obj, view};
-  const int64_t R2 = (int64_t)R * R, np = (int64_t)nobj * 4 * R2;
+/* gradient sample pair with n proportional paths 0..n-1 (path 0 = A, also
+ * evaluated at theta_{t-1}) and the FD path C = path n:
+ *   prop = 2 / (n (n-1)) sum_j (sum_{i != j} r_i) dI_j          (theta_t)
+ *   diff = sum_c 2 r_C dI_A (theta_t) - 2 r_C dI_A (theta_{t-1})
+ *   loss = 2 / (n (n-1)) sum_{i < j} r_i r_j
+ * (n = 2: prop = r_A dI_B + r_B dI_A, loss = r_A r_B).  prop/diff have
+ * nobj * nch * R * R entries. */
+void mgo_meshx_sample_pair(int W, int H, int T, const double* tri, const int32_t* obj, int nobj,
+                           int nch, int R, const double* view, const double* target_img,
+                           const double* now, const double* prev, uint64_t key, uint32_t it,
+                           int row0, int row1, int nprop, double* prop, double* diff,
+                           double* loss_est) {
+  ms_scene S = {W, H, T, R, nch, tri, obj, view};
+  const int64_t R2 = (int64_t)R * R, np = (int64_t)nobj * nch * R2;
   int64_t* fp = (int64_t*)calloc((size_t)np, sizeof(int64_t));
   int64_t* fd = (int64_t*)calloc((size_t)np, sizeof(int64_t));
+  ms_vert* vs = (ms_vert*)malloc(sizeof(ms_vert) * MS_MAXV * (size_t)nprop);
   const double* th[2] = {now, prev};
-  ms_vert va[MS_MAXV], vb[MS_MAXV];
+  const double scale = 2.0 / (nprop * (nprop - 1.0));
   double loss = 0.0;
   for (int py = row0; py < row1; ++py)
     for (int px = 0; px < W; ++px) {
-      double LA[2][3], EA[2][3], LB[2][3], EB[2][3], LC[2][3], EC[2][3];
-      const int na = ms_path(&S, th, 2, px, py, key, it, 0u, LA, va, EA);
-      const int nb = ms_path(&S, th, 1, px, py, key, it, 1u, LB, vb, EB);
-      ms_path(&S, th, 2, px, py, key, it, 2u, LC, NULL, EC);
+      double Lp[8][2][3], Ep[8][2][3], LC[2][3], EC[2][3];
+      int nv[8];
+      for (int j = 0; j < nprop; ++j)
+        nv[j] = ms_path(&S, th, j == 0 ? 2 : 1, px, py, key, it, (uint32_t)j, Lp[j],
+                        vs + (size_t)MS_MAXV * j, Ep[j]);
+      ms_path(&S, th, 2, px, py, key, it, (uint32_t)nprop, LC, NULL, EC);
       const size_t pix = (size_t)py * W + px;
-      double rA[3], rB[3], wC0[3], wC1[3];
+      double r[8][3], wC0[3], wC1[3];
       for (int c = 0; c < 3; ++c) {
         const double Is = target_img[(size_t)c * W * H + pix];
-        rA[c] = LA[0][c] - Is;
-        rB[c] = LB[0][c] - Is;
+        for (int j = 0; j < nprop; ++j) r[j][c] = Lp[j][0][c] - Is;
         wC0[c] = 2.0 * (LC[0][c] - Is);
         wC1[c] = -2.0 * (LC[1][c] - Is);
-        loss += rA[c] * rB[c];
+        double lp = 0.0;
+        for (int i = 0; i < nprop; ++i)
+          for (int j = i + 1; j < nprop; ++j) lp += r[i][c] * r[j][c];
+        loss += lp * scale;
       }
-      ms_scatter(va, na, EA[0], 0, rB, R2, fp);
-      ms_scatter(vb, nb, EB[0], 0, rA, R2, fp);
-      ms_scatter(va, na, EA[0], 0, wC0, R2, fd);
-      ms_scatter(va, na, EA[1], 1, wC1, R2, fd);
+      for (int j = 0; j < nprop; ++j) {
+        double w[3];
+        for (int c = 0; c < 3; ++c) {
+          double acc = 0.0;
+          int first = 1;
+          for (int i = 0; i < nprop; ++i) {
+            if (i == j) continue;
+            acc = first ? r[i][c] : acc + r[i][c];
+            first = 0;
+          }
+          w[c] = acc * scale;
+        }
+        ms_scatter(vs + (size_t)MS_MAXV * j, nv[j], Ep[j][0], 0, w, R2, fp, nch);
+      }
+      ms_scatter(vs, nv[0], Ep[0][0], 0, wC0, R2, fd, nch);
+      ms_scatter(vs, nv[0], Ep[0][1], 1, wC1, R2, fd, nch);
     }
   for (int64_t k = 0; k < np; ++k) {
     prop[k] = (double)fp[k] / QS_FIX;
     diff[k] = (double)fd[k] / QS_FIX;
   }
+  free(vs);
   free(fp);
   free(fd);
   *loss_est = loss;
 }
 
-/* one path's radiance (set 0) and its vertex count, for derivative checks */
-int mgo_mesh_path_radiance(int W, int H, int T, const double* tri, const int32_t* obj, int R,
-                           const double* view, const double* theta, int px, int py, uint64_t key,
-                           uint32_t it, uint32_t path, double L_out[3]) {
-  ms_scene S = {W, H, T, R, tri, obj, view};
+int mgo_meshx_path_radiance(int W, int H, int T, const double* tri, const int32_t* obj, int nch,
+                            int R, const double* view, const double* theta, int px, int py,
+                            uint64_t key, uint32_t it, uint32_t path, double L_out[3]) {
+  ms_scene S = {W, H, T, R, nch, tri, obj, view};
   const double* th[2] = {theta, theta};
   double L[2][3], E[2][3];
   const int nv = ms_path(&S, th, 1, px, py, key, it, path, L, NULL, E);
   for (int c = 0; c < 3; ++c) L_out[c] = L[0][c];
   return nv;
+}
+
+void mgo_mesh_render(int W, int H, int T, const double* tri, const int32_t* obj, int R,
+                     const double* view, const double* theta, int spp, uint64_t key,
+                     double* img) {
+  mgo_meshx_render(W, H, T, tri, obj, 4, R, view, theta, spp, key, img);
+}
+
+void mgo_mesh_sample_pair(int W, int H, int T, const double* tri, const int32_t* obj, int nobj,
+                          int R, const double* view, const double* target_img, const double* now,
+                          const double* prev, uint64_t key, uint32_t it, int row0, int row1,
+                          double* prop, double* diff, double* loss_est) {
+  mgo_meshx_sample_pair(W, H, T, tri, obj, nobj, 4, R, view, target_img, now, prev, key, it, row0,
+                        row1, 2, prop, diff, loss_est);
+}
+
+int mgo_mesh_path_radiance(int W, int H, int T, const double* tri, const int32_t* obj, int R,
+                           const double* view, const double* theta, int px, int py, uint64_t key,
+                           uint32_t it, uint32_t path, double L_out[3]) {
+  return mgo_meshx_path_radiance(W, H, T, tri, obj, 4, R, view, theta, px, py, key, it, path,
+                                 L_out);
 }

@@ -161,3 +161,16 @@ void mgo_mesh_sample_pair(int W, int H, int T, const double* tri, const int32_t*
 int mgo_mesh_path_radiance(int W, int H, int T, const double* tri, const int32_t* obj, int R,
                            const double* view, const double* theta, int px, int py, uint64_t key,
                            uint32_t it, uint32_t path, double L_out[3]);
+/* general form (configs[4]): nch = 4 (base rgb, rough; metal 0) or 5 (+ metal
+ * as channel 4, full principled BSDF derivatives); nprop proportional paths
+ * (2..8) plus the FD path. */
+void mgo_meshx_render(int W, int H, int T, const double* tri, const int32_t* obj, int nch, int R,
+                      const double* view, const double* theta, int spp, uint64_t key, double* img);
+void mgo_meshx_sample_pair(int W, int H, int T, const double* tri, const int32_t* obj, int nobj,
+                           int nch, int R, const double* view, const double* target_img,
+                           const double* now, const double* prev, uint64_t key, uint32_t it,
+                           int row0, int row1, int nprop, double* prop, double* diff,
+                           double* loss_est);
+int mgo_meshx_path_radiance(int W, int H, int T, const double* tri, const int32_t* obj, int nch,
+                            int R, const double* view, const double* theta, int px, int py,
+                            uint64_t key, uint32_t it, uint32_t path, double L_out[3]);

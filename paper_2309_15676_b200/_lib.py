@@ -112,7 +112,8 @@ def load():
                                              C.c_int32, _vp, P(_abi.RunSeriesC), _vp, _vp]),
         "mg_mt64_set_state": (C.c_int, [_vp, _vp, C.c_int32, _vp, C.c_int32]),
         "mg_mt64_get_state": (C.c_int, [_vp, _vp, C.c_int32, _vp, _vp]),
-        "mg_meshscene_create": (C.c_int, [_vp, C.c_int32, _vp, _vp, C.c_int32, C.c_int32, _vp]),
+        "mg_meshscene_create": (C.c_int, [_vp, C.c_int32, _vp, _vp, C.c_int32, C.c_int32,
+                                          C.c_int32, _vp]),
         "mg_meshscene_destroy": (C.c_int, [_vp]),
         "mg_meshscene_info": (C.c_int, [_vp, _vp, _vp, _vp]),
         "mg_meshscene_intersect": (C.c_int, [_vp, _vp, C.c_int32, _vp, _vp, _vp]),
@@ -120,7 +121,7 @@ def load():
                                           C.c_int32, C.c_uint64, _vp, _vp]),
         "mg_meshscene_sample_pair": (C.c_int, [_vp, _vp, C.c_int32, C.c_int32, C.c_int32, _vp,
                                                _vp, _vp, _vp, C.c_uint64, C.c_uint32, C.c_int32,
-                                               C.c_int32, _vp, _vp, _vp, _vp]),
+                                               C.c_int32, C.c_int32, _vp, _vp, _vp, _vp]),
         "mg_host_malloc": (C.c_int, [C.c_size_t, _vp]),
         "mg_host_free": (C.c_int, [_vp]),
         "mg_copy_async": (C.c_int, [_vp, _vp, _vp, C.c_size_t]),

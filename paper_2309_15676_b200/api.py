@@ -37,6 +37,7 @@ __all__ = ["Context", "Rng", "Moment2", "GradientSamplePair", "MetaEstimator", "
            "FusedAdamUpdate", "MiniRenderRun", "QuadTextureProblem", "QuadTextureRun",
            "HelixProblem", "HelixRun", "helix_spheres", "MeshScene", "MeshTextureProblem",
            "MeshTextureRun", "mesh_scene_geometry", "mesh_scene_view", "smooth_noise_textures",
+           "MeshLargeProblem", "mesh_large_scene_geometry", "large_scene_view",
            "ExperimentConfig", "RunRecord", "AggregateReport", "run_single",
            "run_experiment", "InvalidArgument", "LogicError", "DomainError", "mix64"]
 
@@ -875,35 +876,73 @@ def mesh_scene_geometry(sphere_res=(24, 48), displaced_res=(100, 100), seed: int
     return np.ascontiguousarray(rec), obj, 3
 
 
+def mesh_large_scene_geometry(n_spheres: int = 15, res=(130, 130), seed: int = 5,
+                              displacement: float = 0.15):
+    """BASELINE.json configs[4] geometry: object 0 a ground quad, objects
+    1..n_spheres seeded displaced spheres (radius 0.35) on a 5-wide grid —
+    16 objects and ~502k triangles at the default 130 x 130 tessellation."""
+    quad_v = np.array([[[-3.0, 0.0, -2.5], [3.0, 0.0, -2.5], [3.0, 0.0, 2.5]],
+                       [[-3.0, 0.0, -2.5], [3.0, 0.0, 2.5], [-3.0, 0.0, 2.5]]])
+    quad_w = np.stack([(quad_v[:, :, 0] + 3.0) / 6.0, (quad_v[:, :, 2] + 2.5) / 5.0], axis=-1)
+    rs = np.random.RandomState(seed)
+    Vs, Ws, objs = [quad_v], [quad_w], [np.zeros(2)]
+    for k in range(n_spheres):
+        cx = -2.0 + 1.0 * (k % 5) + rs.uniform(-0.1, 0.1)
+        cz = -1.2 + 1.0 * (k // 5) + rs.uniform(-0.1, 0.1)
+        waves = [(rs.uniform(-1, 1), rs.randint(1, 6), rs.randint(1, 7), rs.uniform(0, 2 * np.pi))
+                 for _ in range(5)]
+
+        def rad(t, p, waves=waves):
+            noise = sum(a * np.sin(m * t) * np.cos(g * p + q) for a, m, g, q in waves) / len(waves)
+            return 0.35 * (1.0 + displacement * noise * 2.0)
+        v, w = _sphere_triangles((cx, 0.4, cz), rad, *res)
+        Vs.append(v)
+        Ws.append(w)
+        objs.append(np.full(len(v), k + 1))
+    V, Wuv = np.concatenate(Vs), np.concatenate(Ws)
+    obj = np.concatenate(objs).astype(np.int32)
+    e1 = V[:, 1] - V[:, 0]
+    e2 = V[:, 2] - V[:, 0]
+    n = np.cross(e1, e2)
+    n = n / np.linalg.norm(n, axis=1, keepdims=True)
+    rec = np.concatenate([V[:, 0], e1, e2, n, Wuv[:, 0], Wuv[:, 1] - Wuv[:, 0],
+                          Wuv[:, 2] - Wuv[:, 0]], axis=1)
+    return np.ascontiguousarray(rec), obj, n_spheres + 1
+
+
 def mesh_scene_view(max_vertices: int = 6, light=(6.0, 6.0, 6.0), env=(0.25, 0.3, 0.35),
-                    cam=(0.0, 1.6, 4.5), look_at=(0.0, 0.45, 0.0), tan_half_fov: float = 0.45):
+                    cam=(0.0, 1.6, 4.5), look_at=(0.0, 0.45, 0.0), tan_half_fov: float = 0.45,
+                    light_y: float = 3.0, light_rect=(-1.0, 1.0, -1.0, 1.0)):
     """view[25] (layout MESH_VIEW_LAYOUT): pinhole camera, rectangular light
-    at y = 3 over x, z in [-1, 1] facing down, constant environment."""
+    at y = light_y over x in [x0, x1], z in [z0, z1] facing down, constant
+    environment."""
     cam = np.asarray(cam, dtype=np.float64)
     fwd = np.asarray(look_at, dtype=np.float64) - cam
     fwd /= np.linalg.norm(fwd)
     right = np.cross(fwd, [0.0, 1.0, 0.0])
     right /= np.linalg.norm(right)
     up = np.cross(right, fwd)
-    return np.concatenate([cam, fwd, right, up, [tan_half_fov, 3.0, -1.0, 1.0, -1.0, 1.0],
+    return np.concatenate([cam, fwd, right, up, [tan_half_fov, light_y, *light_rect],
                            light, env, [float(max_vertices)]]).astype(np.float64)
 
 
 def smooth_noise_textures(nobj: int, R: int, seed: int, grid: int = 6,
-                          base_range=(0.15, 0.85), rough_range=(0.25, 0.9)) -> np.ndarray:
-    """Seeded smooth-noise textures [nobj][4][R*R] (bilinear upsampling of a
-    grid x grid lattice of uniforms): base colour and roughness."""
+                          base_range=(0.15, 0.85), rough_range=(0.25, 0.9), channels: int = 4,
+                          metal_range=(0.0, 0.6)) -> np.ndarray:
+    """Seeded smooth-noise textures [nobj][channels][R*R] (bilinear upsampling
+    of a grid x grid lattice of uniforms): base colour, roughness and (5
+    channels) metalness."""
     rs = np.random.RandomState(seed)
     x = (np.arange(R) + 0.5) / R * (grid - 1)
     i0 = np.minimum(x.astype(int), grid - 2)
     f = x - i0
-    out = np.empty((nobj, 4, R * R))
+    out = np.empty((nobj, channels, R * R))
     for o in range(nobj):
-        for c in range(4):
+        for c in range(channels):
             g = rs.uniform(0, 1, (grid, grid))
             rows = g[i0] * (1 - f)[:, None] + g[i0 + 1] * f[:, None]
             img = rows[:, i0] * (1 - f)[None, :] + rows[:, i0 + 1] * f[None, :]
-            lo, hi = base_range if c < 3 else rough_range
+            lo, hi = base_range if c < 3 else (rough_range if c == 3 else metal_range)
             out[o, c] = (lo + (hi - lo) * img).reshape(-1)
     return out
 
@@ -912,17 +951,17 @@ class MeshScene:
     """A triangle scene on the device (BVH built on the host, mg_meshscene_*)."""
 
     def __init__(self, records: np.ndarray, obj: np.ndarray, nobj: int, tex_res: int, view,
-                 ctx=None):
+                 ctx=None, channels: int = 4):
         self.ctx = ctx or Context.default()
         self.records = np.ascontiguousarray(records, dtype=np.float64)
         self.obj = np.ascontiguousarray(obj, dtype=np.int32)
-        self.nobj, self.R = nobj, tex_res
+        self.nobj, self.R, self.channels = nobj, tex_res, channels
         self.view = np.ascontiguousarray(view, dtype=np.float64)
         h = C.c_void_p()
         check(load().mg_meshscene_create(self.ctx.h, self.records.shape[0],
                                          self.records.ctypes.data_as(C.c_void_p),
                                          self.obj.ctypes.data_as(C.c_void_p), nobj, tex_res,
-                                         C.byref(h)))
+                                         channels, C.byref(h)))
         self.h = h
 
     def info(self):
@@ -932,7 +971,7 @@ class MeshScene:
                 "triangles": self.records.shape[0]}
 
     def params(self) -> int:
-        return self.nobj * 4 * self.R * self.R
+        return self.nobj * self.channels * self.R * self.R
 
     def intersect(self, rays: torch.Tensor):
         """rays: CUDA fp64 [n][6] -> (t [n], triangle [n])"""
@@ -968,15 +1007,22 @@ class MeshTextureProblem:
 
     def __init__(self, width: int = 512, height: int = 512, tex_res: int = 512,
                  sphere_res=(24, 48), displaced_res=(100, 100), max_vertices: int = 6,
-                 target_seed: int = 1, target_spp: int = 16, dtype=torch.float32, ctx=None):
+                 target_seed: int = 1, target_spp: int = 16, dtype=torch.float32, ctx=None,
+                 channels: int = 4, prop_paths: int = 2, geometry=None, view=None):
         self.ctx = ctx or Context.default()
         self.W, self.H, self.R, self.dtype = width, height, tex_res, dtype
-        rec, obj, nobj = mesh_scene_geometry(sphere_res, displaced_res)
-        self.scene = MeshScene(rec, obj, nobj, tex_res, mesh_scene_view(max_vertices), self.ctx)
+        self.channels, self.prop_paths = channels, prop_paths
+        rec, obj, nobj = geometry if geometry is not None else \
+            mesh_scene_geometry(sphere_res, displaced_res)
+        view = view if view is not None else mesh_scene_view(max_vertices)
+        self.scene = MeshScene(rec, obj, nobj, tex_res, view, self.ctx, channels)
         n = self.scene.params()
-        self.target_tex = torch.tensor(smooth_noise_textures(nobj, tex_res, target_seed).reshape(-1),
-                                       device="cuda").to(dtype)
-        init = np.full((nobj, 4, tex_res * tex_res), 0.5)
+        self.target_tex = torch.tensor(
+            smooth_noise_textures(nobj, tex_res, target_seed, channels=channels).reshape(-1),
+            device="cuda").to(dtype)
+        init = np.full((nobj, channels, tex_res * tex_res), 0.5)
+        if channels == 5:
+            init[:, 4] = 0.1
         self.init = torch.tensor(init.reshape(-1), device="cuda").to(dtype)
         self.target_img = self.scene.render(self.target_tex, width, height, target_spp,
                                             int(load().mg_mix64(target_seed)))
@@ -987,7 +1033,8 @@ class MeshTextureProblem:
         return self.scene.params()
 
     def draws_per_sample(self) -> int:
-        return 3 * self.W * self.H
+        """Paths per iteration: prop_paths proportional + 1 finite-difference spp."""
+        return (self.prop_paths + 1) * self.W * self.H
 
     def initial_params(self):
         return self.init.clone()
@@ -998,9 +1045,32 @@ class MeshTextureProblem:
         check(load().mg_meshscene_sample_pair(
             self.ctx.h, self.scene.h, _dtype_code(now), self.W, self.H,
             self.scene.view.ctypes.data_as(C.c_void_p), _p(self.target_img), _p(now.contiguous()),
-            _p(prev.contiguous()), key, iteration, r0, r1, _p(self.accum), _p(prop), _p(diff),
-            _p(self.loss_buf)))
+            _p(prev.contiguous()), key, iteration, r0, r1, self.prop_paths, _p(self.accum),
+            _p(prop), _p(diff), _p(self.loss_buf)))
         return GradientSamplePair(prop, diff)
+
+
+def large_scene_view(max_vertices: int = 8):
+    """configs[4] camera/light over the 5 x 3 grid of objects."""
+    return mesh_scene_view(max_vertices, light=(8.0, 8.0, 8.0), cam=(0.0, 2.8, 4.4),
+                           look_at=(0.0, 0.2, -0.3), tan_half_fov=0.55, light_y=3.5,
+                           light_rect=(-1.5, 1.5, -1.5, 1.0))
+
+
+class MeshLargeProblem(MeshTextureProblem):
+    """BASELINE.json configs[4]: 1024 x 1024 image, 16 objects (ground quad +
+    15 seeded displaced spheres, ~502k triangles), each with a 1024 x 1024
+    texture of base r, g, b, roughness and metalness (16 * 5 * 1024^2 =
+    83.9M parameters), depth 8 with NEE, 1 FD + 4 proportional spp."""
+
+    def __init__(self, width: int = 1024, height: int = 1024, tex_res: int = 1024,
+                 res=(130, 130), max_vertices: int = 8, target_seed: int = 1,
+                 target_spp: int = 4, dtype=torch.float32, ctx=None, prop_paths: int = 4):
+        super().__init__(width, height, tex_res, max_vertices=max_vertices,
+                         target_seed=target_seed, target_spp=target_spp, dtype=dtype, ctx=ctx,
+                         channels=5, prop_paths=prop_paths,
+                         geometry=mesh_large_scene_geometry(res=res),
+                         view=large_scene_view(max_vertices))
 
 
 class MeshTextureRun(QuadTextureRun):

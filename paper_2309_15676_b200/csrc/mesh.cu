@@ -30,7 +30,7 @@
 #include "philox.cuh"
 
 struct mg_mesh_scene {
-  int T = 0, nobj = 0, R = 0, nnodes = 0, depth = 0;
+  int T = 0, nobj = 0, R = 0, nnodes = 0, depth = 0, nch = 4;
   double* tri = nullptr;   // [T][18] in BVH order
   int* orig = nullptr;     // [T] original triangle index
   int* obj = nullptr;      // [T] object id (BVH order)
@@ -189,7 +189,7 @@ struct MeshDev {
 };
 
 struct MeshK {
-  int W, H, R, nobj;
+  int W, H, R, nobj, nch;
   int row0, row1;
   double view[25];
   uint64_t key;
@@ -393,6 +393,46 @@ __device__ __forceinline__ void bsdf_m0(const T base[3], T rough, const T n[3], 
   dS = dDG_drough * F;
 }
 
+// full principled BSDF (configs[4], metalness texture): f[c] and
+// df[c][k] = d f_c / d(base_c, metal, rough) — the oracle's hx_bsdf
+template <class T>
+__device__ __forceinline__ void bsdf_full(const T base[3], T metal, T rough, const T n[3],
+                                          const T wi[3], const T wo[3], T f[3], T df[3][3]) {
+  const T alpha = T(0.05) + T(0.95) * (rough * rough);
+  const T a2 = alpha * alpha;
+  T h[3] = {wi[0] + wo[0], wi[1] + wo[1], wi[2] + wo[2]};
+  const T hl = sqrt((h[0] * h[0] + h[1] * h[1]) + h[2] * h[2]);
+  h[0] /= hl;
+  h[1] /= hl;
+  h[2] /= hl;
+  auto dt = [](const T* a, const T* b) { return (a[0] * b[0] + a[1] * b[1]) + a[2] * b[2]; };
+  const T nh = dt(n, h), ni = dt(n, wi), no = dt(n, wo), ih = dt(wi, h);
+  const T den = nh * nh * (a2 - T(1)) + T(1);
+  const T D = a2 / (T(kPiM) * (den * den));
+  const T dD_da2 = (den - T(2) * a2 * (nh * nh)) / (T(kPiM) * ((den * den) * den));
+  const T si = sqrt(a2 + (T(1) - a2) * (ni * ni));
+  const T so = sqrt(a2 + (T(1) - a2) * (no * no));
+  const T G1i = (T(2) * ni) / (ni + si), G1o = (T(2) * no) / (no + so);
+  const T dG1i = ((T(-2) * ni) / ((ni + si) * (ni + si))) * ((T(1) - ni * ni) / (T(2) * si));
+  const T dG1o = ((T(-2) * no) / ((no + so) * (no + so))) * ((T(1) - no * no) / (T(2) * so));
+  const T G = G1i * G1o;
+  const T dG_da2 = dG1i * G1o + G1i * dG1o;
+  const T q = T(1) - ih;
+  const T q5 = ((q * q) * (q * q)) * q;
+  const T denom = T(4) * ni * no;
+  const T DG = (D * G) / denom;
+  const T dDG_drough = (((dD_da2 * G + D * dG_da2) / denom) * (T(2) * alpha)) * (T(1.9) * rough);
+#pragma unroll
+  for (int c = 0; c < 3; ++c) {
+    const T F0 = T(0.04) * (T(1) - metal) + base[c] * metal;
+    const T F = F0 + (T(1) - F0) * q5;
+    f[c] = ((T(1) - metal) * base[c]) / T(kPiM) + DG * F;
+    df[c][0] = (T(1) - metal) / T(kPiM) + DG * (metal * (T(1) - q5));
+    df[c][1] = (-base[c]) / T(kPiM) + DG * ((base[c] - T(0.04)) * (T(1) - q5));
+    df[c][2] = dDG_drough * F;
+  }
+}
+
 template <class T, int NS>
 struct PathStore {
   int base[kMaxV];
@@ -408,7 +448,7 @@ struct NoStore {};
 // One path for NS parameter sets (th[0] = theta_t, th[1] = theta_{t-1});
 // radiance L[s][c], environment after the last vertex E[s][c]; per-vertex
 // adjoint data into *st when STORE.  Returns the number of vertices.
-template <class T, int NS, bool STORE, class Store>
+template <class T, int NS, bool STORE, class Store, int NCH = 4>
 __device__ __noinline__ int mesh_path(const MeshK& q, const MeshDev& m, const float4* sn, int* stk,
                                      const T* const th[2],
                          int px, int py, uint32_t it, uint32_t path, T L[NS][3], T E[NS][3],
@@ -467,7 +507,8 @@ __device__ __noinline__ int mesh_path(const MeshK& q, const MeshDev& m, const fl
     int tx = int(U * q.R), ty = int(W_ * q.R);
     tx = tx < 0 ? 0 : (tx > q.R - 1 ? q.R - 1 : tx);
     ty = ty < 0 ? 0 : (ty > q.R - 1 ? q.R - 1 : ty);
-    const int pbase = __ldg(&m.obj[slot]) * 4 * R2 + ty * q.R + tx;
+    static_assert(NCH == 4 || !STORE, "stored paths are the configs[3] form");
+    const int pbase = __ldg(&m.obj[slot]) * NCH * R2 + ty * q.R + tx;
     if constexpr (STORE) {
       st->base[nv] = pbase;
 #pragma unroll
@@ -484,12 +525,13 @@ __device__ __noinline__ int mesh_path(const MeshK& q, const MeshDev& m, const fl
     }
     const int vi = nv;
     ++nv;
-    T base[NS][3], rough[NS];
+    T base[NS][3], rough[NS], metal[NS];
 #pragma unroll
     for (int s = 0; s < NS; ++s) {
 #pragma unroll
       for (int c = 0; c < 3; ++c) base[s][c] = th[s][pbase + c * R2];
       rough[s] = th[s][pbase + 3 * R2];
+      metal[s] = NCH == 5 ? th[s][pbase + 4 * R2] : T(0);
     }
     const double wo[3] = {-d[0], -d[1], -d[2]};
     const double xo[3] = {x[0] + kOff * n[0], x[1] + kOff * n[1], x[2] + kOff * n[2]};
@@ -511,7 +553,12 @@ __device__ __noinline__ int mesh_path(const MeshK& q, const MeshDev& m, const fl
 #pragma unroll
         for (int s = 0; s < NS; ++s) {
           T f[3], dS;
-          bsdf_m0<T>(base[s], rough[s], nT, wT, woT, f, dS);
+          if constexpr (NCH == 5) {
+            T df[3][3];
+            bsdf_full<T>(base[s], metal[s], rough[s], nT, wT, woT, f, df);
+          } else {
+            bsdf_m0<T>(base[s], rough[s], nT, wT, woT, f, dS);
+          }
           if constexpr (STORE) st->dSn[s][vi] = dS;
 #pragma unroll
           for (int c = 0; c < 3; ++c) {
@@ -565,7 +612,12 @@ __device__ __noinline__ int mesh_path(const MeshK& q, const MeshDev& m, const fl
 #pragma unroll
     for (int s = 0; s < NS; ++s) {
       T f[3], dS;
-      bsdf_m0<T>(base[s], rough[s], nT, wiT, woT, f, dS);
+      if constexpr (NCH == 5) {
+        T df[3][3];
+        bsdf_full<T>(base[s], metal[s], rough[s], nT, wiT, woT, f, df);
+      } else {
+        bsdf_m0<T>(base[s], rough[s], nT, wiT, woT, f, dS);
+      }
       if constexpr (STORE) st->dSb[s][vi] = dS;
 #pragma unroll
       for (int c = 0; c < 3; ++c) {
@@ -618,7 +670,7 @@ __device__ __forceinline__ void stage_nodes(const MeshDev& m, float4* sn) {
   int* stk = nullptr;                   \
   stage_nodes(m, sn)
 
-template <class T>
+template <class T, int NCH>
 __global__ void __launch_bounds__(kMThreads)
     mesh_render_kernel(MeshK q, MeshDev m, int spp, const T* __restrict__ theta,
                        T* __restrict__ img) {
@@ -630,8 +682,8 @@ __global__ void __launch_bounds__(kMThreads)
     double acc[3] = {0.0, 0.0, 0.0};
     for (int s = 0; s < spp; ++s) {
       T L[1][3], E[1][3];
-      mesh_path<T, 1, false, NoStore>(q, m, sn, stk, th, px, py, 0xffffffffu, uint32_t(s), L, E,
-                                      nullptr);
+      mesh_path<T, 1, false, NoStore, NCH>(q, m, sn, stk, th, px, py, 0xffffffffu, uint32_t(s),
+                                           L, E, nullptr);
 #pragma unroll
       for (int c = 0; c < 3; ++c) acc[c] += double(L[0][c]);
     }
@@ -727,16 +779,30 @@ __global__ void mesh_intersect_kernel(MeshDev m, int n, const double* __restrict
 // ------------------------------------------------------------ wavefront
 // The same estimator as mesh_pair_kernel, restructured into stages over
 // SoA path state (north_star: "wavefront layout with coalesced SoA path
-// state"): paths P = 3 x pixels (A, B, C path-major), then per depth
+// state"): paths P = (nprop + 1) x pixels (proportional paths 0..nprop-1,
+// path 0 also at theta_{t-1}; FD path nprop), then per depth
 //   isect  : closest hit of every live path (all lanes traverse at once)
 //   shade  : texel lookup, NEE sample + shadow-ray set-up, the BSDF values
 //            for both parameter sets, Malley bounce; survivors re-queued
 //   shadow : any-hit of the queued NEE rays; visible -> L += C
 // and finally one thread per pixel forms the residual weights and scatters
-// the stored adjoint data of paths A and B.  Every per-path quantity is the
-// megakernel's (same operations, same order), so results are bit-identical
-// to it and to the oracle.
-constexpr int kVF = 22;  // per-vertex T fields: A[6] dSn[2] invfb[6] dSb[2] C[6]
+// the stored adjoint data of the proportional paths.  Every per-path
+// quantity is the megakernel's / oracle's (same operations, same order),
+// so the results are bit-identical to both.
+//
+// Per-vertex adjoint fields (T, [v][field][PS]):
+//   NCH 4 (metal 0): A[6] dSn[2] invfb[6] dSb[2] C[6]                 = 22
+//   NCH 5          : A[6] invfb[6] C[6] dfn[2][3][3] dfb[2][3][3]      = 54
+template <int NCH>
+struct VF;
+template <>
+struct VF<4> {
+  static constexpr int n = 22, A = 0, dSn = 6, invfb = 8, dSb = 14, C = 16;
+};
+template <>
+struct VF<5> {
+  static constexpr int n = 54, A = 0, invfb = 6, C = 12, dfn = 18, dfb = 36;
+};
 
 template <class T>
 struct WF {
@@ -746,21 +812,21 @@ struct WF {
   T *beta, *L, *E, *pendC;                    // [6][P]
   int *nv, *hslot, *q0, *q1, *sq;             // [P]
   int* vbase;                                 // [kMaxV][PS]
-  T* vdat;                                    // [kMaxV][kVF][PS]
+  T* vdat;                                    // [kMaxV][nvf][PS]
   unsigned int* cnt;                          // [2][kMaxV + 1]: queue / shadow counts
-  int P, PS, npix, pix0;
+  int P, PS, npix, pix0, nprop, nvf;
 };
 
 template <class T>
-size_t wf_bytes(int P) {
-  const size_t PS = size_t(2) * (P / 3);
-  return sizeof(double) * 16 * size_t(P) + sizeof(T) * 24 * size_t(P) + sizeof(int) * 5 * size_t(P) +
-         sizeof(int) * kMaxV * PS + sizeof(T) * kMaxV * kVF * PS +
-         sizeof(unsigned int) * 2 * (kMaxV + 1) + 64 * 40;
+size_t wf_bytes(int npix, int nprop, int nvf) {
+  const size_t P = size_t(npix) * (nprop + 1), PS = size_t(npix) * nprop;
+  return sizeof(double) * 16 * P + sizeof(T) * 24 * P + sizeof(int) * 5 * P +
+         sizeof(int) * kMaxV * PS + sizeof(T) * kMaxV * nvf * PS +
+         sizeof(unsigned int) * 2 * (kMaxV + 1) + 256 * 40;
 }
 
 template <class T>
-WF<T> wf_carve(void* mem, int P) {
+WF<T> wf_carve(void* mem, int npix, int nprop, int nvf) {
   WF<T> w;
   char* c = static_cast<char*>(mem);
   auto take = [&](size_t bytes) {
@@ -768,10 +834,12 @@ WF<T> wf_carve(void* mem, int P) {
     c += (bytes + 255) & ~size_t(255);
     return r;
   };
-  const size_t Pz = size_t(P);
-  w.P = P;
-  w.npix = P / 3;
-  w.PS = 2 * w.npix;
+  w.npix = npix;
+  w.nprop = nprop;
+  w.nvf = nvf;
+  w.P = npix * (nprop + 1);
+  w.PS = npix * nprop;
+  const size_t Pz = size_t(w.P);
   double** dd[] = {&w.ox, &w.oy, &w.oz, &w.dx, &w.dy, &w.dz, &w.ht, &w.hu, &w.hv,
                    &w.sox, &w.soy, &w.soz, &w.sdx, &w.sdy, &w.sdz, &w.stm};
   for (double** d : dd) *d = (double*)take(sizeof(double) * Pz);
@@ -780,7 +848,7 @@ WF<T> wf_carve(void* mem, int P) {
   int** ii[] = {&w.nv, &w.hslot, &w.q0, &w.q1, &w.sq};
   for (int** i : ii) *i = (int*)take(sizeof(int) * Pz);
   w.vbase = (int*)take(sizeof(int) * kMaxV * size_t(w.PS));
-  w.vdat = (T*)take(sizeof(T) * kMaxV * kVF * size_t(w.PS));
+  w.vdat = (T*)take(sizeof(T) * kMaxV * size_t(nvf) * size_t(w.PS));
   w.cnt = (unsigned int*)take(sizeof(unsigned int) * 2 * (kMaxV + 1));
   return w;
 }
@@ -798,7 +866,7 @@ __device__ __forceinline__ int enqueue(bool pred, unsigned int* counter) {
 
 template <class T>
 __device__ __forceinline__ T& vf(const WF<T>& w, int v, int f, int p) {
-  return w.vdat[(size_t(v) * kVF + f) * size_t(w.PS) + p];
+  return w.vdat[(size_t(v) * w.nvf + f) * size_t(w.PS) + p];
 }
 
 template <class T>
@@ -851,10 +919,11 @@ __global__ void __launch_bounds__(kMThreads) wf_isect_kernel(MeshDev m, WF<T> w,
   }
 }
 
-template <class T>
+template <class T, int NCH>
 __global__ void __launch_bounds__(kMThreads)
     wf_shade_kernel(MeshK q, MeshDev m, WF<T> w, int v, const T* __restrict__ th0,
                     const T* __restrict__ th1) {
+  using F = VF<NCH>;
   const double* V = q.view;
   const int maxv = int(V[24]);
   const int R2 = q.R * q.R;
@@ -902,19 +971,19 @@ __global__ void __launch_bounds__(kMThreads)
         int tx = int(U * q.R), ty = int(W_ * q.R);
         tx = tx < 0 ? 0 : (tx > q.R - 1 ? q.R - 1 : tx);
         ty = ty < 0 ? 0 : (ty > q.R - 1 ? q.R - 1 : ty);
-        const int pbase = __ldg(&m.obj[slot]) * 4 * R2 + ty * q.R + tx;
+        const int pbase = __ldg(&m.obj[slot]) * NCH * R2 + ty * q.R + tx;
         w.nv[p] = v + 1;
         if (store) {
           w.vbase[size_t(v) * w.PS + p] = pbase;
-#pragma unroll
-          for (int f = 0; f < kVF; ++f) vf(w, v, f, p) = T(0);
+          for (int f = 0; f < F::n; ++f) vf(w, v, f, p) = T(0);
         }
-        T base[2][3], rough[2];
+        T base[2][3], rough[2], metal[2];
 #pragma unroll
         for (int s = 0; s < 2; ++s) {
 #pragma unroll
           for (int c = 0; c < 3; ++c) base[s][c] = th[s][pbase + c * R2];
           rough[s] = th[s][pbase + 3 * R2];
+          metal[s] = NCH == 5 ? th[s][pbase + 4 * R2] : T(0);
         }
         const double wo[3] = {-d[0], -d[1], -d[2]};
         const double xo[3] = {x[0] + kOff * nn[0], x[1] + kOff * nn[1], x[2] + kOff * nn[2]};
@@ -936,16 +1005,27 @@ __global__ void __launch_bounds__(kMThreads)
           const T wT[3] = {T(wl3[0]), T(wl3[1]), T(wl3[2])};
 #pragma unroll
           for (int s = 0; s < 2; ++s) {
-            T f[3], dS;
-            bsdf_m0<T>(base[s], rough[s], nT, wT, woT, f, dS);
-            if (store) vf(w, v, 6 + s, p) = dS;
+            T f[3];
+            if constexpr (NCH == 5) {
+              T df[3][3];
+              bsdf_full<T>(base[s], metal[s], rough[s], nT, wT, woT, f, df);
+              if (store)
+#pragma unroll
+                for (int c = 0; c < 3; ++c)
+#pragma unroll
+                  for (int kk = 0; kk < 3; ++kk) vf(w, v, F::dfn + s * 9 + c * 3 + kk, p) = df[c][kk];
+            } else {
+              T dS;
+              bsdf_m0<T>(base[s], rough[s], nT, wT, woT, f, dS);
+              if (store) vf(w, v, VF<4>::dSn + s, p) = dS;
+            }
 #pragma unroll
             for (int c = 0; c < 3; ++c) {
               const T A = beta[s][c] * T(gl * V[18 + c]);
               const T Cc = A * f[c];
               if (store) {
-                vf(w, v, s * 3 + c, p) = A;
-                vf(w, v, 16 + s * 3 + c, p) = Cc;
+                vf(w, v, F::A + s * 3 + c, p) = A;
+                vf(w, v, F::C + s * 3 + c, p) = Cc;
               }
               w.pendC[size_t(s * 3 + c) * w.P + p] = Cc;
             }
@@ -995,12 +1075,24 @@ __global__ void __launch_bounds__(kMThreads)
             const T wiT[3] = {T(wi[0]), T(wi[1]), T(wi[2])};
 #pragma unroll
             for (int s = 0; s < 2; ++s) {
-              T f[3], dS;
-              bsdf_m0<T>(base[s], rough[s], nT, wiT, woT, f, dS);
-              if (store) vf(w, v, 14 + s, p) = dS;
+              T f[3];
+              if constexpr (NCH == 5) {
+                T df[3][3];
+                bsdf_full<T>(base[s], metal[s], rough[s], nT, wiT, woT, f, df);
+                if (store)
+#pragma unroll
+                  for (int c = 0; c < 3; ++c)
+#pragma unroll
+                    for (int kk = 0; kk < 3; ++kk)
+                      vf(w, v, F::dfb + s * 9 + c * 3 + kk, p) = df[c][kk];
+              } else {
+                T dS;
+                bsdf_m0<T>(base[s], rough[s], nT, wiT, woT, f, dS);
+                if (store) vf(w, v, VF<4>::dSb + s, p) = dS;
+              }
 #pragma unroll
               for (int c = 0; c < 3; ++c) {
-                if (store) vf(w, v, 8 + s * 3 + c, p) = f[c] != T(0) ? T(1) / f[c] : T(0);
+                if (store) vf(w, v, F::invfb + s * 3 + c, p) = f[c] != T(0) ? T(1) / f[c] : T(0);
                 w.beta[size_t(s * 3 + c) * w.P + p] = beta[s][c] * (f[c] * T(kPiM));
               }
             }
@@ -1022,8 +1114,9 @@ __global__ void __launch_bounds__(kMThreads)
   }
 }
 
-template <class T>
+template <class T, int NCH>
 __global__ void __launch_bounds__(kMThreads) wf_shadow_kernel(MeshDev m, WF<T> w, int v) {
+  using F = VF<NCH>;
   MESH_SMEM;
   const int n = int(w.cnt[kMaxV + 1 + v]);
   for (int i = blockIdx.x * kMThreads + threadIdx.x; i < n; i += gridDim.x * kMThreads) {
@@ -1033,67 +1126,106 @@ __global__ void __launch_bounds__(kMThreads) wf_shadow_kernel(MeshDev m, WF<T> w
     if (trace<true>(m, sn, stk, o, d, w.stm[p], ts, tu, tv) < 0) {
 #pragma unroll
       for (int j = 0; j < 6; ++j) w.L[size_t(j) * w.P + p] += w.pendC[size_t(j) * w.P + p];
-    } else if (p < w.PS) {
+    } else if (p < w.PS) {  // occluded: no NEE data at this vertex
 #pragma unroll
       for (int j = 0; j < 6; ++j) {
-        vf(w, v, j, p) = T(0);
-        vf(w, v, 16 + j, p) = T(0);
+        vf(w, v, F::A + j, p) = T(0);
+        vf(w, v, F::C + j, p) = T(0);
       }
-      vf(w, v, 6, p) = T(0);
-      vf(w, v, 7, p) = T(0);
+      if constexpr (NCH == 5) {
+        for (int j = 0; j < 18; ++j) vf(w, v, VF<5>::dfn + j, p) = T(0);
+      } else {
+        vf(w, v, VF<4>::dSn, p) = T(0);
+        vf(w, v, VF<4>::dSn + 1, p) = T(0);
+      }
     }
   }
 }
 
-// adjoint of stored path p (megakernel `scatter`, SoA storage)
-template <class T>
+// adjoint of stored path p (megakernel `scatter` / oracle ms_scatter)
+template <class T, int NCH>
 __device__ __noinline__ void wf_scatter(const WF<T>& w, int p, int s, const T wt[3], int R2,
                                         unsigned long long* __restrict__ acc) {
+  using F = VF<NCH>;
   T Q[3];
 #pragma unroll
   for (int c = 0; c < 3; ++c) Q[c] = w.E[size_t(s * 3 + c) * w.P + p];
   for (int v = w.nv[p] - 1; v >= 0; --v) {
     const int base = w.vbase[size_t(v) * w.PS + p];
-    const T dSn = vf(w, v, 6 + s, p), dSb = vf(w, v, 14 + s, p);
-    T gr = T(0);
+    if constexpr (NCH == 5) {
+      T gm = T(0), gr = T(0);
 #pragma unroll
-    for (int c = 0; c < 3; ++c) {
-      const T A = vf(w, v, s * 3 + c, p), ifb = vf(w, v, 8 + s * 3 + c, p);
-      const T gb = wt[c] * ((A / T(kPiM)) + Q[c] * (ifb / T(kPiM)));
-      atomicAdd(&acc[base + c * R2], fixq(double(gb)));
-      gr += wt[c] * (A * dSn + Q[c] * (ifb * dSb));
+      for (int c = 0; c < 3; ++c) {
+        const T A = vf(w, v, F::A + s * 3 + c, p), fb = vf(w, v, F::invfb + s * 3 + c, p);
+        const int dn = F::dfn + s * 9 + c * 3, db = F::dfb + s * 9 + c * 3;
+        const T gb = wt[c] * (A * vf(w, v, dn, p) + Q[c] * (fb * vf(w, v, db, p)));
+        atomicAdd(&acc[base + c * R2], fixq(double(gb)));
+        gm += wt[c] * (A * vf(w, v, dn + 1, p) + Q[c] * (fb * vf(w, v, db + 1, p)));
+        gr += wt[c] * (A * vf(w, v, dn + 2, p) + Q[c] * (fb * vf(w, v, db + 2, p)));
+      }
+      atomicAdd(&acc[base + 3 * R2], fixq(double(gr)));
+      atomicAdd(&acc[base + 4 * R2], fixq(double(gm)));
+    } else {
+      const T dSn = vf(w, v, F::dSn + s, p), dSb = vf(w, v, F::dSb + s, p);
+      T gr = T(0);
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        const T A = vf(w, v, F::A + s * 3 + c, p), ifb = vf(w, v, F::invfb + s * 3 + c, p);
+        const T gb = wt[c] * ((A / T(kPiM)) + Q[c] * (ifb / T(kPiM)));
+        atomicAdd(&acc[base + c * R2], fixq(double(gb)));
+        gr += wt[c] * (A * dSn + Q[c] * (ifb * dSb));
+      }
+      atomicAdd(&acc[base + 3 * R2], fixq(double(gr)));
     }
-    atomicAdd(&acc[base + 3 * R2], fixq(double(gr)));
 #pragma unroll
-    for (int c = 0; c < 3; ++c) Q[c] = Q[c] + vf(w, v, 16 + s * 3 + c, p);
+    for (int c = 0; c < 3; ++c) Q[c] = Q[c] + vf(w, v, F::C + s * 3 + c, p);
   }
 }
 
-template <class T>
+constexpr int kMaxProp = 8;
+
+template <class T, int NCH>
 __global__ void __launch_bounds__(kMThreads)
     wf_scatter_kernel(MeshK q, WF<T> w, const T* __restrict__ target_img,
                       unsigned long long* __restrict__ acc, long long np,
                       ReducePartials* partials, unsigned int* counter, double* loss_out) {
   const int npix_img = q.W * q.H;
   const int R2 = q.R * q.R;
+  const int n = w.nprop;
+  const T scale = T(2.0 / (n * (n - 1.0)));
   double loss = 0.0;
   for (int i = blockIdx.x * kMThreads + threadIdx.x; i < w.npix; i += gridDim.x * kMThreads) {
     const int pix = w.pix0 + i;
-    const int pa = i, pb = w.npix + i, pc = 2 * w.npix + i;
-    T rA[3], rB[3], wC0[3], wC1[3];
+    const int pc = n * w.npix + i;
+    T r[kMaxProp][3], wC0[3], wC1[3];
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
       const T Is = target_img[size_t(c) * npix_img + pix];
-      rA[c] = w.L[size_t(c) * w.P + pa] - Is;
-      rB[c] = w.L[size_t(c) * w.P + pb] - Is;
+      for (int j = 0; j < n; ++j) r[j][c] = w.L[size_t(c) * w.P + j * w.npix + i] - Is;
       wC0[c] = T(2) * (w.L[size_t(c) * w.P + pc] - Is);
       wC1[c] = T(-2) * (w.L[size_t(3 + c) * w.P + pc] - Is);
-      loss += double(rA[c] * rB[c]);
+      T lp = T(0);
+      for (int a = 0; a < n; ++a)
+        for (int b = a + 1; b < n; ++b) lp += r[a][c] * r[b][c];
+      loss += double(lp * scale);
     }
-    wf_scatter<T>(w, pa, 0, rB, R2, acc);
-    wf_scatter<T>(w, pa, 0, wC0, R2, acc + np);
-    wf_scatter<T>(w, pa, 1, wC1, R2, acc + np);
-    wf_scatter<T>(w, pb, 0, rA, R2, acc);
+    for (int j = 0; j < n; ++j) {
+      T wt[3];
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        T a = T(0);
+        bool first = true;
+        for (int k = 0; k < n; ++k) {
+          if (k == j) continue;
+          a = first ? r[k][c] : a + r[k][c];
+          first = false;
+        }
+        wt[c] = a * scale;
+      }
+      wf_scatter<T, NCH>(w, j * w.npix + i, 0, wt, R2, acc);
+    }
+    wf_scatter<T, NCH>(w, i, 0, wC0, R2, acc + np);
+    wf_scatter<T, NCH>(w, i, 1, wC1, R2, acc + np);
   }
   Acc a;
   a.ssn = loss;
@@ -1118,6 +1250,7 @@ MeshK make_k(const mg_mesh_scene* s, int W, int H, const double* view, uint64_t 
   q.H = H;
   q.R = s->R;
   q.nobj = s->nobj;
+  q.nch = s->nch;
   q.row0 = 0;
   q.row1 = H;
   for (int i = 0; i < 25; ++i) q.view[i] = view[i];
@@ -1127,8 +1260,8 @@ MeshK make_k(const mg_mesh_scene* s, int W, int H, const double* view, uint64_t 
 }
 
 }  // namespace
-template <class T>
-int wavefront_pair(mg_ctx* ctx, mg_mesh_scene* s, const MeshK& q, const T* target_img,
+template <class T, int NCH>
+int wavefront_pair(mg_ctx* ctx, mg_mesh_scene* s, const MeshK& q, int nprop, const T* target_img,
                    const T* now, const T* prev, unsigned long long* acc, long long np,
                    double* loss_out) {
   const int npix = q.W * (q.row1 - q.row0);
@@ -1136,9 +1269,8 @@ int wavefront_pair(mg_ctx* ctx, mg_mesh_scene* s, const MeshK& q, const T* targe
     MG_CUDA_TRY(cudaMemsetAsync(loss_out, 0, sizeof(double), ctx->stream));
     return MG_OK;
   }
-  if (int64_t(npix) * 3 > 0x7fffffffLL) return fail(MG_EINVAL, "mesh scene: image too large");
-  const int P = 3 * npix;
-  const size_t need = wf_bytes<T>(P);
+  if (int64_t(npix) * (nprop + 1) > 0x7fffffffLL) return fail(MG_EINVAL, "mesh scene: image too large");
+  const size_t need = wf_bytes<T>(npix, nprop, VF<NCH>::n);
   if (need > s->wf_cap) {
     MG_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
     cudaFree(s->wf);
@@ -1147,23 +1279,23 @@ int wavefront_pair(mg_ctx* ctx, mg_mesh_scene* s, const MeshK& q, const T* targe
     MG_CUDA_TRY(cudaMalloc(&s->wf, need));
     s->wf_cap = need;
   }
-  WF<T> w = wf_carve<T>(s->wf, P);
+  WF<T> w = wf_carve<T>(s->wf, npix, nprop, VF<NCH>::n);
   w.pix0 = q.row0 * q.W;
   const MeshDev m = dev_of(s);
   MG_CUDA_TRY(cudaMemsetAsync(w.cnt, 0, sizeof(unsigned int) * 2 * (kMaxV + 1), ctx->stream));
-  const int grid = grid_for(ctx, P, kMThreads, 8);
+  const int grid = grid_for(ctx, w.P, kMThreads, 8);
   wf_gen_kernel<T><<<grid, kMThreads, 0, ctx->stream>>>(q, w);
   MG_LAUNCH_CHECK(ctx);
   const int maxv = int(q.view[24]);
   for (int v = 0; v < maxv; ++v) {
     wf_isect_kernel<T><<<grid, kMThreads, 0, ctx->stream>>>(m, w, v);
     MG_LAUNCH_CHECK(ctx);
-    wf_shade_kernel<T><<<grid, kMThreads, 0, ctx->stream>>>(q, m, w, v, now, prev);
+    wf_shade_kernel<T, NCH><<<grid, kMThreads, 0, ctx->stream>>>(q, m, w, v, now, prev);
     MG_LAUNCH_CHECK(ctx);
-    wf_shadow_kernel<T><<<grid, kMThreads, 0, ctx->stream>>>(m, w, v);
+    wf_shadow_kernel<T, NCH><<<grid, kMThreads, 0, ctx->stream>>>(m, w, v);
     MG_LAUNCH_CHECK(ctx);
   }
-  wf_scatter_kernel<T><<<grid_for(ctx, npix, kMThreads, 8), kMThreads, 0, ctx->stream>>>(
+  wf_scatter_kernel<T, NCH><<<grid_for(ctx, npix, kMThreads, 8), kMThreads, 0, ctx->stream>>>(
       q, w, target_img, acc, np, ctx->partials, ctx->counter, loss_out);
   MG_LAUNCH_CHECK(ctx);
   return MG_OK;
@@ -1176,12 +1308,15 @@ using namespace mg;
 extern "C" {
 
 int mg_meshscene_create(mg_ctx* ctx, int32_t tri_count, const double* tri, const int32_t* obj,
-                        int32_t nobj, int32_t tex_res, mg_mesh_scene** out) {
+                        int32_t nobj, int32_t tex_res, int32_t channels, mg_mesh_scene** out) {
   if (!ctx || !tri || !obj || !out) return fail(MG_EINVAL, "mg_meshscene_create: null argument");
+  if (channels != 4 && channels != 5)
+    return fail(MG_EINVAL, "mg_meshscene_create: channels must be 4 (base rgb, roughness) or 5 "
+                           "(+ metalness)");
   if (tri_count < 1 || nobj < 1 || tex_res < 1)
     return fail(MG_EINVAL, "mg_meshscene_create: bad sizes");
   if (tri_count > (1 << 27)) return fail(MG_EINVAL, "mg_meshscene_create: more than 2^27 triangles");
-  if (int64_t(nobj) * 4 * tex_res * tex_res > 0x7fffffffLL)
+  if (int64_t(nobj) * channels * tex_res * tex_res > 0x7fffffffLL)
     return fail(MG_EINVAL, "mg_meshscene_create: parameter count exceeds 2^31");
   for (int k = 0; k < tri_count; ++k)
     if (obj[k] < 0 || obj[k] >= nobj) return fail(MG_EINVAL, "mg_meshscene_create: bad object id");
@@ -1277,6 +1412,7 @@ int mg_meshscene_create(mg_ctx* ctx, int32_t tri_count, const double* tri, const
   mg_mesh_scene* sc = new mg_mesh_scene();
   sc->T = tri_count;
   sc->nobj = nobj;
+  sc->nch = channels;
   sc->R = tex_res;
   sc->nnodes = nn;
   sc->depth = B.max_depth;
@@ -1320,7 +1456,7 @@ int mg_meshscene_info(const mg_mesh_scene* s, int32_t* nodes, int32_t* depth, in
   if (!s) return fail(MG_EINVAL, "mg_meshscene_info: null scene");
   if (nodes) *nodes = s->nnodes;
   if (depth) *depth = s->depth;
-  if (params) *params = int64_t(s->nobj) * 4 * s->R * s->R;
+  if (params) *params = int64_t(s->nobj) * s->nch * s->R * s->R;
   return MG_OK;
 }
 
@@ -1351,14 +1487,19 @@ int mg_meshscene_render(mg_ctx* ctx, const mg_mesh_scene* s, int32_t dtype, int3
   if (st) return st;
   const MeshK q = make_k(s, W, H, view, key, 0xffffffffu);
   const int grid = grid_for(ctx, int64_t(W) * H, kMThreads, 4);
-  if (dtype == MG_F64)
-    mesh_render_kernel<double><<<grid, kMThreads, 0, ctx->stream>>>(q, dev_of(s), spp,
-                                                                    (const double*)theta,
-                                                                    (double*)img);
+  const bool five = s->nch == 5;
+  if (dtype == MG_F64 && five)
+    mesh_render_kernel<double, 5><<<grid, kMThreads, 0, ctx->stream>>>(
+        q, dev_of(s), spp, (const double*)theta, (double*)img);
+  else if (dtype == MG_F64)
+    mesh_render_kernel<double, 4><<<grid, kMThreads, 0, ctx->stream>>>(
+        q, dev_of(s), spp, (const double*)theta, (double*)img);
+  else if (dtype == MG_F32 && five)
+    mesh_render_kernel<float, 5><<<grid, kMThreads, 0, ctx->stream>>>(
+        q, dev_of(s), spp, (const float*)theta, (float*)img);
   else if (dtype == MG_F32)
-    mesh_render_kernel<float><<<grid, kMThreads, 0, ctx->stream>>>(q, dev_of(s), spp,
-                                                                   (const float*)theta,
-                                                                   (float*)img);
+    mesh_render_kernel<float, 4><<<grid, kMThreads, 0, ctx->stream>>>(
+        q, dev_of(s), spp, (const float*)theta, (float*)img);
   else
     return fail(MG_EINVAL, "mg_meshscene_render: unknown dtype");
   MG_LAUNCH_CHECK(ctx);
@@ -1368,10 +1509,12 @@ int mg_meshscene_render(mg_ctx* ctx, const mg_mesh_scene* s, int32_t dtype, int3
 int mg_meshscene_sample_pair(mg_ctx* ctx, mg_mesh_scene* s, int32_t dtype, int32_t W,
                              int32_t H, const double* view, const void* target_img,
                              const void* now, const void* prev, uint64_t key, uint32_t iteration,
-                             int32_t row0, int32_t row1, void* accum, void* prop, void* diff,
-                             double* loss_out) {
+                             int32_t row0, int32_t row1, int32_t prop_paths, void* accum,
+                             void* prop, void* diff, double* loss_out) {
   if (!ctx || !s || !target_img || !now || !prev || !accum || !prop || !diff || !loss_out)
     return fail(MG_EINVAL, "mg_meshscene_sample_pair: null argument");
+  if (prop_paths < 2 || prop_paths > kMaxProp)
+    return fail(MG_EINVAL, "mg_meshscene_sample_pair: prop_paths must lie in [2, 8]");
   if (W < 1 || H < 1) return fail(MG_EINVAL, "mg_meshscene_sample_pair: bad sizes");
   if (row0 < 0 || row1 > H || row0 > row1)
     return fail(MG_EINVAL, "mg_meshscene_sample_pair: bad rows");
@@ -1380,10 +1523,11 @@ int mg_meshscene_sample_pair(mg_ctx* ctx, mg_mesh_scene* s, int32_t dtype, int32
   MeshK q = make_k(s, W, H, view, key, iteration);
   q.row0 = row0;
   q.row1 = row1;
-  const long long np = (long long)s->nobj * 4 * s->R * s->R;
+  const long long np = (long long)s->nobj * s->nch * s->R * s->R;
   const int grid = grid_for(ctx, int64_t(W) * (row1 - row0) + 1, kMThreads, 4);
   unsigned long long* acc = (unsigned long long*)accum;
-  if (g_mesh_megakernel) {
+  // the megakernel implements the configs[3] form (4 channels, 2 proportional paths)
+  if (g_mesh_megakernel && s->nch == 4 && prop_paths == 2) {
     MG_CUDA_TRY(cudaMemsetAsync(s->work, 0, sizeof(unsigned int), ctx->stream));
     if (dtype == MG_F64)
       mesh_pair_kernel<double><<<grid, kMThreads, 0, ctx->stream>>>(
@@ -1396,12 +1540,18 @@ int mg_meshscene_sample_pair(mg_ctx* ctx, mg_mesh_scene* s, int32_t dtype, int32
     else
       return fail(MG_EINVAL, "mg_meshscene_sample_pair: unknown dtype");
     MG_LAUNCH_CHECK(ctx);
+  } else if (dtype == MG_F64 && s->nch == 5) {
+    st = wavefront_pair<double, 5>(ctx, s, q, prop_paths, (const double*)target_img,
+                                   (const double*)now, (const double*)prev, acc, np, loss_out);
   } else if (dtype == MG_F64) {
-    st = wavefront_pair<double>(ctx, s, q, (const double*)target_img, (const double*)now,
-                                (const double*)prev, acc, np, loss_out);
+    st = wavefront_pair<double, 4>(ctx, s, q, prop_paths, (const double*)target_img,
+                                   (const double*)now, (const double*)prev, acc, np, loss_out);
+  } else if (dtype == MG_F32 && s->nch == 5) {
+    st = wavefront_pair<float, 5>(ctx, s, q, prop_paths, (const float*)target_img,
+                                  (const float*)now, (const float*)prev, acc, np, loss_out);
   } else if (dtype == MG_F32) {
-    st = wavefront_pair<float>(ctx, s, q, (const float*)target_img, (const float*)now,
-                               (const float*)prev, acc, np, loss_out);
+    st = wavefront_pair<float, 4>(ctx, s, q, prop_paths, (const float*)target_img,
+                                  (const float*)now, (const float*)prev, acc, np, loss_out);
   } else {
     return fail(MG_EINVAL, "mg_meshscene_sample_pair: unknown dtype");
   }

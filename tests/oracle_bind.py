@@ -299,6 +299,46 @@ class Oracle:
           _ptr(diff), C.byref(loss))
         return prop, diff, loss.value
 
+    def meshx_render(self, W, H, rec, obj, nch, R, view, theta, spp, key):
+        f = self.lib.mgo_meshx_render
+        f.argtypes = [C.c_int, C.c_int, C.c_int, C.c_void_p, C.c_void_p, C.c_int, C.c_int,
+                      C.c_void_p, C.c_void_p, C.c_int, C.c_uint64, C.c_void_p]
+        img = np.empty(3 * W * H)
+        rec = _f64(rec)
+        obj = np.ascontiguousarray(obj, dtype=np.int32)
+        f(W, H, rec.shape[0], _ptr(rec), obj.ctypes.data_as(C.c_void_p), nch, R, _ptr(_f64(view)),
+          _ptr(_f64(theta)), spp, key, _ptr(img))
+        return img
+
+    def meshx_sample_pair(self, W, H, rec, obj, nobj, nch, R, view, target_img, now, prev, key,
+                          it, nprop, rows=None):
+        f = self.lib.mgo_meshx_sample_pair
+        f.argtypes = [C.c_int, C.c_int, C.c_int, C.c_void_p, C.c_void_p, C.c_int, C.c_int,
+                      C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_uint64,
+                      C.c_uint32, C.c_int, C.c_int, C.c_int, C.c_void_p, C.c_void_p, _dp]
+        r0, r1 = rows if rows is not None else (0, H)
+        n = nobj * nch * R * R
+        prop, diff, loss = np.empty(n), np.empty(n), C.c_double()
+        rec = _f64(rec)
+        obj = np.ascontiguousarray(obj, dtype=np.int32)
+        f(W, H, rec.shape[0], _ptr(rec), obj.ctypes.data_as(C.c_void_p), nobj, nch, R,
+          _ptr(_f64(view)), _ptr(_f64(target_img)), _ptr(_f64(now)), _ptr(_f64(prev)), key, it,
+          r0, r1, nprop, _ptr(prop), _ptr(diff), C.byref(loss))
+        return prop, diff, loss.value
+
+    def meshx_path_radiance(self, W, H, rec, obj, nch, R, view, theta, px, py, key, it, path):
+        f = self.lib.mgo_meshx_path_radiance
+        f.argtypes = [C.c_int, C.c_int, C.c_int, C.c_void_p, C.c_void_p, C.c_int, C.c_int,
+                      C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.c_uint64, C.c_uint32,
+                      C.c_uint32, C.c_void_p]
+        f.restype = C.c_int
+        L = np.empty(3)
+        rec = _f64(rec)
+        obj = np.ascontiguousarray(obj, dtype=np.int32)
+        nv = f(W, H, rec.shape[0], _ptr(rec), obj.ctypes.data_as(C.c_void_p), nch, R,
+               _ptr(_f64(view)), _ptr(_f64(theta)), px, py, key, it, path, _ptr(L))
+        return L, nv
+
     def mesh_path_radiance(self, W, H, rec, obj, R, view, theta, px, py, key, it, path):
         f = self.lib.mgo_mesh_path_radiance
         f.argtypes = [C.c_int, C.c_int, C.c_int, C.c_void_p, C.c_void_p, C.c_int, C.c_void_p,

@@ -103,7 +103,7 @@ def test_sample_pair_bit_exact_vs_oracle(api, oracle, maxv, kernel_mode):
     tn, tp = torch.tensor(now, device="cuda"), torch.tensor(prev, device="cuda")
     check(load().mg_meshscene_sample_pair(sc.ctx.h, sc.h, 1, W, H,
                                           sc.view.ctypes.data_as(C.c_void_p), _p(tgt), _p(tn),
-                                          _p(tp), 1234, 7, 0, H, _p(prob_accum), _p(prop),
+                                          _p(tp), 1234, 7, 0, H, 2, _p(prob_accum), _p(prop),
                                           _p(diff), _p(loss)))
     wp, wd, wl = oracle.mesh_sample_pair(W, H, rec, obj, nobj, R, view, target, now, prev, 1234, 7)
     assert np.array_equal(prop.cpu().numpy(), wp)
@@ -156,3 +156,57 @@ def test_texture_optimisation_fits_the_image(api):
         losses.append(run.loss_estimate())
     first, last = float(np.mean(losses[:3])), float(np.mean(losses[-40:]))
     assert last < 0.2 * first, (first, last)
+
+
+# ------------------------------------------------------ configs[4] form
+@pytest.mark.parametrize("nprop,maxv", [(4, 5), (3, 8), (2, 3)])
+def test_metalness_sample_pair_bit_exact_vs_oracle(api, oracle, nprop, maxv):
+    """5 texture channels (base rgb, roughness, metalness; full principled
+    BSDF derivatives) and n proportional paths: render and gradient sample
+    pair bit-identical to mgo_meshx_* in fp64."""
+    import ctypes as C
+    from paper_2309_15676_b200._lib import check, load
+    from paper_2309_15676_b200.api import _p
+    R, nch = 4, 5
+    rec, obj, nobj = api.mesh_scene_geometry((6, 8), (8, 10))
+    view = api.mesh_scene_view(max_vertices=maxv)
+    sc = api.MeshScene(rec, obj, nobj, R, view, channels=nch)
+    n = nobj * nch * R * R
+    assert sc.params() == n
+    rs = np.random.RandomState(nprop + maxv)
+    now = rs.uniform(0.1, 0.9, n)
+    prev = np.clip(now + rs.uniform(-0.02, 0.02, n), 0, 1)
+    W, H = 9, 7
+    img = sc.render(torch.tensor(now, device="cuda"), W, H, 2, 5).cpu().numpy()
+    assert np.array_equal(img, oracle.meshx_render(W, H, rec, obj, nch, R, view, now, 2, 5))
+    target = rs.uniform(0.0, 0.6, 3 * W * H)
+    acc = torch.zeros(2 * n, dtype=torch.int64, device="cuda")
+    prop = torch.empty(n, dtype=torch.float64, device="cuda")
+    diff = torch.empty_like(prop)
+    loss = torch.zeros(1, dtype=torch.float64, device="cuda")
+    tgt = torch.tensor(target, device="cuda")
+    tn, tp = torch.tensor(now, device="cuda"), torch.tensor(prev, device="cuda")
+    check(load().mg_meshscene_sample_pair(sc.ctx.h, sc.h, 1, W, H,
+                                          sc.view.ctypes.data_as(C.c_void_p), _p(tgt), _p(tn),
+                                          _p(tp), 77, 4, 0, H, nprop, _p(acc), _p(prop), _p(diff),
+                                          _p(loss)))
+    wp, wd, wl = oracle.meshx_sample_pair(W, H, rec, obj, nobj, nch, R, view, target, now, prev,
+                                          77, 4, nprop)
+    assert np.array_equal(prop.cpu().numpy(), wp)
+    assert np.array_equal(diff.cpu().numpy(), wd)
+    assert abs(float(loss[0]) - wl) <= 1e-12 * max(1.0, abs(wl))
+    # metalness gradients present
+    assert np.count_nonzero(wp.reshape(nobj, nch, R * R)[:, 4]) > 0
+
+
+def test_large_scene_builds_and_steps(api):
+    """configs[4] geometry (16 objects, ~502k triangles) at a reduced image
+    and texture size: BVH build, sample pair + fused update run."""
+    prob = api.MeshLargeProblem(96, 96, 32, target_spp=2)
+    info = prob.scene.info()
+    assert info["triangles"] > 500_000 and info["params"] == 16 * 5 * 32 * 32
+    run = api.MeshTextureRun(prob, "meta", lr=0.005)
+    for _ in range(3):
+        pair = run.step()
+    assert torch.isfinite(pair.prop).all() and torch.isfinite(run.params).all()
+    assert int(torch.count_nonzero(pair.prop)) > 1000
