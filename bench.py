@@ -476,6 +476,25 @@ def extras(args, ctx):
                                    "rays_per_s": nr / (a.elapsed_time(b) / 1e3)}
     del mprob, mrun, rays, org, tgt, dirs
     torch.cuda.empty_cache()
+    # F1 slice 4, BASELINE configs[4]: 1024^2, 16 objects / ~502k triangles,
+    # 16 x 5 x 1024^2 = 83.9M texture parameters (base rgb, roughness,
+    # metalness), depth 8, 1 FD + 4 proportional spp
+    lprob = api.MeshLargeProblem(target_spp=2, ctx=ctx)
+    lrun = api.MeshTextureRun(lprob, optimizer="meta", lr=0.005)
+    for _ in range(2):
+        lrun.step()
+    torch.cuda.synchronize()
+    a.record(ctx.stream)
+    for _ in range(3):
+        lrun.step()
+    b.record(ctx.stream)
+    torch.cuda.synchronize()
+    ms = a.elapsed_time(b) / 3
+    out["mesh_large_1024px_f32"] = {"ms_per_iteration": ms, "iterations_per_s": 1e3 / ms,
+                                    "paths_per_s": lprob.draws_per_sample() / (ms / 1e3),
+                                    "texture_params": lprob.dim(), **lprob.scene.info()}
+    del lprob, lrun
+    torch.cuda.empty_cache()
     # mini-render stand-in for configs[0] (P=4096, spp=2, 200 iterations)
     cfg = api.ExperimentConfig(problem="mini-render", pixel_count=4096, spp=2, iterations=200,
                                seed=0, problem_seed=1, lr=0.01, replicates=148)
