@@ -210,3 +210,34 @@ def test_large_scene_builds_and_steps(api):
         pair = run.step()
     assert torch.isfinite(pair.prop).all() and torch.isfinite(run.params).all()
     assert int(torch.count_nonzero(pair.prop)) > 1000
+
+
+@pytest.mark.parametrize("channels,nprop", [(4, 2), (5, 4)])
+def test_mesh_fd_sample_is_unbiased(api, channels, nprop):
+    """E[diff] = E[prop(theta_t)] - E[prop(theta_{t-1})] (the finite
+    difference estimates the change of the gradient), on random projections
+    of the texture gradient; z-test over independent Philox keys.  The FD
+    sample is also far less noisy than the difference of two proportional
+    samples (common random numbers)."""
+    W = H = 16
+    R, K = 4, 600
+    rec, obj, nobj = api.mesh_scene_geometry((6, 8), (8, 10))
+    prob = api.MeshTextureProblem(W, H, R, max_vertices=4, target_spp=8, dtype=torch.float64,
+                                  channels=channels, prop_paths=nprop, geometry=(rec, obj, nobj),
+                                  view=api.mesh_scene_view(max_vertices=4))
+    n = prob.dim()
+    rs = np.random.RandomState(3)
+    a = torch.tensor(rs.uniform(0.3, 0.7, n), device="cuda")
+    b = (a - torch.tensor(rs.uniform(-0.05, 0.05, n), device="cuda")).clamp(0, 1)
+    U = torch.tensor(rs.standard_normal((n, 6)), device="cuda")
+    d, pa, pb = [], [], []
+    for it in range(K):
+        d.append(prob.sample_pair(a, b, it, key=5).diff @ U)
+        pa.append(prob.sample_pair(a, a, it, key=6).prop @ U)
+        pb.append(prob.sample_pair(b, b, it, key=7).prop @ U)
+    d, pa, pb = (torch.stack(x).cpu().numpy() for x in (d, pa, pb))
+    vd = d.var(axis=0) / K
+    vp = pa.var(axis=0) / K + pb.var(axis=0) / K
+    z = np.abs(d.mean(0) - (pa.mean(0) - pb.mean(0))) / np.sqrt(vd + vp)
+    assert z.max() < 4.0, z
+    assert np.all(vd < 0.5 * vp)
