@@ -284,9 +284,9 @@ __device__ __forceinline__ bool tri_hit_rec(const double* __restrict__ rec, cons
 // (stk: reserved for a shared-memory stack; the local-memory stack measured
 // faster — the shared one cut occupancy.)
 template <bool ANY>
-__device__ __noinline__ int trace(const MeshDev& m, const float4* sn, int* stk, const double o[3],
-                                  const double d[3], double tmax, double& t_out, double& u_out,
-                                  double& v_out) {
+__device__ __forceinline__ int trace_impl(const MeshDev& m, const float4* sn, const double o[3],
+                                          const double d[3], double tmax, double& t_out,
+                                          double& u_out, double& v_out) {
   float of[3], inv[3];
 #pragma unroll
   for (int k = 0; k < 3; ++k) {
@@ -347,6 +347,16 @@ __device__ __noinline__ int trace(const MeshDev& m, const float4* sn, int* stk, 
   u_out = bu;
   v_out = bv;
   return bslot;
+}
+
+// out-of-line copy for the megakernel (one body shared by all its call
+// sites keeps its instruction footprint small); the wavefront kernels
+// inline trace_impl at their single call site.
+template <bool ANY>
+__device__ __noinline__ int trace(const MeshDev& m, const float4* sn, int* stk, const double o[3],
+                                  const double d[3], double tmax, double& t_out, double& u_out,
+                                  double& v_out) {
+  return trace_impl<ANY>(m, sn, o, d, tmax, t_out, u_out, v_out);
 }
 
 __device__ __forceinline__ void prng(uint64_t key, uint32_t pix, uint32_t it, uint32_t path,
@@ -903,7 +913,7 @@ __global__ void __launch_bounds__(kMThreads) wf_gen_kernel(MeshK q, WF<T> w) {
 }
 
 template <class T>
-__global__ void __launch_bounds__(kMThreads) wf_isect_kernel(MeshDev m, WF<T> w, int v) {
+__global__ void __launch_bounds__(kMThreads, 8) wf_isect_kernel(MeshDev m, WF<T> w, int v) {
   MESH_SMEM;
   const int n = int(w.cnt[v]);
   const int* qin = (v & 1) ? w.q1 : w.q0;
@@ -911,7 +921,7 @@ __global__ void __launch_bounds__(kMThreads) wf_isect_kernel(MeshDev m, WF<T> w,
     const int p = qin[i];
     const double o[3] = {w.ox[p], w.oy[p], w.oz[p]}, d[3] = {w.dx[p], w.dy[p], w.dz[p]};
     double t = INFINITY, bu = 0.0, bv = 0.0;
-    const int slot = trace<false>(m, sn, stk, o, d, INFINITY, t, bu, bv);
+    const int slot = trace_impl<false>(m, sn, o, d, INFINITY, t, bu, bv);
     w.hslot[p] = slot;
     w.ht[p] = t;
     w.hu[p] = bu;
@@ -1115,7 +1125,7 @@ __global__ void __launch_bounds__(kMThreads)
 }
 
 template <class T, int NCH>
-__global__ void __launch_bounds__(kMThreads) wf_shadow_kernel(MeshDev m, WF<T> w, int v) {
+__global__ void __launch_bounds__(kMThreads, 8) wf_shadow_kernel(MeshDev m, WF<T> w, int v) {
   using F = VF<NCH>;
   MESH_SMEM;
   const int n = int(w.cnt[kMaxV + 1 + v]);
@@ -1123,7 +1133,7 @@ __global__ void __launch_bounds__(kMThreads) wf_shadow_kernel(MeshDev m, WF<T> w
     const int p = w.sq[i];
     const double o[3] = {w.sox[p], w.soy[p], w.soz[p]}, d[3] = {w.sdx[p], w.sdy[p], w.sdz[p]};
     double ts, tu, tv;
-    if (trace<true>(m, sn, stk, o, d, w.stm[p], ts, tu, tv) < 0) {
+    if (trace_impl<true>(m, sn, o, d, w.stm[p], ts, tu, tv) < 0) {
 #pragma unroll
       for (int j = 0; j < 6; ++j) w.L[size_t(j) * w.P + p] += w.pendC[size_t(j) * w.P + p];
     } else if (p < w.PS) {  // occluded: no NEE data at this vertex
