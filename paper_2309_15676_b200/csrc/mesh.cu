@@ -951,6 +951,33 @@ __global__ void __launch_bounds__(kMThreads)
       const int k = p / w.npix, pix = w.pix0 + (p - k * w.npix);
       const int slot = w.hslot[p];
       const bool store = p < w.PS;
+      // parameter sets evaluated: path 0 (A) and the FD path at theta_t and
+      // theta_{t-1}; the other proportional paths at theta_t only
+      const int ns = (k == 0 || k == w.nprop) ? 2 : 1;
+      // every stored field of vertex v is written exactly once below
+      auto zero_nee = [&](int s) {
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+          vf(w, v, F::A + s * 3 + c, p) = T(0);
+          vf(w, v, F::C + s * 3 + c, p) = T(0);
+        }
+        if constexpr (NCH == 5) {
+#pragma unroll
+          for (int j = 0; j < 9; ++j) vf(w, v, VF<5>::dfn + s * 9 + j, p) = T(0);
+        } else {
+          vf(w, v, VF<4>::dSn + s, p) = T(0);
+        }
+      };
+      auto zero_bounce = [&](int s) {
+#pragma unroll
+        for (int c = 0; c < 3; ++c) vf(w, v, F::invfb + s * 3 + c, p) = T(0);
+        if constexpr (NCH == 5) {
+#pragma unroll
+          for (int j = 0; j < 9; ++j) vf(w, v, VF<5>::dfb + s * 9 + j, p) = T(0);
+        } else {
+          vf(w, v, VF<4>::dSb + s, p) = T(0);
+        }
+      };
       T beta[2][3];
 #pragma unroll
       for (int s = 0; s < 2; ++s)
@@ -961,6 +988,7 @@ __global__ void __launch_bounds__(kMThreads)
         for (int s = 0; s < 2; ++s)
 #pragma unroll
           for (int c = 0; c < 3; ++c) {
+            if (s >= ns) break;
             const T e = beta[s][c] * T(V[21 + c]);
             w.E[size_t(s * 3 + c) * w.P + p] = e;
             w.L[size_t(s * 3 + c) * w.P + p] += e;
@@ -983,10 +1011,8 @@ __global__ void __launch_bounds__(kMThreads)
         ty = ty < 0 ? 0 : (ty > q.R - 1 ? q.R - 1 : ty);
         const int pbase = __ldg(&m.obj[slot]) * NCH * R2 + ty * q.R + tx;
         w.nv[p] = v + 1;
-        if (store) {
-          w.vbase[size_t(v) * w.PS + p] = pbase;
-          for (int f = 0; f < F::n; ++f) vf(w, v, f, p) = T(0);
-        }
+        if (store) w.vbase[size_t(v) * w.PS + p] = pbase;
+        bool nee_done = false, bounce_done = false;
         T base[2][3], rough[2], metal[2];
 #pragma unroll
         for (int s = 0; s < 2; ++s) {
@@ -1013,8 +1039,10 @@ __global__ void __launch_bounds__(kMThreads)
           want_shadow = true;
           const double gl = ((cx * cl) / d2) * la;
           const T wT[3] = {T(wl3[0]), T(wl3[1]), T(wl3[2])};
+          nee_done = true;
 #pragma unroll
           for (int s = 0; s < 2; ++s) {
+            if (s >= ns) break;
             T f[3];
             if constexpr (NCH == 5) {
               T df[3][3];
@@ -1083,8 +1111,10 @@ __global__ void __launch_bounds__(kMThreads)
                                   (dx * Tb[1] + dy * Bb[1]) + dz * nn[1],
                                   (dx * Tb[2] + dy * Bb[2]) + dz * nn[2]};
             const T wiT[3] = {T(wi[0]), T(wi[1]), T(wi[2])};
+            bounce_done = true;
 #pragma unroll
             for (int s = 0; s < 2; ++s) {
+              if (s >= ns) break;
               T f[3];
               if constexpr (NCH == 5) {
                 T df[3][3];
@@ -1115,6 +1145,11 @@ __global__ void __launch_bounds__(kMThreads)
             want_bounce = true;
           }
         }
+        if (store)
+          for (int s = 0; s < ns; ++s) {
+            if (!nee_done) zero_nee(s);
+            if (!bounce_done) zero_bounce(s);
+          }
       }
     }
     const int qs = enqueue(want_shadow, &w.cnt[kMaxV + 1 + v]);
@@ -1134,8 +1169,9 @@ __global__ void __launch_bounds__(kMThreads, 8) wf_shadow_kernel(MeshDev m, WF<T
     const double o[3] = {w.sox[p], w.soy[p], w.soz[p]}, d[3] = {w.sdx[p], w.sdy[p], w.sdz[p]};
     double ts, tu, tv;
     if (trace_impl<true>(m, sn, o, d, w.stm[p], ts, tu, tv) < 0) {
-#pragma unroll
-      for (int j = 0; j < 6; ++j) w.L[size_t(j) * w.P + p] += w.pendC[size_t(j) * w.P + p];
+      const int k = p / w.npix;
+      const int nj = (k == 0 || k == w.nprop) ? 6 : 3;
+      for (int j = 0; j < nj; ++j) w.L[size_t(j) * w.P + p] += w.pendC[size_t(j) * w.P + p];
     } else if (p < w.PS) {  // occluded: no NEE data at this vertex
 #pragma unroll
       for (int j = 0; j < 6; ++j) {
