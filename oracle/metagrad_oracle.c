@@ -4,6 +4,12 @@
  * CUDA path (see metagrad_oracle.h).  Pinned against tests/golden/, which
  * oracle/gen_golden.py generates from the unmodified reference (oracle/_ref).
  *
+ * The F1 path-tracing sections (mgo_quad_*, mgo_helix_*, mgo_mesh*_*) have
+ * NO reference counterpart (the reference has no renderer):
+ * parity unpinned against the reference; they restate this repo's own
+ * specification and are checked by finite differences,
+ * unbiasedness tests and brute-force intersection instead.
+ *
  * Build: make -C oracle  (gcc -O2 -ffp-contract=off; no -march: the
  * reference's Release build performs no FMA contraction).
  */
