@@ -162,7 +162,8 @@ class SharedParamStepP2P:
     exercised on >1 GPU yet."""
 
     def __init__(self, n: int, dtype=None, group=None, lr=0.01, beta_f=0.9, beta_delta=0.5,
-                 eps_step=1e-8, eps_alpha=1e-30, clip=True, project_lo=None, init=0.0):
+                 eps_step=1e-8, eps_alpha=1e-30, clip=True, project_lo=None, init=0.0,
+                 project_hi=None):
         import ctypes as C
 
         import torch
@@ -204,6 +205,7 @@ class SharedParamStepP2P:
                                              C.byref(_abi.fresh_scalars())))
         self.meta = _abi.MetaParams(lr, eps_step, eps_alpha, int(clip))
         self.beta_f, self.beta_delta, self.project_lo = beta_f, beta_delta, project_lo
+        self.project_hi = project_hi
         self.t, self.bp = 0, 1.0
 
     def __call__(self, target_shard=None):
@@ -214,8 +216,10 @@ class SharedParamStepP2P:
         self.bp *= self.beta_f
         a = _abi.MetaUpdateArgs(meta=self.meta, prop_coef=(1.0 - self.beta_f) / (1.0 - self.bp),
                                 beta_delta=self.beta_delta, first_step=int(self.t == 1),
-                                project=int(self.project_lo is not None),
-                                proj_lo=self.project_lo or 0.0)
+                                project=(2 if self.project_hi is not None
+                                         else int(self.project_lo is not None)),
+                                proj_lo=self.project_lo or 0.0,
+                                proj_hi=self.project_hi or 0.0)
         arr = lambda ptrs: (C.c_void_p * self.world)(*ptrs)  # noqa: E731
         self.h_prop.barrier()                      # every rank's partials are written
         self._check(self._L.mg_shared_meta_update(
