@@ -44,6 +44,9 @@ namespace mg {
 // mg_set_option("mesh_megakernel", 1): one-thread-per-pixel megakernel
 // instead of the default wavefront stages (A/B comparison; identical results)
 bool g_mesh_megakernel = false;
+// mg_set_option("bvh_leaf_size", k): maximum triangles per BVH leaf (1..7),
+// applied to scenes created afterwards
+int g_bvh_leaf = 2;
 namespace {
 
 constexpr int kMThreads = 128;
@@ -102,7 +105,7 @@ struct Builder {
       nodes[size_t(id)] = nd;
       return id;
     };
-    if (n <= 4) return make_leaf();
+    if (n <= g_bvh_leaf) return make_leaf();
     if (depth >= kStackDepth - 2) {  // deeper than the traversal stack allows
       too_deep = true;
       return make_leaf();

@@ -28,6 +28,7 @@ namespace mg {
 bool g_disable_tma = false;
 extern bool g_render_vec;
 extern bool g_mesh_megakernel;
+extern int g_bvh_leaf;
 // -1: per-dtype default measured on B200 (tools/sweep_update_variants.py,
 // profiles/r01_sweep_update_variants_*): fp32 -> variant 6 (2 CTAs/SM x 192
 // threads, 4 stages of 3 KB tiles: the fp32 body is issue-heavy, so it wants
@@ -717,6 +718,11 @@ int mg_set_option(const char* name, int64_t value) {
   if (!name) return fail(MG_EINVAL, "mg_set_option: null name");
   if (std::string(name) == "disable_tma") {
     g_disable_tma = value != 0;
+    return MG_OK;
+  }
+  if (std::string(name) == "bvh_leaf_size") {
+    if (value < 1 || value > 7) return fail(MG_EINVAL, "bvh_leaf_size must lie in [1, 7]");
+    g_bvh_leaf = int(value);
     return MG_OK;
   }
   if (std::string(name) == "mesh_megakernel") {
