@@ -102,10 +102,11 @@ __device__ int intersect(const T* __restrict__ sph, int nsph, const V3<T>& o, co
   return kind;
 }
 
-// principled BSDF f[c] and df[c][k] (k: base r, g, b, metal, rough)
+// principled BSDF f[c] and its non-zero derivatives df[c][k], k = 0: d/d base_c
+// (base_c' != c does not enter f_c), 1: d/d metal, 2: d/d rough
 template <class T>
 __device__ __forceinline__ void bsdf(const T* th, const V3<T>& n, const V3<T>& wi,
-                                     const V3<T>& wo, T f[3], T df[3][kNP]) {
+                                     const V3<T>& wo, T f[3], T df[3][3]) {
   const T metal = th[3], rough = th[4];
   const T alpha = T(0.05) + T(0.95) * (rough * rough);
   const T a2 = alpha * alpha;
@@ -136,19 +137,20 @@ __device__ __forceinline__ void bsdf(const T* th, const V3<T>& n, const V3<T>& w
     const T F0 = T(0.04) * (T(1) - metal) + base * metal;
     const T F = F0 + (T(1) - F0) * q5;
     f[c] = ((T(1) - metal) * base) / T(kPiH) + DG * F;
-#pragma unroll
-    for (int k = 0; k < kNP; ++k) df[c][k] = T(0);
-    df[c][c] = (T(1) - metal) / T(kPiH) + DG * (metal * (T(1) - q5));
-    df[c][3] = (-base) / T(kPiH) + DG * ((base - T(0.04)) * (T(1) - q5));
-    df[c][4] = dDG_drough * F;
+    df[c][0] = (T(1) - metal) / T(kPiH) + DG * (metal * (T(1) - q5));
+    df[c][1] = (-base) / T(kPiH) + DG * ((base - T(0.04)) * (T(1) - q5));
+    df[c][2] = dDG_drough * F;
   }
 }
 
 // One path evaluated for NSETS parameter sets: radiance L[s][c] and its
-// derivative dL[s][c][k].
+// non-zero derivatives dL[s][c][k] (k: base_c, metal, rough — radiance of
+// channel c depends on no other channel's base colour, so the other
+// entries of d L_c / d theta are exactly zero and are not carried).
+constexpr int kND = 3;
 template <class T, int NSETS>
 __device__ void trace(const HelixK& q, const T* __restrict__ sph, const T (&th)[2][kNP], int px,
-                      int py, uint32_t path, T L[NSETS][3], T dL[NSETS][3][kNP]) {
+                      int py, uint32_t path, T L[NSETS][3], T dL[NSETS][3][kND]) {
   const uint32_t pix = uint32_t(py * q.W + px);
   double u[4];
   hrng(q.key, pix, q.iteration, path, 0u, u);
@@ -160,7 +162,7 @@ __device__ void trace(const HelixK& q, const T* __restrict__ sph, const T (&th)[
   d.x /= dl;
   d.y /= dl;
   d.z /= dl;
-  T beta[NSETS][3], dbeta[NSETS][3][kNP];
+  T beta[NSETS][3], dbeta[NSETS][3][kND];
 #pragma unroll
   for (int s = 0; s < NSETS; ++s)
 #pragma unroll
@@ -168,7 +170,7 @@ __device__ void trace(const HelixK& q, const T* __restrict__ sph, const T (&th)[
       beta[s][c] = T(1);
       L[s][c] = T(0);
 #pragma unroll
-      for (int k = 0; k < kNP; ++k) {
+      for (int k = 0; k < kND; ++k) {
         dbeta[s][c][k] = T(0);
         dL[s][c][k] = T(0);
       }
@@ -184,7 +186,7 @@ __device__ void trace(const HelixK& q, const T* __restrict__ sph, const T (&th)[
         for (int c = 0; c < 3; ++c) {
           L[s][c] += beta[s][c] * T(q.env[c]);
 #pragma unroll
-          for (int j = 0; j < kNP; ++j) dL[s][c][j] += dbeta[s][c][j] * T(q.env[c]);
+          for (int j = 0; j < kND; ++j) dL[s][c][j] += dbeta[s][c][j] * T(q.env[c]);
         }
       return;
     }
@@ -222,7 +224,7 @@ __device__ void trace(const HelixK& q, const T* __restrict__ sph, const T (&th)[
         const T gl = ((cx * cl) / d2) * T(kLA);
 #pragma unroll
         for (int s = 0; s < NSETS; ++s) {
-          T f[3], df[3][kNP];
+          T f[3], df[3][kND];
           if (kind == 1) {
             bsdf<T>(th[s], n, w, wo, f, df);
           } else {
@@ -230,7 +232,7 @@ __device__ void trace(const HelixK& q, const T* __restrict__ sph, const T (&th)[
             for (int c = 0; c < 3; ++c) {
               f[c] = T(q.ground[c]) / T(kPiH);
 #pragma unroll
-              for (int j = 0; j < kNP; ++j) df[c][j] = T(0);
+              for (int j = 0; j < kND; ++j) df[c][j] = T(0);
             }
           }
 #pragma unroll
@@ -238,7 +240,7 @@ __device__ void trace(const HelixK& q, const T* __restrict__ sph, const T (&th)[
             const T g = gl * T(q.Le[c]);
             L[s][c] += beta[s][c] * (f[c] * g);
 #pragma unroll
-            for (int j = 0; j < kNP; ++j)
+            for (int j = 0; j < kND; ++j)
               dL[s][c][j] += dbeta[s][c][j] * (f[c] * g) + beta[s][c] * (df[c][j] * g);
           }
         }
@@ -281,7 +283,7 @@ __device__ void trace(const HelixK& q, const T* __restrict__ sph, const T (&th)[
     if (dz <= T(0)) return;
 #pragma unroll
     for (int s = 0; s < NSETS; ++s) {
-      T f[3], df[3][kNP];
+      T f[3], df[3][kND];
       if (kind == 1) {
         bsdf<T>(th[s], n, wi, wo, f, df);
       } else {
@@ -289,14 +291,14 @@ __device__ void trace(const HelixK& q, const T* __restrict__ sph, const T (&th)[
         for (int c = 0; c < 3; ++c) {
           f[c] = T(q.ground[c]) / T(kPiH);
 #pragma unroll
-          for (int j = 0; j < kNP; ++j) df[c][j] = T(0);
+          for (int j = 0; j < kND; ++j) df[c][j] = T(0);
         }
       }
 #pragma unroll
       for (int c = 0; c < 3; ++c) {
         const T wgt = f[c] * T(kPiH);
 #pragma unroll
-        for (int j = 0; j < kNP; ++j)
+        for (int j = 0; j < kND; ++j)
           dbeta[s][c][j] = dbeta[s][c][j] * wgt + beta[s][c] * (df[c][j] * T(kPiH));
         beta[s][c] = beta[s][c] * wgt;
       }
@@ -334,7 +336,7 @@ __global__ void __launch_bounds__(kHThreads)
     const int px = pix % q.W, py = pix / q.W;
     T acc[3] = {T(0), T(0), T(0)};
     for (int s = 0; s < spp; ++s) {
-      T L[1][3], dL[1][3][kNP];
+      T L[1][3], dL[1][3][kND];
       trace<T, 1>(q, sph, th, px, py, uint32_t(s), L, dL);
 #pragma unroll
       for (int c = 0; c < 3; ++c) acc[c] += L[0][c];
@@ -368,7 +370,7 @@ __global__ void __launch_bounds__(kHThreads)
   for (int pix = q.row0 * q.W + blockIdx.x * kHThreads + threadIdx.x; pix < q.row1 * q.W;
        pix += gridDim.x * kHThreads) {
     const int px = pix % q.W, py = pix / q.W;
-    T LA[2][3], dA[2][3][kNP], LB[1][3], dB[1][3][kNP], LC[2][3], dC[2][3][kNP];
+    T LA[2][3], dA[2][3][kND], LB[1][3], dB[1][3][kND], LC[2][3], dC[2][3][kND];
     trace<T, 2>(q, sph, th, px, py, 0u, LA, dA);
     trace<T, 1>(q, sph, th, px, py, 1u, LB, dB);
     trace<T, 2>(q, sph, th, px, py, 2u, LC, dC);
@@ -380,11 +382,12 @@ __global__ void __launch_bounds__(kHThreads)
       const double rA1 = double(LA[1][c]) - Is, rC1 = double(LC[1][c]) - Is;
       loss += rA * rB;
 #pragma unroll
-      for (int j = 0; j < kNP; ++j) {
-        fp[j] += fixh(rA * double(dB[0][c][j]));
-        fp[j] += fixh(rB * double(dA[0][c][j]));
-        fd[j] += fixh((rC * double(dA[0][c][j]) + rA * double(dC[0][c][j])) -
-                      (rC1 * double(dA[1][c][j]) + rA1 * double(dC[1][c][j])));
+      for (int k = 0; k < kND; ++k) {
+        const int j = k == 0 ? c : k + 2;  // base_c, metal (3), rough (4)
+        fp[j] += fixh(rA * double(dB[0][c][k]));
+        fp[j] += fixh(rB * double(dA[0][c][k]));
+        fd[j] += fixh((rC * double(dA[0][c][k]) + rA * double(dC[0][c][k])) -
+                      (rC1 * double(dA[1][c][k]) + rA1 * double(dC[1][c][k])));
       }
     }
   }
