@@ -1,0 +1,373 @@
+// Shared declarations of the triangle-mesh renderer (F1 slices 3-4,
+// BASELINE.json configs[3] and [4]): the scene object, the
+// kernel parameter blocks and the device building blocks — BVH node layout
+// and traversal, fp64 Moller-Trumbore, Philox addressing, the principled
+// BSDF and its parameter derivatives.  Oracle: oracle/metagrad_oracle.c
+// mgo_mesh*_* (the reference has no renderer).
+//
+//   mesh_bvh.cu        host BVH build, scene create / destroy / info
+//   mesh_megakernel.cu one-thread-per-pixel path (configs[3] form), render,
+//                      ray-query entry point
+//   mesh_wavefront.cu  the default wavefront sample pair (configs[3] and [4])
+#pragma once
+
+#include <math.h>
+#include <stdint.h>
+
+#include <climits>
+
+#include "mg_common.cuh"
+#include "philox.cuh"
+
+struct mg_mesh_scene {
+  int T = 0, nobj = 0, R = 0, nnodes = 0, depth = 0, nch = 4;
+  double* tri = nullptr;   // [T][18] in BVH order
+  int* orig = nullptr;     // [T] original triangle index
+  int* obj = nullptr;      // [T] object id (BVH order)
+  float4* nodes = nullptr; // [2 * nnodes]: (lo.xyz, a) (hi.xyz, b)
+  unsigned int* work = nullptr;  // pixel work counter of the pair kernel
+  void* wf = nullptr;            // wavefront path state (grow-only)
+  size_t wf_cap = 0;
+};
+
+namespace mg {
+// mg_set_option("mesh_megakernel", 1): one-thread-per-pixel megakernel
+// instead of the default wavefront stages (A/B comparison; identical results)
+extern bool g_mesh_megakernel;
+// mg_set_option("bvh_leaf_size", k): maximum triangles per BVH leaf (1..7),
+// applied to scenes created afterwards
+extern int g_bvh_leaf;
+
+namespace mesh {
+
+constexpr int kMThreads = 128;
+constexpr int kMaxV = 8;
+constexpr int kRec = 18;
+constexpr int kSmemNodes = 256;  // top BVH levels staged in shared memory (16 KB)
+constexpr int kStackDepth = 48;  // traversal stack per thread, in shared memory
+constexpr double kTMin = 1e-9, kOff = 1e-6;
+constexpr double kPiM = 3.14159265358979323846;
+constexpr double kFixM = 1099511627776.0;  // 2^40
+
+// ------------------------------------------------------------ device
+struct MeshDev {
+  const double* __restrict__ tri;
+  const int* __restrict__ orig;
+  const int* __restrict__ obj;
+  const float4* __restrict__ nodes;
+  int nnodes;
+};
+
+struct MeshK {
+  int W, H, R, nobj, nch;
+  int row0, row1;
+  double view[25];
+  uint64_t key;
+  uint32_t iteration;
+};
+
+__device__ __forceinline__ double dot3d(const double a[3], const double b[3]) {
+  return (a[0] * b[0] + a[1] * b[1]) + a[2] * b[2];
+}
+
+__device__ __forceinline__ void cross3d(const double a[3], const double b[3], double r[3]) {
+  r[0] = a[1] * b[2] - a[2] * b[1];
+  r[1] = a[2] * b[0] - a[0] * b[2];
+  r[2] = a[0] * b[1] - a[1] * b[0];
+}
+
+// Moller-Trumbore in fp64, same operation order as the oracle (ms_tri_hit)
+__device__ __forceinline__ bool tri_hit(const double* __restrict__ r, const double o[3],
+                                        const double d[3], double& t, double& u, double& v) {
+  const double v0[3] = {r[0], r[1], r[2]}, e1[3] = {r[3], r[4], r[5]}, e2[3] = {r[6], r[7], r[8]};
+  double p[3], q[3], s[3];
+  cross3d(d, e2, p);
+  const double det = dot3d(e1, p);
+  if (det == 0.0) return false;
+  const double inv = 1.0 / det;
+  s[0] = o[0] - v0[0];
+  s[1] = o[1] - v0[1];
+  s[2] = o[2] - v0[2];
+  const double uu = dot3d(s, p) * inv;
+  if (uu < 0.0 || uu > 1.0) return false;
+  cross3d(s, e1, q);
+  const double vv = dot3d(d, q) * inv;
+  if (vv < 0.0 || uu + vv > 1.0) return false;
+  const double tt = dot3d(e2, q) * inv;
+  if (!(tt > kTMin)) return false;
+  t = tt;
+  u = uu;
+  v = vv;
+  return true;
+}
+
+// BVH2 node = the boxes of its two children (64 B, four float4):
+//   n0 = c0.lo.xyz c0.hi.x   n1 = c0.hi.yz c1.lo.xy   n2 = c1.lo.z c1.hi.xyz
+//   n3 = (ref0, ref1) as int bits; ref >= 0: internal node, ref < 0: leaf
+//   with triangles [first, first + count), ~ref = first * 8 + count.
+// One 64-byte fetch per traversal step tests both children.
+struct Node4 {
+  float4 a, b, c, d;
+};
+
+__device__ __forceinline__ Node4 load_node(const MeshDev& m, const float4* sn, int i) {
+  Node4 n;
+  if (i < kSmemNodes) {
+    n.a = sn[4 * i];
+    n.b = sn[4 * i + 1];
+    n.c = sn[4 * i + 2];
+    n.d = sn[4 * i + 3];
+  } else {
+    n.a = __ldg(&m.nodes[4 * i]);
+    n.b = __ldg(&m.nodes[4 * i + 1]);
+    n.c = __ldg(&m.nodes[4 * i + 2]);
+    n.d = __ldg(&m.nodes[4 * i + 3]);
+  }
+  return n;
+}
+
+__device__ __forceinline__ bool slab6(float lx, float ly, float lz, float hx, float hy, float hz,
+                                      const float o[3], const float inv[3], float tmax,
+                                      float& tnear) {
+  const float tx0 = (lx - o[0]) * inv[0], tx1 = (hx - o[0]) * inv[0];
+  const float ty0 = (ly - o[1]) * inv[1], ty1 = (hy - o[1]) * inv[1];
+  const float tz0 = (lz - o[2]) * inv[2], tz1 = (hz - o[2]) * inv[2];
+  const float tn = fmaxf(fmaxf(fminf(tx0, tx1), fminf(ty0, ty1)), fmaxf(fminf(tz0, tz1), 0.0f));
+  const float tf = fminf(fminf(fmaxf(tx0, tx1), fmaxf(ty0, ty1)), fminf(fmaxf(tz0, tz1), tmax));
+  tnear = tn;
+  return tn <= tf;
+}
+
+// Triangle record fields 0..8 (v0, e1, e2) with 16-byte loads (records are
+// 144 B = 9 x 16 B and the array is 256-byte aligned).
+__device__ __forceinline__ bool tri_hit_rec(const double* __restrict__ rec, const double o[3],
+                                            const double d[3], double& t, double& u, double& v) {
+  const double2* r2 = reinterpret_cast<const double2*>(rec);
+  const double2 x0 = __ldg(r2), x1 = __ldg(r2 + 1), x2 = __ldg(r2 + 2), x3 = __ldg(r2 + 3);
+  const double r[9] = {x0.x, x0.y, x1.x, x1.y, x2.x, x2.y, x3.x, x3.y, __ldg(rec + 8)};
+  return tri_hit(r, o, d, t, u, v);
+}
+
+// ANY: any hit with t < tmax (shadow rays).  Otherwise the closest hit with
+// t < tmax; ties on t resolve to the lower original triangle index, so the
+// answer is the oracle's brute-force scan.  Returns the BVH slot or -1.
+// (stk: reserved for a shared-memory stack; the local-memory stack measured
+// faster — the shared one cut occupancy.)
+template <bool ANY>
+__device__ __forceinline__ int trace_impl(const MeshDev& m, const float4* sn, const double o[3],
+                                          const double d[3], double tmax, double& t_out,
+                                          double& u_out, double& v_out) {
+  float of[3], inv[3];
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    of[k] = float(o[k]);
+    const float dk = float(d[k]);
+    inv[k] = 1.0f / (fabsf(dk) > 1e-20f ? dk : copysignf(1e-20f, dk));
+  }
+  int stack[kStackDepth];
+  int sp = 0, node = 0;
+  double best = tmax, bu = 0.0, bv = 0.0;
+  int bslot = -1, bid = INT_MAX;
+  float bestf = __double2float_ru(best);
+  for (;;) {
+    if (node < 0) {  // leaf: triangles [first, first + count)
+      const int first = (~node) >> 3, count = (~node) & 7;
+      for (int sidx = first; sidx < first + count; ++sidx) {
+        double t, u, v;
+        if (!tri_hit_rec(m.tri + size_t(kRec) * sidx, o, d, t, u, v) || !(t <= best)) continue;
+        if (ANY) {
+          if (t < tmax) return sidx;
+          continue;
+        }
+        const int id = __ldg(&m.orig[sidx]);
+        if (t < best || id < bid) {
+          best = t;
+          bu = u;
+          bv = v;
+          bslot = sidx;
+          bid = id;
+          bestf = __double2float_ru(best);
+        }
+      }
+    } else {
+      const Node4 n = load_node(m, sn, node);
+      float t0, t1;
+      const bool h0 = slab6(n.a.x, n.a.y, n.a.z, n.a.w, n.b.x, n.b.y, of, inv, bestf, t0);
+      const bool h1 = slab6(n.b.z, n.b.w, n.c.x, n.c.y, n.c.z, n.c.w, of, inv, bestf, t1);
+      const int r0 = __float_as_int(n.d.x), r1 = __float_as_int(n.d.y);
+      if (h0 && h1) {
+        const bool first0 = t0 <= t1;
+        stack[sp++] = first0 ? r1 : r0;
+        node = first0 ? r0 : r1;
+        continue;
+      }
+      if (h0) {
+        node = r0;
+        continue;
+      }
+      if (h1) {
+        node = r1;
+        continue;
+      }
+    }
+    if (sp == 0) break;
+    node = stack[--sp];
+  }
+  t_out = best;
+  u_out = bu;
+  v_out = bv;
+  return bslot;
+}
+
+// out-of-line copy for the megakernel (one body shared by all its call
+// sites keeps its instruction footprint small); the wavefront kernels
+// inline trace_impl at their single call site.
+template <bool ANY>
+__device__ __noinline__ int trace(const MeshDev& m, const float4* sn, int* stk, const double o[3],
+                                  const double d[3], double tmax, double& t_out, double& u_out,
+                                  double& v_out) {
+  return trace_impl<ANY>(m, sn, o, d, tmax, t_out, u_out, v_out);
+}
+
+__device__ __forceinline__ void prng(uint64_t key, uint32_t pix, uint32_t it, uint32_t path,
+                                     uint32_t slot, double u[4]) {
+  const Philox4 r =
+      philox4x32_10(Philox4{{pix, it, path, slot}}, uint32_t(key), uint32_t(key >> 32));
+#pragma unroll
+  for (int k = 0; k < 4; ++k) u[k] = double(r.x[k]) * 0x1.0p-32;
+}
+
+// principled BSDF with metalness 0 (the helix slice's expressions with
+// metal = 0): f_c = base_c / pi + DG F, and dS/drough = dDG/drough F
+template <class T>
+__device__ __forceinline__ void bsdf_m0(const T base[3], T rough, const T n[3], const T wi[3],
+                                        const T wo[3], T f[3], T& dS) {
+  const T alpha = T(0.05) + T(0.95) * (rough * rough);
+  const T a2 = alpha * alpha;
+  T h[3] = {wi[0] + wo[0], wi[1] + wo[1], wi[2] + wo[2]};
+  const T hl = sqrt((h[0] * h[0] + h[1] * h[1]) + h[2] * h[2]);
+  h[0] /= hl;
+  h[1] /= hl;
+  h[2] /= hl;
+  auto dt = [](const T* a, const T* b) { return (a[0] * b[0] + a[1] * b[1]) + a[2] * b[2]; };
+  const T nh = dt(n, h), ni = dt(n, wi), no = dt(n, wo), ih = dt(wi, h);
+  const T den = nh * nh * (a2 - T(1)) + T(1);
+  const T D = a2 / (T(kPiM) * (den * den));
+  const T dD_da2 = (den - T(2) * a2 * (nh * nh)) / (T(kPiM) * ((den * den) * den));
+  const T si = sqrt(a2 + (T(1) - a2) * (ni * ni));
+  const T so = sqrt(a2 + (T(1) - a2) * (no * no));
+  const T G1i = (T(2) * ni) / (ni + si), G1o = (T(2) * no) / (no + so);
+  const T dG1i = ((T(-2) * ni) / ((ni + si) * (ni + si))) * ((T(1) - ni * ni) / (T(2) * si));
+  const T dG1o = ((T(-2) * no) / ((no + so) * (no + so))) * ((T(1) - no * no) / (T(2) * so));
+  const T G = G1i * G1o;
+  const T dG_da2 = dG1i * G1o + G1i * dG1o;
+  const T q = T(1) - ih;
+  const T q5 = ((q * q) * (q * q)) * q;
+  const T denom = T(4) * ni * no;
+  const T DG = (D * G) / denom;
+  const T dDG_drough = (((dD_da2 * G + D * dG_da2) / denom) * (T(2) * alpha)) * (T(1.9) * rough);
+  const T F0 = T(0.04);
+  const T F = F0 + (T(1) - F0) * q5;
+#pragma unroll
+  for (int c = 0; c < 3; ++c) f[c] = base[c] / T(kPiM) + DG * F;
+  dS = dDG_drough * F;
+}
+
+// full principled BSDF (configs[4], metalness texture): f[c] and
+// df[c][k] = d f_c / d(base_c, metal, rough) — the oracle's hx_bsdf
+template <class T>
+__device__ __forceinline__ void bsdf_full(const T base[3], T metal, T rough, const T n[3],
+                                          const T wi[3], const T wo[3], T f[3], T df[3][3]) {
+  const T alpha = T(0.05) + T(0.95) * (rough * rough);
+  const T a2 = alpha * alpha;
+  T h[3] = {wi[0] + wo[0], wi[1] + wo[1], wi[2] + wo[2]};
+  const T hl = sqrt((h[0] * h[0] + h[1] * h[1]) + h[2] * h[2]);
+  h[0] /= hl;
+  h[1] /= hl;
+  h[2] /= hl;
+  auto dt = [](const T* a, const T* b) { return (a[0] * b[0] + a[1] * b[1]) + a[2] * b[2]; };
+  const T nh = dt(n, h), ni = dt(n, wi), no = dt(n, wo), ih = dt(wi, h);
+  const T den = nh * nh * (a2 - T(1)) + T(1);
+  const T D = a2 / (T(kPiM) * (den * den));
+  const T dD_da2 = (den - T(2) * a2 * (nh * nh)) / (T(kPiM) * ((den * den) * den));
+  const T si = sqrt(a2 + (T(1) - a2) * (ni * ni));
+  const T so = sqrt(a2 + (T(1) - a2) * (no * no));
+  const T G1i = (T(2) * ni) / (ni + si), G1o = (T(2) * no) / (no + so);
+  const T dG1i = ((T(-2) * ni) / ((ni + si) * (ni + si))) * ((T(1) - ni * ni) / (T(2) * si));
+  const T dG1o = ((T(-2) * no) / ((no + so) * (no + so))) * ((T(1) - no * no) / (T(2) * so));
+  const T G = G1i * G1o;
+  const T dG_da2 = dG1i * G1o + G1i * dG1o;
+  const T q = T(1) - ih;
+  const T q5 = ((q * q) * (q * q)) * q;
+  const T denom = T(4) * ni * no;
+  const T DG = (D * G) / denom;
+  const T dDG_drough = (((dD_da2 * G + D * dG_da2) / denom) * (T(2) * alpha)) * (T(1.9) * rough);
+#pragma unroll
+  for (int c = 0; c < 3; ++c) {
+    const T F0 = T(0.04) * (T(1) - metal) + base[c] * metal;
+    const T F = F0 + (T(1) - F0) * q5;
+    f[c] = ((T(1) - metal) * base[c]) / T(kPiM) + DG * F;
+    df[c][0] = (T(1) - metal) / T(kPiM) + DG * (metal * (T(1) - q5));
+    df[c][1] = (-base[c]) / T(kPiM) + DG * ((base[c] - T(0.04)) * (T(1) - q5));
+    df[c][2] = dDG_drough * F;
+  }
+}
+
+__device__ __forceinline__ unsigned long long fixq(double v) {
+  return (unsigned long long)llrint(v * kFixM);
+}
+
+// adjoint of a stored path, set s, channel weights w (oracle ms_scatter)
+__device__ __forceinline__ void stage_nodes(const MeshDev& m, float4* sn) {
+  const int n = 4 * (m.nnodes < kSmemNodes ? m.nnodes : kSmemNodes);
+  for (int i = threadIdx.x; i < n; i += blockDim.x) sn[i] = m.nodes[i];
+  __syncthreads();
+}
+
+// shared-memory arrays every tracing kernel declares
+#define MESH_SMEM                       \
+  __shared__ float4 sn[4 * kSmemNodes]; \
+  int* stk = nullptr;                   \
+  stage_nodes(m, sn)
+
+
+inline MeshDev dev_of(const mg_mesh_scene* s) {
+  MeshDev m;
+  m.tri = s->tri;
+  m.orig = s->orig;
+  m.obj = s->obj;
+  m.nodes = s->nodes;
+  m.nnodes = s->nnodes;
+  return m;
+}
+
+inline MeshK make_k(const mg_mesh_scene* s, int W, int H, const double* view, uint64_t key,
+                    uint32_t it) {
+  MeshK q;
+  q.W = W;
+  q.H = H;
+  q.R = s->R;
+  q.nobj = s->nobj;
+  q.nch = s->nch;
+  q.row0 = 0;
+  q.row1 = H;
+  for (int i = 0; i < 25; ++i) q.view[i] = view[i];
+  q.key = key;
+  q.iteration = it;
+  return q;
+}
+
+inline int check_view(const double* view) {
+  if (!view) return fail(MG_EINVAL, "mesh scene: null view");
+  const int maxv = int(view[24]);
+  if (maxv < 1 || maxv > kMaxV) return fail(MG_EINVAL, "mesh scene: max_vertices must lie in [1, 8]");
+  return MG_OK;
+}
+
+// megakernel sample pair (configs[3] form), mesh_megakernel.cu
+int megakernel_pair(mg_ctx* ctx, mg_mesh_scene* s, const MeshK& q, int32_t dtype,
+                    const void* target_img, const void* now, const void* prev,
+                    unsigned long long* acc, long long np, double* loss_out);
+
+}  // namespace mesh
+}  // namespace mg

@@ -1,0 +1,304 @@
+// Host side of the mesh renderer: binned-SAH BVH build (16 bins, at most
+// g_bvh_leaf triangles per leaf), breadth-first relabelling of the internal
+// nodes so the top levels form one block every CTA stages in shared memory,
+// 64-byte two-child nodes with fp32 boxes rounded outwards and padded (the
+// fp32 slab test never culls a triangle the fp64 test would hit); scene
+// create / destroy / info.  DESIGN.md §12.
+#include <algorithm>
+#include <vector>
+
+#include "mesh.cuh"
+
+namespace mg {
+bool g_mesh_megakernel = false;
+int g_bvh_leaf = 2;
+namespace mesh {
+namespace {
+
+// ------------------------------------------------------------ host BVH
+struct TmpNode {
+  double lo[3], hi[3];
+  int left = -1, right = -1, first = 0, count = 0;
+};
+
+struct Builder {
+  const double* tri;
+  std::vector<double> blo, bhi, cen;  // [T][3]
+  std::vector<int> idx;
+  std::vector<TmpNode> nodes;
+  int max_depth = 0;
+  bool too_deep = false;
+
+  void bounds(int b, int e, double lo[3], double hi[3], bool centroids) const {
+    for (int k = 0; k < 3; ++k) {
+      lo[k] = INFINITY;
+      hi[k] = -INFINITY;
+    }
+    for (int i = b; i < e; ++i) {
+      const int t = idx[size_t(i)];
+      for (int k = 0; k < 3; ++k) {
+        const double l = centroids ? cen[size_t(3 * t + k)] : blo[size_t(3 * t + k)];
+        const double h = centroids ? cen[size_t(3 * t + k)] : bhi[size_t(3 * t + k)];
+        lo[k] = std::min(lo[k], l);
+        hi[k] = std::max(hi[k], h);
+      }
+    }
+  }
+  static double area(const double lo[3], const double hi[3]) {
+    const double x = hi[0] - lo[0], y = hi[1] - lo[1], z = hi[2] - lo[2];
+    return (x < 0 || y < 0 || z < 0) ? 0.0 : 2.0 * (x * y + y * z + z * x);
+  }
+
+  int build(int b, int e, int depth) {
+    max_depth = std::max(max_depth, depth);
+    const int id = int(nodes.size());
+    nodes.emplace_back();
+    TmpNode nd;
+    bounds(b, e, nd.lo, nd.hi, false);
+    const int n = e - b;
+    auto make_leaf = [&]() {
+      nd.first = b;
+      nd.count = n;
+      nodes[size_t(id)] = nd;
+      return id;
+    };
+    if (n <= g_bvh_leaf) return make_leaf();
+    if (depth >= kStackDepth - 2) {  // deeper than the traversal stack allows
+      too_deep = true;
+      return make_leaf();
+    }
+    double clo[3], chi[3];
+    bounds(b, e, clo, chi, true);
+    int axis = 0;
+    for (int k = 1; k < 3; ++k)
+      if (chi[k] - clo[k] > chi[axis] - clo[axis]) axis = k;
+    const double ext = chi[axis] - clo[axis];
+    int mid = -1;
+    if (ext > 0.0) {
+      constexpr int kBins = 16;
+      int cnt[kBins] = {0};
+      double bl[kBins][3], bh[kBins][3];
+      for (int i = 0; i < kBins; ++i)
+        for (int k = 0; k < 3; ++k) {
+          bl[i][k] = INFINITY;
+          bh[i][k] = -INFINITY;
+        }
+      auto bin_of = [&](int t) {
+        int q = int(((cen[size_t(3 * t + axis)] - clo[axis]) / ext) * kBins);
+        return q < 0 ? 0 : (q >= kBins ? kBins - 1 : q);
+      };
+      for (int i = b; i < e; ++i) {
+        const int t = idx[size_t(i)], q = bin_of(t);
+        cnt[q]++;
+        for (int k = 0; k < 3; ++k) {
+          bl[q][k] = std::min(bl[q][k], blo[size_t(3 * t + k)]);
+          bh[q][k] = std::max(bh[q][k], bhi[size_t(3 * t + k)]);
+        }
+      }
+      double best = INFINITY;
+      int best_split = -1;
+      for (int s = 1; s < kBins; ++s) {
+        double l0[3] = {INFINITY, INFINITY, INFINITY}, h0[3] = {-INFINITY, -INFINITY, -INFINITY};
+        double l1[3] = {INFINITY, INFINITY, INFINITY}, h1[3] = {-INFINITY, -INFINITY, -INFINITY};
+        int n0 = 0, n1 = 0;
+        for (int q = 0; q < kBins; ++q) {
+          double* L = q < s ? l0 : l1;
+          double* H = q < s ? h0 : h1;
+          (q < s ? n0 : n1) += cnt[q];
+          for (int k = 0; k < 3; ++k) {
+            L[k] = std::min(L[k], bl[q][k]);
+            H[k] = std::max(H[k], bh[q][k]);
+          }
+        }
+        if (!n0 || !n1) continue;
+        const double c = area(l0, h0) * n0 + area(l1, h1) * n1;
+        if (c < best) {
+          best = c;
+          best_split = s;
+        }
+      }
+      if (best_split > 0) {
+        auto it = std::partition(idx.begin() + b, idx.begin() + e,
+                                 [&](int t) { return bin_of(t) < best_split; });
+        mid = int(it - idx.begin());
+      }
+    }
+    if (mid <= b || mid >= e) {  // degenerate: median split on the axis
+      mid = (b + e) / 2;
+      std::nth_element(idx.begin() + b, idx.begin() + mid, idx.begin() + e, [&](int x, int y) {
+        const double cx = cen[size_t(3 * x + axis)], cy = cen[size_t(3 * y + axis)];
+        return cx < cy || (cx == cy && x < y);
+      });
+    }
+    const int l = build(b, mid, depth + 1);
+    const int r = build(mid, e, depth + 1);
+    nd.left = l;
+    nd.right = r;
+    nodes[size_t(id)] = nd;
+    return id;
+  }
+};
+
+}  // namespace
+}  // namespace mesh
+}  // namespace mg
+
+using namespace mg;
+using namespace mg::mesh;
+
+extern "C" {
+
+int mg_meshscene_create(mg_ctx* ctx, int32_t tri_count, const double* tri, const int32_t* obj,
+                        int32_t nobj, int32_t tex_res, int32_t channels, mg_mesh_scene** out) {
+  if (!ctx || !tri || !obj || !out) return fail(MG_EINVAL, "mg_meshscene_create: null argument");
+  if (channels != 4 && channels != 5)
+    return fail(MG_EINVAL, "mg_meshscene_create: channels must be 4 (base rgb, roughness) or 5 "
+                           "(+ metalness)");
+  if (tri_count < 1 || nobj < 1 || tex_res < 1)
+    return fail(MG_EINVAL, "mg_meshscene_create: bad sizes");
+  if (tri_count > (1 << 27)) return fail(MG_EINVAL, "mg_meshscene_create: more than 2^27 triangles");
+  if (int64_t(nobj) * channels * tex_res * tex_res > 0x7fffffffLL)
+    return fail(MG_EINVAL, "mg_meshscene_create: parameter count exceeds 2^31");
+  for (int k = 0; k < tri_count; ++k)
+    if (obj[k] < 0 || obj[k] >= nobj) return fail(MG_EINVAL, "mg_meshscene_create: bad object id");
+  Builder B;
+  B.tri = tri;
+  const size_t T = size_t(tri_count);
+  B.blo.resize(3 * T);
+  B.bhi.resize(3 * T);
+  B.cen.resize(3 * T);
+  B.idx.resize(T);
+  double slo[3] = {INFINITY, INFINITY, INFINITY}, shi[3] = {-INFINITY, -INFINITY, -INFINITY};
+  for (size_t k = 0; k < T; ++k) {
+    const double* r = tri + kRec * k;
+    for (int a = 0; a < 3; ++a) {
+      const double p0 = r[a], p1 = r[a] + r[3 + a], p2 = r[a] + r[6 + a];
+      const double lo = std::min(p0, std::min(p1, p2)), hi = std::max(p0, std::max(p1, p2));
+      B.blo[3 * k + a] = lo;
+      B.bhi[3 * k + a] = hi;
+      B.cen[3 * k + a] = 0.5 * (lo + hi);
+      slo[a] = std::min(slo[a], lo);
+      shi[a] = std::max(shi[a], hi);
+    }
+    B.idx[k] = int(k);
+  }
+  B.nodes.reserve(2 * T);
+  B.build(0, tri_count, 0);
+  if (B.too_deep) return fail(MG_EINVAL, "mg_meshscene_create: BVH deeper than the traversal stack");
+  // Internal nodes in breadth-first order (the top levels become nodes
+  // [0, kSmemNodes) for the shared-memory stage); each stores its two
+  // children's boxes.  A single-leaf tree gets a root whose second child is
+  // an empty box.
+  const double diag = sqrt((shi[0] - slo[0]) * (shi[0] - slo[0]) +
+                           (shi[1] - slo[1]) * (shi[1] - slo[1]) +
+                           (shi[2] - slo[2]) * (shi[2] - slo[2]));
+  const float pad = float(1e-5 * diag + 1e-7);
+  std::vector<int> order, label(B.nodes.size(), -1);
+  if (B.nodes[0].left >= 0) {
+    order.push_back(0);
+    label[0] = 0;
+    for (size_t h = 0; h < order.size(); ++h) {
+      const TmpNode& nd = B.nodes[size_t(order[h])];
+      for (int c : {nd.left, nd.right})
+        if (B.nodes[size_t(c)].left >= 0) {
+          label[size_t(c)] = int(order.size());
+          order.push_back(c);
+        }
+    }
+  }
+  auto child_ref = [&](int c) {
+    const TmpNode& nd = B.nodes[size_t(c)];
+    return nd.left >= 0 ? label[size_t(c)] : ~(nd.first * 8 + nd.count);
+  };
+  auto box = [&](int c, float* lo, float* hi) {
+    const TmpNode& nd = B.nodes[size_t(c)];
+    for (int a = 0; a < 3; ++a) {
+      lo[a] = nextafterf(float(nd.lo[a]), -INFINITY) - pad;
+      hi[a] = nextafterf(float(nd.hi[a]), INFINITY) + pad;
+    }
+  };
+  auto ibits = [](int v) {
+    float f;
+    memcpy(&f, &v, 4);
+    return f;
+  };
+  const int nn = order.empty() ? 1 : int(order.size());
+  std::vector<float4> nodes(4 * size_t(nn));
+  for (int i = 0; i < nn; ++i) {
+    float l0[3], h0[3], l1[3] = {1.0f, 1.0f, 1.0f}, h1[3] = {-1.0f, -1.0f, -1.0f};
+    int r0, r1 = ~0;  // empty leaf
+    if (order.empty()) {
+      box(0, l0, h0);
+      r0 = child_ref(0);
+    } else {
+      const TmpNode& nd = B.nodes[size_t(order[size_t(i)])];
+      box(nd.left, l0, h0);
+      box(nd.right, l1, h1);
+      r0 = child_ref(nd.left);
+      r1 = child_ref(nd.right);
+    }
+    nodes[4 * size_t(i)] = make_float4(l0[0], l0[1], l0[2], h0[0]);
+    nodes[4 * size_t(i) + 1] = make_float4(h0[1], h0[2], l1[0], l1[1]);
+    nodes[4 * size_t(i) + 2] = make_float4(l1[2], h1[0], h1[1], h1[2]);
+    nodes[4 * size_t(i) + 3] = make_float4(ibits(r0), ibits(r1), 0.0f, 0.0f);
+  }
+  std::vector<double> stri(kRec * T);
+  std::vector<int> sorig(T), sobj(T);
+  for (size_t s = 0; s < T; ++s) {
+    const int k = B.idx[s];
+    memcpy(&stri[kRec * s], tri + kRec * size_t(k), sizeof(double) * kRec);
+    sorig[s] = k;
+    sobj[s] = obj[k];
+  }
+  mg_mesh_scene* sc = new mg_mesh_scene();
+  sc->T = tri_count;
+  sc->nobj = nobj;
+  sc->nch = channels;
+  sc->R = tex_res;
+  sc->nnodes = nn;
+  sc->depth = B.max_depth;
+  cudaError_t e = cudaMalloc(&sc->tri, sizeof(double) * stri.size());
+  if (e == cudaSuccess) e = cudaMalloc(&sc->orig, sizeof(int) * T);
+  if (e == cudaSuccess) e = cudaMalloc(&sc->obj, sizeof(int) * T);
+  if (e == cudaSuccess) e = cudaMalloc(&sc->nodes, sizeof(float4) * nodes.size());
+  if (e == cudaSuccess) e = cudaMalloc(&sc->work, sizeof(unsigned int));
+  if (e == cudaSuccess)
+    e = cudaMemcpy(sc->tri, stri.data(), sizeof(double) * stri.size(), cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = cudaMemcpy(sc->orig, sorig.data(), sizeof(int) * T, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = cudaMemcpy(sc->obj, sobj.data(), sizeof(int) * T, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess)
+    e = cudaMemcpy(sc->nodes, nodes.data(), sizeof(float4) * nodes.size(), cudaMemcpyHostToDevice);
+  if (e != cudaSuccess) {
+    cudaFree(sc->tri);
+    cudaFree(sc->orig);
+    cudaFree(sc->obj);
+    cudaFree(sc->nodes);
+    cudaFree(sc->work);
+    delete sc;
+    return cuda_fail(e, "mg_meshscene_create");
+  }
+  *out = sc;
+  return MG_OK;
+}
+
+int mg_meshscene_destroy(mg_mesh_scene* s) {
+  if (!s) return MG_OK;
+  cudaFree(s->tri);
+  cudaFree(s->orig);
+  cudaFree(s->obj);
+  cudaFree(s->nodes);
+  cudaFree(s->work);
+  cudaFree(s->wf);
+  delete s;
+  return MG_OK;
+}
+
+int mg_meshscene_info(const mg_mesh_scene* s, int32_t* nodes, int32_t* depth, int64_t* params) {
+  if (!s) return fail(MG_EINVAL, "mg_meshscene_info: null scene");
+  if (nodes) *nodes = s->nnodes;
+  if (depth) *depth = s->depth;
+  if (params) *params = int64_t(s->nobj) * s->nch * s->R * s->R;
+  return MG_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,616 @@
+// Mesh renderer, wavefront form (the default for configs[3] and [4]):
+// SoA path state, per-depth isect / shade / shadow stages over compacted
+// queues, per-pixel adjoint scatter; bit-identical to the megakernel and the
+// oracle.  DESIGN.md §12.
+#include "mesh.cuh"
+
+namespace mg {
+namespace mesh {
+namespace {
+
+// ------------------------------------------------------------ wavefront
+// The same estimator as mesh_pair_kernel, restructured into stages over
+// SoA path state (north_star: "wavefront layout with coalesced SoA path
+// state"): paths P = (nprop + 1) x pixels (proportional paths 0..nprop-1,
+// path 0 also at theta_{t-1}; FD path nprop), then per depth
+//   isect  : closest hit of every live path (all lanes traverse at once)
+//   shade  : texel lookup, NEE sample + shadow-ray set-up, the BSDF values
+//            for both parameter sets, Malley bounce; survivors re-queued
+//   shadow : any-hit of the queued NEE rays; visible -> L += C
+// and finally one thread per pixel forms the residual weights and scatters
+// the stored adjoint data of the proportional paths.  Every per-path
+// quantity is the megakernel's / oracle's (same operations, same order),
+// so the results are bit-identical to both.
+//
+// Per-vertex adjoint fields (T, [v][field][PS]):
+//   NCH 4 (metal 0): A[6] dSn[2] invfb[6] dSb[2] C[6]                 = 22
+//   NCH 5          : A[6] invfb[6] C[6] dfn[2][3][3] dfb[2][3][3]      = 54
+template <int NCH>
+struct VF;
+template <>
+struct VF<4> {
+  static constexpr int n = 22, A = 0, dSn = 6, invfb = 8, dSb = 14, C = 16;
+};
+template <>
+struct VF<5> {
+  static constexpr int n = 54, A = 0, invfb = 6, C = 12, dfn = 18, dfb = 36;
+};
+
+template <class T>
+struct WF {
+  double *ox, *oy, *oz, *dx, *dy, *dz;       // [P] ray
+  double *ht, *hu, *hv;                       // [P] hit
+  double *sox, *soy, *soz, *sdx, *sdy, *sdz, *stm;  // [P] shadow ray
+  T *beta, *L, *E, *pendC;                    // [6][P]
+  int *nv, *hslot, *q0, *q1, *sq;             // [P]
+  int* vbase;                                 // [kMaxV][PS]
+  T* vdat;                                    // [kMaxV][nvf][PS]
+  unsigned int* cnt;                          // [2][kMaxV + 1]: queue / shadow counts
+  int P, PS, npix, pix0, nprop, nvf;
+};
+
+template <class T>
+size_t wf_bytes(int npix, int nprop, int nvf) {
+  const size_t P = size_t(npix) * (nprop + 1), PS = size_t(npix) * nprop;
+  return sizeof(double) * 16 * P + sizeof(T) * 24 * P + sizeof(int) * 5 * P +
+         sizeof(int) * kMaxV * PS + sizeof(T) * kMaxV * nvf * PS +
+         sizeof(unsigned int) * 2 * (kMaxV + 1) + 256 * 40;
+}
+
+template <class T>
+WF<T> wf_carve(void* mem, int npix, int nprop, int nvf) {
+  WF<T> w;
+  char* c = static_cast<char*>(mem);
+  auto take = [&](size_t bytes) {
+    void* r = c;
+    c += (bytes + 255) & ~size_t(255);
+    return r;
+  };
+  w.npix = npix;
+  w.nprop = nprop;
+  w.nvf = nvf;
+  w.P = npix * (nprop + 1);
+  w.PS = npix * nprop;
+  const size_t Pz = size_t(w.P);
+  double** dd[] = {&w.ox, &w.oy, &w.oz, &w.dx, &w.dy, &w.dz, &w.ht, &w.hu, &w.hv,
+                   &w.sox, &w.soy, &w.soz, &w.sdx, &w.sdy, &w.sdz, &w.stm};
+  for (double** d : dd) *d = (double*)take(sizeof(double) * Pz);
+  T** tt[] = {&w.beta, &w.L, &w.E, &w.pendC};
+  for (T** t : tt) *t = (T*)take(sizeof(T) * 6 * Pz);
+  int** ii[] = {&w.nv, &w.hslot, &w.q0, &w.q1, &w.sq};
+  for (int** i : ii) *i = (int*)take(sizeof(int) * Pz);
+  w.vbase = (int*)take(sizeof(int) * kMaxV * size_t(w.PS));
+  w.vdat = (T*)take(sizeof(T) * kMaxV * size_t(nvf) * size_t(w.PS));
+  w.cnt = (unsigned int*)take(sizeof(unsigned int) * 2 * (kMaxV + 1));
+  return w;
+}
+
+// warp-aggregated append: slot in the queue, or -1 when !pred
+__device__ __forceinline__ int enqueue(bool pred, unsigned int* counter) {
+  const unsigned act = __activemask();
+  const unsigned m = __ballot_sync(act, pred);
+  const int lane = int(threadIdx.x & 31), leader = __ffs(act) - 1;
+  unsigned base = 0;
+  if (lane == leader && m) base = atomicAdd(counter, unsigned(__popc(m)));
+  base = __shfl_sync(act, base, leader);
+  return pred ? int(base) + __popc(m & ((1u << lane) - 1u)) : -1;
+}
+
+template <class T>
+__device__ __forceinline__ T& vf(const WF<T>& w, int v, int f, int p) {
+  return w.vdat[(size_t(v) * w.nvf + f) * size_t(w.PS) + p];
+}
+
+template <class T>
+__global__ void __launch_bounds__(kMThreads) wf_gen_kernel(MeshK q, WF<T> w) {
+  const double* V = q.view;
+  for (int p = blockIdx.x * kMThreads + threadIdx.x; p < w.P; p += gridDim.x * kMThreads) {
+    const int k = p / w.npix, pix = w.pix0 + (p - k * w.npix);
+    const int px = pix % q.W, py = pix / q.W;
+    double u[4];
+    prng(q.key, uint32_t(pix), q.iteration, uint32_t(k), 0u, u);
+    const double sx = ((double(px) + u[0]) / double(q.W)) * 2.0 - 1.0;
+    const double sy = 1.0 - ((double(py) + u[1]) / double(q.H)) * 2.0;
+    const double ax = sx * (V[12] * (double(q.W) / double(q.H))), ay = sy * V[12];
+    double d[3];
+#pragma unroll
+    for (int i = 0; i < 3; ++i) d[i] = (V[3 + i] + ax * V[6 + i]) + ay * V[9 + i];
+    const double dl = sqrt(dot3d(d, d));
+    w.ox[p] = V[0];
+    w.oy[p] = V[1];
+    w.oz[p] = V[2];
+    w.dx[p] = d[0] / dl;
+    w.dy[p] = d[1] / dl;
+    w.dz[p] = d[2] / dl;
+#pragma unroll
+    for (int j = 0; j < 6; ++j) {
+      w.beta[size_t(j) * w.P + p] = T(1);
+      w.L[size_t(j) * w.P + p] = T(0);
+      w.E[size_t(j) * w.P + p] = T(0);
+    }
+    w.nv[p] = 0;
+    w.q0[p] = p;
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) w.cnt[0] = unsigned(w.P);
+}
+
+template <class T>
+__global__ void __launch_bounds__(kMThreads, 8) wf_isect_kernel(MeshDev m, WF<T> w, int v) {
+  MESH_SMEM;
+  const int n = int(w.cnt[v]);
+  const int* qin = (v & 1) ? w.q1 : w.q0;
+  for (int i = blockIdx.x * kMThreads + threadIdx.x; i < n; i += gridDim.x * kMThreads) {
+    const int p = qin[i];
+    const double o[3] = {w.ox[p], w.oy[p], w.oz[p]}, d[3] = {w.dx[p], w.dy[p], w.dz[p]};
+    double t = INFINITY, bu = 0.0, bv = 0.0;
+    const int slot = trace_impl<false>(m, sn, o, d, INFINITY, t, bu, bv);
+    w.hslot[p] = slot;
+    w.ht[p] = t;
+    w.hu[p] = bu;
+    w.hv[p] = bv;
+  }
+}
+
+template <class T, int NCH>
+__global__ void __launch_bounds__(kMThreads)
+    wf_shade_kernel(MeshK q, MeshDev m, WF<T> w, int v, const T* __restrict__ th0,
+                    const T* __restrict__ th1) {
+  using F = VF<NCH>;
+  const double* V = q.view;
+  const int maxv = int(V[24]);
+  const int R2 = q.R * q.R;
+  const int n = int(w.cnt[v]);
+  const int* qin = (v & 1) ? w.q1 : w.q0;
+  int* qout = (v & 1) ? w.q0 : w.q1;
+  const double la = (V[15] - V[14]) * (V[17] - V[16]);
+  const T* th[2] = {th0, th1};
+  for (int i = blockIdx.x * kMThreads + threadIdx.x; i - int(threadIdx.x) < n;
+       i += gridDim.x * kMThreads) {
+    bool want_shadow = false, want_bounce = false;
+    int p = -1;
+    if (i < n) {
+      p = qin[i];
+      const int k = p / w.npix, pix = w.pix0 + (p - k * w.npix);
+      const int slot = w.hslot[p];
+      const bool store = p < w.PS;
+      // parameter sets evaluated: path 0 (A) and the FD path at theta_t and
+      // theta_{t-1}; the other proportional paths at theta_t only
+      const int ns = (k == 0 || k == w.nprop) ? 2 : 1;
+      // every stored field of vertex v is written exactly once below
+      auto zero_nee = [&](int s) {
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+          vf(w, v, F::A + s * 3 + c, p) = T(0);
+          vf(w, v, F::C + s * 3 + c, p) = T(0);
+        }
+        if constexpr (NCH == 5) {
+#pragma unroll
+          for (int j = 0; j < 9; ++j) vf(w, v, VF<5>::dfn + s * 9 + j, p) = T(0);
+        } else {
+          vf(w, v, VF<4>::dSn + s, p) = T(0);
+        }
+      };
+      auto zero_bounce = [&](int s) {
+#pragma unroll
+        for (int c = 0; c < 3; ++c) vf(w, v, F::invfb + s * 3 + c, p) = T(0);
+        if constexpr (NCH == 5) {
+#pragma unroll
+          for (int j = 0; j < 9; ++j) vf(w, v, VF<5>::dfb + s * 9 + j, p) = T(0);
+        } else {
+          vf(w, v, VF<4>::dSb + s, p) = T(0);
+        }
+      };
+      T beta[2][3];
+#pragma unroll
+      for (int s = 0; s < 2; ++s)
+#pragma unroll
+        for (int c = 0; c < 3; ++c) beta[s][c] = w.beta[size_t(s * 3 + c) * w.P + p];
+      if (slot < 0) {  // escaped: environment
+#pragma unroll
+        for (int s = 0; s < 2; ++s)
+#pragma unroll
+          for (int c = 0; c < 3; ++c) {
+            if (s >= ns) break;
+            const T e = beta[s][c] * T(V[21 + c]);
+            w.E[size_t(s * 3 + c) * w.P + p] = e;
+            w.L[size_t(s * 3 + c) * w.P + p] += e;
+          }
+      } else {
+        const double o[3] = {w.ox[p], w.oy[p], w.oz[p]}, d[3] = {w.dx[p], w.dy[p], w.dz[p]};
+        const double t = w.ht[p], bu = w.hu[p], bv = w.hv[p];
+        const double* r = m.tri + size_t(kRec) * slot;
+        const double x[3] = {o[0] + t * d[0], o[1] + t * d[1], o[2] + t * d[2]};
+        double nn[3] = {r[9], r[10], r[11]};
+        if (dot3d(nn, d) > 0.0) {
+          nn[0] = -nn[0];
+          nn[1] = -nn[1];
+          nn[2] = -nn[2];
+        }
+        const double U = (r[12] + bu * r[14]) + bv * r[16];
+        const double W_ = (r[13] + bu * r[15]) + bv * r[17];
+        int tx = int(U * q.R), ty = int(W_ * q.R);
+        tx = tx < 0 ? 0 : (tx > q.R - 1 ? q.R - 1 : tx);
+        ty = ty < 0 ? 0 : (ty > q.R - 1 ? q.R - 1 : ty);
+        const int pbase = __ldg(&m.obj[slot]) * NCH * R2 + ty * q.R + tx;
+        w.nv[p] = v + 1;
+        if (store) w.vbase[size_t(v) * w.PS + p] = pbase;
+        bool nee_done = false, bounce_done = false;
+        T base[2][3], rough[2], metal[2];
+#pragma unroll
+        for (int s = 0; s < 2; ++s) {
+#pragma unroll
+          for (int c = 0; c < 3; ++c) base[s][c] = th[s][pbase + c * R2];
+          rough[s] = th[s][pbase + 3 * R2];
+          metal[s] = NCH == 5 ? th[s][pbase + 4 * R2] : T(0);
+        }
+        const double wo[3] = {-d[0], -d[1], -d[2]};
+        const double xo[3] = {x[0] + kOff * nn[0], x[1] + kOff * nn[1], x[2] + kOff * nn[2]};
+        double u[4];
+        prng(q.key, uint32_t(pix), q.iteration, uint32_t(k), uint32_t(v * 256 + 1), u);
+        const double lp[3] = {V[14] + u[0] * (V[15] - V[14]), V[13],
+                              V[16] + u[1] * (V[17] - V[16])};
+        double wl3[3] = {lp[0] - x[0], lp[1] - x[1], lp[2] - x[2]};
+        const double d2 = dot3d(wl3, wl3);
+        const double wl = sqrt(d2);
+        wl3[0] /= wl;
+        wl3[1] /= wl;
+        wl3[2] /= wl;
+        const double cx = dot3d(nn, wl3), cl = wl3[1];
+        const T nT[3] = {T(nn[0]), T(nn[1]), T(nn[2])}, woT[3] = {T(wo[0]), T(wo[1]), T(wo[2])};
+        if (cx > 0.0 && cl > 0.0 && dot3d(nn, wo) > 0.0) {
+          want_shadow = true;
+          const double gl = ((cx * cl) / d2) * la;
+          const T wT[3] = {T(wl3[0]), T(wl3[1]), T(wl3[2])};
+          nee_done = true;
+#pragma unroll
+          for (int s = 0; s < 2; ++s) {
+            if (s >= ns) break;
+            T f[3];
+            if constexpr (NCH == 5) {
+              T df[3][3];
+              bsdf_full<T>(base[s], metal[s], rough[s], nT, wT, woT, f, df);
+              if (store)
+#pragma unroll
+                for (int c = 0; c < 3; ++c)
+#pragma unroll
+                  for (int kk = 0; kk < 3; ++kk) vf(w, v, F::dfn + s * 9 + c * 3 + kk, p) = df[c][kk];
+            } else {
+              T dS;
+              bsdf_m0<T>(base[s], rough[s], nT, wT, woT, f, dS);
+              if (store) vf(w, v, VF<4>::dSn + s, p) = dS;
+            }
+#pragma unroll
+            for (int c = 0; c < 3; ++c) {
+              const T A = beta[s][c] * T(gl * V[18 + c]);
+              const T Cc = A * f[c];
+              if (store) {
+                vf(w, v, F::A + s * 3 + c, p) = A;
+                vf(w, v, F::C + s * 3 + c, p) = Cc;
+              }
+              w.pendC[size_t(s * 3 + c) * w.P + p] = Cc;
+            }
+          }
+          w.sox[p] = xo[0];
+          w.soy[p] = xo[1];
+          w.soz[p] = xo[2];
+          w.sdx[p] = wl3[0];
+          w.sdy[p] = wl3[1];
+          w.sdz[p] = wl3[2];
+          w.stm[p] = wl - kOff;
+        }
+        if (!(v == maxv - 1 || dot3d(nn, wo) <= 0.0)) {
+          double dx = 0.0, dy = 0.0;
+          bool got = false;
+          for (uint32_t j = 0; !got && j < 64; ++j) {
+            double c4[4];
+            if (j == 0) {
+              c4[0] = u[2];
+              c4[1] = u[3];
+              c4[2] = 2.0;
+              c4[3] = 2.0;
+            } else {
+              prng(q.key, uint32_t(pix), q.iteration, uint32_t(k), uint32_t(v * 256 + 1) + j, c4);
+            }
+#pragma unroll
+            for (int mm = 0; mm < 4; mm += 2) {
+              if (got) break;
+              const double a = 2.0 * c4[mm] - 1.0, b = 2.0 * c4[mm + 1] - 1.0;
+              if (c4[mm] <= 1.0 && a * a + b * b < 1.0) {
+                dx = a;
+                dy = b;
+                got = true;
+              }
+            }
+          }
+          const double dz = sqrt(fmax(0.0, 1.0 - (dx * dx + dy * dy)));
+          if (dz > 0.0) {
+            const double sign = copysign(1.0, nn[2]);
+            const double aa = -1.0 / (sign + nn[2]);
+            const double bb = nn[0] * nn[1] * aa;
+            const double Tb[3] = {1.0 + sign * (nn[0] * nn[0]) * aa, sign * bb, -sign * nn[0]};
+            const double Bb[3] = {bb, sign + (nn[1] * nn[1]) * aa, -nn[1]};
+            const double wi[3] = {(dx * Tb[0] + dy * Bb[0]) + dz * nn[0],
+                                  (dx * Tb[1] + dy * Bb[1]) + dz * nn[1],
+                                  (dx * Tb[2] + dy * Bb[2]) + dz * nn[2]};
+            const T wiT[3] = {T(wi[0]), T(wi[1]), T(wi[2])};
+            bounce_done = true;
+#pragma unroll
+            for (int s = 0; s < 2; ++s) {
+              if (s >= ns) break;
+              T f[3];
+              if constexpr (NCH == 5) {
+                T df[3][3];
+                bsdf_full<T>(base[s], metal[s], rough[s], nT, wiT, woT, f, df);
+                if (store)
+#pragma unroll
+                  for (int c = 0; c < 3; ++c)
+#pragma unroll
+                    for (int kk = 0; kk < 3; ++kk)
+                      vf(w, v, F::dfb + s * 9 + c * 3 + kk, p) = df[c][kk];
+              } else {
+                T dS;
+                bsdf_m0<T>(base[s], rough[s], nT, wiT, woT, f, dS);
+                if (store) vf(w, v, VF<4>::dSb + s, p) = dS;
+              }
+#pragma unroll
+              for (int c = 0; c < 3; ++c) {
+                if (store) vf(w, v, F::invfb + s * 3 + c, p) = f[c] != T(0) ? T(1) / f[c] : T(0);
+                w.beta[size_t(s * 3 + c) * w.P + p] = beta[s][c] * (f[c] * T(kPiM));
+              }
+            }
+            w.ox[p] = xo[0];
+            w.oy[p] = xo[1];
+            w.oz[p] = xo[2];
+            w.dx[p] = wi[0];
+            w.dy[p] = wi[1];
+            w.dz[p] = wi[2];
+            want_bounce = true;
+          }
+        }
+        if (store)
+          for (int s = 0; s < ns; ++s) {
+            if (!nee_done) zero_nee(s);
+            if (!bounce_done) zero_bounce(s);
+          }
+      }
+    }
+    const int qs = enqueue(want_shadow, &w.cnt[kMaxV + 1 + v]);
+    if (qs >= 0) w.sq[qs] = p;
+    const int qb = enqueue(want_bounce, &w.cnt[v + 1]);
+    if (qb >= 0) qout[qb] = p;
+  }
+}
+
+template <class T, int NCH>
+__global__ void __launch_bounds__(kMThreads, 8) wf_shadow_kernel(MeshDev m, WF<T> w, int v) {
+  using F = VF<NCH>;
+  MESH_SMEM;
+  const int n = int(w.cnt[kMaxV + 1 + v]);
+  for (int i = blockIdx.x * kMThreads + threadIdx.x; i < n; i += gridDim.x * kMThreads) {
+    const int p = w.sq[i];
+    const double o[3] = {w.sox[p], w.soy[p], w.soz[p]}, d[3] = {w.sdx[p], w.sdy[p], w.sdz[p]};
+    double ts, tu, tv;
+    if (trace_impl<true>(m, sn, o, d, w.stm[p], ts, tu, tv) < 0) {
+      const int k = p / w.npix;
+      const int nj = (k == 0 || k == w.nprop) ? 6 : 3;
+      for (int j = 0; j < nj; ++j) w.L[size_t(j) * w.P + p] += w.pendC[size_t(j) * w.P + p];
+    } else if (p < w.PS) {  // occluded: no NEE data at this vertex
+#pragma unroll
+      for (int j = 0; j < 6; ++j) {
+        vf(w, v, F::A + j, p) = T(0);
+        vf(w, v, F::C + j, p) = T(0);
+      }
+      if constexpr (NCH == 5) {
+        for (int j = 0; j < 18; ++j) vf(w, v, VF<5>::dfn + j, p) = T(0);
+      } else {
+        vf(w, v, VF<4>::dSn, p) = T(0);
+        vf(w, v, VF<4>::dSn + 1, p) = T(0);
+      }
+    }
+  }
+}
+
+// adjoint of stored path p (megakernel `scatter` / oracle ms_scatter)
+template <class T, int NCH>
+__device__ __noinline__ void wf_scatter(const WF<T>& w, int p, int s, const T wt[3], int R2,
+                                        unsigned long long* __restrict__ acc) {
+  using F = VF<NCH>;
+  T Q[3];
+#pragma unroll
+  for (int c = 0; c < 3; ++c) Q[c] = w.E[size_t(s * 3 + c) * w.P + p];
+  for (int v = w.nv[p] - 1; v >= 0; --v) {
+    const int base = w.vbase[size_t(v) * w.PS + p];
+    if constexpr (NCH == 5) {
+      T gm = T(0), gr = T(0);
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        const T A = vf(w, v, F::A + s * 3 + c, p), fb = vf(w, v, F::invfb + s * 3 + c, p);
+        const int dn = F::dfn + s * 9 + c * 3, db = F::dfb + s * 9 + c * 3;
+        const T gb = wt[c] * (A * vf(w, v, dn, p) + Q[c] * (fb * vf(w, v, db, p)));
+        atomicAdd(&acc[base + c * R2], fixq(double(gb)));
+        gm += wt[c] * (A * vf(w, v, dn + 1, p) + Q[c] * (fb * vf(w, v, db + 1, p)));
+        gr += wt[c] * (A * vf(w, v, dn + 2, p) + Q[c] * (fb * vf(w, v, db + 2, p)));
+      }
+      atomicAdd(&acc[base + 3 * R2], fixq(double(gr)));
+      atomicAdd(&acc[base + 4 * R2], fixq(double(gm)));
+    } else {
+      const T dSn = vf(w, v, F::dSn + s, p), dSb = vf(w, v, F::dSb + s, p);
+      T gr = T(0);
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        const T A = vf(w, v, F::A + s * 3 + c, p), ifb = vf(w, v, F::invfb + s * 3 + c, p);
+        const T gb = wt[c] * ((A / T(kPiM)) + Q[c] * (ifb / T(kPiM)));
+        atomicAdd(&acc[base + c * R2], fixq(double(gb)));
+        gr += wt[c] * (A * dSn + Q[c] * (ifb * dSb));
+      }
+      atomicAdd(&acc[base + 3 * R2], fixq(double(gr)));
+    }
+#pragma unroll
+    for (int c = 0; c < 3; ++c) Q[c] = Q[c] + vf(w, v, F::C + s * 3 + c, p);
+  }
+}
+
+constexpr int kMaxProp = 8;
+
+template <class T, int NCH>
+__global__ void __launch_bounds__(kMThreads)
+    wf_scatter_kernel(MeshK q, WF<T> w, const T* __restrict__ target_img,
+                      unsigned long long* __restrict__ acc, long long np,
+                      ReducePartials* partials, unsigned int* counter, double* loss_out) {
+  const int npix_img = q.W * q.H;
+  const int R2 = q.R * q.R;
+  const int n = w.nprop;
+  const T scale = T(2.0 / (n * (n - 1.0)));
+  double loss = 0.0;
+  for (int i = blockIdx.x * kMThreads + threadIdx.x; i < w.npix; i += gridDim.x * kMThreads) {
+    const int pix = w.pix0 + i;
+    const int pc = n * w.npix + i;
+    T r[kMaxProp][3], wC0[3], wC1[3];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      const T Is = target_img[size_t(c) * npix_img + pix];
+      for (int j = 0; j < n; ++j) r[j][c] = w.L[size_t(c) * w.P + j * w.npix + i] - Is;
+      wC0[c] = T(2) * (w.L[size_t(c) * w.P + pc] - Is);
+      wC1[c] = T(-2) * (w.L[size_t(3 + c) * w.P + pc] - Is);
+      T lp = T(0);
+      for (int a = 0; a < n; ++a)
+        for (int b = a + 1; b < n; ++b) lp += r[a][c] * r[b][c];
+      loss += double(lp * scale);
+    }
+    for (int j = 0; j < n; ++j) {
+      T wt[3];
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        T a = T(0);
+        bool first = true;
+        for (int k = 0; k < n; ++k) {
+          if (k == j) continue;
+          a = first ? r[k][c] : a + r[k][c];
+          first = false;
+        }
+        wt[c] = a * scale;
+      }
+      wf_scatter<T, NCH>(w, j * w.npix + i, 0, wt, R2, acc);
+    }
+    wf_scatter<T, NCH>(w, i, 0, wC0, R2, acc + np);
+    wf_scatter<T, NCH>(w, i, 1, wC1, R2, acc + np);
+  }
+  Acc a;
+  a.ssn = loss;
+  grid_reduce4<kMThreads>(a.partials(), partials, counter,
+                          [&](const ReducePartials& t) { *loss_out = t.ssn; });
+}
+
+template <class T>
+__global__ void mesh_finalize_kernel(long long n, unsigned long long* __restrict__ acc,
+                                     T* __restrict__ prop, T* __restrict__ diff) {
+  for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < n;
+       k += (long long)gridDim.x * blockDim.x) {
+    prop[k] = T(double((long long)acc[k]) / kFixM);
+    diff[k] = T(double((long long)acc[n + k]) / kFixM);
+    acc[k] = 0ull;
+    acc[n + k] = 0ull;
+  }
+}
+
+}  // namespace
+
+template <class T, int NCH>
+int wavefront_pair(mg_ctx* ctx, mg_mesh_scene* s, const MeshK& q, int nprop, const T* target_img,
+                   const T* now, const T* prev, unsigned long long* acc, long long np,
+                   double* loss_out) {
+  const int npix = q.W * (q.row1 - q.row0);
+  if (npix == 0) {
+    MG_CUDA_TRY(cudaMemsetAsync(loss_out, 0, sizeof(double), ctx->stream));
+    return MG_OK;
+  }
+  if (int64_t(npix) * (nprop + 1) > 0x7fffffffLL) return fail(MG_EINVAL, "mesh scene: image too large");
+  const size_t need = wf_bytes<T>(npix, nprop, VF<NCH>::n);
+  if (need > s->wf_cap) {
+    MG_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+    cudaFree(s->wf);
+    s->wf = nullptr;
+    s->wf_cap = 0;
+    MG_CUDA_TRY(cudaMalloc(&s->wf, need));
+    s->wf_cap = need;
+  }
+  WF<T> w = wf_carve<T>(s->wf, npix, nprop, VF<NCH>::n);
+  w.pix0 = q.row0 * q.W;
+  const MeshDev m = dev_of(s);
+  MG_CUDA_TRY(cudaMemsetAsync(w.cnt, 0, sizeof(unsigned int) * 2 * (kMaxV + 1), ctx->stream));
+  const int grid = grid_for(ctx, w.P, kMThreads, 8);
+  wf_gen_kernel<T><<<grid, kMThreads, 0, ctx->stream>>>(q, w);
+  MG_LAUNCH_CHECK(ctx);
+  const int maxv = int(q.view[24]);
+  for (int v = 0; v < maxv; ++v) {
+    wf_isect_kernel<T><<<grid, kMThreads, 0, ctx->stream>>>(m, w, v);
+    MG_LAUNCH_CHECK(ctx);
+    wf_shade_kernel<T, NCH><<<grid, kMThreads, 0, ctx->stream>>>(q, m, w, v, now, prev);
+    MG_LAUNCH_CHECK(ctx);
+    wf_shadow_kernel<T, NCH><<<grid, kMThreads, 0, ctx->stream>>>(m, w, v);
+    MG_LAUNCH_CHECK(ctx);
+  }
+  wf_scatter_kernel<T, NCH><<<grid_for(ctx, npix, kMThreads, 8), kMThreads, 0, ctx->stream>>>(
+      q, w, target_img, acc, np, ctx->partials, ctx->counter, loss_out);
+  MG_LAUNCH_CHECK(ctx);
+  return MG_OK;
+}
+
+}  // namespace mesh
+}  // namespace mg
+
+using namespace mg;
+using namespace mg::mesh;
+
+extern "C" {
+
+int mg_meshscene_sample_pair(mg_ctx* ctx, mg_mesh_scene* s, int32_t dtype, int32_t W,
+                             int32_t H, const double* view, const void* target_img,
+                             const void* now, const void* prev, uint64_t key, uint32_t iteration,
+                             int32_t row0, int32_t row1, int32_t prop_paths, void* accum,
+                             void* prop, void* diff, double* loss_out) {
+  if (!ctx || !s || !target_img || !now || !prev || !accum || !prop || !diff || !loss_out)
+    return fail(MG_EINVAL, "mg_meshscene_sample_pair: null argument");
+  if (prop_paths < 2 || prop_paths > kMaxProp)
+    return fail(MG_EINVAL, "mg_meshscene_sample_pair: prop_paths must lie in [2, 8]");
+  if (W < 1 || H < 1) return fail(MG_EINVAL, "mg_meshscene_sample_pair: bad sizes");
+  if (row0 < 0 || row1 > H || row0 > row1)
+    return fail(MG_EINVAL, "mg_meshscene_sample_pair: bad rows");
+  int st = check_view(view);
+  if (st) return st;
+  MeshK q = make_k(s, W, H, view, key, iteration);
+  q.row0 = row0;
+  q.row1 = row1;
+  const long long np = (long long)s->nobj * s->nch * s->R * s->R;
+  unsigned long long* acc = (unsigned long long*)accum;
+  // the megakernel implements the configs[3] form (4 channels, 2 proportional paths)
+  if (g_mesh_megakernel && s->nch == 4 && prop_paths == 2) {
+    st = megakernel_pair(ctx, s, q, dtype, target_img, now, prev, acc, np, loss_out);
+  } else if (dtype == MG_F64 && s->nch == 5) {
+    st = wavefront_pair<double, 5>(ctx, s, q, prop_paths, (const double*)target_img,
+                                   (const double*)now, (const double*)prev, acc, np, loss_out);
+  } else if (dtype == MG_F64) {
+    st = wavefront_pair<double, 4>(ctx, s, q, prop_paths, (const double*)target_img,
+                                   (const double*)now, (const double*)prev, acc, np, loss_out);
+  } else if (dtype == MG_F32 && s->nch == 5) {
+    st = wavefront_pair<float, 5>(ctx, s, q, prop_paths, (const float*)target_img,
+                                  (const float*)now, (const float*)prev, acc, np, loss_out);
+  } else if (dtype == MG_F32) {
+    st = wavefront_pair<float, 4>(ctx, s, q, prop_paths, (const float*)target_img,
+                                  (const float*)now, (const float*)prev, acc, np, loss_out);
+  } else {
+    return fail(MG_EINVAL, "mg_meshscene_sample_pair: unknown dtype");
+  }
+  if (st) return st;
+  const int fgrid = grid_for(ctx, np, 256, 8);
+  if (dtype == MG_F64)
+    mesh_finalize_kernel<double><<<fgrid, 256, 0, ctx->stream>>>(np, acc, (double*)prop,
+                                                                 (double*)diff);
+  else
+    mesh_finalize_kernel<float><<<fgrid, 256, 0, ctx->stream>>>(np, acc, (float*)prop,
+                                                                (float*)diff);
+  MG_LAUNCH_CHECK(ctx);
+  return MG_OK;
+}
+
+}  // extern "C"
