@@ -45,7 +45,10 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=None)
     ap.add_argument("--cpu-n", type=int, default=1 << 22, help="reference sample size")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--extras", action="store_true", help="also time Adam and the mini-render runner")
+    ap.add_argument("--extras", action="store_true",
+                    help="force the secondary measurements (default: on for a single GPU)")
+    ap.add_argument("--no-extras", action="store_true",
+                    help="skip the secondary measurements (Adam, fused renders, F1 scenes)")
     ap.add_argument("--no-tma", action="store_true", help="register-streaming kernel instead of TMA")
     return ap.parse_args()
 
@@ -313,7 +316,7 @@ def run_ours(args):
         pg.barrier()
     del props, diffs
     torch.cuda.empty_cache()
-    if rank == 0 and args.extras:
+    if rank == 0 and not args.no_extras and (world == 1 or args.extras):
         line["extras"] = extras(args, ctx)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
@@ -332,177 +335,140 @@ def run_ours(args):
 
 
 def extras(args, ctx):
-    """Secondary measurements: Adam kernel roofline, device runner."""
+    """Secondary measurements, each guarded (a failure is recorded, never
+    fatal): Adam kernel roofline, fused mini-render iterations, the F1
+    path-traced scenes of BASELINE configs[0], [2], [3], [4], BVH ray
+    throughput, the replicate runner."""
     import torch
     from paper_2309_15676_b200 import api
     out = {}
     n = args.n
     dev = torch.device("cuda", ctx.device)
-    g = torch.randn(n, device=dev)
-    pa, pb = torch.zeros(n, device=dev), torch.empty(n, device=dev)
-    ad = api.FusedAdamUpdate(n, ctx=ctx)
-    for i in range(3):
-        ad.step(g, pa if i % 2 == 0 else pb, pb if i % 2 == 0 else pa)
-    torch.cuda.synchronize()
-    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    a.record(ctx.stream)
-    K = 10
-    for i in range(K):
-        ad.step(g, pa if i % 2 == 0 else pb, pb if i % 2 == 0 else pa)
-    b.record(ctx.stream)
-    torch.cuda.synchronize()
-    ms = a.elapsed_time(b) / K
     peak, _ = measured_peak()
-    out["adam_update_f32"] = {"ms": ms, "gbs": 28 * n / (ms / 1e3) / 1e9,
-                              "frac": 28 * n / (ms / 1e3) / 1e9 / peak}
-    del g, pa, pb, ad
-    torch.cuda.empty_cache()
-    # fused mini-render iteration at scale (config 5 image size x 16): one
-    # kernel per iteration, sample pair in registers, Philox draws
-    P, spp, iters = 1 << 24, 2, 50
-    run = api.MiniRenderRun(P, spp, gen_seed=1, lr=0.01, rng="philox", dtype=torch.float32,
-                            ctx=ctx)
-    for _ in range(3):
-        run.step()
-    torch.cuda.synchronize()
-    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    a.record(ctx.stream)
-    for _ in range(iters):
-        run.step()
-    b.record(ctx.stream)
-    torch.cuda.synchronize()
-    ms = a.elapsed_time(b) / iters
-    out["minirender_fused_philox_f32"] = {
-        "pixels": P, "spp": spp, "iterations": iters, "ms_per_iteration": ms,
-        "pairs_per_s": P * spp / (ms / 1e3), "gbs": 60 * P / (ms / 1e3) / 1e9,
-        "frac": 60 * P / (ms / 1e3) / 1e9 / peak, "loss": run.scalars().loss}
-    del run
-    torch.cuda.empty_cache()
-    # same, with the reference's exact mt19937_64 stream: 591 engines on ONE
-    # stream (GF(2) jump-ahead), bit-identical draws to the sequential stream
-    run = api.MiniRenderRun(P, spp, gen_seed=1, lr=0.01, rng="mt64", dtype=torch.float32, ctx=ctx)
-    for _ in range(2):
-        run.step()
-    torch.cuda.synchronize()
-    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    a.record(ctx.stream)
-    for _ in range(10):
-        run.step()
-    b.record(ctx.stream)
-    torch.cuda.synchronize()
-    ms = a.elapsed_time(b) / 10
-    out["minirender_fused_mt64_exact_f32"] = {
-        "pixels": P, "spp": spp, "engines": run.rng.n, "ms_per_iteration": ms,
-        "pairs_per_s": P * spp / (ms / 1e3)}
-    del run
-    torch.cuda.empty_cache()
-    # F1 slice, BASELINE configs[0]: 64x64 textured quad, 32x32 RGB texture,
-    # 1 FD + 2 proportional spp, 200 meta iterations (render+scatter, update)
-    for W, R, iters in ((64, 32, 200), (1024, 512, 50)):
-        prob = api.QuadTextureProblem(W, W, R, target_spp=64, dtype=torch.float32, ctx=ctx)
-        qrun = api.QuadTextureRun(prob, optimizer="meta", lr=0.01)
-        for _ in range(3):
-            qrun.step()
+
+    def timed(step, iters, warm=2):
+        """ms per call of step() on ctx's stream (CUDA events)."""
+        for _ in range(warm):
+            step()
         torch.cuda.synchronize()
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record(ctx.stream)
         for _ in range(iters):
-            qrun.step()
+            step()
         b.record(ctx.stream)
         torch.cuda.synchronize()
-        ms = a.elapsed_time(b) / iters
-        out[f"quad_texture_{W}px_{R}tex_f32"] = {
-            "iterations": iters, "ms_per_iteration": ms, "iterations_per_s": 1e3 / ms,
-            "path_samples_per_s": prob.draws_per_sample() / (ms / 1e3),
-            "texture_params": prob.dim()}
-        del prob, qrun
-    torch.cuda.empty_cache()
-    # F1 slice 2, BASELINE configs[2]: 256x256 helix of 64 spheres, depth-4
-    # path tracing with NEE, 5 principled-BSDF parameters, 1 FD + 2 prop spp
-    for dtn, dt in (("f32", torch.float32), ("f64", torch.float64)):
-        hprob = api.HelixProblem(256, 256, target_spp=16, dtype=dt, ctx=ctx)
-        hrun = api.HelixRun(hprob, optimizer="meta", lr=0.01)
-        for _ in range(2):
-            hrun.step()
-        torch.cuda.synchronize()
-        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        a.record(ctx.stream)
-        for _ in range(10):
-            hrun.step()
-        b.record(ctx.stream)
-        torch.cuda.synchronize()
-        ms = a.elapsed_time(b) / 10
-        out[f"helix_256px_{dtn}"] = {"ms_per_iteration": ms, "iterations_per_s": 1e3 / ms,
-                                     "paths_per_s": hprob.draws_per_sample() / (ms / 1e3)}
-        del hprob, hrun
-    # F1 slice 3, BASELINE configs[3]: 512x512 image of the 3-object mesh
-    # scene (22k triangles, BVH), 3 x 512^2 RGB+roughness textures (3.1M
-    # parameters), depth 6 with NEE, 1 FD + 2 prop spp; sample pair + update
-    mprob = api.MeshTextureProblem(512, 512, 512, max_vertices=6, target_spp=4,
-                                   dtype=torch.float32, ctx=ctx)
-    mrun = api.MeshTextureRun(mprob, optimizer="meta", lr=0.005)
-    for _ in range(2):
-        mrun.step()
-    torch.cuda.synchronize()
-    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    a.record(ctx.stream)
-    for _ in range(5):
-        mrun.step()
-    b.record(ctx.stream)
-    torch.cuda.synchronize()
-    ms = a.elapsed_time(b) / 5
-    out["mesh_texture_512px_f32"] = {"ms_per_iteration": ms, "iterations_per_s": 1e3 / ms,
-                                     "paths_per_s": mprob.draws_per_sample() / (ms / 1e3),
-                                     "texture_params": mprob.dim(), **mprob.scene.info()}
-    # BVH closest-hit throughput on the same scene (random rays at the objects)
-    nr = 1 << 22
-    g = torch.Generator(device="cuda").manual_seed(0)
-    org = torch.stack([torch.rand(nr, device="cuda", generator=g, dtype=torch.float64) * 4 - 2,
-                       torch.rand(nr, device="cuda", generator=g, dtype=torch.float64) * 2 + 0.1,
-                       torch.full((nr,), 4.0, device="cuda", dtype=torch.float64)], 1)
-    tgt = torch.stack([torch.rand(nr, device="cuda", generator=g, dtype=torch.float64) * 3 - 1.5,
-                       torch.rand(nr, device="cuda", generator=g, dtype=torch.float64) * 1.1,
-                       torch.zeros(nr, device="cuda", dtype=torch.float64)], 1)
-    dirs = tgt - org
-    dirs /= torch.linalg.vector_norm(dirs, dim=1, keepdim=True)
-    rays = torch.cat([org, dirs], 1).contiguous()
-    mprob.scene.intersect(rays)
-    torch.cuda.synchronize()
-    a.record(ctx.stream)
-    mprob.scene.intersect(rays)
-    b.record(ctx.stream)
-    torch.cuda.synchronize()
-    out["mesh_bvh_closest_hit"] = {"rays": nr, "ms": a.elapsed_time(b),
-                                   "rays_per_s": nr / (a.elapsed_time(b) / 1e3)}
-    del mprob, mrun, rays, org, tgt, dirs
-    torch.cuda.empty_cache()
-    # F1 slice 4, BASELINE configs[4]: 1024^2, 16 objects / ~502k triangles,
-    # 16 x 5 x 1024^2 = 83.9M texture parameters (base rgb, roughness,
-    # metalness), depth 8, 1 FD + 4 proportional spp
-    lprob = api.MeshLargeProblem(target_spp=2, ctx=ctx)
-    lrun = api.MeshTextureRun(lprob, optimizer="meta", lr=0.005)
-    for _ in range(2):
-        lrun.step()
-    torch.cuda.synchronize()
-    a.record(ctx.stream)
-    for _ in range(3):
-        lrun.step()
-    b.record(ctx.stream)
-    torch.cuda.synchronize()
-    ms = a.elapsed_time(b) / 3
-    out["mesh_large_1024px_f32"] = {"ms_per_iteration": ms, "iterations_per_s": 1e3 / ms,
-                                    "paths_per_s": lprob.draws_per_sample() / (ms / 1e3),
-                                    "texture_params": lprob.dim(), **lprob.scene.info()}
-    del lprob, lrun
-    torch.cuda.empty_cache()
-    # mini-render stand-in for configs[0] (P=4096, spp=2, 200 iterations)
-    cfg = api.ExperimentConfig(problem="mini-render", pixel_count=4096, spp=2, iterations=200,
-                               seed=0, problem_seed=1, lr=0.01, replicates=148)
-    t0 = time.time()
-    api.run_experiment(cfg, ctx=ctx)
-    wall = time.time() - t0
-    out["minirender_runner"] = {"replicates": 148, "iterations": 200, "wall_s": wall,
-                                "pairs_per_s": 148 * 200 * 4096 * 2 / wall}
+        return a.elapsed_time(b) / iters
+
+    def adam():
+        g = torch.randn(n, device=dev)
+        buf = [torch.zeros(n, device=dev), torch.empty(n, device=dev)]
+        ad = api.FusedAdamUpdate(n, ctx=ctx)
+        k = [0]
+
+        def step():
+            ad.step(g, buf[k[0] % 2], buf[(k[0] + 1) % 2])
+            k[0] += 1
+        ms = timed(step, 10, warm=3)
+        out["adam_update_f32"] = {"ms": ms, "gbs": 28 * n / (ms / 1e3) / 1e9,
+                                  "frac": 28 * n / (ms / 1e3) / 1e9 / peak}
+
+    def minirender(rng):
+        # fused mini-render iteration at scale (16.7M pixels): one kernel per
+        # iteration, sample pair in registers; philox draws, or the
+        # reference's exact mt19937_64 stream (engines tiling ONE stream via
+        # GF(2) jump-ahead, bit-identical draws)
+        P, spp = 1 << 24, 2
+        run = api.MiniRenderRun(P, spp, gen_seed=1, lr=0.01, rng=rng, dtype=torch.float32,
+                                ctx=ctx)
+        ms = timed(run.step, 50 if rng == "philox" else 10, warm=3 if rng == "philox" else 2)
+        r = {"pixels": P, "spp": spp, "ms_per_iteration": ms,
+             "pairs_per_s": P * spp / (ms / 1e3)}
+        if rng == "philox":
+            r.update({"gbs": 60 * P / (ms / 1e3) / 1e9, "frac": 60 * P / (ms / 1e3) / 1e9 / peak,
+                      "loss": run.scalars().loss})
+        else:
+            r["engines"] = run.rng.n
+        out["minirender_fused_philox_f32" if rng == "philox" else
+            "minirender_fused_mt64_exact_f32"] = r
+
+    def quad():
+        # F1 slice, configs[0]: 64x64 textured quad, 32x32 RGB texture, 1 FD +
+        # 2 proportional spp; and a 1024^2 / 512^2-texture variant
+        for W, R, iters in ((64, 32, 200), (1024, 512, 50)):
+            prob = api.QuadTextureProblem(W, W, R, target_spp=64, dtype=torch.float32, ctx=ctx)
+            run = api.QuadTextureRun(prob, optimizer="meta", lr=0.01)
+            ms = timed(run.step, iters, warm=3)
+            out[f"quad_texture_{W}px_{R}tex_f32"] = {
+                "iterations": iters, "ms_per_iteration": ms, "iterations_per_s": 1e3 / ms,
+                "path_samples_per_s": prob.draws_per_sample() / (ms / 1e3),
+                "texture_params": prob.dim()}
+
+    def helix():
+        # F1 slice 2, configs[2]: 256x256 helix of 64 spheres, depth 4 + NEE,
+        # 5 principled-BSDF parameters
+        for dtn, dt in (("f32", torch.float32), ("f64", torch.float64)):
+            prob = api.HelixProblem(256, 256, target_spp=16, dtype=dt, ctx=ctx)
+            run = api.HelixRun(prob, optimizer="meta", lr=0.01)
+            ms = timed(run.step, 10)
+            out[f"helix_256px_{dtn}"] = {"ms_per_iteration": ms, "iterations_per_s": 1e3 / ms,
+                                         "paths_per_s": prob.draws_per_sample() / (ms / 1e3)}
+
+    def mesh():
+        # F1 slice 3, configs[3]: 512^2, 3 objects / 22k triangles (BVH),
+        # 3 x 4 x 512^2 = 3.1M texture parameters, depth 6, 1 FD + 2 prop spp
+        prob = api.MeshTextureProblem(512, 512, 512, max_vertices=6, target_spp=4,
+                                      dtype=torch.float32, ctx=ctx)
+        run = api.MeshTextureRun(prob, optimizer="meta", lr=0.005)
+        ms = timed(run.step, 5)
+        out["mesh_texture_512px_f32"] = {"ms_per_iteration": ms, "iterations_per_s": 1e3 / ms,
+                                         "paths_per_s": prob.draws_per_sample() / (ms / 1e3),
+                                         "texture_params": prob.dim(), **prob.scene.info()}
+        # BVH closest-hit throughput on the same scene (rays aimed at the objects)
+        nr = 1 << 22
+        g = torch.Generator(device="cuda").manual_seed(0)
+        rnd = lambda: torch.rand(nr, device="cuda", generator=g, dtype=torch.float64)  # noqa: E731
+        org = torch.stack([rnd() * 4 - 2, rnd() * 2 + 0.1,
+                           torch.full((nr,), 4.0, device="cuda", dtype=torch.float64)], 1)
+        tgt = torch.stack([rnd() * 3 - 1.5, rnd() * 1.1,
+                           torch.zeros(nr, device="cuda", dtype=torch.float64)], 1)
+        dirs = tgt - org
+        dirs /= torch.linalg.vector_norm(dirs, dim=1, keepdim=True)
+        rays = torch.cat([org, dirs], 1).contiguous()
+        ms = timed(lambda: prob.scene.intersect(rays), 1, warm=1)
+        out["mesh_bvh_closest_hit"] = {"rays": nr, "ms": ms, "rays_per_s": nr / (ms / 1e3)}
+
+    def mesh_large():
+        # F1 slice 4, configs[4]: 1024^2, 16 objects / ~503k triangles,
+        # 16 x 5 x 1024^2 = 83.9M texture parameters (base rgb, roughness,
+        # metalness), depth 8, 1 FD + 4 proportional spp
+        prob = api.MeshLargeProblem(target_spp=2, ctx=ctx)
+        run = api.MeshTextureRun(prob, optimizer="meta", lr=0.005)
+        ms = timed(run.step, 3)
+        out["mesh_large_1024px_f32"] = {"ms_per_iteration": ms, "iterations_per_s": 1e3 / ms,
+                                        "paths_per_s": prob.draws_per_sample() / (ms / 1e3),
+                                        "texture_params": prob.dim(), **prob.scene.info()}
+
+    def runner():
+        # reference harness stand-in for configs[0] (mini-render P=4096,
+        # spp=2, 200 iterations), 148 replicates as one device launch
+        cfg = api.ExperimentConfig(problem="mini-render", pixel_count=4096, spp=2,
+                                   iterations=200, seed=0, problem_seed=1, lr=0.01,
+                                   replicates=148)
+        t0 = time.time()
+        api.run_experiment(cfg, ctx=ctx)
+        wall = time.time() - t0
+        out["minirender_runner"] = {"replicates": 148, "iterations": 200, "wall_s": wall,
+                                    "pairs_per_s": 148 * 200 * 4096 * 2 / wall}
+
+    for name, fn in (("adam", adam), ("minirender_philox", lambda: minirender("philox")),
+                     ("minirender_mt64", lambda: minirender("mt64")), ("quad", quad),
+                     ("helix", helix), ("mesh", mesh), ("mesh_large", mesh_large),
+                     ("runner", runner)):
+        try:
+            fn()
+        except Exception as e:  # recorded, never fatal to the headline line
+            out[f"{name}_error"] = f"{type(e).__name__}: {e}"
+        torch.cuda.empty_cache()
     return out
 
 
