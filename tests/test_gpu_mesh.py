@@ -241,3 +241,49 @@ def test_mesh_fd_sample_is_unbiased(api, channels, nprop):
     z = np.abs(d.mean(0) - (pa.mean(0) - pb.mean(0))) / np.sqrt(vd + vp)
     assert z.max() < 4.0, z
     assert np.all(vd < 0.5 * vp)
+
+
+def test_mesh_abi_rejects_bad_arguments(api):
+    import ctypes as C
+    from paper_2309_15676_b200._lib import InvalidArgument, check, load
+    from paper_2309_15676_b200.api import _p
+    L = load()
+    ctx = api.Context.default()
+    rec, obj, nobj = api.mesh_scene_geometry((6, 8), (8, 10))
+    rp = rec.ctypes.data_as(C.c_void_p)
+    h = C.c_void_p()
+    for bad in ((rec.shape[0], nobj, 4, 3), (0, nobj, 4, 4), (rec.shape[0], 0, 4, 4),
+                (rec.shape[0], nobj, 0, 4)):
+        with pytest.raises(InvalidArgument):
+            check(L.mg_meshscene_create(ctx.h, bad[0], rp, obj.ctypes.data_as(C.c_void_p), bad[1],
+                                        bad[2], bad[3], C.byref(h)))
+    bad_obj = obj.copy()
+    bad_obj[5] = nobj
+    with pytest.raises(InvalidArgument):
+        check(L.mg_meshscene_create(ctx.h, rec.shape[0], rp, bad_obj.ctypes.data_as(C.c_void_p),
+                                    nobj, 4, 4, C.byref(h)))
+    sc = api.MeshScene(rec, obj, nobj, 4, api.mesh_scene_view(max_vertices=4))
+    n = sc.params()
+    th = torch.full((n,), 0.5, dtype=torch.float64, device="cuda")
+    img = torch.zeros(3 * 8 * 8, dtype=torch.float64, device="cuda")
+    acc = torch.zeros(2 * n, dtype=torch.int64, device="cuda")
+    out = torch.empty_like(th)
+    loss = torch.zeros(1, dtype=torch.float64, device="cuda")
+
+    def pair(view, rows=(0, 8), nprop=2):
+        check(L.mg_meshscene_sample_pair(ctx.h, sc.h, 1, 8, 8, view.ctypes.data_as(C.c_void_p),
+                                         _p(img), _p(th), _p(th), 1, 0, rows[0], rows[1], nprop,
+                                         _p(acc), _p(out), _p(out), _p(loss)))
+    for nprop in (1, 9):
+        with pytest.raises(InvalidArgument):
+            pair(sc.view, nprop=nprop)
+    for rows in ((-1, 8), (0, 9), (5, 4)):
+        with pytest.raises(InvalidArgument):
+            pair(sc.view, rows=rows)
+    for maxv in (0, 9):
+        with pytest.raises(InvalidArgument):
+            pair(api.mesh_scene_view(max_vertices=maxv))
+    with pytest.raises(InvalidArgument):
+        sc.render(th, 8, 8, 0, 1)
+    pair(sc.view, rows=(3, 3))          # an empty tile is valid: zero pair, zero loss
+    assert float(loss[0]) == 0.0 and int(torch.count_nonzero(out)) == 0
