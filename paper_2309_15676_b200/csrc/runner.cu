@@ -9,7 +9,10 @@
 // with no host round trip.  Reductions over a replicate's vector (step norm,
 // loss, parameter error) are sequential for dim <= kSeqReduceMax, so in fp64
 // the trajectories are bit-identical to the reference's wherever the
-// transcendental functions agree.
+// transcendental functions agree.  Mini-render runs go
+// through pow, so their parity is tolerance-based anyway; they use the
+// fixed block tree at every size (one sequential thread over 4096 values
+// per sum was the runner's bottleneck for the S1 configuration).
 //
 // Recording keeps the reference's extractor series for one coordinate plus
 // scalars (harness.cpp:204-244), not full vectors (O(iterations * dim)).
@@ -54,9 +57,9 @@ struct RunK {
 // out[0..2], valid in every thread after the call).  Sequential (one thread
 // per sum, index order) for n <= kSeqReduceMax, fixed tree otherwise.
 template <class F>
-__device__ void block_sums3(int n, F f, double* out, double* sw) {
+__device__ void block_sums3(int n, F f, double* out, double* sw, bool seq = true) {
   __shared__ double res[3];
-  if (n <= kSeqReduceMax) {
+  if (seq && n <= kSeqReduceMax) {
     const int t = threadIdx.x;
     if (t == 0 || t == 32 || t == 64) {
       const int which = t / 32;
@@ -134,7 +137,7 @@ __device__ bool sample_pair(const RunK<T>& k, MtBlock& eng, const T* now, const 
     block_sums3(d, [&](int j, int) {
       const double dd = double(now[j]) - double(prev[j]);
       return dd * dd;
-    }, r, sw);
+    }, r, sw, c.problem != MG_MINI_RENDER);
     ssn = r[0];
   }
   return true;
@@ -306,7 +309,7 @@ __global__ void __launch_bounds__(kThreads) run_kernel(RunK<T> k) {
     block_sums3(d, [&](int j, int) {
       const double e = double(params[j]) - k.truth[j];
       return e * e;
-    }, sums, sw);
+    }, sums, sw, c.problem != MG_MINI_RENDER);
     if (threadIdx.x == 0) {
       const size_t at = size_t(r) * iters + i;
       double loss;
@@ -379,7 +382,7 @@ __global__ void __launch_bounds__(kThreads) run_kernel(RunK<T> k) {
   block_sums3(d, [&](int j, int) {
     const double e = double(prev[j]) - k.truth[j];
     return e * e;
-  }, fin, sw);
+  }, fin, sw, c.problem != MG_MINI_RENDER);
   if (threadIdx.x == 0) {
     if (status != 2 && c.converge_threshold > 0.0 && iters_run > 0 &&
         sqrt(fin[0]) < c.converge_threshold)
