@@ -263,18 +263,36 @@ def run_ours(args):
     e2e_steps = args.e2e_steps or max(3, min(args.steps, 10))
     hp = [x.cpu().pin_memory() for x in props[:2]]
     hd = [x.cpu().pin_memory() for x in diffs[:2]]
-    dprop, ddiff = torch.empty_like(pa), torch.empty_like(pa)
+    # double-buffered device inputs: step k+1's H2D copy (copy stream)
+    # overlaps step k's update (compute stream); the copy is PCIe-bound
+    dbuf = [(torch.empty_like(pa), torch.empty_like(pa)) for _ in range(2)]
     host_sc = torch.empty(8, dtype=torch.float64).pin_memory()
+    cstream = torch.cuda.Stream(device=dev)
+    copied = [torch.cuda.Event() for _ in range(2)]
+    consumed = [torch.cuda.Event() for _ in range(2)]
     torch.cuda.synchronize()
     if pg is not None:
         pg.barrier()
     f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+
+    def prefetch(k):
+        with torch.cuda.stream(cstream):
+            if k >= 2:
+                cstream.wait_event(consumed[k % 2])     # buffer free again
+            dbuf[k % 2][0].copy_(hp[k % 2], non_blocking=True)
+            dbuf[k % 2][1].copy_(hd[k % 2], non_blocking=True)
+            copied[k % 2].record(cstream)
+
     f0.record(stream)
+    cstream.wait_event(f0)
+    prefetch(0)
     for k in range(e2e_steps):
-        dprop.copy_(hp[k % 2], non_blocking=True)
-        ddiff.copy_(hd[k % 2], non_blocking=True)
+        if k + 1 < e2e_steps:
+            prefetch(k + 1)
+        stream.wait_event(copied[k % 2])
         src, dst = (pa, pb) if t % 2 == 0 else (pb, pa)
-        upd.step(dprop, ddiff, src, dst)
+        upd.step(dbuf[k % 2][0], dbuf[k % 2][1], src, dst)
+        consumed[k % 2].record(stream)
         if pg is not None:
             pg.all_reduce(sc[:4])
         host_sc.copy_(sc, non_blocking=True)
