@@ -43,8 +43,8 @@ namespace mesh {
 constexpr int kMThreads = 128;
 constexpr int kMaxV = 8;
 constexpr int kRec = 18;
-constexpr int kSmemNodes = 256;  // top BVH levels staged in shared memory (16 KB)
-constexpr int kStackDepth = 48;  // traversal stack per thread, in shared memory
+constexpr int kSmemNodes = 128;  // top BVH4 levels staged in shared memory (16 KB)
+constexpr int kStackDepth = 64;  // traversal stack per thread (local memory)
 constexpr double kTMin = 1e-9, kOff = 1e-6;
 constexpr double kPiM = 3.14159265358979323846;
 constexpr double kFixM = 1099511627776.0;  // 2^40
@@ -101,29 +101,41 @@ __device__ __forceinline__ bool tri_hit(const double* __restrict__ r, const doub
   return true;
 }
 
-// BVH2 node = the boxes of its two children (64 B, four float4):
-//   n0 = c0.lo.xyz c0.hi.x   n1 = c0.hi.yz c1.lo.xy   n2 = c1.lo.z c1.hi.xyz
-//   n3 = (ref0, ref1) as int bits; ref >= 0: internal node, ref < 0: leaf
-//   with triangles [first, first + count), ~ref = first * 8 + count.
-// One 64-byte fetch per traversal step tests both children.
-struct Node4 {
-  float4 a, b, c, d;
+// BVH4 node = the boxes of up to four children in SoA form (128 B, eight
+// float4): lo.x[4] lo.y[4] lo.z[4] hi.x[4] hi.y[4] hi.z[4] ref[4] pad;
+// ref >= 0: internal node, ref < 0: leaf with triangles [first, first +
+// count), ~ref = first * 8 + count; empty slots have an inverted box.
+// One 128-byte fetch per traversal step tests all four children.
+constexpr int kNodeF4 = 8;
+struct NodeW {
+  float4 lx, ly, lz, hx, hy, hz, ref;
 };
 
-__device__ __forceinline__ Node4 load_node(const MeshDev& m, const float4* sn, int i) {
-  Node4 n;
+__device__ __forceinline__ NodeW load_node(const MeshDev& m, const float4* sn, int i) {
+  const float4* src = i < kSmemNodes ? sn + kNodeF4 * i : m.nodes + size_t(kNodeF4) * i;
+  NodeW n;
   if (i < kSmemNodes) {
-    n.a = sn[4 * i];
-    n.b = sn[4 * i + 1];
-    n.c = sn[4 * i + 2];
-    n.d = sn[4 * i + 3];
+    n.lx = src[0];
+    n.ly = src[1];
+    n.lz = src[2];
+    n.hx = src[3];
+    n.hy = src[4];
+    n.hz = src[5];
+    n.ref = src[6];
   } else {
-    n.a = __ldg(&m.nodes[4 * i]);
-    n.b = __ldg(&m.nodes[4 * i + 1]);
-    n.c = __ldg(&m.nodes[4 * i + 2]);
-    n.d = __ldg(&m.nodes[4 * i + 3]);
+    n.lx = __ldg(src);
+    n.ly = __ldg(src + 1);
+    n.lz = __ldg(src + 2);
+    n.hx = __ldg(src + 3);
+    n.hy = __ldg(src + 4);
+    n.hz = __ldg(src + 5);
+    n.ref = __ldg(src + 6);
   }
   return n;
+}
+
+__device__ __forceinline__ float f4c(const float4& v, int c) {
+  return c == 0 ? v.x : (c == 1 ? v.y : (c == 2 ? v.z : v.w));
 }
 
 __device__ __forceinline__ bool slab6(float lx, float ly, float lz, float hx, float hy, float hz,
@@ -190,23 +202,39 @@ __device__ __forceinline__ int trace_impl(const MeshDev& m, const float4* sn, co
         }
       }
     } else {
-      const Node4 n = load_node(m, sn, node);
-      float t0, t1;
-      const bool h0 = slab6(n.a.x, n.a.y, n.a.z, n.a.w, n.b.x, n.b.y, of, inv, bestf, t0);
-      const bool h1 = slab6(n.b.z, n.b.w, n.c.x, n.c.y, n.c.z, n.c.w, of, inv, bestf, t1);
-      const int r0 = __float_as_int(n.d.x), r1 = __float_as_int(n.d.y);
-      if (h0 && h1) {
-        const bool first0 = t0 <= t1;
-        stack[sp++] = first0 ? r1 : r0;
-        node = first0 ? r0 : r1;
-        continue;
+      const NodeW n = load_node(m, sn, node);
+      // (entry distance, child) of the hit children, sorted ascending by a
+      // 4-input sorting network (misses carry +inf)
+      float tk[4];
+      int ck[4];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        float tc;
+        const bool h = slab6(f4c(n.lx, c), f4c(n.ly, c), f4c(n.lz, c), f4c(n.hx, c), f4c(n.hy, c),
+                             f4c(n.hz, c), of, inv, bestf, tc);
+        tk[c] = h ? tc : INFINITY;
+        ck[c] = __float_as_int(f4c(n.ref, c));
       }
-      if (h0) {
-        node = r0;
-        continue;
-      }
-      if (h1) {
-        node = r1;
+      auto cx = [&](int a, int b) {
+        if (tk[b] < tk[a]) {
+          const float tt = tk[a];
+          tk[a] = tk[b];
+          tk[b] = tt;
+          const int cc = ck[a];
+          ck[a] = ck[b];
+          ck[b] = cc;
+        }
+      };
+      cx(0, 1);
+      cx(2, 3);
+      cx(0, 2);
+      cx(1, 3);
+      cx(1, 2);
+      if (tk[0] != INFINITY) {
+        if (tk[3] != INFINITY) stack[sp++] = ck[3];
+        if (tk[2] != INFINITY) stack[sp++] = ck[2];
+        if (tk[1] != INFINITY) stack[sp++] = ck[1];
+        node = ck[0];
         continue;
       }
     }
@@ -319,14 +347,14 @@ __device__ __forceinline__ unsigned long long fixq(double v) {
 
 // adjoint of a stored path, set s, channel weights w (oracle ms_scatter)
 __device__ __forceinline__ void stage_nodes(const MeshDev& m, float4* sn) {
-  const int n = 4 * (m.nnodes < kSmemNodes ? m.nnodes : kSmemNodes);
+  const int n = kNodeF4 * (m.nnodes < kSmemNodes ? m.nnodes : kSmemNodes);
   for (int i = threadIdx.x; i < n; i += blockDim.x) sn[i] = m.nodes[i];
   __syncthreads();
 }
 
 // shared-memory arrays every tracing kernel declares
 #define MESH_SMEM                       \
-  __shared__ float4 sn[4 * kSmemNodes]; \
+  __shared__ float4 sn[kNodeF4 * kSmemNodes]; \
   int* stk = nullptr;                   \
   stage_nodes(m, sn)
 

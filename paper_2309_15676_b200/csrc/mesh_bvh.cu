@@ -185,62 +185,101 @@ int mg_meshscene_create(mg_ctx* ctx, int32_t tri_count, const double* tri, const
   B.nodes.reserve(2 * T);
   B.build(0, tri_count, 0);
   if (B.too_deep) return fail(MG_EINVAL, "mg_meshscene_create: BVH deeper than the traversal stack");
-  // Internal nodes in breadth-first order (the top levels become nodes
-  // [0, kSmemNodes) for the shared-memory stage); each stores its two
-  // children's boxes.  A single-leaf tree gets a root whose second child is
-  // an empty box.
+  // Collapse the binary tree into 4-wide nodes (each BVH2 internal node
+  // that becomes a BVH4 node adopts up to four descendants: repeatedly open
+  // the child with the largest surface area), labelled breadth-first so the
+  // top levels become nodes [0, kSmemNodes) for the shared-memory stage.
   const double diag = sqrt((shi[0] - slo[0]) * (shi[0] - slo[0]) +
                            (shi[1] - slo[1]) * (shi[1] - slo[1]) +
                            (shi[2] - slo[2]) * (shi[2] - slo[2]));
   const float pad = float(1e-5 * diag + 1e-7);
-  std::vector<int> order, label(B.nodes.size(), -1);
-  if (B.nodes[0].left >= 0) {
-    order.push_back(0);
-    label[0] = 0;
-    for (size_t h = 0; h < order.size(); ++h) {
-      const TmpNode& nd = B.nodes[size_t(order[h])];
-      for (int c : {nd.left, nd.right})
-        if (B.nodes[size_t(c)].left >= 0) {
-          label[size_t(c)] = int(order.size());
-          order.push_back(c);
-        }
-    }
-  }
-  auto child_ref = [&](int c) {
+  auto sarea = [&](int c) {
     const TmpNode& nd = B.nodes[size_t(c)];
-    return nd.left >= 0 ? label[size_t(c)] : ~(nd.first * 8 + nd.count);
+    return Builder::area(nd.lo, nd.hi);
   };
-  auto box = [&](int c, float* lo, float* hi) {
-    const TmpNode& nd = B.nodes[size_t(c)];
-    for (int a = 0; a < 3; ++a) {
-      lo[a] = nextafterf(float(nd.lo[a]), -INFINITY) - pad;
-      hi[a] = nextafterf(float(nd.hi[a]), INFINITY) + pad;
+  auto wide_children = [&](int x) {
+    std::vector<int> ch;
+    const TmpNode& nd = B.nodes[size_t(x)];
+    if (nd.left < 0) {  // a single-leaf tree: the root's only child
+      ch.push_back(x);
+      return ch;
     }
+    ch = {nd.left, nd.right};
+    while (ch.size() < 4) {
+      int pick = -1;
+      double best = -1.0;
+      for (size_t k = 0; k < ch.size(); ++k)
+        if (B.nodes[size_t(ch[k])].left >= 0 && sarea(ch[k]) > best) {
+          best = sarea(ch[k]);
+          pick = int(k);
+        }
+      if (pick < 0) break;
+      const TmpNode& o = B.nodes[size_t(ch[size_t(pick)])];
+      ch[size_t(pick)] = o.left;
+      ch.push_back(o.right);
+    }
+    return ch;
+  };
+  std::vector<int> order;                 // BVH2 ids of the BVH4 nodes, BFS
+  std::vector<std::vector<int>> kids;     // their children (BVH2 ids)
+  std::vector<int> level;
+  std::vector<int> label(B.nodes.size(), -1);
+  order.push_back(0);
+  label[0] = 0;
+  level.push_back(0);
+  int depth4 = 0;
+  for (size_t h = 0; h < order.size(); ++h) {
+    kids.push_back(wide_children(order[h]));
+    for (int c : kids.back())
+      if (B.nodes[size_t(c)].left >= 0 && c != order[h]) {
+        label[size_t(c)] = int(order.size());
+        order.push_back(c);
+        level.push_back(level[h] + 1);
+        depth4 = std::max(depth4, level[h] + 1);
+      }
+  }
+  // each step pushes at most 3 children: the stack never exceeds 3 per level
+  if (3 * (depth4 + 1) + 1 > kStackDepth)
+    return fail(MG_EINVAL, "mg_meshscene_create: BVH deeper than the traversal stack");
+  auto child_ref = [&](int c, int parent) {
+    const TmpNode& nd = B.nodes[size_t(c)];
+    return (nd.left >= 0 && c != parent) ? label[size_t(c)] : ~(nd.first * 8 + nd.count);
   };
   auto ibits = [](int v) {
     float f;
     memcpy(&f, &v, 4);
     return f;
   };
-  const int nn = order.empty() ? 1 : int(order.size());
-  std::vector<float4> nodes(4 * size_t(nn));
+  const int nn = int(order.size());
+  std::vector<float4> nodes(size_t(kNodeF4) * size_t(nn));
   for (int i = 0; i < nn; ++i) {
-    float l0[3], h0[3], l1[3] = {1.0f, 1.0f, 1.0f}, h1[3] = {-1.0f, -1.0f, -1.0f};
-    int r0, r1 = ~0;  // empty leaf
-    if (order.empty()) {
-      box(0, l0, h0);
-      r0 = child_ref(0);
-    } else {
-      const TmpNode& nd = B.nodes[size_t(order[size_t(i)])];
-      box(nd.left, l0, h0);
-      box(nd.right, l1, h1);
-      r0 = child_ref(nd.left);
-      r1 = child_ref(nd.right);
+    float lo[3][4], hi[3][4];
+    int ref[4];
+    for (int c = 0; c < 4; ++c) {
+      for (int a = 0; a < 3; ++a) {
+        lo[a][c] = 1.0f;  // empty slot: inverted box
+        hi[a][c] = -1.0f;
+      }
+      ref[c] = ~0;
     }
-    nodes[4 * size_t(i)] = make_float4(l0[0], l0[1], l0[2], h0[0]);
-    nodes[4 * size_t(i) + 1] = make_float4(h0[1], h0[2], l1[0], l1[1]);
-    nodes[4 * size_t(i) + 2] = make_float4(l1[2], h1[0], h1[1], h1[2]);
-    nodes[4 * size_t(i) + 3] = make_float4(ibits(r0), ibits(r1), 0.0f, 0.0f);
+    const std::vector<int>& ch = kids[size_t(i)];
+    for (size_t c = 0; c < ch.size(); ++c) {
+      const TmpNode& nd = B.nodes[size_t(ch[c])];
+      for (int a = 0; a < 3; ++a) {
+        lo[a][c] = nextafterf(float(nd.lo[a]), -INFINITY) - pad;
+        hi[a][c] = nextafterf(float(nd.hi[a]), INFINITY) + pad;
+      }
+      ref[c] = child_ref(ch[c], order[size_t(i)]);
+    }
+    float4* dst = &nodes[size_t(kNodeF4) * size_t(i)];
+    dst[0] = make_float4(lo[0][0], lo[0][1], lo[0][2], lo[0][3]);
+    dst[1] = make_float4(lo[1][0], lo[1][1], lo[1][2], lo[1][3]);
+    dst[2] = make_float4(lo[2][0], lo[2][1], lo[2][2], lo[2][3]);
+    dst[3] = make_float4(hi[0][0], hi[0][1], hi[0][2], hi[0][3]);
+    dst[4] = make_float4(hi[1][0], hi[1][1], hi[1][2], hi[1][3]);
+    dst[5] = make_float4(hi[2][0], hi[2][1], hi[2][2], hi[2][3]);
+    dst[6] = make_float4(ibits(ref[0]), ibits(ref[1]), ibits(ref[2]), ibits(ref[3]));
+    dst[7] = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
   }
   std::vector<double> stri(kRec * T);
   std::vector<int> sorig(T), sobj(T);
@@ -256,7 +295,7 @@ int mg_meshscene_create(mg_ctx* ctx, int32_t tri_count, const double* tri, const
   sc->nch = channels;
   sc->R = tex_res;
   sc->nnodes = nn;
-  sc->depth = B.max_depth;
+  sc->depth = depth4;
   cudaError_t e = cudaMalloc(&sc->tri, sizeof(double) * stri.size());
   if (e == cudaSuccess) e = cudaMalloc(&sc->orig, sizeof(int) * T);
   if (e == cudaSuccess) e = cudaMalloc(&sc->obj, sizeof(int) * T);
