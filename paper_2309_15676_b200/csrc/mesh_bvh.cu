@@ -1,7 +1,8 @@
 // Host side of the mesh renderer: binned-SAH BVH build (16 bins, at most
 // g_bvh_leaf triangles per leaf), breadth-first relabelling of the internal
 // nodes so the top levels form one block every CTA stages in shared memory,
-// 64-byte two-child nodes with fp32 boxes rounded outwards and padded (the
+// 128-byte four-child nodes (the binary tree collapsed by opening the
+// largest child first) with fp32 boxes rounded outwards and padded (the
 // fp32 slab test never culls a triangle the fp64 test would hit); scene
 // create / destroy / info.  DESIGN.md §12.
 #include <algorithm>
