@@ -531,3 +531,48 @@ def test_adam_tma_matches_register_kernel(api, dt):
             L.mg_set_option(b"disable_tma", 0)
     for x, y in zip(*outs):
         assert bits_equal(x, y)
+
+
+def test_fused_meta_update_empty_and_nonfinite(api, oracle):
+    """n = 0 is a no-op; non-finite samples propagate silently like the
+    reference (tests/test_moment2.cpp:125-130) and are counted, the other
+    parameters bit-exact with the oracle."""
+    import ctypes as C
+    from paper_2309_15676_b200 import _lib
+    L = _lib.load()
+    upd = api.FusedMetaUpdate(4, dtype=torch.float64)
+    a = upd.args()
+    e = torch.empty(1, dtype=torch.float64, device="cuda")
+    p = lambda t: C.c_void_p(t.data_ptr())  # noqa: E731
+    x = _abi.MetaExtras(None, None, None, None, None)
+    before = upd.scalars()
+    assert L.mg_meta_update(upd.ctx.h, _abi.MG_F64, 0, C.byref(a), p(e), p(e), p(e), p(e), p(e),
+                            p(e), p(e), p(e), p(e), p(upd.scalars_buf), C.byref(x)) == 0
+    after = upd.scalars()
+    assert (after.ssn, after.diff_count) == (before.ssn, before.diff_count)
+    n = 4096 + 3
+    props, diffs = make_inputs(n, 3, seed=12)
+    props[1][17] = np.nan
+    props[2][2000] = np.inf
+    upd = api.FusedMetaUpdate(n, dtype=torch.float64, lr=0.01)
+    st = oracle_state(n)
+    sc = _abi.fresh_scalars()
+    p_host = np.full(n, 0.5)
+    pa, pb = cu(p_host), torch.empty(n, dtype=torch.float64, device="cuda")
+    beta_pow = 1.0
+    for t in range(3):
+        beta_pow *= 0.9
+        args = _abi.MetaUpdateArgs(meta=_abi.MetaParams(0.01, 1e-8, 1e-30, 1),
+                                   prop_coef=(1 - 0.9) / (1 - beta_pow), beta_delta=0.5,
+                                   first_step=int(t == 0), ssn_from_host=1, ssn_host=sc.ssn)
+        p_host, _, rc = oracle.meta_update(args, st, props[t], diffs[t], p_host, sc)
+        assert rc == 0
+        upd.step(cu(props[t]), cu(diffs[t]), pa, pb, ssn_host=args.ssn_host)
+        pa, pb = pb, pa
+        assert upd.scalars().nonfinite == sc.nonfinite
+    got = host(pa)
+    assert np.isnan(got[17]) and not np.isfinite(got[2000])
+    fin = np.isfinite(p_host)
+    assert np.array_equal(np.isfinite(got), fin)
+    assert bits_equal(got[fin], p_host[fin])
+    assert upd.scalars().nonfinite >= 2
