@@ -149,7 +149,7 @@ __device__ __forceinline__ void bsdf(const T* th, const V3<T>& n, const V3<T>& w
 // entries of d L_c / d theta are exactly zero and are not carried).
 constexpr int kND = 3;
 template <class T, int NSETS>
-__device__ void trace(const HelixK& q, const T* __restrict__ sph, const T (&th)[2][kNP], int px,
+__device__ __noinline__ void trace(const HelixK& q, const T* __restrict__ sph, const T (&th)[2][kNP], int px,
                       int py, uint32_t path, T L[NSETS][3], T dL[NSETS][3][kND]) {
   const uint32_t pix = uint32_t(py * q.W + px);
   double u[4];
@@ -370,24 +370,39 @@ __global__ void __launch_bounds__(kHThreads)
   for (int pix = q.row0 * q.W + blockIdx.x * kHThreads + threadIdx.x; pix < q.row1 * q.W;
        pix += gridDim.x * kHThreads) {
     const int px = pix % q.W, py = pix / q.W;
-    T LA[2][3], dA[2][3][kND], LB[1][3], dB[1][3][kND], LC[2][3], dC[2][3][kND];
-    trace<T, 2>(q, sph, th, px, py, 0u, LA, dA);
-    trace<T, 1>(q, sph, th, px, py, 1u, LB, dB);
+    // B, then A (prop terms accumulated, B's data dropped), then C: fewer
+    // values live across each trace (same arithmetic as before)
+    T LA[2][3], dA[2][3][kND], LC[2][3], dC[2][3][kND];
+    double rA[3], rA1[3];
+    {
+      T LB[1][3], dB[1][3][kND];
+      trace<T, 1>(q, sph, th, px, py, 1u, LB, dB);
+      trace<T, 2>(q, sph, th, px, py, 0u, LA, dA);
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        const double Is = double(target[size_t(c) * npix + pix]);
+        const double rB = double(LB[0][c]) - Is;
+        rA[c] = double(LA[0][c]) - Is;
+        rA1[c] = double(LA[1][c]) - Is;
+        loss += rA[c] * rB;
+#pragma unroll
+        for (int k = 0; k < kND; ++k) {
+          const int j = k == 0 ? c : k + 2;  // base_c, metal (3), rough (4)
+          fp[j] += fixh(rA[c] * double(dB[0][c][k]));
+          fp[j] += fixh(rB * double(dA[0][c][k]));
+        }
+      }
+    }
     trace<T, 2>(q, sph, th, px, py, 2u, LC, dC);
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
       const double Is = double(target[size_t(c) * npix + pix]);
-      const double rA = double(LA[0][c]) - Is, rB = double(LB[0][c]) - Is;
-      const double rC = double(LC[0][c]) - Is;
-      const double rA1 = double(LA[1][c]) - Is, rC1 = double(LC[1][c]) - Is;
-      loss += rA * rB;
+      const double rC = double(LC[0][c]) - Is, rC1 = double(LC[1][c]) - Is;
 #pragma unroll
       for (int k = 0; k < kND; ++k) {
-        const int j = k == 0 ? c : k + 2;  // base_c, metal (3), rough (4)
-        fp[j] += fixh(rA * double(dB[0][c][k]));
-        fp[j] += fixh(rB * double(dA[0][c][k]));
-        fd[j] += fixh((rC * double(dA[0][c][k]) + rA * double(dC[0][c][k])) -
-                      (rC1 * double(dA[1][c][k]) + rA1 * double(dC[1][c][k])));
+        const int j = k == 0 ? c : k + 2;
+        fd[j] += fixh((rC * double(dA[0][c][k]) + rA[c] * double(dC[0][c][k])) -
+                      (rC1 * double(dA[1][c][k]) + rA1[c] * double(dC[1][c][k])));
       }
     }
   }
