@@ -477,6 +477,23 @@ int mg_meshscene_sample_pair(mg_ctx* ctx, mg_mesh_scene* s, int32_t dtype, int32
                              int32_t row0, int32_t row1, int32_t prop_paths, void* accum,
                              void* prop, void* diff, double* loss_out);
 
+/* Tile-sharded sample pair with the reduce-scatter fused into the adjoint
+ * scatter: parameter j's contributions are added (2^-40 fixed-point int64
+ * atomics, order independent) into rank (j / shard)'s accumulator
+ * acc_ptrs[rank] = device int64 [2][shard] (prop | diff), typically peer
+ * pointers of symmetric memory over NVLink.  world * shard must equal the
+ * parameter count.  After all ranks' launches complete (a barrier), each
+ * rank converts its own shard with mg_fixed_finalize. */
+int mg_meshscene_sample_pair_sharded(mg_ctx* ctx, mg_mesh_scene* s, int32_t dtype, int32_t W,
+                                     int32_t H, const double* view, const void* target_img,
+                                     const void* now, const void* prev, uint64_t key,
+                                     uint32_t iteration, int32_t row0, int32_t row1,
+                                     int32_t prop_paths, int32_t world, void* const* acc_ptrs,
+                                     int64_t shard, double* loss_out);
+/* accum (device int64 [2][n], prop | diff in 2^-40 units) -> prop, diff
+ * (dtype [n]); accum left zeroed. */
+int mg_fixed_finalize(mg_ctx* ctx, int32_t dtype, int64_t n, void* accum, void* prop, void* diff);
+
 /* ------------------------------- device-resident run_single (A13, A14) */
 /* Per-replicate record of one coordinate plus scalars (harness.hpp:73-90;
  * full vectors are O(iterations*N) and are not recorded on the device). */

@@ -60,6 +60,7 @@ from .scenes import (  # noqa: F401
     MeshScene,
     MeshTextureProblem,
     large_scene_view,
+    fixed_finalize,
     MeshLargeProblem,
     MeshTextureRun,
 )

@@ -410,10 +410,26 @@ __global__ void __launch_bounds__(kMThreads, 8) wf_shadow_kernel(MeshDev m, WF<T
   }
 }
 
+// Where the fixed-point adjoints go.  One rank: one accumulator [2][np]
+// (prop | diff).  Tile-sharded ranks (configs[3]/[4] over NVLink): parameter
+// j is owned by rank j / shard, whose accumulator [2][shard] is reached
+// through a peer pointer — the scatter IS the reduce-scatter (integer atomics
+// commute, so the owner's sums are independent of the ranks' order).
+constexpr int kMaxRanks = 8;
+struct AccTable {
+  unsigned long long* ptr[kMaxRanks];
+  int shard;  // parameters per rank
+};
+
+__device__ __forceinline__ unsigned long long* acc_slot(const AccTable& a, int j, int which) {
+  const int r = j / a.shard;
+  return a.ptr[r] + size_t(which) * a.shard + (j - r * a.shard);
+}
+
 // adjoint of stored path p (megakernel `scatter` / oracle ms_scatter)
 template <class T, int NCH>
 __device__ __noinline__ void wf_scatter(const WF<T>& w, int p, int s, const T wt[3], int R2,
-                                        unsigned long long* __restrict__ acc) {
+                                        const AccTable& acc, int which) {
   using F = VF<NCH>;
   T Q[3];
 #pragma unroll
@@ -427,12 +443,12 @@ __device__ __noinline__ void wf_scatter(const WF<T>& w, int p, int s, const T wt
         const T A = vf(w, v, F::A + s * 3 + c, p), fb = vf(w, v, F::invfb + s * 3 + c, p);
         const int dn = F::dfn + s * 9 + c * 3, db = F::dfb + s * 9 + c * 3;
         const T gb = wt[c] * (A * vf(w, v, dn, p) + Q[c] * (fb * vf(w, v, db, p)));
-        atomicAdd(&acc[base + c * R2], fixq(double(gb)));
+        atomicAdd(acc_slot(acc, base + c * R2, which), fixq(double(gb)));
         gm += wt[c] * (A * vf(w, v, dn + 1, p) + Q[c] * (fb * vf(w, v, db + 1, p)));
         gr += wt[c] * (A * vf(w, v, dn + 2, p) + Q[c] * (fb * vf(w, v, db + 2, p)));
       }
-      atomicAdd(&acc[base + 3 * R2], fixq(double(gr)));
-      atomicAdd(&acc[base + 4 * R2], fixq(double(gm)));
+      atomicAdd(acc_slot(acc, base + 3 * R2, which), fixq(double(gr)));
+      atomicAdd(acc_slot(acc, base + 4 * R2, which), fixq(double(gm)));
     } else {
       const T dSn = vf(w, v, F::dSn + s, p), dSb = vf(w, v, F::dSb + s, p);
       T gr = T(0);
@@ -440,10 +456,10 @@ __device__ __noinline__ void wf_scatter(const WF<T>& w, int p, int s, const T wt
       for (int c = 0; c < 3; ++c) {
         const T A = vf(w, v, F::A + s * 3 + c, p), ifb = vf(w, v, F::invfb + s * 3 + c, p);
         const T gb = wt[c] * ((A / T(kPiM)) + Q[c] * (ifb / T(kPiM)));
-        atomicAdd(&acc[base + c * R2], fixq(double(gb)));
+        atomicAdd(acc_slot(acc, base + c * R2, which), fixq(double(gb)));
         gr += wt[c] * (A * dSn + Q[c] * (ifb * dSb));
       }
-      atomicAdd(&acc[base + 3 * R2], fixq(double(gr)));
+      atomicAdd(acc_slot(acc, base + 3 * R2, which), fixq(double(gr)));
     }
 #pragma unroll
     for (int c = 0; c < 3; ++c) Q[c] = Q[c] + vf(w, v, F::C + s * 3 + c, p);
@@ -454,8 +470,7 @@ constexpr int kMaxProp = 8;
 
 template <class T, int NCH>
 __global__ void __launch_bounds__(kMThreads)
-    wf_scatter_kernel(MeshK q, WF<T> w, const T* __restrict__ target_img,
-                      unsigned long long* __restrict__ acc, long long np,
+    wf_scatter_kernel(MeshK q, WF<T> w, const T* __restrict__ target_img, AccTable acc,
                       ReducePartials* partials, unsigned int* counter, double* loss_out) {
   const int npix_img = q.W * q.H;
   const int R2 = q.R * q.R;
@@ -490,10 +505,10 @@ __global__ void __launch_bounds__(kMThreads)
         }
         wt[c] = a * scale;
       }
-      wf_scatter<T, NCH>(w, j * w.npix + i, 0, wt, R2, acc);
+      wf_scatter<T, NCH>(w, j * w.npix + i, 0, wt, R2, acc, 0);
     }
-    wf_scatter<T, NCH>(w, i, 0, wC0, R2, acc + np);
-    wf_scatter<T, NCH>(w, i, 1, wC1, R2, acc + np);
+    wf_scatter<T, NCH>(w, i, 0, wC0, R2, acc, 1);
+    wf_scatter<T, NCH>(w, i, 1, wC1, R2, acc, 1);
   }
   Acc a;
   a.ssn = loss;
@@ -517,8 +532,7 @@ __global__ void mesh_finalize_kernel(long long n, unsigned long long* __restrict
 
 template <class T, int NCH>
 int wavefront_pair(mg_ctx* ctx, mg_mesh_scene* s, const MeshK& q, int nprop, const T* target_img,
-                   const T* now, const T* prev, unsigned long long* acc, long long np,
-                   double* loss_out) {
+                   const T* now, const T* prev, const AccTable& acc, double* loss_out) {
   const int npix = q.W * (q.row1 - q.row0);
   if (npix == 0) {
     MG_CUDA_TRY(cudaMemsetAsync(loss_out, 0, sizeof(double), ctx->stream));
@@ -551,9 +565,27 @@ int wavefront_pair(mg_ctx* ctx, mg_mesh_scene* s, const MeshK& q, int nprop, con
     MG_LAUNCH_CHECK(ctx);
   }
   wf_scatter_kernel<T, NCH><<<grid_for(ctx, npix, kMThreads, 8), kMThreads, 0, ctx->stream>>>(
-      q, w, target_img, acc, np, ctx->partials, ctx->counter, loss_out);
+      q, w, target_img, acc, ctx->partials, ctx->counter, loss_out);
   MG_LAUNCH_CHECK(ctx);
   return MG_OK;
+}
+
+int dispatch_wavefront(mg_ctx* ctx, mg_mesh_scene* s, const MeshK& q, int32_t dtype, int nprop,
+                       const void* target_img, const void* now, const void* prev,
+                       const AccTable& tbl, double* loss_out) {
+  if (dtype == MG_F64 && s->nch == 5)
+    return wavefront_pair<double, 5>(ctx, s, q, nprop, (const double*)target_img,
+                                     (const double*)now, (const double*)prev, tbl, loss_out);
+  if (dtype == MG_F64)
+    return wavefront_pair<double, 4>(ctx, s, q, nprop, (const double*)target_img,
+                                     (const double*)now, (const double*)prev, tbl, loss_out);
+  if (dtype == MG_F32 && s->nch == 5)
+    return wavefront_pair<float, 5>(ctx, s, q, nprop, (const float*)target_img,
+                                    (const float*)now, (const float*)prev, tbl, loss_out);
+  if (dtype == MG_F32)
+    return wavefront_pair<float, 4>(ctx, s, q, nprop, (const float*)target_img,
+                                    (const float*)now, (const float*)prev, tbl, loss_out);
+  return fail(MG_EINVAL, "mg_meshscene_sample_pair: unknown dtype");
 }
 
 }  // namespace mesh
@@ -583,24 +615,14 @@ int mg_meshscene_sample_pair(mg_ctx* ctx, mg_mesh_scene* s, int32_t dtype, int32
   q.row1 = row1;
   const long long np = (long long)s->nobj * s->nch * s->R * s->R;
   unsigned long long* acc = (unsigned long long*)accum;
+  AccTable tbl{};
+  tbl.ptr[0] = acc;
+  tbl.shard = int(np);
   // the megakernel implements the configs[3] form (4 channels, 2 proportional paths)
-  if (g_mesh_megakernel && s->nch == 4 && prop_paths == 2) {
+  if (g_mesh_megakernel && s->nch == 4 && prop_paths == 2)
     st = megakernel_pair(ctx, s, q, dtype, target_img, now, prev, acc, np, loss_out);
-  } else if (dtype == MG_F64 && s->nch == 5) {
-    st = wavefront_pair<double, 5>(ctx, s, q, prop_paths, (const double*)target_img,
-                                   (const double*)now, (const double*)prev, acc, np, loss_out);
-  } else if (dtype == MG_F64) {
-    st = wavefront_pair<double, 4>(ctx, s, q, prop_paths, (const double*)target_img,
-                                   (const double*)now, (const double*)prev, acc, np, loss_out);
-  } else if (dtype == MG_F32 && s->nch == 5) {
-    st = wavefront_pair<float, 5>(ctx, s, q, prop_paths, (const float*)target_img,
-                                  (const float*)now, (const float*)prev, acc, np, loss_out);
-  } else if (dtype == MG_F32) {
-    st = wavefront_pair<float, 4>(ctx, s, q, prop_paths, (const float*)target_img,
-                                  (const float*)now, (const float*)prev, acc, np, loss_out);
-  } else {
-    return fail(MG_EINVAL, "mg_meshscene_sample_pair: unknown dtype");
-  }
+  else
+    st = dispatch_wavefront(ctx, s, q, dtype, prop_paths, target_img, now, prev, tbl, loss_out);
   if (st) return st;
   const int fgrid = grid_for(ctx, np, 256, 8);
   if (dtype == MG_F64)
@@ -609,6 +631,63 @@ int mg_meshscene_sample_pair(mg_ctx* ctx, mg_mesh_scene* s, int32_t dtype, int32
   else
     mesh_finalize_kernel<float><<<fgrid, 256, 0, ctx->stream>>>(np, acc, (float*)prop,
                                                                 (float*)diff);
+  MG_LAUNCH_CHECK(ctx);
+  return MG_OK;
+}
+
+// Tile-sharded form (fused scatter + reduce-scatter over peer memory): the
+// partial pair of image rows [row0, row1) is accumulated straight into the
+// owners' accumulators, acc_ptrs[r] = rank r's device int64 [2][shard]
+// (prop | diff; peer pointers, e.g. torch symmetric memory).  No full-length
+// partial buffers, no reduce-scatter launch: after a barrier each rank runs
+// mg_fixed_finalize on its own shard.
+int mg_meshscene_sample_pair_sharded(mg_ctx* ctx, mg_mesh_scene* s, int32_t dtype, int32_t W,
+                                     int32_t H, const double* view, const void* target_img,
+                                     const void* now, const void* prev, uint64_t key,
+                                     uint32_t iteration, int32_t row0, int32_t row1,
+                                     int32_t prop_paths, int32_t world, void* const* acc_ptrs,
+                                     int64_t shard, double* loss_out) {
+  if (!ctx || !s || !target_img || !now || !prev || !acc_ptrs || !loss_out)
+    return fail(MG_EINVAL, "mg_meshscene_sample_pair_sharded: null argument");
+  if (prop_paths < 2 || prop_paths > kMaxProp)
+    return fail(MG_EINVAL, "mg_meshscene_sample_pair_sharded: prop_paths must lie in [2, 8]");
+  if (W < 1 || H < 1 || row0 < 0 || row1 > H || row0 > row1)
+    return fail(MG_EINVAL, "mg_meshscene_sample_pair_sharded: bad sizes or rows");
+  const long long np = (long long)s->nobj * s->nch * s->R * s->R;
+  if (world < 1 || world > kMaxRanks || shard < 1 || shard * world != np)
+    return fail(MG_EINVAL, "mg_meshscene_sample_pair_sharded: world * shard must equal the "
+                           "parameter count (1 <= world <= 8)");
+  int st = check_view(view);
+  if (st) return st;
+  MeshK q = make_k(s, W, H, view, key, iteration);
+  q.row0 = row0;
+  q.row1 = row1;
+  AccTable tbl{};
+  for (int r = 0; r < world; ++r) {
+    if (!acc_ptrs[r]) return fail(MG_EINVAL, "mg_meshscene_sample_pair_sharded: null accumulator");
+    tbl.ptr[r] = static_cast<unsigned long long*>(acc_ptrs[r]);
+  }
+  tbl.shard = int(shard);
+  return dispatch_wavefront(ctx, s, q, dtype, prop_paths, target_img, now, prev, tbl, loss_out);
+}
+
+// Converts one rank's fixed-point accumulator [2][n] into prop / diff (dtype)
+// and zeroes it.
+int mg_fixed_finalize(mg_ctx* ctx, int32_t dtype, int64_t n, void* accum, void* prop,
+                      void* diff) {
+  if (!ctx || (n > 0 && (!accum || !prop || !diff)))
+    return fail(MG_EINVAL, "mg_fixed_finalize: null argument");
+  if (n <= 0) return MG_OK;
+  const int fgrid = grid_for(ctx, n, 256, 8);
+  unsigned long long* acc = static_cast<unsigned long long*>(accum);
+  if (dtype == MG_F64)
+    mesh_finalize_kernel<double><<<fgrid, 256, 0, ctx->stream>>>(n, acc, (double*)prop,
+                                                                 (double*)diff);
+  else if (dtype == MG_F32)
+    mesh_finalize_kernel<float><<<fgrid, 256, 0, ctx->stream>>>(n, acc, (float*)prop,
+                                                                (float*)diff);
+  else
+    return fail(MG_EINVAL, "mg_fixed_finalize: unknown dtype");
   MG_LAUNCH_CHECK(ctx);
   return MG_OK;
 }

@@ -235,3 +235,68 @@ class SharedParamStepP2P:
             self.dist.all_reduce(self.scalars_buf[:4], op=self.dist.ReduceOp.SUM, group=self.group)
         self.params, self.params_next = self.params_next, self.params
         self.h_params, self.h_next = self.h_next, self.h_params
+
+
+class TiledRenderStepP2P:
+    """One iteration of a tile-sharded shared-parameter renderer
+    (configs[3]/[4] over NVLink) with the reduce-scatter FUSED into the
+    adjoint scatter: every rank renders its image rows (tile_rows) and adds
+    each parameter's fixed-point contribution straight into the owning
+    rank's accumulator shard through symmetric-memory peer pointers
+    (mg_meshscene_sample_pair_sharded) — no full-length partial buffers, no
+    reduce-scatter launch.  After a barrier each rank converts its own shard
+    (mg_fixed_finalize), runs the fused meta update on it, and the new
+    parameters are all-gathered (NCCL); the 4 update scalars are
+    all-reduced.  Integer atomics commute, so the result is bit-identical to
+    the single-process run for any number of ranks.
+
+    problem: a MeshTextureProblem (identical on every rank)."""
+
+    def __init__(self, problem, lr: float = 0.01, group=None, seed: int = 0, replicate: int = 0):
+        import torch
+        import torch.distributed as dist
+        import torch.distributed._symmetric_memory as symm_mem
+
+        from .api import FusedMetaUpdate, load
+        self.torch, self.dist = torch, dist
+        self.p = problem
+        self.group = group or dist.group.WORLD
+        self.world = dist.get_world_size(self.group)
+        self.rank = dist.get_rank(self.group)
+        n = problem.dim()
+        if n % self.world:
+            raise ValueError("parameter count must divide evenly across ranks")
+        self.n, self.S = n, n // self.world
+        dev = torch.device("cuda", torch.cuda.current_device())
+        self.acc = symm_mem.empty(2 * self.S, dtype=torch.int64, device=dev)
+        self.acc.zero_()
+        self.h = symm_mem.rendezvous(self.acc, self.group)
+        self.upd = FusedMetaUpdate(self.S, dtype=problem.dtype, lr=lr, project_lo=0.0,
+                                   project_hi=1.0, ctx=problem.ctx)
+        self.params = problem.initial_params()
+        self.prev = self.params.clone()
+        self.prop = torch.empty(self.S, dtype=problem.dtype, device=dev)
+        self.diff = torch.empty_like(self.prop)
+        self.key = int(load().mg_stream_seed(seed, replicate))
+        self.t = 0
+
+    def step(self):
+        torch, dist = self.torch, self.dist
+        from .api import fixed_finalize
+        lo = self.rank * self.S
+        self.h.barrier()                 # owners' accumulators are zero again
+        self.p.sample_pair_sharded(self.params, self.prev, self.t, self.key,
+                                   tile_rows(self.p.H, self.rank, self.world),
+                                   self.h.buffer_ptrs, self.S)
+        self.h.barrier()                 # every rank's atomics have landed
+        fixed_finalize(self.acc, self.prop, self.diff, self.p.ctx)
+        shard_new = torch.empty(self.S, dtype=self.p.dtype, device=self.prop.device)
+        self.upd.step(self.prop, self.diff, self.params[lo:lo + self.S].contiguous(), shard_new)
+        new = torch.empty_like(self.params)
+        if self.world > 1:
+            dist.all_reduce(self.upd.scalars_buf[:4], op=dist.ReduceOp.SUM, group=self.group)
+            dist.all_gather_into_tensor(new, shard_new, group=self.group)
+        else:
+            new.copy_(shard_new)
+        self.prev, self.params = self.params, new
+        self.t += 1

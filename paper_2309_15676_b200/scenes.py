@@ -437,6 +437,28 @@ class MeshTextureProblem:
         return GradientSamplePair(prop, diff)
 
 
+    def sample_pair_sharded(self, now, prev, iteration: int, key: int, rows, acc_ptrs,
+                            shard: int):
+        """Rows `rows` of the image, contributions atomically added into the
+        owning ranks' fixed-point accumulators (acc_ptrs[r]: device int64
+        [2][shard], e.g. symmetric-memory peer pointers): the adjoint
+        scatter and the reduce-scatter of a tile-sharded step in one kernel
+        (mg_meshscene_sample_pair_sharded).  Loss of the rows -> loss_buf."""
+        ptrs = (C.c_void_p * len(acc_ptrs))(*[int(x) for x in acc_ptrs])
+        check(load().mg_meshscene_sample_pair_sharded(
+            self.ctx.h, self.scene.h, _dtype_code(now), self.W, self.H,
+            self.scene.view.ctypes.data_as(C.c_void_p), _p(self.target_img), _p(now.contiguous()),
+            _p(prev.contiguous()), key, iteration, rows[0], rows[1], self.prop_paths,
+            len(acc_ptrs), ptrs, shard, _p(self.loss_buf)))
+
+
+def fixed_finalize(accum, prop, diff, ctx=None):
+    """accum (int64 [2][n], 2^-40 units) -> prop, diff; accum zeroed."""
+    ctx = ctx or Context.default()
+    check(load().mg_fixed_finalize(ctx.h, _dtype_code(prop), prop.numel(), _p(accum), _p(prop),
+                                   _p(diff)))
+
+
 def large_scene_view(max_vertices: int = 8):
     """configs[4] camera/light over the 5 x 3 grid of objects."""
     return mesh_scene_view(max_vertices, light=(8.0, 8.0, 8.0), cam=(0.0, 2.8, 4.4),
