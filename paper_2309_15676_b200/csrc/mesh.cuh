@@ -22,6 +22,7 @@
 struct mg_mesh_scene {
   int T = 0, nobj = 0, R = 0, nnodes = 0, depth = 0, nch = 4;
   double* tri = nullptr;   // [T][18] in BVH order
+  float4* tri32 = nullptr; // [T][3] fp32 v0 e1 e2 (fp32-mode traversal), BVH order
   int* orig = nullptr;     // [T] original triangle index
   int* obj = nullptr;      // [T] object id (BVH order)
   float4* nodes = nullptr; // [2 * nnodes]: (lo.xyz, a) (hi.xyz, b)
@@ -52,6 +53,7 @@ constexpr double kFixM = 1099511627776.0;  // 2^40
 // ------------------------------------------------------------ device
 struct MeshDev {
   const double* __restrict__ tri;
+  const float4* __restrict__ tri32;  // [T][3]: v0, e1, e2 in fp32 (fast-mode traversal)
   const int* __restrict__ orig;
   const int* __restrict__ obj;
   const float4* __restrict__ nodes;
@@ -257,6 +259,133 @@ __device__ __noinline__ int trace(const MeshDev& m, const float4* sn, int* stk, 
   return trace_impl<ANY>(m, sn, o, d, tmax, t_out, u_out, v_out);
 }
 
+// fp32 fast mode: the same traversal with the triangle test in fp32 on fp32
+// copies of the records (half the bytes, twice the arithmetic rate).  Paths
+// may then branch differently from the fp64 parity mode; the fraction of
+// affected pixels is measured (tests/test_gpu_mesh.py) and reported.
+constexpr float kTMin32 = 1e-5f;
+
+__device__ __forceinline__ bool tri_hit32(const float4* __restrict__ r, const float o[3],
+                                          const float d[3], float& t, float& u, float& v) {
+  const float4 a = __ldg(r), b = __ldg(r + 1), c = __ldg(r + 2);
+  const float v0[3] = {a.x, a.y, a.z}, e1[3] = {a.w, b.x, b.y}, e2[3] = {b.z, b.w, c.x};
+  const float p[3] = {d[1] * e2[2] - d[2] * e2[1], d[2] * e2[0] - d[0] * e2[2],
+                      d[0] * e2[1] - d[1] * e2[0]};
+  const float det = (e1[0] * p[0] + e1[1] * p[1]) + e1[2] * p[2];
+  if (det == 0.0f) return false;
+  const float inv = 1.0f / det;
+  const float s[3] = {o[0] - v0[0], o[1] - v0[1], o[2] - v0[2]};
+  const float uu = ((s[0] * p[0] + s[1] * p[1]) + s[2] * p[2]) * inv;
+  if (uu < 0.0f || uu > 1.0f) return false;
+  const float q[3] = {s[1] * e1[2] - s[2] * e1[1], s[2] * e1[0] - s[0] * e1[2],
+                      s[0] * e1[1] - s[1] * e1[0]};
+  const float vv = ((d[0] * q[0] + d[1] * q[1]) + d[2] * q[2]) * inv;
+  if (vv < 0.0f || uu + vv > 1.0f) return false;
+  const float tt = ((e2[0] * q[0] + e2[1] * q[1]) + e2[2] * q[2]) * inv;
+  if (!(tt > kTMin32)) return false;
+  t = tt;
+  u = uu;
+  v = vv;
+  return true;
+}
+
+template <bool ANY>
+__device__ __forceinline__ int trace32_impl(const MeshDev& m, const float4* sn, const double o[3],
+                                            const double d[3], double tmax, double& t_out,
+                                            double& u_out, double& v_out) {
+  float of[3], df[3], inv[3];
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    of[k] = float(o[k]);
+    df[k] = float(d[k]);
+    inv[k] = 1.0f / (fabsf(df[k]) > 1e-20f ? df[k] : copysignf(1e-20f, df[k]));
+  }
+  int stack[kStackDepth];
+  int sp = 0, node = 0;
+  const float tmaxf = float(tmax);
+  float best = tmaxf, bu = 0.0f, bv = 0.0f;
+  int bslot = -1, bid = INT_MAX;
+  for (;;) {
+    if (node < 0) {
+      const int first = (~node) >> 3, count = (~node) & 7;
+      for (int sidx = first; sidx < first + count; ++sidx) {
+        float t, u, v;
+        if (!tri_hit32(m.tri32 + 3 * size_t(sidx), of, df, t, u, v) || !(t <= best)) continue;
+        if (ANY) {
+          if (t < tmaxf) return sidx;
+          continue;
+        }
+        const int id = __ldg(&m.orig[sidx]);
+        if (t < best || id < bid) {
+          best = t;
+          bu = u;
+          bv = v;
+          bslot = sidx;
+          bid = id;
+        }
+      }
+    } else {
+      const NodeW n = load_node(m, sn, node);
+      float tk[4];
+      int ck[4];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        float tc;
+        const bool h = slab6(f4c(n.lx, c), f4c(n.ly, c), f4c(n.lz, c), f4c(n.hx, c), f4c(n.hy, c),
+                             f4c(n.hz, c), of, inv, best, tc);
+        tk[c] = h ? tc : INFINITY;
+        ck[c] = __float_as_int(f4c(n.ref, c));
+      }
+      auto cx = [&](int a, int b) {
+        if (tk[b] < tk[a]) {
+          const float tt = tk[a];
+          tk[a] = tk[b];
+          tk[b] = tt;
+          const int cc = ck[a];
+          ck[a] = ck[b];
+          ck[b] = cc;
+        }
+      };
+      cx(0, 1);
+      cx(2, 3);
+      cx(0, 2);
+      cx(1, 3);
+      cx(1, 2);
+      if (tk[0] != INFINITY) {
+        if (tk[3] != INFINITY) stack[sp++] = ck[3];
+        if (tk[2] != INFINITY) stack[sp++] = ck[2];
+        if (tk[1] != INFINITY) stack[sp++] = ck[1];
+        node = ck[0];
+        continue;
+      }
+    }
+    if (sp == 0) break;
+    node = stack[--sp];
+  }
+  t_out = bslot < 0 ? INFINITY : double(best);
+  u_out = double(bu);
+  v_out = double(bv);
+  return bslot;
+}
+
+// traversal in the precision of the mode: fp64 (parity) or fp32 (fast)
+template <bool ANY, class T>
+__device__ __forceinline__ int trace_mode(const MeshDev& m, const float4* sn, const double o[3],
+                                          const double d[3], double tmax, double& t_out,
+                                          double& u_out, double& v_out) {
+  if constexpr (sizeof(T) == 4)
+    return trace32_impl<ANY>(m, sn, o, d, tmax, t_out, u_out, v_out);
+  else
+    return trace_impl<ANY>(m, sn, o, d, tmax, t_out, u_out, v_out);
+}
+
+template <bool ANY, class T>
+__device__ __noinline__ int trace_t(const MeshDev& m, const float4* sn, const double o[3],
+                                    const double d[3], double tmax, double& t_out, double& u_out,
+                                    double& v_out) {
+  return trace_mode<ANY, T>(m, sn, o, d, tmax, t_out, u_out, v_out);
+}
+
 __device__ __forceinline__ void prng(uint64_t key, uint32_t pix, uint32_t it, uint32_t path,
                                      uint32_t slot, double u[4]) {
   const Philox4 r =
@@ -362,6 +491,7 @@ __device__ __forceinline__ void stage_nodes(const MeshDev& m, float4* sn) {
 inline MeshDev dev_of(const mg_mesh_scene* s) {
   MeshDev m;
   m.tri = s->tri;
+  m.tri32 = s->tri32;
   m.orig = s->orig;
   m.obj = s->obj;
   m.nodes = s->nodes;

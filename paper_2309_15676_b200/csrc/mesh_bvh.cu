@@ -284,11 +284,16 @@ int mg_meshscene_create(mg_ctx* ctx, int32_t tri_count, const double* tri, const
   }
   std::vector<double> stri(kRec * T);
   std::vector<int> sorig(T), sobj(T);
+  std::vector<float4> stri32(3 * T);
   for (size_t s = 0; s < T; ++s) {
     const int k = B.idx[s];
     memcpy(&stri[kRec * s], tri + kRec * size_t(k), sizeof(double) * kRec);
     sorig[s] = k;
     sobj[s] = obj[k];
+    const double* r = tri + kRec * size_t(k);
+    stri32[3 * s] = make_float4(float(r[0]), float(r[1]), float(r[2]), float(r[3]));
+    stri32[3 * s + 1] = make_float4(float(r[4]), float(r[5]), float(r[6]), float(r[7]));
+    stri32[3 * s + 2] = make_float4(float(r[8]), 0.0f, 0.0f, 0.0f);
   }
   mg_mesh_scene* sc = new mg_mesh_scene();
   sc->T = tri_count;
@@ -298,6 +303,9 @@ int mg_meshscene_create(mg_ctx* ctx, int32_t tri_count, const double* tri, const
   sc->nnodes = nn;
   sc->depth = depth4;
   cudaError_t e = cudaMalloc(&sc->tri, sizeof(double) * stri.size());
+  if (e == cudaSuccess) e = cudaMalloc(&sc->tri32, sizeof(float4) * stri32.size());
+  if (e == cudaSuccess)
+    e = cudaMemcpy(sc->tri32, stri32.data(), sizeof(float4) * stri32.size(), cudaMemcpyHostToDevice);
   if (e == cudaSuccess) e = cudaMalloc(&sc->orig, sizeof(int) * T);
   if (e == cudaSuccess) e = cudaMalloc(&sc->obj, sizeof(int) * T);
   if (e == cudaSuccess) e = cudaMalloc(&sc->nodes, sizeof(float4) * nodes.size());
@@ -310,6 +318,7 @@ int mg_meshscene_create(mg_ctx* ctx, int32_t tri_count, const double* tri, const
     e = cudaMemcpy(sc->nodes, nodes.data(), sizeof(float4) * nodes.size(), cudaMemcpyHostToDevice);
   if (e != cudaSuccess) {
     cudaFree(sc->tri);
+    cudaFree(sc->tri32);
     cudaFree(sc->orig);
     cudaFree(sc->obj);
     cudaFree(sc->nodes);
@@ -324,6 +333,7 @@ int mg_meshscene_create(mg_ctx* ctx, int32_t tri_count, const double* tri, const
 int mg_meshscene_destroy(mg_mesh_scene* s) {
   if (!s) return MG_OK;
   cudaFree(s->tri);
+  cudaFree(s->tri32);
   cudaFree(s->orig);
   cudaFree(s->obj);
   cudaFree(s->nodes);

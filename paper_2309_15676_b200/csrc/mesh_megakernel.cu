@@ -62,7 +62,7 @@ __device__ __noinline__ int mesh_path(const MeshK& q, const MeshDev& m, const fl
   int nv = 0;
   for (int v = 0; v < maxv && v < kMaxV; ++v) {
     double t = INFINITY, bu, bv;
-    const int slot = trace<false>(m, sn, stk, o, d, INFINITY, t, bu, bv);
+    const int slot = trace_t<false, T>(m, sn, o, d, INFINITY, t, bu, bv);
     if (slot < 0) {
 #pragma unroll
       for (int s = 0; s < NS; ++s)
@@ -126,7 +126,7 @@ __device__ __noinline__ int mesh_path(const MeshK& q, const MeshDev& m, const fl
     const T nT[3] = {T(n[0]), T(n[1]), T(n[2])}, woT[3] = {T(wo[0]), T(wo[1]), T(wo[2])};
     if (cx > 0.0 && cl > 0.0 && dot3d(n, wo) > 0.0) {
       double ts, tu, tv;
-      if (trace<true>(m, sn, stk, xo, w, wl - kOff, ts, tu, tv) < 0) {
+      if (trace_t<true, T>(m, sn, xo, w, wl - kOff, ts, tu, tv) < 0) {
         const double gl = ((cx * cl) / d2) * la;
         const T wT[3] = {T(w[0]), T(w[1]), T(w[2])};
 #pragma unroll

@@ -143,7 +143,7 @@ __global__ void __launch_bounds__(kMThreads, 8) wf_isect_kernel(MeshDev m, WF<T>
     const int p = qin[i];
     const double o[3] = {w.ox[p], w.oy[p], w.oz[p]}, d[3] = {w.dx[p], w.dy[p], w.dz[p]};
     double t = INFINITY, bu = 0.0, bv = 0.0;
-    const int slot = trace_impl<false>(m, sn, o, d, INFINITY, t, bu, bv);
+    const int slot = trace_mode<false, T>(m, sn, o, d, INFINITY, t, bu, bv);
     w.hslot[p] = slot;
     w.ht[p] = t;
     w.hu[p] = bu;
@@ -390,7 +390,7 @@ __global__ void __launch_bounds__(kMThreads, 8) wf_shadow_kernel(MeshDev m, WF<T
     const int p = w.sq[i];
     const double o[3] = {w.sox[p], w.soy[p], w.soz[p]}, d[3] = {w.sdx[p], w.sdy[p], w.sdz[p]};
     double ts, tu, tv;
-    if (trace_impl<true>(m, sn, o, d, w.stm[p], ts, tu, tv) < 0) {
+    if (trace_mode<true, T>(m, sn, o, d, w.stm[p], ts, tu, tv) < 0) {
       const int k = p / w.npix;
       const int nj = (k == 0 || k == w.nprop) ? 6 : 3;
       for (int j = 0; j < nj; ++j) w.L[size_t(j) * w.P + p] += w.pendC[size_t(j) * w.P + p];
