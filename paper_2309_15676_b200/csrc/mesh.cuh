@@ -165,8 +165,8 @@ __device__ __forceinline__ bool tri_hit_rec(const double* __restrict__ rec, cons
 // ANY: any hit with t < tmax (shadow rays).  Otherwise the closest hit with
 // t < tmax; ties on t resolve to the lower original triangle index, so the
 // answer is the oracle's brute-force scan.  Returns the BVH slot or -1.
-// (stk: reserved for a shared-memory stack; the local-memory stack measured
-// faster — the shared one cut occupancy.)
+// The traversal stack is a per-thread local array (a shared-memory stack
+// measured slower: it cut occupancy).
 template <bool ANY>
 __device__ __forceinline__ int trace_impl(const MeshDev& m, const float4* sn, const double o[3],
                                           const double d[3], double tmax, double& t_out,
@@ -253,7 +253,7 @@ __device__ __forceinline__ int trace_impl(const MeshDev& m, const float4* sn, co
 // sites keeps its instruction footprint small); the wavefront kernels
 // inline trace_impl at their single call site.
 template <bool ANY>
-__device__ __noinline__ int trace(const MeshDev& m, const float4* sn, int* stk, const double o[3],
+__device__ __noinline__ int trace(const MeshDev& m, const float4* sn, const double o[3],
                                   const double d[3], double tmax, double& t_out, double& u_out,
                                   double& v_out) {
   return trace_impl<ANY>(m, sn, o, d, tmax, t_out, u_out, v_out);
@@ -484,7 +484,6 @@ __device__ __forceinline__ void stage_nodes(const MeshDev& m, float4* sn) {
 // shared-memory arrays every tracing kernel declares
 #define MESH_SMEM                       \
   __shared__ float4 sn[kNodeF4 * kSmemNodes]; \
-  int* stk = nullptr;                   \
   stage_nodes(m, sn)
 
 

@@ -28,7 +28,7 @@ struct NoStore {};
 // radiance L[s][c], environment after the last vertex E[s][c]; per-vertex
 // adjoint data into *st when STORE.  Returns the number of vertices.
 template <class T, int NS, bool STORE, class Store, int NCH = 4>
-__device__ __noinline__ int mesh_path(const MeshK& q, const MeshDev& m, const float4* sn, int* stk,
+__device__ __noinline__ int mesh_path(const MeshK& q, const MeshDev& m, const float4* sn,
                                      const T* const th[2],
                          int px, int py, uint32_t it, uint32_t path, T L[NS][3], T E[NS][3],
                          Store* st) {
@@ -244,7 +244,7 @@ __global__ void __launch_bounds__(kMThreads)
     double acc[3] = {0.0, 0.0, 0.0};
     for (int s = 0; s < spp; ++s) {
       T L[1][3], E[1][3];
-      mesh_path<T, 1, false, NoStore, NCH>(q, m, sn, stk, th, px, py, 0xffffffffu, uint32_t(s),
+      mesh_path<T, 1, false, NoStore, NCH>(q, m, sn, th, px, py, 0xffffffffu, uint32_t(s),
                                            L, E, nullptr);
 #pragma unroll
       for (int c = 0; c < 3; ++c) acc[c] += double(L[0][c]);
@@ -280,13 +280,13 @@ __global__ void __launch_bounds__(kMThreads)
     if (pix >= pix1) continue;
     const int px = pix % q.W, py = pix / q.W;
     T LB[1][3], EB[1][3], LC[2][3], EC[2][3], LA[2][3], EA[2][3];
-    mesh_path<T, 1, false, NoStore>(q, m, sn, stk, th, px, py, q.iteration, 1u, LB, EB, nullptr);
-    mesh_path<T, 2, false, NoStore>(q, m, sn, stk, th, px, py, q.iteration, 2u, LC, EC, nullptr);
+    mesh_path<T, 1, false, NoStore>(q, m, sn, th, px, py, q.iteration, 1u, LB, EB, nullptr);
+    mesh_path<T, 2, false, NoStore>(q, m, sn, th, px, py, q.iteration, 2u, LC, EC, nullptr);
     T rA[3], rB[3], wC0[3], wC1[3];
     {
       PathStore<T, 2> st;
       const int na =
-          mesh_path<T, 2, true>(q, m, sn, stk, th, px, py, q.iteration, 0u, LA, EA, &st);
+          mesh_path<T, 2, true>(q, m, sn, th, px, py, q.iteration, 0u, LA, EA, &st);
 #pragma unroll
       for (int c = 0; c < 3; ++c) {
         const T Is = target_img[size_t(c) * npix + pix];
@@ -303,7 +303,7 @@ __global__ void __launch_bounds__(kMThreads)
     {
       PathStore<T, 1> st;
       const int nb =
-          mesh_path<T, 1, true>(q, m, sn, stk, th, px, py, q.iteration, 1u, LB, EB, &st);
+          mesh_path<T, 1, true>(q, m, sn, th, px, py, q.iteration, 1u, LB, EB, &st);
       scatter<T, 1>(st, nb, EB[0], 0, rA, R2, acc);
     }
   }
@@ -320,7 +320,7 @@ __global__ void mesh_intersect_kernel(MeshDev m, int n, const double* __restrict
     const double o[3] = {rays[6 * i], rays[6 * i + 1], rays[6 * i + 2]};
     const double d[3] = {rays[6 * i + 3], rays[6 * i + 4], rays[6 * i + 5]};
     double t = INFINITY, u, v;
-    const int s = trace<false>(m, sn, stk, o, d, INFINITY, t, u, v);
+    const int s = trace<false>(m, sn, o, d, INFINITY, t, u, v);
     t_out[i] = s < 0 ? INFINITY : t;
     tri_out[i] = s < 0 ? -1 : m.orig[s];
   }
