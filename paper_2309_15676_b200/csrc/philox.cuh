@@ -26,7 +26,9 @@ __host__ __device__ __forceinline__ void philox_mulhilo(uint32_t a, uint32_t b, 
 __host__ __device__ __forceinline__ Philox4 philox4x32_10(Philox4 c, uint32_t k0, uint32_t k1) {
   constexpr uint32_t M0 = 0xD2511F53u, M1 = 0xCD9E8D57u;
   constexpr uint32_t W0 = 0x9E3779B9u, W1 = 0xBB67AE85u;
+#ifdef __CUDA_ARCH__
 #pragma unroll
+#endif
   for (int r = 0; r < 10; ++r) {
     uint32_t hi0, lo0, hi1, lo1;
     philox_mulhilo(M0, c.x[0], hi0, lo0);
