@@ -217,17 +217,16 @@ def _sphere_triangles(center, radius_fn, n_theta: int, n_phi: int):
     pos = np.stack([center[0] + rad * np.sin(T_) * np.cos(P_), center[1] + rad * np.cos(T_),
                     center[2] + rad * np.sin(T_) * np.sin(P_)], axis=-1)
     uv = np.stack([P_ / (2.0 * np.pi), T_ / np.pi], axis=-1)
-    tris = []
-    for i in range(n_theta):
-        for j in range(n_phi):
-            a, b, c, d = (i, j), (i, j + 1), (i + 1, j), (i + 1, j + 1)
-            if i != 0:
-                tris.append((a, b, d))
-            if i != n_theta - 1:
-                tris.append((a, d, c))
-    v = np.array([[pos[k] for k in t] for t in tris])
-    w = np.array([[uv[k] for k in t] for t in tris])
-    return v, w
+    # per grid cell (row-major): (a, b, d) unless in the first row, then
+    # (a, d, c) unless in the last row; a = (i, j), b = (i, j+1),
+    # c = (i+1, j), d = (i+1, j+1)
+    I, J = np.meshgrid(np.arange(n_theta), np.arange(n_phi), indexing="ij")
+    I, J = I.reshape(-1), J.reshape(-1)
+    ti = np.stack([np.stack([I, I, I + 1], 1), np.stack([I, I + 1, I + 1], 1)], 1)
+    tj = np.stack([np.stack([J, J + 1, J + 1], 1), np.stack([J, J + 1, J], 1)], 1)
+    keep = np.stack([I != 0, I != n_theta - 1], 1).reshape(-1)
+    ti, tj = ti.reshape(-1, 3)[keep], tj.reshape(-1, 3)[keep]
+    return pos[ti, tj], uv[ti, tj]
 
 
 def mesh_scene_geometry(sphere_res=(24, 48), displaced_res=(100, 100), seed: int = 3,
