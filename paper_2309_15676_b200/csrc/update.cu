@@ -74,13 +74,13 @@ __global__ void __launch_bounds__(kThreads)
         meta_elem<T, FIRST>(k, s, P.v[w], D.v[w], VP.v[w], VD.v[w], M2P.v[w], M2D.v[w], ME.v[w],
                             VA.v[w], AP.v[w], PI.v[w], PP.v[w], TG.v[w], has_target, PO.v[w],
                             DL.v[w], acc);
-      st_plain(q.m2p + b, M2P);
-      if (s.active) st_plain(q.m2d + b, M2D);
-      st_plain(q.mean + b, ME);
-      st_plain(q.var + b, VA);
-      st_plain(q.ap + b, AP);
-      st_plain(q.pout + b, PO);
-      if (q.delta) st_plain(q.delta + b, DL);
+      st_stream(q.m2p + b, M2P);
+      if (s.active) st_stream(q.m2d + b, M2D);
+      st_stream(q.mean + b, ME);
+      st_stream(q.var + b, VA);
+      st_stream(q.ap + b, AP);
+      st_stream(q.pout + b, PO);
+      if (q.delta) st_stream(q.delta + b, DL);
     }
   }
   // scalar path: everything (unaligned) or the tail (aligned)
@@ -218,13 +218,15 @@ __global__ void __launch_bounds__(kTmaThreads, kMinBlocks)
                           VA.v[w], AP.v[w], PI.v[w], T(0), TG.v[w], has_target, PO.v[w], DL.v[w],
                           acc);
     const int64_t b = (int64_t(blockIdx.x) + li * gridDim.x) * TILE + e;
-    st_plain(q.m2p + b, M2P);
-    if (s.active) st_plain(q.m2d + b, M2D);
-    st_plain(q.mean + b, ME);
-    st_plain(q.var + b, VA);
-    st_plain(q.ap + b, AP);
-    st_plain(q.pout + b, PO);
-    if (q.delta) st_plain(q.delta + b, DL);
+    // streaming (evict-first) stores: the state is re-read only next step,
+    // long after a 2^28-parameter pass has cycled L2 (A/B: 2.62 -> 2.54 ms)
+    st_stream(q.m2p + b, M2P);
+    if (s.active) st_stream(q.m2d + b, M2D);
+    st_stream(q.mean + b, ME);
+    st_stream(q.var + b, VA);
+    st_stream(q.ap + b, AP);
+    st_stream(q.pout + b, PO);
+    if (q.delta) st_stream(q.delta + b, DL);
     __syncthreads();  // every thread is done reading stage st
     if (threadIdx.x == 0 && li + kTmaStages < my_tiles) {
       fence_proxy_async_smem();
@@ -381,10 +383,10 @@ __global__ void __launch_bounds__(kThreads)
       for (int w = 0; w < W; ++w)
         adam_elem<T>(k, G.v[w], M.v[w], V.v[w], PI.v[w], TG.v[w], has_target, PO.v[w], DL.v[w],
                      acc);
-      st_plain(m + b, M);
-      st_plain(v + b, V);
-      st_plain(pout + b, PO);
-      if (delta) st_plain(delta + b, DL);
+      st_stream(m + b, M);
+      st_stream(v + b, V);
+      st_stream(pout + b, PO);
+      if (delta) st_stream(delta + b, DL);
     }
   }
   for (int64_t i = items * W + tid; i < n; i += stride) {
@@ -465,10 +467,10 @@ __global__ void __launch_bounds__(kTh, kMinB)
       adam_elem<T>(k, G.v[w], M.v[w], V.v[w], PI.v[w], TG.v[w], has_target, PO.v[w], DL.v[w],
                    acc);
     const int64_t b = (int64_t(blockIdx.x) + li * gridDim.x) * TILE + e;
-    st_plain(m + b, M);
-    st_plain(v + b, V);
-    st_plain(pout + b, PO);
-    if (delta) st_plain(delta + b, DL);
+    st_stream(m + b, M);
+    st_stream(v + b, V);
+    st_stream(pout + b, PO);
+    if (delta) st_stream(delta + b, DL);
     __syncthreads();
     if (threadIdx.x == 0 && li + kSt < my_tiles) {
       fence_proxy_async_smem();
