@@ -179,7 +179,7 @@ def run_ours(args):
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     pg = None
-    if world > 1:
+    if world > 1 or "TORCHELASTIC_RUN_ID" in os.environ:  # torchrun: NCCL even for N = 1
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=dev)
         pg = dist
