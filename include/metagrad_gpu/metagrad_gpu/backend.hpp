@@ -77,8 +77,11 @@ inline mg_ctx* ctx() { return thread_state().ctx; }
 
 // Device initialisation (CUDA context creation, ~0.1-0.5 s) happens when the
 // program loads, not inside the first timed estimator call.  Without a
-// device it is deferred: the first call then throws.
+// device it is deferred: the first call then throws.  MG_LAZY_INIT=1 defers
+// it in any case (e.g. for programs that fork before using the estimators).
 inline const bool kDeviceInitialised = [] {
+  const char* lazy = std::getenv("MG_LAZY_INIT");
+  if (lazy && lazy[0] == '1') return false;
   try {
     ctx();
     return true;
