@@ -316,6 +316,9 @@ int mg_meshscene_create(mg_ctx* ctx, int32_t tri_count, const double* tri, const
   if (e == cudaSuccess) e = cudaMemcpy(sc->obj, sobj.data(), sizeof(int) * T, cudaMemcpyHostToDevice);
   if (e == cudaSuccess)
     e = cudaMemcpy(sc->nodes, nodes.data(), sizeof(float4) * nodes.size(), cudaMemcpyHostToDevice);
+  // pageable copies may return before the DMA lands; later kernels run on
+  // non-blocking context streams, so fence once here
+  if (e == cudaSuccess) e = cudaDeviceSynchronize();
   if (e != cudaSuccess) {
     cudaFree(sc->tri);
     cudaFree(sc->tri32);

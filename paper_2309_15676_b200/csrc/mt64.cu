@@ -163,6 +163,9 @@ static int get_jump_poly(uint64_t distance, JumpPoly* out) {
   MG_CUDA_TRY(cudaMalloc(&jp.dev, sizeof(uint64_t) * kMtJumpWords));
   MG_CUDA_TRY(cudaMemcpy(jp.dev, w.data(), sizeof(uint64_t) * kMtJumpWords,
                          cudaMemcpyHostToDevice));
+  // a pageable cudaMemcpy may return before its DMA lands; the jump kernel
+  // runs on a (possibly non-blocking) context stream, so fence the device
+  MG_CUDA_TRY(cudaDeviceSynchronize());
   cache[distance] = jp;
   *out = jp;
   return MG_OK;
@@ -261,10 +264,13 @@ int mg_mt64_split(mg_ctx* ctx, uint64_t engine_seed, int32_t segments, uint64_t 
   std::vector<uint8_t> mask(static_cast<size_t>(segments));
   for (int bit = 0; bit < 31 && (int64_t(1) << bit) < segments; ++bit) {
     for (int c = 0; c < segments; ++c) mask[size_t(c)] = uint8_t((c >> bit) & 1);
-    cudaMemcpy(dmask, mask.data(), size_t(segments), cudaMemcpyHostToDevice);
+    // ordered on the context's stream: the previous jump may still be
+    // reading the mask (the stream need not synchronise with the legacy one)
+    cudaMemcpyAsync(dmask, mask.data(), size_t(segments), cudaMemcpyHostToDevice, ctx->stream);
     st = mt64_jump(ctx, g, segment_len << bit, dmask);
     if (st) break;
   }
+  cudaStreamSynchronize(ctx->stream);
   cudaFree(dmask);
   if (st) {
     mt64_destroy(g);

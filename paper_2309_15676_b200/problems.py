@@ -222,14 +222,23 @@ class MiniRenderRun:
                 block = K * D
                 L = 312 * (-(-(-(-block // gmax)) // 312))
                 G = -(-block // L)
+                # the engines run on their own stream: block b+1's draws and
+                # jump overlap block b's render iterations (double buffer)
+                self.side = torch.cuda.Stream(device=self.ctx.device)
+                self.rng_ctx = Context(self.ctx.device, stream=self.side)
                 self.rng = Rng.split(int(load().mg_stream_seed(seed, replicate)), G, L,
-                                     ctx=self.ctx)
+                                     ctx=self.rng_ctx)
                 self.seg_len, self.block_iters = L, K
             else:
                 self.rng = Rng.stream(seed, replicate, ctx=self.ctx)
                 self.seg_len, self.block_iters = None, 1
             rows = self.rng.n * self.seg_len if self.seg_len else D
             self.u = torch.empty(rows, dtype=torch.float64, device="cuda")
+            if self.seg_len:
+                self.ubuf = [self.u, torch.empty(rows, dtype=torch.float64, device="cuda")]
+                self.ready = [torch.cuda.Event(), torch.cuda.Event()]
+                self.done = [torch.cuda.Event(), torch.cuda.Event()]
+                self._fill(0)
         else:
             self.rng, self.u = None, None
             self.seg_len, self.block_iters = None, 1
@@ -238,6 +247,17 @@ class MiniRenderRun:
 
     def draws_per_sample(self) -> int:
         return self.P * self.spp
+
+    def _fill(self, blk: int):
+        """Block blk's draws (K iterations of the stream, all engines) into
+        ubuf[blk % 2] on the side stream, then jump the engines past them."""
+        j = blk % 2
+        if blk >= 2:
+            self.side.wait_event(self.done[j])       # block blk-2 no longer reads it
+        check(load().mg_mt64_draw(self.rng_ctx.h, self.rng.h, self.seg_len, 1,
+                                  _p(self.ubuf[j])))
+        self.rng.jump(self.block_iters * self.D - self.seg_len)
+        self.ready[j].record(self.side)
 
     def step(self, prop_out=None, diff_out=None, record: Optional[int] = None):
         """One iteration.  prop_out/diff_out receive this iteration's sample
@@ -254,12 +274,15 @@ class MiniRenderRun:
                             record_plus1=0 if record is None else record + 1)
         L = load()
         u = None
+        main = self.ctx.stream
         if self.rng is not None:
             k = (self.t - 1) % self.block_iters
             if self.seg_len:
-                if k == 0:  # draws for the next K iterations, then jump past them
-                    check(L.mg_mt64_draw(self.ctx.h, self.rng.h, self.seg_len, 1, _p(self.u)))
-                    self.rng.jump(self.block_iters * self.D - self.seg_len)
+                blk = (self.t - 1) // self.block_iters
+                if k == 0:  # block blk ready; start generating block blk + 1
+                    main.wait_event(self.ready[blk % 2])
+                    self._fill(blk + 1)
+                self.u = self.ubuf[blk % 2]
             else:
                 check(L.mg_mt64_draw(self.ctx.h, self.rng.h, self.D, 1, _p(self.u)))
             u = C.c_void_p(self.u.data_ptr() + 8 * (k * self.D + self.lo * self.spp))
@@ -268,6 +291,8 @@ class MiniRenderRun:
             u, _p(self.params), _p(self.prev), _p(self.m2_prop), _p(self.m2_diff),
             _p(self.mean), _p(self.var), _p(self.alpha_prev), _p(self.scalars_buf),
             _p(prop_out), _p(diff_out)))
+        if self.seg_len and k == self.block_iters - 1:
+            self.done[blk % 2].record(main)            # buffer free for block blk + 2
         # prev now holds pi_{t+1}: swap roles
         self.params, self.prev = self.prev, self.params
 
