@@ -470,7 +470,8 @@ int mg_meshscene_render(mg_ctx* ctx, const mg_mesh_scene* s, int32_t dtype, int3
  *   loss_out (device double) = 2/(n(n-1)) sum_c sum_{i<j} r_i r_j.
  * accum: device scratch of 2 * params int64, zero on first use (left
  * zeroed).  Exact fixed-point accumulation: tiles sum exactly to the full
- * pair. */
+ * pair.  The scene owns the path-state workspace: calls on one scene must
+ * be ordered (one stream at a time). */
 int mg_meshscene_sample_pair(mg_ctx* ctx, mg_mesh_scene* s, int32_t dtype, int32_t W,
                              int32_t H, const double* view, const void* target_img,
                              const void* now, const void* prev, uint64_t key, uint32_t iteration,

@@ -150,7 +150,9 @@ int mg_ctx_create(int device, void* stream, mg_ctx** out) {
   e = cudaMalloc(&ctx->partials, sizeof(ReducePartials) * kMaxReduceBlocks);
   if (e == cudaSuccess) e = cudaMalloc(&ctx->counter, sizeof(unsigned int));
   if (e == cudaSuccess) e = cudaMalloc(&ctx->flag, sizeof(int));
-  if (e == cudaSuccess) e = cudaMemset(ctx->counter, 0, sizeof(unsigned int));
+  // ordered on the context's stream (it may not synchronise with the legacy one)
+  if (e == cudaSuccess) e = cudaMemsetAsync(ctx->counter, 0, sizeof(unsigned int), ctx->stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
   if (e != cudaSuccess) {
     mg_ctx_destroy(ctx);
     return cuda_fail(e, "mg_ctx_create workspace");
