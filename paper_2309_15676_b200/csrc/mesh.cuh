@@ -108,6 +108,9 @@ __device__ __forceinline__ bool tri_hit(const double* __restrict__ r, const doub
 // ref >= 0: internal node, ref < 0: leaf with triangles [first, first +
 // count), ~ref = first * 8 + count; empty slots have an inverted box.
 // One 128-byte fetch per traversal step tests all four children.
+#ifndef MG_ANY_SORT
+#define MG_ANY_SORT 0
+#endif
 constexpr int kNodeF4 = 8;
 struct NodeW {
   float4 lx, ly, lz, hx, hy, hz, ref;
@@ -140,12 +143,16 @@ __device__ __forceinline__ float f4c(const float4& v, int c) {
   return c == 0 ? v.x : (c == 1 ? v.y : (c == 2 ? v.z : v.w));
 }
 
+// Slab test in FMA form: t = box * inv - o * inv (ooi = o * inv once per
+// ray, one FFMA per plane).  The rounding of ooi is of the order of the
+// fp32 rounding of the origin itself, which the outward box padding
+// (1e-5 of the scene diagonal) already absorbs.
 __device__ __forceinline__ bool slab6(float lx, float ly, float lz, float hx, float hy, float hz,
-                                      const float o[3], const float inv[3], float tmax,
+                                      const float ooi[3], const float inv[3], float tmax,
                                       float& tnear) {
-  const float tx0 = (lx - o[0]) * inv[0], tx1 = (hx - o[0]) * inv[0];
-  const float ty0 = (ly - o[1]) * inv[1], ty1 = (hy - o[1]) * inv[1];
-  const float tz0 = (lz - o[2]) * inv[2], tz1 = (hz - o[2]) * inv[2];
+  const float tx0 = fmaf(lx, inv[0], -ooi[0]), tx1 = fmaf(hx, inv[0], -ooi[0]);
+  const float ty0 = fmaf(ly, inv[1], -ooi[1]), ty1 = fmaf(hy, inv[1], -ooi[1]);
+  const float tz0 = fmaf(lz, inv[2], -ooi[2]), tz1 = fmaf(hz, inv[2], -ooi[2]);
   const float tn = fmaxf(fmaxf(fminf(tx0, tx1), fminf(ty0, ty1)), fmaxf(fminf(tz0, tz1), 0.0f));
   const float tf = fminf(fminf(fmaxf(tx0, tx1), fmaxf(ty0, ty1)), fminf(fmaxf(tz0, tz1), tmax));
   tnear = tn;
@@ -171,12 +178,12 @@ template <bool ANY>
 __device__ __forceinline__ int trace_impl(const MeshDev& m, const float4* sn, const double o[3],
                                           const double d[3], double tmax, double& t_out,
                                           double& u_out, double& v_out) {
-  float of[3], inv[3];
+  float ooi[3], inv[3];
 #pragma unroll
   for (int k = 0; k < 3; ++k) {
-    of[k] = float(o[k]);
     const float dk = float(d[k]);
     inv[k] = 1.0f / (fabsf(dk) > 1e-20f ? dk : copysignf(1e-20f, dk));
+    ooi[k] = float(o[k]) * inv[k];
   }
   int stack[kStackDepth];
   int sp = 0, node = 0;
@@ -213,7 +220,7 @@ __device__ __forceinline__ int trace_impl(const MeshDev& m, const float4* sn, co
       for (int c = 0; c < 4; ++c) {
         float tc;
         const bool h = slab6(f4c(n.lx, c), f4c(n.ly, c), f4c(n.lz, c), f4c(n.hx, c), f4c(n.hy, c),
-                             f4c(n.hz, c), of, inv, bestf, tc);
+                             f4c(n.hz, c), ooi, inv, bestf, tc);
         tk[c] = h ? tc : INFINITY;
         ck[c] = __float_as_int(f4c(n.ref, c));
       }
@@ -227,12 +234,28 @@ __device__ __forceinline__ int trace_impl(const MeshDev& m, const float4* sn, co
           ck[b] = cc;
         }
       };
-      cx(0, 1);
-      cx(2, 3);
-      cx(0, 2);
-      cx(1, 3);
-      cx(1, 2);
-      if (tk[0] != INFINITY) {
+      if (!ANY || MG_ANY_SORT) {  // any-hit rays need no front-to-back order
+        cx(0, 1);
+        cx(2, 3);
+        cx(0, 2);
+        cx(1, 3);
+        cx(1, 2);
+      }
+      if (ANY && !MG_ANY_SORT) {
+        int nx = 0;
+        bool have = false;
+#pragma unroll
+        for (int c = 3; c >= 0; --c) {
+          if (tk[c] == INFINITY) continue;
+          if (have) stack[sp++] = nx;
+          nx = ck[c];
+          have = true;
+        }
+        if (have) {
+          node = nx;
+          continue;
+        }
+      } else if (tk[0] != INFINITY) {
         if (tk[3] != INFINITY) stack[sp++] = ck[3];
         if (tk[2] != INFINITY) stack[sp++] = ck[2];
         if (tk[1] != INFINITY) stack[sp++] = ck[1];
@@ -293,12 +316,13 @@ template <bool ANY>
 __device__ __forceinline__ int trace32_impl(const MeshDev& m, const float4* sn, const double o[3],
                                             const double d[3], double tmax, double& t_out,
                                             double& u_out, double& v_out) {
-  float of[3], df[3], inv[3];
+  float of[3], df[3], inv[3], ooi[3];
 #pragma unroll
   for (int k = 0; k < 3; ++k) {
     of[k] = float(o[k]);
     df[k] = float(d[k]);
     inv[k] = 1.0f / (fabsf(df[k]) > 1e-20f ? df[k] : copysignf(1e-20f, df[k]));
+    ooi[k] = of[k] * inv[k];
   }
   int stack[kStackDepth];
   int sp = 0, node = 0;
@@ -332,7 +356,7 @@ __device__ __forceinline__ int trace32_impl(const MeshDev& m, const float4* sn, 
       for (int c = 0; c < 4; ++c) {
         float tc;
         const bool h = slab6(f4c(n.lx, c), f4c(n.ly, c), f4c(n.lz, c), f4c(n.hx, c), f4c(n.hy, c),
-                             f4c(n.hz, c), of, inv, best, tc);
+                             f4c(n.hz, c), ooi, inv, best, tc);
         tk[c] = h ? tc : INFINITY;
         ck[c] = __float_as_int(f4c(n.ref, c));
       }
@@ -346,12 +370,28 @@ __device__ __forceinline__ int trace32_impl(const MeshDev& m, const float4* sn, 
           ck[b] = cc;
         }
       };
-      cx(0, 1);
-      cx(2, 3);
-      cx(0, 2);
-      cx(1, 3);
-      cx(1, 2);
-      if (tk[0] != INFINITY) {
+      if (!ANY || MG_ANY_SORT) {  // any-hit rays need no front-to-back order
+        cx(0, 1);
+        cx(2, 3);
+        cx(0, 2);
+        cx(1, 3);
+        cx(1, 2);
+      }
+      if (ANY && !MG_ANY_SORT) {
+        int nx = 0;
+        bool have = false;
+#pragma unroll
+        for (int c = 3; c >= 0; --c) {
+          if (tk[c] == INFINITY) continue;
+          if (have) stack[sp++] = nx;
+          nx = ck[c];
+          have = true;
+        }
+        if (have) {
+          node = nx;
+          continue;
+        }
+      } else if (tk[0] != INFINITY) {
         if (tk[3] != INFINITY) stack[sp++] = ck[3];
         if (tk[2] != INFINITY) stack[sp++] = ck[2];
         if (tk[1] != INFINITY) stack[sp++] = ck[1];
