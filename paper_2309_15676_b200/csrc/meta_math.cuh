@@ -58,6 +58,39 @@ __device__ __forceinline__ StepScal load_step_scalars(const MetaK& k, const mg_u
   return s;
 }
 
+// IEEE a / b and sqrt(v) that keep zero operands off the slow path.  The
+// compiler's correctly rounded division and square root send a zero dividend
+// (FCHK) and a zero radicand (range test) to an out-of-line subroutine; in a
+// texture fit most parameters see no sample in an iteration, so prop = diff =
+// 0 and the fused update ran 40 % slower (tools/update_size_probe.py).  The
+// results are unchanged bit for bit: 0 / b = a * b (a signed zero) for finite
+// nonzero b, sqrt(+-0) = +-0.
+// (opaque() hides the substituted operand from the compiler, which would
+// otherwise see that the quotient is unused when z holds and fold the
+// substitution away.)
+__device__ __forceinline__ float opaque(float x) {
+  float y;
+  asm("mov.b32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ double opaque(double x) {
+  double y;
+  asm("mov.b64 %0, %1;" : "=d"(y) : "d"(x));
+  return y;
+}
+template <class T>
+__device__ __forceinline__ T div_z(T a, T b) {
+  const bool z = a == T(0) && isfinite(b) && b != T(0);
+  const T q = opaque(z ? T(1) : a) / b;
+  return z ? a * b : q;
+}
+template <class T>
+__device__ __forceinline__ T sqrt_z(T v) {
+  const bool z = v == T(0);
+  const T r = sqrt(opaque(z ? T(1) : v));
+  return z ? v : r;
+}
+
 // One parameter of the fused meta iteration.  All inputs already loaded.
 template <class T, bool FIRST>
 __device__ __forceinline__ void meta_elem(const MetaK& k, const StepScal& s, T prop, T diff,
@@ -75,13 +108,13 @@ __device__ __forceinline__ void meta_elem(const MetaK& k, const StepScal& s, T p
     const T cs = fabs(pin - pprev);                          // harness.cpp:147
     const T tiny = sizeof(T) == 8 ? T(1e-150) : T(1e-37);    // kTinyCoordStep (fp32: FLT_MIN-ish)
     if (s.active) {
-      const T x = vdiff / std_max(cs, tiny);                 // harness.cpp:149
+      const T x = div_z(vdiff, std_max(cs, tiny));                 // harness.cpp:149
       m2d_v = m2d_v + T(s.c_diff) * (x * x - m2d_v);
     }
     if (s.cnt > 0) var_diff = m2d_v * (cs * cs);             // harness.cpp:150
   } else {
     if (s.active) {
-      const T x = vdiff / T(s.norm);                         // harness.cpp:154
+      const T x = div_z(vdiff, T(s.norm));                         // harness.cpp:154
       m2d_v = m2d_v + T(s.c_diff) * (x * x - m2d_v);
     }
     if (s.cnt > 0) var_diff = m2d_v * T(s.ssn);              // meta.hpp:51-53
@@ -91,7 +124,7 @@ __device__ __forceinline__ void meta_elem(const MetaK& k, const StepScal& s, T p
   T m = (FIRST ? T(0) : mean) + diff;
   T v = (FIRST ? T(0) : var) + var_diff;
   const T a_prev = FIRST ? T(-INFINITY) : ap;
-  T al = m2p / ((m2p + v) + T(k.eps_alpha));
+  T al = div_z(m2p, (m2p + v) + T(k.eps_alpha));
   if (k.clip) al = std_min(al, T(1) / (T(2) - a_prev));      // meta.hpp:30-32
   ap = al;
   const T om = T(1) - al;
@@ -99,7 +132,7 @@ __device__ __forceinline__ void meta_elem(const MetaK& k, const StepScal& s, T p
   v = (al * al) * v + (om * om) * m2p;
   mean = m;
   var = v;
-  delta = (T(-k.lr) * m) / (sqrt(v) + T(k.eps_step));
+  delta = div_z(T(-k.lr) * m, sqrt_z(v) + T(k.eps_step));
   // params += delta; project (harness.cpp:186-187, problems.cpp:228)
   T p = pin + delta;
   if (k.project) p = std_max(p, T(k.proj_lo));

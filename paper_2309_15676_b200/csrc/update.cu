@@ -339,9 +339,9 @@ __device__ __forceinline__ void adam_elem(const AdamK& k, T g, T& m, T& v, T pin
                                           Acc& acc) {
   m = T(k.beta1) * m + T(k.c1) * g;          // adam.hpp:32
   v = T(k.beta2) * v + T(k.c2) * (g * g);    // adam.hpp:33
-  const T mh = m / T(k.d1);                  // adam.hpp:34
-  const T vh = v / T(k.d2);                  // adam.hpp:35
-  delta = (T(-k.lr) * mh) / (sqrt(vh) + T(k.eps));  // adam.hpp:36
+  const T mh = div_z(m, T(k.d1));            // adam.hpp:34
+  const T vh = div_z(v, T(k.d2));            // adam.hpp:35
+  delta = div_z(T(-k.lr) * mh, sqrt_z(vh) + T(k.eps));  // adam.hpp:36  (div_z/sqrt_z: meta_math.cuh)
   T p = pin + delta;
   if (k.project) p = std_max(p, T(k.proj_lo));
   pout = p;
@@ -528,7 +528,7 @@ __global__ void meta_step_kernel(int64_t n, MetaK k, bool first, T* __restrict__
     T v = (first ? T(0) : var[i]) + vd[i];
     const T a_prev = first ? T(-INFINITY) : ap[i];
     const T vpi = vp[i];
-    T al = vpi / ((vpi + v) + T(k.eps_alpha));
+    T al = div_z(vpi, (vpi + v) + T(k.eps_alpha));
     if (k.clip) al = std_min(al, T(1) / (T(2) - a_prev));
     ap[i] = al;
     const T om = T(1) - al;
@@ -536,7 +536,7 @@ __global__ void meta_step_kernel(int64_t n, MetaK k, bool first, T* __restrict__
     v = (al * al) * v + (om * om) * vpi;
     mean[i] = m;
     var[i] = v;
-    delta[i] = (T(-k.lr) * m) / (sqrt(v) + T(k.eps_step));
+    delta[i] = div_z(T(-k.lr) * m, sqrt_z(v) + T(k.eps_step));
   }
 }
 
@@ -548,7 +548,7 @@ __global__ void compute_alpha_kernel(int64_t n, double eps_alpha, const T* __res
                                      const T* __restrict__ ap, T* __restrict__ out) {
   for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
        i += int64_t(gridDim.x) * blockDim.x) {
-    const T raw = vp[i] / (((vp[i] + vm[i]) + vd[i]) + T(eps_alpha));
+    const T raw = div_z(vp[i], ((vp[i] + vm[i]) + vd[i]) + T(eps_alpha));
     out[i] = std_min(raw, T(1) / (T(2) - ap[i]));
   }
 }

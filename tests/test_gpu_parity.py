@@ -279,6 +279,64 @@ def test_fused_meta_update_f64_bit_exact_per_step(api, oracle, n):
         pa, pb = pb, pa
 
 
+@pytest.mark.parametrize("diff_norm", [0, 1])
+def test_fused_update_zero_samples_bit_exact(api, oracle, diff_norm):
+    """Sparse gradient samples as in the texture fits (most texels unseen in
+    an iteration): exact +-0 prop/diff take the zero-operand route of
+    div_z/sqrt_z (meta_math.cuh) and stay bit-exact with the oracle."""
+    n, steps = 4099, 5
+    props, diffs = make_inputs(n, steps, seed=9)
+    rs = np.random.RandomState(5)
+    for t in range(steps):
+        z = rs.uniform(size=n) < 0.7
+        props[t][z] = 0.0
+        diffs[t][z] = 0.0
+        props[t][z & (rs.uniform(size=n) < 0.3)] = -0.0
+    upd = api.FusedMetaUpdate(n, dtype=torch.float64, lr=0.01, project_lo=0.0,
+                              diff_norm="per-param" if diff_norm else "global")
+    st = oracle_state(n)
+    sc = _abi.fresh_scalars()
+    p_host = rs.uniform(0, 1, n)
+    p_host[:64] = 0.0  # zero coordinate steps for the per-parameter norm
+    p_prev = p_host.copy()
+    pa, pb = cu(p_host), torch.empty(n, dtype=torch.float64, device="cuda")
+    pprev = cu(p_prev)
+    beta_pow = 1.0
+    for t in range(steps):
+        beta_pow *= 0.9
+        a = _abi.MetaUpdateArgs(meta=_abi.MetaParams(0.01, 1e-8, 1e-30, 1),
+                                prop_coef=(1 - 0.9) / (1 - beta_pow), beta_delta=0.5,
+                                first_step=int(t == 0), diff_norm=diff_norm, project=1,
+                                ssn_from_host=1, proj_lo=0.0, ssn_host=sc.ssn)
+        p_new, _, rc = oracle.meta_update(a, st, props[t], diffs[t], p_host, sc,
+                                          params_prev=p_prev if diff_norm else None)
+        assert rc == 0
+        upd.step(cu(props[t]), cu(diffs[t]), pa, pb, ssn_host=a.ssn_host,
+                 params_prev=pprev if diff_norm else None)
+        assert bits_equal(host(pb), p_new), t
+        for k, buf in (("m2_prop", upd.m2_prop), ("mean", upd.mean), ("var", upd.var),
+                       ("alpha_prev", upd.alpha_prev), ("m2_diff", upd.m2_diff)):
+            if k != "m2_diff" or sc.diff_count > 0:
+                assert bits_equal(host(buf), st[k]), (t, k)
+        p_prev, p_host = p_host, p_new
+        pprev = pa.clone()
+        pa, pb = pb, pa
+    # Adam with zero gradients: 0 / d1 and sqrt(0) on the zero route
+    g = rs.standard_normal((3, n))
+    g[:, ::3] = 0.0
+    up = api.FusedAdamUpdate(n, dtype=torch.float64, lr=0.02)
+    s = _abi.AdamScalars(0.02, 0.9, 0.999, 1e-8, 1.0, 1.0, 0)
+    m, v = np.zeros(n), np.zeros(n)
+    sc = _abi.fresh_scalars()
+    p = np.zeros(n)
+    pa, pb = cu(p), torch.empty(n, dtype=torch.float64, device="cuda")
+    for k in range(3):
+        p = oracle.adam_update(s, g[k], m, v, p, sc)
+        up.step(cu(g[k]), pa, pb)
+        pa, pb = pb, pa
+    assert bits_equal(host(pa), p) and bits_equal(host(up.v), v)
+
+
 def test_fused_meta_update_f64_device_ssn_chain(api, oracle):
     """100 steps with the step norm produced on the device (tree order):
     trajectories agree with the sequential oracle to 1e-10 relative."""
