@@ -320,6 +320,7 @@ def run_ours(args):
                        "kernel": "register-streaming" if args.no_tma else "tma-bulk-pipeline"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": ncu_traffic(n, args.dtype),
+                         "frac_vs_8tbs_spec": achieved / 8000.0,
                          "peak_kind": peak_kind,
                          "kernel_ms": k_ms, "algorithmic_bytes": algo_bytes},
             "e2e": {"value": e2e_val, "unit": UNIT, "h2d_bytes_per_step": 2 * esz * n,
@@ -388,6 +389,63 @@ def extras(args, ctx):
         ms = timed(step, 10, warm=3)
         out["adam_update_f32"] = {"ms": ms, "gbs": 28 * n / (ms / 1e3) / 1e9,
                                   "frac": 28 * n / (ms / 1e3) / 1e9 / peak}
+
+    def update_sizes():
+        # configs[1]'s smaller sizes, 100 steps with state carried: 2^24 eager;
+        # 2^20 (59 MB, L2-resident, launch-bound) as ONE CUDA graph holding
+        # the 100 captured steps (each step's host scalars baked in at
+        # capture), replayed; no roofline judgement at 2^20
+        side = torch.cuda.Stream(device=dev)
+        gctx = api.Context(ctx.device, stream=side)
+        for m in (1 << 20, 1 << 24):
+            gen = torch.Generator(device=dev).manual_seed(7)
+            mu = torch.rand(m, device=dev, generator=gen) * 2 - 1
+            sg = torch.rand(m, device=dev, generator=gen) * 1.9 + 0.1
+            pr = [mu + sg * torch.randn(m, device=dev, generator=gen) for _ in range(2)]
+            df = [0.1 * sg * torch.randn(m, device=dev, generator=gen) for _ in range(2)]
+            bufs = [torch.zeros(m, device=dev), torch.empty(m, device=dev)]
+            up = api.FusedMetaUpdate(m, lr=0.01, ctx=gctx)
+
+            def hundred():
+                up.reset()
+                for t in range(100):
+                    up.step(pr[t % 2], df[t % 2], bufs[t % 2], bufs[(t + 1) % 2])
+            torch.cuda.synchronize()
+            with torch.cuda.stream(side):
+                hundred()
+                torch.cuda.synchronize()
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                if m == 1 << 20:
+                    g = torch.cuda.CUDAGraph()
+                    up.reset()
+                    with torch.cuda.graph(g, stream=side):
+                        for t in range(100):
+                            up.step(pr[t % 2], df[t % 2], bufs[t % 2], bufs[(t + 1) % 2])
+                    g.replay()
+                    torch.cuda.synchronize()
+                    a.record(side)
+                    for _ in range(5):
+                        g.replay()
+                    b.record(side)
+                    torch.cuda.synchronize()
+                    ms = a.elapsed_time(b) / 500
+                    mode = "cuda graph of 100 steps"
+                else:
+                    a.record(side)
+                    hundred()
+                    b.record(side)
+                    torch.cuda.synchronize()
+                    ms = a.elapsed_time(b) / 100
+                    mode = "eager"
+            gbs = BYTES_PER_PARAM["f32"] * m / (ms / 1e3) / 1e9
+            r = {"params": m, "ms_per_step": ms, "pairs_per_s": m / (ms / 1e3), "gbs": gbs,
+                 "mode": mode}
+            if m == 1 << 24:
+                r["frac"] = gbs / peak
+            else:
+                r["note"] = "L2-resident (59 MB < 126 MB L2): launch-bound, not roofline-judged"
+            out[f"meta_update_2^{m.bit_length() - 1}_f32"] = r
+            del pr, df, bufs, up
 
     def minirender(rng):
         # fused mini-render iteration at scale (16.7M pixels): one kernel per
@@ -477,7 +535,7 @@ def extras(args, ctx):
         out["minirender_runner"] = {"replicates": 148, "iterations": 200, "wall_s": wall,
                                     "pairs_per_s": 148 * 200 * 4096 * 2 / wall}
 
-    for name, fn in (("adam", adam), ("minirender_philox", lambda: minirender("philox")),
+    for name, fn in (("update_sizes", update_sizes), ("adam", adam), ("minirender_philox", lambda: minirender("philox")),
                      ("minirender_mt64", lambda: minirender("mt64")), ("quad", quad),
                      ("helix", helix), ("mesh", mesh), ("mesh_large", mesh_large),
                      ("runner", runner)):
