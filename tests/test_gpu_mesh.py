@@ -137,7 +137,12 @@ def test_problem_tiles_sum_exactly_and_f32_tracks_f64(api, kernel_mode):
     p32 = prob32.sample_pair(now.float(), prev.float(), 3, key=11)
     scale = float(full[0].abs().max())
     err = (p32.prop.double() - full[0]).abs()
-    assert float(err.max()) <= 1e-3 * scale
+    # north_star's fp32 bar: 1e-4 relative to the gradient scale (measured:
+    # no parameter beyond it here; a path that branched differently in fp32
+    # would show up as a parameter fraction, reported below)
+    frac = float((err > 1e-4 * scale).double().mean())
+    print("mesh f32 gradient: fraction of parameters beyond 1e-4 of scale", frac)
+    assert float(err.max()) <= 1e-4 * scale
     assert float((err > 1e-5 * scale).double().mean()) < 0.01
 
 
@@ -301,8 +306,10 @@ def test_mesh_f32_path_divergence_pixel_fraction(api, record_property):
     i64 = prob.scene.render(th, 128, 128, 1, 77).cpu().numpy().reshape(3, -1)
     i32 = prob.scene.render(th.float(), 128, 128, 1, 77).double().cpu().numpy().reshape(3, -1)
     rel = (np.abs(i32 - i64) / np.maximum(np.abs(i64), 1e-2)).max(axis=0)
-    diverged = float(np.mean(rel > 1e-3))
+    # north_star's fp32 bar: 1e-4 relative per pixel; beyond it = diverged
+    diverged = float(np.mean(rel > 1e-4))
     record_property("mesh_f32_diverged_pixel_fraction", diverged)
-    print("mesh f32 path-divergence pixel fraction", diverged)
-    assert diverged < 1e-3                 # measured 1.5e-5 at 256^2
-    assert np.median(rel[rel <= 1e-3]) < 1e-5
+    print("mesh f32 path-divergence pixel fraction (rel > 1e-4)", diverged,
+          "max rel of the rest", float(rel[rel <= 1e-4].max()))
+    assert diverged < 1e-3                 # measured 1.5e-5 at 256^2 (rel > 1e-3)
+    assert np.median(rel[rel <= 1e-4]) < 1e-5
