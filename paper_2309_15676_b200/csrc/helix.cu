@@ -70,11 +70,31 @@ __device__ int intersect(const T* __restrict__ sph, int nsph, const V3<T>& o, co
     const V3<T> oc{o.x - c[0], o.y - c[1], o.z - c[2]};
     const T b = dot3(oc, d);
     const T cc = dot3(oc, oc) - c[3] * c[3];
-    const T disc = b * b - cc;
-    if (disc < T(0)) continue;
-    const T sq = sqrt(disc);
-    T t = -b - sq;
-    if (t < T(kEps)) t = -b + sq;
+    T t;
+    if constexpr (sizeof(T) == 8) {  // the oracle's expression order (parity)
+      const T disc = b * b - cc;
+      if (disc < T(0)) continue;
+      const T sq = sqrt(disc);
+      t = -b - sq;
+      if (t < T(kEps)) t = -b + sq;
+    } else {
+      // fp32: b*b - cc cancels for a distant sphere (|oc|^2 ~ 36 vs r^2 =
+      // 0.01), leaving ~1e-5 error in t and ~1e-4 in the normal, which the
+      // GGX lobe amplifies.  Discriminant from the ray's closest approach
+      // (r^2 - |oc - b d|^2) and the cancellation-free pair of roots q,
+      // cc / q instead.
+      // cheap reject first: the cancelling form is off by at most a few
+      // ulp of b^2 (+ |oc|^2), so a clear miss stays a miss
+      if (b * b - cc < T(-1e-6) * (b * b + dot3(oc, oc))) continue;
+      const V3<T> f{oc.x - b * d.x, oc.y - b * d.y, oc.z - b * d.z};
+      const T disc = c[3] * c[3] - dot3(f, f);
+      if (disc < T(0)) continue;
+      const T qq = -b - copysign(sqrt(disc), b);
+      if (qq == T(0)) continue;
+      const T r0 = cc / qq;
+      const T t0 = fmin(qq, r0), t1 = fmax(qq, r0);
+      t = t0 < T(kEps) ? t1 : t0;
+    }
     if (t < T(kEps) || t >= best) continue;
     best = t;
     kind = 1;

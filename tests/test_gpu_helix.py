@@ -120,7 +120,9 @@ def test_helix_f32_path_divergence_pixel_fraction(api, record_property):
     diverged = float(np.mean(rel.max(axis=0) > 1e-3))
     record_property("helix_f32_diverged_pixel_fraction", diverged)
     print("helix f32 path-divergence pixel fraction", diverged)
-    assert diverged < 0.06      # measured 3.5% (128 x 128, 1 spp)
+    # measured 3.7e-4 (128 x 128, 1 spp) with the cancellation-free fp32
+    # sphere test (3.5e-2 with the fp64 expression order evaluated in fp32)
+    assert diverged < 2e-3
     # the remaining pixels agree to fp32 precision
     same = rel.max(axis=0) <= 1e-3
     assert np.median(rel.max(axis=0)[same]) < 1e-5
