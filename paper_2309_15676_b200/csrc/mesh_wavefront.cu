@@ -238,6 +238,12 @@ __global__ void __launch_bounds__(kMThreads)
         T base[2][3], rough[2], metal[2];
 #pragma unroll
         for (int s = 0; s < 2; ++s) {
+          if (s >= ns) {  // the set is not evaluated: no texel gathers
+#pragma unroll
+            for (int c = 0; c < 3; ++c) base[s][c] = T(0);
+            rough[s] = metal[s] = T(0);
+            continue;
+          }
 #pragma unroll
           for (int c = 0; c < 3; ++c) base[s][c] = th[s][pbase + c * R2];
           rough[s] = th[s][pbase + 3 * R2];
