@@ -468,8 +468,8 @@ int mg_meshscene_render(mg_ctx* ctx, const mg_mesh_scene* s, int32_t dtype, int3
  *   prop = 2/(n(n-1)) sum_c sum_j (sum_{i != j} r_i) dI_j   (n = 2: r_A dI_B + r_B dI_A)
  *   diff = sum_c 2 r_C dI_A (theta_t) - 2 r_C dI_A (theta_{t-1})
  *   loss_out (device double) = 2/(n(n-1)) sum_c sum_{i<j} r_i r_j.
- * accum: device scratch of 2 * params int64, zero on first use (left
- * zeroed).  Exact fixed-point accumulation: tiles sum exactly to the full
+ * accum: device scratch of 2 * params int64 (internal layout), zero on
+ * first use (left zeroed).  Exact fixed-point accumulation: tiles sum exactly to the full
  * pair.  The scene owns the path-state workspace: calls on one scene must
  * be ordered (one stream at a time). */
 int mg_meshscene_sample_pair(mg_ctx* ctx, mg_mesh_scene* s, int32_t dtype, int32_t W,

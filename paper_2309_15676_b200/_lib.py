@@ -10,7 +10,8 @@ import os
 from . import _abi
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libmgcuda.so")
+# MG_LIB overrides the library path (A/B timing of two builds only)
+LIB_PATH = os.environ.get("MG_LIB") or os.path.join(HERE, "libmgcuda.so")
 
 _vp = C.c_void_p
 _lib = None

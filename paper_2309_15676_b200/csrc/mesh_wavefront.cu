@@ -416,15 +416,23 @@ __global__ void __launch_bounds__(kMThreads, 8) wf_shadow_kernel(MeshDev m, WF<T
   }
 }
 
-// Where the fixed-point adjoints go.  One rank: one accumulator [2][np]
-// (prop | diff).  Tile-sharded ranks (configs[3]/[4] over NVLink): parameter
-// j is owned by rank j / shard, whose accumulator [2][shard] is reached
-// through a peer pointer — the scatter IS the reduce-scatter (integer atomics
-// commute, so the owner's sums are independent of the ranks' order).
+// Where the fixed-point adjoints go.
+//  * One rank (ilv = 1): one accumulator, texel-interleaved
+//    [obj][texel][prop | diff][NCH] — the NCH channel atomics of a vertex
+//    land in 1-2 adjacent 32-byte sectors instead of NCH sectors a plane
+//    apart (the accumulator is larger than L2, so every sector touched is a
+//    DRAM read-modify-write).  mesh_finalize_ilv transposes it back into the
+//    planar parameter order [obj][ch][texel].
+//  * Tile-sharded ranks (configs[3]/[4] over NVLink, ilv = 0): parameter j
+//    (planar order) is owned by rank j / shard, whose accumulator
+//    [2][shard] is reached through a peer pointer — the scatter IS the
+//    reduce-scatter (integer atomics commute, so the owner's sums are
+//    independent of the ranks' order).
 constexpr int kMaxRanks = 8;
 struct AccTable {
   unsigned long long* ptr[kMaxRanks];
   int shard;  // parameters per rank
+  int ilv;    // 1: single texel-interleaved accumulator
 };
 
 __device__ __forceinline__ unsigned long long* acc_slot(const AccTable& a, int j, int which) {
@@ -432,49 +440,124 @@ __device__ __forceinline__ unsigned long long* acc_slot(const AccTable& a, int j
   return a.ptr[r] + size_t(which) * a.shard + (j - r * a.shard);
 }
 
-// adjoint of stored path p (megakernel `scatter` / oracle ms_scatter)
+// the accumulator cells of vertex parameter base `base` (= obj*NCH*R2 + texel)
+template <int NCH, bool ILV>
+struct AccCell {
+  unsigned long long* q;  // ILV: the texel's [2][NCH] cell
+  int base, R2;
+  __device__ __forceinline__ AccCell(const AccTable& a, int b, int r2) : base(b), R2(r2) {
+    if (ILV) {
+      const int obj = b / (NCH * r2), tex = b - obj * NCH * r2;
+      q = a.ptr[0] + (size_t(obj) * r2 + tex) * (2 * NCH);
+    }
+  }
+  __device__ __forceinline__ unsigned long long* at(const AccTable& a, int which, int k) const {
+    return ILV ? q + which * NCH + k : acc_slot(a, base + k * R2, which);
+  }
+};
+
+// Per-vertex adjoint terms of stored path p, parameter set s (megakernel
+// `scatter` / oracle ms_scatter), before the channel weights: X[c][0] for
+// base colour c, X[c][1] roughness, X[c][2] metalness (NCH 5); Q is the
+// suffix radiance.  combine() applies weights wt:
+//   g[c] = wt[c] X[c][0],  g[3] = sum_c wt[c] X[c][1],  g[4] = sum_c wt[c] X[c][2].
 template <class T, int NCH>
-__device__ __noinline__ void wf_scatter(const WF<T>& w, int p, int s, const T wt[3], int R2,
-                                        const AccTable& acc, int which) {
+__device__ __forceinline__ void vertex_terms(const WF<T>& w, int v, int p, int s, const T Q[3],
+                                             T X[3][NCH - 2]) {
+  using F = VF<NCH>;
+  if constexpr (NCH == 5) {
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      const T A = vf(w, v, F::A + s * 3 + c, p), fb = vf(w, v, F::invfb + s * 3 + c, p);
+      const int dn = F::dfn + s * 9 + c * 3, db = F::dfb + s * 9 + c * 3;
+      X[c][0] = A * vf(w, v, dn, p) + Q[c] * (fb * vf(w, v, db, p));
+      X[c][2] = A * vf(w, v, dn + 1, p) + Q[c] * (fb * vf(w, v, db + 1, p));
+      X[c][1] = A * vf(w, v, dn + 2, p) + Q[c] * (fb * vf(w, v, db + 2, p));
+    }
+  } else {
+    const T dSn = vf(w, v, F::dSn + s, p), dSb = vf(w, v, F::dSb + s, p);
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      const T A = vf(w, v, F::A + s * 3 + c, p), ifb = vf(w, v, F::invfb + s * 3 + c, p);
+      X[c][0] = (A / T(kPiM)) + Q[c] * (ifb / T(kPiM));
+      X[c][1] = A * dSn + Q[c] * (ifb * dSb);
+    }
+  }
+}
+
+template <class T, int NCH>
+__device__ __forceinline__ void combine(const T X[3][NCH - 2], const T wt[3], T g[NCH]) {
+#pragma unroll
+  for (int c = 0; c < 3; ++c) g[c] = wt[c] * X[c][0];
+#pragma unroll
+  for (int k = 1; k < NCH - 2; ++k) {
+    T a = T(0);
+#pragma unroll
+    for (int c = 0; c < 3; ++c) a += wt[c] * X[c][k];
+    g[2 + k] = a;
+  }
+}
+
+// adjoint of stored proportional path p (set 0) into the prop accumulator
+template <class T, int NCH, bool ILV>
+__device__ __noinline__ void wf_scatter(const WF<T>& w, int p, const T wt[3], int R2,
+                                        const AccTable& acc) {
   using F = VF<NCH>;
   T Q[3];
 #pragma unroll
-  for (int c = 0; c < 3; ++c) Q[c] = w.E[size_t(s * 3 + c) * w.P + p];
+  for (int c = 0; c < 3; ++c) Q[c] = w.E[size_t(c) * w.P + p];
   for (int v = w.nv[p] - 1; v >= 0; --v) {
-    const int base = w.vbase[size_t(v) * w.PS + p];
-    if constexpr (NCH == 5) {
-      T gm = T(0), gr = T(0);
+    const AccCell<NCH, ILV> cell(acc, w.vbase[size_t(v) * w.PS + p], R2);
+    T X[3][NCH - 2], g[NCH];
+    vertex_terms<T, NCH>(w, v, p, 0, Q, X);
+    combine<T, NCH>(X, wt, g);
 #pragma unroll
-      for (int c = 0; c < 3; ++c) {
-        const T A = vf(w, v, F::A + s * 3 + c, p), fb = vf(w, v, F::invfb + s * 3 + c, p);
-        const int dn = F::dfn + s * 9 + c * 3, db = F::dfb + s * 9 + c * 3;
-        const T gb = wt[c] * (A * vf(w, v, dn, p) + Q[c] * (fb * vf(w, v, db, p)));
-        atomicAdd(acc_slot(acc, base + c * R2, which), fixq(double(gb)));
-        gm += wt[c] * (A * vf(w, v, dn + 1, p) + Q[c] * (fb * vf(w, v, db + 1, p)));
-        gr += wt[c] * (A * vf(w, v, dn + 2, p) + Q[c] * (fb * vf(w, v, db + 2, p)));
-      }
-      atomicAdd(acc_slot(acc, base + 3 * R2, which), fixq(double(gr)));
-      atomicAdd(acc_slot(acc, base + 4 * R2, which), fixq(double(gm)));
-    } else {
-      const T dSn = vf(w, v, F::dSn + s, p), dSb = vf(w, v, F::dSb + s, p);
-      T gr = T(0);
+    for (int k = 0; k < NCH; ++k) atomicAdd(cell.at(acc, 0, k), fixq(double(g[k])));
 #pragma unroll
-      for (int c = 0; c < 3; ++c) {
-        const T A = vf(w, v, F::A + s * 3 + c, p), ifb = vf(w, v, F::invfb + s * 3 + c, p);
-        const T gb = wt[c] * ((A / T(kPiM)) + Q[c] * (ifb / T(kPiM)));
-        atomicAdd(acc_slot(acc, base + c * R2, which), fixq(double(gb)));
-        gr += wt[c] * (A * dSn + Q[c] * (ifb * dSb));
-      }
-      atomicAdd(acc_slot(acc, base + 3 * R2, which), fixq(double(gr)));
+    for (int c = 0; c < 3; ++c) Q[c] = Q[c] + vf(w, v, F::C + c, p);
+  }
+}
+
+// Path A (p = pixel i) in ONE walk: its proportional adjoint (set 0,
+// weights wt) and both finite-difference adjoints (set 0 with wC0, set 1
+// with wC1).  The two FD terms of a parameter are added as integers before
+// the atomic — the same fixed-point sum as two separate atomics, bit for bit.
+template <class T, int NCH, bool ILV>
+__device__ __noinline__ void wf_scatter_a(const WF<T>& w, int p, const T wt[3], const T wC0[3],
+                                          const T wC1[3], int R2, const AccTable& acc) {
+  using F = VF<NCH>;
+  T Q0[3], Q1[3];
+#pragma unroll
+  for (int c = 0; c < 3; ++c) {
+    Q0[c] = w.E[size_t(c) * w.P + p];
+    Q1[c] = w.E[size_t(3 + c) * w.P + p];
+  }
+  for (int v = w.nv[p] - 1; v >= 0; --v) {
+    const AccCell<NCH, ILV> cell(acc, w.vbase[size_t(v) * w.PS + p], R2);
+    T X[3][NCH - 2], g[NCH];
+    unsigned long long d[NCH];
+    vertex_terms<T, NCH>(w, v, p, 0, Q0, X);
+    combine<T, NCH>(X, wt, g);
+#pragma unroll
+    for (int k = 0; k < NCH; ++k) atomicAdd(cell.at(acc, 0, k), fixq(double(g[k])));
+    combine<T, NCH>(X, wC0, g);
+#pragma unroll
+    for (int k = 0; k < NCH; ++k) d[k] = fixq(double(g[k]));
+    vertex_terms<T, NCH>(w, v, p, 1, Q1, X);
+    combine<T, NCH>(X, wC1, g);
+#pragma unroll
+    for (int k = 0; k < NCH; ++k) atomicAdd(cell.at(acc, 1, k), d[k] + fixq(double(g[k])));
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      Q0[c] = Q0[c] + vf(w, v, F::C + c, p);
+      Q1[c] = Q1[c] + vf(w, v, F::C + 3 + c, p);
     }
-#pragma unroll
-    for (int c = 0; c < 3; ++c) Q[c] = Q[c] + vf(w, v, F::C + s * 3 + c, p);
   }
 }
 
 constexpr int kMaxProp = 8;
 
-template <class T, int NCH>
+template <class T, int NCH, bool ILV>
 __global__ void __launch_bounds__(kMThreads)
     wf_scatter_kernel(MeshK q, WF<T> w, const T* __restrict__ target_img, AccTable acc,
                       ReducePartials* partials, unsigned int* counter, double* loss_out) {
@@ -511,10 +594,11 @@ __global__ void __launch_bounds__(kMThreads)
         }
         wt[c] = a * scale;
       }
-      wf_scatter<T, NCH>(w, j * w.npix + i, 0, wt, R2, acc, 0);
+      if (j == 0)
+        wf_scatter_a<T, NCH, ILV>(w, i, wt, wC0, wC1, R2, acc);
+      else
+        wf_scatter<T, NCH, ILV>(w, j * w.npix + i, wt, R2, acc);
     }
-    wf_scatter<T, NCH>(w, i, 0, wC0, R2, acc, 1);
-    wf_scatter<T, NCH>(w, i, 1, wC1, R2, acc, 1);
   }
   Acc a;
   a.ssn = loss;
@@ -532,6 +616,79 @@ __global__ void mesh_finalize_kernel(long long n, unsigned long long* __restrict
     acc[k] = 0ull;
     acc[n + k] = 0ull;
   }
+}
+
+// texel-interleaved accumulator [cells = nobj*R2][2][NCH] -> planar prop /
+// diff [obj][ch][texel]; accumulator zeroed.  A CTA takes 256 consecutive
+// cells per step: the 256 x 2 x NCH words are copied to shared memory with
+// 16-byte cp.async (double-buffered: the next tile is in flight while this
+// one is written out), zeroed in global memory with coalesced 16-byte
+// stores, then written one thread per cell (coalesced along the texel).
+constexpr int kFinCells = 256;
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  const unsigned sa = unsigned(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(gmem) : "memory");
+}
+
+template <class T, int NCH>
+__global__ void __launch_bounds__(kFinCells)
+    mesh_finalize_ilv_kernel(long long cells, int R2, unsigned long long* __restrict__ acc,
+                             T* __restrict__ prop, T* __restrict__ diff) {
+  constexpr int kW = 2 * NCH;  // words per cell (even: tiles are 16-byte aligned)
+  __shared__ __align__(16) long long sm[2][kFinCells * kW];
+  const long long step = (long long)gridDim.x * kFinCells;
+  auto issue = [&](long long c0, int b) {
+    if (c0 < cells) {
+      const int n2 = int(cells - c0 < kFinCells ? cells - c0 : kFinCells) * (kW / 2);
+      const ulonglong2* a2 = reinterpret_cast<const ulonglong2*>(acc + c0 * kW);
+#pragma unroll
+      for (int u = 0; u < NCH; ++u) {
+        const int j = threadIdx.x + u * kFinCells;
+        if (j < n2) cp_async16(&sm[b][2 * j], a2 + j);
+      }
+    }
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
+  };
+  int b = 0;
+  long long c0 = blockIdx.x * (long long)kFinCells;
+  issue(c0, 0);
+  for (; c0 < cells; c0 += step, b ^= 1) {
+    issue(c0 + step, b ^ 1);
+    asm volatile("cp.async.wait_group 1;\n" ::: "memory");
+    const int nc = int(cells - c0 < kFinCells ? cells - c0 : kFinCells);
+    ulonglong2* a2 = reinterpret_cast<ulonglong2*>(acc + c0 * kW);
+#pragma unroll
+    for (int u = 0; u < NCH; ++u) {  // this thread's own copies have landed
+      const int j = threadIdx.x + u * kFinCells;
+      if (j < nc * (kW / 2)) a2[j] = make_ulonglong2(0ull, 0ull);
+    }
+    __syncthreads();
+    const int t = threadIdx.x;
+    if (t < nc) {
+      const long long k = c0 + t, obj = k / R2, tex = k - obj * R2;
+#pragma unroll
+      for (int c = 0; c < NCH; ++c) {
+        const long long o = (obj * NCH + c) * R2 + tex;
+        prop[o] = T(double(sm[b][t * kW + c]) / kFixM);
+        diff[o] = T(double(sm[b][t * kW + NCH + c]) / kFixM);
+      }
+    }
+    __syncthreads();  // buffer b is refilled by the next issue
+  }
+  asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+}
+
+template <class T>
+int finalize_ilv(mg_ctx* ctx, int nch, long long cells, int R2, unsigned long long* acc, T* prop,
+                 T* diff) {
+  const int grid = grid_for(ctx, cells, kFinCells, 8);
+  if (nch == 5)
+    mesh_finalize_ilv_kernel<T, 5><<<grid, kFinCells, 0, ctx->stream>>>(cells, R2, acc, prop, diff);
+  else
+    mesh_finalize_ilv_kernel<T, 4><<<grid, kFinCells, 0, ctx->stream>>>(cells, R2, acc, prop, diff);
+  MG_LAUNCH_CHECK(ctx);
+  return MG_OK;
 }
 
 }  // namespace
@@ -570,8 +727,13 @@ int wavefront_pair(mg_ctx* ctx, mg_mesh_scene* s, const MeshK& q, int nprop, con
     wf_shadow_kernel<T, NCH><<<grid, kMThreads, 0, ctx->stream>>>(m, w, v);
     MG_LAUNCH_CHECK(ctx);
   }
-  wf_scatter_kernel<T, NCH><<<grid_for(ctx, npix, kMThreads, 8), kMThreads, 0, ctx->stream>>>(
-      q, w, target_img, acc, ctx->partials, ctx->counter, loss_out);
+  const int sgrid = grid_for(ctx, npix, kMThreads, 8);
+  if (acc.ilv)
+    wf_scatter_kernel<T, NCH, true><<<sgrid, kMThreads, 0, ctx->stream>>>(
+        q, w, target_img, acc, ctx->partials, ctx->counter, loss_out);
+  else
+    wf_scatter_kernel<T, NCH, false><<<sgrid, kMThreads, 0, ctx->stream>>>(
+        q, w, target_img, acc, ctx->partials, ctx->counter, loss_out);
   MG_LAUNCH_CHECK(ctx);
   return MG_OK;
 }
@@ -624,12 +786,22 @@ int mg_meshscene_sample_pair(mg_ctx* ctx, mg_mesh_scene* s, int32_t dtype, int32
   AccTable tbl{};
   tbl.ptr[0] = acc;
   tbl.shard = int(np);
-  // the megakernel implements the configs[3] form (4 channels, 2 proportional paths)
-  if (g_mesh_megakernel && s->nch == 4 && prop_paths == 2)
+  tbl.ilv = 1;
+  // the megakernel implements the configs[3] form (4 channels, 2 proportional
+  // paths) and accumulates in planar order
+  const bool mega = g_mesh_megakernel && s->nch == 4 && prop_paths == 2;
+  if (mega)
     st = megakernel_pair(ctx, s, q, dtype, target_img, now, prev, acc, np, loss_out);
   else
     st = dispatch_wavefront(ctx, s, q, dtype, prop_paths, target_img, now, prev, tbl, loss_out);
   if (st) return st;
+  if (!mega) {
+    const long long cells = (long long)s->nobj * s->R * s->R;
+    if (dtype == MG_F64)
+      return finalize_ilv<double>(ctx, s->nch, cells, s->R * s->R, acc, (double*)prop,
+                                  (double*)diff);
+    return finalize_ilv<float>(ctx, s->nch, cells, s->R * s->R, acc, (float*)prop, (float*)diff);
+  }
   const int fgrid = grid_for(ctx, np, 256, 8);
   if (dtype == MG_F64)
     mesh_finalize_kernel<double><<<fgrid, 256, 0, ctx->stream>>>(np, acc, (double*)prop,
@@ -674,6 +846,7 @@ int mg_meshscene_sample_pair_sharded(mg_ctx* ctx, mg_mesh_scene* s, int32_t dtyp
     tbl.ptr[r] = static_cast<unsigned long long*>(acc_ptrs[r]);
   }
   tbl.shard = int(shard);
+  tbl.ilv = 0;
   return dispatch_wavefront(ctx, s, q, dtype, prop_paths, target_img, now, prev, tbl, loss_out);
 }
 
