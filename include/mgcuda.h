@@ -452,6 +452,12 @@ int mg_meshscene_create(mg_ctx* ctx, int32_t tri_count, const double* tri, const
                         int32_t nobj, int32_t tex_res, int32_t channels, mg_mesh_scene** out);
 int mg_meshscene_destroy(mg_mesh_scene* s);
 int mg_meshscene_info(const mg_mesh_scene* s, int32_t* nodes, int32_t* depth, int64_t* params);
+/* Opt-in for optimisation loops that ping-pong their parameter buffers: the
+ * caller promises that whenever a sample-pair call's `prev` equals the
+ * previous call's `now` pointer, it still holds the values it held then.
+ * The shade stage's texel-major copy of that buffer is then reused instead
+ * of rebuilt (one relayout per iteration instead of two). */
+int mg_meshscene_set_prev_reuse(mg_mesh_scene* s, int32_t enable);
 /* closest hit of n rays (device fp64 [n][6] = origin, direction): t (inf on
  * a miss) and the original triangle index (-1 on a miss); ties on t go to
  * the lower index (= a brute-force scan). */

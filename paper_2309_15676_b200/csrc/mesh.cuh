@@ -29,6 +29,11 @@ struct mg_mesh_scene {
   unsigned int* work = nullptr;  // pixel work counter of the pair kernel
   void* wf = nullptr;            // wavefront path state (grow-only)
   size_t wf_cap = 0;
+  // texel-major parameter copies in the workspace (mg_meshscene_set_prev_reuse)
+  bool prev_reuse = false;
+  const void* last_now = nullptr;  // `now` of the previous wavefront call ...
+  int last_now_slot = -1;          // ... the copy slot holding it (-1: none)
+  int last_dtype = -1;
 };
 
 namespace mg {

@@ -58,6 +58,45 @@ size_t wf_bytes(int npix, int nprop, int nvf) {
          sizeof(unsigned int) * 2 * (kMaxV + 1) + 256 * 40;
 }
 
+// Texel-major copies of the two parameter sets for the shade stage: texel
+// (obj, t) at cell obj*R2 + t holds its NCH channels in TS slots (padded to
+// one 16/32-byte aligned group), so a path vertex gathers its texel with one
+// or two vector loads from one sector instead of NCH sectors a plane apart.
+template <class T, int NCH>
+struct TexIlv {
+  static constexpr int TS = NCH == 4 ? 4 : 8;
+};
+
+// planar [obj][ch][R2] -> texel-major [cell][TS]: a CTA reads 256 cells
+// channel by channel (coalesced), transposes through shared memory and
+// stores the 256 x TS block with 16-byte vector stores.
+template <class T, int NCH>
+__global__ void __launch_bounds__(256) tex_ilv_kernel(int cells, int R2, const T* __restrict__ th,
+                                                      T* __restrict__ out) {
+  constexpr int TS = TexIlv<T, NCH>::TS;
+  constexpr int VW = 16 / sizeof(T);  // elements per 16-byte store
+  __shared__ __align__(16) T sm[256 * TS];
+  for (int c0 = blockIdx.x * 256; c0 < cells; c0 += gridDim.x * 256) {
+    const int k = c0 + threadIdx.x;
+    if (k < cells) {
+      const int obj = k / R2, tex = k - obj * R2;
+#pragma unroll
+      for (int c = 0; c < TS; ++c)
+        sm[threadIdx.x * TS + c] = c < NCH ? th[(size_t(obj) * NCH + c) * R2 + tex] : T(0);
+    }
+    __syncthreads();
+    const int nv = (cells - c0 < 256 ? cells - c0 : 256) * TS / VW;
+    const uint4* src = reinterpret_cast<const uint4*>(sm);
+    uint4* dst = reinterpret_cast<uint4*>(out + size_t(c0) * TS);
+#pragma unroll
+    for (int u = 0; u < TS * 256 / VW / 256; ++u) {
+      const int j = threadIdx.x + u * 256;
+      if (j < nv) dst[j] = src[j];
+    }
+    __syncthreads();
+  }
+}
+
 template <class T>
 WF<T> wf_carve(void* mem, int npix, int nprop, int nvf) {
   WF<T> w;
@@ -156,6 +195,7 @@ template <class T, int NCH>
 __global__ void __launch_bounds__(kMThreads)
     wf_shade_kernel(MeshK q, MeshDev m, WF<T> w, int v, const T* __restrict__ th0,
                     const T* __restrict__ th1) {
+  constexpr int TS = TexIlv<T, NCH>::TS;  // th0 / th1: texel-major copies
   using F = VF<NCH>;
   const double* V = q.view;
   const int maxv = int(V[24]);
@@ -212,9 +252,10 @@ __global__ void __launch_bounds__(kMThreads)
 #pragma unroll
           for (int c = 0; c < 3; ++c) {
             if (s >= ns) break;
-            const T e = beta[s][c] * T(V[21 + c]);
-            w.E[size_t(s * 3 + c) * w.P + p] = e;
-            w.L[size_t(s * 3 + c) * w.P + p] += e;
+            // L += E is left to the consumer (wf_scatter_kernel): the
+            // escape is the path's last event, so (L + E) there is the same
+            // sum, and the scattered read-modify-write of L is saved
+            w.E[size_t(s * 3 + c) * w.P + p] = beta[s][c] * T(V[21 + c]);
           }
       } else {
         const double o[3] = {w.ox[p], w.oy[p], w.oz[p]}, d[3] = {w.dx[p], w.dy[p], w.dz[p]};
@@ -232,7 +273,9 @@ __global__ void __launch_bounds__(kMThreads)
         int tx = int(U * q.R), ty = int(W_ * q.R);
         tx = tx < 0 ? 0 : (tx > q.R - 1 ? q.R - 1 : tx);
         ty = ty < 0 ? 0 : (ty > q.R - 1 ? q.R - 1 : ty);
-        const int pbase = __ldg(&m.obj[slot]) * NCH * R2 + ty * q.R + tx;
+        const int oid = __ldg(&m.obj[slot]), tex = ty * q.R + tx;
+        const int pbase = oid * NCH * R2 + tex;
+        const size_t cell = size_t(oid) * R2 + tex;
         w.nv[p] = v + 1;
         if (store) w.vbase[size_t(v) * w.PS + p] = pbase;
         bool nee_done = false, bounce_done = false;
@@ -245,10 +288,29 @@ __global__ void __launch_bounds__(kMThreads)
             rough[s] = metal[s] = T(0);
             continue;
           }
+          T x[TS];
+          const T* tp = th[s] + cell * TS;
+          if constexpr (sizeof(T) == 4) {
 #pragma unroll
-          for (int c = 0; c < 3; ++c) base[s][c] = th[s][pbase + c * R2];
-          rough[s] = th[s][pbase + 3 * R2];
-          metal[s] = NCH == 5 ? th[s][pbase + 4 * R2] : T(0);
+            for (int g = 0; g < TS; g += 4) {
+              const float4 f4 = __ldg(reinterpret_cast<const float4*>(tp + g));
+              x[g] = f4.x;
+              x[g + 1] = f4.y;
+              x[g + 2] = f4.z;
+              x[g + 3] = f4.w;
+            }
+          } else {
+#pragma unroll
+            for (int g = 0; g < (NCH + 1) / 2 * 2; g += 2) {
+              const double2 d2 = __ldg(reinterpret_cast<const double2*>(tp + g));
+              x[g] = d2.x;
+              x[g + 1] = d2.y;
+            }
+          }
+#pragma unroll
+          for (int c = 0; c < 3; ++c) base[s][c] = x[c];
+          rough[s] = x[3];
+          metal[s] = NCH == 5 ? x[4] : T(0);
         }
         const double wo[3] = {-d[0], -d[1], -d[2]};
         const double xo[3] = {x[0] + kOff * nn[0], x[1] + kOff * nn[1], x[2] + kOff * nn[2]};
@@ -576,9 +638,13 @@ __global__ void __launch_bounds__(kMThreads, 4)
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
       const T Is = target_img[size_t(c) * npix_img + pix];
-      for (int j = 0; j < n; ++j) r[j][c] = w.L[size_t(c) * w.P + j * w.npix + i] - Is;
-      wC0[c] = T(2) * (w.L[size_t(c) * w.P + pc] - Is);
-      wC1[c] = T(-2) * (w.L[size_t(3 + c) * w.P + pc] - Is);
+      auto rad = [&](int ch, int path) {  // path radiance L + E (escape term deferred)
+        const size_t o = size_t(ch) * w.P + path;
+        return w.L[o] + w.E[o];
+      };
+      for (int j = 0; j < n; ++j) r[j][c] = rad(c, j * w.npix + i) - Is;
+      wC0[c] = T(2) * (rad(c, pc) - Is);
+      wC1[c] = T(-2) * (rad(3 + c, pc) - Is);
       T lp = T(0);
       for (int a = 0; a < n; ++a)
         for (int b = a + 1; b < n; ++b) lp += r[a][c] * r[b][c];
@@ -705,17 +771,43 @@ int wavefront_pair(mg_ctx* ctx, mg_mesh_scene* s, const MeshK& q, int nprop, con
     return MG_OK;
   }
   if (int64_t(npix) * (nprop + 1) > 0x7fffffffLL) return fail(MG_EINVAL, "mesh scene: image too large");
-  const size_t need = wf_bytes<T>(npix, nprop, VF<NCH>::n);
+  constexpr int TS = TexIlv<T, NCH>::TS;
+  const long long cells = (long long)s->nobj * q.R * q.R;
+  const size_t tex_bytes = (sizeof(T) * TS * size_t(cells) + 255) & ~size_t(255);
+  // the two texel-copy slots come first: their addresses depend on the scene
+  // only, not on the tile size, so a copy can outlive the call that made it
+  const size_t need = 2 * tex_bytes + wf_bytes<T>(npix, nprop, VF<NCH>::n);
   if (need > s->wf_cap) {
     MG_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
     cudaFree(s->wf);
     s->wf = nullptr;
     s->wf_cap = 0;
+    s->last_now_slot = -1;
     MG_CUDA_TRY(cudaMalloc(&s->wf, need));
     s->wf_cap = need;
   }
-  WF<T> w = wf_carve<T>(s->wf, npix, nprop, VF<NCH>::n);
+  WF<T> w = wf_carve<T>(static_cast<char*>(s->wf) + 2 * tex_bytes, npix, nprop, VF<NCH>::n);
   w.pix0 = q.row0 * q.W;
+  T* slot[2];
+  slot[0] = static_cast<T*>(s->wf);
+  slot[1] = reinterpret_cast<T*>(static_cast<char*>(s->wf) + tex_bytes);
+  T* thI[2];
+  {
+    const int dt = sizeof(T) == 8 ? MG_F64 : MG_F32;
+    const bool reuse = s->prev_reuse && s->last_now_slot >= 0 && s->last_dtype == dt &&
+                       prev == s->last_now && now != prev;
+    const int sp = reuse ? s->last_now_slot : 1, sn = 1 - sp;
+    const int tg = grid_for(ctx, cells, 256, 8);
+    thI[0] = slot[sn];
+    thI[1] = slot[sp];
+    tex_ilv_kernel<T, NCH><<<tg, 256, 0, ctx->stream>>>(int(cells), q.R * q.R, now, thI[0]);
+    if (!reuse)
+      tex_ilv_kernel<T, NCH><<<tg, 256, 0, ctx->stream>>>(int(cells), q.R * q.R, prev, thI[1]);
+    MG_LAUNCH_CHECK(ctx);
+    s->last_now = now;
+    s->last_now_slot = sn;
+    s->last_dtype = dt;
+  }
   const MeshDev m = dev_of(s);
   MG_CUDA_TRY(cudaMemsetAsync(w.cnt, 0, sizeof(unsigned int) * 2 * (kMaxV + 1), ctx->stream));
   const int grid = grid_for(ctx, w.P, kMThreads, 8);
@@ -725,7 +817,7 @@ int wavefront_pair(mg_ctx* ctx, mg_mesh_scene* s, const MeshK& q, int nprop, con
   for (int v = 0; v < maxv; ++v) {
     wf_isect_kernel<T><<<grid, kMThreads, 0, ctx->stream>>>(m, w, v);
     MG_LAUNCH_CHECK(ctx);
-    wf_shade_kernel<T, NCH><<<grid, kMThreads, 0, ctx->stream>>>(q, m, w, v, now, prev);
+    wf_shade_kernel<T, NCH><<<grid, kMThreads, 0, ctx->stream>>>(q, m, w, v, thI[0], thI[1]);
     MG_LAUNCH_CHECK(ctx);
     wf_shadow_kernel<T, NCH><<<grid, kMThreads, 0, ctx->stream>>>(m, w, v);
     MG_LAUNCH_CHECK(ctx);
@@ -793,10 +885,12 @@ int mg_meshscene_sample_pair(mg_ctx* ctx, mg_mesh_scene* s, int32_t dtype, int32
   // the megakernel implements the configs[3] form (4 channels, 2 proportional
   // paths) and accumulates in planar order
   const bool mega = g_mesh_megakernel && s->nch == 4 && prop_paths == 2;
-  if (mega)
+  if (mega) {
+    s->last_now_slot = -1;  // the texel-copy reuse chain follows wavefront calls only
     st = megakernel_pair(ctx, s, q, dtype, target_img, now, prev, acc, np, loss_out);
-  else
+  } else {
     st = dispatch_wavefront(ctx, s, q, dtype, prop_paths, target_img, now, prev, tbl, loss_out);
+  }
   if (st) return st;
   if (!mega) {
     const long long cells = (long long)s->nobj * s->R * s->R;
@@ -851,6 +945,16 @@ int mg_meshscene_sample_pair_sharded(mg_ctx* ctx, mg_mesh_scene* s, int32_t dtyp
   tbl.shard = int(shard);
   tbl.ilv = 0;
   return dispatch_wavefront(ctx, s, q, dtype, prop_paths, target_img, now, prev, tbl, loss_out);
+}
+
+#ifndef MG_PREV_REUSE
+#define MG_PREV_REUSE 1  // 0: ignore the opt-in (A/B builds)
+#endif
+int mg_meshscene_set_prev_reuse(mg_mesh_scene* s, int32_t enable) {
+  if (!s) return fail(MG_EINVAL, "mg_meshscene_set_prev_reuse: null scene");
+  s->prev_reuse = MG_PREV_REUSE && enable != 0;
+  s->last_now_slot = -1;
+  return MG_OK;
 }
 
 // Converts one rank's fixed-point accumulator [2][n] into prop / diff (dtype)

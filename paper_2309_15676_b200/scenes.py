@@ -200,6 +200,9 @@ class HelixRun(QuadTextureRun):
         if optimizer == "meta":
             kw.setdefault("project_hi", 1.0)
         super().__init__(problem, optimizer, lr, seed, replicate, **kw)
+        # the loop ping-pongs its parameter buffers (prev at t+1 == now at t,
+        # untouched in between): the scene may reuse prev's texel-major copy
+        check(load().mg_meshscene_set_prev_reuse(problem.scene.h, 1))
 
 
 # ------------------------------------- F1 slice 3: textured mesh scene
@@ -490,3 +493,6 @@ class MeshTextureRun(QuadTextureRun):
         if optimizer == "meta":
             kw.setdefault("project_hi", 1.0)
         super().__init__(problem, optimizer, lr, seed, replicate, **kw)
+        # the loop ping-pongs its parameter buffers (prev at t+1 == now at t,
+        # untouched in between): the scene may reuse prev's texel-major copy
+        check(load().mg_meshscene_set_prev_reuse(problem.scene.h, 1))

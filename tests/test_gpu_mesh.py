@@ -163,6 +163,40 @@ def test_texture_optimisation_fits_the_image(api):
     assert last < 0.2 * first, (first, last)
 
 
+@pytest.mark.parametrize("channels,nprop", [(4, 2), (5, 4)])
+def test_prev_copy_reuse_is_bit_identical(api, channels, nprop):
+    """MeshTextureRun opts into mg_meshscene_set_prev_reuse (prev's
+    texel-major copy carried over from the previous iteration's now): the
+    trajectory equals one that rebuilds both copies every call, bit for bit,
+    and a tiled call sequence (same now/prev twice) stays correct."""
+    from paper_2309_15676_b200._lib import check, load
+
+    def traj(reuse):
+        prob = api.MeshTextureProblem(32, 24, 8, (8, 12), (10, 12), max_vertices=4,
+                                      target_spp=4, dtype=torch.float32, channels=channels,
+                                      prop_paths=nprop)
+        run = api.MeshTextureRun(prob, "meta", lr=0.01)
+        check(load().mg_meshscene_set_prev_reuse(prob.scene.h, int(reuse)))
+        out = []
+        for _ in range(5):
+            run.step()
+            out.append(run.params.clone())
+        # tiles after the loop: two calls on the same (now, prev)
+        a = prob.sample_pair(run.params, run.prev, 99, 5, rows=(0, 12))
+        b = prob.sample_pair(run.params, run.prev, 99, 5, rows=(12, 24))
+        full = prob.sample_pair(run.params, run.prev, 99, 5)
+        return out, (a.prop + b.prop, a.diff + b.diff), (full.prop, full.diff)
+
+    p1, tiles1, full1 = traj(True)
+    p0, tiles0, full0 = traj(False)
+    for x, y in zip(p1, p0):
+        assert torch.equal(x, y)
+    for x, y in zip(full1, full0):
+        assert torch.equal(x, y)
+    for x, y in zip(tiles1, full1):
+        torch.testing.assert_close(x, y, rtol=1e-5, atol=1e-6)
+
+
 # ------------------------------------------------------ configs[4] form
 @pytest.mark.parametrize("nprop,maxv", [(4, 5), (3, 8), (2, 3)])
 def test_metalness_sample_pair_bit_exact_vs_oracle(api, oracle, nprop, maxv):
