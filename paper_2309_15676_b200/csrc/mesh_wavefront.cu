@@ -44,6 +44,10 @@ struct WF {
   T *beta, *L, *E, *pendC;                    // [6][P]
   int *nv, *hslot, *q0, *q1, *sq;             // [P]
   int* vbase;                                 // [kMaxV][PS]
+  // [kMaxV][PS]: the vertex's NEE (vnee) / bounce (vbnc) fields are valid;
+  // invalid fields are never read (the scatter substitutes zeros), so they
+  // need not be written
+  unsigned char *vnee, *vbnc;
   T* vdat;                                    // [kMaxV][nvf][PS]
   unsigned int* cnt;                          // [2][kMaxV + 1]: queue / shadow counts
   int P, PS, npix, pix0, nprop, nvf;
@@ -54,7 +58,7 @@ template <class T>
 size_t wf_bytes(int npix, int nprop, int nvf) {
   const size_t P = size_t(npix) * (nprop + 1), PS = size_t(npix) * nprop;
   return sizeof(double) * 16 * P + sizeof(T) * 24 * P + sizeof(int) * 5 * P +
-         sizeof(int) * kMaxV * PS + sizeof(T) * kMaxV * nvf * PS +
+         sizeof(int) * kMaxV * PS + sizeof(T) * kMaxV * nvf * PS + 2 * kMaxV * PS +
          sizeof(unsigned int) * 2 * (kMaxV + 1) + 256 * 40;
 }
 
@@ -120,6 +124,8 @@ WF<T> wf_carve(void* mem, int npix, int nprop, int nvf) {
   int** ii[] = {&w.nv, &w.hslot, &w.q0, &w.q1, &w.sq};
   for (int** i : ii) *i = (int*)take(sizeof(int) * Pz);
   w.vbase = (int*)take(sizeof(int) * kMaxV * size_t(w.PS));
+  w.vnee = (unsigned char*)take(kMaxV * size_t(w.PS));
+  w.vbnc = (unsigned char*)take(kMaxV * size_t(w.PS));
   w.vdat = (T*)take(sizeof(T) * kMaxV * size_t(nvf) * size_t(w.PS));
   w.cnt = (unsigned int*)take(sizeof(unsigned int) * 2 * (kMaxV + 1));
   return w;
@@ -217,35 +223,12 @@ __global__ void __launch_bounds__(kMThreads)
       // parameter sets evaluated: path 0 (A) and the FD path at theta_t and
       // theta_{t-1}; the other proportional paths at theta_t only
       const int ns = (k == 0 || k == w.nprop) ? 2 : 1;
-      // every stored field of vertex v is written exactly once below
-      auto zero_nee = [&](int s) {
-#pragma unroll
-        for (int c = 0; c < 3; ++c) {
-          vf(w, v, F::A + s * 3 + c, p) = T(0);
-          vf(w, v, F::C + s * 3 + c, p) = T(0);
-        }
-        if constexpr (NCH == 5) {
-#pragma unroll
-          for (int j = 0; j < 9; ++j) vf(w, v, VF<5>::dfn + s * 9 + j, p) = T(0);
-        } else {
-          vf(w, v, VF<4>::dSn + s, p) = T(0);
-        }
-      };
-      auto zero_bounce = [&](int s) {
-#pragma unroll
-        for (int c = 0; c < 3; ++c) vf(w, v, F::invfb + s * 3 + c, p) = T(0);
-        if constexpr (NCH == 5) {
-#pragma unroll
-          for (int j = 0; j < 9; ++j) vf(w, v, VF<5>::dfb + s * 9 + j, p) = T(0);
-        } else {
-          vf(w, v, VF<4>::dSb + s, p) = T(0);
-        }
-      };
       T beta[2][3];
 #pragma unroll
       for (int s = 0; s < 2; ++s)
 #pragma unroll
-        for (int c = 0; c < 3; ++c) beta[s][c] = w.beta[size_t(s * 3 + c) * w.P + p];
+        for (int c = 0; c < 3; ++c)
+          beta[s][c] = s < ns ? w.beta[size_t(s * 3 + c) * w.P + p] : T(0);
       if (slot < 0) {  // escaped: environment
 #pragma unroll
         for (int s = 0; s < 2; ++s)
@@ -436,11 +419,10 @@ __global__ void __launch_bounds__(kMThreads)
             want_bounce = true;
           }
         }
-        if (store)
-          for (int s = 0; s < ns; ++s) {
-            if (!nee_done) zero_nee(s);
-            if (!bounce_done) zero_bounce(s);
-          }
+        if (store) {
+          w.vnee[size_t(v) * w.PS + p] = nee_done;
+          w.vbnc[size_t(v) * w.PS + p] = bounce_done;
+        }
       }
     }
     const int qs = enqueue(want_shadow, &w.cnt[kMaxV + 1 + v]);
@@ -452,7 +434,6 @@ __global__ void __launch_bounds__(kMThreads)
 
 template <class T, int NCH>
 __global__ void __launch_bounds__(kMThreads, 8) wf_shadow_kernel(MeshDev m, WF<T> w, int v) {
-  using F = VF<NCH>;
   MESH_SMEM;
   const int n = int(w.cnt[kMaxV + 1 + v]);
   for (int i = blockIdx.x * kMThreads + threadIdx.x; i < n; i += gridDim.x * kMThreads) {
@@ -464,17 +445,7 @@ __global__ void __launch_bounds__(kMThreads, 8) wf_shadow_kernel(MeshDev m, WF<T
       const int nj = (k == 0 || k == w.nprop) ? 6 : 3;
       for (int j = 0; j < nj; ++j) w.L[size_t(j) * w.P + p] += w.pendC[size_t(j) * w.P + p];
     } else if (p < w.PS) {  // occluded: no NEE data at this vertex
-#pragma unroll
-      for (int j = 0; j < 6; ++j) {
-        vf(w, v, F::A + j, p) = T(0);
-        vf(w, v, F::C + j, p) = T(0);
-      }
-      if constexpr (NCH == 5) {
-        for (int j = 0; j < 18; ++j) vf(w, v, VF<5>::dfn + j, p) = T(0);
-      } else {
-        vf(w, v, VF<4>::dSn, p) = T(0);
-        vf(w, v, VF<4>::dSn + 1, p) = T(0);
-      }
+      w.vnee[size_t(v) * w.PS + p] = 0;
     }
   }
 }
@@ -526,22 +497,26 @@ struct AccCell {
 //   g[c] = wt[c] X[c][0],  g[3] = sum_c wt[c] X[c][1],  g[4] = sum_c wt[c] X[c][2].
 template <class T, int NCH>
 __device__ __forceinline__ void vertex_terms(const WF<T>& w, int v, int p, int s, const T Q[3],
-                                             T X[3][NCH - 2]) {
+                                             bool ne, bool bn, T X[3][NCH - 2]) {
   using F = VF<NCH>;
+  // fields of an absent NEE / bounce event read as +0 (what the megakernel
+  // and the oracle store for them)
+  auto fn = [&](int f) { return ne ? vf(w, v, f, p) : T(0); };
+  auto fbn = [&](int f) { return bn ? vf(w, v, f, p) : T(0); };
   if constexpr (NCH == 5) {
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
-      const T A = vf(w, v, F::A + s * 3 + c, p), fb = vf(w, v, F::invfb + s * 3 + c, p);
+      const T A = fn(F::A + s * 3 + c), fb = fbn(F::invfb + s * 3 + c);
       const int dn = F::dfn + s * 9 + c * 3, db = F::dfb + s * 9 + c * 3;
-      X[c][0] = A * vf(w, v, dn, p) + Q[c] * (fb * vf(w, v, db, p));
-      X[c][2] = A * vf(w, v, dn + 1, p) + Q[c] * (fb * vf(w, v, db + 1, p));
-      X[c][1] = A * vf(w, v, dn + 2, p) + Q[c] * (fb * vf(w, v, db + 2, p));
+      X[c][0] = A * fn(dn) + Q[c] * (fb * fbn(db));
+      X[c][2] = A * fn(dn + 1) + Q[c] * (fb * fbn(db + 1));
+      X[c][1] = A * fn(dn + 2) + Q[c] * (fb * fbn(db + 2));
     }
   } else {
-    const T dSn = vf(w, v, F::dSn + s, p), dSb = vf(w, v, F::dSb + s, p);
+    const T dSn = fn(F::dSn + s), dSb = fbn(F::dSb + s);
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
-      const T A = vf(w, v, F::A + s * 3 + c, p), ifb = vf(w, v, F::invfb + s * 3 + c, p);
+      const T A = fn(F::A + s * 3 + c), ifb = fbn(F::invfb + s * 3 + c);
       X[c][0] = (A / T(kPiM)) + Q[c] * (ifb / T(kPiM));
       X[c][1] = A * dSn + Q[c] * (ifb * dSb);
     }
@@ -571,13 +546,14 @@ __device__ __noinline__ void wf_scatter(const WF<T>& w, int p, const T wt[3], in
   for (int c = 0; c < 3; ++c) Q[c] = w.E[size_t(c) * w.P + p];
   for (int v = w.nv[p] - 1; v >= 0; --v) {
     const AccCell<NCH, ILV> cell(acc, w.vbase[size_t(v) * w.PS + p], R2);
+    const bool ne = w.vnee[size_t(v) * w.PS + p], bn = w.vbnc[size_t(v) * w.PS + p];
     T X[3][NCH - 2], g[NCH];
-    vertex_terms<T, NCH>(w, v, p, 0, Q, X);
+    vertex_terms<T, NCH>(w, v, p, 0, Q, ne, bn, X);
     combine<T, NCH>(X, wt, g);
 #pragma unroll
     for (int k = 0; k < NCH; ++k) atomicAdd(cell.at(acc, 0, k), fixq(double(g[k])));
 #pragma unroll
-    for (int c = 0; c < 3; ++c) Q[c] = Q[c] + vf(w, v, F::C + c, p);
+    for (int c = 0; c < 3; ++c) Q[c] = Q[c] + (ne ? vf(w, v, F::C + c, p) : T(0));
   }
 }
 
@@ -597,23 +573,24 @@ __device__ __noinline__ void wf_scatter_a(const WF<T>& w, int p, const T wt[3], 
   }
   for (int v = w.nv[p] - 1; v >= 0; --v) {
     const AccCell<NCH, ILV> cell(acc, w.vbase[size_t(v) * w.PS + p], R2);
+    const bool ne = w.vnee[size_t(v) * w.PS + p], bn = w.vbnc[size_t(v) * w.PS + p];
     T X[3][NCH - 2], g[NCH];
     unsigned long long d[NCH];
-    vertex_terms<T, NCH>(w, v, p, 0, Q0, X);
+    vertex_terms<T, NCH>(w, v, p, 0, Q0, ne, bn, X);
     combine<T, NCH>(X, wt, g);
 #pragma unroll
     for (int k = 0; k < NCH; ++k) atomicAdd(cell.at(acc, 0, k), fixq(double(g[k])));
     combine<T, NCH>(X, wC0, g);
 #pragma unroll
     for (int k = 0; k < NCH; ++k) d[k] = fixq(double(g[k]));
-    vertex_terms<T, NCH>(w, v, p, 1, Q1, X);
+    vertex_terms<T, NCH>(w, v, p, 1, Q1, ne, bn, X);
     combine<T, NCH>(X, wC1, g);
 #pragma unroll
     for (int k = 0; k < NCH; ++k) atomicAdd(cell.at(acc, 1, k), d[k] + fixq(double(g[k])));
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
-      Q0[c] = Q0[c] + vf(w, v, F::C + c, p);
-      Q1[c] = Q1[c] + vf(w, v, F::C + 3 + c, p);
+      Q0[c] = Q0[c] + (ne ? vf(w, v, F::C + c, p) : T(0));
+      Q1[c] = Q1[c] + (ne ? vf(w, v, F::C + 3 + c, p) : T(0));
     }
   }
 }
