@@ -468,14 +468,36 @@ def extras(args, ctx):
 
     def quad():
         # F1 slice, configs[0]: 64x64 textured quad, 32x32 RGB texture, 1 FD +
-        # 2 proportional spp; and a 1024^2 / 512^2-texture variant
+        # 2 proportional spp; and a 1024^2 / 512^2-texture variant.  A context
+        # on its own stream, so the loop can also run as a CUDA graph.
+        qs = torch.cuda.Stream(device=dev)
+        qctx = api.Context(ctx.device, stream=qs)
+
+        def qtimed(fn, iters):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            torch.cuda.synchronize()
+            a.record(qs)
+            fn(iters)
+            b.record(qs)
+            torch.cuda.synchronize()
+            return a.elapsed_time(b) / iters
+
         for W, R, iters in ((64, 32, 200), (1024, 512, 50)):
-            prob = api.QuadTextureProblem(W, W, R, target_spp=64, dtype=torch.float32, ctx=ctx)
-            run = api.QuadTextureRun(prob, optimizer="meta", lr=0.01)
-            ms = timed(run.step, iters, warm=3)
+            with torch.cuda.stream(qs):
+                prob = api.QuadTextureProblem(W, W, R, target_spp=64, dtype=torch.float32,
+                                              ctx=qctx)
+                run = api.QuadTextureRun(prob, optimizer="meta", lr=0.01)
+                run.run(3)
+                ms = qtimed(run.run, iters)
+                # the same loop as one captured two-step CUDA graph, replayed
+                # (device iteration counter and Moment2 coefficient;
+                # bit-identical to the eager loop, tests/test_gpu_quad.py)
+                run.run(2, graph=True)
+                ms_g = qtimed(lambda k: run.run(k, graph=True), iters)
             out[f"quad_texture_{W}px_{R}tex_f32"] = {
                 "iterations": iters, "ms_per_iteration": ms, "iterations_per_s": 1e3 / ms,
                 "path_samples_per_s": prob.draws_per_sample() / (ms / 1e3),
+                "graph_ms_per_iteration": ms_g, "graph_iterations_per_s": 1e3 / ms_g,
                 "texture_params": prob.dim()}
 
     def helix():

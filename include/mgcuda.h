@@ -112,6 +112,13 @@ int mg_ctx_create(int device, void* stream, mg_ctx** out);
 int mg_ctx_destroy(mg_ctx* ctx);
 int mg_ctx_synchronize(mg_ctx* ctx);
 void* mg_ctx_stream(mg_ctx* ctx);
+/* Device-side iteration index for graph-replayable optimisation loops: while
+ * set (non-NULL), the quad and helix sample-pair kernels launched on ctx use
+ * iteration + *dev_counter as their Philox iteration counter, and
+ * mg_iteration_offset_add (a one-thread kernel on ctx's stream) advances it,
+ * so a captured block of iterations replays with fresh random numbers. */
+int mg_ctx_set_iteration_offset(mg_ctx* ctx, const uint32_t* dev_counter);
+int mg_iteration_offset_add(mg_ctx* ctx, uint32_t* dev_counter, uint32_t inc);
 /* Number of kernels this context has launched so far (bench gpu_launches). */
 int64_t mg_ctx_launch_count(mg_ctx* ctx);
 
@@ -253,7 +260,9 @@ typedef struct mg_update_scalars {
   int64_t diff_count;
   /* What step t consumed, for recording (harness.cpp:174). */
   double ssn_used;
-  double reserved;
+  /* beta_f^t of Moment2(beta_f) (moment2.hpp:35), advanced on the device by
+   * every launch whose args carry beta_f > 0; read when prop_coef_device. */
+  double prop_decay_pow;
 } mg_update_scalars;
 
 typedef struct mg_meta_update_args {
@@ -268,6 +277,12 @@ typedef struct mg_meta_update_args {
   double proj_lo;
   double ssn_host;
   double proj_hi;
+  double beta_f;            /* > 0: advance scalars->prop_decay_pow *= beta_f on the device */
+  int32_t prop_coef_device; /* 1: Moment2(beta_f) coefficient (1-beta_f)/(1-prop_decay_pow)
+                               from the device power instead of prop_coef — steps that
+                               carry no per-step host scalar, so one captured CUDA graph
+                               can be replayed (same bits: same IEEE multiply chain) */
+  int32_t pad_;
 } mg_meta_update_args;
 
 /* Optional side inputs/outputs of the fused update.  Any may be NULL. */

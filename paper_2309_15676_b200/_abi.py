@@ -59,14 +59,15 @@ class AdamScalars(C.Structure):
 class UpdateScalars(C.Structure):
     _fields_ = [("ssn", C.c_double), ("changed", C.c_double), ("loss", C.c_double),
                 ("nonfinite", C.c_double), ("diff_decay_pow", C.c_double),
-                ("diff_count", C.c_int64), ("ssn_used", C.c_double), ("reserved", C.c_double)]
+                ("diff_count", C.c_int64), ("ssn_used", C.c_double), ("prop_decay_pow", C.c_double)]
 
 
 class MetaUpdateArgs(C.Structure):
     _fields_ = [("meta", MetaParams), ("prop_coef", C.c_double), ("beta_delta", C.c_double),
                 ("first_step", C.c_int32), ("diff_norm", C.c_int32), ("project", C.c_int32),
                 ("ssn_from_host", C.c_int32), ("proj_lo", C.c_double), ("ssn_host", C.c_double),
-                ("proj_hi", C.c_double)]
+                ("proj_hi", C.c_double), ("beta_f", C.c_double), ("prop_coef_device", C.c_int32),
+                ("pad_", C.c_int32)]
 
 
 class MetaExtras(C.Structure):
@@ -96,7 +97,7 @@ class RunSeriesC(C.Structure):
 def fresh_scalars():
     """Initial mg_update_scalars of a run: no step taken, diff EMA empty."""
     return UpdateScalars(ssn=0.0, changed=0.0, loss=float("nan"), nonfinite=0.0,
-                         diff_decay_pow=1.0, diff_count=0, ssn_used=0.0, reserved=0.0)
+                         diff_decay_pow=1.0, diff_count=0, ssn_used=0.0, prop_decay_pow=1.0)
 
 
 def config_from(**kw):

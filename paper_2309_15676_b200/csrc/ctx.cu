@@ -34,6 +34,10 @@ __global__ void fill_kernel(int64_t n, T* dst, T v) {
 }
 }  // namespace
 
+namespace mg {
+__global__ void counter_add_kernel(uint32_t* c, uint32_t inc) { *c += inc; }
+}  // namespace mg
+
 extern "C" {
 
 int mg_fill(mg_ctx* ctx, int32_t dtype, int64_t n, void* dst, double value) {
@@ -180,6 +184,19 @@ int mg_ctx_synchronize(mg_ctx* ctx) {
 }
 
 void* mg_ctx_stream(mg_ctx* ctx) { return ctx ? static_cast<void*>(ctx->stream) : nullptr; }
+
+int mg_ctx_set_iteration_offset(mg_ctx* ctx, const uint32_t* dev_counter) {
+  if (!ctx) return fail(MG_EINVAL, "mg_ctx_set_iteration_offset: null context");
+  ctx->it_offset = dev_counter;
+  return MG_OK;
+}
+
+int mg_iteration_offset_add(mg_ctx* ctx, uint32_t* dev_counter, uint32_t inc) {
+  if (!ctx || !dev_counter) return fail(MG_EINVAL, "mg_iteration_offset_add: null argument");
+  mg::counter_add_kernel<<<1, 1, 0, ctx->stream>>>(dev_counter, inc);
+  MG_LAUNCH_CHECK(ctx);
+  return MG_OK;
+}
 
 int64_t mg_ctx_launch_count(mg_ctx* ctx) { return ctx ? ctx->launches : 0; }
 

@@ -39,6 +39,7 @@ struct HelixK {
   double Le[3], env[3], ground[3];
   uint64_t key;
   uint32_t iteration;
+  const uint32_t* it_offset;  // device iteration offset or null (mg_ctx_set_iteration_offset)
 };
 
 template <class T>
@@ -382,6 +383,7 @@ __global__ void __launch_bounds__(kHThreads)
                       unsigned int* counter, double* loss_out) {
   __shared__ T sph[4 * kMaxSph];
   __shared__ long long red[kHThreads / 32][2 * kNP];
+  if (q.it_offset) q.iteration += __ldg(q.it_offset);
   T th[2][kNP];
   load_scene<T>(q, sph_g, now, prev, sph, th);
   const int npix = q.W * q.H;
@@ -475,6 +477,7 @@ HelixK make_helix(int W, int H, int nsph, const double* Le, const double* env, c
   }
   q.key = key;
   q.iteration = it;
+  q.it_offset = nullptr;
   return q;
 }
 
@@ -521,6 +524,7 @@ int mg_helix_sample_pair(mg_ctx* ctx, int32_t dtype, int32_t W, int32_t H, int32
   HelixK q = make_helix(W, H, nsph, Le, env, ground, key, iteration);
   q.row0 = row0;
   q.row1 = row1;
+  q.it_offset = ctx->it_offset;
   const int grid = grid_for(ctx, int64_t(W) * (row1 - row0) + 1, kHThreads, 8);
   if (dtype == MG_F64) {
     helix_pair_kernel<double><<<grid, kHThreads, 0, ctx->stream>>>(

@@ -13,7 +13,9 @@ namespace mg {
 
 struct MetaK {
   double lr, eps_step, eps_alpha, prop_coef, beta_delta, proj_lo, ssn_host, proj_hi;
+  double beta_f = 0.0;  // > 0: advance the device beta_f power
   int clip, diff_norm, project, ssn_from_host;
+  int prop_dev = 0;     // 1: prop coefficient from the device power
 };
 
 template <class T>
@@ -37,7 +39,7 @@ struct MetaPtrs {
 // Per-launch scalar state, identical in every thread (read once from the
 // device scalars written by the previous launch's epilogue).
 struct StepScal {
-  double ssn, norm, c_diff, dpow;
+  double ssn, norm, c_diff, dpow, ppow, c_prop;
   int64_t cnt0, cnt;
   bool active;
 };
@@ -55,6 +57,11 @@ __device__ __forceinline__ StepScal load_step_scalars(const MetaK& k, const mg_u
   }
   s.c_diff = (1.0 - k.beta_delta) / (1.0 - s.dpow);  // moment2.hpp:36-38
   s.norm = sqrt(s.ssn);                           // harness.cpp:154
+  // Moment2(beta_f): the host passes (1-b)/(1-b^t) computed by the repeated
+  // multiply of moment2.hpp:35, or the device forms the same chain
+  s.ppow = __ldcg(&sc->prop_decay_pow);
+  if (k.beta_f > 0.0) s.ppow = s.ppow * k.beta_f;
+  s.c_prop = k.prop_dev ? (1.0 - k.beta_f) / (1.0 - s.ppow) : k.prop_coef;
   return s;
 }
 
@@ -99,7 +106,7 @@ __device__ __forceinline__ void meta_elem(const MetaK& k, const StepScal& s, T p
                                           T& pout, T& delta, Acc& acc) {
   // Moment2(beta_f).step(prop): m2 += (w/w_sum) * (x^2 - m2)
   const T m2p_old = FIRST ? T(0) : m2p;
-  const T cp = T(k.prop_coef);
+  const T cp = T(s.c_prop);
   m2p = m2p_old + cp * (vprop * vprop - m2p_old);
   // decoupled diff variance (global or per-param norm)
   T m2d_v = s.cnt0 > 0 ? m2d : T(0);

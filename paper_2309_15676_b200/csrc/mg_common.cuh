@@ -64,6 +64,9 @@ struct mg_ctx {
   mg::ReducePartials* partials = nullptr;  // [kMaxReduceBlocks]
   unsigned int* counter = nullptr;         // arrival counter (self-resetting)
   int* flag = nullptr;                     // error flag for validation kernels
+  // device iteration offset (mg_ctx_set_iteration_offset): sample-pair
+  // kernels launched on this context use iteration + *it_offset
+  const uint32_t* it_offset = nullptr;
 };
 
 namespace mg {

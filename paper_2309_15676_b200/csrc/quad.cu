@@ -32,6 +32,7 @@ struct QuadK {
   double Le[3];
   uint64_t key;
   uint32_t iteration, stream;
+  const uint32_t* it_offset;  // device iteration offset or null (mg_ctx_set_iteration_offset)
 };
 
 __device__ __forceinline__ void quad_uniforms(uint64_t key, uint32_t pix, uint32_t it, uint32_t sid,
@@ -97,6 +98,7 @@ __global__ void __launch_bounds__(kQThreads)
                      const T* __restrict__ prev, unsigned long long* __restrict__ acc_g,
                      ReducePartials* partials, unsigned int* counter, double* loss_out) {
   extern __shared__ unsigned long long acc_s[];
+  if (q.it_offset) q.iteration += __ldg(q.it_offset);
   const int npix = q.W * q.H;
   const int T_ = q.R * q.R;
   const int pix0 = q.row0 * q.W, pix1 = q.row1 * q.W;
@@ -167,6 +169,7 @@ QuadK make_quad(int W, int H, int R, const double* Le, uint64_t key, uint32_t it
   q.key = key;
   q.iteration = it;
   q.stream = st;
+  q.it_offset = nullptr;
   return q;
 }
 
@@ -207,6 +210,7 @@ int mg_quad_sample_pair(mg_ctx* ctx, int32_t dtype, int32_t W, int32_t H, int32_
   QuadK q = make_quad(W, H, R, Le, key, iteration, stream);
   q.row0 = row0;
   q.row1 = row1;
+  q.it_offset = ctx->it_offset;
   const int T_ = R * R;
   const size_t smem = sizeof(unsigned long long) * 6 * size_t(T_);
   const bool shared = smem <= 96 * 1024;

@@ -172,6 +172,7 @@ __global__ void __launch_bounds__(kThreads, sizeof(T) == 4 ? 3 : 2)
     sc->nonfinite = t.nonfinite;
     sc->diff_count = s.cnt;
     sc->diff_decay_pow = s.dpow;
+    sc->prop_decay_pow = s.ppow;
     sc->ssn_used = s.ssn;
   });
 }
@@ -229,6 +230,8 @@ extern "C" int mg_minirender_meta_iteration(mg_ctx* ctx, int32_t dtype, int64_t 
   k.meta.eps_alpha = a->update.meta.eps_alpha;
   k.meta.clip = a->update.meta.clip_enabled;
   k.meta.prop_coef = a->update.prop_coef;
+  k.meta.beta_f = a->update.beta_f;
+  k.meta.prop_dev = a->update.prop_coef_device;
   k.meta.beta_delta = a->update.beta_delta;
   k.meta.diff_norm = MG_DIFF_NORM_GLOBAL;
   k.meta.project = 1;  // problems.cpp:228: params = params.max(0.0)

@@ -114,6 +114,7 @@ __global__ void __launch_bounds__(kThreads)
     sc->nonfinite = t.nonfinite;
     sc->diff_count = s.cnt;
     sc->diff_decay_pow = s.dpow;
+    sc->prop_decay_pow = s.ppow;
     sc->ssn_used = s.ssn;
   });
 }
@@ -262,6 +263,7 @@ __global__ void __launch_bounds__(kTmaThreads, kMinBlocks)
     sc->nonfinite = t.nonfinite;
     sc->diff_count = s.cnt;
     sc->diff_decay_pow = s.dpow;
+    sc->prop_decay_pow = s.ppow;
     sc->ssn_used = s.ssn;
   });
 }
@@ -323,6 +325,7 @@ __global__ void __launch_bounds__(kThreads)
     sc->nonfinite = t.nonfinite;
     sc->diff_count = s.cnt;
     sc->diff_decay_pow = s.dpow;
+    sc->prop_decay_pow = s.ppow;
     sc->ssn_used = s.ssn;
   });
 }
@@ -679,6 +682,8 @@ MetaK make_meta_k(const mg_meta_update_args* a) {
   k.eps_alpha = a->meta.eps_alpha;
   k.clip = a->meta.clip_enabled;
   k.prop_coef = a->prop_coef;
+  k.beta_f = a->beta_f;
+  k.prop_dev = a->prop_coef_device;
   k.beta_delta = a->beta_delta;
   k.diff_norm = a->diff_norm;
   k.project = a->project;

@@ -144,13 +144,17 @@ class FusedMetaUpdate:
                  beta_delta: float = 0.5, eps_step: float = 1e-8, eps_alpha: float = 1e-30,
                  clip: bool = True, project_lo: Optional[float] = None,
                  diff_norm: str = "global", ctx=None, device="cuda",
-                 project_hi: Optional[float] = None):
+                 project_hi: Optional[float] = None, device_coef: bool = False):
         self.ctx = ctx or Context.default()
         self.n, self.dtype = n, dtype
         self.beta_f, self.beta_delta = beta_f, beta_delta
         self.meta = _abi.MetaParams(lr, eps_step, eps_alpha, int(clip))
         self.project_lo, self.project_hi = project_lo, project_hi
         self.diff_norm = _abi.DIFF_NORMS[diff_norm]
+        # device_coef: the Moment2(beta_f) coefficient of steps after the
+        # first is formed on the device (mg_meta_update_args.prop_coef_device),
+        # so a captured step is replayable
+        self.device_coef = device_coef
         mk = lambda: torch.empty(n, dtype=dtype, device=device)  # noqa: E731
         self.m2_prop, self.m2_diff, self.mean, self.var, self.alpha_prev = (mk() for _ in range(5))
         self.scalars_buf = torch.zeros(C.sizeof(_abi.UpdateScalars) // 8, dtype=torch.float64,
@@ -180,7 +184,8 @@ class FusedMetaUpdate:
             ssn_from_host=int(ssn_host is not None),
             proj_lo=0.0 if self.project_lo is None else self.project_lo,
             ssn_host=0.0 if ssn_host is None else ssn_host,
-            proj_hi=0.0 if self.project_hi is None else self.project_hi)
+            proj_hi=0.0 if self.project_hi is None else self.project_hi,
+            beta_f=self.beta_f, prop_coef_device=int(self.device_coef and self.t > 1))
 
     def step(self, prop, diff, params_in, params_out, target=None, vprop=None, vdiff=None,
              params_prev=None, delta_out=None, ssn_host=None):

@@ -30,6 +30,7 @@ class QuadTextureProblem:
     image is a target_spp-sample render of the target texture."""
 
     STREAM_TARGET = 7
+    ITERATION_OFFSET = True  # the sampler honours mg_ctx_set_iteration_offset
 
     def __init__(self, width: int = 64, height: int = 64, tex_res: int = 32,
                  light=(8.0, 7.0, 6.0), init_seed: int = 0, target_seed: int = 1,
@@ -116,6 +117,75 @@ class QuadTextureRun:
         self.t += 1
         return pair
 
+    def _step_at(self, iteration: int):
+        pair = self.p.sample_pair(self.params, self.prev if self.optimizer == "meta" else
+                                  self.params, iteration, self.key)
+        new = self.prev
+        if self.optimizer == "meta":
+            self.upd.step(pair.prop, pair.diff, self.params, new)
+        else:
+            self.upd.step(pair.prop, self.params, new)
+        self.prev, self.params = self.params, new
+
+    def run(self, iterations: int, graph: bool = False):
+        """`iterations` steps.  graph=True (meta optimiser): after the first
+        (eager) step, a block of two steps — one ping-pong period — is
+        captured once as a CUDA graph and replayed.  Nothing in a captured
+        step comes from the host: the Philox iteration index is a device
+        counter (mg_ctx_set_iteration_offset, advanced by the graph's last
+        node) and the Moment2(beta_f) coefficient is formed on the device
+        (prop_coef_device), so the replayed steps are the eager steps bit for
+        bit.  Needs problem.ctx on a capturable (non-default) stream."""
+        if not graph:
+            for _ in range(iterations):
+                self.step()
+            return
+        if self.optimizer != "meta":
+            raise InvalidArgument(_abi.MG_EINVAL, "graph runs need the meta optimiser")
+        if not getattr(self.p, "ITERATION_OFFSET", False):
+            raise InvalidArgument(_abi.MG_EINVAL, "this problem's sampler has no device "
+                                  "iteration offset; graph runs are unavailable")
+        ctx = self.p.ctx
+        if ctx.stream.cuda_stream == 0:
+            raise InvalidArgument(_abi.MG_EINVAL, "graph runs need a context on a non-default stream")
+        done = 0
+        while self.t < 1 and done < iterations:  # the first step initialises the state
+            self.step()
+            done += 1
+        left = iterations - done
+        if left >= 2:
+            g = getattr(self, "_graph", None)
+            if g is None:
+                g = self._capture()
+            with torch.cuda.stream(ctx.stream):
+                self._it_dev.fill_(self.t)
+            for _ in range(left // 2):
+                g.replay()
+                for _ in range(2):  # the host mirror of what the replay advanced
+                    self.upd.t += 1
+                    self.upd.beta_f_pow *= self.upd.beta_f
+                self.t += 2
+        if left % 2:
+            self.step()
+
+    def _capture(self):
+        ctx, L = self.p.ctx, load()
+        self._it_dev = torch.zeros(1, dtype=torch.int32, device="cuda")
+        saved = (self.upd.t, self.upd.beta_f_pow, self.upd.device_coef)
+        self.upd.device_coef = True
+        g = torch.cuda.CUDAGraph()
+        check(L.mg_ctx_set_iteration_offset(ctx.h, _p(self._it_dev)))
+        try:
+            with torch.cuda.graph(g, stream=ctx.stream):
+                self._step_at(0)
+                self._step_at(1)
+                check(L.mg_iteration_offset_add(ctx.h, _p(self._it_dev), 2))
+        finally:
+            check(L.mg_ctx_set_iteration_offset(ctx.h, None))
+            self.upd.t, self.upd.beta_f_pow, _ = saved
+        self._graph = g
+        return g
+
     def loss_estimate(self) -> float:
         return float(self.p.loss_buf[0])
 
@@ -143,6 +213,8 @@ class HelixProblem:
     metalness, roughness), initialised U(0,1) from seed 0 against seeded
     target values (seed 1).  Own renderer (oracle
     mgo_helix_*)."""
+
+    ITERATION_OFFSET = True  # the sampler honours mg_ctx_set_iteration_offset
 
     def __init__(self, width: int = 256, height: int = 256, light=(10.0, 10.0, 10.0),
                  env=(0.2, 0.2, 0.2), ground=(0.5, 0.5, 0.5), init_seed: int = 0,
@@ -200,9 +272,6 @@ class HelixRun(QuadTextureRun):
         if optimizer == "meta":
             kw.setdefault("project_hi", 1.0)
         super().__init__(problem, optimizer, lr, seed, replicate, **kw)
-        # the loop ping-pongs its parameter buffers (prev at t+1 == now at t,
-        # untouched in between): the scene may reuse prev's texel-major copy
-        check(load().mg_meshscene_set_prev_reuse(problem.scene.h, 1))
 
 
 # ------------------------------------- F1 slice 3: textured mesh scene

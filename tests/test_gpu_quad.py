@@ -151,3 +151,38 @@ def test_tile_sharded_gradients_sum_exactly(api, tiles):
         sp += part.prop
         sd += part.diff
     assert torch.equal(sp, full[0]) and torch.equal(sd, full[1])
+
+
+@pytest.mark.parametrize("kind,dtype", [("quad", torch.float32), ("quad", torch.float64),
+                                        ("helix", torch.float32)])
+def test_graph_replayed_run_is_bit_identical(api, kind, dtype):
+    """run(k, graph=True) replays one captured two-step block (device
+    iteration counter, device Moment2 coefficient): the parameters, the
+    optimiser state and the loss equal the eager loop's bit for bit, over
+    an odd count (the last step eager) and a second run() call."""
+    side = torch.cuda.Stream()
+    ctx = api.Context(0, stream=side)
+
+    def make():
+        if kind == "quad":
+            prob = api.QuadTextureProblem(32, 32, 8, target_spp=16, dtype=dtype, ctx=ctx)
+            return prob, api.QuadTextureRun(prob, optimizer="meta", lr=0.01)
+        prob = api.HelixProblem(32, 24, target_spp=4, dtype=dtype, ctx=ctx)
+        return prob, api.HelixRun(prob, optimizer="meta", lr=0.01)
+
+    with torch.cuda.stream(side):
+        pe, re_ = make()
+        re_.run(13)
+        re_.run(6)
+        pg, rg = make()
+        rg.run(13, graph=True)
+        rg.run(6, graph=True)
+        torch.cuda.synchronize()
+    assert re_.t == rg.t == 19
+    assert torch.equal(re_.params, rg.params) and torch.equal(re_.prev, rg.prev)
+    for a in ("m2_prop", "m2_diff", "mean", "var", "alpha_prev"):
+        assert torch.equal(getattr(re_.upd, a), getattr(rg.upd, a)), a
+    assert pe.loss_buf.item() == pg.loss_buf.item()
+    se, sg = re_.upd.scalars(), rg.upd.scalars()
+    assert (se.ssn, se.diff_count, se.prop_decay_pow) == (sg.ssn, sg.diff_count, sg.prop_decay_pow)
+    assert se.prop_decay_pow == re_.upd.beta_f_pow  # device chain == host chain
