@@ -15,8 +15,8 @@ for r in rows[hi + 1:]:
     d[r[h.index("Metric Name")]] = float(r[h.index("Metric Value")].replace(",", ""))
 launches = list(L.values())
 gen = [i for i, x in enumerate(launches) if "wf_gen" in x["k"]]
-if gen[-1] >= 2 and "tex_ilv" in launches[gen[-1] - 2]["k"]:
-    gen[-1] -= 2
+while gen[-1] >= 1 and "tex_ilv" in launches[gen[-1] - 1]["k"]:
+    gen[-1] -= 1
 last = launches[gen[-1]:]
 
 

@@ -9,7 +9,7 @@ mkdir -p gpurun_out
 CMD="python tools/mesh_large_probe.py"
 timeout 600 $CMD > gpurun_out/pm_plain.log 2>&1 || { echo "plain run failed"; cat gpurun_out/pm_plain.log; exit 1; }
 M=gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,smsp__issue_active.avg.pct_of_peak_sustained_active,smsp__thread_inst_executed_per_inst_executed.ratio,sm__warps_active.avg.pct_of_peak_sustained_active,lts__t_bytes.sum
-timeout 1200 ncu --metrics $M --clock-control none --csv -k regex:'wf_|mesh_|meta_update|fixed' \
+timeout 1200 ncu --metrics $M --clock-control none --csv -k regex:'wf_|mesh_|meta_update|fixed|tex_ilv' \
   --log-file gpurun_out/pm_launches.csv $CMD > gpurun_out/pm_ncu_launch.log 2>&1
 for k in wf_isect:17 wf_shade:17 wf_shadow:17 wf_scatter:2 mesh_finalize:2; do
   name=${k%%:*}; skip=${k##*:}
