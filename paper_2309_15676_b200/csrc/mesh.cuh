@@ -293,9 +293,15 @@ __device__ __noinline__ int trace(const MeshDev& m, const float4* sn, const doub
 // affected pixels is measured (tests/test_gpu_mesh.py) and reported.
 constexpr float kTMin32 = 1e-5f;
 
-__device__ __forceinline__ bool tri_hit32(const float4* __restrict__ r, const float o[3],
-                                          const float d[3], float& t, float& u, float& v) {
-  const float4 a = __ldg(r), b = __ldg(r + 1), c = __ldg(r + 2);
+struct Tri32 {
+  float4 a, b, c;
+};
+__device__ __forceinline__ Tri32 load_tri32(const float4* __restrict__ r) {
+  return Tri32{__ldg(r), __ldg(r + 1), __ldg(r + 2)};
+}
+__device__ __forceinline__ bool tri_test32(const Tri32& T, const float o[3], const float d[3],
+                                           float& t, float& u, float& v) {
+  const float4 a = T.a, b = T.b, c = T.c;
   const float v0[3] = {a.x, a.y, a.z}, e1[3] = {a.w, b.x, b.y}, e2[3] = {b.z, b.w, c.x};
   const float p[3] = {d[1] * e2[2] - d[2] * e2[1], d[2] * e2[0] - d[0] * e2[2],
                       d[0] * e2[1] - d[1] * e2[0]};
@@ -315,6 +321,10 @@ __device__ __forceinline__ bool tri_hit32(const float4* __restrict__ r, const fl
   u = uu;
   v = vv;
   return true;
+}
+__device__ __forceinline__ bool tri_hit32(const float4* __restrict__ r, const float o[3],
+                                          const float d[3], float& t, float& u, float& v) {
+  return tri_test32(load_tri32(r), o, d, t, u, v);
 }
 
 template <bool ANY>
@@ -336,21 +346,32 @@ __device__ __forceinline__ int trace32_impl(const MeshDev& m, const float4* sn, 
   int bslot = -1, bid = INT_MAX;
   for (;;) {
     if (node < 0) {
-      const int first = (~node) >> 3, count = (~node) & 7;
-      for (int sidx = first; sidx < first + count; ++sidx) {
-        float t, u, v;
-        if (!tri_hit32(m.tri32 + 3 * size_t(sidx), of, df, t, u, v) || !(t <= best)) continue;
-        if (ANY) {
-          if (t < tmaxf) return sidx;
-          continue;
-        }
-        const int id = __ldg(&m.orig[sidx]);
-        if (t < best || id < bid) {
-          best = t;
-          bu = u;
-          bv = v;
-          bslot = sidx;
-          bid = id;
+      // triangles two at a time: both records are requested before the
+      // first test, so a two-triangle leaf costs one memory latency, not
+      // two (tests and their order unchanged)
+      const int first = (~node) >> 3, end = first + ((~node) & 7);
+      for (int s0 = first; s0 < end; s0 += 2) {
+        Tri32 tr[2];
+        tr[0] = load_tri32(m.tri32 + 3 * size_t(s0));
+        if (s0 + 1 < end) tr[1] = load_tri32(m.tri32 + 3 * size_t(s0 + 1));
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int sidx = s0 + e;
+          if (sidx >= end) break;
+          float t, u, v;
+          if (!tri_test32(tr[e], of, df, t, u, v) || !(t <= best)) continue;
+          if (ANY) {
+            if (t < tmaxf) return sidx;
+            continue;
+          }
+          const int id = __ldg(&m.orig[sidx]);
+          if (t < best || id < bid) {
+            best = t;
+            bu = u;
+            bv = v;
+            bslot = sidx;
+            bid = id;
+          }
         }
       }
     } else {
