@@ -517,7 +517,24 @@ def extras(args, ctx):
                                       dtype=torch.float32, ctx=ctx)
         run = api.MeshTextureRun(prob, optimizer="meta", lr=0.005)
         ms = timed(run.step, 5)
+        # the same loop replayed as a captured two-iteration CUDA graph (56
+        # launches), on a context of its own stream; bit-identical
+        gs = torch.cuda.Stream(device=dev)
+        with torch.cuda.stream(gs):
+            gprob = api.MeshTextureProblem(512, 512, 512, max_vertices=6, target_spp=4,
+                                           dtype=torch.float32, ctx=api.Context(ctx.device, stream=gs))
+            grun = api.MeshTextureRun(gprob, optimizer="meta", lr=0.005)
+            grun.run(3)
+            grun.run(2, graph=True)
+            torch.cuda.synchronize()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(gs)
+            grun.run(10, graph=True)
+            b.record(gs)
+            torch.cuda.synchronize()
+            ms_g = a.elapsed_time(b) / 10
         out["mesh_texture_512px_f32"] = {"ms_per_iteration": ms, "iterations_per_s": 1e3 / ms,
+                                         "graph_ms_per_iteration": ms_g,
                                          "paths_per_s": prob.draws_per_sample() / (ms / 1e3),
                                          "texture_params": prob.dim(), **prob.scene.info()}
         # BVH closest-hit throughput on the same scene (rays aimed at the objects)

@@ -71,6 +71,7 @@ struct MeshK {
   double view[25];
   uint64_t key;
   uint32_t iteration;
+  const uint32_t* it_offset;  // device iteration offset or null (mg_ctx_set_iteration_offset)
 };
 
 __device__ __forceinline__ double dot3d(const double a[3], const double b[3]) {
@@ -577,6 +578,7 @@ inline MeshK make_k(const mg_mesh_scene* s, int W, int H, const double* view, ui
   for (int i = 0; i < 25; ++i) q.view[i] = view[i];
   q.key = key;
   q.iteration = it;
+  q.it_offset = nullptr;
   return q;
 }
 

@@ -270,6 +270,7 @@ __global__ void __launch_bounds__(kMThreads)
                      unsigned long long* __restrict__ acc, long long np, unsigned int* work,
                      ReducePartials* partials, unsigned int* counter, double* loss_out) {
   MESH_SMEM;
+  if (q.it_offset) q.iteration += __ldg(q.it_offset);
   const int npix = q.W * q.H;
   const int R2 = q.R * q.R;
   const T* th[2] = {now, prev};

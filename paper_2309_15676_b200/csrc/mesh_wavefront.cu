@@ -149,6 +149,7 @@ __device__ __forceinline__ T& vf(const WF<T>& w, int v, int f, int p) {
 
 template <class T>
 __global__ void __launch_bounds__(kMThreads) wf_gen_kernel(MeshK q, WF<T> w) {
+  if (q.it_offset) q.iteration += __ldg(q.it_offset);
   const double* V = q.view;
   for (int p = blockIdx.x * kMThreads + threadIdx.x; p < w.P; p += gridDim.x * kMThreads) {
     const int k = p / w.npix, pix = w.pix0 + (p - k * w.npix);
@@ -202,6 +203,7 @@ __global__ void __launch_bounds__(kMThreads)
     wf_shade_kernel(MeshK q, MeshDev m, WF<T> w, int v, const T* __restrict__ th0,
                     const T* __restrict__ th1) {
   constexpr int TS = TexIlv<T, NCH>::TS;  // th0 / th1: texel-major copies
+  if (q.it_offset) q.iteration += __ldg(q.it_offset);
   using F = VF<NCH>;
   const double* V = q.view;
   const int maxv = int(V[24]);
@@ -851,6 +853,7 @@ int mg_meshscene_sample_pair(mg_ctx* ctx, mg_mesh_scene* s, int32_t dtype, int32
   int st = check_view(view);
   if (st) return st;
   MeshK q = make_k(s, W, H, view, key, iteration);
+  q.it_offset = ctx->it_offset;
   q.row0 = row0;
   q.row1 = row1;
   const long long np = (long long)s->nobj * s->nch * s->R * s->R;
@@ -912,6 +915,7 @@ int mg_meshscene_sample_pair_sharded(mg_ctx* ctx, mg_mesh_scene* s, int32_t dtyp
   int st = check_view(view);
   if (st) return st;
   MeshK q = make_k(s, W, H, view, key, iteration);
+  q.it_offset = ctx->it_offset;
   q.row0 = row0;
   q.row1 = row1;
   AccTable tbl{};

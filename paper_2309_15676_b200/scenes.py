@@ -463,6 +463,8 @@ class MeshTextureProblem:
     1 FD + 2 proportional spp (paths A, B, C).  Own renderer (DESIGN.md §12,
     oracle mgo_mesh_*)."""
 
+    ITERATION_OFFSET = True  # the sampler honours mg_ctx_set_iteration_offset
+
     def __init__(self, width: int = 512, height: int = 512, tex_res: int = 512,
                  sphere_res=(24, 48), displaced_res=(100, 100), max_vertices: int = 6,
                  target_seed: int = 1, target_spp: int = 16, dtype=torch.float32, ctx=None,

@@ -154,7 +154,8 @@ def test_tile_sharded_gradients_sum_exactly(api, tiles):
 
 
 @pytest.mark.parametrize("kind,dtype", [("quad", torch.float32), ("quad", torch.float64),
-                                        ("helix", torch.float32)])
+                                        ("helix", torch.float32), ("mesh", torch.float32),
+                                        ("meshx", torch.float32)])
 def test_graph_replayed_run_is_bit_identical(api, kind, dtype):
     """run(k, graph=True) replays one captured two-step block (device
     iteration counter, device Moment2 coefficient): the parameters, the
@@ -167,8 +168,15 @@ def test_graph_replayed_run_is_bit_identical(api, kind, dtype):
         if kind == "quad":
             prob = api.QuadTextureProblem(32, 32, 8, target_spp=16, dtype=dtype, ctx=ctx)
             return prob, api.QuadTextureRun(prob, optimizer="meta", lr=0.01)
-        prob = api.HelixProblem(32, 24, target_spp=4, dtype=dtype, ctx=ctx)
-        return prob, api.HelixRun(prob, optimizer="meta", lr=0.01)
+        if kind == "helix":
+            prob = api.HelixProblem(32, 24, target_spp=4, dtype=dtype, ctx=ctx)
+            return prob, api.HelixRun(prob, optimizer="meta", lr=0.01)
+        # mesh wavefront (28 launches per iteration, prev-copy reuse on);
+        # meshx: 5 channels, 4 proportional paths (the configs[4] form)
+        ch, nprop = (4, 2) if kind == "mesh" else (5, 4)
+        prob = api.MeshTextureProblem(32, 24, 8, (8, 12), (10, 12), max_vertices=4, target_spp=4,
+                                      dtype=dtype, ctx=ctx, channels=ch, prop_paths=nprop)
+        return prob, api.MeshTextureRun(prob, "meta", lr=0.01)
 
     with torch.cuda.stream(side):
         pe, re_ = make()
