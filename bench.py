@@ -43,7 +43,10 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--pool", type=int, default=4)
     ap.add_argument("--e2e-steps", type=int, default=None)
-    ap.add_argument("--cpu-n", type=int, default=1 << 22, help="reference sample size")
+    ap.add_argument("--cpu-n", type=int, default=None,
+                    help="cpu_baseline sample size (default: --n, the full workload)")
+    ap.add_argument("--dry-run", action="store_true",
+                    help="form the process group (gloo without a GPU) and print its shape only")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--extras", action="store_true",
                     help="force the secondary measurements (default: on for a single GPU)")
@@ -126,43 +129,66 @@ def measured_peak():
         return 6650.0, "fallback"
 
 
+def workload_config(n, world):
+    """The `config` object of BOTH arms (same workload, same keys)."""
+    return {"workload": "meta-update-microbench (BASELINE configs[1])",
+            "params_per_gpu": n, "global_params": n * world,
+            "l2": "inputs > L2 (no flush)", "parallelism": f"param-shard x{world}",
+            "beta_f": 0.9, "beta_delta": 0.5, "lr": 0.01, "steps_state_carried": True}
+
+
 # --------------------------------------------------------------- reference
-def cpu_reference(n, steps, threads, pool=2, seed=0):
+def cpu_reference(n, steps, threads, warmup=1, pool=2, seed=0):
     """Times the UNMODIFIED reference (oracle/_ref) meta update: Moment2 x2 +
-    diff decoupling + MetaEstimator::step + params += delta, fp64."""
+    diff decoupling + MetaEstimator::step + params += delta, fp64, on the
+    configs[1] input distributions (seeded numpy PCG64).  Returns (pairs/s,
+    mean seconds per timed step, kind)."""
     import numpy as np
     sys.path.insert(0, os.path.join(ROOT, "tests"))
     from oracle_bind import RefLib, ref_available
-    rs = np.random.RandomState(seed)
+    if not ref_available():
+        raise RuntimeError("oracle/_ref not built (make -C oracle/ref)")
+    rs = np.random.default_rng(seed)
     mu = rs.uniform(-1, 1, n)
     sig = rs.uniform(0.1, 2.0, n)
-    props = np.stack([mu + sig * rs.standard_normal(n) for _ in range(pool)])
-    diffs = np.stack([0.1 * sig * rs.standard_normal(n) for _ in range(pool)])
-    if ref_available():
-        sec = RefLib().meta_update_bench(props, diffs, 1e-4, steps, threads)
-        kind = "reference"
-    else:  # the C restatement of the same algorithm
-        raise RuntimeError("oracle/_ref not built (make -C oracle/ref)")
-    return n / sec, sec, kind
+    props = np.empty((pool, n))
+    diffs = np.empty((pool, n))
+    for k in range(pool):
+        rs.standard_normal(out=props[k])
+        props[k] *= sig
+        props[k] += mu
+        rs.standard_normal(out=diffs[k])
+        diffs[k] *= sig
+        diffs[k] *= 0.1
+    del mu, sig
+    sec, _ = RefLib().meta_update_bench(props, diffs, 1e-4, steps, threads, warmup=warmup)
+    return n / sec, sec, "reference"
 
 
 def run_reference_arm(args):
+    """The reference's own CPU implementation of the path (oracle/_ref: the
+    unmodified reference sources), on the SAME workload as our arm: N =
+    --n parameters per GPU (2^28 by default), configs[1] inputs, state
+    carried, all host threads.  At --gpus N the job's N x --n parameters
+    are processed shard after shard by the same cores, so the throughput
+    (pairs/s) is the one measured on one shard.  Rank 0 alone runs."""
     rank, world, _ = dist_env()
     if rank != 0:
         return 0
     threads = os.cpu_count() or 1
-    n = args.cpu_n
+    n = args.n
+    gpus = max(args.gpus, world)
     t0 = time.time()
-    val, sec, kind = cpu_reference(n, max(args.steps, 3), threads)
+    val, sec, kind = cpu_reference(n, args.steps, threads, warmup=args.warmup)
     line = {
-        "metric": METRIC, "value": val, "unit": UNIT, "impl": "reference", "n_gpus": args.gpus,
+        "metric": METRIC, "value": val, "unit": UNIT, "impl": "reference", "n_gpus": gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": sec * 1e3,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic", "config": {"workload": "meta-update-microbench (BASELINE configs[1])",
-                                        "params_per_step": n, "precision": "fp64 (reference)"},
+        "data": "synthetic", "config": workload_config(n, gpus),
         "cpu_baseline": {"value": val, "unit": UNIT, "cores": threads, "kind": kind,
-                         "sample": f"{n} params/step, median of {max(args.steps, 3)} steps, "
-                                   f"{threads} std::threads over contiguous chunks"},
+                         "sample": f"{n} params/step (the full per-GPU workload), mean of "
+                                   f"{args.steps} timed steps after {args.warmup} warm-up, "
+                                   f"{threads} std::threads over contiguous chunks, fp64"},
         "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "wall_s": time.time() - t0,
     }
@@ -313,11 +339,9 @@ def run_ours(args):
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": args.dtype, "data": "synthetic",
             "iterations_per_s": 1e3 / ms_step,
-            "config": {"workload": "meta-update-microbench (BASELINE configs[1])",
-                       "params_per_gpu": n, "global_params": n * world, "pool_batches": args.pool,
-                       "l2": "inputs > L2 (no flush)", "parallelism": f"param-shard x{world}",
-                       "beta_f": 0.9, "beta_delta": 0.5, "lr": 0.01,
-                       "kernel": "register-streaming" if args.no_tma else "tma-bulk-pipeline"},
+            "impl": "ours", "config": workload_config(n, world),
+            "kernel": "register-streaming" if args.no_tma else "tma-bulk-pipeline",
+            "pool_batches": args.pool,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": ncu_traffic(n, args.dtype),
                          "frac_vs_8tbs_spec": achieved / 8000.0,
@@ -334,13 +358,20 @@ def run_ours(args):
         pg.barrier()
     del props, diffs
     torch.cuda.empty_cache()
+    if world > 1 and not args.no_extras:
+        sh = sharded_extras(args, ctx, pg, rank, world)
+        if rank == 0:
+            line["extras"] = sh
     if rank == 0 and not args.no_extras and (world == 1 or args.extras):
-        line["extras"] = extras(args, ctx)
+        line.setdefault("extras", {}).update(extras(args, ctx))
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cn = args.cpu_n or n
         try:
-            cv, csec, kind = cpu_reference(args.cpu_n, 5, 1)
+            cv, csec, kind = cpu_reference(cn, 1, 1, warmup=1)
             line["cpu_baseline"] = {"value": cv, "unit": UNIT, "cores": 1, "kind": kind,
-                                    "sample": f"{args.cpu_n} params x 5 steps fp64, median step"}
+                                    "sample": f"{cn} params fp64 (the full workload), 1 warm-up "
+                                              f"+ 1 timed step, 1 thread (the reference's "
+                                              f"per-run math is single-threaded)"}
         except Exception as e:  # reported, never replaces our number
             line["cpu_baseline"] = {"value": None, "unit": UNIT, "cores": 1, "kind": "reference",
                                     "sample": f"unavailable: {e}"}
@@ -350,6 +381,81 @@ def run_ours(args):
         pg.barrier()
         pg.destroy_process_group()
     return 0
+
+
+def sharded_extras(args, ctx, pg, rank, world):
+    """N > 1: north_star's real split, BASELINE configs[4] (1024^2, 16
+    objects / ~503k triangles, 83.9M texture parameters, depth 8, 1 FD + 4
+    proportional spp) with the image rows sharded across the ranks
+    (dist.TiledRenderStepP2P: each rank adds its adjoints straight into the
+    owning rank's fixed-point shard over NVLink, fused update on the shard,
+    parameters all-gathered, 4 scalars all-reduced).  Strong scaling (same
+    image).  Also the all-gather of the 83.9M-float parameter vector alone,
+    as bus bandwidth.  Every rank takes part; times are max over ranks
+    (CUDA events)."""
+    import torch
+    from paper_2309_15676_b200 import api
+    from paper_2309_15676_b200.dist import TiledRenderStepP2P
+    out = {}
+    dev = torch.device("cuda", ctx.device)
+
+    def agree(ok):
+        f = torch.tensor([0.0 if ok else 1.0], device=dev, dtype=torch.float64)
+        pg.all_reduce(f)
+        return f.item() == 0.0
+
+    def max_ms(ms):
+        t = torch.tensor([ms], device=dev, dtype=torch.float64)
+        pg.all_reduce(t, op=pg.ReduceOp.MAX)
+        return float(t.item())
+
+    err = None
+    try:
+        prob = api.MeshLargeProblem(target_spp=2, ctx=ctx)
+        step = TiledRenderStepP2P(prob, lr=0.005)
+    except Exception as e:
+        err = f"{type(e).__name__}: {e}"
+    if not agree(err is None):
+        out["mesh_large_tiled_error"] = err or "another rank failed to build the scene"
+        return out
+    for _ in range(2):
+        step.step()
+    torch.cuda.synchronize()
+    pg.barrier()
+    K = 5
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record(ctx.stream)
+    for _ in range(K):
+        step.step()
+    b.record(ctx.stream)
+    torch.cuda.synchronize()
+    ms = max_ms(a.elapsed_time(b) / K)
+    n = prob.dim()
+    gather_bytes = 4 * n  # the whole parameter vector lands on every rank
+    # the all-gather alone (NCCL over NVLink), bus bandwidth convention
+    shard = torch.empty(n // world, device=dev)
+    full = torch.empty(n, device=dev)
+    for _ in range(2):
+        pg.all_gather_into_tensor(full, shard)
+    torch.cuda.synchronize()
+    pg.barrier()
+    a.record()
+    for _ in range(5):
+        pg.all_gather_into_tensor(full, shard)
+    b.record()
+    torch.cuda.synchronize()
+    ag_ms = max_ms(a.elapsed_time(b) / 5)
+    out["mesh_large_1024px_tiled_p2p"] = {
+        "n_gpus": world, "ms_per_iteration": ms, "iterations_per_s": 1e3 / ms,
+        "paths_per_s": prob.draws_per_sample() / (ms / 1e3), "texture_params": n,
+        "scaling": "strong (same image, rows split)",
+        "allgather_bytes_per_iteration": gather_bytes,
+        "allgather_ms": ag_ms,
+        "allgather_busbw_gbs": gather_bytes * (world - 1) / world / (ag_ms / 1e3) / 1e9,
+        "scalar_allreduce_bytes": 32}
+    del step, prob, shard, full
+    torch.cuda.empty_cache()
+    return out
 
 
 def extras(args, ctx):
@@ -446,6 +552,42 @@ def extras(args, ctx):
                 r["note"] = "L2-resident (59 MB < 126 MB L2): launch-bound, not roofline-judged"
             out[f"meta_update_2^{m.bit_length() - 1}_f32"] = r
             del pr, df, bufs, up
+
+    def update_f64():
+        # the parity-mode (fp64, bit-exact with the reference) fused update at
+        # the headline size, 2^28 parameters, state carried, 20 steps (the
+        # like-for-like arithmetic of the reference arm)
+        m = n
+        gen = torch.Generator(device=dev).manual_seed(8)
+        mu = torch.rand(m, device=dev, dtype=torch.float64, generator=gen) * 2 - 1
+        sg = torch.rand(m, device=dev, dtype=torch.float64, generator=gen) * 1.9 + 0.1
+        pr = [mu + sg * torch.randn(m, device=dev, dtype=torch.float64, generator=gen)
+              for _ in range(2)]
+        del mu
+        df = [0.1 * sg * torch.randn(m, device=dev, dtype=torch.float64, generator=gen)
+              for _ in range(2)]
+        del sg
+        bufs = [torch.zeros(m, device=dev, dtype=torch.float64),
+                torch.empty(m, device=dev, dtype=torch.float64)]
+        up = api.FusedMetaUpdate(m, dtype=torch.float64, lr=0.01, ctx=ctx)
+        ev = []
+        for t in range(24):
+            if t >= 4:
+                e = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+                e[0].record(ctx.stream)
+            up.step(pr[t % 2], df[t % 2] if t else torch.zeros_like(bufs[0]), bufs[t % 2],
+                    bufs[(t + 1) % 2])
+            if t >= 4:
+                e[1].record(ctx.stream)
+                ev.append(e)
+        torch.cuda.synchronize()
+        ms = sum(a.elapsed_time(b) for a, b in ev) / len(ev)
+        gbs = BYTES_PER_PARAM["f64"] * m / (ms / 1e3) / 1e9
+        out["meta_update_2^28_f64"] = {"params": m, "ms_per_step": ms,
+                                       "pairs_per_s": m / (ms / 1e3), "gbs": gbs,
+                                       "frac": gbs / peak, "steps_timed": len(ev),
+                                       "bytes_per_param": BYTES_PER_PARAM["f64"]}
+        del pr, df, bufs, up
 
     def minirender(rng):
         # fused mini-render iteration at scale (16.7M pixels): one kernel per
@@ -574,7 +716,7 @@ def extras(args, ctx):
         out["minirender_runner"] = {"replicates": 148, "iterations": 200, "wall_s": wall,
                                     "pairs_per_s": 148 * 200 * 4096 * 2 / wall}
 
-    for name, fn in (("update_sizes", update_sizes), ("adam", adam), ("minirender_philox", lambda: minirender("philox")),
+    for name, fn in (("update_f64", update_f64), ("update_sizes", update_sizes), ("adam", adam), ("minirender_philox", lambda: minirender("philox")),
                      ("minirender_mt64", lambda: minirender("mt64")), ("quad", quad),
                      ("helix", helix), ("mesh", mesh), ("mesh_large", mesh_large),
                      ("runner", runner)):
@@ -586,8 +728,59 @@ def extras(args, ctx):
     return out
 
 
+def free_port():
+    import socket
+    with socket.socket(socket.AF_INET, socket.SOCK_STREAM) as so:
+        so.bind(("127.0.0.1", 0))
+        return so.getsockname()[1]
+
+
+def spawn_ranks(n):
+    """`bench.py --gpus N` without a launcher: re-exec this command as N
+    ranks under torch.distributed.run (one process per GPU, rendezvous on
+    127.0.0.1); rank 0 prints the JSON line.  Returns the launcher's exit
+    code."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={n}", "--master-addr=127.0.0.1", f"--master-port={free_port()}",
+           os.path.abspath(__file__)] + sys.argv[1:]
+    env = dict(os.environ)
+    env.setdefault("OMP_NUM_THREADS", "1")
+    return subprocess.call(cmd, env=env)
+
+
+def dry_run(args):
+    """Form the process group exactly as a real run would (NCCL on GPUs,
+    gloo without) and print its shape: the launcher's CPU test."""
+    import torch
+    import torch.distributed as dist
+    rank, world, local = dist_env()
+    if "WORLD_SIZE" in os.environ:
+        backend = "nccl" if torch.cuda.is_available() else "gloo"
+        dist.init_process_group(backend)
+        ranks = [None] * world
+        dist.all_gather_object(ranks, (rank, local, os.getpid()))
+        dist.destroy_process_group()
+    else:
+        ranks = [(rank, local, os.getpid())]
+    if rank == 0:
+        print(json.dumps({"dry_run": True, "impl": args.impl, "n_gpus": world,
+                          "ranks": [r[0] for r in ranks], "local_ranks": [r[1] for r in ranks],
+                          "distinct_pids": len({r[2] for r in ranks})}), flush=True)
+    return 0
+
+
 def main():
     args = parse()
+    launched = "WORLD_SIZE" in os.environ
+    if not launched and args.gpus > 1 and args.impl == "ours":
+        return spawn_ranks(args.gpus)
+    _, world, _ = dist_env()
+    if launched and args.impl == "ours" and world != args.gpus:
+        print(f"bench.py: --gpus {args.gpus} but the launcher started {world} ranks",
+              file=sys.stderr)
+        return 2
+    if args.dry_run:
+        return dry_run(args)
     if args.impl == "reference":
         return run_reference_arm(args)
     return run_ours(args)

@@ -261,7 +261,8 @@ typedef struct mg_update_scalars {
   /* What step t consumed, for recording (harness.cpp:174). */
   double ssn_used;
   /* beta_f^t of Moment2(beta_f) (moment2.hpp:35), advanced on the device by
-   * every launch whose args carry beta_f > 0; read when prop_coef_device. */
+   * every launch whose args carry prop_pow_advance (or beta_f > 0); read when
+   * prop_coef_device. */
   double prop_decay_pow;
 } mg_update_scalars;
 
@@ -277,12 +278,16 @@ typedef struct mg_meta_update_args {
   double proj_lo;
   double ssn_host;
   double proj_hi;
-  double beta_f;            /* > 0: advance scalars->prop_decay_pow *= beta_f on the device */
+  double beta_f;            /* decay of Moment2(beta_f); see prop_pow_advance */
   int32_t prop_coef_device; /* 1: Moment2(beta_f) coefficient (1-beta_f)/(1-prop_decay_pow)
                                from the device power instead of prop_coef — steps that
                                carry no per-step host scalar, so one captured CUDA graph
                                can be replayed (same bits: same IEEE multiply chain) */
-  int32_t pad_;
+  int32_t prop_pow_advance; /* 1: advance scalars->prop_decay_pow *= beta_f on the device
+                               (every step of a run that uses prop_coef_device).  Legacy:
+                               beta_f > 0 also advances.  beta_f = 0 is a valid decay
+                               (coefficient 1, moment2.hpp:36-38); with prop_coef_device it
+                               needs this flag, else MG_EINVAL. */
 } mg_meta_update_args;
 
 /* Optional side inputs/outputs of the fused update.  Any may be NULL. */

@@ -357,9 +357,11 @@ int ref_run_experiment(const char* cfg_text, const char* csv_path, double* out_s
 // (each chunk its own estimator objects on its own std::thread; the update
 // is elementwise, so chunking is exact except for the global ssn, which is
 // given).  Inputs cycle over `pool` (prop, diff) batches of n doubles each.
-// Returns seconds per step (median over steps) in *out_sec_per_step.
-int ref_meta_update_bench(std::int64_t n, int steps, int threads, int pool, const double* props,
-                          const double* diffs, double ssn, double* out_sec_per_step) {
+// The first `warmup` steps are untimed; returns the mean seconds per timed
+// step in *out_sec_per_step and the median in *out_median (may be null).
+int ref_meta_update_bench(std::int64_t n, int warmup, int steps, int threads, int pool,
+                          const double* props, const double* diffs, double ssn,
+                          double* out_sec_per_step, double* out_median) {
   return guarded([&] {
     const int T = threads < 1 ? 1 : threads;
     struct Chunk {
@@ -375,7 +377,7 @@ int ref_meta_update_bench(std::int64_t n, int steps, int threads, int pool, cons
       chunks[t].params = Vec::Zero(chunks[t].hi - chunks[t].lo);
     }
     std::vector<double> times;
-    for (int s = 0; s < steps; ++s) {
+    for (int s = 0; s < warmup + steps; ++s) {
       const double* P = props + static_cast<std::size_t>(s % pool) * n;
       const double* D = diffs + static_cast<std::size_t>(s % pool) * n;
       const double step_ssn = s == 0 ? 0.0 : ssn;
@@ -398,10 +400,15 @@ int ref_meta_update_bench(std::int64_t n, int steps, int threads, int pool, cons
         for (auto& c : chunks) ws.emplace_back([&work, &c] { work(c); });
         for (auto& w : ws) w.join();
       }
-      times.push_back(std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count());
+      if (s >= warmup)
+        times.push_back(std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count());
     }
+    if (times.empty()) throw std::invalid_argument("ref_meta_update_bench: no timed step");
+    double sum = 0.0;
+    for (double x : times) sum += x;
+    *out_sec_per_step = sum / double(times.size());
     std::sort(times.begin(), times.end());
-    *out_sec_per_step = times[times.size() / 2];
+    if (out_median) *out_median = times[times.size() / 2];
   });
 }
 

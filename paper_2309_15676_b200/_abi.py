@@ -67,7 +67,7 @@ class MetaUpdateArgs(C.Structure):
                 ("first_step", C.c_int32), ("diff_norm", C.c_int32), ("project", C.c_int32),
                 ("ssn_from_host", C.c_int32), ("proj_lo", C.c_double), ("ssn_host", C.c_double),
                 ("proj_hi", C.c_double), ("beta_f", C.c_double), ("prop_coef_device", C.c_int32),
-                ("pad_", C.c_int32)]
+                ("prop_pow_advance", C.c_int32)]
 
 
 class MetaExtras(C.Structure):

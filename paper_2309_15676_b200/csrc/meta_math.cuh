@@ -13,9 +13,10 @@ namespace mg {
 
 struct MetaK {
   double lr, eps_step, eps_alpha, prop_coef, beta_delta, proj_lo, ssn_host, proj_hi;
-  double beta_f = 0.0;  // > 0: advance the device beta_f power
+  double beta_f = 0.0;
   int clip, diff_norm, project, ssn_from_host;
   int prop_dev = 0;     // 1: prop coefficient from the device power
+  int prop_adv = 0;     // 1: advance the device beta_f power (also when beta_f > 0)
 };
 
 template <class T>
@@ -60,7 +61,7 @@ __device__ __forceinline__ StepScal load_step_scalars(const MetaK& k, const mg_u
   // Moment2(beta_f): the host passes (1-b)/(1-b^t) computed by the repeated
   // multiply of moment2.hpp:35, or the device forms the same chain
   s.ppow = __ldcg(&sc->prop_decay_pow);
-  if (k.beta_f > 0.0) s.ppow = s.ppow * k.beta_f;
+  if (k.prop_adv || k.beta_f > 0.0) s.ppow = s.ppow * k.beta_f;
   s.c_prop = k.prop_dev ? (1.0 - k.beta_f) / (1.0 - s.ppow) : k.prop_coef;
   return s;
 }

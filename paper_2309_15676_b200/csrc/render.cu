@@ -224,6 +224,12 @@ extern "C" int mg_minirender_meta_iteration(mg_ctx* ctx, int32_t dtype, int64_t 
     return fail(MG_EINVAL, "mg_minirender_meta_iteration: null buffer");
   if (a->update.diff_norm != MG_DIFF_NORM_GLOBAL)
     return fail(MG_EUNSUPPORTED, "mg_minirender_meta_iteration: global diff norm only");
+  {
+    const mg_meta_update_args* u = &a->update;
+    if (u->prop_coef_device && !(u->beta_f > 0.0) && !u->prop_pow_advance)
+      return fail(MG_EINVAL,
+                  "mg_minirender_meta_iteration: prop_coef_device with beta_f = 0 needs prop_pow_advance");
+  }
   RenderK k;
   k.meta.lr = a->update.meta.lr;
   k.meta.eps_step = a->update.meta.eps_step;
@@ -232,6 +238,7 @@ extern "C" int mg_minirender_meta_iteration(mg_ctx* ctx, int32_t dtype, int64_t 
   k.meta.prop_coef = a->update.prop_coef;
   k.meta.beta_f = a->update.beta_f;
   k.meta.prop_dev = a->update.prop_coef_device;
+  k.meta.prop_adv = a->update.prop_pow_advance;
   k.meta.beta_delta = a->update.beta_delta;
   k.meta.diff_norm = MG_DIFF_NORM_GLOBAL;
   k.meta.project = 1;  // problems.cpp:228: params = params.max(0.0)

@@ -684,6 +684,7 @@ MetaK make_meta_k(const mg_meta_update_args* a) {
   k.prop_coef = a->prop_coef;
   k.beta_f = a->beta_f;
   k.prop_dev = a->prop_coef_device;
+  k.prop_adv = a->prop_pow_advance;
   k.beta_delta = a->beta_delta;
   k.diff_norm = a->diff_norm;
   k.project = a->project;
@@ -761,6 +762,8 @@ int mg_meta_update(mg_ctx* ctx, int32_t dtype, int64_t n, const mg_meta_update_a
   if (a->diff_norm == MG_DIFF_NORM_PER_PARAM && !(x && x->params_prev))
     return fail(MG_EINVAL, "mg_meta_update: per-param diff norm needs params_prev");
   if (!(a->meta.lr > 0.0)) return fail(MG_EINVAL, "MetaEstimator: lr must be positive");
+  if (a->prop_coef_device && !(a->beta_f > 0.0) && !a->prop_pow_advance)
+    return fail(MG_EINVAL, "mg_meta_update: prop_coef_device with beta_f = 0 needs prop_pow_advance");
   const MetaK k = make_meta_k(a);
   const mg_meta_extras none{};
   const mg_meta_extras& e = x ? *x : none;
@@ -797,6 +800,8 @@ int mg_shared_meta_update(mg_ctx* ctx, int32_t dtype, int64_t shard_n, int64_t s
   if (a->diff_norm != MG_DIFF_NORM_GLOBAL)
     return fail(MG_EUNSUPPORTED, "mg_shared_meta_update: global diff norm only");
   if (shard_n == 0) return MG_OK;
+  if (a->prop_coef_device && !(a->beta_f > 0.0) && !a->prop_pow_advance)
+    return fail(MG_EINVAL, "mg_shared_meta_update: prop_coef_device with beta_f = 0 needs prop_pow_advance");
   const MetaK k = make_meta_k(a);
   const bool first = a->first_step != 0;
   const int grid = grid_for(ctx, shard_n, kThreads, 8);

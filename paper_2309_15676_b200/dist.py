@@ -219,7 +219,8 @@ class SharedParamStepP2P:
                                 project=(2 if self.project_hi is not None
                                          else int(self.project_lo is not None)),
                                 proj_lo=self.project_lo or 0.0,
-                                proj_hi=self.project_hi or 0.0)
+                                proj_hi=self.project_hi or 0.0, beta_f=self.beta_f,
+                                prop_pow_advance=1)
         arr = lambda ptrs: (C.c_void_p * self.world)(*ptrs)  # noqa: E731
         self.h_prop.barrier()                      # every rank's partials are written
         self._check(self._L.mg_shared_meta_update(

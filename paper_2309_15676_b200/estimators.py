@@ -185,7 +185,8 @@ class FusedMetaUpdate:
             proj_lo=0.0 if self.project_lo is None else self.project_lo,
             ssn_host=0.0 if ssn_host is None else ssn_host,
             proj_hi=0.0 if self.project_hi is None else self.project_hi,
-            beta_f=self.beta_f, prop_coef_device=int(self.device_coef and self.t > 1))
+            beta_f=self.beta_f, prop_coef_device=int(self.device_coef and self.t > 1),
+            prop_pow_advance=1)
 
     def step(self, prop, diff, params_in, params_out, target=None, vprop=None, vdiff=None,
              params_prev=None, delta_out=None, ssn_host=None):
@@ -212,6 +213,11 @@ class FusedAdamUpdate:
                                        device=device)
         host = _abi.fresh_scalars()
         check(load().mg_scalars_write(self.ctx.h, _p(self.scalars_buf), C.byref(host)))
+
+    def scalars(self) -> _abi.UpdateScalars:
+        out = _abi.UpdateScalars()
+        check(load().mg_scalars_read(self.ctx.h, _p(self.scalars_buf), C.byref(out)))
+        return out
 
     def step(self, grad, params_in, params_out, target=None):
         check(load().mg_adam_update(self.ctx.h, _dtype_code(grad), self.n, C.byref(self.s),

@@ -268,7 +268,8 @@ class MiniRenderRun:
         upd = _abi.MetaUpdateArgs(meta=self.meta,
                                   prop_coef=(1.0 - self.beta_f) / (1.0 - self.beta_f_pow),
                                   beta_delta=self.beta_delta, first_step=int(self.t == 1),
-                                  diff_norm=_abi.MG_DIFF_NORM_GLOBAL, project=1)
+                                  diff_norm=_abi.MG_DIFF_NORM_GLOBAL, project=1,
+                                  beta_f=self.beta_f, prop_pow_advance=1)
         a = _abi.RenderArgs(update=upd, spp=self.spp, rng_kind=self.rng_kind, key=self.key,
                             iteration=self.t - 1, stream=0, pixel_offset=self.lo,
                             record_plus1=0 if record is None else record + 1)

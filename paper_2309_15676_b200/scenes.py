@@ -149,24 +149,32 @@ class QuadTextureRun:
         if ctx.stream.cuda_stream == 0:
             raise InvalidArgument(_abi.MG_EINVAL, "graph runs need a context on a non-default stream")
         done = 0
-        while self.t < 1 and done < iterations:  # the first step initialises the state
-            self.step()
-            done += 1
-        left = iterations - done
-        if left >= 2:
-            g = getattr(self, "_graph", None)
-            if g is None:
-                g = self._capture()
-            with torch.cuda.stream(ctx.stream):
+        with torch.cuda.stream(ctx.stream):  # replays launch on the current stream
+            while self.t < 1 and done < iterations:  # the first step initialises the state
+                self.step()
+                done += 1
+            left = iterations - done
+            if left >= 2:
+                g = getattr(self, "_graph", None)
+                if g is None:
+                    g = self._capture()
+                # the graph's buffer roles are fixed at capture: it expects
+                # pi_t in the buffer that was `params` then.  After an odd
+                # number of eager steps the roles are swapped; one eager step
+                # realigns them
+                if self.params.data_ptr() != self._graph_params_ptr:
+                    self.step()
+                    left -= 1
                 self._it_dev.fill_(self.t)
-            for _ in range(left // 2):
-                g.replay()
-                for _ in range(2):  # the host mirror of what the replay advanced
-                    self.upd.t += 1
-                    self.upd.beta_f_pow *= self.upd.beta_f
-                self.t += 2
-        if left % 2:
-            self.step()
+                for _ in range(left // 2):
+                    g.replay()
+                    for _ in range(2):  # the host mirror of what the replay advanced
+                        self.upd.t += 1
+                        self.upd.beta_f_pow *= self.upd.beta_f
+                    self.t += 2
+                left %= 2
+            for _ in range(left):
+                self.step()
 
     def _capture(self):
         ctx, L = self.p.ctx, load()
@@ -184,6 +192,7 @@ class QuadTextureRun:
             check(L.mg_ctx_set_iteration_offset(ctx.h, None))
             self.upd.t, self.upd.beta_f_pow, _ = saved
         self._graph = g
+        self._graph_params_ptr = self.params.data_ptr()
         return g
 
     def loss_estimate(self) -> float:

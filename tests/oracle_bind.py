@@ -421,8 +421,8 @@ class RefLib:
                                      C.POINTER(C.c_int), C.POINTER(C.c_int64),
                                      C.POINTER(C.c_int64)] + [C.c_void_p] * 10
         L.ref_run_experiment.argtypes = [C.c_char_p, C.c_char_p, _dp, C.POINTER(C.c_int)]
-        L.ref_meta_update_bench.argtypes = [C.c_int64, C.c_int, C.c_int, C.c_int, C.c_void_p,
-                                            C.c_void_p, C.c_double, _dp]
+        L.ref_meta_update_bench.argtypes = [C.c_int64, C.c_int, C.c_int, C.c_int, C.c_int,
+                                            C.c_void_p, C.c_void_p, C.c_double, _dp, _dp]
         L.ref_validation_suite.argtypes = [C.c_uint64, C.POINTER(C.c_int), C.POINTER(C.c_int)]
 
     def _check(self, rc):
@@ -527,13 +527,15 @@ class RefLib:
                                                 C.byref(div)))
         return sec.value, div.value
 
-    def meta_update_bench(self, props, diffs, ssn, steps, threads):
+    def meta_update_bench(self, props, diffs, ssn, steps, threads, warmup=0):
+        """Seconds per timed step (mean, median) of the reference's meta
+        update over `threads` contiguous chunks; props/diffs [pool][n]."""
         props, diffs = _f64(props), _f64(diffs)
         pool, n = props.shape
-        out = C.c_double()
-        self._check(self.lib.ref_meta_update_bench(n, steps, threads, pool, _ptr(props),
-                                                   _ptr(diffs), ssn, C.byref(out)))
-        return out.value
+        out, med = C.c_double(), C.c_double()
+        self._check(self.lib.ref_meta_update_bench(n, warmup, steps, threads, pool, _ptr(props),
+                                                   _ptr(diffs), ssn, C.byref(out), C.byref(med)))
+        return out.value, med.value
 
 
 def ref_available():

@@ -46,7 +46,11 @@ def test_bench_line_has_every_contract_key():
     assert {"sm_mhz", "sm_max_mhz", "reasons"} <= set(d["clocks"])
 
 
-def test_reference_arm_line():
-    d = _run(["--impl", "reference", "--steps", "3", "--warmup", "1", "--cpu-n", str(1 << 18)])
+def test_reference_arm_line_same_config():
+    n = 1 << 18
+    ours = _run(["--steps", "4", "--warmup", "3", "--n", str(n), "--no-extras", "--cpu-n", str(n)])
+    d = _run(["--impl", "reference", "--steps", "3", "--warmup", "1", "--n", str(n)])
     assert d["impl"] == "reference" and d["value"] > 0 and d["unit"] == "pairs/s"
     assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["cpu_baseline"]["kind"] in ("reference", "port")
+    assert ours["impl"] == "ours" and d["config"] == ours["config"]
+    assert d["metric"] == ours["metric"] and d["higher_is_better"] == ours["higher_is_better"]

@@ -194,3 +194,60 @@ def test_graph_replayed_run_is_bit_identical(api, kind, dtype):
     se, sg = re_.upd.scalars(), rg.upd.scalars()
     assert (se.ssn, se.diff_count, se.prop_decay_pow) == (sg.ssn, sg.diff_count, sg.prop_decay_pow)
     assert se.prop_decay_pow == re_.upd.beta_f_pow  # device chain == host chain
+
+
+@pytest.mark.parametrize("kind", ["quad", "mesh"])
+def test_graph_run_after_odd_eager_tail_realigns(api, kind):
+    """A graph captured with pi_t in buffer A must not be replayed while
+    pi_t sits in buffer B (after a trailing eager step, or a user step()):
+    run(13, graph) -> run(5, graph) -> step() -> run(4, graph) equals 23
+    eager steps bit for bit.  The calls are made OUTSIDE any stream context
+    (the replays must still be ordered on ctx.stream)."""
+    side = torch.cuda.Stream()
+    ctx = api.Context(0, stream=side)
+
+    def make():
+        if kind == "quad":
+            prob = api.QuadTextureProblem(32, 32, 8, target_spp=16, dtype=torch.float32, ctx=ctx)
+            return prob, api.QuadTextureRun(prob, optimizer="meta", lr=0.01)
+        prob = api.MeshTextureProblem(32, 24, 8, (8, 12), (10, 12), max_vertices=4, target_spp=4,
+                                      dtype=torch.float32, ctx=ctx, channels=4, prop_paths=2)
+        return prob, api.MeshTextureRun(prob, "meta", lr=0.01)
+
+    with torch.cuda.stream(side):
+        pe, re_ = make()
+        re_.run(23)
+        pg, rg = make()
+    torch.cuda.synchronize()
+    rg.run(13, graph=True)
+    rg.run(5, graph=True)
+    with torch.cuda.stream(side):
+        rg.step()
+    rg.run(4, graph=True)
+    torch.cuda.synchronize()
+    assert re_.t == rg.t == 23
+    assert torch.equal(re_.params, rg.params) and torch.equal(re_.prev, rg.prev)
+    for a in ("m2_prop", "m2_diff", "mean", "var", "alpha_prev"):
+        assert torch.equal(getattr(re_.upd, a), getattr(rg.upd, a)), a
+    assert pe.loss_buf.item() == pg.loss_buf.item()
+
+
+def test_device_coef_beta_f_zero(api):
+    """beta_f = 0 is a valid Moment2 decay (coefficient 1, moment2.hpp:36-38):
+    with the device-formed coefficient (graph runs) the state equals the
+    host-coefficient run bit for bit and stays finite."""
+    n = 5000
+    g = torch.Generator(device="cuda").manual_seed(3)
+    props = [torch.randn(n, device="cuda", generator=g) for _ in range(4)]
+    diffs = [0.1 * torch.randn(n, device="cuda", generator=g) for _ in range(4)]
+    outs = []
+    for dev_coef in (False, True):
+        u = api.FusedMetaUpdate(n, lr=0.01, beta_f=0.0, device_coef=dev_coef)
+        bufs = [torch.zeros(n, device="cuda"), torch.empty(n, device="cuda")]
+        for t in range(6):
+            u.step(props[t % 4], diffs[t % 4] if t else torch.zeros(n, device="cuda"),
+                   bufs[t % 2], bufs[(t + 1) % 2])
+        torch.cuda.synchronize()
+        outs.append((bufs[0].clone(), u.m2_prop.clone(), u.var.clone()))
+    for a, b in zip(*outs):
+        assert torch.isfinite(a).all() and torch.equal(a, b)

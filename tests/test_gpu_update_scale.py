@@ -1,0 +1,261 @@
+"""Parity of the headline kernel at the sizes it is benchmarked
+(BASELINE.json configs[1]): the fused meta update
+(Moment2 x2 + diff decoupling + MetaEstimator::step + update,
+moment2.hpp:30-39, meta.hpp:90-113, harness.cpp:144-187) against the
+oracle at N = 2^20 over all 100 steps, a strided subset at N = 2^24 over
+100 steps, and the TMA ring at sizes where every CTA wraps its ring at
+least twice (all 10 schedule variants + Adam, fp32 and fp64).
+
+Bars: fp64 BIT-EXACT given the same step norm; fp32 vs the fp64 oracle on
+the same (fp32) inputs rel <= 1e-4 against max(|x|, RMS of the array)."""
+import numpy as np
+import pytest
+import torch
+
+from paper_2309_15676_b200 import _abi
+
+pytestmark = pytest.mark.gpu
+
+STATE = ("m2_prop", "m2_diff", "mean", "var", "alpha_prev")
+
+
+@pytest.fixture(scope="module")
+def api():
+    from paper_2309_15676_b200 import api as a
+    return a
+
+
+def host(t):
+    return t.detach().double().cpu().numpy()
+
+
+def bits_equal(a, b):
+    a, b = np.asarray(a, dtype=np.float64), np.asarray(b, dtype=np.float64)
+    return a.shape == b.shape and np.array_equal(a.view(np.uint64), b.view(np.uint64))
+
+
+def rel_err(got, ref):
+    ok = np.isfinite(ref)
+    floor = np.sqrt(np.mean(ref[ok] ** 2)) if ok.any() else 1.0
+    return float(np.max(np.abs(got - ref) / np.maximum(np.abs(ref), max(floor, 1e-300))))
+
+
+def device_pool(n, dt, pool, seed):
+    """configs[1] inputs on the device: prop ~ N(mu, sig^2), diff ~ N(0,
+    (0.1 sig)^2), mu ~ U(-1, 1), sig ~ U(0.1, 2) (as bench.py)."""
+    g = torch.Generator(device="cuda").manual_seed(seed)
+    mu = torch.rand(n, device="cuda", dtype=dt, generator=g) * 2 - 1
+    sig = torch.rand(n, device="cuda", dtype=dt, generator=g) * 1.9 + 0.1
+    props = [mu + sig * torch.randn(n, device="cuda", dtype=dt, generator=g) for _ in range(pool)]
+    diffs = [0.1 * sig * torch.randn(n, device="cuda", dtype=dt, generator=g) for _ in range(pool)]
+    return props, diffs
+
+
+def oracle_args(t, beta_pow, ssn_host=None):
+    return _abi.MetaUpdateArgs(meta=_abi.MetaParams(0.01, 1e-8, 1e-30, 1),
+                               prop_coef=(1 - 0.9) / (1 - beta_pow), beta_delta=0.5,
+                               first_step=int(t == 0), ssn_from_host=int(ssn_host is not None),
+                               ssn_host=0.0 if ssn_host is None else ssn_host)
+
+
+def test_meta_update_f64_2p20_100_steps_bit_exact(api, oracle):
+    """N = 2^20 fp64, all 100 configs[1] steps: parameters bit-exact every
+    step, the whole state bit-exact at steps 1, 2, 10, 50, 100 (the TMA
+    ring: 2048 tiles over 148 CTAs, ~14 per CTA)."""
+    n, steps, pool = 1 << 20, 100, 4
+    props, diffs = device_pool(n, torch.float64, pool, seed=20)
+    hp, hd = [host(x) for x in props], [host(x) for x in diffs]
+    zero = torch.zeros(n, dtype=torch.float64, device="cuda")
+    upd = api.FusedMetaUpdate(n, dtype=torch.float64, lr=0.01)
+    st = {k: np.zeros(n) for k in STATE}
+    sc = _abi.fresh_scalars()
+    p = np.zeros(n)
+    pa, pb = torch.zeros(n, dtype=torch.float64, device="cuda"), torch.empty(n, dtype=torch.float64,
+                                                                              device="cuda")
+    bp = 1.0
+    for t in range(steps):
+        bp *= 0.9
+        a = oracle_args(t, bp, ssn_host=sc.ssn)
+        k = t % pool
+        p, _, rc = oracle.meta_update(a, st, hp[k], hd[k] if t else np.zeros(n), p, sc)
+        assert rc == 0
+        upd.step(props[k], diffs[k] if t else zero, pa, pb, ssn_host=a.ssn_host)
+        pa, pb = pb, pa
+        assert bits_equal(host(pa), p), t
+        if t + 1 in (1, 2, 10, 50, 100):
+            for name in STATE:
+                if name != "m2_diff" or sc.diff_count > 0:
+                    assert bits_equal(host(getattr(upd, name)), st[name]), (t, name)
+            d = upd.scalars()
+            assert d.diff_count == sc.diff_count and d.diff_decay_pow == sc.diff_decay_pow
+            assert d.changed == sc.changed and d.nonfinite == sc.nonfinite
+            np.testing.assert_allclose(d.ssn, sc.ssn, rtol=1e-12)
+
+
+def test_meta_update_f32_2p20_100_steps(api, oracle):
+    """N = 2^20 fp32, 100 steps, the bench path exactly (device step norm):
+    every array within 1e-4 of the fp64 oracle run on the same inputs."""
+    n, steps, pool = 1 << 20, 100, 4
+    props, diffs = device_pool(n, torch.float32, pool, seed=21)
+    hp, hd = [host(x) for x in props], [host(x) for x in diffs]
+    zero = torch.zeros(n, device="cuda")
+    upd = api.FusedMetaUpdate(n, dtype=torch.float32, lr=0.01)
+    st = {k: np.zeros(n) for k in STATE}
+    sc = _abi.fresh_scalars()
+    p = np.zeros(n)
+    pa, pb = torch.zeros(n, device="cuda"), torch.empty(n, device="cuda")
+    bp = 1.0
+    worst = 0.0
+    for t in range(steps):
+        bp *= 0.9
+        k = t % pool
+        p, _, rc = oracle.meta_update(oracle_args(t, bp), st, hp[k], hd[k] if t else np.zeros(n),
+                                      p, sc)
+        assert rc == 0
+        upd.step(props[k], diffs[k] if t else zero, pa, pb)
+        pa, pb = pb, pa
+        if t % 10 == 9:
+            worst = max(worst, rel_err(host(pa), p))
+    assert worst < 1e-4, worst
+    for name in STATE:
+        assert rel_err(host(getattr(upd, name)), st[name]) < 1e-4, name
+    d = upd.scalars()
+    np.testing.assert_allclose(d.ssn, sc.ssn, rtol=1e-4)
+    assert d.diff_count == sc.diff_count and d.nonfinite == 0
+
+
+@pytest.mark.parametrize("dt", [torch.float32, torch.float64])
+def test_meta_update_2p24_strided_subset(api, oracle, dt):
+    """N = 2^24, 100 steps with the device step norm (the bench path): a
+    stride-97 subset of every state array against the oracle run on that
+    subset with the step norm the device consumed (scalars.ssn_used) —
+    bit-exact in fp64, rel 1e-4 in fp32; the device step norm itself
+    against a full fp64 host sum at steps 1, 10 and 100."""
+    n, steps, pool, stride = 1 << 24, 100, 4, 97
+    props, diffs = device_pool(n, dt, pool, seed=24)
+    idx = torch.arange(0, n, stride, device="cuda")
+    hp = [host(x[idx]) for x in props]
+    hd = [host(x[idx]) for x in diffs]
+    m = idx.numel()
+    zero = torch.zeros(n, dtype=dt, device="cuda")
+    upd = api.FusedMetaUpdate(n, dtype=dt, lr=0.01)
+    st = {k: np.zeros(m) for k in STATE}
+    sc = _abi.fresh_scalars()
+    p = np.zeros(m)
+    pa, pb = torch.zeros(n, dtype=dt, device="cuda"), torch.empty(n, dtype=dt, device="cuda")
+    bp = 1.0
+    for t in range(steps):
+        bp *= 0.9
+        k = t % pool
+        p_old_full = pa.double() if t + 1 in (1, 10, 100) else None
+        upd.step(props[k], diffs[k] if t else zero, pa, pb)
+        pa, pb = pb, pa
+        d = upd.scalars()
+        p, _, rc = oracle.meta_update(oracle_args(t, bp, ssn_host=d.ssn_used), st, hp[k],
+                                      hd[k] if t else np.zeros(m), p, sc)
+        assert rc == 0
+        if p_old_full is not None:
+            ssn = float(((pa.double() - p_old_full) ** 2).sum())
+            np.testing.assert_allclose(d.ssn, ssn, rtol=1e-9 if dt == torch.float64 else 1e-6)
+            del p_old_full
+        got = host(pa[idx])
+        if dt == torch.float64:
+            assert bits_equal(got, p), t
+        elif t % 10 == 9:
+            assert rel_err(got, p) < 1e-4, t
+    for name in STATE:
+        got = host(getattr(upd, name)[idx])
+        if dt == torch.float64:
+            assert bits_equal(got, st[name]), name
+        else:
+            assert rel_err(got, st[name]) < 1e-4, name
+
+
+# ---------------------------------------------------- TMA ring wrap-around
+# csrc/update.cu tma_variant(): (threads, stages, CTAs per SM)
+VARIANTS = [(256, 4, 1), (256, 3, 2), (512, 3, 1), (128, 3, 4), (256, 2, 3), (160, 5, 2),
+            (192, 4, 2), (224, 3, 2), (96, 4, 4), (192, 3, 2)]
+N_WRAP = (1 << 21) + 777
+
+
+def tiles_per_cta(n, threads, ctas_per_sm, esz, sms):
+    tile = threads * (16 // esz)
+    return (n // tile) / min(n // tile, sms * ctas_per_sm)
+
+
+@pytest.mark.parametrize("dt", [torch.float32, torch.float64])
+@pytest.mark.parametrize("variant", range(10))
+def test_tma_ring_wraps_matches_register_kernel(api, dt, variant):
+    """Every CTA processes >= 2 x stages tiles, so the ring refill and the
+    mbarrier phase flip run many times: the TMA schedule equals the
+    register kernel bit for bit (4 steps, fixed step norms)."""
+    from paper_2309_15676_b200 import _lib
+    L = _lib.load()
+    sms = torch.cuda.get_device_properties(0).multi_processor_count
+    th, stages, cps = VARIANTS[variant]
+    esz = 4 if dt == torch.float32 else 8
+    assert tiles_per_cta(N_WRAP, th, cps, esz, sms) >= 2 * stages
+    n = N_WRAP
+    props, diffs = device_pool(n, dt, 4, seed=30 + variant)
+    target = torch.rand(n, dtype=dt, device="cuda")
+    outs = []
+    for disable in (0, 1):
+        L.mg_set_option(b"disable_tma", disable)
+        L.mg_set_option(b"tma_variant", variant)
+        try:
+            upd = api.FusedMetaUpdate(n, dtype=dt, lr=0.01, project_lo=0.0)
+            pa = torch.full((n,), 0.3, dtype=dt, device="cuda")
+            pb = torch.empty_like(pa)
+            for t in range(4):
+                upd.step(props[t], diffs[t] if t else torch.zeros_like(pa), pa, pb, target=target,
+                         ssn_host=0.0 if t == 0 else 1e-3 * t)
+                pa, pb = pb, pa
+            outs.append((pa.clone(),) + tuple(getattr(upd, s).clone() for s in STATE)
+                        + (upd.scalars(),))
+        finally:
+            L.mg_set_option(b"disable_tma", 0)
+            L.mg_set_option(b"tma_variant", -1)
+    a, b = outs
+    for x, y in zip(a[:6], b[:6]):
+        assert torch.equal(x.view(torch.int32 if esz == 4 else torch.int64),
+                           y.view(torch.int32 if esz == 4 else torch.int64))
+    for f in ("changed", "nonfinite", "diff_count", "diff_decay_pow"):
+        assert getattr(a[6], f) == getattr(b[6], f), f
+    np.testing.assert_allclose(a[6].loss, b[6].loss, rtol=1e-12)
+
+
+@pytest.mark.parametrize("dt", [torch.float32, torch.float64])
+def test_adam_tma_ring_wraps_matches_register_kernel(api, dt):
+    """Adam's TMA ring (192 threads x 4 stages, 2 CTAs/SM) with >= 8 tiles
+    per CTA equals the register kernel bit for bit."""
+    from paper_2309_15676_b200 import _lib
+    L = _lib.load()
+    sms = torch.cuda.get_device_properties(0).multi_processor_count
+    esz = 4 if dt == torch.float32 else 8
+    assert tiles_per_cta(N_WRAP, 192, 2, esz, sms) >= 8
+    n = N_WRAP
+    g = torch.Generator(device="cuda").manual_seed(5)
+    grads = [torch.randn(n, dtype=dt, device="cuda", generator=g) for _ in range(4)]
+    grads[1][::3] = 0.0
+    target = torch.rand(n, dtype=dt, device="cuda")
+    outs = []
+    for disable in (0, 1):
+        L.mg_set_option(b"disable_tma", disable)
+        try:
+            up = api.FusedAdamUpdate(n, dtype=dt, lr=0.02, project_lo=0.0)
+            pa = torch.full((n,), 0.5, dtype=dt, device="cuda")
+            pb = torch.empty_like(pa)
+            for t in range(4):
+                up.step(grads[t], pa, pb, target=target)
+                pa, pb = pb, pa
+            sc = up.scalars()
+            outs.append((pa.clone(), up.m.clone(), up.v.clone(), sc))
+        finally:
+            L.mg_set_option(b"disable_tma", 0)
+    a, b = outs
+    iv = torch.int32 if esz == 4 else torch.int64
+    for x, y in zip(a[:3], b[:3]):
+        assert torch.equal(x.view(iv), y.view(iv))
+    assert a[3].changed == b[3].changed and a[3].nonfinite == b[3].nonfinite
+    np.testing.assert_allclose(a[3].ssn, b[3].ssn, rtol=1e-12)
+    np.testing.assert_allclose(a[3].loss, b[3].loss, rtol=1e-12)
