@@ -100,7 +100,11 @@ const char* mg_last_error(void);
 int mg_abi_version(void);
 /* Process-wide tuning switches (tests/benchmarks): "disable_tma" = 1 forces
  * the register-streaming variant of mg_meta_update instead of the TMA
- * bulk-copy pipeline.  Unknown names -> MG_EINVAL. */
+ * bulk-copy pipeline; "tma_variant" (-1 = default, 0..9) picks its schedule;
+ * "render_fast" = 0 runs the IEEE fp32 mini-render kernel instead of the
+ * TMA-fed fast one; "render_fast_variant" (-1, 0..10) picks the latter's
+ * schedule; "render_vec", "bvh_leaf_size", "mesh_megakernel" as documented
+ * in DESIGN.md.  Unknown names -> MG_EINVAL. */
 int mg_set_option(const char* name, int64_t value);
 
 /* ---------------------------------------------------------------- context */

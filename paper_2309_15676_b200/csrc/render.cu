@@ -17,21 +17,14 @@
 #include "mg_common.cuh"
 #include "philox.cuh"
 #include "problems.cuh"
+#include "render.cuh"
 
 namespace mg {
-bool g_render_vec = true;  // mg_set_option("render_vec", 0) forces one pixel per thread
+bool g_render_vec = true;
+bool g_render_fast = true;  // mg_set_option("render_fast", 0): IEEE fp32 kernel everywhere  // mg_set_option("render_vec", 0) forces one pixel per thread
 namespace {
 
 constexpr int kThreads = 256;
-
-struct RenderK {
-  MetaK meta;
-  int spp;
-  int philox;  // 0: uniforms buffer (mt19937_64 stream), 1: Philox counter
-  uint64_t key;
-  uint32_t iteration, stream, pixel_offset;
-  int64_t record;  // -1: full prop/diff outputs, else only this local pixel
-};
 
 // Uniforms of one pixel into u[0..spp): Philox in pairs (one 4x32 block
 // gives two 53-bit doubles) or the mt19937_64 buffer (pixel-major).
@@ -181,6 +174,14 @@ template <class T>
 int launch(mg_ctx* ctx, int64_t P, const RenderK& k, bool first, const void* b, const void* t,
            const double* u, const void* pnow, void* pprev, void* m2p, void* m2d, void* mean,
            void* var, void* ap, void* prop_out, void* diff_out, mg_update_scalars* sc) {
+  // fp32 Philox, no per-pixel outputs, large P: the TMA-fed fast kernel
+  // (render_fast.cu)
+  if (sizeof(T) == 4 && g_render_fast && k.philox && k.record < 0 && !prop_out && !diff_out) {
+    const int rc = launch_minirender_fast(ctx, P, k, first, (const float*)b, (const float*)t,
+                                          (const float*)pnow, (float*)pprev, (float*)m2p,
+                                          (float*)m2d, (float*)mean, (float*)var, (float*)ap, sc);
+    if (rc != MG_EUNSUPPORTED) return rc;
+  }
   // fp32: 4 pixels per thread (16-byte packs, ILP across 4 Philox/pow
   // chains); fp64: one pixel per thread (the packed fp64 body needs 155 regs)
   const bool vec = g_render_vec && sizeof(T) == 4 && aligned16(b) && aligned16(t) && aligned16(pnow) && aligned16(pprev) &&

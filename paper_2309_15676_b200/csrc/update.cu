@@ -27,6 +27,9 @@ namespace mg {
 // Test/benchmark switch: force the register-streaming kernel (mg_set_option).
 bool g_disable_tma = false;
 extern bool g_render_vec;
+extern bool g_render_fast;
+extern int g_render_fast_variant;
+int render_fast_variants();
 extern bool g_mesh_megakernel;
 extern int g_bvh_leaf;
 // -1: per-dtype default measured on B200 (tools/sweep_update_variants.py,
@@ -739,6 +742,16 @@ int mg_set_option(const char* name, int64_t value) {
   }
   if (std::string(name) == "render_vec") {
     g_render_vec = value != 0;
+    return MG_OK;
+  }
+  if (std::string(name) == "render_fast") {
+    g_render_fast = value != 0;
+    return MG_OK;
+  }
+  if (std::string(name) == "render_fast_variant") {
+    if (value < -1 || value >= render_fast_variants())
+      return fail(MG_EINVAL, "render_fast_variant out of range");
+    g_render_fast_variant = int(value);
     return MG_OK;
   }
   if (std::string(name) == "tma_variant") {
