@@ -103,7 +103,8 @@ int mg_abi_version(void);
  * bulk-copy pipeline; "tma_variant" (-1 = default, 0..9) picks its schedule;
  * "render_fast" = 0 runs the IEEE fp32 mini-render kernel instead of the
  * TMA-fed fast one; "render_fast_variant" (-1, 0..10) picks the latter's
- * schedule; "render_vec", "bvh_leaf_size", "mesh_megakernel" as documented
+ * schedule; "cluster_runner" = 0 keeps few-replicate mini-render runs on the
+ * one-CTA-per-replicate runner; "render_vec", "bvh_leaf_size", "mesh_megakernel" as documented
  * in DESIGN.md.  Unknown names -> MG_EINVAL. */
 int mg_set_option(const char* name, int64_t value);
 

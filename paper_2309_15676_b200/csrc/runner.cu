@@ -25,6 +25,9 @@
 #include "problems.cuh"
 
 namespace mg {
+// mg_set_option("cluster_runner", 0): few-replicate mini-render runs on the
+// one-CTA-per-replicate kernel too
+bool g_cluster_runner = true;
 namespace {
 
 constexpr int kThreads = 256;
@@ -398,6 +401,476 @@ __global__ void __launch_bounds__(kThreads) run_kernel(RunK<T> k) {
     for (int j = threadIdx.x; j < d; j += kThreads) k.final_params[off + j] = double(prev[j]);
 }
 
+// --------------------------------------------- one replicate per cluster
+// run_single (harness.cpp:90-200) of ONE mini-render replicate spread over a
+// thread-block cluster instead of one CTA, for the few-replicate case (the
+// S1 configuration: P = 4096, 200 iterations, one replicate would otherwise
+// use 1 of 148 SMs).  CTA rank 0 is the producer: it runs the replicate's
+// exact std::mt19937_64 stream (Rng::stream, rng.hpp:23-36) and writes each
+// iteration's D uniforms to global memory (L2-resident), publishing its
+// progress with a release store.  Ranks 1..NC-1 are consumers: each owns a
+// contiguous pixel range with the whole optimiser state in REGISTERS for
+// the entire run, and per iteration computes the sample pair
+// (problems.cpp:197-217), Moment2 x2, MetaEstimator::step / Adam::step,
+// the record of `coord`, and the update + projection.  The four sums the
+// next iteration needs (step norm and loss of the new parameters, all
+// finite, params == prev) are block-reduced and exchanged through
+// distributed shared memory: every consumer stores its partials into every
+// consumer's slot and arrives on that CTA's mbarrier; each then sums the
+// slots in rank order, so all consumers hold identical totals (fixed order:
+// deterministic) after ONE exchange per iteration.
+constexpr int kClusterMax = 16;
+constexpr int kPPT = 4;  // pixels per consumer thread (registers)
+
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ uint32_t cluster_size() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_nctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;"
+               ::: "memory");
+}
+__device__ __forceinline__ uint32_t map_rank(const void* p, uint32_t rank) {
+  uint32_t out;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;"
+               : "=r"(out) : "r"(uint32_t(__cvta_generic_to_shared(p))), "r"(rank));
+  return out;
+}
+__device__ __forceinline__ void st_cluster_f64(uint32_t addr, double v) {
+  asm volatile("st.shared::cluster.f64 [%0], %1;" ::"r"(addr), "d"(v) : "memory");
+}
+__device__ __forceinline__ void arrive_cluster(uint32_t bar_addr) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(bar_addr)
+               : "memory");
+}
+__device__ __forceinline__ bool try_wait_cluster(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(uint32_t(__cvta_generic_to_shared(bar))), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+__device__ __forceinline__ void mbar_init_cta(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(uint32_t(__cvta_generic_to_shared(bar))),
+               "r"(count) : "memory");
+}
+
+// The producer: the replicate's std::mt19937_64 stream written to `out`
+// as uniform() doubles (rng.hpp:28), `total` of them, with `progress`
+// (draws published) advanced by release stores.  The state recurrence
+// w[j] = w[j-156] ^ mag(w[j-312], w[j-311]) (the twist of
+// random.tcc:399, sequential form) advances in chunks of 156 words, each
+// depending only on the two chunks before it: warp 0 computes the chunks
+// (5 words per lane, one __syncwarp per chunk) into a shared ring while
+// warps 1..7 temper, convert and store finished batches of 8 chunks,
+// double-buffered through two mbarrier pairs.  Output o is temper(w[312 +
+// o]), as after libstdc++'s seeding (random.tcc:328-343, first call
+// twists).
+constexpr int kChunkW = kMtM;                    // 156 words per chunk
+constexpr int kBatchChunks = 8;                  // chunks per emitted batch
+constexpr int kRingChunks = 2 * kBatchChunks;    // two batches in flight
+constexpr int kBatchWords = kBatchChunks * kChunkW;
+constexpr int kEmitThreads = kThreads - 32;
+
+__device__ __forceinline__ void named_sync(int id, int n) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+
+__device__ void produce_stream(uint64_t* ring, uint64_t* pbar, uint64_t seed, uint64_t rep,
+                               int64_t total, double* out, unsigned long long* progress) {
+  uint64_t* full = pbar;       // [2]: batch written (count 1)
+  uint64_t* empty = pbar + 2;  // [2]: batch emitted (count 1)
+  auto slot = [&](int64_t chunk) {
+    return ring + size_t(((chunk % kRingChunks) + kRingChunks) % kRingChunks) * kChunkW;
+  };
+  if (threadIdx.x == 0) {
+    // Rng::stream(seed, rep) (rng.hpp:23-25): w[0..311] = chunks -2, -1
+    uint64_t w[2];
+    const uint64_t s0 = mg_mix64_dev(mg_mix64_dev(seed) ^ (rep + 0x51ed2701e35f3a6dULL));
+    uint64_t* c2 = slot(-2);
+    uint64_t* c1 = slot(-1);
+    w[0] = s0;
+    c2[0] = s0;
+    for (int i = 1; i < kMtN; ++i) {
+      uint64_t x = w[0];
+      x ^= x >> 62;
+      w[0] = 6364136223846793005ULL * x + static_cast<uint64_t>(i);
+      (i < kChunkW ? c2[i] : c1[i - kChunkW]) = w[0];
+    }
+    (void)w[1];
+    for (int q = 0; q < 4; ++q) mbar_init_cta(&pbar[q], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  const int64_t chunks = (total + kChunkW - 1) / kChunkW;
+  const int64_t batches = (chunks + kBatchChunks - 1) / kBatchChunks;
+  if (threadIdx.x < 32) {  // twister warp
+    const int l = threadIdx.x;
+    for (int64_t b = 0; b < batches; ++b) {
+      if (b >= 2) {  // the emitters are done with this half of the ring
+        while (!try_wait_cluster(&empty[b & 1], uint32_t(((b - 2) >> 1) & 1))) {
+        }
+      }
+      for (int64_t kc = b * kBatchChunks; kc < (b + 1) * kBatchChunks; ++kc) {
+        const uint64_t* p1 = slot(kc - 1);
+        const uint64_t* p2 = slot(kc - 2);
+        uint64_t* nw = slot(kc);
+        uint64_t v[5];
+#pragma unroll
+        for (int q = 0; q < 5; ++q) {
+          const int t = l + 32 * q;
+          if (t < kChunkW) {
+            const uint64_t nxt = t + 1 < kChunkW ? p2[t + 1] : p1[0];
+            v[q] = p1[t] ^ mt_mag(p2[t], nxt);
+          }
+        }
+#pragma unroll
+        for (int q = 0; q < 5; ++q)
+          if (l + 32 * q < kChunkW) nw[l + 32 * q] = v[q];
+        __syncwarp();
+      }
+      if (l == 0)
+        asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(
+                         uint32_t(__cvta_generic_to_shared(&full[b & 1])))
+                     : "memory");
+    }
+  } else {  // emitter warps
+    const int e = threadIdx.x - 32;
+    for (int64_t b = 0; b < batches; ++b) {
+      while (!try_wait_cluster(&full[b & 1], uint32_t((b >> 1) & 1))) {
+      }
+      const int64_t base = b * kBatchWords;
+      for (int o = e; o < kBatchWords; o += kEmitThreads) {
+        const int64_t g = base + o;
+        if (g < total) out[g] = mt_uniform(mt_temper(slot(b * kBatchChunks + o / kChunkW)[o % kChunkW]));
+      }
+      named_sync(1, kEmitThreads);
+      if (e == 0) {
+        asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(
+                         uint32_t(__cvta_generic_to_shared(&empty[b & 1])))
+                     : "memory");
+        __threadfence();
+        const int64_t done = base + kBatchWords < total ? base + kBatchWords : total;
+        asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(progress),
+                     "l"((unsigned long long)done)
+                     : "memory");
+      }
+    }
+  }
+}
+
+template <class T>
+__global__ void __launch_bounds__(kThreads) run_cluster_kernel(RunK<T> k, double* ubuf_all,
+                                                               unsigned long long* progress_all) {
+  __shared__ uint64_t ring[kRingChunks * kChunkW];
+  __shared__ __align__(8) uint64_t pbar[4];
+  __shared__ double sw[kThreads / 32];
+  __shared__ double xch[2][kClusterMax][4];  // [parity][source rank][sum]
+  __shared__ double wsum[kThreads / 32][4];
+  __shared__ __align__(8) uint64_t xbar[2];
+  __shared__ double tot[4];
+  const mg_experiment_config& c = k.cfg;
+  const uint32_t rank = cluster_rank(), NC = cluster_size(), M = NC - 1;
+  const int r = blockIdx.x / NC;  // replicate within the launch
+  const int d = k.dim, iters = c.iterations, spp = c.spp;
+  const int64_t D = k.D;
+  double* ubuf = ubuf_all + size_t(r) * iters * D;
+  unsigned long long* progress = progress_all + r;
+  if (threadIdx.x == 0) {
+    mbar_init_cta(&xbar[0], M);
+    mbar_init_cta(&xbar[1], M);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  cluster_sync_all();  // every CTA of the cluster is running and initialised
+
+  if (rank == 0) {  // ------------------------------------------ producer
+    produce_stream(ring, pbar, c.seed, uint64_t(k.rep_begin + r), int64_t(iters) * D, ubuf,
+                   progress);
+    cluster_sync_all();
+    return;
+  }
+  // ------------------------------------------------------------ consumers
+  const int me = int(rank) - 1;
+  const int lo = int((int64_t(d) * me) / M), hi = int((int64_t(d) * (me + 1)) / M);
+  const bool use_meta = c.optimizer == MG_OPT_META;
+  const bool per_param = c.diff_norm == MG_DIFF_NORM_PER_PARAM;
+  T p[kPPT], pv[kPPT], m2p[kPPT], m2d[kPPT], mean[kPPT], var[kPPT], ap[kPPT];
+  double bj[kPPT], tj[kPPT];
+  bool own[kPPT];
+#pragma unroll
+  for (int q = 0; q < kPPT; ++q) {
+    const int j = lo + int(threadIdx.x) + q * kThreads;
+    own[q] = j < hi;
+    bj[q] = own[q] ? k.exponents[j] : 0.0;
+    tj[q] = own[q] ? k.truth[j] : 0.0;
+    p[q] = pv[q] = T(own[q] ? k.init[j] : 0.0);
+    m2p[q] = m2d[q] = mean[q] = var[q] = ap[q] = T(0);
+  }
+  // cluster-wide sums of 4 per-thread values; identical in every consumer
+  int xi = 0;  // exchange counter (parity = xi & 1, phase = (xi >> 1) & 1)
+  auto exchange = [&](double a0, double a1, double a2, double a3) {
+    // one fixed-shape block tree for the four sums (warp shuffles, then
+    // warp 0 over the warp partials)
+    double v[4] = {a0, a1, a2, a3};
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+      for (int q = 0; q < 4; ++q) v[q] += __shfl_down_sync(0xffffffffu, v[q], o);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (lane == 0)
+#pragma unroll
+      for (int q = 0; q < 4; ++q) wsum[warp][q] = v[q];
+    __syncthreads();
+    const int par = xi & 1;
+    if (warp == 0) {
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        double x = lane < kThreads / 32 ? wsum[lane][q] : 0.0;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) x += __shfl_down_sync(0xffffffffu, x, o);
+        v[q] = __shfl_sync(0xffffffffu, x, 0);
+      }
+      // lane t < M stores this CTA's sums into consumer t+1's slot and
+      // arrives on its barrier: the M remote round trips run in parallel
+      if (lane < int(M)) {
+        const uint32_t dst = uint32_t(lane) + 1;
+        const uint32_t slot = map_rank(&xch[par][rank][0], dst);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) st_cluster_f64(slot + 8u * q, v[q]);
+        arrive_cluster(map_rank(&xbar[par], dst));
+      }
+      if (lane == 0) {
+        while (!try_wait_cluster(&xbar[par], uint32_t((xi >> 1) & 1))) {
+        }
+        double t[4] = {0.0, 0.0, 0.0, 0.0};
+        for (uint32_t src = 1; src < NC; ++src)
+#pragma unroll
+          for (int q = 0; q < 4; ++q) t[q] += xch[par][src][q];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) tot[q] = t[q];
+      }
+    }
+    ++xi;
+    __syncthreads();
+  };
+  // sums over the initial parameters: loss, all finite
+  {
+    double l = 0.0, nf = 0.0;
+#pragma unroll
+    for (int q = 0; q < kPPT; ++q)
+      if (own[q]) {
+        const double e = double(p[q]) - tj[q];
+        l += e * e;
+        nf += isfinite(double(p[q])) ? 0.0 : 1.0;
+      }
+    exchange(0.0, l, nf, 0.0);
+  }
+  double ssn = 0.0, loss = tot[1], loss_rec = 0.0;
+  bool finite = tot[2] == 0.0, same_pp = true;  // params == prev at the start
+  double pf_pow = 1.0, pd_pow = 1.0, b1p = 1.0, b2p = 1.0;
+  int64_t pf_cnt = 0, pd_cnt = 0, t_adam = 0;
+  bool meta_first = true;
+  int status = 0, iters_run = 0;
+  int64_t draws = 0, evals = 0;
+  const int coord = c.coord;
+  for (int i = 0; i < iters; ++i) {
+    if (!finite) {  // harness.cpp:116-119
+      status = 2;
+      break;
+    }
+    const bool same = use_meta ? same_pp : true;
+    loss_rec = loss;
+    if (threadIdx.x == 0) {  // this iteration's uniforms are drawn
+      const unsigned long long need = (unsigned long long)(i + 1) * (unsigned long long)D;
+      unsigned long long v;
+      do {
+        asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(progress) : "memory");
+      } while (v < need);
+    }
+    __syncthreads();
+    const double* u = ubuf + size_t(i) * D;
+    const bool two_point = use_meta && !same_pp;  // :129
+    draws += D;
+    evals += D * (two_point ? 2 : 1);
+    // Moment2 / Adam scalars (moment2.hpp:34-38, adam.hpp:29-31), uniform
+    const bool pf_first = pf_cnt == 0;
+    double cp = 0.0, cd = 0.0, norm = 0.0;
+    const bool active = ssn > 0.0;
+    const bool pd_had = pd_cnt > 0;
+    if (use_meta) {
+      pf_cnt += 1;
+      pf_pow = pf_pow * c.beta_f;
+      cp = (1.0 - c.beta_f) / (1.0 - pf_pow);
+      if (active) {
+        pd_cnt += 1;
+        pd_pow = pd_pow * c.beta_delta;
+      }
+      cd = (1.0 - c.beta_delta) / (1.0 - pd_pow);
+      norm = sqrt(ssn);
+    }
+    const bool adam_first = t_adam == 0;
+    if (!use_meta) {
+      t_adam += 1;
+      b1p = b1p * c.beta1;
+      b2p = b2p * c.beta2;
+    }
+    double a_ssn = 0.0, a_loss = 0.0, a_nf = 0.0, a_ne = 0.0;
+#pragma unroll
+    for (int q = 0; q < kPPT; ++q) {
+      if (!own[q]) continue;
+      const int j = lo + int(threadIdx.x) + q * kThreads;
+      // sample_pair (problems.cpp:197-217)
+      T cross, mb;
+      const double* uj = u + size_t(j) * spp;
+      minirender_terms_fn<T>(bj[q], spp, [&](int s) { return __ldcg(uj + s); }, cross, mb);
+      const T a = p[q];
+      const T prop = (T(2) * a) * cross - (T(2) * T(tj[q])) * mb;
+      const T diff = same ? T(0) : (T(2) * (a - (use_meta ? pv[q] : a))) * cross;
+      T mest, vest, al = T(0), dl;
+      if (use_meta) {
+        const T m2p_old = pf_first ? T(0) : m2p[q];
+        const T m2pv = m2p_old + T(cp) * (prop * prop - m2p_old);  // :144
+        m2p[q] = m2pv;
+        T m2dv = pd_had ? m2d[q] : T(0);
+        T var_diff = T(0);
+        if (per_param) {  // :146-151
+          const T cs = fabs(p[q] - pv[q]);
+          if (active) {
+            const T tiny = sizeof(T) == 8 ? T(1e-150) : T(1e-37);
+            const T xd = diff / std_max(cs, tiny);
+            m2dv = m2dv + T(cd) * (xd * xd - m2dv);
+            m2d[q] = m2dv;
+          }
+          if (pd_cnt > 0) var_diff = m2dv * (cs * cs);
+        } else {  // :153-157
+          if (active) {
+            const T xd = diff / T(norm);
+            m2dv = m2dv + T(cd) * (xd * xd - m2dv);
+            m2d[q] = m2dv;
+          }
+          if (pd_cnt > 0) var_diff = m2dv * T(ssn);
+        }
+        T m = (meta_first ? T(0) : mean[q]) + diff;  // meta.hpp:92-112
+        T v = (meta_first ? T(0) : var[q]) + var_diff;
+        const T a_prev = meta_first ? T(-INFINITY) : ap[q];
+        al = m2pv / ((m2pv + v) + T(c.eps_alpha));
+        if (!c.no_alpha_clip) al = std_min(al, T(1) / (T(2) - a_prev));
+        ap[q] = al;
+        const T om = T(1) - al;
+        m = al * m + om * prop;
+        v = (al * al) * v + (om * om) * m2pv;
+        mean[q] = m;
+        var[q] = v;
+        mest = m;
+        vest = v;
+        dl = (T(-c.lr) * m) / (sqrt(v) + T(c.eps_step));
+      } else {  // Adam (adam.hpp:23-37); m2p/m2d hold m/v
+        const T c1 = T(1.0 - c.beta1), c2 = T(1.0 - c.beta2);
+        const T d1 = T(1.0 - b1p), d2 = T(1.0 - b2p);
+        const T mm = T(c.beta1) * (adam_first ? T(0) : m2p[q]) + c1 * prop;
+        const T vv = T(c.beta2) * (adam_first ? T(0) : m2d[q]) + c2 * (prop * prop);
+        m2p[q] = mm;
+        m2d[q] = vv;
+        mest = mm / d1;
+        vest = vv / d2;
+        dl = (T(-c.lr) * mest) / (sqrt(vest) + T(c.adam_eps));
+      }
+      if (j == coord) {  // record iteration i (harness.cpp:170-180)
+        const size_t at = size_t(r) * iters + i;
+        const double x = double(a);
+        const double vals[kNumSeries] = {sqrt(loss), loss, double(prop), double(diff),
+                                         double(mest), double(vest),
+                                         use_meta ? double(al) : nan(""), double(dl),
+                                         2.0 * (x - tj[q]), ssn, x};
+        for (int sx = 0; sx < kNumSeries; ++sx)
+          if (k.series[sx]) k.series[sx][at] = vals[sx];
+      }
+      // prev = params; params += delta; project (harness.cpp:182-188, problems.cpp:228)
+      const T np = std_max(a + dl, T(0));
+      pv[q] = a;
+      p[q] = np;
+      const double dd = double(np) - double(a);
+      a_ssn += dd * dd;
+      const double e = double(np) - tj[q];
+      a_loss += e * e;
+      a_nf += isfinite(double(np)) ? 0.0 : 1.0;
+      a_ne += (np == a) ? 0.0 : 1.0;
+    }
+    if (use_meta) meta_first = false;
+    iters_run = i + 1;
+    exchange(a_ssn, a_loss, a_nf, a_ne);
+    same_pp = tot[3] == 0.0;
+    ssn = (use_meta && !same_pp) ? tot[0] : 0.0;  // problems.cpp:206-209, 214 (Adam: no FD)
+    loss = tot[1];
+    finite = tot[2] == 0.0;
+  }
+  // final params = prev = the last recorded params (harness.cpp:116-119,
+  // 182-188); converged status (harness.cpp:191-198) on their loss
+  if (k.final_params)
+#pragma unroll
+    for (int q = 0; q < kPPT; ++q) {
+      const int j = lo + int(threadIdx.x) + q * kThreads;
+      if (own[q]) k.final_params[size_t(r) * d + j] = double(pv[q]);
+    }
+  if (me == 0 && threadIdx.x == 0) {
+    if (status != 2 && c.converge_threshold > 0.0 && iters_run > 0 &&
+        sqrt(loss_rec) < c.converge_threshold)
+      status = 1;
+    mg_run_record rec;
+    rec.iterations_run = iters_run;
+    rec.status = status;
+    rec.draws_used = draws;
+    rec.evals_used = evals;
+    k.recs[r] = rec;
+  }
+  cluster_sync_all();
+}
+
+// Cluster size for the one-replicate-per-cluster runner: 16 CTAs (15
+// consumers) when the device can co-schedule them, else 8; 0 = use the
+// one-CTA-per-replicate kernel (many replicates fill the GPU better that
+// way, or the pixels do not fit the consumers' registers).
+template <class T>
+int cluster_runner_size(mg_ctx* ctx, int d, int R) {
+  for (int nc : {16, 8}) {
+    if (d > (nc - 1) * kThreads * kPPT) continue;
+    if (int64_t(R) * nc > int64_t(ctx->sm_count)) continue;
+    if (nc > 8 && cudaFuncSetAttribute(run_cluster_kernel<T>,
+                                       cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess) {
+      cudaGetLastError();
+      continue;
+    }
+    cudaLaunchConfig_t lc = {};
+    lc.gridDim = dim3(unsigned(R * nc));
+    lc.blockDim = dim3(kThreads);
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = unsigned(nc);
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    lc.attrs = at;
+    lc.numAttrs = 1;
+    int clusters = 0;
+    if (cudaOccupancyMaxActiveClusters(&clusters, run_cluster_kernel<T>, &lc) != cudaSuccess) {
+      cudaGetLastError();
+      continue;
+    }
+    if (clusters >= R) return nc;  // every replicate's cluster co-resident
+  }
+  return 0;
+}
+
 // ------------------------------------------------------------- host side
 int problem_dim(const mg_experiment_config* c) {
   return c->problem == MG_EXP_RATE ? 1 : (c->problem == MG_MULT_NOISE ? c->dim : c->pixel_count);
@@ -579,7 +1052,39 @@ int run_replicates(mg_ctx* ctx, const mg_experiment_config* cfg, int rep_begin, 
     }
     cudaMemsetAsync(k.full, 0xff, full_bytes, s);  // NaN past iterations_run
   }
-  run_kernel<T><<<R, kThreads, 0, s>>>(k);
+  // few replicates of a mini-render run: one cluster per replicate
+  int nc = 0;
+  if (g_cluster_runner && cfg->problem == MG_MINI_RENDER && cfg->trajectory == MG_TRAJ_OPTIMISE &&
+      !cfg->independent_variance_samples && !full &&
+      sizeof(double) * size_t(R) * iters * D <= (size_t(1) << 30))
+    nc = cluster_runner_size<T>(ctx, d, R);
+  if (nc > 0) {
+    double* ubuf = (double*)dalloc(sizeof(double) * size_t(R) * iters * D);
+    auto* progress = (unsigned long long*)dalloc(sizeof(unsigned long long) * size_t(R));
+    if (!ubuf || !progress) {
+      cleanup();
+      return fail(MG_ENOMEM, "run: allocation failed (cluster runner)");
+    }
+    cudaMemsetAsync(progress, 0, sizeof(unsigned long long) * size_t(R), s);
+    cudaLaunchConfig_t lc = {};
+    lc.gridDim = dim3(unsigned(R * nc));
+    lc.blockDim = dim3(kThreads);
+    lc.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = unsigned(nc);
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    lc.attrs = at;
+    lc.numAttrs = 1;
+    cudaError_t le = cudaLaunchKernelEx(&lc, run_cluster_kernel<T>, k, ubuf, progress);
+    if (le != cudaSuccess) {
+      cleanup();
+      return cuda_fail(le, "run_cluster_kernel");
+    }
+  } else {
+    run_kernel<T><<<R, kThreads, 0, s>>>(k);
+  }
   ctx->launches++;
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {

@@ -28,6 +28,7 @@ namespace mg {
 bool g_disable_tma = false;
 extern bool g_render_vec;
 extern bool g_render_fast;
+extern bool g_cluster_runner;
 extern int g_render_fast_variant;
 int render_fast_variants();
 extern bool g_mesh_megakernel;
@@ -742,6 +743,10 @@ int mg_set_option(const char* name, int64_t value) {
   }
   if (std::string(name) == "render_vec") {
     g_render_vec = value != 0;
+    return MG_OK;
+  }
+  if (std::string(name) == "cluster_runner") {
+    g_cluster_runner = value != 0;
     return MG_OK;
   }
   if (std::string(name) == "render_fast") {

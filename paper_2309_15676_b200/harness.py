@@ -222,12 +222,13 @@ class AggregateReport:
 
 
 def _seq_sum(x: np.ndarray, axis: int = 0) -> np.ndarray:
-    """Sequential (index-order) sum along axis: the last element of a prefix
-    sum, which numpy evaluates left to right — identical to stats.hpp's
-    `for (double x : xs) s += x` (np.sum would sum pairwise)."""
-    if x.shape[axis] == 0:
-        return np.zeros(np.delete(x.shape, axis))
-    return np.take(np.cumsum(x, axis=axis), -1, axis=axis)
+    """Sequential (index-order) sum along axis starting from 0.0: the last
+    element of a prefix sum over a leading zero, which numpy evaluates left
+    to right — identical to stats.hpp's `double s = 0.0; for (double x : xs)
+    s += x` (np.sum would sum pairwise; a bare cumsum would keep a lone -0.0)."""
+    x = np.moveaxis(np.asarray(x, dtype=np.float64), axis, 0)
+    z = np.concatenate([np.zeros((1,) + x.shape[1:]), x], axis=0)
+    return np.cumsum(z, axis=0)[-1]
 
 
 def _column_stats(vals: np.ndarray):
@@ -253,20 +254,51 @@ SERIES_ORDER = ["param_err", "loss", "prop", "diff", "grad_est", "est_var", "alp
                 "true_grad", "step_sq_norm"]
 
 
+def _stats_columns(cols: np.ndarray, mask: np.ndarray):
+    """_column_stats of every iteration column at once: cols [R][T] in
+    replicate order, mask [R][T] = replicate active at that iteration.
+    The same arithmetic per column (stats.hpp:45-68): sums sequential in
+    replicate order starting from 0.0 (cumsum over a leading zero row; the
+    masked-out entries add +0.0, which leaves every partial sum unchanged),
+    quantiles by linear interpolation over the sorted active values (NaN
+    last, as std::sort places them for these inputs)."""
+    R, T = cols.shape
+    n = mask.sum(axis=0)
+    z = np.zeros((R + 1, T))
+    z[1:] = np.where(mask, cols, 0.0)
+    with np.errstate(invalid="ignore", divide="ignore"):
+        mean = np.cumsum(z, axis=0)[-1] / n
+        mean = np.where(n > 0, mean, math.nan)
+        dev = cols - mean
+        z[1:] = np.where(mask, dev * dev, 0.0)
+        var = np.where(n >= 2, np.cumsum(z, axis=0)[-1] / (n - 1), 0.0)
+    srt = np.sort(np.where(mask, cols, math.nan), axis=0)
+    cidx = np.arange(T)
+
+    def q(p):
+        pos = p * (n - 1)
+        lo = np.maximum(pos, 0).astype(np.int64)
+        last = srt[np.maximum(n - 1, 0), cidx]
+        lo_c = np.minimum(lo, max(R - 1, 0))
+        hi_c = np.minimum(lo + 1, max(R - 1, 0))
+        frac = pos - lo
+        interp = srt[lo_c, cidx] * (1.0 - frac) + srt[hi_c, cidx] * frac
+        out = np.where(lo + 1 >= n, last, interp)
+        return np.where(n > 0, out, math.nan)
+    return mean, var, q(0.5), q(0.25), q(0.75)
+
+
 def aggregate(cfg: ExperimentConfig, records: List[RunRecord]) -> AggregateReport:
     """Per-iteration reduction in replicate order (harness.cpp:274-302)."""
     it = cfg.iterations
     names = [n for n in SERIES_ORDER if cfg.optimizer == "meta" or n != "alpha"]
     runs = np.array([r.iterations_run for r in records])
-    active = np.array([int(np.sum(runs > i)) for i in range(it)])
+    mask = runs[:, None] > np.arange(it)[None, :]
+    active = mask.sum(axis=0)
     stats = {}
     for n in names:
-        cols = np.stack([r.series[n] for r in records])  # [R][it], replicate order
-        st = SeriesStats(*(np.empty(it) for _ in range(5)))
-        for i in range(it):
-            vals = cols[runs > i, i]
-            st.mean[i], st.variance[i], st.median[i], st.q25[i], st.q75[i] = _column_stats(vals)
-        stats[n] = st
+        cols = np.stack([np.asarray(r.series[n], dtype=np.float64) for r in records])
+        stats[n] = SeriesStats(*_stats_columns(cols, mask))
     div = sum(1 for r in records if r.status == "diverged")
     return AggregateReport(cfg, names, stats, active, div, records)
 

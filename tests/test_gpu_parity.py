@@ -634,3 +634,53 @@ def test_fused_meta_update_empty_and_nonfinite(api, oracle):
     assert np.array_equal(np.isfinite(got), fin)
     assert bits_equal(got[fin], p_host[fin])
     assert upd.scalars().nonfinite >= 2
+
+
+CLUSTER_CFGS = [
+    dict(problem="mini-render", pixel_count=4096, spp=2, iterations=60, lr=0.01, seed=0,
+         problem_seed=1),
+    dict(problem="mini-render", pixel_count=3001, spp=3, iterations=40, lr=0.03, seed=5,
+         problem_seed=2, coord=2999, diff_norm="per-param"),
+    dict(problem="mini-render", pixel_count=777, spp=2, iterations=30, lr=0.02, seed=1,
+         problem_seed=3, optimizer="adam", coord=5),
+    dict(problem="mini-render", pixel_count=2048, spp=2, iterations=50, lr=0.05, seed=2,
+         problem_seed=4, no_alpha_clip=True, converge_threshold=30.0),
+    dict(problem="mini-render", pixel_count=9000, spp=2, iterations=25, lr=0.01, seed=3,
+         problem_seed=5, coord=8999),
+    dict(problem="mini-render", pixel_count=1000, spp=2, iterations=30, lr=1e300, seed=4,
+         problem_seed=6),
+]
+
+
+@pytest.mark.parametrize("i", range(len(CLUSTER_CFGS)))
+@pytest.mark.parametrize("dtype", ["f64", "f32"])
+def test_cluster_runner_matches_cta_runner(api, i, dtype):
+    """The one-replicate-per-cluster runner (producer CTA + consumer CTAs
+    holding the state in registers, DSMEM all-reduce) against the
+    one-CTA-per-replicate runner on the same configurations (meta, Adam,
+    per-parameter norm, no clip, convergence, divergence, several
+    replicates): identical records (iterations, status, draws, evals) and
+    series within 1e-9 (fp64; the sums are trees of different shape) / 1e-5
+    (fp32)."""
+    from paper_2309_15676_b200 import _lib
+    L = _lib.load()
+    cfg = api.ExperimentConfig(dtype=dtype, replicates=3, **CLUSTER_CFGS[i])
+    out = {}
+    for flag in (1, 0):
+        L.mg_set_option(b"cluster_runner", flag)
+        try:
+            out[flag] = [api.run_single(cfg, r) for r in (0, 2)] + \
+                api._run_device(cfg, 0, 3)
+        finally:
+            L.mg_set_option(b"cluster_runner", 1)
+    tol = 1e-9 if dtype == "f64" else 1e-5
+    for a, b in zip(out[1], out[0]):
+        assert (a.status, a.iterations_run, a.draws_used, a.evals_used) == \
+            (b.status, b.iterations_run, b.draws_used, b.evals_used)
+        for name in a.series:
+            x, y = np.asarray(a.series[name]), np.asarray(b.series[name])
+            assert np.array_equal(np.isnan(x), np.isnan(y)), name
+            ok = ~np.isnan(x)
+            scale = np.max(np.abs(y[ok])) if ok.any() else 1.0
+            np.testing.assert_allclose(x[ok], y[ok], rtol=tol, atol=tol * scale, err_msg=name)
+        np.testing.assert_allclose(a.final_params, b.final_params, rtol=tol, atol=tol)

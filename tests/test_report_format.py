@@ -179,3 +179,26 @@ def test_device_run_all_writers_byte_identical_to_reference(tmp_path, kw, rep):
     ours_rep = str(tmp_path / "ours_rep.csv")
     report.write_replicate_csv(rec, ours_rep)
     assert open(ours_rep, "rb").read() == open(ref_rep, "rb").read()
+
+
+def test_vectorised_aggregate_equals_per_column_stats():
+    """harness.aggregate reduces every iteration column at once; it must
+    equal _column_stats (stats.hpp:45-68) column by column, bit for bit,
+    with ragged replicates (diverged early), NaN values, signed zeros,
+    one-replicate and empty columns."""
+    from paper_2309_15676_b200 import harness as H
+    rs = np.random.RandomState(3)
+    for R, T in ((1, 7), (2, 5), (9, 40), (33, 17)):
+        cols = rs.standard_normal((R, T)) * 10 ** rs.uniform(-3, 3, (R, T))
+        cols[rs.uniform(size=(R, T)) < 0.05] = np.nan
+        cols[rs.uniform(size=(R, T)) < 0.05] = -0.0
+        cols[:, 0] = -0.0
+        runs = rs.randint(0, T + 1, R)
+        runs[0] = T
+        mask = runs[:, None] > np.arange(T)[None, :]
+        got = H._stats_columns(cols, mask)
+        for i in range(T):
+            ref = H._column_stats(cols[mask[:, i], i])
+            for k in range(5):
+                a, b = np.float64(got[k][i]), np.float64(ref[k])
+                assert (np.isnan(a) and np.isnan(b)) or a.tobytes() == b.tobytes(), (R, T, i, k, a, b)
