@@ -104,7 +104,8 @@ int mg_abi_version(void);
  * "render_fast" = 0 runs the IEEE fp32 mini-render kernel instead of the
  * TMA-fed fast one; "render_fast_variant" (-1, 0..10) picks the latter's
  * schedule; "cluster_runner" = 0 keeps few-replicate mini-render runs on the
- * one-CTA-per-replicate runner; "render_vec", "bvh_leaf_size", "mesh_megakernel" as documented
+ * one-CTA-per-replicate runner; "mesh_persistent" (-1 auto, bit 0 isect, bit 1 shadow; 0 runs the fp32 mesh
+ * isect / shadow stages one ray per thread); "render_vec", "bvh_leaf_size", "mesh_megakernel" as documented
  * in DESIGN.md.  Unknown names -> MG_EINVAL. */
 int mg_set_option(const char* name, int64_t value);
 

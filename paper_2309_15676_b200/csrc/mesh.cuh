@@ -40,6 +40,13 @@ namespace mg {
 // mg_set_option("mesh_megakernel", 1): one-thread-per-pixel megakernel
 // instead of the default wavefront stages (A/B comparison; identical results)
 extern bool g_mesh_megakernel;
+// mg_set_option("mesh_persistent", 0): fp32 isect / shadow stages with the
+// grid-stride one-ray-per-thread traversal instead of the persistent warp loop
+// bit 0: isect, bit 1: shadow; -1 (default): shadow always, isect for scenes
+// of >= kPersistentIsectNodes BVH nodes (configs[4]: -0.4 ms; on configs[3]'s
+// 5.9k-node BVH the fetch overhead outweighs the gain: +0.035 ms)
+extern int g_mesh_persistent;
+constexpr int kPersistentIsectNodes = 32768;
 // mg_set_option("bvh_leaf_size", k): maximum triangles per BVH leaf (1..7),
 // applied to scenes created afterwards
 extern int g_bvh_leaf;
@@ -433,6 +440,173 @@ __device__ __forceinline__ int trace32_impl(const MeshDev& m, const float4* sn, 
   u_out = double(bu);
   v_out = double(bv);
   return bslot;
+}
+
+// fp32 traversal as a persistent warp loop (Aila & Laine, "Understanding
+// the efficiency of ray traversal on GPUs", HPG 2009: while-while with
+// speculative traversal and replacement of terminated rays).  Each lane
+// runs rays fetched from a queue counter in warp-aggregated batches; a lane
+// whose ray terminates takes a new one at the top of the loop, so lanes of
+// a warp do not idle until the warp's slowest ray is done.  Within a ray,
+// inner nodes are traversed until every active lane holds a leaf (a lane
+// that meets a leaf postpones it and keeps descending), then leaves are
+// intersected together — fewer divergent inner/leaf iterations.  Same
+// node / triangle tests and the same closest-hit rule (t, then the lower
+// original index: independent of the visiting order) as trace32_impl, so
+// the hits are identical.
+//   fetch(i, o, d, tmax) -> id: loads queue entry i, returns the ray's id
+//   finish(id, slot, t, u, v): writes the result (slot -1: no hit)
+constexpr int kDone = INT_MAX;
+
+template <bool ANY, class Fetch, class Finish>
+__device__ __forceinline__ void trace32_persistent(const MeshDev& m, const float4* sn, int n,
+                                                   unsigned int* counter, Fetch fetch,
+                                                   Finish finish) {
+  const int lane = int(threadIdx.x & 31);
+  int rid = -1;
+  bool done = false;
+  float of[3], df[3], inv[3], ooi[3];
+  float tmaxf = 0.0f, best = 0.0f, bu = 0.0f, bv = 0.0f;
+  int bslot = -1, bid = INT_MAX, node = kDone, leaf = 0, sp = 0;
+  int stack[kStackDepth];
+  for (;;) {
+    const bool need = rid < 0 && !done;
+    const unsigned needm = __ballot_sync(0xffffffffu, need);
+    if (needm) {
+      const int leader = __ffs(needm) - 1;
+      unsigned base = 0;
+      if (lane == leader) base = atomicAdd(counter, unsigned(__popc(needm)));
+      base = __shfl_sync(0xffffffffu, base, leader);
+      if (need) {
+        const int idx = int(base + unsigned(__popc(needm & ((1u << lane) - 1u))));
+        if (idx < n) {
+          double o[3], d[3], tm;
+          rid = fetch(idx, o, d, tm);
+#pragma unroll
+          for (int k = 0; k < 3; ++k) {
+            of[k] = float(o[k]);
+            df[k] = float(d[k]);
+            inv[k] = 1.0f / (fabsf(df[k]) > 1e-20f ? df[k] : copysignf(1e-20f, df[k]));
+            ooi[k] = of[k] * inv[k];
+          }
+          tmaxf = float(tm);
+          best = tmaxf;
+          bu = bv = 0.0f;
+          bslot = -1;
+          bid = INT_MAX;
+          node = 0;
+          leaf = 0;
+          sp = 0;
+        } else {
+          done = true;
+        }
+      }
+    }
+    if (__all_sync(0xffffffffu, done)) break;
+    if (rid < 0) continue;
+    // inner nodes until every active lane has a leaf waiting
+    while (node >= 0 && node != kDone) {
+      const NodeW nd = load_node(m, sn, node);
+      float tk[4];
+      int ck[4];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        float tc;
+        const bool h = slab6(f4c(nd.lx, c), f4c(nd.ly, c), f4c(nd.lz, c), f4c(nd.hx, c),
+                             f4c(nd.hy, c), f4c(nd.hz, c), ooi, inv, best, tc);
+        tk[c] = h ? tc : INFINITY;
+        ck[c] = __float_as_int(f4c(nd.ref, c));
+      }
+      auto cx = [&](int a, int b) {
+        if (tk[b] < tk[a]) {
+          const float tt = tk[a];
+          tk[a] = tk[b];
+          tk[b] = tt;
+          const int cc = ck[a];
+          ck[a] = ck[b];
+          ck[b] = cc;
+        }
+      };
+      if (!ANY) {
+        cx(0, 1);
+        cx(2, 3);
+        cx(0, 2);
+        cx(1, 3);
+        cx(1, 2);
+        if (tk[0] != INFINITY) {
+          if (tk[3] != INFINITY) stack[sp++] = ck[3];
+          if (tk[2] != INFINITY) stack[sp++] = ck[2];
+          if (tk[1] != INFINITY) stack[sp++] = ck[1];
+          node = ck[0];
+        } else {
+          node = sp ? stack[--sp] : kDone;
+        }
+      } else {
+        int nx = 0;
+        bool have = false;
+#pragma unroll
+        for (int c = 3; c >= 0; --c) {
+          if (tk[c] == INFINITY) continue;
+          if (have) stack[sp++] = nx;
+          nx = ck[c];
+          have = true;
+        }
+        node = have ? nx : (sp ? stack[--sp] : kDone);
+      }
+      if (node < 0 && leaf == 0) {  // postpone the leaf, keep descending
+        leaf = node;
+        node = sp ? stack[--sp] : kDone;
+      }
+      if (!__any_sync(__activemask(), leaf == 0)) break;
+    }
+    // the waiting leaves (and any leaf met next) of this lane
+    bool hit_any = false;
+    while (leaf < 0) {
+      const int first = (~leaf) >> 3, end = first + ((~leaf) & 7);
+      for (int s0 = first; s0 < end && !hit_any; s0 += 2) {
+        Tri32 tr[2];
+        tr[0] = load_tri32(m.tri32 + 3 * size_t(s0));
+        if (s0 + 1 < end) tr[1] = load_tri32(m.tri32 + 3 * size_t(s0 + 1));
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int sidx = s0 + e;
+          if (sidx >= end) break;
+          float t, u, v;
+          if (!tri_test32(tr[e], of, df, t, u, v) || !(t <= best)) continue;
+          if (ANY) {
+            if (t < tmaxf) {
+              bslot = sidx;
+              hit_any = true;
+              break;
+            }
+            continue;
+          }
+          const int id = __ldg(&m.orig[sidx]);
+          if (t < best || id < bid) {
+            best = t;
+            bu = u;
+            bv = v;
+            bslot = sidx;
+            bid = id;
+          }
+        }
+      }
+      if (hit_any) {
+        leaf = 0;
+        node = kDone;
+        break;
+      }
+      leaf = 0;
+      if (node < 0) {
+        leaf = node;
+        node = sp ? stack[--sp] : kDone;
+      }
+    }
+    if (node == kDone && leaf == 0) {
+      finish(rid, bslot, bslot < 0 ? double(INFINITY) : double(best), double(bu), double(bv));
+      rid = -1;
+    }
+  }
 }
 
 // traversal in the precision of the mode: fp64 (parity) or fp32 (fast)

@@ -12,6 +12,7 @@
 
 namespace mg {
 bool g_mesh_megakernel = false;
+int g_mesh_persistent = -1;
 int g_bvh_leaf = 2;
 namespace mesh {
 namespace {

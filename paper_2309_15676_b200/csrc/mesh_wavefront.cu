@@ -49,7 +49,9 @@ struct WF {
   // need not be written
   unsigned char *vnee, *vbnc;
   T* vdat;                                    // [kMaxV][nvf][PS]
-  unsigned int* cnt;                          // [2][kMaxV + 1]: queue / shadow counts
+  // [4][kMaxV + 1]: queue counts, shadow-queue counts, and the fetch
+  // counters of the persistent isect / shadow traversals
+  unsigned int* cnt;
   int P, PS, npix, pix0, nprop, nvf;
 };
 
@@ -59,7 +61,7 @@ size_t wf_bytes(int npix, int nprop, int nvf) {
   const size_t P = size_t(npix) * (nprop + 1), PS = size_t(npix) * nprop;
   return sizeof(double) * 16 * P + sizeof(T) * 24 * P + sizeof(int) * 5 * P +
          sizeof(int) * kMaxV * PS + sizeof(T) * kMaxV * nvf * PS + 2 * kMaxV * PS +
-         sizeof(unsigned int) * 2 * (kMaxV + 1) + 256 * 40;
+         sizeof(unsigned int) * 4 * (kMaxV + 1) + 256 * 40;
 }
 
 // Texel-major copies of the two parameter sets for the shade stage: texel
@@ -127,7 +129,7 @@ WF<T> wf_carve(void* mem, int npix, int nprop, int nvf) {
   w.vnee = (unsigned char*)take(kMaxV * size_t(w.PS));
   w.vbnc = (unsigned char*)take(kMaxV * size_t(w.PS));
   w.vdat = (T*)take(sizeof(T) * kMaxV * size_t(nvf) * size_t(w.PS));
-  w.cnt = (unsigned int*)take(sizeof(unsigned int) * 2 * (kMaxV + 1));
+  w.cnt = (unsigned int*)take(sizeof(unsigned int) * 4 * (kMaxV + 1));
   return w;
 }
 
@@ -196,6 +198,32 @@ __global__ void __launch_bounds__(kMThreads, 8) wf_isect_kernel(MeshDev m, WF<T>
     w.hu[p] = bu;
     w.hv[p] = bv;
   }
+}
+
+// fp32 mode: persistent closest-hit traversal (trace32_persistent)
+__global__ void __launch_bounds__(kMThreads, 8) wf_isect_p_kernel(MeshDev m, WF<float> w, int v) {
+  MESH_SMEM;
+  const int n = int(w.cnt[v]);
+  const int* qin = (v & 1) ? w.q1 : w.q0;
+  trace32_persistent<false>(
+      m, sn, n, &w.cnt[2 * (kMaxV + 1) + v],
+      [&](int i, double o[3], double d[3], double& tm) {
+        const int p = qin[i];
+        o[0] = w.ox[p];
+        o[1] = w.oy[p];
+        o[2] = w.oz[p];
+        d[0] = w.dx[p];
+        d[1] = w.dy[p];
+        d[2] = w.dz[p];
+        tm = INFINITY;
+        return p;
+      },
+      [&](int p, int slot, double t, double u, double vv) {
+        w.hslot[p] = slot;
+        w.ht[p] = t;
+        w.hu[p] = u;
+        w.hv[p] = vv;
+      });
 }
 
 template <class T, int NCH>
@@ -450,6 +478,35 @@ __global__ void __launch_bounds__(kMThreads, 8) wf_shadow_kernel(MeshDev m, WF<T
       w.vnee[size_t(v) * w.PS + p] = 0;
     }
   }
+}
+
+// fp32 mode: persistent any-hit traversal of the NEE rays
+template <int NCH>
+__global__ void __launch_bounds__(kMThreads, 8) wf_shadow_p_kernel(MeshDev m, WF<float> w, int v) {
+  MESH_SMEM;
+  const int n = int(w.cnt[kMaxV + 1 + v]);
+  trace32_persistent<true>(
+      m, sn, n, &w.cnt[3 * (kMaxV + 1) + v],
+      [&](int i, double o[3], double d[3], double& tm) {
+        const int p = w.sq[i];
+        o[0] = w.sox[p];
+        o[1] = w.soy[p];
+        o[2] = w.soz[p];
+        d[0] = w.sdx[p];
+        d[1] = w.sdy[p];
+        d[2] = w.sdz[p];
+        tm = w.stm[p];
+        return p;
+      },
+      [&](int p, int slot, double, double, double) {
+        if (slot < 0) {
+          const int k = p / w.npix;
+          const int nj = (k == 0 || k == w.nprop) ? 6 : 3;
+          for (int j = 0; j < nj; ++j) w.L[size_t(j) * w.P + p] += w.pendC[size_t(j) * w.P + p];
+        } else if (p < w.PS) {  // occluded: no NEE data at this vertex
+          w.vnee[size_t(v) * w.PS + p] = 0;
+        }
+      });
 }
 
 // Where the fixed-point adjoints go.
@@ -788,17 +845,35 @@ int wavefront_pair(mg_ctx* ctx, mg_mesh_scene* s, const MeshK& q, int nprop, con
     s->last_dtype = dt;
   }
   const MeshDev m = dev_of(s);
-  MG_CUDA_TRY(cudaMemsetAsync(w.cnt, 0, sizeof(unsigned int) * 2 * (kMaxV + 1), ctx->stream));
+  MG_CUDA_TRY(cudaMemsetAsync(w.cnt, 0, sizeof(unsigned int) * 4 * (kMaxV + 1), ctx->stream));
   const int grid = grid_for(ctx, w.P, kMThreads, 8);
+  // persistent traversals: one resident wave (8 CTAs of 128 per SM)
+  const int pgrid = grid;
+  const int pmode = g_mesh_persistent >= 0 ? g_mesh_persistent
+                                            : (s->nnodes >= kPersistentIsectNodes ? 3 : 2);
   wf_gen_kernel<T><<<grid, kMThreads, 0, ctx->stream>>>(q, w);
   MG_LAUNCH_CHECK(ctx);
   const int maxv = int(q.view[24]);
   for (int v = 0; v < maxv; ++v) {
-    wf_isect_kernel<T><<<grid, kMThreads, 0, ctx->stream>>>(m, w, v);
+    if constexpr (sizeof(T) == 4) {
+      if (pmode & 1)
+        wf_isect_p_kernel<<<pgrid, kMThreads, 0, ctx->stream>>>(m, w, v);
+      else
+        wf_isect_kernel<T><<<grid, kMThreads, 0, ctx->stream>>>(m, w, v);
+    } else {
+      wf_isect_kernel<T><<<grid, kMThreads, 0, ctx->stream>>>(m, w, v);
+    }
     MG_LAUNCH_CHECK(ctx);
     wf_shade_kernel<T, NCH><<<grid, kMThreads, 0, ctx->stream>>>(q, m, w, v, thI[0], thI[1]);
     MG_LAUNCH_CHECK(ctx);
-    wf_shadow_kernel<T, NCH><<<grid, kMThreads, 0, ctx->stream>>>(m, w, v);
+    if constexpr (sizeof(T) == 4) {
+      if (pmode & 2)
+        wf_shadow_p_kernel<NCH><<<pgrid, kMThreads, 0, ctx->stream>>>(m, w, v);
+      else
+        wf_shadow_kernel<T, NCH><<<grid, kMThreads, 0, ctx->stream>>>(m, w, v);
+    } else {
+      wf_shadow_kernel<T, NCH><<<grid, kMThreads, 0, ctx->stream>>>(m, w, v);
+    }
     MG_LAUNCH_CHECK(ctx);
   }
   const int sgrid = grid_for(ctx, npix, kMThreads, 8);

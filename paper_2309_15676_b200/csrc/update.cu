@@ -32,6 +32,7 @@ extern bool g_cluster_runner;
 extern int g_render_fast_variant;
 int render_fast_variants();
 extern bool g_mesh_megakernel;
+extern int g_mesh_persistent;
 extern int g_bvh_leaf;
 // -1: per-dtype default measured on B200 (tools/sweep_update_variants.py,
 // profiles/r01_sweep_update_variants_*): fp32 -> variant 6 (2 CTAs/SM x 192
@@ -735,6 +736,11 @@ int mg_set_option(const char* name, int64_t value) {
   if (std::string(name) == "bvh_leaf_size") {
     if (value < 1 || value > 7) return fail(MG_EINVAL, "bvh_leaf_size must lie in [1, 7]");
     g_bvh_leaf = int(value);
+    return MG_OK;
+  }
+  if (std::string(name) == "mesh_persistent") {
+    if (value < -1 || value > 3) return fail(MG_EINVAL, "mesh_persistent must lie in [-1, 3]");
+    g_mesh_persistent = int(value);
     return MG_OK;
   }
   if (std::string(name) == "mesh_megakernel") {
