@@ -98,15 +98,21 @@ int mg_config_validate(const mg_experiment_config* cfg);
 
 const char* mg_last_error(void);
 int mg_abi_version(void);
-/* Process-wide tuning switches (tests/benchmarks): "disable_tma" = 1 forces
- * the register-streaming variant of mg_meta_update instead of the TMA
- * bulk-copy pipeline; "tma_variant" (-1 = default, 0..9) picks its schedule;
- * "render_fast" = 0 runs the IEEE fp32 mini-render kernel instead of the
- * TMA-fed fast one; "render_fast_variant" (-1, 0..10) picks the latter's
- * schedule; "cluster_runner" = 0 keeps few-replicate mini-render runs on the
- * one-CTA-per-replicate runner; "mesh_persistent" (-1 auto, bit 0 isect, bit 1 shadow; 0 runs the fp32 mesh
- * isect / shadow stages one ray per thread); "render_vec", "bvh_leaf_size", "mesh_megakernel" as documented
- * in DESIGN.md.  Unknown names -> MG_EINVAL. */
+/* Process-wide tuning switches (tests/benchmarks; unknown names -> MG_EINVAL):
+ *   "disable_tma" = 1          mg_meta_update / mg_adam_update on the
+ *                              register-streaming kernels instead of the TMA
+ *                              bulk-copy pipelines
+ *   "tma_variant"  -1 | 0..9   schedule of the TMA meta update (-1 default)
+ *   "render_fast" = 0          fp32 mini-render on the IEEE kernel instead of
+ *                              the TMA-fed fast one (render_fast.cu)
+ *   "render_fast_variant"      -1 | 0..10: the fast kernel's schedule
+ *   "cluster_runner" = 0       few-replicate mini-render runs on the
+ *                              one-CTA-per-replicate runner
+ *   "mesh_persistent"          -1 (auto) | 0..3: bit 0 persistent fp32 isect,
+ *                              bit 1 persistent fp32 shadow traversal
+ *   "mesh_scatter_aggregate"=1 warp-aggregated mesh adjoint scatter (measured
+ *                              slower at configs[3]/[4]; off by default)
+ *   "render_vec", "bvh_leaf_size", "mesh_megakernel": see DESIGN.md */
 int mg_set_option(const char* name, int64_t value);
 
 /* ---------------------------------------------------------------- context */

@@ -47,6 +47,12 @@ extern bool g_mesh_megakernel;
 // 5.9k-node BVH the fetch overhead outweighs the gain: +0.035 ms)
 extern int g_mesh_persistent;
 constexpr int kPersistentIsectNodes = 32768;
+// mg_set_option("mesh_scatter_aggregate", 1): warp-aggregated adjoint
+// scatter (__match_any_sync per texel cell).  Off by default: the paths of
+// one warp almost never share a texel at configs[3]/[4] texture densities,
+// so the match costs more than it saves (configs[4] 9.05 -> 9.14 ms,
+// configs[3] unchanged; tools/mesh_ab_options.py, bit-identical)
+extern bool g_mesh_scatter_agg;
 // mg_set_option("bvh_leaf_size", k): maximum triangles per BVH leaf (1..7),
 // applied to scenes created afterwards
 extern int g_bvh_leaf;

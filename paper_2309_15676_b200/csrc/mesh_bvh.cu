@@ -13,6 +13,7 @@
 namespace mg {
 bool g_mesh_megakernel = false;
 int g_mesh_persistent = -1;
+bool g_mesh_scatter_agg = false;
 int g_bvh_leaf = 2;
 namespace mesh {
 namespace {

@@ -549,6 +549,41 @@ struct AccCell {
   }
 };
 
+// Adds val[k] (fixed point) to the NCH accumulator words of `cell`, set
+// `which`.  agg: warp-aggregated — the converged lanes adding to the same
+// cell (__match_any_sync on the parameter base) are summed first and one
+// lane per cell issues the NCH atomics (integer sums: the same result in any
+// order, so bit-identical to one atomic per lane).
+template <int NCH, bool ILV>
+__device__ __forceinline__ void cell_add(bool agg, const AccTable& acc,
+                                         const AccCell<NCH, ILV>& cell, int which,
+                                         const unsigned long long (&val)[NCH]) {
+  if (!agg) {
+#pragma unroll
+    for (int k = 0; k < NCH; ++k) atomicAdd(cell.at(acc, which, k), val[k]);
+    return;
+  }
+  const unsigned act = __activemask();
+  const unsigned peers = __match_any_sync(act, cell.base);
+  const int lane = int(threadIdx.x & 31), leader = __ffs(peers) - 1;
+  unsigned rem = lane == leader ? (peers & ~(1u << lane)) : 0u;
+  unsigned long long sum[NCH];
+#pragma unroll
+  for (int k = 0; k < NCH; ++k) sum[k] = val[k];
+  while (__any_sync(act, rem != 0u)) {
+    const int src = rem ? __ffs(rem) - 1 : lane;
+#pragma unroll
+    for (int k = 0; k < NCH; ++k) {
+      const unsigned long long y = __shfl_sync(act, val[k], src);
+      if (rem) sum[k] += y;
+    }
+    rem &= rem - 1u;
+  }
+  if (lane == leader)
+#pragma unroll
+    for (int k = 0; k < NCH; ++k) atomicAdd(cell.at(acc, which, k), sum[k]);
+}
+
 // Per-vertex adjoint terms of stored path p, parameter set s (megakernel
 // `scatter` / oracle ms_scatter), before the channel weights: X[c][0] for
 // base colour c, X[c][1] roughness, X[c][2] metalness (NCH 5); Q is the
@@ -598,7 +633,7 @@ __device__ __forceinline__ void combine(const T X[3][NCH - 2], const T wt[3], T 
 // adjoint of stored proportional path p (set 0) into the prop accumulator
 template <class T, int NCH, bool ILV>
 __device__ __noinline__ void wf_scatter(const WF<T>& w, int p, const T wt[3], int R2,
-                                        const AccTable& acc) {
+                                        const AccTable& acc, bool agg) {
   using F = VF<NCH>;
   T Q[3];
 #pragma unroll
@@ -609,8 +644,10 @@ __device__ __noinline__ void wf_scatter(const WF<T>& w, int p, const T wt[3], in
     T X[3][NCH - 2], g[NCH];
     vertex_terms<T, NCH>(w, v, p, 0, Q, ne, bn, X);
     combine<T, NCH>(X, wt, g);
+    unsigned long long d[NCH];
 #pragma unroll
-    for (int k = 0; k < NCH; ++k) atomicAdd(cell.at(acc, 0, k), fixq(double(g[k])));
+    for (int k = 0; k < NCH; ++k) d[k] = fixq(double(g[k]));
+    cell_add<NCH, ILV>(agg, acc, cell, 0, d);
 #pragma unroll
     for (int c = 0; c < 3; ++c) Q[c] = Q[c] + (ne ? vf(w, v, F::C + c, p) : T(0));
   }
@@ -622,7 +659,8 @@ __device__ __noinline__ void wf_scatter(const WF<T>& w, int p, const T wt[3], in
 // the atomic — the same fixed-point sum as two separate atomics, bit for bit.
 template <class T, int NCH, bool ILV>
 __device__ __noinline__ void wf_scatter_a(const WF<T>& w, int p, const T wt[3], const T wC0[3],
-                                          const T wC1[3], int R2, const AccTable& acc) {
+                                          const T wC1[3], int R2, const AccTable& acc,
+                                          bool agg) {
   using F = VF<NCH>;
   T Q0[3], Q1[3];
 #pragma unroll
@@ -638,14 +676,16 @@ __device__ __noinline__ void wf_scatter_a(const WF<T>& w, int p, const T wt[3], 
     vertex_terms<T, NCH>(w, v, p, 0, Q0, ne, bn, X);
     combine<T, NCH>(X, wt, g);
 #pragma unroll
-    for (int k = 0; k < NCH; ++k) atomicAdd(cell.at(acc, 0, k), fixq(double(g[k])));
+    for (int k = 0; k < NCH; ++k) d[k] = fixq(double(g[k]));
+    cell_add<NCH, ILV>(agg, acc, cell, 0, d);
     combine<T, NCH>(X, wC0, g);
 #pragma unroll
     for (int k = 0; k < NCH; ++k) d[k] = fixq(double(g[k]));
     vertex_terms<T, NCH>(w, v, p, 1, Q1, ne, bn, X);
     combine<T, NCH>(X, wC1, g);
 #pragma unroll
-    for (int k = 0; k < NCH; ++k) atomicAdd(cell.at(acc, 1, k), d[k] + fixq(double(g[k])));
+    for (int k = 0; k < NCH; ++k) d[k] = d[k] + fixq(double(g[k]));
+    cell_add<NCH, ILV>(agg, acc, cell, 1, d);
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
       Q0[c] = Q0[c] + (ne ? vf(w, v, F::C + c, p) : T(0));
@@ -661,7 +701,8 @@ constexpr int kMaxProp = 8;
 template <class T, int NCH, bool ILV>
 __global__ void __launch_bounds__(kMThreads, 4)
     wf_scatter_kernel(MeshK q, WF<T> w, const T* __restrict__ target_img, AccTable acc,
-                      ReducePartials* partials, unsigned int* counter, double* loss_out) {
+                      ReducePartials* partials, unsigned int* counter, double* loss_out,
+                      bool agg) {
   const int npix_img = q.W * q.H;
   const int R2 = q.R * q.R;
   const int n = w.nprop;
@@ -700,9 +741,9 @@ __global__ void __launch_bounds__(kMThreads, 4)
         wt[c] = a * scale;
       }
       if (j == 0)
-        wf_scatter_a<T, NCH, ILV>(w, i, wt, wC0, wC1, R2, acc);
+        wf_scatter_a<T, NCH, ILV>(w, i, wt, wC0, wC1, R2, acc, agg);
       else
-        wf_scatter<T, NCH, ILV>(w, j * w.npix + i, wt, R2, acc);
+        wf_scatter<T, NCH, ILV>(w, j * w.npix + i, wt, R2, acc, agg);
     }
   }
   Acc a;
@@ -879,10 +920,10 @@ int wavefront_pair(mg_ctx* ctx, mg_mesh_scene* s, const MeshK& q, int nprop, con
   const int sgrid = grid_for(ctx, npix, kMThreads, 8);
   if (acc.ilv)
     wf_scatter_kernel<T, NCH, true><<<sgrid, kMThreads, 0, ctx->stream>>>(
-        q, w, target_img, acc, ctx->partials, ctx->counter, loss_out);
+        q, w, target_img, acc, ctx->partials, ctx->counter, loss_out, g_mesh_scatter_agg);
   else
     wf_scatter_kernel<T, NCH, false><<<sgrid, kMThreads, 0, ctx->stream>>>(
-        q, w, target_img, acc, ctx->partials, ctx->counter, loss_out);
+        q, w, target_img, acc, ctx->partials, ctx->counter, loss_out, g_mesh_scatter_agg);
   MG_LAUNCH_CHECK(ctx);
   return MG_OK;
 }
