@@ -482,8 +482,40 @@ HelixK make_helix(int W, int H, int nsph, const double* Le, const double* env, c
 }
 
 }  // namespace
+
+// The fp32 launches live in helix_f32.cu: this file compiled again with
+// --fmad=true (FMA contraction is allowed in the tolerance-judged fp32
+// mode; configs[2] iteration 0.245 -> 0.227 ms), while the fp64 parity
+// kernels here keep --fmad=false.
+// (the kernel parameter block is passed as void*: HelixK lives in each
+// translation unit's anonymous namespace, identical in both)
+void helix_render_f32(mg_ctx* ctx, int grid, const void* qp, int spp, const double* spheres,
+                      const float* theta, float* img)
+#ifdef MG_HELIX_F32_TU
+{
+  const HelixK& q = *static_cast<const HelixK*>(qp);
+  helix_render_kernel<float><<<grid, kHThreads, 0, ctx->stream>>>(q, spp, spheres, theta, img);
+}
+#else
+    ;
+#endif
+void helix_pair_f32(mg_ctx* ctx, int grid, const void* qp, const double* spheres,
+                    const float* now, const float* prev, const float* target_img,
+                    unsigned long long* accum, double* loss_out, float* prop, float* diff)
+#ifdef MG_HELIX_F32_TU
+{
+  const HelixK& q = *static_cast<const HelixK*>(qp);
+  helix_pair_kernel<float><<<grid, kHThreads, 0, ctx->stream>>>(
+      q, spheres, now, prev, target_img, accum, ctx->partials, ctx->counter, loss_out);
+  helix_finalize_kernel<float><<<1, 32, 0, ctx->stream>>>(accum, prop, diff);
+}
+#else
+    ;
+#endif
+
 }  // namespace mg
 
+#ifndef MG_HELIX_F32_TU
 using namespace mg;
 
 extern "C" {
@@ -502,8 +534,7 @@ int mg_helix_render(mg_ctx* ctx, int32_t dtype, int32_t W, int32_t H, int32_t ns
     helix_render_kernel<double><<<grid, kHThreads, 0, ctx->stream>>>(
         q, spp, spheres, (const double*)theta, (double*)img);
   else if (dtype == MG_F32)
-    helix_render_kernel<float><<<grid, kHThreads, 0, ctx->stream>>>(
-        q, spp, spheres, (const float*)theta, (float*)img);
+    helix_render_f32(ctx, grid, &q, spp, spheres, (const float*)theta, (float*)img);
   else
     return fail(MG_EINVAL, "mg_helix_render: unknown dtype");
   MG_LAUNCH_CHECK(ctx);
@@ -534,12 +565,9 @@ int mg_helix_sample_pair(mg_ctx* ctx, int32_t dtype, int32_t W, int32_t H, int32
     helix_finalize_kernel<double><<<1, 32, 0, ctx->stream>>>((unsigned long long*)accum,
                                                              (double*)prop, (double*)diff);
   } else if (dtype == MG_F32) {
-    helix_pair_kernel<float><<<grid, kHThreads, 0, ctx->stream>>>(
-        q, spheres, (const float*)now, (const float*)prev, (const float*)target_img,
-        (unsigned long long*)accum, ctx->partials,
-        ctx->counter, loss_out);
-    helix_finalize_kernel<float><<<1, 32, 0, ctx->stream>>>((unsigned long long*)accum,
-                                                            (float*)prop, (float*)diff);
+    helix_pair_f32(ctx, grid, &q, spheres, (const float*)now, (const float*)prev,
+                   (const float*)target_img, (unsigned long long*)accum, loss_out, (float*)prop,
+                   (float*)diff);
   } else {
     return fail(MG_EINVAL, "mg_helix_sample_pair: unknown dtype");
   }
@@ -549,3 +577,4 @@ int mg_helix_sample_pair(mg_ctx* ctx, int32_t dtype, int32_t W, int32_t H, int32
 }
 
 }  // extern "C"
+#endif  // MG_HELIX_F32_TU
