@@ -895,7 +895,12 @@ int wavefront_pair(mg_ctx* ctx, mg_mesh_scene* s, const MeshK& q, int nprop, con
   wf_gen_kernel<T><<<grid, kMThreads, 0, ctx->stream>>>(q, w);
   MG_LAUNCH_CHECK(ctx);
   const int maxv = int(q.view[24]);
+  static const char* kDepthName[kMaxV] = {"wavefront depth 0", "wavefront depth 1",
+                                          "wavefront depth 2", "wavefront depth 3",
+                                          "wavefront depth 4", "wavefront depth 5",
+                                          "wavefront depth 6", "wavefront depth 7"};
   for (int v = 0; v < maxv; ++v) {
+    MG_NVTX(kDepthName[v]);
     if constexpr (sizeof(T) == 4) {
       if (pmode & 1)
         wf_isect_p_kernel<<<pgrid, kMThreads, 0, ctx->stream>>>(m, w, v);
@@ -917,6 +922,7 @@ int wavefront_pair(mg_ctx* ctx, mg_mesh_scene* s, const MeshK& q, int nprop, con
     }
     MG_LAUNCH_CHECK(ctx);
   }
+  MG_NVTX("wavefront scatter");
   const int sgrid = grid_for(ctx, npix, kMThreads, 8);
   if (acc.ilv)
     wf_scatter_kernel<T, NCH, true><<<sgrid, kMThreads, 0, ctx->stream>>>(
@@ -959,6 +965,7 @@ int mg_meshscene_sample_pair(mg_ctx* ctx, mg_mesh_scene* s, int32_t dtype, int32
                              const void* now, const void* prev, uint64_t key, uint32_t iteration,
                              int32_t row0, int32_t row1, int32_t prop_paths, void* accum,
                              void* prop, void* diff, double* loss_out) {
+  MG_NVTX("mg_meshscene_sample_pair");
   if (!ctx || !s || !target_img || !now || !prev || !accum || !prop || !diff || !loss_out)
     return fail(MG_EINVAL, "mg_meshscene_sample_pair: null argument");
   if (prop_paths < 2 || prop_paths > kMaxProp)

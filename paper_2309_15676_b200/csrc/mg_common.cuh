@@ -6,6 +6,8 @@
 
 #include <string>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "mgcuda.h"
 
 #if defined(__CUDA_ARCH__) && (__CUDA_ARCH__ < 1000)
@@ -31,6 +33,19 @@ int cuda_fail(cudaError_t e, const char* what);
     cudaError_t mg_e_ = cudaGetLastError();                \
     if (mg_e_ != cudaSuccess) return ::mg::cuda_fail(mg_e_, "kernel launch"); \
   } while (0)
+
+// NVTX range over a host entry point / pipeline stage (header-only NVTX3: a
+// no-op unless a profiler injects itself; ncu --nvtx --nvtx-include can
+// filter kernels by these names)
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
+#define MG_NVTX_CAT2(a, b) a##b
+#define MG_NVTX_CAT(a, b) MG_NVTX_CAT2(a, b)
+#define MG_NVTX(name) ::mg::NvtxRange MG_NVTX_CAT(mg_nvtx_, __LINE__)(name)
 
 // across-replicate aggregation (aggregate.cu); runs[r * runs_stride] are the
 // replicates' iterations_run

@@ -215,6 +215,7 @@ extern "C" int mg_minirender_meta_iteration(mg_ctx* ctx, int32_t dtype, int64_t 
                                             void* m2_prop, void* m2_diff, void* mean, void* var,
                                             void* alpha_prev, mg_update_scalars* scalars,
                                             void* prop_out, void* diff_out) {
+  MG_NVTX("mg_minirender_meta_iteration");
   if (!ctx || !a || !scalars) return fail(MG_EINVAL, "mg_minirender_meta_iteration: null argument");
   if (P < 1) return fail(MG_EINVAL, "mini-render: pixel_count must be >= 1");
   if (a->spp < 2) return fail(MG_EINVAL, "mini-render: spp must be at least 2");

@@ -907,6 +907,7 @@ template <class T>
 int run_replicates(mg_ctx* ctx, const mg_experiment_config* cfg, int rep_begin, int R,
                    mg_run_record* records, const mg_run_series* series, double* final_params,
                    double* stats = nullptr, int32_t* active = nullptr, double* full = nullptr) {
+  MG_NVTX("run_replicates");
   const int d = problem_dim(cfg);
   const int iters = cfg->iterations;
   std::vector<double> truth(d, 0.0), init(d, 0.0);

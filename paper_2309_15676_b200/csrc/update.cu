@@ -782,6 +782,7 @@ int mg_meta_update(mg_ctx* ctx, int32_t dtype, int64_t n, const mg_meta_update_a
                    const void* prop, const void* diff, void* m2_prop, void* m2_diff, void* mean,
                    void* var, void* alpha_prev, const void* params_in, void* params_out,
                    mg_update_scalars* scalars, const mg_meta_extras* x) {
+  MG_NVTX("mg_meta_update");
   if (!ctx || !a || !scalars) return fail(MG_EINVAL, "mg_meta_update: null argument");
   if (n < 0) return fail(MG_EINVAL, "mg_meta_update: negative dimension");
   if (n == 0) return MG_OK;
@@ -864,6 +865,7 @@ int mg_shared_meta_update(mg_ctx* ctx, int32_t dtype, int64_t shard_n, int64_t s
 int mg_adam_update(mg_ctx* ctx, int32_t dtype, int64_t n, mg_adam_scalars* s, int32_t project,
                    double proj_lo, const void* grad, void* m, void* v, const void* params_in,
                    void* params_out, const void* target, mg_update_scalars* scalars) {
+  MG_NVTX("mg_adam_update");
   if (!ctx || !s || !scalars) return fail(MG_EINVAL, "mg_adam_update: null argument");
   if (n < 0) return fail(MG_EINVAL, "mg_adam_update: negative dimension");
   if (n == 0) return MG_OK;
