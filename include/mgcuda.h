@@ -110,6 +110,10 @@ int mg_abi_version(void);
  *                              one-CTA-per-replicate runner
  *   "mesh_persistent"          -1 (auto) | 0..3: bit 0 persistent fp32 isect,
  *                              bit 1 persistent fp32 shadow traversal
+ *   "mesh_bvh8" = 1            the persistent traversals walk an eight-wide
+ *                              BVH (measured slower; off by default)
+ *   "mesh_smem_stack"          1 (default): persistent BVH4 traversal stack in
+ *                              shared memory; 0: local memory + top nodes staged
  *   "mesh_scatter_aggregate"=1 warp-aggregated mesh adjoint scatter (measured
  *                              slower at configs[3]/[4]; off by default)
  *   "render_vec", "bvh_leaf_size", "mesh_megakernel": see DESIGN.md */

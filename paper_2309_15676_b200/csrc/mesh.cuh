@@ -25,7 +25,9 @@ struct mg_mesh_scene {
   float4* tri32 = nullptr; // [T][3] fp32 v0 e1 e2 (fp32-mode traversal), BVH order
   int* orig = nullptr;     // [T] original triangle index
   int* obj = nullptr;      // [T] object id (BVH order)
-  float4* nodes = nullptr; // [2 * nnodes]: (lo.xyz, a) (hi.xyz, b)
+  float4* nodes = nullptr; // [kNodeF4 * nnodes]: BVH4 (see NodeW)
+  float4* nodes8 = nullptr; // [kNode8F4 * nnodes8]: BVH8 of the fp32 persistent traversal
+  int nnodes8 = 0, depth8 = 0;
   unsigned int* work = nullptr;  // pixel work counter of the pair kernel
   void* wf = nullptr;            // wavefront path state (grow-only)
   size_t wf_cap = 0;
@@ -47,6 +49,13 @@ extern bool g_mesh_megakernel;
 // 5.9k-node BVH the fetch overhead outweighs the gain: +0.035 ms)
 extern int g_mesh_persistent;
 constexpr int kPersistentIsectNodes = 32768;
+// mg_set_option("mesh_smem_stack", 1): the persistent BVH4 traversals keep
+// their stack in shared memory ([entry][thread], conflict-free) instead of
+// staging the top nodes there
+extern bool g_mesh_smem_stack;
+// mg_set_option("mesh_bvh8", 0): the persistent fp32 traversals walk the
+// BVH4 instead of the BVH8
+extern bool g_mesh_bvh8;
 // mg_set_option("mesh_scatter_aggregate", 1): warp-aggregated adjoint
 // scatter (__match_any_sync per texel cell).  Off by default: the paths of
 // one warp almost never share a texel at configs[3]/[4] texture densities,
@@ -76,6 +85,8 @@ struct MeshDev {
   const int* __restrict__ obj;
   const float4* __restrict__ nodes;
   int nnodes;
+  const float4* __restrict__ nodes8;
+  int nnodes8;
 };
 
 struct MeshK {
@@ -135,10 +146,12 @@ struct NodeW {
   float4 lx, ly, lz, hx, hy, hz, ref;
 };
 
+template <bool STAGED = true>
 __device__ __forceinline__ NodeW load_node(const MeshDev& m, const float4* sn, int i) {
-  const float4* src = i < kSmemNodes ? sn + kNodeF4 * i : m.nodes + size_t(kNodeF4) * i;
+  const bool shared = STAGED && i < kSmemNodes;
+  const float4* src = shared ? sn + kNodeF4 * i : m.nodes + size_t(kNodeF4) * i;
   NodeW n;
-  if (i < kSmemNodes) {
+  if (shared) {
     n.lx = src[0];
     n.ly = src[1];
     n.lz = src[2];
@@ -464,17 +477,42 @@ __device__ __forceinline__ int trace32_impl(const MeshDev& m, const float4* sn, 
 //   finish(id, slot, t, u, v): writes the result (slot -1: no hit)
 constexpr int kDone = INT_MAX;
 
-template <bool ANY, class Fetch, class Finish>
+// Traversal stack of the persistent loop.  Local memory interleaves a
+// thread's entries with its warp-mates' at the same index, so lanes at
+// different depths touch a different 128-byte row each (ncu: 1.8 of 32
+// bytes used per local sector).  SMEM_STACK keeps the stack in shared
+// memory laid out [entry][thread] instead: every lane hits its own bank at
+// any depth.  kSmemStack entries (24 KB per 128-thread CTA) hold any BVH4 of
+// depth <= kSmemStackMaxDepth (3 pushes per level); deeper scenes use the
+// local-memory form.
+constexpr int kSmemStack = 48;
+constexpr int kSmemStackMaxDepth = (kSmemStack - 1) / 3 - 1;
+
+template <bool ANY, bool SMEM_STACK = false, class Fetch, class Finish>
 __device__ __forceinline__ void trace32_persistent(const MeshDev& m, const float4* sn, int n,
                                                    unsigned int* counter, Fetch fetch,
-                                                   Finish finish) {
+                                                   Finish finish, int* smem_stack = nullptr) {
   const int lane = int(threadIdx.x & 31);
   int rid = -1;
   bool done = false;
   float of[3], df[3], inv[3], ooi[3];
   float tmaxf = 0.0f, best = 0.0f, bu = 0.0f, bv = 0.0f;
   int bslot = -1, bid = INT_MAX, node = kDone, leaf = 0, sp = 0;
-  int stack[kStackDepth];
+  int lstack[SMEM_STACK ? 1 : kStackDepth];
+  int* const sstack = SMEM_STACK ? smem_stack + threadIdx.x : nullptr;
+  auto push = [&](int v) {
+    if constexpr (SMEM_STACK)
+      sstack[(sp++) * kMThreads] = v;
+    else
+      lstack[sp++] = v;
+  };
+  auto pop = [&]() {
+    if (sp == 0) return kDone;
+    if constexpr (SMEM_STACK)
+      return sstack[(--sp) * kMThreads];
+    else
+      return lstack[--sp];
+  };
   for (;;) {
     const bool need = rid < 0 && !done;
     const unsigned needm = __ballot_sync(0xffffffffu, need);
@@ -512,7 +550,7 @@ __device__ __forceinline__ void trace32_persistent(const MeshDev& m, const float
     if (rid < 0) continue;
     // inner nodes until every active lane has a leaf waiting
     while (node >= 0 && node != kDone) {
-      const NodeW nd = load_node(m, sn, node);
+      const NodeW nd = load_node<!SMEM_STACK>(m, sn, node);
       float tk[4];
       int ck[4];
 #pragma unroll
@@ -540,12 +578,12 @@ __device__ __forceinline__ void trace32_persistent(const MeshDev& m, const float
         cx(1, 3);
         cx(1, 2);
         if (tk[0] != INFINITY) {
-          if (tk[3] != INFINITY) stack[sp++] = ck[3];
-          if (tk[2] != INFINITY) stack[sp++] = ck[2];
-          if (tk[1] != INFINITY) stack[sp++] = ck[1];
+          if (tk[3] != INFINITY) push(ck[3]);
+          if (tk[2] != INFINITY) push(ck[2]);
+          if (tk[1] != INFINITY) push(ck[1]);
           node = ck[0];
         } else {
-          node = sp ? stack[--sp] : kDone;
+          node = pop();
         }
       } else {
         int nx = 0;
@@ -553,15 +591,15 @@ __device__ __forceinline__ void trace32_persistent(const MeshDev& m, const float
 #pragma unroll
         for (int c = 3; c >= 0; --c) {
           if (tk[c] == INFINITY) continue;
-          if (have) stack[sp++] = nx;
+          if (have) push(nx);
           nx = ck[c];
           have = true;
         }
-        node = have ? nx : (sp ? stack[--sp] : kDone);
+        node = have ? nx : pop();
       }
       if (node < 0 && leaf == 0) {  // postpone the leaf, keep descending
         leaf = node;
-        node = sp ? stack[--sp] : kDone;
+        node = pop();
       }
       if (!__any_sync(__activemask(), leaf == 0)) break;
     }
@@ -605,7 +643,190 @@ __device__ __forceinline__ void trace32_persistent(const MeshDev& m, const float
       leaf = 0;
       if (node < 0) {
         leaf = node;
-        node = sp ? stack[--sp] : kDone;
+        node = pop();
+      }
+    }
+    if (node == kDone && leaf == 0) {
+      finish(rid, bslot, bslot < 0 ? double(INFINITY) : double(best), double(bu), double(bv));
+      rid = -1;
+    }
+  }
+}
+
+// ---------------------------------------------------------------- BVH8
+// Eight-child nodes (224 B, SoA: lo.x[8] lo.y[8] lo.z[8] hi.x[8] hi.y[8]
+// hi.z[8] ref[8]; fp32 boxes rounded outwards and padded exactly like the
+// BVH4 ones; empty slots: inverted box and ref ~0, an empty leaf) built from
+// the same binary tree by opening the largest child until eight.  Half the
+// levels of the BVH4: fewer dependent node fetches per ray, eight boxes
+// tested per fetch.  Used by the fp32 persistent traversal only.
+constexpr int kNode8F4 = 14;
+constexpr int kSmemNodes8 = 64;  // top BVH8 nodes staged in shared memory (14 KB)
+
+__device__ __forceinline__ void stage_nodes8(const MeshDev& m, float4* sn) {
+  const int n = kNode8F4 * (m.nnodes8 < kSmemNodes8 ? m.nnodes8 : kSmemNodes8);
+  for (int i = threadIdx.x; i < n; i += blockDim.x) sn[i] = m.nodes8[i];
+  __syncthreads();
+}
+
+// half h (children 4h..4h+3) of node i: lx ly lz hx hy hz ref as float4s
+struct Node8Half {
+  float4 lx, ly, lz, hx, hy, hz, ref;
+};
+__device__ __forceinline__ Node8Half load_node8_half(const MeshDev& m, const float4* sn, int i,
+                                                     int h) {
+  const bool shared = i < kSmemNodes8;
+  const float4* src = (shared ? sn : m.nodes8) + size_t(kNode8F4) * i + h;
+  Node8Half n;
+  if (shared) {
+    n.lx = src[0];
+    n.ly = src[2];
+    n.lz = src[4];
+    n.hx = src[6];
+    n.hy = src[8];
+    n.hz = src[10];
+    n.ref = src[12];
+  } else {
+    n.lx = __ldg(src);
+    n.ly = __ldg(src + 2);
+    n.lz = __ldg(src + 4);
+    n.hx = __ldg(src + 6);
+    n.hy = __ldg(src + 8);
+    n.hz = __ldg(src + 10);
+    n.ref = __ldg(src + 12);
+  }
+  return n;
+}
+
+template <bool ANY, class Fetch, class Finish>
+__device__ __forceinline__ void trace32_persistent8(const MeshDev& m, const float4* sn, int n,
+                                                    unsigned int* counter, Fetch fetch,
+                                                    Finish finish) {
+  const int lane = int(threadIdx.x & 31);
+  int rid = -1;
+  bool done = false;
+  float of[3], df[3], inv[3], ooi[3];
+  float tmaxf = 0.0f, best = 0.0f, bu = 0.0f, bv = 0.0f;
+  int bslot = -1, bid = INT_MAX, node = kDone, leaf = 0, sp = 0;
+  int stack[kStackDepth];
+  float stackt[kStackDepth];  // entry distance of each pushed child (culled when popped)
+  Node8Half nh;
+  auto pop = [&]() {
+    while (sp > 0) {
+      --sp;
+      if (ANY || stackt[sp] <= best) return stack[sp];
+    }
+    return kDone;
+  };
+  for (;;) {
+    const bool need = rid < 0 && !done;
+    const unsigned needm = __ballot_sync(0xffffffffu, need);
+    if (needm) {
+      const int leader = __ffs(needm) - 1;
+      unsigned base = 0;
+      if (lane == leader) base = atomicAdd(counter, unsigned(__popc(needm)));
+      base = __shfl_sync(0xffffffffu, base, leader);
+      if (need) {
+        const int idx = int(base + unsigned(__popc(needm & ((1u << lane) - 1u))));
+        if (idx < n) {
+          double o[3], d[3], tm;
+          rid = fetch(idx, o, d, tm);
+#pragma unroll
+          for (int k = 0; k < 3; ++k) {
+            of[k] = float(o[k]);
+            df[k] = float(d[k]);
+            inv[k] = 1.0f / (fabsf(df[k]) > 1e-20f ? df[k] : copysignf(1e-20f, df[k]));
+            ooi[k] = of[k] * inv[k];
+          }
+          tmaxf = float(tm);
+          best = tmaxf;
+          bu = bv = 0.0f;
+          bslot = -1;
+          bid = INT_MAX;
+          node = 0;
+          leaf = 0;
+          sp = 0;
+        } else {
+          done = true;
+        }
+      }
+    }
+    if (__all_sync(0xffffffffu, done)) break;
+    if (rid < 0) continue;
+    while (node >= 0 && node != kDone) {
+      // nearest hit child goes next, the other hits are pushed with their
+      // entry distances; the node is read in two halves of four children
+      int nx = kDone;
+      float tn = INFINITY;
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        if ((c & 3) == 0) nh = load_node8_half(m, sn, node, c >> 2);
+        float tc;
+        if (!slab6(f4c(nh.lx, c & 3), f4c(nh.ly, c & 3), f4c(nh.lz, c & 3), f4c(nh.hx, c & 3),
+                   f4c(nh.hy, c & 3), f4c(nh.hz, c & 3), ooi, inv, best, tc))
+          continue;
+        const int cr = __float_as_int(f4c(nh.ref, c & 3));
+        if (ANY || tc < tn) {
+          if (nx != kDone) {
+            stack[sp] = nx;
+            stackt[sp] = tn;
+            ++sp;
+          }
+          nx = cr;
+          tn = tc;
+        } else {
+          stack[sp] = cr;
+          stackt[sp] = tc;
+          ++sp;
+        }
+      }
+      node = nx != kDone ? nx : pop();
+      if (node < 0 && leaf == 0) {  // postpone the leaf, keep descending
+        leaf = node;
+        node = pop();
+      }
+      if (!__any_sync(__activemask(), leaf == 0)) break;
+    }
+    bool hit_any = false;
+    while (leaf < 0) {
+      const int first = (~leaf) >> 3, end = first + ((~leaf) & 7);
+      for (int s0 = first; s0 < end && !hit_any; s0 += 2) {
+        Tri32 tr[2];
+        tr[0] = load_tri32(m.tri32 + 3 * size_t(s0));
+        if (s0 + 1 < end) tr[1] = load_tri32(m.tri32 + 3 * size_t(s0 + 1));
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int sidx = s0 + e;
+          if (sidx >= end) break;
+          float t, u, v;
+          if (!tri_test32(tr[e], of, df, t, u, v) || !(t <= best)) continue;
+          if (ANY) {
+            if (t < tmaxf) {
+              bslot = sidx;
+              hit_any = true;
+              break;
+            }
+            continue;
+          }
+          const int id = __ldg(&m.orig[sidx]);
+          if (t < best || id < bid) {
+            best = t;
+            bu = u;
+            bv = v;
+            bslot = sidx;
+            bid = id;
+          }
+        }
+      }
+      if (hit_any) {
+        leaf = 0;
+        node = kDone;
+        break;
+      }
+      leaf = 0;
+      if (node < 0) {
+        leaf = node;
+        node = pop();
       }
     }
     if (node == kDone && leaf == 0) {
@@ -742,6 +963,8 @@ inline MeshDev dev_of(const mg_mesh_scene* s) {
   m.obj = s->obj;
   m.nodes = s->nodes;
   m.nnodes = s->nnodes;
+  m.nodes8 = s->nodes8;
+  m.nnodes8 = s->nnodes8;
   return m;
 }
 

@@ -14,6 +14,8 @@ namespace mg {
 bool g_mesh_megakernel = false;
 int g_mesh_persistent = -1;
 bool g_mesh_scatter_agg = false;
+bool g_mesh_bvh8 = false;
+bool g_mesh_smem_stack = true;
 int g_bvh_leaf = 2;
 namespace mesh {
 namespace {
@@ -284,6 +286,79 @@ int mg_meshscene_create(mg_ctx* ctx, int32_t tri_count, const double* tri, const
     dst[6] = make_float4(ibits(ref[0]), ibits(ref[1]), ibits(ref[2]), ibits(ref[3]));
     dst[7] = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
   }
+  // The BVH8 of the fp32 persistent traversal: the same binary tree
+  // collapsed eight-wide (open the largest-area internal child until eight
+  // children), breadth-first labels, boxes rounded and padded as above.
+  auto wide_children8 = [&](int x) {
+    std::vector<int> ch;
+    const TmpNode& nd = B.nodes[size_t(x)];
+    if (nd.left < 0) {
+      ch.push_back(x);
+      return ch;
+    }
+    ch = {nd.left, nd.right};
+    while (ch.size() < 8) {
+      int pick = -1;
+      double best = -1.0;
+      for (size_t k = 0; k < ch.size(); ++k)
+        if (B.nodes[size_t(ch[k])].left >= 0 && sarea(ch[k]) > best) {
+          best = sarea(ch[k]);
+          pick = int(k);
+        }
+      if (pick < 0) break;
+      const TmpNode& o = B.nodes[size_t(ch[size_t(pick)])];
+      ch[size_t(pick)] = o.left;
+      ch.push_back(o.right);
+    }
+    return ch;
+  };
+  std::vector<int> order8{0}, level8{0};
+  std::vector<std::vector<int>> kids8;
+  std::vector<int> label8(B.nodes.size(), -1);
+  label8[0] = 0;
+  int depth8 = 0;
+  for (size_t h = 0; h < order8.size(); ++h) {
+    kids8.push_back(wide_children8(order8[h]));
+    for (int c : kids8.back())
+      if (B.nodes[size_t(c)].left >= 0 && c != order8[h]) {
+        label8[size_t(c)] = int(order8.size());
+        order8.push_back(c);
+        level8.push_back(level8[h] + 1);
+        depth8 = std::max(depth8, level8[h] + 1);
+      }
+  }
+  // each step pushes at most 7 children
+  if (7 * (depth8 + 1) + 1 > kStackDepth)
+    return fail(MG_EINVAL, "mg_meshscene_create: BVH8 deeper than the traversal stack");
+  const int nn8 = int(order8.size());
+  std::vector<float4> nodes8(size_t(kNode8F4) * size_t(nn8));
+  for (int i = 0; i < nn8; ++i) {
+    float f[7][8];
+    for (int c = 0; c < 8; ++c) {
+      for (int a = 0; a < 3; ++a) {
+        f[a][c] = 1.0f;  // empty slot: inverted box, empty leaf
+        f[3 + a][c] = -1.0f;
+      }
+      f[6][c] = ibits(~0);
+    }
+    const std::vector<int>& ch = kids8[size_t(i)];
+    for (size_t c = 0; c < ch.size(); ++c) {
+      const TmpNode& nd = B.nodes[size_t(ch[c])];
+      for (int a = 0; a < 3; ++a) {
+        f[a][c] = nextafterf(float(nd.lo[a]), -INFINITY) - pad;
+        f[3 + a][c] = nextafterf(float(nd.hi[a]), INFINITY) + pad;
+      }
+      const int ref = (nd.left >= 0 && ch[c] != order8[size_t(i)])
+                          ? label8[size_t(ch[c])]
+                          : ~(nd.first * 8 + nd.count);
+      f[6][c] = ibits(ref);
+    }
+    float4* dst = &nodes8[size_t(kNode8F4) * size_t(i)];
+    for (int fl = 0; fl < 7; ++fl)
+      for (int hlf = 0; hlf < 2; ++hlf)
+        dst[2 * fl + hlf] = make_float4(f[fl][4 * hlf], f[fl][4 * hlf + 1], f[fl][4 * hlf + 2],
+                                        f[fl][4 * hlf + 3]);
+  }
   std::vector<double> stri(kRec * T);
   std::vector<int> sorig(T), sobj(T);
   std::vector<float4> stri32(3 * T);
@@ -304,6 +379,8 @@ int mg_meshscene_create(mg_ctx* ctx, int32_t tri_count, const double* tri, const
   sc->R = tex_res;
   sc->nnodes = nn;
   sc->depth = depth4;
+  sc->nnodes8 = nn8;
+  sc->depth8 = depth8;
   cudaError_t e = cudaMalloc(&sc->tri, sizeof(double) * stri.size());
   if (e == cudaSuccess) e = cudaMalloc(&sc->tri32, sizeof(float4) * stri32.size());
   if (e == cudaSuccess)
@@ -311,6 +388,9 @@ int mg_meshscene_create(mg_ctx* ctx, int32_t tri_count, const double* tri, const
   if (e == cudaSuccess) e = cudaMalloc(&sc->orig, sizeof(int) * T);
   if (e == cudaSuccess) e = cudaMalloc(&sc->obj, sizeof(int) * T);
   if (e == cudaSuccess) e = cudaMalloc(&sc->nodes, sizeof(float4) * nodes.size());
+  if (e == cudaSuccess) e = cudaMalloc(&sc->nodes8, sizeof(float4) * nodes8.size());
+  if (e == cudaSuccess)
+    e = cudaMemcpy(sc->nodes8, nodes8.data(), sizeof(float4) * nodes8.size(), cudaMemcpyHostToDevice);
   if (e == cudaSuccess) e = cudaMalloc(&sc->work, sizeof(unsigned int));
   if (e == cudaSuccess)
     e = cudaMemcpy(sc->tri, stri.data(), sizeof(double) * stri.size(), cudaMemcpyHostToDevice);
@@ -327,6 +407,7 @@ int mg_meshscene_create(mg_ctx* ctx, int32_t tri_count, const double* tri, const
     cudaFree(sc->orig);
     cudaFree(sc->obj);
     cudaFree(sc->nodes);
+    cudaFree(sc->nodes8);
     cudaFree(sc->work);
     delete sc;
     return cuda_fail(e, "mg_meshscene_create");
@@ -342,6 +423,7 @@ int mg_meshscene_destroy(mg_mesh_scene* s) {
   cudaFree(s->orig);
   cudaFree(s->obj);
   cudaFree(s->nodes);
+  cudaFree(s->nodes8);
   cudaFree(s->work);
   cudaFree(s->wf);
   delete s;

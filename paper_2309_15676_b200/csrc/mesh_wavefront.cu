@@ -200,12 +200,19 @@ __global__ void __launch_bounds__(kMThreads, 8) wf_isect_kernel(MeshDev m, WF<T>
   }
 }
 
-// fp32 mode: persistent closest-hit traversal (trace32_persistent)
-__global__ void __launch_bounds__(kMThreads, 8) wf_isect_p_kernel(MeshDev m, WF<float> w, int v) {
-  MESH_SMEM;
+// fp32 mode, BVH8: the persistent traversals over the eight-wide tree
+// (kP8Blocks CTAs of 128 per SM: 85 registers hold a node's 56 box / ref
+// words without spilling)
+#ifndef MG_P8_BLOCKS
+#define MG_P8_BLOCKS 6
+#endif
+constexpr int kP8Blocks = MG_P8_BLOCKS;
+__global__ void __launch_bounds__(kMThreads, kP8Blocks) wf_isect_p8_kernel(MeshDev m, WF<float> w, int v) {
+  __shared__ float4 sn[kNode8F4 * kSmemNodes8];
+  stage_nodes8(m, sn);
   const int n = int(w.cnt[v]);
   const int* qin = (v & 1) ? w.q1 : w.q0;
-  trace32_persistent<false>(
+  trace32_persistent8<false>(
       m, sn, n, &w.cnt[2 * (kMaxV + 1) + v],
       [&](int i, double o[3], double d[3], double& tm) {
         const int p = qin[i];
@@ -224,6 +231,38 @@ __global__ void __launch_bounds__(kMThreads, 8) wf_isect_p_kernel(MeshDev m, WF<
         w.hu[p] = u;
         w.hv[p] = vv;
       });
+}
+
+// fp32 mode: persistent closest-hit traversal (trace32_persistent)
+// SSTK: traversal stack in shared memory (24 KB per CTA; the top-node
+// stage is then off)
+template <bool SSTK>
+__global__ void __launch_bounds__(kMThreads, 8) wf_isect_p_kernel(MeshDev m, WF<float> w, int v) {
+  __shared__ float4 sn[SSTK ? 1 : kNodeF4 * kSmemNodes];
+  __shared__ int sstk[SSTK ? kSmemStack * kMThreads : 1];
+  if (!SSTK) stage_nodes(m, sn);
+  const int n = int(w.cnt[v]);
+  const int* qin = (v & 1) ? w.q1 : w.q0;
+  trace32_persistent<false, SSTK>(
+      m, sn, n, &w.cnt[2 * (kMaxV + 1) + v],
+      [&](int i, double o[3], double d[3], double& tm) {
+        const int p = qin[i];
+        o[0] = w.ox[p];
+        o[1] = w.oy[p];
+        o[2] = w.oz[p];
+        d[0] = w.dx[p];
+        d[1] = w.dy[p];
+        d[2] = w.dz[p];
+        tm = INFINITY;
+        return p;
+      },
+      [&](int p, int slot, double t, double u, double vv) {
+        w.hslot[p] = slot;
+        w.ht[p] = t;
+        w.hu[p] = u;
+        w.hv[p] = vv;
+      },
+      sstk);
 }
 
 template <class T, int NCH>
@@ -481,11 +520,43 @@ __global__ void __launch_bounds__(kMThreads, 8) wf_shadow_kernel(MeshDev m, WF<T
 }
 
 // fp32 mode: persistent any-hit traversal of the NEE rays
-template <int NCH>
+template <int NCH, bool SSTK>
 __global__ void __launch_bounds__(kMThreads, 8) wf_shadow_p_kernel(MeshDev m, WF<float> w, int v) {
-  MESH_SMEM;
+  __shared__ float4 sn[SSTK ? 1 : kNodeF4 * kSmemNodes];
+  __shared__ int sstk[SSTK ? kSmemStack * kMThreads : 1];
+  if (!SSTK) stage_nodes(m, sn);
   const int n = int(w.cnt[kMaxV + 1 + v]);
-  trace32_persistent<true>(
+  trace32_persistent<true, SSTK>(
+      m, sn, n, &w.cnt[3 * (kMaxV + 1) + v],
+      [&](int i, double o[3], double d[3], double& tm) {
+        const int p = w.sq[i];
+        o[0] = w.sox[p];
+        o[1] = w.soy[p];
+        o[2] = w.soz[p];
+        d[0] = w.sdx[p];
+        d[1] = w.sdy[p];
+        d[2] = w.sdz[p];
+        tm = w.stm[p];
+        return p;
+      },
+      [&](int p, int slot, double, double, double) {
+        if (slot < 0) {
+          const int k = p / w.npix;
+          const int nj = (k == 0 || k == w.nprop) ? 6 : 3;
+          for (int j = 0; j < nj; ++j) w.L[size_t(j) * w.P + p] += w.pendC[size_t(j) * w.P + p];
+        } else if (p < w.PS) {  // occluded: no NEE data at this vertex
+          w.vnee[size_t(v) * w.PS + p] = 0;
+        }
+      },
+      sstk);
+}
+
+template <int NCH>
+__global__ void __launch_bounds__(kMThreads, kP8Blocks) wf_shadow_p8_kernel(MeshDev m, WF<float> w, int v) {
+  __shared__ float4 sn[kNode8F4 * kSmemNodes8];
+  stage_nodes8(m, sn);
+  const int n = int(w.cnt[kMaxV + 1 + v]);
+  trace32_persistent8<true>(
       m, sn, n, &w.cnt[3 * (kMaxV + 1) + v],
       [&](int i, double o[3], double d[3], double& tm) {
         const int p = w.sq[i];
@@ -888,8 +959,11 @@ int wavefront_pair(mg_ctx* ctx, mg_mesh_scene* s, const MeshK& q, int nprop, con
   const MeshDev m = dev_of(s);
   MG_CUDA_TRY(cudaMemsetAsync(w.cnt, 0, sizeof(unsigned int) * 4 * (kMaxV + 1), ctx->stream));
   const int grid = grid_for(ctx, w.P, kMThreads, 8);
-  // persistent traversals: one resident wave (8 CTAs of 128 per SM)
+  // persistent traversals: one resident wave (8 CTAs of 128 per SM; the
+  // BVH8 kernels kP8Blocks)
   const int pgrid = grid;
+  const int pgrid8 = grid_for(ctx, w.P, kMThreads, kP8Blocks);
+  const bool sstk = g_mesh_smem_stack && s->depth <= kSmemStackMaxDepth;
   const int pmode = g_mesh_persistent >= 0 ? g_mesh_persistent
                                             : (s->nnodes >= kPersistentIsectNodes ? 3 : 2);
   wf_gen_kernel<T><<<grid, kMThreads, 0, ctx->stream>>>(q, w);
@@ -902,8 +976,12 @@ int wavefront_pair(mg_ctx* ctx, mg_mesh_scene* s, const MeshK& q, int nprop, con
   for (int v = 0; v < maxv; ++v) {
     MG_NVTX(kDepthName[v]);
     if constexpr (sizeof(T) == 4) {
-      if (pmode & 1)
-        wf_isect_p_kernel<<<pgrid, kMThreads, 0, ctx->stream>>>(m, w, v);
+      if ((pmode & 1) && g_mesh_bvh8)
+        wf_isect_p8_kernel<<<pgrid8, kMThreads, 0, ctx->stream>>>(m, w, v);
+      else if ((pmode & 1) && sstk)
+        wf_isect_p_kernel<true><<<pgrid, kMThreads, 0, ctx->stream>>>(m, w, v);
+      else if (pmode & 1)
+        wf_isect_p_kernel<false><<<pgrid, kMThreads, 0, ctx->stream>>>(m, w, v);
       else
         wf_isect_kernel<T><<<grid, kMThreads, 0, ctx->stream>>>(m, w, v);
     } else {
@@ -913,8 +991,12 @@ int wavefront_pair(mg_ctx* ctx, mg_mesh_scene* s, const MeshK& q, int nprop, con
     wf_shade_kernel<T, NCH><<<grid, kMThreads, 0, ctx->stream>>>(q, m, w, v, thI[0], thI[1]);
     MG_LAUNCH_CHECK(ctx);
     if constexpr (sizeof(T) == 4) {
-      if (pmode & 2)
-        wf_shadow_p_kernel<NCH><<<pgrid, kMThreads, 0, ctx->stream>>>(m, w, v);
+      if ((pmode & 2) && g_mesh_bvh8)
+        wf_shadow_p8_kernel<NCH><<<pgrid8, kMThreads, 0, ctx->stream>>>(m, w, v);
+      else if ((pmode & 2) && sstk)
+        wf_shadow_p_kernel<NCH, true><<<pgrid, kMThreads, 0, ctx->stream>>>(m, w, v);
+      else if (pmode & 2)
+        wf_shadow_p_kernel<NCH, false><<<pgrid, kMThreads, 0, ctx->stream>>>(m, w, v);
       else
         wf_shadow_kernel<T, NCH><<<grid, kMThreads, 0, ctx->stream>>>(m, w, v);
     } else {
