@@ -127,6 +127,9 @@ typedef struct mg_ctx mg_ctx;
 int mg_ctx_create(int device, void* stream, mg_ctx** out);
 int mg_ctx_destroy(mg_ctx* ctx);
 int mg_ctx_synchronize(mg_ctx* ctx);
+/* Device-check build (libmgcuda_debug.so, MG_DEBUG_CHECKS) only: trips one
+ * device assert on purpose -> MG_ECUDA; release builds -> MG_EUNSUPPORTED. */
+int mg_debug_selftest(mg_ctx* ctx);
 void* mg_ctx_stream(mg_ctx* ctx);
 /* Device-side iteration index for graph-replayable optimisation loops: while
  * set (non-NULL), the quad and helix sample-pair kernels launched on ctx use

@@ -58,6 +58,23 @@ const char* mg_last_error(void) { return g_last_error.c_str(); }
 
 int mg_abi_version(void) { return MGCUDA_ABI_VERSION; }
 
+// Debug-check builds only: launches one kernel whose MG_DCHECK fails, so a
+// harness can prove the checks are compiled in (the launch then reports
+// the device assert as MG_ECUDA).  Release builds: MG_EUNSUPPORTED.
+__global__ void mg_dcheck_selftest_kernel(int x) { MG_DCHECK(x == 0); }
+
+int mg_debug_selftest(mg_ctx* ctx) {
+#ifdef MG_DEBUG_CHECKS
+  if (!ctx) return mg::fail(MG_EINVAL, "mg_debug_selftest: null context");
+  mg_dcheck_selftest_kernel<<<1, 1, 0, ctx->stream>>>(1);
+  MG_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+  return MG_OK;
+#else
+  (void)ctx;
+  return mg::fail(MG_EUNSUPPORTED, "mg_debug_selftest: release build (no device checks)");
+#endif
+}
+
 // harness.hpp:18-67 field defaults
 void mg_config_defaults(mg_experiment_config* c) {
   memset(c, 0, sizeof(*c));

@@ -243,6 +243,7 @@ __device__ __forceinline__ int trace_impl(const MeshDev& m, const float4* sn, co
         }
       }
     } else {
+      MG_DCHECK(node < m.nnodes && sp + 4 <= kStackDepth);
       const NodeW n = load_node(m, sn, node);
       // (entry distance, child) of the hit children, sorted ascending by a
       // 4-input sorting network (misses carry +inf)
@@ -402,6 +403,7 @@ __device__ __forceinline__ int trace32_impl(const MeshDev& m, const float4* sn, 
         }
       }
     } else {
+      MG_DCHECK(node < m.nnodes && sp + 4 <= kStackDepth);
       const NodeW n = load_node(m, sn, node);
       float tk[4];
       int ck[4];
@@ -501,6 +503,7 @@ __device__ __forceinline__ void trace32_persistent(const MeshDev& m, const float
   int lstack[SMEM_STACK ? 1 : kStackDepth];
   int* const sstack = SMEM_STACK ? smem_stack + threadIdx.x : nullptr;
   auto push = [&](int v) {
+    MG_DCHECK(sp < (SMEM_STACK ? kSmemStack : kStackDepth));
     if constexpr (SMEM_STACK)
       sstack[(sp++) * kMThreads] = v;
     else
@@ -768,6 +771,7 @@ __device__ __forceinline__ void trace32_persistent8(const MeshDev& m, const floa
         const int cr = __float_as_int(f4c(nh.ref, c & 3));
         if (ANY || tc < tn) {
           if (nx != kDone) {
+            MG_DCHECK(sp < kStackDepth);
             stack[sp] = nx;
             stackt[sp] = tn;
             ++sp;
@@ -775,6 +779,7 @@ __device__ __forceinline__ void trace32_persistent8(const MeshDev& m, const floa
           nx = cr;
           tn = tc;
         } else {
+          MG_DCHECK(sp < kStackDepth);
           stack[sp] = cr;
           stackt[sp] = tc;
           ++sp;

@@ -143,6 +143,7 @@ __device__ __forceinline__ int enqueue(bool pred, unsigned int* counter) {
   base = __shfl_sync(act, base, leader);
   return pred ? int(base) + __popc(m & ((1u << lane) - 1u)) : -1;
 }
+// (callers check the slot against their queue's capacity with MG_DCHECK)
 
 template <class T>
 __device__ __forceinline__ T& vf(const WF<T>& w, int v, int f, int p) {
@@ -495,8 +496,10 @@ __global__ void __launch_bounds__(kMThreads)
       }
     }
     const int qs = enqueue(want_shadow, &w.cnt[kMaxV + 1 + v]);
+    MG_DCHECK(qs < w.P);
     if (qs >= 0) w.sq[qs] = p;
     const int qb = enqueue(want_bounce, &w.cnt[v + 1]);
+    MG_DCHECK(qb < w.P);
     if (qb >= 0) qout[qb] = p;
   }
 }
@@ -616,6 +619,9 @@ struct AccCell {
     }
   }
   __device__ __forceinline__ unsigned long long* at(const AccTable& a, int which, int k) const {
+    MG_DCHECK(which >= 0 && which < 2 && k >= 0 && k < NCH && base >= 0);
+    MG_DCHECK(ILV ? (q + which * NCH + k) < a.ptr[0] + 2 * size_t(a.shard)
+                  : (base + k * R2) / a.shard < kMaxRanks);
     return ILV ? q + which * NCH + k : acc_slot(a, base + k * R2, which);
   }
 };

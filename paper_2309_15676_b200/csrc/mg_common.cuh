@@ -34,6 +34,19 @@ int cuda_fail(cudaError_t e, const char* what);
     if (mg_e_ != cudaSuccess) return ::mg::cuda_fail(mg_e_, "kernel launch"); \
   } while (0)
 
+// Device-side invariant checks, compiled in only for the debug-check build
+// (make -C paper_2309_15676_b200/csrc debug -> libmgcuda_debug.so, used by
+// tools/debug_checks.sh in place of compute-sanitizer, which is closed on
+// the GPU pool): ring / tile bounds, queue and stack capacities,
+// accumulator cells, reduction grid sizes.  A failed check is a device
+// assert (message + trap).
+#ifdef MG_DEBUG_CHECKS
+#include <assert.h>
+#define MG_DCHECK(x) assert(x)
+#else
+#define MG_DCHECK(x) ((void)0)
+#endif
+
 // NVTX range over a host entry point / pipeline stage (header-only NVTX3: a
 // no-op unless a profiler injects itself; ncu --nvtx --nvtx-include can
 // filter kernels by these names)
@@ -176,6 +189,7 @@ __device__ __forceinline__ void grid_reduce4(ReducePartials acc, ReducePartials*
                                              unsigned int* counter, Fin fin) {
   __shared__ double sw[kThreads / 32];
   __shared__ bool is_last;
+  MG_DCHECK(gridDim.x <= unsigned(kMaxReduceBlocks) && blockDim.x == unsigned(kThreads));
   const double s0 = block_sum<kThreads>(acc.ssn, sw);
   const double s1 = block_sum<kThreads>(acc.changed, sw);
   const double s2 = block_sum<kThreads>(acc.loss, sw);

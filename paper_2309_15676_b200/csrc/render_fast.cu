@@ -235,6 +235,7 @@ __global__ void __launch_bounds__(THREADS, CTAS)
   auto issue = [&](int64_t li) {  // r == 0 only
     const int st = int(li % STAGES);
     const int64_t tile = gunit + li * nunits;
+    MG_DCHECK((tile + 1) * TILE <= P && st < STAGES);
     mbar_arrive_expect_tx(&full[st], tx);
 #pragma unroll
     for (int a = 0; a < kArrays; ++a)

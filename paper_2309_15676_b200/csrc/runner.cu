@@ -550,6 +550,7 @@ __device__ void produce_stream(uint64_t* ring, uint64_t* pbar, uint64_t seed, ui
       while (!try_wait_cluster(&full[b & 1], uint32_t((b >> 1) & 1))) {
       }
       const int64_t base = b * kBatchWords;
+      MG_DCHECK(b >= 0 && (base < total || total == 0));
       for (int o = e; o < kBatchWords; o += kEmitThreads) {
         const int64_t g = base + o;
         if (g < total) out[g] = mt_uniform(mt_temper(slot(b * kBatchChunks + o / kChunkW)[o % kChunkW]));
@@ -581,6 +582,7 @@ __global__ void __launch_bounds__(kThreads) run_cluster_kernel(RunK<T> k, double
   __shared__ double tot[4];
   const mg_experiment_config& c = k.cfg;
   const uint32_t rank = cluster_rank(), NC = cluster_size(), M = NC - 1;
+  MG_DCHECK(NC >= 2 && NC <= uint32_t(kClusterMax) && blockDim.x == unsigned(kThreads));
   const int r = blockIdx.x / NC;  // replicate within the launch
   const int d = k.dim, iters = c.iterations, spp = c.spp;
   const int64_t D = k.D;
@@ -730,6 +732,7 @@ __global__ void __launch_bounds__(kThreads) run_cluster_kernel(RunK<T> k, double
     for (int q = 0; q < kPPT; ++q) {
       if (!own[q]) continue;
       const int j = lo + int(threadIdx.x) + q * kThreads;
+      MG_DCHECK(j < hi && hi <= d);
       // sample_pair (problems.cpp:197-217)
       T cross, mb;
       const double* uj = u + size_t(j) * spp;

@@ -193,6 +193,7 @@ __global__ void __launch_bounds__(kTmaThreads, kMinBlocks)
   auto issue = [&](int64_t li) {  // thread 0 only
     const int st = int(li % kTmaStages);
     const int64_t tile = int64_t(blockIdx.x) + li * gridDim.x;
+    MG_DCHECK((tile + 1) * TILE <= n && st < kTmaStages);
     mbar_arrive_expect_tx(&full[st], tx);
 #pragma unroll
     for (int a = 0; a < kTmaArrays; ++a)
