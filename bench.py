@@ -108,13 +108,16 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.samples)}
 
 
+TRAFFIC_FILE = os.path.join("profiles", "r02_meta_update_traffic.json")
+
+
 def ncu_traffic(n, dtype):
-    """DRAM bytes per launch of the fused update from the committed ncu
-    capture (profiles/r01_meta_update_traffic.json: dram__bytes_read.sum +
-    dram__bytes_write.sum at 2^28 fp32), scaled to n; None if not captured
-    for this dtype."""
+    """DRAM bytes per launch of the fused update: NOT measured by this run —
+    the committed ncu capture (TRAFFIC_FILE: dram__bytes_read.sum +
+    dram__bytes_write.sum of one launch at 2^28 fp32, tools/profile_r02.sh)
+    scaled to n; None for a dtype not captured."""
     try:
-        with open(os.path.join(ROOT, "profiles", "r01_meta_update_traffic.json")) as f:
+        with open(os.path.join(ROOT, TRAFFIC_FILE)) as f:
             d = json.load(f)
         return d["bytes_per_param"] * n if dtype == "f32" else None
     except Exception:
@@ -344,6 +347,8 @@ def run_ours(args):
             "pool_batches": args.pool,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": ncu_traffic(n, args.dtype),
+                         "traffic_source": f"committed ncu capture {TRAFFIC_FILE} "
+                                           "(bytes/param x n), not this run",
                          "frac_vs_8tbs_spec": achieved / 8000.0,
                          "peak_kind": peak_kind,
                          "kernel_ms": k_ms, "algorithmic_bytes": algo_bytes},
@@ -705,16 +710,27 @@ def extras(args, ctx):
                                         "texture_params": prob.dim(), **prob.scene.info()}
 
     def runner():
-        # reference harness stand-in for configs[0] (mini-render P=4096,
-        # spp=2, 200 iterations), 148 replicates as one device launch
-        cfg = api.ExperimentConfig(problem="mini-render", pixel_count=4096, spp=2,
-                                   iterations=200, seed=0, problem_seed=1, lr=0.01,
-                                   replicates=148)
-        t0 = time.time()
-        api.run_experiment(cfg, ctx=ctx)
-        wall = time.time() - t0
-        out["minirender_runner"] = {"replicates": 148, "iterations": 200, "wall_s": wall,
-                                    "pairs_per_s": 148 * 200 * 4096 * 2 / wall}
+        # reference harness stand-in for configs[0] (S1: mini-render P=4096,
+        # spp=2, 200 iterations, meta) through api.run_experiment, wall clock
+        # around the call (median of 5 after one warm-up): one replicate (a
+        # thread-block cluster: producer CTA for the exact mt19937_64 stream,
+        # consumer CTAs holding the state in registers) and 148 replicates
+        # (one CTA each, one launch)
+        import statistics
+        for reps, key in ((1, "minirender_s1_single_replicate"), (148, "minirender_runner")):
+            cfg = api.ExperimentConfig(problem="mini-render", pixel_count=4096, spp=2,
+                                       iterations=200, seed=0, problem_seed=1, lr=0.01,
+                                       replicates=reps)
+            api.run_experiment(cfg, ctx=ctx)
+            walls = []
+            for _ in range(5):
+                t0 = time.time()
+                api.run_experiment(cfg, ctx=ctx)
+                walls.append(time.time() - t0)
+            wall = statistics.median(walls)
+            out[key] = {"replicates": reps, "iterations": 200, "wall_s": wall,
+                        "pairs_per_s": reps * 200 * 4096 * 2 / wall,
+                        "runner": "cluster" if reps == 1 else "one CTA per replicate"}
 
     for name, fn in (("update_f64", update_f64), ("update_sizes", update_sizes), ("adam", adam), ("minirender_philox", lambda: minirender("philox")),
                      ("minirender_mt64", lambda: minirender("mt64")), ("quad", quad),
