@@ -364,7 +364,23 @@ def run_ours(args):
     del props, diffs
     torch.cuda.empty_cache()
     if world > 1 and not args.no_extras:
-        sh = sharded_extras(args, ctx, pg, rank, world)
+        # first multi-rank run of the peer-memory path happens on the
+        # driver's box: a watchdog keeps the headline line if the extra
+        # hangs (every rank exits 0 after rank 0 has printed it)
+        def give_up():
+            if rank == 0:
+                out = dict(line)
+                out["extras"] = {"mesh_large_tiled_error": "timed out after 300 s"}
+                print(json.dumps(out), flush=True)
+            os._exit(0)
+        dog = threading.Timer(300.0, give_up)
+        dog.daemon = True
+        dog.start()
+        try:
+            sh = sharded_extras(args, ctx, pg, rank, world)
+        except Exception as e:  # recorded; the other ranks hit the watchdog
+            sh = {"mesh_large_tiled_error": f"{type(e).__name__}: {e}"}
+        dog.cancel()
         if rank == 0:
             line["extras"] = sh
     if rank == 0 and not args.no_extras and (world == 1 or args.extras):
@@ -423,9 +439,16 @@ def sharded_extras(args, ctx, pg, rank, world):
     if not agree(err is None):
         out["mesh_large_tiled_error"] = err or "another rank failed to build the scene"
         return out
-    for _ in range(2):
-        step.step()
-    torch.cuda.synchronize()
+    try:
+        for _ in range(2):
+            step.step()
+        torch.cuda.synchronize()
+        ok = True
+    except Exception as e:
+        err, ok = f"{type(e).__name__}: {e}", False
+    if not agree(ok):
+        out["mesh_large_tiled_error"] = err or "another rank failed in the warm-up iterations"
+        return out
     pg.barrier()
     K = 5
     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
