@@ -114,6 +114,8 @@ int mg_abi_version(void);
  *                              BVH (measured slower; off by default)
  *   "mesh_smem_stack"          1 (default): persistent BVH4 traversal stack in
  *                              shared memory; 0: local memory + top nodes staged
+ *   "mesh_qnodes"              1 (default): that traversal reads 64-byte nodes
+ *                              with 8-bit quantised child boxes; 0: fp32 nodes
  *   "mesh_scatter_aggregate"=1 warp-aggregated mesh adjoint scatter (measured
  *                              slower at configs[3]/[4]; off by default)
  *   "render_vec", "bvh_leaf_size", "mesh_megakernel": see DESIGN.md */

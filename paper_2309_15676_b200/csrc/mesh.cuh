@@ -27,6 +27,7 @@ struct mg_mesh_scene {
   int* obj = nullptr;      // [T] object id (BVH order)
   float4* nodes = nullptr; // [kNodeF4 * nnodes]: BVH4 (see NodeW)
   float4* nodes8 = nullptr; // [kNode8F4 * nnodes8]: BVH8 of the fp32 persistent traversal
+  float4* nodesq = nullptr; // [kNodeQF4 * nnodes]: the BVH4 with quantised child boxes
   int nnodes8 = 0, depth8 = 0;
   unsigned int* work = nullptr;  // pixel work counter of the pair kernel
   void* wf = nullptr;            // wavefront path state (grow-only)
@@ -53,6 +54,9 @@ constexpr int kPersistentIsectNodes = 32768;
 // their stack in shared memory ([entry][thread], conflict-free) instead of
 // staging the top nodes there
 extern bool g_mesh_smem_stack;
+// mg_set_option("mesh_qnodes", 0): the shared-memory-stack traversal reads
+// the full fp32 BVH4 nodes instead of the quantised 64-byte copies
+extern bool g_mesh_qnodes;
 // mg_set_option("mesh_bvh8", 0): the persistent fp32 traversals walk the
 // BVH4 instead of the BVH8
 extern bool g_mesh_bvh8;
@@ -87,6 +91,7 @@ struct MeshDev {
   int nnodes;
   const float4* __restrict__ nodes8;
   int nnodes8;
+  const float4* __restrict__ nodesq;
 };
 
 struct MeshK {
@@ -142,6 +147,7 @@ __device__ __forceinline__ bool tri_hit(const double* __restrict__ r, const doub
 #define MG_ANY_SORT 0
 #endif
 constexpr int kNodeF4 = 8;
+constexpr int kNodeQF4 = 4;  // quantised BVH4 node: 64 bytes
 struct NodeW {
   float4 lx, ly, lz, hx, hy, hz, ref;
 };
@@ -490,7 +496,7 @@ constexpr int kDone = INT_MAX;
 constexpr int kSmemStack = 48;
 constexpr int kSmemStackMaxDepth = (kSmemStack - 1) / 3 - 1;
 
-template <bool ANY, bool SMEM_STACK = false, class Fetch, class Finish>
+template <bool ANY, bool SMEM_STACK = false, bool QNODES = false, class Fetch, class Finish>
 __device__ __forceinline__ void trace32_persistent(const MeshDev& m, const float4* sn, int n,
                                                    unsigned int* counter, Fetch fetch,
                                                    Finish finish, int* smem_stack = nullptr) {
@@ -553,16 +559,52 @@ __device__ __forceinline__ void trace32_persistent(const MeshDev& m, const float
     if (rid < 0) continue;
     // inner nodes until every active lane has a leaf waiting
     while (node >= 0 && node != kDone) {
-      const NodeW nd = load_node<!SMEM_STACK>(m, sn, node);
       float tk[4];
       int ck[4];
+      if constexpr (QNODES) {
+        // 64-byte node: header, 24 plane bytes, refs.  Plane t of child c,
+        // axis a: (p + q s - o) inv = q (s inv) + (p - o) inv, q decoded
+        // exactly from its byte (0x4B0000qq as a float is 2^23 + q)
+        const float4* src = m.nodesq + size_t(kNodeQF4) * node;
+        const float4 hd = __ldg(src), q0 = __ldg(src + 1), q1 = __ldg(src + 2), rf = __ldg(src + 3);
+        const unsigned eb = __float_as_uint(hd.w);
+        const float pa[3] = {hd.x, hd.y, hd.z};
+        float A[3], Bo[3];
 #pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        float tc;
-        const bool h = slab6(f4c(nd.lx, c), f4c(nd.ly, c), f4c(nd.lz, c), f4c(nd.hx, c),
-                             f4c(nd.hy, c), f4c(nd.hz, c), ooi, inv, best, tc);
-        tk[c] = h ? tc : INFINITY;
-        ck[c] = __float_as_int(f4c(nd.ref, c));
+        for (int a = 0; a < 3; ++a) {
+          A[a] = __uint_as_float(((eb >> (8 * a)) & 255u) << 23) * inv[a];
+          Bo[a] = (pa[a] - of[a]) * inv[a];
+        }
+        const unsigned qw[6] = {__float_as_uint(q0.x), __float_as_uint(q0.y),
+                                __float_as_uint(q0.z), __float_as_uint(q0.w),
+                                __float_as_uint(q1.x), __float_as_uint(q1.y)};
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          float t[6];
+#pragma unroll
+          for (int f = 0; f < 6; ++f) {
+            const float qf =
+                __uint_as_float(__byte_perm(qw[f], 0x4B000000u, 0x7650u | unsigned(c))) -
+                8388608.0f;
+            t[f] = fmaf(qf, A[f % 3], Bo[f % 3]);
+          }
+          const float tn = fmaxf(fmaxf(fminf(t[0], t[3]), fminf(t[1], t[4])),
+                                 fmaxf(fminf(t[2], t[5]), 0.0f));
+          const float tf = fminf(fminf(fmaxf(t[0], t[3]), fmaxf(t[1], t[4])),
+                                 fminf(fmaxf(t[2], t[5]), best));
+          tk[c] = tn <= tf ? tn : INFINITY;
+          ck[c] = __float_as_int(f4c(rf, c));
+        }
+      } else {
+        const NodeW nd = load_node<!SMEM_STACK>(m, sn, node);
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          float tc;
+          const bool h = slab6(f4c(nd.lx, c), f4c(nd.ly, c), f4c(nd.lz, c), f4c(nd.hx, c),
+                               f4c(nd.hy, c), f4c(nd.hz, c), ooi, inv, best, tc);
+          tk[c] = h ? tc : INFINITY;
+          ck[c] = __float_as_int(f4c(nd.ref, c));
+        }
       }
       auto cx = [&](int a, int b) {
         if (tk[b] < tk[a]) {
@@ -970,6 +1012,7 @@ inline MeshDev dev_of(const mg_mesh_scene* s) {
   m.nnodes = s->nnodes;
   m.nodes8 = s->nodes8;
   m.nnodes8 = s->nnodes8;
+  m.nodesq = s->nodesq;
   return m;
 }
 

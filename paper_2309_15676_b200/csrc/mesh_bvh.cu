@@ -16,9 +16,12 @@ int g_mesh_persistent = -1;
 bool g_mesh_scatter_agg = false;
 bool g_mesh_bvh8 = false;
 bool g_mesh_smem_stack = true;
+bool g_mesh_qnodes = true;
 int g_bvh_leaf = 2;
 namespace mesh {
 namespace {
+
+float f4c_host(const float4& v, int c) { return c == 0 ? v.x : (c == 1 ? v.y : (c == 2 ? v.z : v.w)); }
 
 // ------------------------------------------------------------ host BVH
 struct TmpNode {
@@ -286,6 +289,67 @@ int mg_meshscene_create(mg_ctx* ctx, int32_t tri_count, const double* tri, const
     dst[6] = make_float4(ibits(ref[0]), ibits(ref[1]), ibits(ref[2]), ibits(ref[3]));
     dst[7] = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
   }
+  // Quantised copy of the BVH4 for the fp32 persistent traversal (64-byte
+  // nodes): header (p.xyz = the node box's lower corner as the children's
+  // float minimum, w = three biased exponents e: scale s = 2^(e-127) >=
+  // extent / 255 per axis), then per axis and child one byte each for the
+  // lower and upper plane, q_lo = floor((lo - p) / s), q_hi = ceil((hi - p)
+  // / s) — exact in double, so the decoded box p + q s contains the padded
+  // fp32 box (conservative like it); the child refs unchanged.  Empty slots
+  // decode to the single point p (q = 0: hit with probability zero).
+  std::vector<float4> nodesq(size_t(kNodeQF4) * size_t(nn));
+  for (int i = 0; i < nn; ++i) {
+    const float4* src = &nodes[size_t(kNodeF4) * size_t(i)];
+    float lo[3][4], hi[3][4];
+    bool used[4];
+    for (int c = 0; c < 4; ++c) {
+      for (int a = 0; a < 3; ++a) {
+        lo[a][c] = f4c_host(src[a], c);
+        hi[a][c] = f4c_host(src[3 + a], c);
+      }
+      used[c] = lo[0][c] <= hi[0][c];
+    }
+    float P[3];
+    unsigned ex[3];
+    double sc[3];
+    for (int a = 0; a < 3; ++a) {
+      float mn = INFINITY, mx = -INFINITY;
+      for (int c = 0; c < 4; ++c)
+        if (used[c]) {
+          mn = std::min(mn, lo[a][c]);
+          mx = std::max(mx, hi[a][c]);
+        }
+      if (!(mn <= mx)) mn = mx = 0.0f;  // no child (cannot happen for a built node)
+      P[a] = mn;
+      const double ext = double(mx) - double(mn);
+      int e = -126;
+      while (e < 127 && std::ldexp(255.0, e) < ext) ++e;
+      ex[a] = unsigned(e + 127);
+      sc[a] = std::ldexp(1.0, e);
+    }
+    unsigned q[6] = {0, 0, 0, 0, 0, 0};  // lo x, y, z, hi x, y, z (byte c = child c)
+    for (int c = 0; c < 4; ++c) {
+      if (!used[c]) continue;
+      for (int a = 0; a < 3; ++a) {
+        double ql = std::floor((double(lo[a][c]) - double(P[a])) / sc[a]);
+        double qh = std::ceil((double(hi[a][c]) - double(P[a])) / sc[a]);
+        ql = std::min(255.0, std::max(0.0, ql));
+        qh = std::min(255.0, std::max(0.0, qh));
+        q[a] |= unsigned(ql) << (8 * c);
+        q[3 + a] |= unsigned(qh) << (8 * c);
+      }
+    }
+    float4* dst = &nodesq[size_t(kNodeQF4) * size_t(i)];
+    auto ubits = [](unsigned v) {
+      float f;
+      memcpy(&f, &v, 4);
+      return f;
+    };
+    dst[0] = make_float4(P[0], P[1], P[2], ubits(ex[0] | (ex[1] << 8) | (ex[2] << 16)));
+    dst[1] = make_float4(ubits(q[0]), ubits(q[1]), ubits(q[2]), ubits(q[3]));
+    dst[2] = make_float4(ubits(q[4]), ubits(q[5]), 0.0f, 0.0f);
+    dst[3] = src[6];
+  }
   // The BVH8 of the fp32 persistent traversal: the same binary tree
   // collapsed eight-wide (open the largest-area internal child until eight
   // children), breadth-first labels, boxes rounded and padded as above.
@@ -388,6 +452,9 @@ int mg_meshscene_create(mg_ctx* ctx, int32_t tri_count, const double* tri, const
   if (e == cudaSuccess) e = cudaMalloc(&sc->orig, sizeof(int) * T);
   if (e == cudaSuccess) e = cudaMalloc(&sc->obj, sizeof(int) * T);
   if (e == cudaSuccess) e = cudaMalloc(&sc->nodes, sizeof(float4) * nodes.size());
+  if (e == cudaSuccess) e = cudaMalloc(&sc->nodesq, sizeof(float4) * nodesq.size());
+  if (e == cudaSuccess)
+    e = cudaMemcpy(sc->nodesq, nodesq.data(), sizeof(float4) * nodesq.size(), cudaMemcpyHostToDevice);
   if (e == cudaSuccess) e = cudaMalloc(&sc->nodes8, sizeof(float4) * nodes8.size());
   if (e == cudaSuccess)
     e = cudaMemcpy(sc->nodes8, nodes8.data(), sizeof(float4) * nodes8.size(), cudaMemcpyHostToDevice);
@@ -408,6 +475,7 @@ int mg_meshscene_create(mg_ctx* ctx, int32_t tri_count, const double* tri, const
     cudaFree(sc->obj);
     cudaFree(sc->nodes);
     cudaFree(sc->nodes8);
+    cudaFree(sc->nodesq);
     cudaFree(sc->work);
     delete sc;
     return cuda_fail(e, "mg_meshscene_create");
@@ -424,6 +492,7 @@ int mg_meshscene_destroy(mg_mesh_scene* s) {
   cudaFree(s->obj);
   cudaFree(s->nodes);
   cudaFree(s->nodes8);
+  cudaFree(s->nodesq);
   cudaFree(s->work);
   cudaFree(s->wf);
   delete s;

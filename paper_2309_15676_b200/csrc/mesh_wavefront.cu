@@ -237,14 +237,14 @@ __global__ void __launch_bounds__(kMThreads, kP8Blocks) wf_isect_p8_kernel(MeshD
 // fp32 mode: persistent closest-hit traversal (trace32_persistent)
 // SSTK: traversal stack in shared memory (24 KB per CTA; the top-node
 // stage is then off)
-template <bool SSTK>
+template <bool SSTK, bool QN = false>
 __global__ void __launch_bounds__(kMThreads, 8) wf_isect_p_kernel(MeshDev m, WF<float> w, int v) {
   __shared__ float4 sn[SSTK ? 1 : kNodeF4 * kSmemNodes];
   __shared__ int sstk[SSTK ? kSmemStack * kMThreads : 1];
   if (!SSTK) stage_nodes(m, sn);
   const int n = int(w.cnt[v]);
   const int* qin = (v & 1) ? w.q1 : w.q0;
-  trace32_persistent<false, SSTK>(
+  trace32_persistent<false, SSTK, QN>(
       m, sn, n, &w.cnt[2 * (kMaxV + 1) + v],
       [&](int i, double o[3], double d[3], double& tm) {
         const int p = qin[i];
@@ -523,13 +523,13 @@ __global__ void __launch_bounds__(kMThreads, 8) wf_shadow_kernel(MeshDev m, WF<T
 }
 
 // fp32 mode: persistent any-hit traversal of the NEE rays
-template <int NCH, bool SSTK>
+template <int NCH, bool SSTK, bool QN = false>
 __global__ void __launch_bounds__(kMThreads, 8) wf_shadow_p_kernel(MeshDev m, WF<float> w, int v) {
   __shared__ float4 sn[SSTK ? 1 : kNodeF4 * kSmemNodes];
   __shared__ int sstk[SSTK ? kSmemStack * kMThreads : 1];
   if (!SSTK) stage_nodes(m, sn);
   const int n = int(w.cnt[kMaxV + 1 + v]);
-  trace32_persistent<true, SSTK>(
+  trace32_persistent<true, SSTK, QN>(
       m, sn, n, &w.cnt[3 * (kMaxV + 1) + v],
       [&](int i, double o[3], double d[3], double& tm) {
         const int p = w.sq[i];
@@ -984,6 +984,8 @@ int wavefront_pair(mg_ctx* ctx, mg_mesh_scene* s, const MeshK& q, int nprop, con
     if constexpr (sizeof(T) == 4) {
       if ((pmode & 1) && g_mesh_bvh8)
         wf_isect_p8_kernel<<<pgrid8, kMThreads, 0, ctx->stream>>>(m, w, v);
+      else if ((pmode & 1) && sstk && g_mesh_qnodes)
+        wf_isect_p_kernel<true, true><<<pgrid, kMThreads, 0, ctx->stream>>>(m, w, v);
       else if ((pmode & 1) && sstk)
         wf_isect_p_kernel<true><<<pgrid, kMThreads, 0, ctx->stream>>>(m, w, v);
       else if (pmode & 1)
@@ -999,6 +1001,8 @@ int wavefront_pair(mg_ctx* ctx, mg_mesh_scene* s, const MeshK& q, int nprop, con
     if constexpr (sizeof(T) == 4) {
       if ((pmode & 2) && g_mesh_bvh8)
         wf_shadow_p8_kernel<NCH><<<pgrid8, kMThreads, 0, ctx->stream>>>(m, w, v);
+      else if ((pmode & 2) && sstk && g_mesh_qnodes)
+        wf_shadow_p_kernel<NCH, true, true><<<pgrid, kMThreads, 0, ctx->stream>>>(m, w, v);
       else if ((pmode & 2) && sstk)
         wf_shadow_p_kernel<NCH, true><<<pgrid, kMThreads, 0, ctx->stream>>>(m, w, v);
       else if (pmode & 2)

@@ -36,6 +36,7 @@ extern int g_mesh_persistent;
 extern bool g_mesh_scatter_agg;
 extern bool g_mesh_bvh8;
 extern bool g_mesh_smem_stack;
+extern bool g_mesh_qnodes;
 extern int g_bvh_leaf;
 // -1: per-dtype default measured on B200 (tools/sweep_update_variants.py,
 // profiles/r01_sweep_update_variants_*): fp32 -> variant 6 (2 CTAs/SM x 192
@@ -740,6 +741,10 @@ int mg_set_option(const char* name, int64_t value) {
   if (std::string(name) == "bvh_leaf_size") {
     if (value < 1 || value > 7) return fail(MG_EINVAL, "bvh_leaf_size must lie in [1, 7]");
     g_bvh_leaf = int(value);
+    return MG_OK;
+  }
+  if (std::string(name) == "mesh_qnodes") {
+    g_mesh_qnodes = value != 0;
     return MG_OK;
   }
   if (std::string(name) == "mesh_smem_stack") {
