@@ -45,11 +45,11 @@ namespace mg {
 extern bool g_mesh_megakernel;
 // mg_set_option("mesh_persistent", 0): fp32 isect / shadow stages with the
 // grid-stride one-ray-per-thread traversal instead of the persistent warp loop
-// bit 0: isect, bit 1: shadow; -1 (default): shadow always, isect for scenes
-// of >= kPersistentIsectNodes BVH nodes (configs[4]: -0.4 ms; on configs[3]'s
-// 5.9k-node BVH the fetch overhead outweighs the gain: +0.035 ms)
+// bit 0: isect, bit 1: shadow; -1 (default): both.  (With the local-memory
+// stack and fp32 nodes, the persistent isect lost on configs[3]'s 5.9k-node
+// BVH, +0.035 ms; with the shared-memory stack and quantised nodes it wins
+// there too, 1.211 -> 1.143 ms.)
 extern int g_mesh_persistent;
-constexpr int kPersistentIsectNodes = 32768;
 // mg_set_option("mesh_smem_stack", 1): the persistent BVH4 traversals keep
 // their stack in shared memory ([entry][thread], conflict-free) instead of
 // staging the top nodes there

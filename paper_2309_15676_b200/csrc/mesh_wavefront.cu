@@ -970,8 +970,7 @@ int wavefront_pair(mg_ctx* ctx, mg_mesh_scene* s, const MeshK& q, int nprop, con
   const int pgrid = grid;
   const int pgrid8 = grid_for(ctx, w.P, kMThreads, kP8Blocks);
   const bool sstk = g_mesh_smem_stack && s->depth <= kSmemStackMaxDepth;
-  const int pmode = g_mesh_persistent >= 0 ? g_mesh_persistent
-                                            : (s->nnodes >= kPersistentIsectNodes ? 3 : 2);
+  const int pmode = g_mesh_persistent >= 0 ? g_mesh_persistent : 3;
   wf_gen_kernel<T><<<grid, kMThreads, 0, ctx->stream>>>(q, w);
   MG_LAUNCH_CHECK(ctx);
   const int maxv = int(q.view[24]);
