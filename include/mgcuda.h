@@ -118,6 +118,8 @@ int mg_abi_version(void);
  *                              with 8-bit quantised child boxes; 0: fp32 nodes
  *   "mesh_scatter_aggregate"=1 warp-aggregated mesh adjoint scatter (measured
  *                              slower at configs[3]/[4]; off by default)
+ *   "helix_split" = 0          configs[2] sample pair in one kernel (whole
+ *                              pixels per thread) instead of path / combine
  *   "render_vec", "bvh_leaf_size", "mesh_megakernel": see DESIGN.md */
 int mg_set_option(const char* name, int64_t value);
 

@@ -171,6 +171,7 @@ int mg_ctx_create(int device, void* stream, mg_ctx** out) {
   e = cudaMalloc(&ctx->partials, sizeof(ReducePartials) * kMaxReduceBlocks);
   if (e == cudaSuccess) e = cudaMalloc(&ctx->counter, sizeof(unsigned int));
   if (e == cudaSuccess) e = cudaMalloc(&ctx->flag, sizeof(int));
+  if (e == cudaSuccess) e = cudaMalloc(&ctx->work, sizeof(unsigned int));
   // ordered on the context's stream (it may not synchronise with the legacy one)
   if (e == cudaSuccess) e = cudaMemsetAsync(ctx->counter, 0, sizeof(unsigned int), ctx->stream);
   if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
@@ -189,6 +190,8 @@ int mg_ctx_destroy(mg_ctx* ctx) {
   cudaFree(ctx->partials);
   cudaFree(ctx->counter);
   cudaFree(ctx->flag);
+  cudaFree(ctx->work);
+  cudaFree(ctx->scratch);
   if (ctx->owns_stream) cudaStreamDestroy(ctx->stream);
   delete ctx;
   return MG_OK;

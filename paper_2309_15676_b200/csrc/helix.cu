@@ -23,6 +23,12 @@
 #include "philox.cuh"
 
 namespace mg {
+// mg_set_option("helix_split", 0): the one-kernel sample pair instead of
+// the path / combine stages (defined in the fp64 translation unit)
+extern bool g_helix_split;
+#ifndef MG_HELIX_F32_TU
+bool g_helix_split = true;
+#endif
 namespace {
 
 constexpr int kHThreads = 128;
@@ -450,6 +456,157 @@ __global__ void __launch_bounds__(kHThreads)
                           [&](const ReducePartials& t) { *loss_out = t.ssn; });
 }
 
+// ------------------------------------------------ two-stage sample pair
+// The one-kernel form above gives each thread whole pixels (three paths,
+// ~1.15 pixels per resident thread at 65k pixels): the last wave is a
+// partial one, and the slowest threads trace six paths.  Here every PATH is
+// a work item (A, B, C of each pixel: 3 x pixels items, path-major so a
+// warp's items share their parameter-set count), fetched 32 at a time by
+// each warp from a counter; a path writes its radiance and derivatives
+// (both parameter sets, SoA [kHRes][items]) to a scratch buffer, and a
+// second kernel combines each pixel's three paths with exactly the
+// expressions of helix_pair_kernel (fixed-point sums: order-independent;
+// the loss in a fixed pixel order).
+constexpr int kHRes = 2 * (3 + 3 * kND);  // per path: [set][L c | dL c k]
+
+template <class T>
+__global__ void __launch_bounds__(kHThreads)
+    helix_path_kernel(HelixK q, const double* __restrict__ sph_g, const T* __restrict__ now,
+                      const T* __restrict__ prev, T* __restrict__ res, unsigned int* work) {
+  __shared__ T sph[4 * kMaxSph];
+  if (q.it_offset) q.iteration += __ldg(q.it_offset);
+  T th[2][kNP];
+  load_scene<T>(q, sph_g, now, prev, sph, th);
+  const int npt = (q.row1 - q.row0) * q.W;  // pixels of the tile
+  const int items = 3 * npt;
+  const int lane = threadIdx.x & 31;
+  for (;;) {
+    unsigned base = 0;
+    if (lane == 0) base = atomicAdd(work, 32u);
+    base = __shfl_sync(0xffffffffu, base, 0);
+    if (int(base) >= items) break;
+    const int j = int(base) + lane;
+    if (j >= items) continue;
+    const int k = j / npt, i = j - k * npt;  // k: 0 = A, 1 = B, 2 = C
+    const int pix = q.row0 * q.W + i;
+    const int px = pix % q.W, py = pix / q.W;
+    T L[2][3], dL[2][3][kND];
+    if (k == 1) {
+      T L1[1][3], d1[1][3][kND];
+      trace<T, 1>(q, sph, th, px, py, 1u, L1, d1);
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        L[0][c] = L1[0][c];
+        L[1][c] = T(0);
+#pragma unroll
+        for (int kk = 0; kk < kND; ++kk) {
+          dL[0][c][kk] = d1[0][c][kk];
+          dL[1][c][kk] = T(0);
+        }
+      }
+    } else {
+      trace<T, 2>(q, sph, th, px, py, k == 0 ? 0u : 2u, L, dL);
+    }
+#pragma unroll
+    for (int st = 0; st < 2; ++st)
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        res[size_t(st * 12 + c) * items + j] = L[st][c];
+#pragma unroll
+        for (int kk = 0; kk < kND; ++kk)
+          res[size_t(st * 12 + 3 + c * kND + kk) * items + j] = dL[st][c][kk];
+      }
+  }
+}
+
+template <class T>
+__global__ void __launch_bounds__(kHThreads)
+    helix_combine_kernel(HelixK q, const T* __restrict__ target, const T* __restrict__ res,
+                         unsigned long long* __restrict__ acc_g, ReducePartials* partials,
+                         unsigned int* counter, double* loss_out) {
+  __shared__ long long red[kHThreads / 32][2 * kNP];
+  const int npix = q.W * q.H;
+  const int npt = (q.row1 - q.row0) * q.W;
+  const int items = 3 * npt;
+  auto Lv = [&](int k, int i, int st, int c) { return res[size_t(st * 12 + c) * items + k * npt + i]; };
+  auto dv = [&](int k, int i, int st, int c, int kk) {
+    return res[size_t(st * 12 + 3 + c * kND + kk) * items + k * npt + i];
+  };
+  long long fp[kNP] = {0, 0, 0, 0, 0}, fd[kNP] = {0, 0, 0, 0, 0};
+  double loss = 0.0;
+  for (int i = blockIdx.x * kHThreads + threadIdx.x; i < npt; i += gridDim.x * kHThreads) {
+    const int pix = q.row0 * q.W + i;
+    double rA[3], rA1[3];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {  // helix_pair_kernel's expressions, same order
+      const double Is = double(target[size_t(c) * npix + pix]);
+      const double rB = double(Lv(1, i, 0, c)) - Is;
+      rA[c] = double(Lv(0, i, 0, c)) - Is;
+      rA1[c] = double(Lv(0, i, 1, c)) - Is;
+      loss += rA[c] * rB;
+#pragma unroll
+      for (int k = 0; k < kND; ++k) {
+        const int jj = k == 0 ? c : k + 2;
+        fp[jj] += fixh(rA[c] * double(dv(1, i, 0, c, k)));
+        fp[jj] += fixh(rB * double(dv(0, i, 0, c, k)));
+      }
+    }
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      const double Is = double(target[size_t(c) * npix + pix]);
+      const double rC = double(Lv(2, i, 0, c)) - Is, rC1 = double(Lv(2, i, 1, c)) - Is;
+#pragma unroll
+      for (int k = 0; k < kND; ++k) {
+        const int jj = k == 0 ? c : k + 2;
+        fd[jj] += fixh((rC * double(dv(0, i, 0, c, k)) + rA[c] * double(dv(2, i, 0, c, k))) -
+                       (rC1 * double(dv(0, i, 1, c, k)) + rA1[c] * double(dv(2, i, 1, c, k))));
+      }
+    }
+  }
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int j = 0; j < kNP; ++j) {
+    const long long a = warp_sum_ll(fp[j]), b = warp_sum_ll(fd[j]);
+    if (lane == 0) {
+      red[warp][j] = a;
+      red[warp][kNP + j] = b;
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x < 2 * kNP) {
+    long long s = 0;
+    for (int w = 0; w < kHThreads / 32; ++w) s += red[w][threadIdx.x];
+    if (s) atomicAdd(&acc_g[threadIdx.x], (unsigned long long)s);
+  }
+  Acc a;
+  a.ssn = loss;
+  grid_reduce4<kHThreads>(a.partials(), partials, counter,
+                          [&](const ReducePartials& t) { *loss_out = t.ssn; });
+}
+
+// Both stages on the context's stream; res = ctx scratch (kHRes x 3 x tile
+// pixels of T).  Returns false when the scratch cannot be had.
+template <class T>
+bool helix_pair_split(mg_ctx* ctx, const HelixK& q, const double* spheres, const T* now,
+                      const T* prev, const T* target_img, unsigned long long* accum,
+                      double* loss_out) {
+  const int npt = (q.row1 - q.row0) * q.W;
+  if (npt == 0) return false;
+  T* res = static_cast<T*>(ctx_scratch(ctx, sizeof(T) * size_t(kHRes) * 3 * size_t(npt)));
+  if (!res) return false;
+  cudaMemsetAsync(ctx->work, 0, sizeof(unsigned int), ctx->stream);
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, helix_path_kernel<T>, kHThreads, 0);
+  const int pgrid = ctx->sm_count * (per_sm > 0 ? per_sm : 1);
+  helix_path_kernel<T><<<pgrid, kHThreads, 0, ctx->stream>>>(q, spheres, now, prev, res,
+                                                              ctx->work);
+  const int cgrid = grid_for(ctx, npt, kHThreads, 8);
+  helix_combine_kernel<T><<<cgrid, kHThreads, 0, ctx->stream>>>(
+      q, target_img, res, accum, ctx->partials, ctx->counter, loss_out);
+  ctx->launches += 1;
+  return true;
+}
+
 template <class T>
 __global__ void helix_finalize_kernel(unsigned long long* __restrict__ acc, T* __restrict__ prop,
                                       T* __restrict__ diff) {
@@ -505,8 +662,10 @@ void helix_pair_f32(mg_ctx* ctx, int grid, const void* qp, const double* spheres
 #ifdef MG_HELIX_F32_TU
 {
   const HelixK& q = *static_cast<const HelixK*>(qp);
-  helix_pair_kernel<float><<<grid, kHThreads, 0, ctx->stream>>>(
-      q, spheres, now, prev, target_img, accum, ctx->partials, ctx->counter, loss_out);
+  if (!(g_helix_split &&
+        helix_pair_split<float>(ctx, q, spheres, now, prev, target_img, accum, loss_out)))
+    helix_pair_kernel<float><<<grid, kHThreads, 0, ctx->stream>>>(
+        q, spheres, now, prev, target_img, accum, ctx->partials, ctx->counter, loss_out);
   helix_finalize_kernel<float><<<1, 32, 0, ctx->stream>>>(accum, prop, diff);
 }
 #else
@@ -558,10 +717,13 @@ int mg_helix_sample_pair(mg_ctx* ctx, int32_t dtype, int32_t W, int32_t H, int32
   q.it_offset = ctx->it_offset;
   const int grid = grid_for(ctx, int64_t(W) * (row1 - row0) + 1, kHThreads, 8);
   if (dtype == MG_F64) {
-    helix_pair_kernel<double><<<grid, kHThreads, 0, ctx->stream>>>(
-        q, spheres, (const double*)now, (const double*)prev, (const double*)target_img,
-        (unsigned long long*)accum, ctx->partials,
-        ctx->counter, loss_out);
+    if (!(g_helix_split &&
+          helix_pair_split<double>(ctx, q, spheres, (const double*)now, (const double*)prev,
+                                   (const double*)target_img, (unsigned long long*)accum,
+                                   loss_out)))
+      helix_pair_kernel<double><<<grid, kHThreads, 0, ctx->stream>>>(
+          q, spheres, (const double*)now, (const double*)prev, (const double*)target_img,
+          (unsigned long long*)accum, ctx->partials, ctx->counter, loss_out);
     helix_finalize_kernel<double><<<1, 32, 0, ctx->stream>>>((unsigned long long*)accum,
                                                              (double*)prop, (double*)diff);
   } else if (dtype == MG_F32) {

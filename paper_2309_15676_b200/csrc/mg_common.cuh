@@ -95,6 +95,12 @@ struct mg_ctx {
   // device iteration offset (mg_ctx_set_iteration_offset): sample-pair
   // kernels launched on this context use iteration + *it_offset
   const uint32_t* it_offset = nullptr;
+  // work counter of dynamically scheduled kernels (zeroed before each use)
+  unsigned int* work = nullptr;
+  // grow-only scratch (mg::ctx_scratch); stream-ordered reuse by one call at
+  // a time, like the reduction workspace
+  void* scratch = nullptr;
+  size_t scratch_bytes = 0;
 };
 
 namespace mg {
@@ -220,6 +226,20 @@ __device__ __forceinline__ void grid_reduce4(ReducePartials acc, ReducePartials*
     fin(ReducePartials{r0, r1, r2, r3});
     *counter = 0u;
   }
+}
+
+// The context's scratch with at least `bytes` (grown with a synchronising
+// reallocation, so a size reached once is stable — e.g. across CUDA-graph
+// capture of a loop whose first step ran eagerly); nullptr on failure.
+inline void* ctx_scratch(mg_ctx* ctx, size_t bytes) {
+  if (bytes <= ctx->scratch_bytes) return ctx->scratch;
+  if (cudaStreamSynchronize(ctx->stream) != cudaSuccess) return nullptr;
+  cudaFree(ctx->scratch);
+  ctx->scratch = nullptr;
+  ctx->scratch_bytes = 0;
+  if (cudaMalloc(&ctx->scratch, bytes) != cudaSuccess) return nullptr;
+  ctx->scratch_bytes = bytes;
+  return ctx->scratch;
 }
 
 inline int grid_for(const mg_ctx* ctx, int64_t items, int threads, int blocks_per_sm) {

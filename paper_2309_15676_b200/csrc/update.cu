@@ -37,6 +37,7 @@ extern bool g_mesh_scatter_agg;
 extern bool g_mesh_bvh8;
 extern bool g_mesh_smem_stack;
 extern bool g_mesh_qnodes;
+extern bool g_helix_split;
 extern int g_bvh_leaf;
 // -1: per-dtype default measured on B200 (tools/sweep_update_variants.py,
 // profiles/r01_sweep_update_variants_*): fp32 -> variant 6 (2 CTAs/SM x 192
@@ -741,6 +742,10 @@ int mg_set_option(const char* name, int64_t value) {
   if (std::string(name) == "bvh_leaf_size") {
     if (value < 1 || value > 7) return fail(MG_EINVAL, "bvh_leaf_size must lie in [1, 7]");
     g_bvh_leaf = int(value);
+    return MG_OK;
+  }
+  if (std::string(name) == "helix_split") {
+    g_helix_split = value != 0;
     return MG_OK;
   }
   if (std::string(name) == "mesh_qnodes") {
