@@ -18,6 +18,9 @@
 // scalars (harness.cpp:204-244), not full vectors (O(iterations * dim)).
 #include <math.h>
 
+#include <map>
+#include <mutex>
+#include <tuple>
 #include <vector>
 
 #include "mg_common.cuh"
@@ -845,7 +848,28 @@ __global__ void __launch_bounds__(kThreads) run_cluster_kernel(RunK<T> k, double
 // one-CTA-per-replicate kernel (many replicates fill the GPU better that
 // way, or the pixels do not fit the consumers' registers).
 template <class T>
+int cluster_runner_size_query(mg_ctx* ctx, int d, int R);
+
+// memoised per (device, dtype, d, R): the occupancy query costs more than
+// an S1 run's iterations
+template <class T>
 int cluster_runner_size(mg_ctx* ctx, int d, int R) {
+  static std::mutex mu;
+  static std::map<std::tuple<int, int, int>, int> memo;
+  const auto key = std::make_tuple(ctx->device, d, R);
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    const auto it = memo.find(key);
+    if (it != memo.end()) return it->second;
+  }
+  const int nc = cluster_runner_size_query<T>(ctx, d, R);
+  std::lock_guard<std::mutex> lk(mu);
+  memo[key] = nc;
+  return nc;
+}
+
+template <class T>
+int cluster_runner_size_query(mg_ctx* ctx, int d, int R) {
   for (int nc : {16, 8}) {
     if (d > (nc - 1) * kThreads * kPPT) continue;
     if (int64_t(R) * nc > int64_t(ctx->sm_count)) continue;
@@ -916,6 +940,7 @@ int run_replicates(mg_ctx* ctx, const mg_experiment_config* cfg, int rep_begin, 
   std::vector<double> truth(d, 0.0), init(d, 0.0);
   int64_t D = 0;
   double* dexp = nullptr;
+  double* dtruth_dev = nullptr;  // mini-render: the generated target, already on the device
   cudaStream_t s = ctx->stream;
   std::vector<void*> allocs;
   auto dalloc = [&](size_t bytes) -> void* {
@@ -960,7 +985,12 @@ int run_replicates(mg_ctx* ctx, const mg_experiment_config* cfg, int rep_begin, 
         cleanup();
         return st;
       }
-      MG_CUDA_TRY(cudaMemcpy(truth.data(), dT, sizeof(double) * d, cudaMemcpyDeviceToHost));
+      // the device copy serves as the run's truth; the host needs it only
+      // for a scripted trajectory's schedule (no synchronous round trip)
+      if (cfg->trajectory != MG_TRAJ_OPTIMISE)
+        MG_CUDA_TRY(cudaMemcpy(truth.data(), dT, sizeof(double) * d, cudaMemcpyDeviceToHost));
+      else
+        dtruth_dev = dT;
       for (int j = 0; j < d; ++j) init[j] = cfg->albedo_init;
       D = int64_t(d) * cfg->spp;
     }
@@ -976,13 +1006,14 @@ int run_replicates(mg_ctx* ctx, const mg_experiment_config* cfg, int rep_begin, 
   k.rep_begin = rep_begin;
   k.R = R;
   k.exponents = dexp;
-  double* dtruth = (double*)dalloc(sizeof(double) * d);
+  double* dtruth = dtruth_dev ? dtruth_dev : (double*)dalloc(sizeof(double) * d);
   double* dinit = (double*)dalloc(sizeof(double) * d);
   if (!dtruth || !dinit) {
     cleanup();
     return fail(MG_ENOMEM, "run: allocation failed");
   }
-  cudaMemcpyAsync(dtruth, truth.data(), sizeof(double) * d, cudaMemcpyHostToDevice, s);
+  if (!dtruth_dev)
+    cudaMemcpyAsync(dtruth, truth.data(), sizeof(double) * d, cudaMemcpyHostToDevice, s);
   cudaMemcpyAsync(dinit, init.data(), sizeof(double) * d, cudaMemcpyHostToDevice, s);
   k.truth = dtruth;
   k.init = dinit;

@@ -295,10 +295,12 @@ def aggregate(cfg: ExperimentConfig, records: List[RunRecord]) -> AggregateRepor
     runs = np.array([r.iterations_run for r in records])
     mask = runs[:, None] > np.arange(it)[None, :]
     active = mask.sum(axis=0)
-    stats = {}
-    for n in names:
-        cols = np.stack([np.asarray(r.series[n], dtype=np.float64) for r in records])
-        stats[n] = SeriesStats(*_stats_columns(cols, mask))
+    # every (series, iteration) column of every series in one pass: [R][S*T]
+    S = len(names)
+    cols = np.stack([np.concatenate([np.asarray(r.series[n], dtype=np.float64) for n in names])
+                     for r in records]) if records else np.zeros((0, S * it))
+    st = _stats_columns(cols, np.tile(mask, (1, S)))
+    stats = {n: SeriesStats(*(q[k * it:(k + 1) * it] for q in st)) for k, n in enumerate(names)}
     div = sum(1 for r in records if r.status == "diverged")
     return AggregateReport(cfg, names, stats, active, div, records)
 
