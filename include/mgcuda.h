@@ -131,6 +131,11 @@ typedef struct mg_ctx mg_ctx;
 int mg_ctx_create(int device, void* stream, mg_ctx** out);
 int mg_ctx_destroy(mg_ctx* ctx);
 int mg_ctx_synchronize(mg_ctx* ctx);
+/* Probe (tools/s1_producer_probe.py): the cluster runner's mt19937_64
+ * producer alone, one CTA streaming `total` uniform() draws of
+ * Rng::stream(seed, rep) into out (device doubles); progress = device u64. */
+int mg_mt_stream_probe(mg_ctx* ctx, uint64_t seed, uint64_t rep, int64_t total, double* out,
+                       unsigned long long* progress);
 /* Device-check build (libmgcuda_debug.so, MG_DEBUG_CHECKS) only: trips one
  * device assert on purpose -> MG_ECUDA; release builds -> MG_EUNSUPPORTED. */
 int mg_debug_selftest(mg_ctx* ctx);

@@ -133,6 +133,7 @@ def load():
                                                        _vp]),
         "mg_fixed_finalize": (C.c_int, [_vp, C.c_int32, C.c_int64, _vp, _vp, _vp]),
         "mg_debug_selftest": (C.c_int, [_vp]),
+        "mg_mt_stream_probe": (C.c_int, [_vp, C.c_uint64, C.c_uint64, C.c_int64, _vp, _vp]),
         "mg_host_malloc": (C.c_int, [C.c_size_t, _vp]),
         "mg_host_free": (C.c_int, [_vp]),
         "mg_copy_async": (C.c_int, [_vp, _vp, _vp, C.c_size_t]),

@@ -483,18 +483,24 @@ constexpr int kChunkW = kMtM;                    // 156 words per chunk
 constexpr int kBatchChunks = 8;                  // chunks per emitted batch
 constexpr int kRingChunks = 2 * kBatchChunks;    // two batches in flight
 constexpr int kBatchWords = kBatchChunks * kChunkW;
-constexpr int kEmitThreads = kThreads - 32;
+constexpr int kPublishBatches = 4;
+#ifndef MG_PRODUCER_PROBE
+#define MG_PRODUCER_PROBE 0  // 1: emitters skip their work, 2: the twister skips (probes)
+#endif
 
 __device__ __forceinline__ void named_sync(int id, int n) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
 }
 
+template <int CT>
 __device__ void produce_stream(uint64_t* ring, uint64_t* pbar, uint64_t seed, uint64_t rep,
                                int64_t total, double* out, unsigned long long* progress) {
+  constexpr int kEmitThreads = CT - 32;
   uint64_t* full = pbar;       // [2]: batch written (count 1)
   uint64_t* empty = pbar + 2;  // [2]: batch emitted (count 1)
-  auto slot = [&](int64_t chunk) {
-    return ring + size_t(((chunk % kRingChunks) + kRingChunks) % kRingChunks) * kChunkW;
+  static_assert((kRingChunks & (kRingChunks - 1)) == 0, "power-of-two ring");
+  auto slot = [&](int64_t chunk) {  // two's complement: chunk -1 -> slot 15
+    return ring + (unsigned(chunk) & unsigned(kRingChunks - 1)) * kChunkW;
   };
   if (threadIdx.x == 0) {
     // Rng::stream(seed, rep) (rng.hpp:23-25): w[0..311] = chunks -2, -1
@@ -518,30 +524,51 @@ __device__ void produce_stream(uint64_t* ring, uint64_t* pbar, uint64_t seed, ui
   const int64_t chunks = (total + kChunkW - 1) / kChunkW;
   const int64_t batches = (chunks + kBatchChunks - 1) / kBatchChunks;
   if (threadIdx.x < 32) {  // twister warp
+    // Lane l owns the contiguous words t = 5l .. 5l+4 (t < 156; lane 31
+    // owns t = 155 only) of every chunk and keeps them for the last two
+    // chunks in registers.  Word t of chunk k needs words t of chunks k-1
+    // and k-2 and word t+1 of chunk k-2 — in-lane except for the last word
+    // of a lane (lane l+1's first word, shuffled from two chunks back, off
+    // the critical path) and t = 155 (word 0 of chunk k-1, one shuffle).
+    // No shared-memory round trip between chunks; each chunk is stored to
+    // the ring for the emitters.
     const int l = threadIdx.x;
+    const int t0 = 5 * l;
+    const int nw_l = l < 31 ? 5 : 1;  // words owned (lane 31: t = 155)
+    uint64_t v1[5], v2[5];            // chunks k-1, k-2
+#pragma unroll
+    for (int q = 0; q < 5; ++q) {
+      v2[q] = q < nw_l ? slot(-2)[t0 + q] : 0ull;
+      v1[q] = q < nw_l ? slot(-1)[t0 + q] : 0ull;
+    }
     for (int64_t b = 0; b < batches; ++b) {
       if (b >= 2) {  // the emitters are done with this half of the ring
         while (!try_wait_cluster(&empty[b & 1], uint32_t(((b - 2) >> 1) & 1))) {
         }
       }
-      for (int64_t kc = b * kBatchChunks; kc < (b + 1) * kBatchChunks; ++kc) {
-        const uint64_t* p1 = slot(kc - 1);
-        const uint64_t* p2 = slot(kc - 2);
-        uint64_t* nw = slot(kc);
-        uint64_t v[5];
+#if MG_PRODUCER_PROBE != 2
+      // unrolled: the two-chunk register rotation resolves at compile time
+      // (as a loop it cost ~20 moves per chunk)
+#pragma unroll
+      for (int kc = 0; kc < kBatchChunks; ++kc) {
+        uint64_t* nw = slot(b * kBatchChunks + kc);
+        // word t0 + 5 of chunk k-2 (lane l+1's first) and word 0 of chunk k-1
+        const uint64_t right = __shfl_down_sync(0xffffffffu, v2[0], 1);
+        const uint64_t head1 = __shfl_sync(0xffffffffu, v1[0], 0);
+        uint64_t v0[5];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) v0[q] = v1[q] ^ mt_mag(v2[q], v2[q + 1]);
+        v0[4] = v1[4] ^ mt_mag(v2[4], right);
+        if (l == 31) v0[0] = v1[0] ^ mt_mag(v2[0], head1);  // t = 155
 #pragma unroll
         for (int q = 0; q < 5; ++q) {
-          const int t = l + 32 * q;
-          if (t < kChunkW) {
-            const uint64_t nxt = t + 1 < kChunkW ? p2[t + 1] : p1[0];
-            v[q] = p1[t] ^ mt_mag(p2[t], nxt);
-          }
+          if (q < nw_l) nw[t0 + q] = v0[q];
+          v2[q] = v1[q];
+          v1[q] = v0[q];
         }
-#pragma unroll
-        for (int q = 0; q < 5; ++q)
-          if (l + 32 * q < kChunkW) nw[l + 32 * q] = v[q];
-        __syncwarp();
       }
+#endif
+      __syncwarp();  // the batch's stores precede lane 0's release
       if (l == 0)
         asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(
                          uint32_t(__cvta_generic_to_shared(&full[b & 1])))
@@ -554,44 +581,54 @@ __device__ void produce_stream(uint64_t* ring, uint64_t* pbar, uint64_t seed, ui
       }
       const int64_t base = b * kBatchWords;
       MG_DCHECK(b >= 0 && (base < total || total == 0));
+#if MG_PRODUCER_PROBE != 1
       for (int o = e; o < kBatchWords; o += kEmitThreads) {
         const int64_t g = base + o;
         if (g < total) out[g] = mt_uniform(mt_temper(slot(b * kBatchChunks + o / kChunkW)[o % kChunkW]));
       }
+#endif
       named_sync(1, kEmitThreads);
       if (e == 0) {
         asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(
                          uint32_t(__cvta_generic_to_shared(&empty[b & 1])))
                      : "memory");
-        __threadfence();
-        const int64_t done = base + kBatchWords < total ? base + kBatchWords : total;
-        asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(progress),
-                     "l"((unsigned long long)done)
-                     : "memory");
+        // publish every kPublishBatches batches (and the last): the release
+        // store orders the emitters' stores, which the named barrier made
+        // happen-before it; a fence per batch serialised the emitters
+        // (each batch waited for the previous publication's MEMBAR)
+        if ((b + 1) % kPublishBatches == 0 || b + 1 == batches) {
+          const int64_t done = base + kBatchWords < total ? base + kBatchWords : total;
+          asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(progress),
+                       "l"((unsigned long long)done)
+                       : "memory");
+        }
       }
     }
   }
 }
 
-template <class T>
-__global__ void __launch_bounds__(kThreads) run_cluster_kernel(RunK<T> k, double* ubuf_all,
+// CT threads per CTA, PPT pixels per consumer thread (registers)
+template <class T, int CT, int PPT>
+__global__ void __launch_bounds__(CT) run_cluster_kernel(RunK<T> k, double* ubuf_all,
                                                                unsigned long long* progress_all) {
   __shared__ uint64_t ring[kRingChunks * kChunkW];
   __shared__ __align__(8) uint64_t pbar[4];
-  __shared__ double sw[kThreads / 32];
+  __shared__ double sw[CT / 32];
   __shared__ double xch[2][kClusterMax][4];  // [parity][source rank][sum]
-  __shared__ double wsum[kThreads / 32][4];
+  __shared__ double wsum[CT / 32][4];
+  __shared__ unsigned long long s_seen;  // producer progress acquired so far
   __shared__ __align__(8) uint64_t xbar[2];
   __shared__ double tot[4];
   const mg_experiment_config& c = k.cfg;
   const uint32_t rank = cluster_rank(), NC = cluster_size(), M = NC - 1;
-  MG_DCHECK(NC >= 2 && NC <= uint32_t(kClusterMax) && blockDim.x == unsigned(kThreads));
+  MG_DCHECK(NC >= 2 && NC <= uint32_t(kClusterMax) && blockDim.x == unsigned(CT));
   const int r = blockIdx.x / NC;  // replicate within the launch
   const int d = k.dim, iters = c.iterations, spp = c.spp;
   const int64_t D = k.D;
   double* ubuf = ubuf_all + size_t(r) * iters * D;
   unsigned long long* progress = progress_all + r;
   if (threadIdx.x == 0) {
+    s_seen = 0;
     mbar_init_cta(&xbar[0], M);
     mbar_init_cta(&xbar[1], M);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -600,7 +637,7 @@ __global__ void __launch_bounds__(kThreads) run_cluster_kernel(RunK<T> k, double
   cluster_sync_all();  // every CTA of the cluster is running and initialised
 
   if (rank == 0) {  // ------------------------------------------ producer
-    produce_stream(ring, pbar, c.seed, uint64_t(k.rep_begin + r), int64_t(iters) * D, ubuf,
+    produce_stream<CT>(ring, pbar, c.seed, uint64_t(k.rep_begin + r), int64_t(iters) * D, ubuf,
                    progress);
     cluster_sync_all();
     return;
@@ -610,12 +647,12 @@ __global__ void __launch_bounds__(kThreads) run_cluster_kernel(RunK<T> k, double
   const int lo = int((int64_t(d) * me) / M), hi = int((int64_t(d) * (me + 1)) / M);
   const bool use_meta = c.optimizer == MG_OPT_META;
   const bool per_param = c.diff_norm == MG_DIFF_NORM_PER_PARAM;
-  T p[kPPT], pv[kPPT], m2p[kPPT], m2d[kPPT], mean[kPPT], var[kPPT], ap[kPPT];
-  double bj[kPPT], tj[kPPT];
-  bool own[kPPT];
+  T p[PPT], pv[PPT], m2p[PPT], m2d[PPT], mean[PPT], var[PPT], ap[PPT];
+  double bj[PPT], tj[PPT];
+  bool own[PPT];
 #pragma unroll
-  for (int q = 0; q < kPPT; ++q) {
-    const int j = lo + int(threadIdx.x) + q * kThreads;
+  for (int q = 0; q < PPT; ++q) {
+    const int j = lo + int(threadIdx.x) + q * CT;
     own[q] = j < hi;
     bj[q] = own[q] ? k.exponents[j] : 0.0;
     tj[q] = own[q] ? k.truth[j] : 0.0;
@@ -641,7 +678,7 @@ __global__ void __launch_bounds__(kThreads) run_cluster_kernel(RunK<T> k, double
     if (warp == 0) {
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
-        double x = lane < kThreads / 32 ? wsum[lane][q] : 0.0;
+        double x = lane < CT / 32 ? wsum[lane][q] : 0.0;
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) x += __shfl_down_sync(0xffffffffu, x, o);
         v[q] = __shfl_sync(0xffffffffu, x, 0);
@@ -673,7 +710,7 @@ __global__ void __launch_bounds__(kThreads) run_cluster_kernel(RunK<T> k, double
   {
     double l = 0.0, nf = 0.0;
 #pragma unroll
-    for (int q = 0; q < kPPT; ++q)
+    for (int q = 0; q < PPT; ++q)
       if (own[q]) {
         const double e = double(p[q]) - tj[q];
         l += e * e;
@@ -696,14 +733,22 @@ __global__ void __launch_bounds__(kThreads) run_cluster_kernel(RunK<T> k, double
     }
     const bool same = use_meta ? same_pp : true;
     loss_rec = loss;
-    if (threadIdx.x == 0) {  // this iteration's uniforms are drawn
+    {  // this iteration's uniforms are drawn: poll only when the progress
+       // seen so far (acquired, then published by a barrier) falls short —
+       // the producer runs ahead, so after the first iterations never
       const unsigned long long need = (unsigned long long)(i + 1) * (unsigned long long)D;
-      unsigned long long v;
-      do {
-        asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(progress) : "memory");
-      } while (v < need);
+      if (s_seen < need) {  // uniform: s_seen changes only before a barrier
+        __syncthreads();
+        if (threadIdx.x == 0) {
+          unsigned long long v;
+          do {
+            asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(progress) : "memory");
+          } while (v < need);
+          s_seen = v;
+        }
+        __syncthreads();
+      }
     }
-    __syncthreads();
     const double* u = ubuf + size_t(i) * D;
     const bool two_point = use_meta && !same_pp;  // :129
     draws += D;
@@ -732,9 +777,9 @@ __global__ void __launch_bounds__(kThreads) run_cluster_kernel(RunK<T> k, double
     }
     double a_ssn = 0.0, a_loss = 0.0, a_nf = 0.0, a_ne = 0.0;
 #pragma unroll
-    for (int q = 0; q < kPPT; ++q) {
+    for (int q = 0; q < PPT; ++q) {
       if (!own[q]) continue;
-      const int j = lo + int(threadIdx.x) + q * kThreads;
+      const int j = lo + int(threadIdx.x) + q * CT;
       MG_DCHECK(j < hi && hi <= d);
       // sample_pair (problems.cpp:197-217)
       T cross, mb;
@@ -825,8 +870,8 @@ __global__ void __launch_bounds__(kThreads) run_cluster_kernel(RunK<T> k, double
   // 182-188); converged status (harness.cpp:191-198) on their loss
   if (k.final_params)
 #pragma unroll
-    for (int q = 0; q < kPPT; ++q) {
-      const int j = lo + int(threadIdx.x) + q * kThreads;
+    for (int q = 0; q < PPT; ++q) {
+      const int j = lo + int(threadIdx.x) + q * CT;
       if (own[q]) k.final_params[size_t(r) * d + j] = double(pv[q]);
     }
   if (me == 0 && threadIdx.x == 0) {
@@ -843,59 +888,79 @@ __global__ void __launch_bounds__(kThreads) run_cluster_kernel(RunK<T> k, double
   cluster_sync_all();
 }
 
-// Cluster size for the one-replicate-per-cluster runner: 16 CTAs (15
-// consumers) when the device can co-schedule them, else 8; 0 = use the
-// one-CTA-per-replicate kernel (many replicates fill the GPU better that
-// way, or the pixels do not fit the consumers' registers).
-template <class T>
-int cluster_runner_size_query(mg_ctx* ctx, int d, int R);
+// The producer alone (probe for tools/s1_producer_probe.py): one CTA of CT
+// threads streams `total` uniforms of Rng::stream(seed, rep) into out.
+template <int CT>
+__global__ void __launch_bounds__(CT) mt_stream_probe_kernel(uint64_t seed, uint64_t rep,
+                                                             int64_t total, double* out,
+                                                             unsigned long long* progress) {
+  __shared__ uint64_t ring[kRingChunks * kChunkW];
+  __shared__ __align__(8) uint64_t pbar[4];
+  produce_stream<CT>(ring, pbar, seed, rep, total, out, progress);
+}
 
-// memoised per (device, dtype, d, R): the occupancy query costs more than
-// an S1 run's iterations
+// Shape of the one-replicate-per-cluster runner: cluster size (16 CTAs, 15
+// consumers, when the device can co-schedule them, else 8) and CTA shape
+// (512 threads x 2 pixels when the pixels fit: one pixel per thread at S1,
+// else 256 x 4); nc = 0: use the one-CTA-per-replicate kernel (many
+// replicates fill the GPU better that way, or the pixels do not fit the
+// consumers' registers).
+struct ClusterShape {
+  int nc = 0, threads = 0;
+};
+
+template <class T, int CT, int PPT>
+int cluster_query(mg_ctx* ctx, int nc, int R) {
+  auto kernel = run_cluster_kernel<T, CT, PPT>;
+  if (nc > 8 &&
+      cudaFuncSetAttribute(kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  cudaLaunchConfig_t lc = {};
+  lc.gridDim = dim3(unsigned(R * nc));
+  lc.blockDim = dim3(CT);
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = unsigned(nc);
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  lc.attrs = at;
+  lc.numAttrs = 1;
+  int clusters = 0;
+  if (cudaOccupancyMaxActiveClusters(&clusters, kernel, &lc) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return clusters;
+}
+
 template <class T>
-int cluster_runner_size(mg_ctx* ctx, int d, int R) {
+ClusterShape cluster_shape_query(mg_ctx* ctx, int d, int R) {
+  for (int nc : {16, 8}) {
+    if (int64_t(R) * nc > int64_t(ctx->sm_count)) continue;
+    if (d <= (nc - 1) * 512 * 2 && cluster_query<T, 512, 2>(ctx, nc, R) >= R) return {nc, 512};
+    if (d <= (nc - 1) * 256 * 4 && cluster_query<T, 256, 4>(ctx, nc, R) >= R) return {nc, 256};
+  }
+  return {};
+}
+
+// memoised per (device, d, R): the occupancy queries cost more than an S1
+// run's iterations
+template <class T>
+ClusterShape cluster_shape(mg_ctx* ctx, int d, int R) {
   static std::mutex mu;
-  static std::map<std::tuple<int, int, int>, int> memo;
+  static std::map<std::tuple<int, int, int>, ClusterShape> memo;
   const auto key = std::make_tuple(ctx->device, d, R);
   {
     std::lock_guard<std::mutex> lk(mu);
     const auto it = memo.find(key);
     if (it != memo.end()) return it->second;
   }
-  const int nc = cluster_runner_size_query<T>(ctx, d, R);
+  const ClusterShape cs = cluster_shape_query<T>(ctx, d, R);
   std::lock_guard<std::mutex> lk(mu);
-  memo[key] = nc;
-  return nc;
-}
-
-template <class T>
-int cluster_runner_size_query(mg_ctx* ctx, int d, int R) {
-  for (int nc : {16, 8}) {
-    if (d > (nc - 1) * kThreads * kPPT) continue;
-    if (int64_t(R) * nc > int64_t(ctx->sm_count)) continue;
-    if (nc > 8 && cudaFuncSetAttribute(run_cluster_kernel<T>,
-                                       cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess) {
-      cudaGetLastError();
-      continue;
-    }
-    cudaLaunchConfig_t lc = {};
-    lc.gridDim = dim3(unsigned(R * nc));
-    lc.blockDim = dim3(kThreads);
-    cudaLaunchAttribute at[1];
-    at[0].id = cudaLaunchAttributeClusterDimension;
-    at[0].val.clusterDim.x = unsigned(nc);
-    at[0].val.clusterDim.y = 1;
-    at[0].val.clusterDim.z = 1;
-    lc.attrs = at;
-    lc.numAttrs = 1;
-    int clusters = 0;
-    if (cudaOccupancyMaxActiveClusters(&clusters, run_cluster_kernel<T>, &lc) != cudaSuccess) {
-      cudaGetLastError();
-      continue;
-    }
-    if (clusters >= R) return nc;  // every replicate's cluster co-resident
-  }
-  return 0;
+  memo[key] = cs;
+  return cs;
 }
 
 // ------------------------------------------------------------- host side
@@ -1088,12 +1153,12 @@ int run_replicates(mg_ctx* ctx, const mg_experiment_config* cfg, int rep_begin, 
     cudaMemsetAsync(k.full, 0xff, full_bytes, s);  // NaN past iterations_run
   }
   // few replicates of a mini-render run: one cluster per replicate
-  int nc = 0;
+  ClusterShape cs;
   if (g_cluster_runner && cfg->problem == MG_MINI_RENDER && cfg->trajectory == MG_TRAJ_OPTIMISE &&
       !cfg->independent_variance_samples && !full &&
       sizeof(double) * size_t(R) * iters * D <= (size_t(1) << 30))
-    nc = cluster_runner_size<T>(ctx, d, R);
-  if (nc > 0) {
+    cs = cluster_shape<T>(ctx, d, R);
+  if (cs.nc > 0) {
     double* ubuf = (double*)dalloc(sizeof(double) * size_t(R) * iters * D);
     auto* progress = (unsigned long long*)dalloc(sizeof(unsigned long long) * size_t(R));
     if (!ubuf || !progress) {
@@ -1102,17 +1167,19 @@ int run_replicates(mg_ctx* ctx, const mg_experiment_config* cfg, int rep_begin, 
     }
     cudaMemsetAsync(progress, 0, sizeof(unsigned long long) * size_t(R), s);
     cudaLaunchConfig_t lc = {};
-    lc.gridDim = dim3(unsigned(R * nc));
-    lc.blockDim = dim3(kThreads);
+    lc.gridDim = dim3(unsigned(R * cs.nc));
+    lc.blockDim = dim3(unsigned(cs.threads));
     lc.stream = s;
     cudaLaunchAttribute at[1];
     at[0].id = cudaLaunchAttributeClusterDimension;
-    at[0].val.clusterDim.x = unsigned(nc);
+    at[0].val.clusterDim.x = unsigned(cs.nc);
     at[0].val.clusterDim.y = 1;
     at[0].val.clusterDim.z = 1;
     lc.attrs = at;
     lc.numAttrs = 1;
-    cudaError_t le = cudaLaunchKernelEx(&lc, run_cluster_kernel<T>, k, ubuf, progress);
+    cudaError_t le = cs.threads == 512
+                         ? cudaLaunchKernelEx(&lc, run_cluster_kernel<T, 512, 2>, k, ubuf, progress)
+                         : cudaLaunchKernelEx(&lc, run_cluster_kernel<T, 256, 4>, k, ubuf, progress);
     if (le != cudaSuccess) {
       cleanup();
       return cuda_fail(le, "run_cluster_kernel");
@@ -1157,6 +1224,14 @@ int run_replicates(mg_ctx* ctx, const mg_experiment_config* cfg, int rep_begin, 
 }  // namespace mg
 
 using namespace mg;
+
+extern "C" int mg_mt_stream_probe(mg_ctx* ctx, uint64_t seed, uint64_t rep, int64_t total,
+                                  double* out, unsigned long long* progress) {
+  if (!ctx || !out || !progress || total < 1) return fail(MG_EINVAL, "mg_mt_stream_probe: bad arguments");
+  mt_stream_probe_kernel<512><<<1, 512, 0, ctx->stream>>>(seed, rep, total, out, progress);
+  MG_LAUNCH_CHECK(ctx);
+  return MG_OK;
+}
 
 extern "C" int mg_run_replicates_full(mg_ctx* ctx, const mg_experiment_config* cfg,
                                       int32_t rep_begin, int32_t rep_count,

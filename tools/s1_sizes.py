@@ -1,0 +1,7 @@
+import sys
+sys.path.insert(0, ".")
+from paper_2309_15676_b200 import api
+for P in (512, 1024, 4096, 8192):
+    S1 = dict(problem="mini-render", pixel_count=P, spp=2, iterations=200, lr=0.01, seed=0, problem_seed=1)
+    for _ in range(2):
+        api.run_experiment(api.ExperimentConfig(**S1, replicates=1))
