@@ -174,12 +174,13 @@ template <class T>
 int launch(mg_ctx* ctx, int64_t P, const RenderK& k, bool first, const void* b, const void* t,
            const double* u, const void* pnow, void* pprev, void* m2p, void* m2d, void* mean,
            void* var, void* ap, void* prop_out, void* diff_out, mg_update_scalars* sc) {
-  // fp32 Philox, no per-pixel outputs, large P: the TMA-fed fast kernel
-  // (render_fast.cu)
-  if (sizeof(T) == 4 && g_render_fast && k.philox && k.record < 0 && !prop_out && !diff_out) {
+  // fp32, no per-pixel outputs, large P: the TMA-fed fast kernel
+  // (render_fast.cu; Philox, or the exact mt64 draws as a tenth stream)
+  if (sizeof(T) == 4 && g_render_fast && k.record < 0 && !prop_out && !diff_out) {
     const int rc = launch_minirender_fast(ctx, P, k, first, (const float*)b, (const float*)t,
                                           (const float*)pnow, (float*)pprev, (float*)m2p,
-                                          (float*)m2d, (float*)mean, (float*)var, (float*)ap, sc);
+                                          (float*)m2d, (float*)mean, (float*)var, (float*)ap, sc,
+                                          u);
     if (rc != MG_EUNSUPPORTED) return rc;
   }
   // fp32: 4 pixels per thread (16-byte packs, ILP across 4 Philox/pow

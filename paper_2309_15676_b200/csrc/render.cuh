@@ -21,11 +21,14 @@ struct RenderK {
 extern bool g_render_fast;
 extern int g_render_fast_variant;
 
-// fp32, Philox draws, no per-pixel outputs.  Returns MG_EUNSUPPORTED when
+// fp32, no per-pixel outputs (Philox draws, or the mt64 draws streamed).  Returns MG_EUNSUPPORTED when
 // the launch does not fit the fast kernel (spp > 4, unaligned views, P below
 // one tile per SM); the caller then runs the IEEE kernel.
+// uniforms: the pre-drawn mt19937_64 draws (mt64 mode, pixel-major, 16-byte
+// aligned), ignored in Philox mode.
 int launch_minirender_fast(mg_ctx* ctx, int64_t P, const RenderK& k, bool first, const float* b,
                            const float* tgt, const float* pnow, float* pprev_next, float* m2p,
-                           float* m2d, float* mean, float* var, float* ap, mg_update_scalars* sc);
+                           float* m2d, float* mean, float* var, float* ap, mg_update_scalars* sc,
+                           const double* uniforms);
 
 }  // namespace mg

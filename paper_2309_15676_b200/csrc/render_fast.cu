@@ -44,13 +44,18 @@ __host__ __device__ constexpr FastVariant fast_variant(int i) {
        : i == 7 ? FastVariant{192, 4, 2, 32}
        : i == 8 ? FastVariant{256, 3, 2, 32}
        : i == 9 ? FastVariant{128, 2, 6, 32}
-                : FastVariant{256, 2, 3, 32};
+       : i == 10 ? FastVariant{256, 2, 3, 32}
+       : i == 11 ? FastVariant{128, 3, 2, 32}
+                 : FastVariant{192, 2, 2, 192};
 }
-constexpr int kNumFastVariants = 11;
+constexpr int kNumFastVariants = 13;
 // interleaved sweep at 16.7M pixels (tools/render_fast_sweep.py): spp 2 ->
 // per-warp rings (variant 5: 0.172 ms, 0.89 of HBM); spp >= 3 (more
 // arithmetic per byte) -> one ring per 192-thread CTA (variant 3)
 constexpr int default_fast_variant(int spp) { return spp == 2 ? 5 : 3; }
+// the exact-stream form moves SPP doubles more per pixel: two 192-thread
+// stages (ncu, 16.7M px: 0.197 ms spp 2 / 0.218 ms spp 3 vs IEEE 0.276 / 0.297)
+constexpr int default_fast_variant_mt(int) { return 12; }
 
 __device__ __forceinline__ float fdiv(float a, float b) {
   float r;
@@ -180,7 +185,17 @@ struct PixAcc {  // per-thread partial sums of one tile (fp32), folded into Acc
 // UNIT = THREADS: one ring per CTA (thread 0 issues, __syncthreads between
 // consume and refill).  UNIT = 32: one ring per warp (lane 0 issues,
 // __syncwarp), so no warp ever waits for another CTA-mate.
-template <bool FIRST, int SPP, int THREADS, int STAGES, int CTAS, int UNIT>
+// Per-stage shared bytes of one ring: the nine fp32 arrays, and with MT the
+// tile's SPP pre-drawn doubles per pixel (the reference's mt19937_64 stream)
+template <int TILE, int SPP, bool MT>
+__host__ __device__ constexpr int stage_bytes() {
+  return kArrays * TILE * int(sizeof(float)) + (MT ? TILE * SPP * int(sizeof(double)) : 0);
+}
+
+// MT: the draws are the replicate's exact std::mt19937_64 stream, pre-drawn
+// pixel-major (problems.cpp:201-202) and streamed as a tenth TMA array;
+// otherwise Philox in registers.
+template <bool FIRST, int SPP, int THREADS, int STAGES, int CTAS, int UNIT, bool MT = false>
 __global__ void __launch_bounds__(THREADS, CTAS)
     minirender_fast_kernel(int64_t P, RenderK k, const float* __restrict__ b,
                            const float* __restrict__ tgt, const float* __restrict__ pnow,
@@ -188,16 +203,21 @@ __global__ void __launch_bounds__(THREADS, CTAS)
                            float* __restrict__ m2d, float* __restrict__ mean,
                            float* __restrict__ var, float* __restrict__ ap,
                            mg_update_scalars* sc, ReducePartials* partials,
-                           unsigned int* counter) {
+                           unsigned int* counter, const double* __restrict__ uni) {
   static_assert(UNIT == THREADS || UNIT == 32, "one ring per CTA or per warp");
   constexpr int UNITS = THREADS / UNIT;  // rings per CTA
   extern __shared__ __align__(128) unsigned char smem_raw[];
   __shared__ __align__(8) uint64_t full_all[UNITS * STAGES];
   constexpr int W = 4;
   constexpr int TILE = UNIT * W;
+  constexpr int SB = stage_bytes<TILE, SPP, MT>();
   const int unit = threadIdx.x / UNIT, r = threadIdx.x % UNIT;
   uint64_t* full = full_all + unit * STAGES;
-  float* sbuf = reinterpret_cast<float*>(smem_raw) + size_t(unit) * STAGES * kArrays * TILE;
+  unsigned char* ubase = smem_raw + size_t(unit) * STAGES * SB;
+  auto stage_f = [&](int st) { return reinterpret_cast<float*>(ubase + size_t(st) * SB); };
+  auto stage_u = [&](int st) {
+    return reinterpret_cast<double*>(ubase + size_t(st) * SB + kArrays * TILE * sizeof(float));
+  };
   auto unit_sync = [] {
     if constexpr (UNIT == 32) __syncwarp(); else __syncthreads();
   };
@@ -222,6 +242,7 @@ __global__ void __launch_bounds__(THREADS, CTAS)
   uint32_t tx = 0;
 #pragma unroll
   for (int a = 0; a < kArrays; ++a) tx += use[a] ? uint32_t(TILE * sizeof(float)) : 0u;
+  if (MT) tx += uint32_t(TILE * SPP * sizeof(double));
 
   const int64_t tiles = P / TILE;
   const int64_t gunit = int64_t(blockIdx.x) * UNITS + unit, nunits = int64_t(gridDim.x) * UNITS;
@@ -240,8 +261,11 @@ __global__ void __launch_bounds__(THREADS, CTAS)
 #pragma unroll
     for (int a = 0; a < kArrays; ++a)
       if (use[a])
-        bulk_g2s_hint(sbuf + (size_t(st) * kArrays + a) * TILE, src[a] + tile * TILE,
+        bulk_g2s_hint(stage_f(st) + a * TILE, src[a] + tile * TILE,
                       uint32_t(TILE * sizeof(float)), &full[st], pol);
+    if (MT)
+      bulk_g2s_hint(stage_u(st), uni + tile * TILE * SPP, uint32_t(TILE * SPP * sizeof(double)),
+                    &full[st], pol);
   };
   if (r == 0)
     for (int64_t li = 0; li < my_tiles && li < STAGES; ++li) issue(li);
@@ -251,13 +275,22 @@ __global__ void __launch_bounds__(THREADS, CTAS)
   for (int64_t li = 0; li < my_tiles; ++li) {
     const int st = int(li % STAGES);
     const int64_t base = (gunit + li * nunits) * TILE + e;
-    // the draws do not depend on the tile's data: form them before waiting
+    // Philox draws do not depend on the tile's data: form them before waiting
     float u[W][SPP];
+    if constexpr (!MT) {
 #pragma unroll
-    for (int w = 0; w < W; ++w)
-      fast_uniforms<SPP>(k, uint32_t(base + w) + k.pixel_offset, u[w]);
+      for (int w = 0; w < W; ++w)
+        fast_uniforms<SPP>(k, uint32_t(base + w) + k.pixel_offset, u[w]);
+    }
     mbar_wait(&full[st], uint32_t((li / STAGES) & 1));
-    const float* sb = sbuf + size_t(st) * kArrays * TILE + e;
+    if constexpr (MT) {  // float(u) of the drawn doubles, as the IEEE kernel rounds them
+      const double* su = stage_u(st) + e * SPP;
+#pragma unroll
+      for (int w = 0; w < W; ++w)
+#pragma unroll
+        for (int q = 0; q < SPP; ++q) u[w][q] = float(su[w * SPP + q]);
+    }
+    const float* sb = stage_f(st) + e;
     const Pack<float> B = ld_plain(sb + 0 * TILE), TG = ld_plain(sb + 1 * TILE);
     const Pack<float> A = ld_plain(sb + 2 * TILE), AQ = ld_plain(sb + 3 * TILE);
     Pack<float> M2P{}, M2D{}, ME{}, VA{}, AL{}, PO;
@@ -292,7 +325,12 @@ __global__ void __launch_bounds__(THREADS, CTAS)
   const int64_t tid = int64_t(blockIdx.x) * THREADS + threadIdx.x;
   for (int64_t j = tiles * TILE + tid; j < P; j += int64_t(gridDim.x) * THREADS) {
     float u[SPP];
-    fast_uniforms<SPP>(k, uint32_t(j) + k.pixel_offset, u);
+    if constexpr (MT) {
+#pragma unroll
+      for (int q = 0; q < SPP; ++q) u[q] = float(uni[j * SPP + q]);
+    } else {
+      fast_uniforms<SPP>(k, uint32_t(j) + k.pixel_offset, u);
+    }
     float M2P = FIRST ? 0.f : m2p[j];
     float M2D = f.has_m2d ? m2d[j] : 0.f;
     float ME = FIRST ? 0.f : mean[j];
@@ -323,21 +361,26 @@ __global__ void __launch_bounds__(THREADS, CTAS)
   });
 }
 
-template <int V, bool FIRST, int SPP>
+template <int V, bool FIRST, int SPP, bool MT>
 int run_fast(mg_ctx* ctx, int64_t P, const RenderK& k, const float* b, const float* t,
              const float* pnow, float* pprev, float* m2p, float* m2d, float* mean, float* var,
-             float* ap, mg_update_scalars* sc) {
+             float* ap, mg_update_scalars* sc, const double* uni) {
   constexpr FastVariant v = fast_variant(V);
   constexpr int TILE = v.threads * 4;  // pixels per CTA per stage
-  constexpr size_t smem = size_t(v.stages) * kArrays * TILE * sizeof(float);
-  auto kernel = minirender_fast_kernel<FIRST, SPP, v.threads, v.stages, v.ctas_per_sm, v.unit>;
+  constexpr size_t smem = size_t(v.stages) * (v.threads / v.unit) *
+                          stage_bytes<v.unit * 4, SPP, MT>();
+  auto kernel =
+      minirender_fast_kernel<FIRST, SPP, v.threads, v.stages, v.ctas_per_sm, v.unit, MT>;
+  if (smem > size_t(227) * 1024) return MG_EUNSUPPORTED;
   cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
   const int64_t tiles = P / TILE;
-  const int64_t want = int64_t(ctx->sm_count) * v.ctas_per_sm;
+  const int fit = int(size_t(227) * 1024 / (smem + 1024));  // CTAs per SM by shared memory
+  const int per_sm = v.ctas_per_sm < fit ? v.ctas_per_sm : (fit > 0 ? fit : 1);
+  const int64_t want = int64_t(ctx->sm_count) * per_sm;
   int grid = int(tiles < want ? tiles : want);
   if (grid > kMaxReduceBlocks) grid = kMaxReduceBlocks;
   kernel<<<grid, v.threads, smem, ctx->stream>>>(P, k, b, t, pnow, pprev, m2p, m2d, mean, var,
-                                                 ap, sc, ctx->partials, ctx->counter);
+                                                 ap, sc, ctx->partials, ctx->counter, uni);
   MG_LAUNCH_CHECK(ctx);
   return MG_OK;
 }
@@ -345,13 +388,18 @@ int run_fast(mg_ctx* ctx, int64_t P, const RenderK& k, const float* b, const flo
 template <int V>
 int pick_spp(mg_ctx* ctx, int64_t P, const RenderK& k, bool first, const float* b,
              const float* t, const float* pnow, float* pprev, float* m2p, float* m2d,
-             float* mean, float* var, float* ap, mg_update_scalars* sc) {
-#define MG_FAST_CASE(S)                                                                       \
-  case S:                                                                                     \
-    return first ? run_fast<V, true, S>(ctx, P, k, b, t, pnow, pprev, m2p, m2d, mean, var, ap, \
-                                        sc)                                                   \
-                 : run_fast<V, false, S>(ctx, P, k, b, t, pnow, pprev, m2p, m2d, mean, var,   \
-                                         ap, sc);
+             float* mean, float* var, float* ap, mg_update_scalars* sc, const double* uni) {
+#define MG_FAST_CASE(S)                                                                        \
+  case S:                                                                                      \
+    if (uni)                                                                                   \
+      return first ? run_fast<V, true, S, true>(ctx, P, k, b, t, pnow, pprev, m2p, m2d, mean,  \
+                                                var, ap, sc, uni)                              \
+                   : run_fast<V, false, S, true>(ctx, P, k, b, t, pnow, pprev, m2p, m2d, mean, \
+                                                 var, ap, sc, uni);                            \
+    return first ? run_fast<V, true, S, false>(ctx, P, k, b, t, pnow, pprev, m2p, m2d, mean,   \
+                                               var, ap, sc, nullptr)                           \
+                 : run_fast<V, false, S, false>(ctx, P, k, b, t, pnow, pprev, m2p, m2d, mean,  \
+                                                var, ap, sc, nullptr);
   switch (k.spp) {
     MG_FAST_CASE(2)
     MG_FAST_CASE(3)
@@ -369,19 +417,24 @@ int render_fast_variants() { return kNumFastVariants; }
 int launch_minirender_fast(mg_ctx* ctx, int64_t P, const RenderK& k, bool first, const float* b,
                            const float* tgt, const float* pnow, float* pprev_next, float* m2p,
                            float* m2d, float* mean, float* var, float* ap,
-                           mg_update_scalars* sc) {
+                           mg_update_scalars* sc, const double* uniforms) {
   if (k.spp < 2 || k.spp > 4) return MG_EUNSUPPORTED;
+  const double* uni = k.philox ? nullptr : uniforms;
+  if (!k.philox && !(uniforms && aligned16(uniforms))) return MG_EUNSUPPORTED;
   if (!(aligned16(b) && aligned16(tgt) && aligned16(pnow) && aligned16(pprev_next) &&
         aligned16(m2p) && aligned16(m2d) && aligned16(mean) && aligned16(var) && aligned16(ap)))
     return MG_EUNSUPPORTED;
-  const int v = g_render_fast_variant >= 0 ? g_render_fast_variant : default_fast_variant(k.spp);
+  const int v = g_render_fast_variant >= 0 ? g_render_fast_variant
+                                          : (uni ? default_fast_variant_mt(k.spp)
+                                                 : default_fast_variant(k.spp));
   // at least one full 256x4 tile per SM, else the IEEE kernel
   if (P < int64_t(1024) * ctx->sm_count) return MG_EUNSUPPORTED;
   switch (v) {
 #define MG_FAST_V(V) \
-  case V: return pick_spp<V>(ctx, P, k, first, b, tgt, pnow, pprev_next, m2p, m2d, mean, var, ap, sc);
+  case V: return pick_spp<V>(ctx, P, k, first, b, tgt, pnow, pprev_next, m2p, m2d, mean, var, ap, sc, uni);
     MG_FAST_V(0) MG_FAST_V(1) MG_FAST_V(2) MG_FAST_V(3) MG_FAST_V(4)
     MG_FAST_V(5) MG_FAST_V(6) MG_FAST_V(7) MG_FAST_V(8) MG_FAST_V(9) MG_FAST_V(10)
+    MG_FAST_V(11) MG_FAST_V(12)
 #undef MG_FAST_V
     default: return MG_EINVAL;
   }

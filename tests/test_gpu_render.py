@@ -154,19 +154,21 @@ def test_scaled_run_single_matches_reference_series(api, oracle, dt, rtol):
                                    err_msg=name)
 
 
+@pytest.mark.parametrize("rng", ["philox", "mt64"])
 @pytest.mark.parametrize("spp", [2, 3, 4])
-def test_fast_f32_kernel_tracks_fp64_run(api, spp):
+def test_fast_f32_kernel_tracks_fp64_run(api, spp, rng):
     """The TMA-fed fp32 fast kernel (render_fast.cu: FMA, approximate
     divide/sqrt/rcp, fp32 per-thread partial sums) at a size that runs it
     (>= one 1024-pixel tile per SM, ring wrapping, plus a ragged tail) stays
-    within the fp32 bar of the fp64 run on the same Philox draws — whose
-    pair math is pinned to the oracle above — over 12 iterations, and within
+    within the fp32 bar of the fp64 run on the same draws — Philox, or the
+    exact mt19937_64 stream streamed in as a tenth TMA array; both pair
+    maths are pinned to the oracle above — over 12 iterations, and within
     1e-5 of the IEEE fp32 kernel."""
     from paper_2309_15676_b200 import _lib
     L = _lib.load()
     sms = torch.cuda.get_device_properties(0).multi_processor_count
     P = 1024 * sms * 9 + 333
-    kw = dict(gen_seed=3, lr=0.02, seed=5, replicate=0, rng="philox")
+    kw = dict(gen_seed=3, lr=0.02, seed=5, replicate=0, rng=rng)
     runs = {"f64": api.MiniRenderRun(P, spp, dtype=torch.float64, **kw),
             "fast": api.MiniRenderRun(P, spp, dtype=torch.float32, **kw)}
     L.mg_set_option(b"render_fast", 0)
