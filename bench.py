@@ -752,6 +752,8 @@ def extras(args, ctx):
                 walls.append(time.time() - t0)
             wall = statistics.median(walls)
             out[key] = {"replicates": reps, "iterations": 200, "wall_s": wall,
+                        "wall_min_s": min(walls),
+                        "walls_ms": [round(x * 1e3, 3) for x in walls],
                         "pairs_per_s": reps * 200 * 4096 * 2 / wall,
                         "runner": "cluster" if reps == 1 else "one CTA per replicate"}
 

@@ -120,6 +120,9 @@ int mg_abi_version(void);
  *                              slower at configs[3]/[4]; off by default)
  *   "helix_split" = 0          configs[2] sample pair in one kernel (whole
  *                              pixels per thread) instead of path / combine
+ *   "pool_keep_bytes" = n      bytes the default stream-ordered memory pool
+ *                              keeps mapped across synchronisations (runner
+ *                              workspaces; default 512 MiB, CUDA's own is 0)
  *   "render_vec", "bvh_leaf_size", "mesh_megakernel": see DESIGN.md */
 int mg_set_option(const char* name, int64_t value);
 

@@ -35,6 +35,20 @@ __global__ void fill_kernel(int64_t n, T* dst, T v) {
 }  // namespace
 
 namespace mg {
+// Bytes the device's default stream-ordered pool keeps mapped across
+// synchronisations (cudaMemPoolAttrReleaseThreshold; the CUDA default is 0:
+// every sync unmaps what was freed, so each runner call re-maps its
+// workspace).  mg_set_option("pool_keep_bytes", n).
+uint64_t g_pool_keep = uint64_t(512) << 20;
+
+int apply_pool_keep(int device) {
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, device) != cudaSuccess) return MG_ECUDA;
+  uint64_t keep = g_pool_keep;
+  return cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep) == cudaSuccess
+             ? MG_OK
+             : MG_ECUDA;
+}
 __global__ void counter_add_kernel(uint32_t* c, uint32_t inc) { *c += inc; }
 }  // namespace mg
 
@@ -155,6 +169,7 @@ int mg_ctx_create(int device, void* stream, mg_ctx** out) {
     return fail(MG_ECUDA, std::string("libmgcuda is built for sm_100a only; device is sm_") +
                               std::to_string(prop.major) + std::to_string(prop.minor));
   MG_CUDA_TRY(cudaSetDevice(device));
+  apply_pool_keep(device);
   mg_ctx* ctx = new mg_ctx();
   ctx->device = device;
   ctx->sm_count = prop.multiProcessorCount;

@@ -29,6 +29,8 @@ bool g_disable_tma = false;
 extern bool g_render_vec;
 extern bool g_render_fast;
 extern bool g_cluster_runner;
+extern uint64_t g_pool_keep;
+int apply_pool_keep(int device);
 extern int g_render_fast_variant;
 int render_fast_variants();
 extern bool g_mesh_megakernel;
@@ -775,6 +777,13 @@ int mg_set_option(const char* name, int64_t value) {
   }
   if (std::string(name) == "render_vec") {
     g_render_vec = value != 0;
+    return MG_OK;
+  }
+  if (std::string(name) == "pool_keep_bytes") {
+    if (value < 0) return fail(MG_EINVAL, "pool_keep_bytes must be non-negative");
+    g_pool_keep = uint64_t(value);
+    int dev = 0;
+    if (cudaGetDevice(&dev) == cudaSuccess) apply_pool_keep(dev);
     return MG_OK;
   }
   if (std::string(name) == "cluster_runner") {
