@@ -509,6 +509,10 @@ int mg_meshscene_info(const mg_mesh_scene* s, int32_t* nodes, int32_t* depth, in
  * The shade stage's texel-major copy of that buffer is then reused instead
  * of rebuilt (one relayout per iteration instead of two). */
 int mg_meshscene_set_prev_reuse(mg_mesh_scene* s, int32_t enable);
+/* Diagnostics (no reference counterpart): the queue counters of the scene's
+ * last wavefront sample pair — paths entering each depth, then shadow rays
+ * per depth (2 x (max depth + 1) entries, n_out >= 18).  Synchronises. */
+int mg_meshscene_queue_counts(mg_ctx* ctx, const mg_mesh_scene* s, int32_t n_out, uint32_t* out);
 /* closest hit of n rays (device fp64 [n][6] = origin, direction): t (inf on
  * a miss) and the original triangle index (-1 on a miss); ties on t go to
  * the lower index (= a brute-force scan). */

@@ -118,6 +118,7 @@ def load():
         "mg_meshscene_destroy": (C.c_int, [_vp]),
         "mg_meshscene_info": (C.c_int, [_vp, _vp, _vp, _vp]),
         "mg_meshscene_set_prev_reuse": (C.c_int, [_vp, C.c_int32]),
+        "mg_meshscene_queue_counts": (C.c_int, [_vp, _vp, C.c_int32, _vp]),
         "mg_ctx_set_iteration_offset": (C.c_int, [_vp, _vp]),
         "mg_iteration_offset_add": (C.c_int, [_vp, _vp, C.c_uint32]),
         "mg_meshscene_intersect": (C.c_int, [_vp, _vp, C.c_int32, _vp, _vp, _vp]),

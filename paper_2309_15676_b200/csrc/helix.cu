@@ -448,7 +448,7 @@ __global__ void __launch_bounds__(kHThreads)
   if (threadIdx.x < 2 * kNP) {
     long long s = 0;
     for (int w = 0; w < kHThreads / 32; ++w) s += red[w][threadIdx.x];
-    if (s) atomicAdd(&acc_g[threadIdx.x], (unsigned long long)s);
+    if (s) red_add_u64(&acc_g[threadIdx.x], (unsigned long long)s);
   }
   Acc a;
   a.ssn = loss;
@@ -576,7 +576,7 @@ __global__ void __launch_bounds__(kHThreads)
   if (threadIdx.x < 2 * kNP) {
     long long s = 0;
     for (int w = 0; w < kHThreads / 32; ++w) s += red[w][threadIdx.x];
-    if (s) atomicAdd(&acc_g[threadIdx.x], (unsigned long long)s);
+    if (s) red_add_u64(&acc_g[threadIdx.x], (unsigned long long)s);
   }
   Acc a;
   a.ssn = loss;

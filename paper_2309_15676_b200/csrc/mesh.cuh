@@ -37,6 +37,7 @@ struct mg_mesh_scene {
   const void* last_now = nullptr;  // `now` of the previous wavefront call ...
   int last_now_slot = -1;          // ... the copy slot holding it (-1: none)
   int last_dtype = -1;
+  unsigned int* last_cnt = nullptr;  // queue counters of the last wavefront call
 };
 
 namespace mg {
@@ -50,6 +51,12 @@ extern bool g_mesh_megakernel;
 // BVH, +0.035 ms; with the shared-memory stack and quantised nodes it wins
 // there too, 1.211 -> 1.143 ms.)
 extern int g_mesh_persistent;
+// mg_set_option("mesh_tail", d): fp32 wavefront depths >= d (0-based) run in
+// one wf_tail_kernel launch; 0 = never; -1 (default): the last kMeshTailDepths
+// depths (from depth 1 at the earliest) — measured best on configs[3] (depth
+// 6: tail from 2) and configs[4] (depth 8: 3 and 4 equal)
+extern int g_mesh_tail;
+constexpr int kMeshTailDepths = 4;
 // mg_set_option("mesh_smem_stack", 1): the persistent BVH4 traversals keep
 // their stack in shared memory ([entry][thread], conflict-free) instead of
 // staging the top nodes there
@@ -361,10 +368,15 @@ __device__ __forceinline__ bool tri_hit32(const float4* __restrict__ r, const fl
   return tri_test32(load_tri32(r), o, d, t, u, v);
 }
 
-template <bool ANY>
+// SSTK: stack in shared memory laid out [entry][thread] (kSmemStackT
+// entries of a kMThreads-thread CTA at smem_stack; see trace32_persistent);
+// QN: quantised 64-byte nodes (m.nodesq).  Same hits in every form.
+constexpr int kSmemStackT = 48;
+template <bool ANY, bool SSTK = false, bool QN = false>
 __device__ __forceinline__ int trace32_impl(const MeshDev& m, const float4* sn, const double o[3],
                                             const double d[3], double tmax, double& t_out,
-                                            double& u_out, double& v_out) {
+                                            double& u_out, double& v_out,
+                                            int* smem_stack = nullptr) {
   float of[3], df[3], inv[3], ooi[3];
 #pragma unroll
   for (int k = 0; k < 3; ++k) {
@@ -373,7 +385,20 @@ __device__ __forceinline__ int trace32_impl(const MeshDev& m, const float4* sn, 
     inv[k] = 1.0f / (fabsf(df[k]) > 1e-20f ? df[k] : copysignf(1e-20f, df[k]));
     ooi[k] = of[k] * inv[k];
   }
-  int stack[kStackDepth];
+  int lstack[SSTK ? 1 : kStackDepth];
+  int* const sstack = SSTK ? smem_stack + threadIdx.x : nullptr;
+  auto push = [&](int sp, int val) {
+    if constexpr (SSTK)
+      sstack[sp * kMThreads] = val;
+    else
+      lstack[sp] = val;
+  };
+  auto top = [&](int sp) {
+    if constexpr (SSTK)
+      return sstack[sp * kMThreads];
+    else
+      return lstack[sp];
+  };
   int sp = 0, node = 0;
   const float tmaxf = float(tmax);
   float best = tmaxf, bu = 0.0f, bv = 0.0f;
@@ -409,17 +434,50 @@ __device__ __forceinline__ int trace32_impl(const MeshDev& m, const float4* sn, 
         }
       }
     } else {
-      MG_DCHECK(node < m.nnodes && sp + 4 <= kStackDepth);
-      const NodeW n = load_node(m, sn, node);
+      MG_DCHECK(node < m.nnodes && sp + 4 <= (SSTK ? kSmemStackT : kStackDepth));
       float tk[4];
       int ck[4];
+      if constexpr (QN) {  // trace32_persistent's decode of the quantised node
+        const float4* src = m.nodesq + size_t(kNodeQF4) * node;
+        const float4 hd = __ldg(src), q0 = __ldg(src + 1), q1 = __ldg(src + 2), rf = __ldg(src + 3);
+        const unsigned eb = __float_as_uint(hd.w);
+        const float pa[3] = {hd.x, hd.y, hd.z};
+        float A[3], Bo[3];
 #pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        float tc;
-        const bool h = slab6(f4c(n.lx, c), f4c(n.ly, c), f4c(n.lz, c), f4c(n.hx, c), f4c(n.hy, c),
-                             f4c(n.hz, c), ooi, inv, best, tc);
-        tk[c] = h ? tc : INFINITY;
-        ck[c] = __float_as_int(f4c(n.ref, c));
+        for (int a = 0; a < 3; ++a) {
+          A[a] = __uint_as_float(((eb >> (8 * a)) & 255u) << 23) * inv[a];
+          Bo[a] = (pa[a] - of[a]) * inv[a];
+        }
+        const unsigned qw[6] = {__float_as_uint(q0.x), __float_as_uint(q0.y),
+                                __float_as_uint(q0.z), __float_as_uint(q0.w),
+                                __float_as_uint(q1.x), __float_as_uint(q1.y)};
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          float t[6];
+#pragma unroll
+          for (int f = 0; f < 6; ++f) {
+            const float qf =
+                __uint_as_float(__byte_perm(qw[f], 0x4B000000u, 0x7650u | unsigned(c))) -
+                8388608.0f;
+            t[f] = fmaf(qf, A[f % 3], Bo[f % 3]);
+          }
+          const float tn = fmaxf(fmaxf(fminf(t[0], t[3]), fminf(t[1], t[4])),
+                                 fmaxf(fminf(t[2], t[5]), 0.0f));
+          const float tf = fminf(fminf(fmaxf(t[0], t[3]), fmaxf(t[1], t[4])),
+                                 fminf(fmaxf(t[2], t[5]), best));
+          tk[c] = tn <= tf ? tn : INFINITY;
+          ck[c] = __float_as_int(f4c(rf, c));
+        }
+      } else {
+        const NodeW n = load_node<!SSTK>(m, sn, node);
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          float tc;
+          const bool h = slab6(f4c(n.lx, c), f4c(n.ly, c), f4c(n.lz, c), f4c(n.hx, c),
+                               f4c(n.hy, c), f4c(n.hz, c), ooi, inv, best, tc);
+          tk[c] = h ? tc : INFINITY;
+          ck[c] = __float_as_int(f4c(n.ref, c));
+        }
       }
       auto cx = [&](int a, int b) {
         if (tk[b] < tk[a]) {
@@ -444,7 +502,7 @@ __device__ __forceinline__ int trace32_impl(const MeshDev& m, const float4* sn, 
 #pragma unroll
         for (int c = 3; c >= 0; --c) {
           if (tk[c] == INFINITY) continue;
-          if (have) stack[sp++] = nx;
+          if (have) push(sp++, nx);
           nx = ck[c];
           have = true;
         }
@@ -453,15 +511,15 @@ __device__ __forceinline__ int trace32_impl(const MeshDev& m, const float4* sn, 
           continue;
         }
       } else if (tk[0] != INFINITY) {
-        if (tk[3] != INFINITY) stack[sp++] = ck[3];
-        if (tk[2] != INFINITY) stack[sp++] = ck[2];
-        if (tk[1] != INFINITY) stack[sp++] = ck[1];
+        if (tk[3] != INFINITY) push(sp++, ck[3]);
+        if (tk[2] != INFINITY) push(sp++, ck[2]);
+        if (tk[1] != INFINITY) push(sp++, ck[1]);
         node = ck[0];
         continue;
       }
     }
     if (sp == 0) break;
-    node = stack[--sp];
+    node = top(--sp);
   }
   t_out = bslot < 0 ? INFINITY : double(best);
   u_out = double(bu);

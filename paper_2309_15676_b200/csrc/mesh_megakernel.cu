@@ -223,10 +223,10 @@ __device__ __noinline__ void scatter(const PathStore<T, NS>& st, int nv, const T
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
       const T gb = w[c] * ((st.A[s][v][c] / T(kPiM)) + Q[c] * (st.invfb[s][v][c] / T(kPiM)));
-      atomicAdd(&acc[st.base[v] + c * R2], fixq(double(gb)));
+      red_add_u64(&acc[st.base[v] + c * R2], fixq(double(gb)));
       gr += w[c] * (st.A[s][v][c] * st.dSn[s][v] + Q[c] * (st.invfb[s][v][c] * st.dSb[s][v]));
     }
-    atomicAdd(&acc[st.base[v] + 3 * R2], fixq(double(gr)));
+    red_add_u64(&acc[st.base[v] + 3 * R2], fixq(double(gr)));
 #pragma unroll
     for (int c = 0; c < 3; ++c) Q[c] = Q[c] + st.C[s][v][c];
   }

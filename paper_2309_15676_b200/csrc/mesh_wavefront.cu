@@ -266,13 +266,234 @@ __global__ void __launch_bounds__(kMThreads, 8) wf_isect_p_kernel(MeshDev m, WF<
       sstk);
 }
 
+// One queued path's shade step at depth v: texel, NEE sample + shadow-ray
+// set-up, the BSDF values of the evaluated parameter sets, the Malley bounce
+// and the stored adjoint fields.  want_shadow / want_bounce: the path joins
+// this depth's shadow queue / the next depth's queue.  Shared by
+// wf_shade_kernel and wf_tail_kernel (identical per-path arithmetic).
+template <class T, int NCH>
+__device__ __forceinline__ void shade_path(const MeshK& q, const MeshDev& m, const WF<T>& w, int v,
+                                           int p, const T* __restrict__ th0,
+                                           const T* __restrict__ th1, int maxv, int R2, double la,
+                                           bool& want_shadow, bool& want_bounce) {
+  constexpr int TS = TexIlv<T, NCH>::TS;  // th0 / th1: texel-major copies
+  using F = VF<NCH>;
+  const double* V = q.view;
+  const T* th[2] = {th0, th1};
+  const int k = p / w.npix, pix = w.pix0 + (p - k * w.npix);
+  const int slot = w.hslot[p];
+  const bool store = p < w.PS;
+  // parameter sets evaluated: path 0 (A) and the FD path at theta_t and
+  // theta_{t-1}; the other proportional paths at theta_t only
+  const int ns = (k == 0 || k == w.nprop) ? 2 : 1;
+  T beta[2][3];
+#pragma unroll
+  for (int s = 0; s < 2; ++s)
+#pragma unroll
+    for (int c = 0; c < 3; ++c)
+      beta[s][c] = s < ns ? w.beta[size_t(s * 3 + c) * w.P + p] : T(0);
+  if (slot < 0) {  // escaped: environment
+#pragma unroll
+    for (int s = 0; s < 2; ++s)
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        if (s >= ns) break;
+        // L += E is left to the consumer (wf_scatter_kernel): the
+        // escape is the path's last event, so (L + E) there is the same
+        // sum, and the scattered read-modify-write of L is saved
+        w.E[size_t(s * 3 + c) * w.P + p] = beta[s][c] * T(V[21 + c]);
+      }
+  } else {
+    const double o[3] = {w.ox[p], w.oy[p], w.oz[p]}, d[3] = {w.dx[p], w.dy[p], w.dz[p]};
+    const double t = w.ht[p], bu = w.hu[p], bv = w.hv[p];
+    const double* r = m.tri + size_t(kRec) * slot;
+    const double x[3] = {o[0] + t * d[0], o[1] + t * d[1], o[2] + t * d[2]};
+    double nn[3] = {r[9], r[10], r[11]};
+    if (dot3d(nn, d) > 0.0) {
+      nn[0] = -nn[0];
+      nn[1] = -nn[1];
+      nn[2] = -nn[2];
+    }
+    const double U = (r[12] + bu * r[14]) + bv * r[16];
+    const double W_ = (r[13] + bu * r[15]) + bv * r[17];
+    int tx = int(U * q.R), ty = int(W_ * q.R);
+    tx = tx < 0 ? 0 : (tx > q.R - 1 ? q.R - 1 : tx);
+    ty = ty < 0 ? 0 : (ty > q.R - 1 ? q.R - 1 : ty);
+    const int oid = __ldg(&m.obj[slot]), tex = ty * q.R + tx;
+    const int pbase = oid * NCH * R2 + tex;
+    const size_t cell = size_t(oid) * R2 + tex;
+    w.nv[p] = v + 1;
+    if (store) w.vbase[size_t(v) * w.PS + p] = pbase;
+    bool nee_done = false, bounce_done = false;
+    T base[2][3], rough[2], metal[2];
+#pragma unroll
+    for (int s = 0; s < 2; ++s) {
+      if (s >= ns) {  // the set is not evaluated: no texel gathers
+#pragma unroll
+        for (int c = 0; c < 3; ++c) base[s][c] = T(0);
+        rough[s] = metal[s] = T(0);
+        continue;
+      }
+      T x[TS];
+      const T* tp = th[s] + cell * TS;
+      if constexpr (sizeof(T) == 4) {
+#pragma unroll
+        for (int g = 0; g < TS; g += 4) {
+          const float4 f4 = __ldg(reinterpret_cast<const float4*>(tp + g));
+          x[g] = f4.x;
+          x[g + 1] = f4.y;
+          x[g + 2] = f4.z;
+          x[g + 3] = f4.w;
+        }
+      } else {
+#pragma unroll
+        for (int g = 0; g < (NCH + 1) / 2 * 2; g += 2) {
+          const double2 d2 = __ldg(reinterpret_cast<const double2*>(tp + g));
+          x[g] = d2.x;
+          x[g + 1] = d2.y;
+        }
+      }
+#pragma unroll
+      for (int c = 0; c < 3; ++c) base[s][c] = x[c];
+      rough[s] = x[3];
+      metal[s] = NCH == 5 ? x[4] : T(0);
+    }
+    const double wo[3] = {-d[0], -d[1], -d[2]};
+    const double xo[3] = {x[0] + kOff * nn[0], x[1] + kOff * nn[1], x[2] + kOff * nn[2]};
+    double u[4];
+    prng(q.key, uint32_t(pix), q.iteration, uint32_t(k), uint32_t(v * 256 + 1), u);
+    const double lp[3] = {V[14] + u[0] * (V[15] - V[14]), V[13],
+                          V[16] + u[1] * (V[17] - V[16])};
+    double wl3[3] = {lp[0] - x[0], lp[1] - x[1], lp[2] - x[2]};
+    const double d2 = dot3d(wl3, wl3);
+    const double wl = sqrt(d2);
+    wl3[0] /= wl;
+    wl3[1] /= wl;
+    wl3[2] /= wl;
+    const double cx = dot3d(nn, wl3), cl = wl3[1];
+    const T nT[3] = {T(nn[0]), T(nn[1]), T(nn[2])}, woT[3] = {T(wo[0]), T(wo[1]), T(wo[2])};
+    if (cx > 0.0 && cl > 0.0 && dot3d(nn, wo) > 0.0) {
+      want_shadow = true;
+      const double gl = ((cx * cl) / d2) * la;
+      const T wT[3] = {T(wl3[0]), T(wl3[1]), T(wl3[2])};
+      nee_done = true;
+#pragma unroll
+      for (int s = 0; s < 2; ++s) {
+        if (s >= ns) break;
+        T f[3];
+        if constexpr (NCH == 5) {
+          T df[3][3];
+          bsdf_full<T>(base[s], metal[s], rough[s], nT, wT, woT, f, df);
+          if (store)
+#pragma unroll
+            for (int c = 0; c < 3; ++c)
+#pragma unroll
+              for (int kk = 0; kk < 3; ++kk) vf(w, v, F::dfn + s * 9 + c * 3 + kk, p) = df[c][kk];
+        } else {
+          T dS;
+          bsdf_m0<T>(base[s], rough[s], nT, wT, woT, f, dS);
+          if (store) vf(w, v, VF<4>::dSn + s, p) = dS;
+        }
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+          const T A = beta[s][c] * T(gl * V[18 + c]);
+          const T Cc = A * f[c];
+          if (store) {
+            vf(w, v, F::A + s * 3 + c, p) = A;
+            vf(w, v, F::C + s * 3 + c, p) = Cc;
+          }
+          w.pendC[size_t(s * 3 + c) * w.P + p] = Cc;
+        }
+      }
+      w.sox[p] = xo[0];
+      w.soy[p] = xo[1];
+      w.soz[p] = xo[2];
+      w.sdx[p] = wl3[0];
+      w.sdy[p] = wl3[1];
+      w.sdz[p] = wl3[2];
+      w.stm[p] = wl - kOff;
+    }
+    if (!(v == maxv - 1 || dot3d(nn, wo) <= 0.0)) {
+      double dx = 0.0, dy = 0.0;
+      bool got = false;
+      for (uint32_t j = 0; !got && j < 64; ++j) {
+        double c4[4];
+        if (j == 0) {
+          c4[0] = u[2];
+          c4[1] = u[3];
+          c4[2] = 2.0;
+          c4[3] = 2.0;
+        } else {
+          prng(q.key, uint32_t(pix), q.iteration, uint32_t(k), uint32_t(v * 256 + 1) + j, c4);
+        }
+#pragma unroll
+        for (int mm = 0; mm < 4; mm += 2) {
+          if (got) break;
+          const double a = 2.0 * c4[mm] - 1.0, b = 2.0 * c4[mm + 1] - 1.0;
+          if (c4[mm] <= 1.0 && a * a + b * b < 1.0) {
+            dx = a;
+            dy = b;
+            got = true;
+          }
+        }
+      }
+      const double dz = sqrt(fmax(0.0, 1.0 - (dx * dx + dy * dy)));
+      if (dz > 0.0) {
+        const double sign = copysign(1.0, nn[2]);
+        const double aa = -1.0 / (sign + nn[2]);
+        const double bb = nn[0] * nn[1] * aa;
+        const double Tb[3] = {1.0 + sign * (nn[0] * nn[0]) * aa, sign * bb, -sign * nn[0]};
+        const double Bb[3] = {bb, sign + (nn[1] * nn[1]) * aa, -nn[1]};
+        const double wi[3] = {(dx * Tb[0] + dy * Bb[0]) + dz * nn[0],
+                              (dx * Tb[1] + dy * Bb[1]) + dz * nn[1],
+                              (dx * Tb[2] + dy * Bb[2]) + dz * nn[2]};
+        const T wiT[3] = {T(wi[0]), T(wi[1]), T(wi[2])};
+        bounce_done = true;
+#pragma unroll
+        for (int s = 0; s < 2; ++s) {
+          if (s >= ns) break;
+          T f[3];
+          if constexpr (NCH == 5) {
+            T df[3][3];
+            bsdf_full<T>(base[s], metal[s], rough[s], nT, wiT, woT, f, df);
+            if (store)
+#pragma unroll
+              for (int c = 0; c < 3; ++c)
+#pragma unroll
+                for (int kk = 0; kk < 3; ++kk)
+                  vf(w, v, F::dfb + s * 9 + c * 3 + kk, p) = df[c][kk];
+          } else {
+            T dS;
+            bsdf_m0<T>(base[s], rough[s], nT, wiT, woT, f, dS);
+            if (store) vf(w, v, VF<4>::dSb + s, p) = dS;
+          }
+#pragma unroll
+          for (int c = 0; c < 3; ++c) {
+            if (store) vf(w, v, F::invfb + s * 3 + c, p) = f[c] != T(0) ? T(1) / f[c] : T(0);
+            w.beta[size_t(s * 3 + c) * w.P + p] = beta[s][c] * (f[c] * T(kPiM));
+          }
+        }
+        w.ox[p] = xo[0];
+        w.oy[p] = xo[1];
+        w.oz[p] = xo[2];
+        w.dx[p] = wi[0];
+        w.dy[p] = wi[1];
+        w.dz[p] = wi[2];
+        want_bounce = true;
+      }
+    }
+    if (store) {
+      w.vnee[size_t(v) * w.PS + p] = nee_done;
+      w.vbnc[size_t(v) * w.PS + p] = bounce_done;
+    }
+  }
+}
+
 template <class T, int NCH>
 __global__ void __launch_bounds__(kMThreads)
     wf_shade_kernel(MeshK q, MeshDev m, WF<T> w, int v, const T* __restrict__ th0,
                     const T* __restrict__ th1) {
-  constexpr int TS = TexIlv<T, NCH>::TS;  // th0 / th1: texel-major copies
   if (q.it_offset) q.iteration += __ldg(q.it_offset);
-  using F = VF<NCH>;
   const double* V = q.view;
   const int maxv = int(V[24]);
   const int R2 = q.R * q.R;
@@ -280,220 +501,13 @@ __global__ void __launch_bounds__(kMThreads)
   const int* qin = (v & 1) ? w.q1 : w.q0;
   int* qout = (v & 1) ? w.q0 : w.q1;
   const double la = (V[15] - V[14]) * (V[17] - V[16]);
-  const T* th[2] = {th0, th1};
   for (int i = blockIdx.x * kMThreads + threadIdx.x; i - int(threadIdx.x) < n;
        i += gridDim.x * kMThreads) {
     bool want_shadow = false, want_bounce = false;
     int p = -1;
     if (i < n) {
       p = qin[i];
-      const int k = p / w.npix, pix = w.pix0 + (p - k * w.npix);
-      const int slot = w.hslot[p];
-      const bool store = p < w.PS;
-      // parameter sets evaluated: path 0 (A) and the FD path at theta_t and
-      // theta_{t-1}; the other proportional paths at theta_t only
-      const int ns = (k == 0 || k == w.nprop) ? 2 : 1;
-      T beta[2][3];
-#pragma unroll
-      for (int s = 0; s < 2; ++s)
-#pragma unroll
-        for (int c = 0; c < 3; ++c)
-          beta[s][c] = s < ns ? w.beta[size_t(s * 3 + c) * w.P + p] : T(0);
-      if (slot < 0) {  // escaped: environment
-#pragma unroll
-        for (int s = 0; s < 2; ++s)
-#pragma unroll
-          for (int c = 0; c < 3; ++c) {
-            if (s >= ns) break;
-            // L += E is left to the consumer (wf_scatter_kernel): the
-            // escape is the path's last event, so (L + E) there is the same
-            // sum, and the scattered read-modify-write of L is saved
-            w.E[size_t(s * 3 + c) * w.P + p] = beta[s][c] * T(V[21 + c]);
-          }
-      } else {
-        const double o[3] = {w.ox[p], w.oy[p], w.oz[p]}, d[3] = {w.dx[p], w.dy[p], w.dz[p]};
-        const double t = w.ht[p], bu = w.hu[p], bv = w.hv[p];
-        const double* r = m.tri + size_t(kRec) * slot;
-        const double x[3] = {o[0] + t * d[0], o[1] + t * d[1], o[2] + t * d[2]};
-        double nn[3] = {r[9], r[10], r[11]};
-        if (dot3d(nn, d) > 0.0) {
-          nn[0] = -nn[0];
-          nn[1] = -nn[1];
-          nn[2] = -nn[2];
-        }
-        const double U = (r[12] + bu * r[14]) + bv * r[16];
-        const double W_ = (r[13] + bu * r[15]) + bv * r[17];
-        int tx = int(U * q.R), ty = int(W_ * q.R);
-        tx = tx < 0 ? 0 : (tx > q.R - 1 ? q.R - 1 : tx);
-        ty = ty < 0 ? 0 : (ty > q.R - 1 ? q.R - 1 : ty);
-        const int oid = __ldg(&m.obj[slot]), tex = ty * q.R + tx;
-        const int pbase = oid * NCH * R2 + tex;
-        const size_t cell = size_t(oid) * R2 + tex;
-        w.nv[p] = v + 1;
-        if (store) w.vbase[size_t(v) * w.PS + p] = pbase;
-        bool nee_done = false, bounce_done = false;
-        T base[2][3], rough[2], metal[2];
-#pragma unroll
-        for (int s = 0; s < 2; ++s) {
-          if (s >= ns) {  // the set is not evaluated: no texel gathers
-#pragma unroll
-            for (int c = 0; c < 3; ++c) base[s][c] = T(0);
-            rough[s] = metal[s] = T(0);
-            continue;
-          }
-          T x[TS];
-          const T* tp = th[s] + cell * TS;
-          if constexpr (sizeof(T) == 4) {
-#pragma unroll
-            for (int g = 0; g < TS; g += 4) {
-              const float4 f4 = __ldg(reinterpret_cast<const float4*>(tp + g));
-              x[g] = f4.x;
-              x[g + 1] = f4.y;
-              x[g + 2] = f4.z;
-              x[g + 3] = f4.w;
-            }
-          } else {
-#pragma unroll
-            for (int g = 0; g < (NCH + 1) / 2 * 2; g += 2) {
-              const double2 d2 = __ldg(reinterpret_cast<const double2*>(tp + g));
-              x[g] = d2.x;
-              x[g + 1] = d2.y;
-            }
-          }
-#pragma unroll
-          for (int c = 0; c < 3; ++c) base[s][c] = x[c];
-          rough[s] = x[3];
-          metal[s] = NCH == 5 ? x[4] : T(0);
-        }
-        const double wo[3] = {-d[0], -d[1], -d[2]};
-        const double xo[3] = {x[0] + kOff * nn[0], x[1] + kOff * nn[1], x[2] + kOff * nn[2]};
-        double u[4];
-        prng(q.key, uint32_t(pix), q.iteration, uint32_t(k), uint32_t(v * 256 + 1), u);
-        const double lp[3] = {V[14] + u[0] * (V[15] - V[14]), V[13],
-                              V[16] + u[1] * (V[17] - V[16])};
-        double wl3[3] = {lp[0] - x[0], lp[1] - x[1], lp[2] - x[2]};
-        const double d2 = dot3d(wl3, wl3);
-        const double wl = sqrt(d2);
-        wl3[0] /= wl;
-        wl3[1] /= wl;
-        wl3[2] /= wl;
-        const double cx = dot3d(nn, wl3), cl = wl3[1];
-        const T nT[3] = {T(nn[0]), T(nn[1]), T(nn[2])}, woT[3] = {T(wo[0]), T(wo[1]), T(wo[2])};
-        if (cx > 0.0 && cl > 0.0 && dot3d(nn, wo) > 0.0) {
-          want_shadow = true;
-          const double gl = ((cx * cl) / d2) * la;
-          const T wT[3] = {T(wl3[0]), T(wl3[1]), T(wl3[2])};
-          nee_done = true;
-#pragma unroll
-          for (int s = 0; s < 2; ++s) {
-            if (s >= ns) break;
-            T f[3];
-            if constexpr (NCH == 5) {
-              T df[3][3];
-              bsdf_full<T>(base[s], metal[s], rough[s], nT, wT, woT, f, df);
-              if (store)
-#pragma unroll
-                for (int c = 0; c < 3; ++c)
-#pragma unroll
-                  for (int kk = 0; kk < 3; ++kk) vf(w, v, F::dfn + s * 9 + c * 3 + kk, p) = df[c][kk];
-            } else {
-              T dS;
-              bsdf_m0<T>(base[s], rough[s], nT, wT, woT, f, dS);
-              if (store) vf(w, v, VF<4>::dSn + s, p) = dS;
-            }
-#pragma unroll
-            for (int c = 0; c < 3; ++c) {
-              const T A = beta[s][c] * T(gl * V[18 + c]);
-              const T Cc = A * f[c];
-              if (store) {
-                vf(w, v, F::A + s * 3 + c, p) = A;
-                vf(w, v, F::C + s * 3 + c, p) = Cc;
-              }
-              w.pendC[size_t(s * 3 + c) * w.P + p] = Cc;
-            }
-          }
-          w.sox[p] = xo[0];
-          w.soy[p] = xo[1];
-          w.soz[p] = xo[2];
-          w.sdx[p] = wl3[0];
-          w.sdy[p] = wl3[1];
-          w.sdz[p] = wl3[2];
-          w.stm[p] = wl - kOff;
-        }
-        if (!(v == maxv - 1 || dot3d(nn, wo) <= 0.0)) {
-          double dx = 0.0, dy = 0.0;
-          bool got = false;
-          for (uint32_t j = 0; !got && j < 64; ++j) {
-            double c4[4];
-            if (j == 0) {
-              c4[0] = u[2];
-              c4[1] = u[3];
-              c4[2] = 2.0;
-              c4[3] = 2.0;
-            } else {
-              prng(q.key, uint32_t(pix), q.iteration, uint32_t(k), uint32_t(v * 256 + 1) + j, c4);
-            }
-#pragma unroll
-            for (int mm = 0; mm < 4; mm += 2) {
-              if (got) break;
-              const double a = 2.0 * c4[mm] - 1.0, b = 2.0 * c4[mm + 1] - 1.0;
-              if (c4[mm] <= 1.0 && a * a + b * b < 1.0) {
-                dx = a;
-                dy = b;
-                got = true;
-              }
-            }
-          }
-          const double dz = sqrt(fmax(0.0, 1.0 - (dx * dx + dy * dy)));
-          if (dz > 0.0) {
-            const double sign = copysign(1.0, nn[2]);
-            const double aa = -1.0 / (sign + nn[2]);
-            const double bb = nn[0] * nn[1] * aa;
-            const double Tb[3] = {1.0 + sign * (nn[0] * nn[0]) * aa, sign * bb, -sign * nn[0]};
-            const double Bb[3] = {bb, sign + (nn[1] * nn[1]) * aa, -nn[1]};
-            const double wi[3] = {(dx * Tb[0] + dy * Bb[0]) + dz * nn[0],
-                                  (dx * Tb[1] + dy * Bb[1]) + dz * nn[1],
-                                  (dx * Tb[2] + dy * Bb[2]) + dz * nn[2]};
-            const T wiT[3] = {T(wi[0]), T(wi[1]), T(wi[2])};
-            bounce_done = true;
-#pragma unroll
-            for (int s = 0; s < 2; ++s) {
-              if (s >= ns) break;
-              T f[3];
-              if constexpr (NCH == 5) {
-                T df[3][3];
-                bsdf_full<T>(base[s], metal[s], rough[s], nT, wiT, woT, f, df);
-                if (store)
-#pragma unroll
-                  for (int c = 0; c < 3; ++c)
-#pragma unroll
-                    for (int kk = 0; kk < 3; ++kk)
-                      vf(w, v, F::dfb + s * 9 + c * 3 + kk, p) = df[c][kk];
-              } else {
-                T dS;
-                bsdf_m0<T>(base[s], rough[s], nT, wiT, woT, f, dS);
-                if (store) vf(w, v, VF<4>::dSb + s, p) = dS;
-              }
-#pragma unroll
-              for (int c = 0; c < 3; ++c) {
-                if (store) vf(w, v, F::invfb + s * 3 + c, p) = f[c] != T(0) ? T(1) / f[c] : T(0);
-                w.beta[size_t(s * 3 + c) * w.P + p] = beta[s][c] * (f[c] * T(kPiM));
-              }
-            }
-            w.ox[p] = xo[0];
-            w.oy[p] = xo[1];
-            w.oz[p] = xo[2];
-            w.dx[p] = wi[0];
-            w.dy[p] = wi[1];
-            w.dz[p] = wi[2];
-            want_bounce = true;
-          }
-        }
-        if (store) {
-          w.vnee[size_t(v) * w.PS + p] = nee_done;
-          w.vbnc[size_t(v) * w.PS + p] = bounce_done;
-        }
-      }
+      shade_path<T, NCH>(q, m, w, v, p, th0, th1, maxv, R2, la, want_shadow, want_bounce);
     }
     const int qs = enqueue(want_shadow, &w.cnt[kMaxV + 1 + v]);
     MG_DCHECK(qs < w.P);
@@ -583,6 +597,92 @@ __global__ void __launch_bounds__(kMThreads, kP8Blocks) wf_shadow_p8_kernel(Mesh
       });
 }
 
+// Tail of the wavefront (fp32 mode).  After a few depths the queues are
+// small (configs[4]: 5.2M paths enter depth 1, 0.69M depth 3, 75k depth 8)
+// and every stage launch is bounded by its slowest ray, not by throughput:
+// the depth-8 shadow stage takes 0.11 ms for 24k rays.  From depth v0 on,
+// one launch carries each remaining path through all its remaining depths —
+// closest hit, shade_path, any-hit NEE ray, next bounce — so the long
+// traversals of different depths overlap instead of each stage waiting for
+// its slowest ray.  Lanes whose path ends take the next queue entry
+// (warp-aggregated fetch at the top of every depth step).  The per-path
+// arithmetic is the wavefront's (same traversal results: closest hit by t,
+// then the lower original index; any-hit is a visibility test), so the
+// result is bit-identical.
+// SSTK / QN: the traversal stack in shared memory, quantised nodes (as the
+// persistent stages).
+#ifndef MG_TAIL_BLOCKS
+#define MG_TAIL_BLOCKS 4
+#endif
+template <int NCH, bool SSTK, bool QN>
+__global__ void __launch_bounds__(kMThreads, MG_TAIL_BLOCKS)
+    wf_tail_kernel(MeshK q, MeshDev m, WF<float> w, int v0, const float* __restrict__ th0,
+                   const float* __restrict__ th1) {
+  __shared__ float4 sn[SSTK ? 1 : kNodeF4 * kSmemNodes];
+  __shared__ int sstk[SSTK ? kSmemStackT * kMThreads : 1];
+  if (!SSTK) stage_nodes(m, sn);
+  if (q.it_offset) q.iteration += __ldg(q.it_offset);
+  const double* V = q.view;
+  const int maxv = int(V[24]);
+  const int R2 = q.R * q.R;
+  const double la = (V[15] - V[14]) * (V[17] - V[16]);
+  const int n = int(w.cnt[v0]);
+  const int* qin = (v0 & 1) ? w.q1 : w.q0;
+  // depth v0's isect fetch counter: that stage does not run
+  unsigned int* fetch = &w.cnt[2 * (kMaxV + 1) + v0];
+  const int lane = int(threadIdx.x & 31);
+  int p = -1, v = v0;
+  bool done = false;
+  for (;;) {
+    const bool need = p < 0 && !done;
+    const unsigned needm = __ballot_sync(0xffffffffu, need);
+    if (needm) {
+      const int leader = __ffs(needm) - 1;
+      unsigned base = 0;
+      if (lane == leader) base = atomicAdd(fetch, unsigned(__popc(needm)));
+      base = __shfl_sync(0xffffffffu, base, leader);
+      if (need) {
+        const int idx = int(base + unsigned(__popc(needm & ((1u << lane) - 1u))));
+        if (idx < n) {
+          p = qin[idx];
+          v = v0;
+        } else {
+          done = true;
+        }
+      }
+    }
+    if (__all_sync(0xffffffffu, done)) break;
+    if (p < 0) continue;
+    {
+      const double o[3] = {w.ox[p], w.oy[p], w.oz[p]}, d[3] = {w.dx[p], w.dy[p], w.dz[p]};
+      double t = INFINITY, bu = 0.0, bv = 0.0;
+      const int slot = trace32_impl<false, SSTK, QN>(m, sn, o, d, INFINITY, t, bu, bv, sstk);
+      w.hslot[p] = slot;
+      w.ht[p] = t;
+      w.hu[p] = bu;
+      w.hv[p] = bv;
+    }
+    bool want_shadow = false, want_bounce = false;
+    shade_path<float, NCH>(q, m, w, v, p, th0, th1, maxv, R2, la, want_shadow, want_bounce);
+    if (want_shadow) {
+      const double o[3] = {w.sox[p], w.soy[p], w.soz[p]}, d[3] = {w.sdx[p], w.sdy[p], w.sdz[p]};
+      double ts, tu, tv;
+      if (trace32_impl<true, SSTK, QN>(m, sn, o, d, w.stm[p], ts, tu, tv, sstk) < 0) {
+        const int k = p / w.npix;
+        const int nj = (k == 0 || k == w.nprop) ? 6 : 3;
+        for (int j = 0; j < nj; ++j) w.L[size_t(j) * w.P + p] += w.pendC[size_t(j) * w.P + p];
+      } else if (p < w.PS) {  // occluded: no NEE data at this vertex
+        w.vnee[size_t(v) * w.PS + p] = 0;
+      }
+    }
+    if (want_bounce) {
+      ++v;
+    } else {
+      p = -1;
+    }
+  }
+}
+
 // Where the fixed-point adjoints go.
 //  * One rank (ilv = 1): one accumulator, texel-interleaved
 //    [obj][texel][prop | diff][NCH] — the NCH channel atomics of a vertex
@@ -637,7 +737,7 @@ __device__ __forceinline__ void cell_add(bool agg, const AccTable& acc,
                                          const unsigned long long (&val)[NCH]) {
   if (!agg) {
 #pragma unroll
-    for (int k = 0; k < NCH; ++k) atomicAdd(cell.at(acc, which, k), val[k]);
+    for (int k = 0; k < NCH; ++k) red_add_u64(cell.at(acc, which, k), val[k]);
     return;
   }
   const unsigned act = __activemask();
@@ -658,7 +758,7 @@ __device__ __forceinline__ void cell_add(bool agg, const AccTable& acc,
   }
   if (lane == leader)
 #pragma unroll
-    for (int k = 0; k < NCH; ++k) atomicAdd(cell.at(acc, which, k), sum[k]);
+    for (int k = 0; k < NCH; ++k) red_add_u64(cell.at(acc, which, k), sum[k]);
 }
 
 // Per-vertex adjoint terms of stored path p, parameter set s (megakernel
@@ -963,6 +1063,7 @@ int wavefront_pair(mg_ctx* ctx, mg_mesh_scene* s, const MeshK& q, int nprop, con
     s->last_dtype = dt;
   }
   const MeshDev m = dev_of(s);
+  s->last_cnt = w.cnt;
   MG_CUDA_TRY(cudaMemsetAsync(w.cnt, 0, sizeof(unsigned int) * 4 * (kMaxV + 1), ctx->stream));
   const int grid = grid_for(ctx, w.P, kMThreads, 8);
   // persistent traversals: one resident wave (8 CTAs of 128 per SM; the
@@ -978,8 +1079,23 @@ int wavefront_pair(mg_ctx* ctx, mg_mesh_scene* s, const MeshK& q, int nprop, con
                                           "wavefront depth 2", "wavefront depth 3",
                                           "wavefront depth 4", "wavefront depth 5",
                                           "wavefront depth 6", "wavefront depth 7"};
+  const int tail_from =
+      g_mesh_tail >= 0 ? g_mesh_tail : (maxv - kMeshTailDepths > 1 ? maxv - kMeshTailDepths : 1);
   for (int v = 0; v < maxv; ++v) {
     MG_NVTX(kDepthName[v]);
+    if constexpr (sizeof(T) == 4) {
+      if (tail_from > 0 && v >= tail_from) {
+        const int tgrid = grid_for(ctx, w.P, kMThreads, MG_TAIL_BLOCKS);
+        if (sstk && g_mesh_qnodes)
+          wf_tail_kernel<NCH, true, true><<<tgrid, kMThreads, 0, ctx->stream>>>(q, m, w, v, thI[0],
+                                                                                thI[1]);
+        else
+          wf_tail_kernel<NCH, false, false><<<tgrid, kMThreads, 0, ctx->stream>>>(q, m, w, v,
+                                                                                  thI[0], thI[1]);
+        MG_LAUNCH_CHECK(ctx);
+        break;
+      }
+    }
     if constexpr (sizeof(T) == 4) {
       if ((pmode & 1) && g_mesh_bvh8)
         wf_isect_p8_kernel<<<pgrid8, kMThreads, 0, ctx->stream>>>(m, w, v);
@@ -1140,6 +1256,20 @@ int mg_meshscene_sample_pair_sharded(mg_ctx* ctx, mg_mesh_scene* s, int32_t dtyp
   tbl.shard = int(shard);
   tbl.ilv = 0;
   return dispatch_wavefront(ctx, s, q, dtype, prop_paths, target_img, now, prev, tbl, loss_out);
+}
+
+// Queue counters of the scene's last wavefront sample pair (diagnostics):
+// out[0..kMaxV] = paths entering isect at each depth (entry kMaxV: bounce
+// survivors of the last depth), out[kMaxV+1 .. 2kMaxV+1] = shadow rays per
+// depth.  n_out >= 2 * (kMaxV + 1); synchronises the context's stream.
+int mg_meshscene_queue_counts(mg_ctx* ctx, const mg_mesh_scene* s, int32_t n_out, uint32_t* out) {
+  if (!ctx || !s || !out || n_out < 2 * (kMaxV + 1))
+    return fail(MG_EINVAL, "mg_meshscene_queue_counts: bad arguments");
+  if (!s->last_cnt) return fail(MG_EINVAL, "mg_meshscene_queue_counts: no wavefront call yet");
+  MG_CUDA_TRY(cudaMemcpyAsync(out, s->last_cnt, sizeof(uint32_t) * 2 * (kMaxV + 1),
+                              cudaMemcpyDeviceToHost, ctx->stream));
+  MG_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+  return MG_OK;
 }
 
 #ifndef MG_PREV_REUSE

@@ -105,6 +105,18 @@ struct mg_ctx {
 
 namespace mg {
 
+// ------------------------------------------------- fixed-point accumulation
+// Fire-and-forget 64-bit integer add into GLOBAL memory (RED: no value comes
+// back).  atomicAdd on a pointer the compiler cannot prove global compiles
+// to a generic-address ATOM with a return value plus a shared-window CAS
+// branch; the adjoint scatters discard the result, so RED is the whole
+// operation.  No "memory" clobber: nothing in a scattering kernel reads the
+// accumulator, so independent loads may be scheduled across the adds.
+// Integer adds commute: the sums are the same bits in any order.
+__device__ __forceinline__ void red_add_u64(unsigned long long* p, unsigned long long v) {
+  asm volatile("red.relaxed.gpu.global.add.u64 [%0], %1;" ::"l"(p), "l"(v));
+}
+
 // --------------------------------------------------------------- dtype utils
 template <class T>
 struct VecOf;

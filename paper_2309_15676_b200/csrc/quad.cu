@@ -91,6 +91,15 @@ __global__ void __launch_bounds__(kQThreads)
 
 __device__ __forceinline__ long long to_fix(double v) { return llrint(v * kFix); }
 
+// shared-memory accumulator: atomicAdd (ATOMS); global: a RED (red_add_u64)
+template <bool SHARED>
+__device__ __forceinline__ void acc_add(unsigned long long* p, unsigned long long v) {
+  if constexpr (SHARED)
+    atomicAdd(p, v);
+  else
+    red_add_u64(p, v);
+}
+
 // SHARED: privatised accumulators [2][3][T] in dynamic shared memory.
 template <class T, bool SHARED>
 __global__ void __launch_bounds__(kQThreads)
@@ -127,19 +136,19 @@ __global__ void __launch_bounds__(kQThreads)
           tC >= 0 ? (double(now[c * T_ + tC]) - double(prev[c * T_ + tC])) * KC[c] : 0.0;
       loss += rA * rB;
       if (tB >= 0) {
-        atomicAdd(&acc[c * T_ + tB], (unsigned long long)to_fix(rA * KB[c]));
-        atomicAdd(&acc[3 * T_ + c * T_ + tB], (unsigned long long)to_fix(dI * KB[c]));
+        acc_add<SHARED>(&acc[c * T_ + tB], (unsigned long long)to_fix(rA * KB[c]));
+        acc_add<SHARED>(&acc[3 * T_ + c * T_ + tB], (unsigned long long)to_fix(dI * KB[c]));
       }
       if (tA >= 0) {
-        atomicAdd(&acc[c * T_ + tA], (unsigned long long)to_fix(rB * KA[c]));
-        atomicAdd(&acc[3 * T_ + c * T_ + tA], (unsigned long long)to_fix(dI * KA[c]));
+        acc_add<SHARED>(&acc[c * T_ + tA], (unsigned long long)to_fix(rB * KA[c]));
+        acc_add<SHARED>(&acc[3 * T_ + c * T_ + tA], (unsigned long long)to_fix(dI * KA[c]));
       }
     }
   }
   if (SHARED) {
     __syncthreads();
     for (int k = threadIdx.x; k < 6 * T_; k += kQThreads)
-      if (acc_s[k]) atomicAdd(&acc_g[k], acc_s[k]);
+      if (acc_s[k]) red_add_u64(&acc_g[k], acc_s[k]);
   }
   Acc a;
   a.ssn = loss;

@@ -197,6 +197,40 @@ def test_prev_copy_reuse_is_bit_identical(api, channels, nprop):
         torch.testing.assert_close(x, y, rtol=1e-5, atol=1e-6)
 
 
+@pytest.mark.parametrize("channels,nprop", [(4, 2), (5, 4)])
+def test_wavefront_tail_is_bit_identical(api, channels, nprop):
+    """fp32 wavefront tail (wf_tail_kernel: one launch carries every path
+    still alive at depth d through its remaining depths): the sample pair
+    and the loss estimate equal the all-stages wavefront's bit for bit for
+    every tail depth, and the default (-1: the last 4 depths) is one of
+    them; image tiles too."""
+    from paper_2309_15676_b200._lib import check, load
+    L = load()
+    prob = api.MeshTextureProblem(48, 40, 16, (8, 12), (10, 12), max_vertices=6, target_spp=4,
+                                  dtype=torch.float32, channels=channels, prop_paths=nprop)
+    n = prob.dim()
+    rs = np.random.RandomState(3)
+    now = torch.tensor(rs.uniform(0.1, 0.9, n), dtype=torch.float32, device="cuda")
+    prev = torch.tensor(rs.uniform(0.1, 0.9, n), dtype=torch.float32, device="cuda")
+    out = {}
+    try:
+        for tail in (0, 1, 2, 3, 5, -1):
+            check(L.mg_set_option(b"mesh_tail", tail))
+            pr = prob.sample_pair(now, prev, 7, 11)
+            t0 = prob.sample_pair(now, prev, 7, 11, rows=(0, 17))
+            t1 = prob.sample_pair(now, prev, 7, 11, rows=(17, 40))
+            out[tail] = (pr.prop.clone(), pr.diff.clone(), float(prob.loss_buf[0]),
+                         t0.prop + t1.prop, t0.diff + t1.diff)
+    finally:
+        check(L.mg_set_option(b"mesh_tail", -1))
+    ref = out[0]
+    assert torch.count_nonzero(ref[0]) > 0
+    for tail, o in out.items():
+        assert torch.equal(o[0], ref[0]) and torch.equal(o[1], ref[1]), tail
+        assert o[2] == ref[2], tail
+        assert torch.equal(o[3], ref[3]) and torch.equal(o[4], ref[4]), tail
+
+
 # ------------------------------------------------------ configs[4] form
 @pytest.mark.parametrize("nprop,maxv", [(4, 5), (3, 8), (2, 3)])
 def test_metalness_sample_pair_bit_exact_vs_oracle(api, oracle, nprop, maxv):
