@@ -343,6 +343,22 @@ int mg_meta_update(mg_ctx* ctx, int32_t dtype, int64_t n, const mg_meta_update_a
                    void* var, void* alpha_prev, const void* params_in, void* params_out,
                    mg_update_scalars* scalars, const mg_meta_extras* x);
 
+/* mg_meta_update whose sample pair is the texel-interleaved 2^-40
+ * fixed-point accumulator a mesh sample pair leaves behind when called with
+ * prop = diff = NULL (mg_meshscene_sample_pair): accum = int64
+ * [cells][prop | diff][nch], cells = objects * r2; parameters planar
+ * [object][nch][r2], n = cells * nch.  prop_i / diff_i = (double)word / 2^40
+ * rounded to dtype — exactly what mg_meshscene_sample_pair would have written
+ * — and the accumulator is zeroed, so every element equals the unfused
+ * finalize + mg_meta_update (the reductions may sum in another order).  One
+ * pass: the planar pair is never stored (16 B less HBM traffic per
+ * parameter).  No reference counterpart beyond mg_meta_update's
+ * (harness.cpp:144-188); x->vprop / vdiff -> MG_EUNSUPPORTED. */
+int mg_meta_update_fixed(mg_ctx* ctx, int32_t dtype, int64_t cells, int32_t nch, int32_t r2,
+                         const mg_meta_update_args* a, void* accum, void* m2_prop, void* m2_diff,
+                         void* mean, void* var, void* alpha_prev, const void* params_in,
+                         void* params_out, mg_update_scalars* scalars, const mg_meta_extras* x);
+
 /* Tile-sharded SHARED parameters (configs 4/5 shape), one rank's step as one
  * kernel over peer memory: for the parameter shard [shard_lo, shard_lo +
  * shard_n) it sums the world ranks' partial sample pairs prop_parts[q],
@@ -531,7 +547,9 @@ int mg_meshscene_render(mg_ctx* ctx, const mg_mesh_scene* s, int32_t dtype, int3
  *   loss_out (device double) = 2/(n(n-1)) sum_c sum_{i<j} r_i r_j.
  * accum: device scratch of 2 * params int64 (internal layout), zero on
  * first use (left zeroed).  Exact fixed-point accumulation: tiles sum exactly to the full
- * pair.  The scene owns the path-state workspace: calls on one scene must
+ * pair.  prop = diff = NULL (wavefront form): the pair is left in accum as
+ * the texel-interleaved fixed-point words [objects * R^2][prop | diff][nch]
+ * for mg_meta_update_fixed to consume (which zeroes it) — no planar pair.  The scene owns the path-state workspace: calls on one scene must
  * be ordered (one stream at a time). */
 int mg_meshscene_sample_pair(mg_ctx* ctx, mg_mesh_scene* s, int32_t dtype, int32_t W,
                              int32_t H, const double* view, const void* target_img,

@@ -82,6 +82,9 @@ def load():
         "mg_adam_step": (C.c_int, [_vp, C.c_int32, C.c_int64, P(_abi.AdamScalars)] + [_vp] * 4),
         "mg_meta_update": (C.c_int, [_vp, C.c_int32, C.c_int64, P(_abi.MetaUpdateArgs)] +
                            [_vp] * 9 + [_vp, P(_abi.MetaExtras)]),
+        "mg_meta_update_fixed": (C.c_int, [_vp, C.c_int32, C.c_int64, C.c_int32, C.c_int32,
+                                           P(_abi.MetaUpdateArgs)] + [_vp] * 8 +
+                                 [_vp, P(_abi.MetaExtras)]),
         "mg_shared_meta_update": (C.c_int, [_vp, C.c_int32, C.c_int64, C.c_int64, C.c_int32,
                                             P(_abi.MetaUpdateArgs), _vp, _vp, _vp] +
                                   [_vp] * 7 + [_vp]),

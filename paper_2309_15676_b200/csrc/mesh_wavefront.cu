@@ -1173,8 +1173,9 @@ int mg_meshscene_sample_pair(mg_ctx* ctx, mg_mesh_scene* s, int32_t dtype, int32
                              int32_t row0, int32_t row1, int32_t prop_paths, void* accum,
                              void* prop, void* diff, double* loss_out) {
   MG_NVTX("mg_meshscene_sample_pair");
-  if (!ctx || !s || !target_img || !now || !prev || !accum || !prop || !diff || !loss_out)
+  if (!ctx || !s || !target_img || !now || !prev || !accum || !loss_out || (!prop != !diff))
     return fail(MG_EINVAL, "mg_meshscene_sample_pair: null argument");
+  const bool keep_acc = !prop;  // pair left in accum for mg_meta_update_fixed
   if (prop_paths < 2 || prop_paths > kMaxProp)
     return fail(MG_EINVAL, "mg_meshscene_sample_pair: prop_paths must lie in [2, 8]");
   if (W < 1 || H < 1) return fail(MG_EINVAL, "mg_meshscene_sample_pair: bad sizes");
@@ -1194,7 +1195,7 @@ int mg_meshscene_sample_pair(mg_ctx* ctx, mg_mesh_scene* s, int32_t dtype, int32
   tbl.ilv = 1;
   // the megakernel implements the configs[3] form (4 channels, 2 proportional
   // paths) and accumulates in planar order
-  const bool mega = g_mesh_megakernel && s->nch == 4 && prop_paths == 2;
+  const bool mega = g_mesh_megakernel && s->nch == 4 && prop_paths == 2 && !keep_acc;
   if (mega) {
     s->last_now_slot = -1;  // the texel-copy reuse chain follows wavefront calls only
     st = megakernel_pair(ctx, s, q, dtype, target_img, now, prev, acc, np, loss_out);
@@ -1202,6 +1203,7 @@ int mg_meshscene_sample_pair(mg_ctx* ctx, mg_mesh_scene* s, int32_t dtype, int32
     st = dispatch_wavefront(ctx, s, q, dtype, prop_paths, target_img, now, prev, tbl, loss_out);
   }
   if (st) return st;
+  if (keep_acc) return MG_OK;
   if (!mega) {
     const long long cells = (long long)s->nobj * s->R * s->R;
     if (dtype == MG_F64)

@@ -282,6 +282,209 @@ __global__ void __launch_bounds__(kTmaThreads, kMinBlocks)
   });
 }
 
+// ------------------------------ fused update from a fixed-point accumulator
+// The mesh renderers' adjoints arrive as a texel-interleaved 2^-40
+// fixed-point accumulator [cell = obj*R2 + texel][prop | diff][NCH] (int64);
+// the parameters stay planar [obj][ch][texel].  This kernel converts,
+// zeroes and consumes the accumulator in the same pass as the meta update,
+// so the planar prop / diff arrays of mesh_finalize_ilv_kernel are never
+// written nor read back: 16 B of HBM traffic less per parameter.  A tile is
+// K = THREADS texels of one object: the accumulator tile (K x 2 x NCH words,
+// contiguous) and, per state array, NCH contiguous K-runs (one per channel
+// plane) arrive by 1-D bulk copies into a STAGES-deep ring (lanes of warp 0
+// issue them in parallel); thread t owns texel t's NCH parameters, reads
+// its fixed-point words from shared memory, zeroes the global tile with
+// coalesced 16-byte stores and writes its outputs (coalesced per channel
+// plane).  prop/diff = T(double(word) / 2^40), exactly mesh_finalize's
+// conversion, so every element equals finalize + mg_meta_update's.
+constexpr double kFixScale = 1099511627776.0;  // 2^40 (mesh.cuh kFixM)
+constexpr int kFixArrays = 6;                   // m2p m2d mean var ap pin
+
+template <class T, int NCH, int K>
+__host__ __device__ constexpr size_t fix_stage_bytes() {
+  return size_t(K) * 2 * NCH * 8 + size_t(kFixArrays) * NCH * K * sizeof(T);
+}
+
+// Thread t owns texels t, t + THREADS, ... (TPT of them): the tile is
+// K = THREADS * TPT texels, so each channel run is one K-element copy.
+// (16-byte packs of 4 consecutive texels per thread, i.e. 4x fewer threads
+// for the same smem, measured 10-40 % slower: too few warps for the IEEE
+// division chains.)
+template <class T, bool FIRST, int NCH, int THREADS, int TPT, int STAGES, int MINB>
+__global__ void __launch_bounds__(THREADS, MINB)
+    meta_update_fixed_tma_kernel(int64_t tiles, int R2, MetaK k, MetaPtrs<T> q,
+                                 unsigned long long* __restrict__ acc, mg_update_scalars* sc,
+                                 ReducePartials* partials, unsigned int* counter) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  __shared__ __align__(8) uint64_t full[STAGES];
+  constexpr int K = THREADS * TPT;
+  constexpr size_t kAccBytes = size_t(K) * 2 * NCH * 8;
+  constexpr size_t kStage = fix_stage_bytes<T, NCH, K>();
+  const StepScal s = load_step_scalars(k, sc);
+  T* const dst_arr[kFixArrays] = {q.m2p, q.m2d, q.mean, q.var, q.ap, nullptr};
+  const T* const src_arr[kFixArrays] = {q.m2p, q.m2d, q.mean, q.var, q.ap, q.pin};
+  const bool use[kFixArrays] = {!FIRST, s.cnt0 > 0, !FIRST, !FIRST, !FIRST, true};
+  (void)dst_arr;
+  uint32_t tx = uint32_t(kAccBytes);
+  int ncopy = 1;
+#pragma unroll
+  for (int a = 0; a < kFixArrays; ++a)
+    if (use[a]) {
+      tx += uint32_t(NCH * K * sizeof(T));
+      ncopy += NCH;
+    }
+  const int64_t my_tiles =
+      int64_t(blockIdx.x) < tiles ? (tiles - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
+  if (threadIdx.x == 0) {
+    for (int st = 0; st < STAGES; ++st) mbar_init(&full[st], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  const uint64_t pol = l2_evict_first_policy();
+  // warp 0: lane 0 arms the stage's barrier, lanes 0..ncopy-1 issue one copy each
+  auto issue = [&](int64_t li) {
+    const int st = int(li % STAGES);
+    const int64_t tile = int64_t(blockIdx.x) + li * gridDim.x;
+    const int64_t cell0 = tile * K;
+    const int64_t obj = cell0 / R2, tex0 = cell0 - obj * R2;
+    unsigned char* sb = smem_raw + size_t(st) * kStage;
+    const int lane = int(threadIdx.x);
+    if (lane == 0) mbar_arrive_expect_tx(&full[st], tx);
+    __syncwarp();
+    if (lane == 0) {
+      bulk_g2s_hint(sb, acc + cell0 * 2 * NCH, uint32_t(kAccBytes), &full[st], pol);
+    } else if (lane < ncopy) {
+      // lane j >= 1: the (j-1)-th used (array, channel) run
+      int r = lane - 1, a = 0;
+#pragma unroll
+      for (int b = 0; b < kFixArrays; ++b)
+        if (use[b]) {
+          if (r >= NCH) {
+            r -= NCH;
+          } else {
+            a = b;
+            break;
+          }
+        }
+      const int c = r;
+      T* dst = reinterpret_cast<T*>(sb + kAccBytes) + (size_t(a) * NCH + c) * K;
+      bulk_g2s_hint(dst, src_arr[a] + (obj * NCH + c) * int64_t(R2) + tex0,
+                    uint32_t(K * sizeof(T)), &full[st], pol);
+    }
+  };
+  if (threadIdx.x < 32)
+    for (int64_t li = 0; li < my_tiles && li < STAGES; ++li) issue(li);
+
+  Acc red;
+  const int t = int(threadIdx.x);
+  for (int64_t li = 0; li < my_tiles; ++li) {
+    const int st = int(li % STAGES);
+    mbar_wait(&full[st], uint32_t((li / STAGES) & 1));
+    const unsigned char* sb = smem_raw + size_t(st) * kStage;
+    const int64_t tile = int64_t(blockIdx.x) + li * gridDim.x;
+    const int64_t cell0 = tile * K;
+    const int64_t obj = cell0 / R2, tex0 = cell0 - obj * R2;
+    // zero the global accumulator tile (its words are in shared memory now)
+    {
+      uint4* g = reinterpret_cast<uint4*>(acc + cell0 * 2 * NCH);
+#pragma unroll
+      for (int u = 0; u < NCH * TPT; ++u) g[t + u * THREADS] = make_uint4(0u, 0u, 0u, 0u);
+    }
+#pragma unroll
+    for (int j = 0; j < TPT; ++j) {
+      const int tt = t + j * THREADS;
+      const long long* aw = reinterpret_cast<const long long*>(sb) + size_t(tt) * 2 * NCH;
+      const T* sv = reinterpret_cast<const T*>(sb + kAccBytes) + tt;
+#pragma unroll
+      for (int c = 0; c < NCH; ++c) {
+        const T P = T(double(aw[c]) / kFixScale);
+        const T D = T(double(aw[NCH + c]) / kFixScale);
+        T M2P = FIRST ? T(0) : sv[(0 * NCH + c) * K];
+        T M2D = s.cnt0 > 0 ? sv[(1 * NCH + c) * K] : T(0);
+        T ME = FIRST ? T(0) : sv[(2 * NCH + c) * K];
+        T VA = FIRST ? T(0) : sv[(3 * NCH + c) * K];
+        T AP = FIRST ? T(0) : sv[(4 * NCH + c) * K];
+        const T PI = sv[(5 * NCH + c) * K];
+        T PO, DL;
+        meta_elem<T, FIRST>(k, s, P, D, P, D, M2P, M2D, ME, VA, AP, PI, T(0), T(0), false, PO,
+                            DL, red);
+        const int64_t i = (obj * NCH + c) * int64_t(R2) + tex0 + tt;
+        __stcs(q.m2p + i, M2P);
+        if (s.active) __stcs(q.m2d + i, M2D);
+        __stcs(q.mean + i, ME);
+        __stcs(q.var + i, VA);
+        __stcs(q.ap + i, AP);
+        __stcs(q.pout + i, PO);
+      }
+    }
+    __syncthreads();  // every thread is done reading stage st
+    if (threadIdx.x < 32 && li + STAGES < my_tiles) {
+      fence_proxy_async_smem();
+      issue(li + STAGES);
+    }
+  }
+  grid_reduce4<THREADS>(red.partials(), partials, counter, [&](const ReducePartials& r) {
+    sc->ssn = r.ssn;
+    sc->changed = r.changed;
+    sc->loss = nan("");
+    sc->nonfinite = r.nonfinite;
+    sc->diff_count = s.cnt;
+    sc->diff_decay_pow = s.dpow;
+    sc->prop_decay_pow = s.ppow;
+    sc->ssn_used = s.ssn;
+  });
+}
+
+// Any shape / alignment / extras: one thread per parameter, the two
+// fixed-point words read (and zeroed) straight from the accumulator.
+template <class T, bool FIRST>
+__global__ void __launch_bounds__(kThreads)
+    meta_update_fixed_kernel(int64_t n, int nch, int R2, MetaK k, MetaPtrs<T> q,
+                             unsigned long long* __restrict__ acc, mg_update_scalars* sc,
+                             ReducePartials* partials, unsigned int* counter) {
+  const StepScal s = load_step_scalars(k, sc);
+  const bool has_target = q.target != nullptr;
+  Acc red;
+  for (int64_t i = int64_t(blockIdx.x) * kThreads + threadIdx.x; i < n;
+       i += int64_t(gridDim.x) * kThreads) {
+    const int64_t plane = i / R2, tex = i - plane * R2;
+    const int64_t obj = plane / nch, c = plane - obj * nch;
+    unsigned long long* w = acc + (obj * R2 + tex) * 2 * nch + c;
+    const T P = T(double((long long)w[0]) / kFixScale);
+    const T D = T(double((long long)w[nch]) / kFixScale);
+    w[0] = 0ull;
+    w[nch] = 0ull;
+    T M2P = FIRST ? T(0) : q.m2p[i];
+    T M2D = s.cnt0 > 0 ? q.m2d[i] : T(0);
+    T ME = FIRST ? T(0) : q.mean[i];
+    T VA = FIRST ? T(0) : q.var[i];
+    T AP = FIRST ? T(0) : q.ap[i];
+    const T PI = q.pin[i];
+    const T PP = k.diff_norm == MG_DIFF_NORM_PER_PARAM ? q.pprev[i] : T(0);
+    const T TG = has_target ? q.target[i] : T(0);
+    T PO, DL;
+    meta_elem<T, FIRST>(k, s, P, D, P, D, M2P, M2D, ME, VA, AP, PI, PP, TG, has_target, PO, DL,
+                        red);
+    q.m2p[i] = M2P;
+    if (s.active) q.m2d[i] = M2D;
+    q.mean[i] = ME;
+    q.var[i] = VA;
+    q.ap[i] = AP;
+    q.pout[i] = PO;
+    if (q.delta) q.delta[i] = DL;
+  }
+  grid_reduce4<kThreads>(red.partials(), partials, counter, [&](const ReducePartials& r) {
+    sc->ssn = r.ssn;
+    sc->changed = r.changed;
+    sc->loss = has_target ? r.loss : nan("");
+    sc->nonfinite = r.nonfinite;
+    sc->diff_count = s.cnt;
+    sc->diff_decay_pow = s.dpow;
+    sc->prop_decay_pow = s.ppow;
+    sc->ssn_used = s.ssn;
+  });
+}
+
 // ------------------------------------- shared-parameter fused step (peers)
 // One rank's part of a tile-sharded shared-parameter iteration (SURVEY.md
 // §8(e), configs 4/5 shape) as ONE kernel over NVLink peer memory: for its
@@ -729,6 +932,66 @@ AdamK advance_adam(mg_adam_scalars* s, int project, double proj_lo) {
   return k;
 }
 
+// fp32: MG_FIX_* (default 512 texels x 5 channels per tile, one per thread,
+// 2 stages of 102 KB, 1 CTA/SM: measured best of 9 shapes on configs[4],
+// with 256 x 1 x 2 stages x 2 CTAs and 128 x 2 x 2 x 2 within 0.3 %);
+// fp64: 128 texels, 3 stages (40 KB each), 1 CTA/SM
+#ifndef MG_FIX_THREADS
+#define MG_FIX_THREADS 512
+#endif
+#ifndef MG_FIX_TPT
+#define MG_FIX_TPT 1
+#endif
+#ifndef MG_FIX_STAGES
+#define MG_FIX_STAGES 2
+#endif
+#ifndef MG_FIX_MINB
+#define MG_FIX_MINB 1
+#endif
+template <class T, int NCH>
+struct FixShape {
+  static constexpr int threads = sizeof(T) == 4 ? MG_FIX_THREADS : 128,
+                       tpt = sizeof(T) == 4 ? MG_FIX_TPT : 1,
+                       stages = sizeof(T) == 4 ? MG_FIX_STAGES : 3,
+                       minb = sizeof(T) == 4 ? MG_FIX_MINB : 1;
+  static constexpr int texels = threads * tpt;
+};
+template <class T, int NCH>
+int launch_meta_update_fixed(mg_ctx* ctx, int64_t cells, int R2, const MetaK& k,
+                             const MetaPtrs<T>& q, bool first, unsigned long long* acc,
+                             mg_update_scalars* sc) {
+  using S = FixShape<T, NCH>;
+  const int64_t n = cells * NCH;
+  const bool tma_ok = !g_disable_tma && R2 % S::texels == 0 && k.diff_norm == MG_DIFF_NORM_GLOBAL &&
+                      !q.target && !q.delta && aligned16(acc) && aligned16(q.m2p) &&
+                      aligned16(q.m2d) && aligned16(q.mean) && aligned16(q.var) &&
+                      aligned16(q.ap) && aligned16(q.pin) && (R2 * sizeof(T)) % 16 == 0 &&
+                      cells / S::texels >= ctx->sm_count;
+  if (tma_ok) {
+    constexpr size_t smem = size_t(S::stages) * fix_stage_bytes<T, NCH, S::texels>();
+    const int64_t tiles = cells / S::texels;
+    const int64_t want = int64_t(ctx->sm_count) * S::minb;
+    const int grid = int(tiles < want ? tiles : want);
+    auto run = [&](auto kernel) {
+      cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+      kernel<<<grid, S::threads, smem, ctx->stream>>>(tiles, R2, k, q, acc, sc, ctx->partials,
+                                                      ctx->counter);
+    };
+    if (first)
+      run(meta_update_fixed_tma_kernel<T, true, NCH, S::threads, S::tpt, S::stages, S::minb>);
+    else
+      run(meta_update_fixed_tma_kernel<T, false, NCH, S::threads, S::tpt, S::stages, S::minb>);
+  } else {
+    const int grid = grid_for(ctx, n, kThreads, 8);
+    auto run = [&](auto kernel) {
+      kernel<<<grid, kThreads, 0, ctx->stream>>>(n, NCH, R2, k, q, acc, sc, ctx->partials,
+                                                 ctx->counter);
+    };
+    first ? run(meta_update_fixed_kernel<T, true>) : run(meta_update_fixed_kernel<T, false>);
+  }
+  MG_LAUNCH_CHECK(ctx);
+  return MG_OK;
+}
 }  // namespace
 }  // namespace mg
 
@@ -850,6 +1113,45 @@ int mg_meta_update(mg_ctx* ctx, int32_t dtype, int64_t n, const mg_meta_update_a
     return launch_meta_update<double>(ctx, n, k, q, a->first_step != 0, scalars);
   }
   return fail(MG_EINVAL, "mg_meta_update: unknown dtype");
+}
+
+// mg_meta_update with the sample pair in a texel-interleaved fixed-point
+// accumulator (see meta_update_fixed_tma_kernel); the accumulator is zeroed.
+int mg_meta_update_fixed(mg_ctx* ctx, int32_t dtype, int64_t cells, int32_t nch, int32_t r2,
+                         const mg_meta_update_args* a, void* accum, void* m2_prop, void* m2_diff,
+                         void* mean, void* var, void* alpha_prev, const void* params_in,
+                         void* params_out, mg_update_scalars* scalars, const mg_meta_extras* x) {
+  MG_NVTX("mg_meta_update_fixed");
+  if (!ctx || !a || !scalars) return fail(MG_EINVAL, "mg_meta_update_fixed: null argument");
+  if (cells < 0 || r2 < 1 || (nch != 4 && nch != 5) || cells % r2 != 0)
+    return fail(MG_EINVAL, "mg_meta_update_fixed: cells must be a multiple of r2 >= 1, nch 4 or 5");
+  if (cells == 0) return MG_OK;
+  if (!accum || !m2_prop || !m2_diff || !mean || !var || !alpha_prev || !params_in || !params_out)
+    return fail(MG_EINVAL, "mg_meta_update_fixed: null buffer");
+  if (x && (x->vprop || x->vdiff))
+    return fail(MG_EUNSUPPORTED, "mg_meta_update_fixed: no independent variance pair");
+  if (a->diff_norm == MG_DIFF_NORM_PER_PARAM && !(x && x->params_prev))
+    return fail(MG_EINVAL, "mg_meta_update_fixed: per-param diff norm needs params_prev");
+  if (!(a->meta.lr > 0.0)) return fail(MG_EINVAL, "MetaEstimator: lr must be positive");
+  if (a->prop_coef_device && !(a->beta_f > 0.0) && !a->prop_pow_advance)
+    return fail(MG_EINVAL, "mg_meta_update_fixed: prop_coef_device with beta_f = 0 needs prop_pow_advance");
+  const MetaK k = make_meta_k(a);
+  const mg_meta_extras none{};
+  const mg_meta_extras& e = x ? *x : none;
+  auto* acc = static_cast<unsigned long long*>(accum);
+  auto go = [&](auto tag) {
+    using T = decltype(tag);
+    MetaPtrs<T> q{nullptr, nullptr, nullptr, nullptr, (T*)m2_prop, (T*)m2_diff, (T*)mean,
+                  (T*)var, (T*)alpha_prev, (const T*)params_in, (T*)params_out,
+                  (const T*)e.params_prev, (const T*)e.target, (T*)e.delta_out};
+    return nch == 5 ? launch_meta_update_fixed<T, 5>(ctx, cells, r2, k, q, a->first_step != 0, acc,
+                                                     scalars)
+                    : launch_meta_update_fixed<T, 4>(ctx, cells, r2, k, q, a->first_step != 0, acc,
+                                                     scalars);
+  };
+  if (dtype == MG_F32) return go(float{});
+  if (dtype == MG_F64) return go(double{});
+  return fail(MG_EINVAL, "mg_meta_update_fixed: unknown dtype");
 }
 
 int mg_shared_meta_update(mg_ctx* ctx, int32_t dtype, int64_t shard_n, int64_t shard_lo,

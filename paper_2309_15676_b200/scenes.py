@@ -508,15 +508,22 @@ class MeshTextureProblem:
     def initial_params(self):
         return self.init.clone()
 
-    def sample_pair(self, now, prev, iteration: int, key: int, rows=None):
+    def sample_pair(self, now, prev, iteration: int, key: int, rows=None, finalize: bool = True):
+        """finalize=False: the pair stays in self.accum (texel-interleaved
+        fixed point) for FusedMetaUpdate.step_fixed; returns None."""
         r0, r1 = rows if rows is not None else (0, self.H)
-        prop, diff = torch.empty_like(now), torch.empty_like(now)
+        prop, diff = (torch.empty_like(now), torch.empty_like(now)) if finalize else (None, None)
         check(load().mg_meshscene_sample_pair(
             self.ctx.h, self.scene.h, _dtype_code(now), self.W, self.H,
             self.scene.view.ctypes.data_as(C.c_void_p), _p(self.target_img), _p(now.contiguous()),
             _p(prev.contiguous()), key, iteration, r0, r1, self.prop_paths, _p(self.accum),
             _p(prop), _p(diff), _p(self.loss_buf)))
-        return GradientSamplePair(prop, diff)
+        return GradientSamplePair(prop, diff) if finalize else None
+
+    def fixed_layout(self):
+        """(cells, channels, texels per object) of self.accum's pair."""
+        R2 = self.scene.R * self.scene.R
+        return self.dim() // self.scene.channels, self.scene.channels, R2
 
 
     def sample_pair_sharded(self, now, prev, iteration: int, key: int, rows, acc_ptrs,
@@ -569,10 +576,30 @@ class MeshTextureRun(QuadTextureRun):
     iteration; texture values projected to [0, 1] (meta)."""
 
     def __init__(self, problem, optimizer: str = "meta", lr: float = 0.01, seed: int = 0,
-                 replicate: int = 0, **kw):
+                 replicate: int = 0, fused: bool = True, **kw):
         if optimizer == "meta":
             kw.setdefault("project_hi", 1.0)
         super().__init__(problem, optimizer, lr, seed, replicate, **kw)
         # the loop ping-pongs its parameter buffers (prev at t+1 == now at t,
         # untouched in between): the scene may reuse prev's texel-major copy
         check(load().mg_meshscene_set_prev_reuse(problem.scene.h, 1))
+        # meta optimiser: the update consumes the fixed-point accumulator
+        # directly (mg_meta_update_fixed) — step() then returns None;
+        # fused=False keeps the planar pair (step() returns it)
+        self.fused = bool(fused) and optimizer == "meta"
+
+    def step(self):
+        if not self.fused:
+            return super().step()
+        self._step_at(self.t)
+        self.t += 1
+        return None
+
+    def _step_at(self, iteration: int):
+        if not self.fused:
+            return super()._step_at(iteration)
+        self.p.sample_pair(self.params, self.prev, iteration, self.key, finalize=False)
+        new = self.prev
+        cells, nch, r2 = self.p.fixed_layout()
+        self.upd.step_fixed(self.p.accum, cells, nch, r2, self.params, new)
+        self.prev, self.params = self.params, new

@@ -43,7 +43,7 @@ def test_tile_sharded_shared_param_step_matches_single_process(pg):
     from paper_2309_15676_b200.dist import SharedParamStep, tile_rows
     K = 8
     prob = _problem(api)
-    ref = api.MeshTextureRun(prob, "meta", lr=0.02)
+    ref = api.MeshTextureRun(prob, "meta", lr=0.02, fused=False)
     ref_traj = []
     for _ in range(K):
         ref.step()
@@ -69,7 +69,7 @@ def test_peer_memory_shared_step_tracks_single_process(pg):
     from paper_2309_15676_b200.dist import SharedParamStepP2P, tile_rows
     K = 8
     prob = _problem(api)
-    ref = api.MeshTextureRun(prob, "meta", lr=0.02)
+    ref = api.MeshTextureRun(prob, "meta", lr=0.02, fused=False)
     ref_traj = []
     for _ in range(K):
         ref.step()
@@ -133,7 +133,7 @@ def test_tiled_render_step_p2p_matches_single_process(pg):
     from paper_2309_15676_b200 import api
     from paper_2309_15676_b200.dist import TiledRenderStepP2P
     prob = _problem(api)
-    ref = api.MeshTextureRun(prob, "meta", lr=0.02)
+    ref = api.MeshTextureRun(prob, "meta", lr=0.02, fused=False)
     step = TiledRenderStepP2P(prob, lr=0.02)
     for t in range(6):
         ref.step()

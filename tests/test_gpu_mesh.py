@@ -278,11 +278,84 @@ def test_large_scene_builds_and_steps(api):
     prob = api.MeshLargeProblem(96, 96, 32, target_spp=2)
     info = prob.scene.info()
     assert info["triangles"] > 500_000 and info["params"] == 16 * 5 * 32 * 32
-    run = api.MeshTextureRun(prob, "meta", lr=0.005)
+    run = api.MeshTextureRun(prob, "meta", lr=0.005, fused=False)
     for _ in range(3):
         pair = run.step()
     assert torch.isfinite(pair.prop).all() and torch.isfinite(run.params).all()
     assert int(torch.count_nonzero(pair.prop)) > 1000
+
+
+def _ilv_to_planar(acc, nobj, nch, R2, dtype):
+    """texel-interleaved fixed-point accumulator -> planar (prop, diff), the
+    conversion of mesh_finalize_ilv_kernel: dtype(double(word) / 2^40)."""
+    a = acc.view(nobj, R2, 2, nch).double() / 2.0 ** 40
+    prop = a[:, :, 0, :].permute(0, 2, 1).reshape(-1).to(dtype)
+    diff = a[:, :, 1, :].permute(0, 2, 1).reshape(-1).to(dtype)
+    return prop, diff
+
+
+@pytest.mark.parametrize("dtype", [torch.float32, torch.float64])
+@pytest.mark.parametrize("nobj,nch,R", [(3, 4, 8), (2, 5, 128), (3, 4, 128), (1, 5, 20)])
+def test_fused_fixed_update_matches_finalize_plus_update(api, dtype, nobj, nch, R):
+    """mg_meta_update_fixed (the mesh pair consumed straight from the
+    texel-interleaved fixed-point accumulator; TMA tile form for R^2 a
+    multiple of 128 with >= 148 tiles, one thread per parameter otherwise)
+    equals finalize + mg_meta_update element for element, from the same
+    state, on the first, second and a later step (lazy init, diff-EMA start,
+    steady state), and leaves the accumulator zeroed."""
+    R2 = R * R
+    cells = nobj * R2
+    n = cells * nch
+    g = torch.Generator(device="cuda").manual_seed(nobj * 100 + R)
+    A = api.FusedMetaUpdate(n, dtype=dtype, lr=0.01, project_lo=0.0, project_hi=1.0)
+    B = api.FusedMetaUpdate(n, dtype=dtype, lr=0.01, project_lo=0.0, project_hi=1.0)
+    pin = torch.rand(n, generator=g, device="cuda", dtype=torch.float64).to(dtype)
+    names = ("m2_prop", "m2_diff", "mean", "var", "alpha_prev")
+    for step in range(4):
+        acc = torch.randint(-(1 << 44), 1 << 44, (2 * n,), generator=g, device="cuda",
+                            dtype=torch.int64)
+        if step == 0:
+            acc.view(cells, 2, nch)[:, 1, :] = 0  # no FD sample on the first step
+        prop, diff = _ilv_to_planar(acc, nobj, nch, R2, dtype)
+        # B starts from A's exact state (device scalars included)
+        for nm in names:
+            getattr(B, nm).copy_(getattr(A, nm))
+        B.scalars_buf.copy_(A.scalars_buf)
+        B.t, B.beta_f_pow = A.t, A.beta_f_pow
+        outA, outB = torch.empty_like(pin), torch.empty_like(pin)
+        A.step(prop, diff, pin, outA)
+        B.step_fixed(acc, cells, nch, R2, pin, outB)
+        torch.cuda.synchronize()
+        assert int(torch.count_nonzero(acc)) == 0, step
+        # bitwise (untouched state buffers may hold NaN patterns on step 0)
+        ib = torch.int32 if dtype == torch.float32 else torch.int64
+        assert torch.equal(outA.view(ib), outB.view(ib)), step
+        for nm in names:
+            assert torch.equal(getattr(A, nm).view(ib), getattr(B, nm).view(ib)), (step, nm)
+        sa, sb = A.scalars(), B.scalars()
+        assert abs(sa.ssn - sb.ssn) <= 1e-12 * abs(sa.ssn), step
+        assert sa.changed == sb.changed and sa.nonfinite == sb.nonfinite, step
+        pin = outA
+
+
+def test_fused_mesh_run_tracks_unfused(api):
+    """MeshTextureRun's default fused update (sample pair left in the
+    fixed-point accumulator) follows the finalize + update trajectory: the
+    first step bit for bit, later steps within fp32 rounding of the step-norm
+    reductions (summed in another order)."""
+    def make(fused):
+        prob = api.MeshTextureProblem(48, 40, 16, (8, 12), (10, 12), max_vertices=4,
+                                      target_spp=4, dtype=torch.float32, channels=5,
+                                      prop_paths=4)
+        return api.MeshTextureRun(prob, "meta", lr=0.01, fused=fused)
+    a, b = make(True), make(False)
+    for k in range(6):
+        a.step()
+        b.step()
+        if k == 0:
+            assert torch.equal(a.params, b.params)
+        torch.testing.assert_close(a.params, b.params, rtol=0, atol=1e-5)
+    assert torch.isfinite(a.params).all()
 
 
 @pytest.mark.parametrize("channels,nprop", [(4, 2), (5, 4)])
