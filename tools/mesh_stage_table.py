@@ -21,8 +21,8 @@ last = launches[gen[-1]:]
 
 
 def stage(name):
-    for s in ("tex_ilv", "wf_gen", "wf_isect", "wf_shade", "wf_shadow", "wf_scatter", "finalize",
-              "meta_update"):
+    for s in ("tex_ilv", "wf_gen", "wf_isect", "wf_shade", "wf_shadow", "wf_tail", "wf_scatter",
+              "finalize", "meta_update_fixed", "meta_update"):
         if s in name:
             return s
     return name.split("(")[0][-30:]
