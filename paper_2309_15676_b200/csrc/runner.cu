@@ -480,10 +480,23 @@ __device__ __forceinline__ void mbar_init_cta(uint64_t* bar, uint32_t count) {
 // o]), as after libstdc++'s seeding (random.tcc:328-343, first call
 // twists).
 constexpr int kChunkW = kMtM;                    // 156 words per chunk
-constexpr int kBatchChunks = 8;                  // chunks per emitted batch
-constexpr int kRingChunks = 2 * kBatchChunks;    // two batches in flight
+#ifndef MG_S1_BATCH_CHUNKS
+#define MG_S1_BATCH_CHUNKS 16
+#endif
+#ifndef MG_S1_RING_BATCHES
+#define MG_S1_RING_BATCHES 2
+#endif
+// 16-chunk batches: S1 kernel 1.283 -> 1.245 ms against 8 (half the
+// emitters' batch hand-offs); 4 or 8 batches in flight instead of 2: +-0
+// (the twister warp bounds the producer)
+constexpr int kBatchChunks = MG_S1_BATCH_CHUNKS;  // chunks per emitted batch
+constexpr int kRingBatches = MG_S1_RING_BATCHES;  // batches in flight
+constexpr int kRingChunks = kRingBatches * kBatchChunks;
 constexpr int kBatchWords = kBatchChunks * kChunkW;
-constexpr int kPublishBatches = 4;
+#ifndef MG_S1_PUBLISH_BATCHES
+#define MG_S1_PUBLISH_BATCHES 4
+#endif
+constexpr int kPublishBatches = MG_S1_PUBLISH_BATCHES;
 #ifndef MG_PRODUCER_PROBE
 #define MG_PRODUCER_PROBE 0  // 1: emitters skip their work, 2: the twister skips (probes)
 #endif
@@ -496,8 +509,8 @@ template <int CT>
 __device__ void produce_stream(uint64_t* ring, uint64_t* pbar, uint64_t seed, uint64_t rep,
                                int64_t total, double* out, unsigned long long* progress) {
   constexpr int kEmitThreads = CT - 32;
-  uint64_t* full = pbar;       // [2]: batch written (count 1)
-  uint64_t* empty = pbar + 2;  // [2]: batch emitted (count 1)
+  uint64_t* full = pbar;                 // [kRingBatches]: batch written (count 1)
+  uint64_t* empty = pbar + kRingBatches;  // [kRingBatches]: batch emitted (count 1)
   static_assert((kRingChunks & (kRingChunks - 1)) == 0, "power-of-two ring");
   auto slot = [&](int64_t chunk) {  // two's complement: chunk -1 -> slot 15
     return ring + (unsigned(chunk) & unsigned(kRingChunks - 1)) * kChunkW;
@@ -517,7 +530,7 @@ __device__ void produce_stream(uint64_t* ring, uint64_t* pbar, uint64_t seed, ui
       (i < kChunkW ? c2[i] : c1[i - kChunkW]) = w[0];
     }
     (void)w[1];
-    for (int q = 0; q < 4; ++q) mbar_init_cta(&pbar[q], 1);
+    for (int q = 0; q < 2 * kRingBatches; ++q) mbar_init_cta(&pbar[q], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
@@ -542,8 +555,9 @@ __device__ void produce_stream(uint64_t* ring, uint64_t* pbar, uint64_t seed, ui
       v1[q] = q < nw_l ? slot(-1)[t0 + q] : 0ull;
     }
     for (int64_t b = 0; b < batches; ++b) {
-      if (b >= 2) {  // the emitters are done with this half of the ring
-        while (!try_wait_cluster(&empty[b & 1], uint32_t(((b - 2) >> 1) & 1))) {
+      if (b >= kRingBatches) {  // the emitters are done with this part of the ring
+        while (!try_wait_cluster(&empty[b % kRingBatches],
+                                 uint32_t(((b - kRingBatches) / kRingBatches) & 1))) {
         }
       }
 #if MG_PRODUCER_PROBE != 2
@@ -571,13 +585,13 @@ __device__ void produce_stream(uint64_t* ring, uint64_t* pbar, uint64_t seed, ui
       __syncwarp();  // the batch's stores precede lane 0's release
       if (l == 0)
         asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(
-                         uint32_t(__cvta_generic_to_shared(&full[b & 1])))
+                         uint32_t(__cvta_generic_to_shared(&full[b % kRingBatches])))
                      : "memory");
     }
   } else {  // emitter warps
     const int e = threadIdx.x - 32;
     for (int64_t b = 0; b < batches; ++b) {
-      while (!try_wait_cluster(&full[b & 1], uint32_t((b >> 1) & 1))) {
+      while (!try_wait_cluster(&full[b % kRingBatches], uint32_t((b / kRingBatches) & 1))) {
       }
       const int64_t base = b * kBatchWords;
       MG_DCHECK(b >= 0 && (base < total || total == 0));
@@ -590,7 +604,7 @@ __device__ void produce_stream(uint64_t* ring, uint64_t* pbar, uint64_t seed, ui
       named_sync(1, kEmitThreads);
       if (e == 0) {
         asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(
-                         uint32_t(__cvta_generic_to_shared(&empty[b & 1])))
+                         uint32_t(__cvta_generic_to_shared(&empty[b % kRingBatches])))
                      : "memory");
         // publish every kPublishBatches batches (and the last): the release
         // store orders the emitters' stores, which the named barrier made
@@ -612,7 +626,7 @@ template <class T, int CT, int PPT>
 __global__ void __launch_bounds__(CT) run_cluster_kernel(RunK<T> k, double* ubuf_all,
                                                                unsigned long long* progress_all) {
   __shared__ uint64_t ring[kRingChunks * kChunkW];
-  __shared__ __align__(8) uint64_t pbar[4];
+  __shared__ __align__(8) uint64_t pbar[2 * kRingBatches];
   __shared__ double sw[CT / 32];
   __shared__ double xch[2][kClusterMax][4];  // [parity][source rank][sum]
   __shared__ double wsum[CT / 32][4];
@@ -895,7 +909,7 @@ __global__ void __launch_bounds__(CT) mt_stream_probe_kernel(uint64_t seed, uint
                                                              int64_t total, double* out,
                                                              unsigned long long* progress) {
   __shared__ uint64_t ring[kRingChunks * kChunkW];
-  __shared__ __align__(8) uint64_t pbar[4];
+  __shared__ __align__(8) uint64_t pbar[2 * kRingBatches];
   produce_stream<CT>(ring, pbar, seed, rep, total, out, progress);
 }
 
