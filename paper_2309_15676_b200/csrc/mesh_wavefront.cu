@@ -815,7 +815,19 @@ __device__ __noinline__ void wf_scatter(const WF<T>& w, int p, const T wt[3], in
   T Q[3];
 #pragma unroll
   for (int c = 0; c < 3; ++c) Q[c] = w.E[size_t(c) * w.P + p];
-  for (int v = w.nv[p] - 1; v >= 0; --v) {
+  // the warp's lanes walk their vertices in lockstep by vertex index (lane
+  // idle while v >= its own count): every field load of an iteration reads
+  // one [v][field] plane, coalesced across the warp's neighbouring paths.
+  // Walking each lane from its own last vertex put lanes of one iteration
+  // in different planes (ncu: 57 % of the scatter's L2 sectors excessive).
+  // Same per-lane operation order, same warp iteration count.
+  const int nvp = w.nv[p];
+#ifndef MG_SCATTER_LOCKSTEP
+#define MG_SCATTER_LOCKSTEP 1
+#endif
+  const int vtop = MG_SCATTER_LOCKSTEP ? __reduce_max_sync(__activemask(), unsigned(nvp)) : nvp;
+  for (int v = vtop - 1; v >= 0; --v) {
+    if (v >= nvp) continue;
     const AccCell<NCH, ILV> cell(acc, w.vbase[size_t(v) * w.PS + p], R2);
     const bool ne = w.vnee[size_t(v) * w.PS + p], bn = w.vbnc[size_t(v) * w.PS + p];
     T X[3][NCH - 2], g[NCH];
@@ -845,7 +857,19 @@ __device__ __noinline__ void wf_scatter_a(const WF<T>& w, int p, const T wt[3], 
     Q0[c] = w.E[size_t(c) * w.P + p];
     Q1[c] = w.E[size_t(3 + c) * w.P + p];
   }
-  for (int v = w.nv[p] - 1; v >= 0; --v) {
+  // the warp's lanes walk their vertices in lockstep by vertex index (lane
+  // idle while v >= its own count): every field load of an iteration reads
+  // one [v][field] plane, coalesced across the warp's neighbouring paths.
+  // Walking each lane from its own last vertex put lanes of one iteration
+  // in different planes (ncu: 57 % of the scatter's L2 sectors excessive).
+  // Same per-lane operation order, same warp iteration count.
+  const int nvp = w.nv[p];
+#ifndef MG_SCATTER_LOCKSTEP
+#define MG_SCATTER_LOCKSTEP 1
+#endif
+  const int vtop = MG_SCATTER_LOCKSTEP ? __reduce_max_sync(__activemask(), unsigned(nvp)) : nvp;
+  for (int v = vtop - 1; v >= 0; --v) {
+    if (v >= nvp) continue;
     const AccCell<NCH, ILV> cell(acc, w.vbase[size_t(v) * w.PS + p], R2);
     const bool ne = w.vnee[size_t(v) * w.PS + p], bn = w.vbnc[size_t(v) * w.PS + p];
     T X[3][NCH - 2], g[NCH];
@@ -875,8 +899,11 @@ constexpr int kMaxProp = 8;
 
 // 4 CTAs/SM (<= 128 registers): measured 2 % faster on configs[4] than the
 // unconstrained 168-227 registers
+#ifndef MG_SCATTER_BLOCKS
+#define MG_SCATTER_BLOCKS 4
+#endif
 template <class T, int NCH, bool ILV>
-__global__ void __launch_bounds__(kMThreads, 4)
+__global__ void __launch_bounds__(kMThreads, MG_SCATTER_BLOCKS)
     wf_scatter_kernel(MeshK q, WF<T> w, const T* __restrict__ target_img, AccTable acc,
                       ReducePartials* partials, unsigned int* counter, double* loss_out,
                       bool agg) {
