@@ -508,7 +508,16 @@ __device__ __forceinline__ void named_sync(int id, int n) {
 template <int CT>
 __device__ void produce_stream(uint64_t* ring, uint64_t* pbar, uint64_t seed, uint64_t rep,
                                int64_t total, double* out, unsigned long long* progress) {
-  constexpr int kEmitThreads = CT - 32;
+  // Warps share an SM sub-partition's scheduler by warp index mod 4.  The
+  // emitters spin on their mbarriers and would take issue slots from the
+  // twister warp (warp 0), which bounds the whole run: with MG_S1_ISOLATE
+  // the warps 4, 8, ... of the twister's sub-partition stay idle and the
+  // emitters are the warps with index mod 4 != 0.
+#ifndef MG_S1_ISOLATE
+#define MG_S1_ISOLATE 1
+#endif
+  constexpr bool kIsolate = MG_S1_ISOLATE != 0;
+  constexpr int kEmitThreads = kIsolate ? (CT / 32 - CT / 128) * 32 : CT - 32;
   uint64_t* full = pbar;                 // [kRingBatches]: batch written (count 1)
   uint64_t* empty = pbar + kRingBatches;  // [kRingBatches]: batch emitted (count 1)
   static_assert((kRingChunks & (kRingChunks - 1)) == 0, "power-of-two ring");
@@ -588,8 +597,9 @@ __device__ void produce_stream(uint64_t* ring, uint64_t* pbar, uint64_t seed, ui
                          uint32_t(__cvta_generic_to_shared(&full[b % kRingBatches])))
                      : "memory");
     }
-  } else {  // emitter warps
-    const int e = threadIdx.x - 32;
+  } else if (!kIsolate || ((threadIdx.x >> 5) & 3) != 0) {  // emitter warps
+    const int wv = int(threadIdx.x >> 5);
+    const int e = kIsolate ? (wv - wv / 4 - 1) * 32 + int(threadIdx.x & 31) : int(threadIdx.x) - 32;
     for (int64_t b = 0; b < batches; ++b) {
       while (!try_wait_cluster(&full[b % kRingBatches], uint32_t((b / kRingBatches) & 1))) {
       }
