@@ -135,8 +135,10 @@ int mg_ctx_create(int device, void* stream, mg_ctx** out);
 int mg_ctx_destroy(mg_ctx* ctx);
 int mg_ctx_synchronize(mg_ctx* ctx);
 /* Probe (tools/s1_producer_probe.py): the cluster runner's mt19937_64
- * producer alone, one CTA streaming `total` uniform() draws of
- * Rng::stream(seed, rep) into out (device doubles); progress = device u64. */
+ * producer alone, one CTA streaming the `total` raw (untempered) engine state
+ * words behind Rng::stream(seed, rep)'s first `total` outputs into out
+ * (device u64, viewed as double*: output o = temper(out[o])); progress =
+ * device u64. */
 int mg_mt_stream_probe(mg_ctx* ctx, uint64_t seed, uint64_t rep, int64_t total, double* out,
                        unsigned long long* progress);
 /* Device-check build (libmgcuda_debug.so, MG_DEBUG_CHECKS) only: trips one

@@ -468,79 +468,70 @@ __device__ __forceinline__ void mbar_init_cta(uint64_t* bar, uint32_t count) {
                "r"(count) : "memory");
 }
 
-// The producer: the replicate's std::mt19937_64 stream written to `out`
-// as uniform() doubles (rng.hpp:28), `total` of them, with `progress`
-// (draws published) advanced by release stores.  The state recurrence
-// w[j] = w[j-156] ^ mag(w[j-312], w[j-311]) (the twist of
-// random.tcc:399, sequential form) advances in chunks of 156 words, each
-// depending only on the two chunks before it: warp 0 computes the chunks
-// (5 words per lane, one __syncwarp per chunk) into a shared ring while
-// warps 1..7 temper, convert and store finished batches of 8 chunks,
-// double-buffered through two mbarrier pairs.  Output o is temper(w[312 +
-// o]), as after libstdc++'s seeding (random.tcc:328-343, first call
-// twists).
+// The producer: the replicate's std::mt19937_64 state words w[312 + o]
+// (o = 0 .. total-1; output o of the engine is temper(w[312 + o]), as after
+// libstdc++'s seeding, random.tcc:328-343, whose first call twists) written
+// RAW to `out`; the consumers temper and convert them (rng.hpp:28) as they
+// read them.  The state recurrence w[j] = w[j-156] ^ mag(w[j-312],
+// w[j-311]) (the twist of random.tcc:399 in sequential form) advances in
+// chunks of 156 words, each depending only on the two chunks before it:
+// warp 0 computes the chunks (5 words per lane, registers only, one
+// __syncwarp per chunk) and stores them straight to global memory; after
+// every batch of kBatchChunks chunks its lane 0 publishes the batch count in
+// shared memory (release, CTA scope) and warp 1 turns that into the global
+// progress word the consumers acquire (release, GPU scope, every
+// kPublishBatches batches), so no fence ever stalls the twister.  The
+// producer CTA's other warps idle: the twister owns its SM sub-partition's
+// issue slots (warps share a scheduler by index mod 4; warps spinning there
+// cost it half its rate).
 constexpr int kChunkW = kMtM;                    // 156 words per chunk
 #ifndef MG_S1_BATCH_CHUNKS
 #define MG_S1_BATCH_CHUNKS 16
 #endif
-#ifndef MG_S1_RING_BATCHES
-#define MG_S1_RING_BATCHES 2
-#endif
-// 16-chunk batches: S1 kernel 1.283 -> 1.245 ms against 8 (half the
-// emitters' batch hand-offs); 4 or 8 batches in flight instead of 2: +-0
-// (the twister warp bounds the producer)
-constexpr int kBatchChunks = MG_S1_BATCH_CHUNKS;  // chunks per emitted batch
-constexpr int kRingBatches = MG_S1_RING_BATCHES;  // batches in flight
-constexpr int kRingChunks = kRingBatches * kBatchChunks;
+constexpr int kBatchChunks = MG_S1_BATCH_CHUNKS;  // chunks per published batch
 constexpr int kBatchWords = kBatchChunks * kChunkW;
 #ifndef MG_S1_PUBLISH_BATCHES
 #define MG_S1_PUBLISH_BATCHES 4
 #endif
 constexpr int kPublishBatches = MG_S1_PUBLISH_BATCHES;
 #ifndef MG_PRODUCER_PROBE
-#define MG_PRODUCER_PROBE 0  // 1: emitters skip their work, 2: the twister skips (probes)
+#define MG_PRODUCER_PROBE 0  // 2: the twister skips its arithmetic (probe builds)
 #endif
 
-__device__ __forceinline__ void named_sync(int id, int n) {
-  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+__device__ __forceinline__ void st_release_cta_u32(unsigned int* p, unsigned int v) {
+  asm volatile("st.release.cta.shared::cta.u32 [%0], %1;" ::"r"(uint32_t(__cvta_generic_to_shared(p))),
+               "r"(v)
+               : "memory");
+}
+__device__ __forceinline__ unsigned int ld_acquire_cta_u32(const unsigned int* p) {
+  unsigned int v;
+  asm volatile("ld.acquire.cta.shared::cta.u32 %0, [%1];"
+               : "=r"(v)
+               : "r"(uint32_t(__cvta_generic_to_shared(p)))
+               : "memory");
+  return v;
 }
 
+// words the producer writes for `total` outputs: whole batches
+__host__ __device__ constexpr int64_t raw_stream_words(int64_t total) {
+  return (total + kBatchWords - 1) / kBatchWords * kBatchWords;
+}
+
+// seedbuf: kMtN shared words; s_done: shared batch counter.  out: at least
+// raw_stream_words(total) words.
 template <int CT>
-__device__ void produce_stream(uint64_t* ring, uint64_t* pbar, uint64_t seed, uint64_t rep,
-                               int64_t total, double* out, unsigned long long* progress) {
-  // Warps share an SM sub-partition's scheduler by warp index mod 4.  The
-  // emitters spin on their mbarriers and would take issue slots from the
-  // twister warp (warp 0), which bounds the whole run: with MG_S1_ISOLATE
-  // the warps 4, 8, ... of the twister's sub-partition stay idle and the
-  // emitters are the warps with index mod 4 != 0.
-#ifndef MG_S1_ISOLATE
-#define MG_S1_ISOLATE 1
-#endif
-  constexpr bool kIsolate = MG_S1_ISOLATE != 0;
-  constexpr int kEmitThreads = kIsolate ? (CT / 32 - CT / 128) * 32 : CT - 32;
-  uint64_t* full = pbar;                 // [kRingBatches]: batch written (count 1)
-  uint64_t* empty = pbar + kRingBatches;  // [kRingBatches]: batch emitted (count 1)
-  static_assert((kRingChunks & (kRingChunks - 1)) == 0, "power-of-two ring");
-  auto slot = [&](int64_t chunk) {  // two's complement: chunk -1 -> slot 15
-    return ring + (unsigned(chunk) & unsigned(kRingChunks - 1)) * kChunkW;
-  };
+__device__ void produce_raw(uint64_t* seedbuf, unsigned int* s_done, uint64_t seed, uint64_t rep,
+                            int64_t total, uint64_t* out, unsigned long long* progress) {
   if (threadIdx.x == 0) {
     // Rng::stream(seed, rep) (rng.hpp:23-25): w[0..311] = chunks -2, -1
-    uint64_t w[2];
-    const uint64_t s0 = mg_mix64_dev(mg_mix64_dev(seed) ^ (rep + 0x51ed2701e35f3a6dULL));
-    uint64_t* c2 = slot(-2);
-    uint64_t* c1 = slot(-1);
-    w[0] = s0;
-    c2[0] = s0;
+    uint64_t x = mg_mix64_dev(mg_mix64_dev(seed) ^ (rep + 0x51ed2701e35f3a6dULL));
+    seedbuf[0] = x;
     for (int i = 1; i < kMtN; ++i) {
-      uint64_t x = w[0];
       x ^= x >> 62;
-      w[0] = 6364136223846793005ULL * x + static_cast<uint64_t>(i);
-      (i < kChunkW ? c2[i] : c1[i - kChunkW]) = w[0];
+      x = 6364136223846793005ULL * x + static_cast<uint64_t>(i);
+      seedbuf[i] = x;
     }
-    (void)w[1];
-    for (int q = 0; q < 2 * kRingBatches; ++q) mbar_init_cta(&pbar[q], 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    *s_done = 0u;
   }
   __syncthreads();
   const int64_t chunks = (total + kChunkW - 1) / kChunkW;
@@ -552,29 +543,22 @@ __device__ void produce_stream(uint64_t* ring, uint64_t* pbar, uint64_t seed, ui
     // and k-2 and word t+1 of chunk k-2 — in-lane except for the last word
     // of a lane (lane l+1's first word, shuffled from two chunks back, off
     // the critical path) and t = 155 (word 0 of chunk k-1, one shuffle).
-    // No shared-memory round trip between chunks; each chunk is stored to
-    // the ring for the emitters.
     const int l = threadIdx.x;
     const int t0 = 5 * l;
     const int nw_l = l < 31 ? 5 : 1;  // words owned (lane 31: t = 155)
     uint64_t v1[5], v2[5];            // chunks k-1, k-2
 #pragma unroll
     for (int q = 0; q < 5; ++q) {
-      v2[q] = q < nw_l ? slot(-2)[t0 + q] : 0ull;
-      v1[q] = q < nw_l ? slot(-1)[t0 + q] : 0ull;
+      v2[q] = q < nw_l ? seedbuf[t0 + q] : 0ull;
+      v1[q] = q < nw_l ? seedbuf[kChunkW + t0 + q] : 0ull;
     }
+    uint64_t* wp = out + t0;  // this lane's words of the current chunk
     for (int64_t b = 0; b < batches; ++b) {
-      if (b >= kRingBatches) {  // the emitters are done with this part of the ring
-        while (!try_wait_cluster(&empty[b % kRingBatches],
-                                 uint32_t(((b - kRingBatches) / kRingBatches) & 1))) {
-        }
-      }
 #if MG_PRODUCER_PROBE != 2
       // unrolled: the two-chunk register rotation resolves at compile time
       // (as a loop it cost ~20 moves per chunk)
 #pragma unroll
       for (int kc = 0; kc < kBatchChunks; ++kc) {
-        uint64_t* nw = slot(b * kBatchChunks + kc);
         // word t0 + 5 of chunk k-2 (lane l+1's first) and word 0 of chunk k-1
         const uint64_t right = __shfl_down_sync(0xffffffffu, v2[0], 1);
         const uint64_t head1 = __shfl_sync(0xffffffffu, v1[0], 0);
@@ -585,48 +569,28 @@ __device__ void produce_stream(uint64_t* ring, uint64_t* pbar, uint64_t seed, ui
         if (l == 31) v0[0] = v1[0] ^ mt_mag(v2[0], head1);  // t = 155
 #pragma unroll
         for (int q = 0; q < 5; ++q) {
-          if (q < nw_l) nw[t0 + q] = v0[q];
+          if (q < nw_l) wp[q] = v0[q];  // out holds whole batches (padded)
           v2[q] = v1[q];
           v1[q] = v0[q];
         }
+        wp += kChunkW;
       }
 #endif
       __syncwarp();  // the batch's stores precede lane 0's release
-      if (l == 0)
-        asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(
-                         uint32_t(__cvta_generic_to_shared(&full[b % kRingBatches])))
-                     : "memory");
+      if (l == 0) st_release_cta_u32(s_done, unsigned(b + 1));
     }
-  } else if (!kIsolate || ((threadIdx.x >> 5) & 3) != 0) {  // emitter warps
-    const int wv = int(threadIdx.x >> 5);
-    const int e = kIsolate ? (wv - wv / 4 - 1) * 32 + int(threadIdx.x & 31) : int(threadIdx.x) - 32;
-    for (int64_t b = 0; b < batches; ++b) {
-      while (!try_wait_cluster(&full[b % kRingBatches], uint32_t((b / kRingBatches) & 1))) {
+  } else if (threadIdx.x == 32) {  // publisher (warp 1, another sub-partition)
+    int64_t pub = 0;
+    while (pub < batches) {
+      const int64_t want = pub + kPublishBatches < batches ? pub + kPublishBatches : batches;
+      unsigned int done;
+      while ((done = ld_acquire_cta_u32(s_done)) < unsigned(want)) {
       }
-      const int64_t base = b * kBatchWords;
-      MG_DCHECK(b >= 0 && (base < total || total == 0));
-#if MG_PRODUCER_PROBE != 1
-      for (int o = e; o < kBatchWords; o += kEmitThreads) {
-        const int64_t g = base + o;
-        if (g < total) out[g] = mt_uniform(mt_temper(slot(b * kBatchChunks + o / kChunkW)[o % kChunkW]));
-      }
-#endif
-      named_sync(1, kEmitThreads);
-      if (e == 0) {
-        asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(
-                         uint32_t(__cvta_generic_to_shared(&empty[b % kRingBatches])))
-                     : "memory");
-        // publish every kPublishBatches batches (and the last): the release
-        // store orders the emitters' stores, which the named barrier made
-        // happen-before it; a fence per batch serialised the emitters
-        // (each batch waited for the previous publication's MEMBAR)
-        if ((b + 1) % kPublishBatches == 0 || b + 1 == batches) {
-          const int64_t done = base + kBatchWords < total ? base + kBatchWords : total;
-          asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(progress),
-                       "l"((unsigned long long)done)
-                       : "memory");
-        }
-      }
+      pub = done;
+      const int64_t words = pub * kBatchWords < total ? pub * kBatchWords : total;
+      asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(progress),
+                   "l"((unsigned long long)words)
+                   : "memory");
     }
   }
 }
@@ -635,8 +599,8 @@ __device__ void produce_stream(uint64_t* ring, uint64_t* pbar, uint64_t seed, ui
 template <class T, int CT, int PPT>
 __global__ void __launch_bounds__(CT) run_cluster_kernel(RunK<T> k, double* ubuf_all,
                                                                unsigned long long* progress_all) {
-  __shared__ uint64_t ring[kRingChunks * kChunkW];
-  __shared__ __align__(8) uint64_t pbar[2 * kRingBatches];
+  __shared__ uint64_t seedbuf[kMtN];
+  __shared__ unsigned int s_done;
   __shared__ double sw[CT / 32];
   __shared__ double xch[2][kClusterMax][4];  // [parity][source rank][sum]
   __shared__ double wsum[CT / 32][4];
@@ -649,7 +613,7 @@ __global__ void __launch_bounds__(CT) run_cluster_kernel(RunK<T> k, double* ubuf
   const int r = blockIdx.x / NC;  // replicate within the launch
   const int d = k.dim, iters = c.iterations, spp = c.spp;
   const int64_t D = k.D;
-  double* ubuf = ubuf_all + size_t(r) * iters * D;
+  double* ubuf = ubuf_all + size_t(r) * raw_stream_words(int64_t(iters) * D);
   unsigned long long* progress = progress_all + r;
   if (threadIdx.x == 0) {
     s_seen = 0;
@@ -661,8 +625,8 @@ __global__ void __launch_bounds__(CT) run_cluster_kernel(RunK<T> k, double* ubuf
   cluster_sync_all();  // every CTA of the cluster is running and initialised
 
   if (rank == 0) {  // ------------------------------------------ producer
-    produce_stream<CT>(ring, pbar, c.seed, uint64_t(k.rep_begin + r), int64_t(iters) * D, ubuf,
-                   progress);
+    produce_raw<CT>(seedbuf, &s_done, c.seed, uint64_t(k.rep_begin + r), int64_t(iters) * D,
+                    reinterpret_cast<uint64_t*>(ubuf), progress);
     cluster_sync_all();
     return;
   }
@@ -773,7 +737,8 @@ __global__ void __launch_bounds__(CT) run_cluster_kernel(RunK<T> k, double* ubuf
         __syncthreads();
       }
     }
-    const double* u = ubuf + size_t(i) * D;
+    // raw engine words: temper + uniform() here (rng.hpp:28)
+    const unsigned long long* u = reinterpret_cast<const unsigned long long*>(ubuf) + size_t(i) * D;
     const bool two_point = use_meta && !same_pp;  // :129
     draws += D;
     evals += D * (two_point ? 2 : 1);
@@ -807,8 +772,9 @@ __global__ void __launch_bounds__(CT) run_cluster_kernel(RunK<T> k, double* ubuf
       MG_DCHECK(j < hi && hi <= d);
       // sample_pair (problems.cpp:197-217)
       T cross, mb;
-      const double* uj = u + size_t(j) * spp;
-      minirender_terms_fn<T>(bj[q], spp, [&](int s) { return __ldcg(uj + s); }, cross, mb);
+      const unsigned long long* uj = u + size_t(j) * spp;
+      minirender_terms_fn<T>(
+          bj[q], spp, [&](int s) { return mt_uniform(mt_temper(__ldcg(uj + s))); }, cross, mb);
       const T a = p[q];
       const T prop = (T(2) * a) * cross - (T(2) * T(tj[q])) * mb;
       const T diff = same ? T(0) : (T(2) * (a - (use_meta ? pv[q] : a))) * cross;
@@ -918,9 +884,9 @@ template <int CT>
 __global__ void __launch_bounds__(CT) mt_stream_probe_kernel(uint64_t seed, uint64_t rep,
                                                              int64_t total, double* out,
                                                              unsigned long long* progress) {
-  __shared__ uint64_t ring[kRingChunks * kChunkW];
-  __shared__ __align__(8) uint64_t pbar[2 * kRingBatches];
-  produce_stream<CT>(ring, pbar, seed, rep, total, out, progress);
+  __shared__ uint64_t seedbuf[kMtN];
+  __shared__ unsigned int s_done;
+  produce_raw<CT>(seedbuf, &s_done, seed, rep, total, reinterpret_cast<uint64_t*>(out), progress);
 }
 
 // Shape of the one-replicate-per-cluster runner: cluster size (16 CTAs, 15
@@ -1183,7 +1149,7 @@ int run_replicates(mg_ctx* ctx, const mg_experiment_config* cfg, int rep_begin, 
       sizeof(double) * size_t(R) * iters * D <= (size_t(1) << 30))
     cs = cluster_shape<T>(ctx, d, R);
   if (cs.nc > 0) {
-    double* ubuf = (double*)dalloc(sizeof(double) * size_t(R) * iters * D);
+    double* ubuf = (double*)dalloc(sizeof(double) * size_t(R) * raw_stream_words(int64_t(iters) * D));
     auto* progress = (unsigned long long*)dalloc(sizeof(unsigned long long) * size_t(R));
     if (!ubuf || !progress) {
       cleanup();
@@ -1252,8 +1218,13 @@ using namespace mg;
 extern "C" int mg_mt_stream_probe(mg_ctx* ctx, uint64_t seed, uint64_t rep, int64_t total,
                                   double* out, unsigned long long* progress) {
   if (!ctx || !out || !progress || total < 1) return fail(MG_EINVAL, "mg_mt_stream_probe: bad arguments");
-  mt_stream_probe_kernel<512><<<1, 512, 0, ctx->stream>>>(seed, rep, total, out, progress);
+  // the producer writes whole batches: stream into scratch, copy `total`
+  double* scratch = static_cast<double*>(ctx_scratch(ctx, sizeof(double) * raw_stream_words(total)));
+  if (!scratch) return fail(MG_ENOMEM, "mg_mt_stream_probe: scratch allocation failed");
+  mt_stream_probe_kernel<512><<<1, 512, 0, ctx->stream>>>(seed, rep, total, scratch, progress);
   MG_LAUNCH_CHECK(ctx);
+  MG_CUDA_TRY(cudaMemcpyAsync(out, scratch, sizeof(double) * total, cudaMemcpyDeviceToDevice,
+                              ctx->stream));
   return MG_OK;
 }
 
