@@ -927,7 +927,10 @@ int cluster_query(mg_ctx* ctx, int nc, int R) {
 
 template <class T>
 ClusterShape cluster_shape_query(mg_ctx* ctx, int d, int R) {
-  for (int nc : {16, 8}) {
+#ifndef MG_S1_NC_FIRST
+#define MG_S1_NC_FIRST 16
+#endif
+  for (int nc : {MG_S1_NC_FIRST, 16, 8}) {
     if (int64_t(R) * nc > int64_t(ctx->sm_count)) continue;
     if (d <= (nc - 1) * 512 * 2 && cluster_query<T, 512, 2>(ctx, nc, R) >= R) return {nc, 512};
     if (d <= (nc - 1) * 256 * 4 && cluster_query<T, 256, 4>(ctx, nc, R) >= R) return {nc, 256};
