@@ -175,8 +175,19 @@ __device__ __forceinline__ void bsdf(const T* th, const V3<T>& n, const V3<T>& w
 // channel c depends on no other channel's base colour, so the other
 // entries of d L_c / d theta are exactly zero and are not carried).
 constexpr int kND = 3;
+// inlined into the path kernels (out of line: an ABI call with a 304-byte
+// stack frame; inlined fp32 141 registers, no spills): configs[2] fp32
+// 0.175 -> 0.153 ms, fp64 0.299 -> 0.235 ms per iteration
+#ifndef MG_HELIX_INLINE
+#define MG_HELIX_INLINE 1
+#endif
+#if MG_HELIX_INLINE
+#define MG_HELIX_TRACE __device__ __forceinline__
+#else
+#define MG_HELIX_TRACE __device__ __noinline__
+#endif
 template <class T, int NSETS>
-__device__ __noinline__ void trace(const HelixK& q, const T* __restrict__ sph, const T (&th)[2][kNP], int px,
+MG_HELIX_TRACE void trace(const HelixK& q, const T* __restrict__ sph, const T (&th)[2][kNP], int px,
                       int py, uint32_t path, T L[NSETS][3], T dL[NSETS][3][kND]) {
   const uint32_t pix = uint32_t(py * q.W + px);
   double u[4];
