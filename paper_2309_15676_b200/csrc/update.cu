@@ -42,10 +42,13 @@ extern bool g_mesh_smem_stack;
 extern bool g_mesh_qnodes;
 extern bool g_helix_split;
 extern int g_bvh_leaf;
-// -1: per-dtype default measured on B200 (tools/sweep_update_variants.py,
-// profiles/r01_sweep_update_variants_*): fp32 -> variant 6 (2 CTAs/SM x 192
-// threads, 4 stages of 3 KB tiles: the fp32 body is issue-heavy, so it wants
-// both warps and depth), fp64 -> variant 0 (1 CTA/SM x 256 thr, 4 stages).
+// -1: per-dtype default measured on B200: fp32 -> variant 8 (1 CTA/SM x 640
+// threads, 2 stages of 10 KB tiles: 20 warps to issue the body and ~180 KB
+// in flight; interleaved A/B over 30 blocks of 20 launches,
+// tools/ab_update_variants.py: 2.31 ms at 2^28 against 2.52 for round 1's
+// variant 6, whose pick came from a sequential sweep that the launch-to-
+// launch drift of HBM biased), fp64 -> variant 9 (1 CTA/SM x 512 threads,
+// 2 stages of 8 KB tiles: 4.63 ms against 5.4-5.7 for variant 0).
 int g_tma_variant = -1;
 namespace {
 
@@ -150,13 +153,13 @@ __host__ __device__ constexpr TmaVariant tma_variant(int i) {
   return i == 0 ? TmaVariant{256, 4, 1}
        : i == 1 ? TmaVariant{256, 3, 2}
        : i == 2 ? TmaVariant{512, 3, 1}
-       : i == 3 ? TmaVariant{128, 3, 4}
+       : i == 3 ? TmaVariant{768, 2, 1}
        : i == 4 ? TmaVariant{256, 2, 3}
        : i == 5 ? TmaVariant{160, 5, 2}
        : i == 6 ? TmaVariant{192, 4, 2}
        : i == 7 ? TmaVariant{224, 3, 2}
-       : i == 8 ? TmaVariant{96, 4, 4}
-                : TmaVariant{192, 3, 2};
+       : i == 8 ? TmaVariant{640, 2, 1}
+                : TmaVariant{512, 2, 1};
 }
 constexpr int kNumTmaVariants = 10;
 
@@ -228,10 +231,20 @@ __global__ void __launch_bounds__(kTmaThreads, kMinBlocks)
     const Pack<T> PI = ld_plain(sb + 7 * TILE);
     if (has_target) TG = ld_plain(sb + 8 * TILE);
 #pragma unroll
-    for (int w = 0; w < W; ++w)
+    for (int w = 0; w < W; ++w) {
+#if MG_TMA_NOMATH  // probe builds only: the same traffic without the arithmetic
+      M2P.v[w] += P.v[w];
+      M2D.v[w] += D.v[w];
+      ME.v[w] += P.v[w];
+      VA.v[w] += D.v[w];
+      AP.v[w] += P.v[w];
+      PO.v[w] = PI.v[w] + D.v[w];
+#else
       meta_elem<T, FIRST>(k, s, P.v[w], D.v[w], P.v[w], D.v[w], M2P.v[w], M2D.v[w], ME.v[w],
                           VA.v[w], AP.v[w], PI.v[w], T(0), TG.v[w], has_target, PO.v[w], DL.v[w],
                           acc);
+#endif
+    }
     const int64_t b = (int64_t(blockIdx.x) + li * gridDim.x) * TILE + e;
     // streaming (evict-first) stores: the state is re-read only next step,
     // long after a 2^28-parameter pass has cycled L2 (A/B: 2.62 -> 2.54 ms)
@@ -826,7 +839,7 @@ int launch_meta_update(mg_ctx* ctx, int64_t n, const MetaK& k, const MetaPtrs<T>
       else
         run_tma(meta_update_tma_kernel<T, false, v.threads, v.stages, v.ctas_per_sm>, vc);
     };
-    const int variant = g_tma_variant >= 0 ? g_tma_variant : (sizeof(T) == 4 ? 6 : 0);
+    const int variant = g_tma_variant >= 0 ? g_tma_variant : (sizeof(T) == 4 ? 8 : 9);
     switch (variant) {
       case 1: pick(std::integral_constant<int, 1>{}); break;
       case 2: pick(std::integral_constant<int, 2>{}); break;
@@ -862,19 +875,27 @@ int launch_adam_update(mg_ctx* ctx, int64_t n, const AdamK& k, bool first, const
   const bool vec = aligned16(grad) && aligned16(m) && aligned16(v) && aligned16(pin) &&
                    aligned16(pout) && (!target || aligned16(target)) &&
                    (!delta || aligned16(delta));
-  // TMA ring: 192 threads x 4 stages x 5 arrays x 3 KB (fp32) per CTA, 2 CTAs/SM
-  constexpr int kTh = 192, kSt = 4;
+  // TMA ring: MG_ADAM_THREADS threads x MG_ADAM_STAGES stages x 5 arrays per
+  // CTA, MG_ADAM_CTAS CTAs/SM
+  // (640 x 3 x 1: 1.19 ms at 2^28 fp32 against 1.29 for 192 x 4 x 2 and
+  // 1.21-1.33 for 384-768 threads x 2-4 stages; tools/adam_probe.py)
+#ifndef MG_ADAM_THREADS
+#define MG_ADAM_THREADS 640
+#define MG_ADAM_STAGES 3
+#define MG_ADAM_CTAS 1
+#endif
+  constexpr int kTh = MG_ADAM_THREADS, kSt = MG_ADAM_STAGES;
   if (vec && !g_disable_tma && n >= int64_t(kTh) * VecOf<T>::width * ctx->sm_count) {
     constexpr size_t smem = size_t(kSt) * kAdamArrays * kTh * VecOf<T>::width * sizeof(T);
     auto run_tma = [&](auto kernel) {
       cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
       const int64_t tiles = n / (int64_t(kTh) * VecOf<T>::width);
-      const int64_t want = int64_t(ctx->sm_count) * 2;
+      const int64_t want = int64_t(ctx->sm_count) * MG_ADAM_CTAS;
       kernel<<<int(tiles < want ? tiles : want), kTh, smem, ctx->stream>>>(
           n, k, grad, m, v, pin, pout, target, delta, sc, ctx->partials, ctx->counter);
     };
-    first ? run_tma(adam_update_tma_kernel<T, true, kTh, kSt, 2>)
-          : run_tma(adam_update_tma_kernel<T, false, kTh, kSt, 2>);
+    first ? run_tma(adam_update_tma_kernel<T, true, kTh, kSt, MG_ADAM_CTAS>)
+          : run_tma(adam_update_tma_kernel<T, false, kTh, kSt, MG_ADAM_CTAS>);
     MG_LAUNCH_CHECK(ctx);
     return MG_OK;
   }

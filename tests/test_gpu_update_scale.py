@@ -173,8 +173,8 @@ def test_meta_update_2p24_strided_subset(api, oracle, dt):
 
 # ---------------------------------------------------- TMA ring wrap-around
 # csrc/update.cu tma_variant(): (threads, stages, CTAs per SM)
-VARIANTS = [(256, 4, 1), (256, 3, 2), (512, 3, 1), (128, 3, 4), (256, 2, 3), (160, 5, 2),
-            (192, 4, 2), (224, 3, 2), (96, 4, 4), (192, 3, 2)]
+VARIANTS = [(256, 4, 1), (256, 3, 2), (512, 3, 1), (768, 2, 1), (256, 2, 3), (160, 5, 2),
+            (192, 4, 2), (224, 3, 2), (640, 2, 1), (512, 2, 1)]
 N_WRAP = (1 << 21) + 777
 
 
@@ -226,14 +226,14 @@ def test_tma_ring_wraps_matches_register_kernel(api, dt, variant):
 
 @pytest.mark.parametrize("dt", [torch.float32, torch.float64])
 def test_adam_tma_ring_wraps_matches_register_kernel(api, dt):
-    """Adam's TMA ring (192 threads x 4 stages, 2 CTAs/SM) with >= 8 tiles
+    """Adam's TMA ring (640 threads x 3 stages, 1 CTA/SM) with >= 8 tiles
     per CTA equals the register kernel bit for bit."""
     from paper_2309_15676_b200 import _lib
     L = _lib.load()
     sms = torch.cuda.get_device_properties(0).multi_processor_count
     esz = 4 if dt == torch.float32 else 8
-    assert tiles_per_cta(N_WRAP, 192, 2, esz, sms) >= 8
-    n = N_WRAP
+    n = (1 << 22) + 777
+    assert tiles_per_cta(n, 640, 1, esz, sms) >= 8
     g = torch.Generator(device="cuda").manual_seed(5)
     grads = [torch.randn(n, dtype=dt, device="cuda", generator=g) for _ in range(4)]
     grads[1][::3] = 0.0

@@ -12,13 +12,15 @@ from paper_2309_15676_b200 import _lib, api  # noqa: E402
 variants = [int(v) for v in (sys.argv[1:] or ["4", "6"])]
 L = _lib.load()
 n = 1 << 28
-props = [torch.randn(n, device="cuda") for _ in range(4)]
-diffs = [0.1 * torch.randn(n, device="cuda") for _ in range(4)]
-pa, pb = torch.zeros(n, device="cuda"), torch.zeros(n, device="cuda")
-upd = api.FusedMetaUpdate(n, dtype=torch.float32)
+dt = torch.float64 if os.environ.get("AB_DTYPE") == "f64" else torch.float32
+bpp = 112 if dt == torch.float64 else 56
+props = [torch.randn(n, device="cuda", dtype=dt) for _ in range(4)]
+diffs = [0.1 * torch.randn(n, device="cuda", dtype=dt) for _ in range(4)]
+pa, pb = torch.zeros(n, device="cuda", dtype=dt), torch.zeros(n, device="cuda", dtype=dt)
+upd = api.FusedMetaUpdate(n, dtype=dt)
 res = {v: [] for v in variants}
 t = 0
-for rnd in range(8):
+for rnd in range(int(os.environ.get("AB_ROUNDS", "8"))):
     for v in variants:
         L.mg_set_option(b"tma_variant", v)
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -33,5 +35,5 @@ for rnd in range(8):
             res[v].append(a.elapsed_time(b) / 20)
 for v in variants:
     ms = np.mean(res[v])
-    print(f"variant {v}: {ms:.4f} ms  {56 * n / ms / 1e6:.1f} GB/s  (per block: "
+    print(f"variant {v}: {ms:.4f} ms  {bpp * n / ms / 1e6:.1f} GB/s  (per block: "
           f"{' '.join(f'{x:.3f}' for x in res[v])})", flush=True)
