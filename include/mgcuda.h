@@ -105,7 +105,7 @@ int mg_abi_version(void);
  *   "tma_variant"  -1 | 0..9   schedule of the TMA meta update (-1 default)
  *   "render_fast" = 0          fp32 mini-render on the IEEE kernel instead of
  *                              the TMA-fed fast one (render_fast.cu)
- *   "render_fast_variant"      -1 | 0..12: the fast kernel's schedule
+ *   "render_fast_variant"      -1 | 0..16: the fast kernel's schedule
  *   "cluster_runner" = 0       few-replicate mini-render runs on the
  *                              one-CTA-per-replicate runner
  *   "mesh_persistent"          -1 (auto) | 0..3: bit 0 persistent fp32 isect,

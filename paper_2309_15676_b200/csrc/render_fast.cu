@@ -46,13 +46,19 @@ __host__ __device__ constexpr FastVariant fast_variant(int i) {
        : i == 9 ? FastVariant{128, 2, 6, 32}
        : i == 10 ? FastVariant{256, 2, 3, 32}
        : i == 11 ? FastVariant{128, 3, 2, 32}
-                 : FastVariant{192, 2, 2, 192};
+       : i == 12 ? FastVariant{192, 2, 2, 192}
+       : i == 13 ? FastVariant{512, 2, 1, 32}
+       : i == 14 ? FastVariant{640, 2, 1, 32}
+       : i == 15 ? FastVariant{768, 2, 1, 32}
+                 : FastVariant{512, 3, 1, 32};
 }
-constexpr int kNumFastVariants = 13;
+constexpr int kNumFastVariants = 17;
 // interleaved sweep at 16.7M pixels (tools/render_fast_sweep.py): spp 2 ->
-// per-warp rings (variant 5: 0.172 ms, 0.89 of HBM); spp >= 3 (more
-// arithmetic per byte) -> one ring per 192-thread CTA (variant 3)
-constexpr int default_fast_variant(int spp) { return spp == 2 ? 5 : 3; }
+// per-warp rings in one 512-thread CTA per SM (variant 13: 0.162 ms, 0.95
+// of HBM; the 128-256-thread shapes 0.172-0.193 ms); spp >= 3 (more
+// arithmetic per byte) -> one ring per 192-thread CTA (variant 3; the wide
+// shapes 0.222-0.229 ms against 0.208)
+constexpr int default_fast_variant(int spp) { return spp == 2 ? 13 : 3; }
 // the exact-stream form moves SPP doubles more per pixel: two 192-thread
 // stages (ncu, 16.7M px: 0.197 ms spp 2 / 0.218 ms spp 3 vs IEEE 0.276 / 0.297)
 constexpr int default_fast_variant_mt(int) { return 12; }
@@ -434,7 +440,7 @@ int launch_minirender_fast(mg_ctx* ctx, int64_t P, const RenderK& k, bool first,
   case V: return pick_spp<V>(ctx, P, k, first, b, tgt, pnow, pprev_next, m2p, m2d, mean, var, ap, sc, uni);
     MG_FAST_V(0) MG_FAST_V(1) MG_FAST_V(2) MG_FAST_V(3) MG_FAST_V(4)
     MG_FAST_V(5) MG_FAST_V(6) MG_FAST_V(7) MG_FAST_V(8) MG_FAST_V(9) MG_FAST_V(10)
-    MG_FAST_V(11) MG_FAST_V(12)
+    MG_FAST_V(11) MG_FAST_V(12) MG_FAST_V(13) MG_FAST_V(14) MG_FAST_V(15) MG_FAST_V(16)
 #undef MG_FAST_V
     default: return MG_EINVAL;
   }

@@ -16,12 +16,14 @@ P, spp = 1 << 24, int(sys.argv[1]) if len(sys.argv) > 1 else 2
 rng = sys.argv[2] if len(sys.argv) > 2 else "philox"
 peak = json.load(open(os.path.join(os.path.dirname(__file__), "..", "MEASURED_PEAKS.json")))["hbm_gbs"]
 run = api.MiniRenderRun(P, spp, gen_seed=1, lr=0.01, rng=rng, dtype=torch.float32)
-cfgs = [("ieee", 0, -1), ("fast_default", 1, -1)] + [(f"fast{v}", 1, v) for v in range(13)]
+nv = int(os.environ.get("RF_VARIANTS", "16"))
+only = [int(x) for x in os.environ.get("RF_ONLY", "").split(",") if x]
+cfgs = [("ieee", 0, -1), ("fast_default", 1, -1)] + [(f"fast{v}", 1, v) for v in (only or range(nv))]
 res = {c[0]: [] for c in cfgs}
 s = run.ctx.stream
 for _ in range(3):
     run.step()
-for rep in range(4):
+for rep in range(int(os.environ.get("RF_REPS", "4"))):
     for name, fast, v in cfgs:
         L.mg_set_option(b"render_fast", fast)
         L.mg_set_option(b"render_fast_variant", v)
