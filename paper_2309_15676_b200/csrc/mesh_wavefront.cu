@@ -30,11 +30,44 @@ struct VF;
 template <>
 struct VF<4> {
   static constexpr int n = 22, A = 0, dSn = 6, invfb = 8, dSb = 14, C = 16;
+  // record layout (sparse depths): [base, validity, set 0, set 1], a set =
+  // [A C dSn | invfb dSb] = 11 slots
+  static constexpr int stride = 24;
+  __host__ __device__ static constexpr int slot(int f) {
+    return 2 + (f < 6    ? (f / 3) * 11 + f % 3
+                : f < 8  ? (f - 6) * 11 + 6
+                : f < 14 ? ((f - 8) / 3) * 11 + 7 + (f - 8) % 3
+                : f < 16 ? (f - 14) * 11 + 10
+                         : ((f - 16) / 3) * 11 + 3 + (f - 16) % 3);
+  }
 };
 template <>
 struct VF<5> {
   static constexpr int n = 54, A = 0, invfb = 6, C = 12, dfn = 18, dfb = 36;
+  // record layout (sparse depths): [base, validity, set 0, set 1], a set =
+  // [A C dfn | invfb dfb] = 27 slots
+  static constexpr int stride = 56;
+  __host__ __device__ static constexpr int slot(int f) {
+    return 2 + (f < 6    ? (f / 3) * 27 + f % 3
+                : f < 12 ? ((f - 6) / 3) * 27 + 15 + (f - 6) % 3
+                : f < 18 ? ((f - 12) / 3) * 27 + 3 + (f - 12) % 3
+                : f < 36 ? ((f - 18) / 9) * 27 + 6 + (f - 18) % 9
+                         : ((f - 36) / 9) * 27 + 18 + (f - 36) % 9);
+  }
 };
+
+// every field has a slot of its own behind the two header slots
+template <int NCH>
+constexpr bool vf_slots_ok() {
+  bool used[VF<NCH>::stride] = {};
+  for (int f = 0; f < VF<NCH>::n; ++f) {
+    const int k = VF<NCH>::slot(f);
+    if (k < 2 || k >= VF<NCH>::stride || used[k]) return false;
+    used[k] = true;
+  }
+  return true;
+}
+static_assert(vf_slots_ok<4>() && vf_slots_ok<5>(), "vertex record layout");
 
 template <class T>
 struct WF {
@@ -48,11 +81,14 @@ struct WF {
   // invalid fields are never read (the scatter substitutes zeros), so they
   // need not be written
   unsigned char *vnee, *vbnc;
-  T* vdat;                                    // [kMaxV][nvf][PS]
+  // depths < vrec: [v][field][PS] planes (every path alive: coalesced);
+  // depths >= vrec: [v][PS][stride] records (few survivors: a path's fields
+  // share 4-7 sectors instead of one sector per field)
+  T* vdat;
   // [4][kMaxV + 1]: queue counts, shadow-queue counts, and the fetch
   // counters of the persistent isect / shadow traversals
   unsigned int* cnt;
-  int P, PS, npix, pix0, nprop, nvf;
+  int P, PS, npix, pix0, nprop, nvf, vrec;
 };
 
 
@@ -145,9 +181,33 @@ __device__ __forceinline__ int enqueue(bool pred, unsigned int* counter) {
 }
 // (callers check the slot against their queue's capacity with MG_DCHECK)
 
+// vertex header: the texel's parameter base and the NEE / bounce validity
+// bytes; at record depths they live in the record's two spare slots
+// (slot 0: base, slot 1: validity bytes 0 and 1)
 template <class T>
+__device__ __forceinline__ int& vh_base(const WF<T>& w, int v, int p) {
+  static_assert(sizeof(T) >= 4, "header slots");
+  if (v >= w.vrec)
+    return *reinterpret_cast<int*>(&w.vdat[(size_t(v) * w.PS + p) * w.nvf]);
+  return w.vbase[size_t(v) * w.PS + p];
+}
+template <class T>
+__device__ __forceinline__ unsigned char& vh_nee(const WF<T>& w, int v, int p) {
+  if (v >= w.vrec)
+    return reinterpret_cast<unsigned char*>(&w.vdat[(size_t(v) * w.PS + p) * w.nvf + 1])[0];
+  return w.vnee[size_t(v) * w.PS + p];
+}
+template <class T>
+__device__ __forceinline__ unsigned char& vh_bnc(const WF<T>& w, int v, int p) {
+  if (v >= w.vrec)
+    return reinterpret_cast<unsigned char*>(&w.vdat[(size_t(v) * w.PS + p) * w.nvf + 1])[1];
+  return w.vbnc[size_t(v) * w.PS + p];
+}
+template <int NCH, class T>
 __device__ __forceinline__ T& vf(const WF<T>& w, int v, int f, int p) {
-  return w.vdat[(size_t(v) * w.nvf + f) * size_t(w.PS) + p];
+  using F = VF<NCH>;
+  if (v >= w.vrec) return w.vdat[(size_t(v) * w.PS + p) * F::stride + F::slot(f)];
+  return w.vdat[(size_t(v) * F::stride + f) * size_t(w.PS) + p];
 }
 
 template <class T>
@@ -323,7 +383,7 @@ __device__ __forceinline__ void shade_path(const MeshK& q, const MeshDev& m, con
     const int pbase = oid * NCH * R2 + tex;
     const size_t cell = size_t(oid) * R2 + tex;
     w.nv[p] = v + 1;
-    if (store) w.vbase[size_t(v) * w.PS + p] = pbase;
+    if (store) vh_base(w, v, p) = pbase;
     bool nee_done = false, bounce_done = false;
     T base[2][3], rough[2], metal[2];
 #pragma unroll
@@ -388,19 +448,19 @@ __device__ __forceinline__ void shade_path(const MeshK& q, const MeshDev& m, con
 #pragma unroll
             for (int c = 0; c < 3; ++c)
 #pragma unroll
-              for (int kk = 0; kk < 3; ++kk) vf(w, v, F::dfn + s * 9 + c * 3 + kk, p) = df[c][kk];
+              for (int kk = 0; kk < 3; ++kk) vf<NCH>(w, v, F::dfn + s * 9 + c * 3 + kk, p) = df[c][kk];
         } else {
           T dS;
           bsdf_m0<T>(base[s], rough[s], nT, wT, woT, f, dS);
-          if (store) vf(w, v, VF<4>::dSn + s, p) = dS;
+          if (store) vf<NCH>(w, v, VF<4>::dSn + s, p) = dS;
         }
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
           const T A = beta[s][c] * T(gl * V[18 + c]);
           const T Cc = A * f[c];
           if (store) {
-            vf(w, v, F::A + s * 3 + c, p) = A;
-            vf(w, v, F::C + s * 3 + c, p) = Cc;
+            vf<NCH>(w, v, F::A + s * 3 + c, p) = A;
+            vf<NCH>(w, v, F::C + s * 3 + c, p) = Cc;
           }
           w.pendC[size_t(s * 3 + c) * w.P + p] = Cc;
         }
@@ -461,15 +521,15 @@ __device__ __forceinline__ void shade_path(const MeshK& q, const MeshDev& m, con
               for (int c = 0; c < 3; ++c)
 #pragma unroll
                 for (int kk = 0; kk < 3; ++kk)
-                  vf(w, v, F::dfb + s * 9 + c * 3 + kk, p) = df[c][kk];
+                  vf<NCH>(w, v, F::dfb + s * 9 + c * 3 + kk, p) = df[c][kk];
           } else {
             T dS;
             bsdf_m0<T>(base[s], rough[s], nT, wiT, woT, f, dS);
-            if (store) vf(w, v, VF<4>::dSb + s, p) = dS;
+            if (store) vf<NCH>(w, v, VF<4>::dSb + s, p) = dS;
           }
 #pragma unroll
           for (int c = 0; c < 3; ++c) {
-            if (store) vf(w, v, F::invfb + s * 3 + c, p) = f[c] != T(0) ? T(1) / f[c] : T(0);
+            if (store) vf<NCH>(w, v, F::invfb + s * 3 + c, p) = f[c] != T(0) ? T(1) / f[c] : T(0);
             w.beta[size_t(s * 3 + c) * w.P + p] = beta[s][c] * (f[c] * T(kPiM));
           }
         }
@@ -483,8 +543,8 @@ __device__ __forceinline__ void shade_path(const MeshK& q, const MeshDev& m, con
       }
     }
     if (store) {
-      w.vnee[size_t(v) * w.PS + p] = nee_done;
-      w.vbnc[size_t(v) * w.PS + p] = bounce_done;
+      vh_nee(w, v, p) = nee_done;
+      vh_bnc(w, v, p) = bounce_done;
     }
   }
 }
@@ -531,7 +591,7 @@ __global__ void __launch_bounds__(kMThreads, 8) wf_shadow_kernel(MeshDev m, WF<T
       const int nj = (k == 0 || k == w.nprop) ? 6 : 3;
       for (int j = 0; j < nj; ++j) w.L[size_t(j) * w.P + p] += w.pendC[size_t(j) * w.P + p];
     } else if (p < w.PS) {  // occluded: no NEE data at this vertex
-      w.vnee[size_t(v) * w.PS + p] = 0;
+      vh_nee(w, v, p) = 0;
     }
   }
 }
@@ -562,7 +622,7 @@ __global__ void __launch_bounds__(kMThreads, 8) wf_shadow_p_kernel(MeshDev m, WF
           const int nj = (k == 0 || k == w.nprop) ? 6 : 3;
           for (int j = 0; j < nj; ++j) w.L[size_t(j) * w.P + p] += w.pendC[size_t(j) * w.P + p];
         } else if (p < w.PS) {  // occluded: no NEE data at this vertex
-          w.vnee[size_t(v) * w.PS + p] = 0;
+          vh_nee(w, v, p) = 0;
         }
       },
       sstk);
@@ -592,7 +652,7 @@ __global__ void __launch_bounds__(kMThreads, kP8Blocks) wf_shadow_p8_kernel(Mesh
           const int nj = (k == 0 || k == w.nprop) ? 6 : 3;
           for (int j = 0; j < nj; ++j) w.L[size_t(j) * w.P + p] += w.pendC[size_t(j) * w.P + p];
         } else if (p < w.PS) {  // occluded: no NEE data at this vertex
-          w.vnee[size_t(v) * w.PS + p] = 0;
+          vh_nee(w, v, p) = 0;
         }
       });
 }
@@ -672,7 +732,7 @@ __global__ void __launch_bounds__(kMThreads, MG_TAIL_BLOCKS)
         const int nj = (k == 0 || k == w.nprop) ? 6 : 3;
         for (int j = 0; j < nj; ++j) w.L[size_t(j) * w.P + p] += w.pendC[size_t(j) * w.P + p];
       } else if (p < w.PS) {  // occluded: no NEE data at this vertex
-        w.vnee[size_t(v) * w.PS + p] = 0;
+        vh_nee(w, v, p) = 0;
       }
     }
     if (want_bounce) {
@@ -772,8 +832,8 @@ __device__ __forceinline__ void vertex_terms(const WF<T>& w, int v, int p, int s
   using F = VF<NCH>;
   // fields of an absent NEE / bounce event read as +0 (what the megakernel
   // and the oracle store for them)
-  auto fn = [&](int f) { return ne ? vf(w, v, f, p) : T(0); };
-  auto fbn = [&](int f) { return bn ? vf(w, v, f, p) : T(0); };
+  auto fn = [&](int f) { return ne ? vf<NCH>(w, v, f, p) : T(0); };
+  auto fbn = [&](int f) { return bn ? vf<NCH>(w, v, f, p) : T(0); };
   if constexpr (NCH == 5) {
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
@@ -839,8 +899,8 @@ MG_SCATTER_INLINE void wf_scatter(const WF<T>& w, int p, const T wt[3], int R2,
   const int vtop = MG_SCATTER_LOCKSTEP ? __reduce_max_sync(__activemask(), unsigned(nvp)) : nvp;
   for (int v = vtop - 1; v >= 0; --v) {
     if (v >= nvp) continue;
-    const AccCell<NCH, ILV> cell(acc, w.vbase[size_t(v) * w.PS + p], R2);
-    const bool ne = w.vnee[size_t(v) * w.PS + p], bn = w.vbnc[size_t(v) * w.PS + p];
+    const AccCell<NCH, ILV> cell(acc, vh_base(w, v, p), R2);
+    const bool ne = vh_nee(w, v, p), bn = vh_bnc(w, v, p);
     T X[3][NCH - 2], g[NCH];
     vertex_terms<T, NCH>(w, v, p, 0, Q, ne, bn, X);
     combine<T, NCH>(X, wt, g);
@@ -849,7 +909,7 @@ MG_SCATTER_INLINE void wf_scatter(const WF<T>& w, int p, const T wt[3], int R2,
     for (int k = 0; k < NCH; ++k) d[k] = fixq(double(g[k]));
     cell_add<NCH, ILV>(agg, acc, cell, 0, d);
 #pragma unroll
-    for (int c = 0; c < 3; ++c) Q[c] = Q[c] + (ne ? vf(w, v, F::C + c, p) : T(0));
+    for (int c = 0; c < 3; ++c) Q[c] = Q[c] + (ne ? vf<NCH>(w, v, F::C + c, p) : T(0));
   }
 }
 
@@ -881,8 +941,8 @@ MG_SCATTER_INLINE void wf_scatter_a(const WF<T>& w, int p, const T wt[3], const 
   const int vtop = MG_SCATTER_LOCKSTEP ? __reduce_max_sync(__activemask(), unsigned(nvp)) : nvp;
   for (int v = vtop - 1; v >= 0; --v) {
     if (v >= nvp) continue;
-    const AccCell<NCH, ILV> cell(acc, w.vbase[size_t(v) * w.PS + p], R2);
-    const bool ne = w.vnee[size_t(v) * w.PS + p], bn = w.vbnc[size_t(v) * w.PS + p];
+    const AccCell<NCH, ILV> cell(acc, vh_base(w, v, p), R2);
+    const bool ne = vh_nee(w, v, p), bn = vh_bnc(w, v, p);
     T X[3][NCH - 2], g[NCH];
     unsigned long long d[NCH];
     vertex_terms<T, NCH>(w, v, p, 0, Q0, ne, bn, X);
@@ -900,8 +960,8 @@ MG_SCATTER_INLINE void wf_scatter_a(const WF<T>& w, int p, const T wt[3], const 
     cell_add<NCH, ILV>(agg, acc, cell, 1, d);
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
-      Q0[c] = Q0[c] + (ne ? vf(w, v, F::C + c, p) : T(0));
-      Q1[c] = Q1[c] + (ne ? vf(w, v, F::C + 3 + c, p) : T(0));
+      Q0[c] = Q0[c] + (ne ? vf<NCH>(w, v, F::C + c, p) : T(0));
+      Q1[c] = Q1[c] + (ne ? vf<NCH>(w, v, F::C + 3 + c, p) : T(0));
     }
   }
 }
@@ -1068,7 +1128,7 @@ int wavefront_pair(mg_ctx* ctx, mg_mesh_scene* s, const MeshK& q, int nprop, con
   const size_t tex_bytes = (sizeof(T) * TS * size_t(cells) + 255) & ~size_t(255);
   // the two texel-copy slots come first: their addresses depend on the scene
   // only, not on the tile size, so a copy can outlive the call that made it
-  const size_t need = 2 * tex_bytes + wf_bytes<T>(npix, nprop, VF<NCH>::n);
+  const size_t need = 2 * tex_bytes + wf_bytes<T>(npix, nprop, VF<NCH>::stride);
   if (need > s->wf_cap) {
     MG_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
     cudaFree(s->wf);
@@ -1078,7 +1138,8 @@ int wavefront_pair(mg_ctx* ctx, mg_mesh_scene* s, const MeshK& q, int nprop, con
     MG_CUDA_TRY(cudaMalloc(&s->wf, need));
     s->wf_cap = need;
   }
-  WF<T> w = wf_carve<T>(static_cast<char*>(s->wf) + 2 * tex_bytes, npix, nprop, VF<NCH>::n);
+  WF<T> w = wf_carve<T>(static_cast<char*>(s->wf) + 2 * tex_bytes, npix, nprop, VF<NCH>::stride);
+  w.vrec = g_mesh_vf_records >= 0 ? g_mesh_vf_records : kMaxV;
   w.pix0 = q.row0 * q.W;
   T* slot[2];
   slot[0] = static_cast<T*>(s->wf);
