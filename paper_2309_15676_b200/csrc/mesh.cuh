@@ -51,10 +51,6 @@ extern bool g_mesh_megakernel;
 // BVH, +0.035 ms; with the shared-memory stack and quantised nodes it wins
 // there too, 1.211 -> 1.143 ms.)
 extern int g_mesh_persistent;
-// mg_set_option("mesh_vf_records", d): the wavefront stores the per-vertex
-// adjoint fields of depths >= d (0-based) as one record per path vertex
-// instead of one plane per field (-1: planes at every depth).
-extern int g_mesh_vf_records;
 // mg_set_option("mesh_tail", d): fp32 wavefront depths >= d (0-based) run in
 // one wf_tail_kernel launch; 0 = never; -1 (default): the last kMeshTailDepths
 // depths (from depth 1 at the earliest) — measured best on configs[3] (depth

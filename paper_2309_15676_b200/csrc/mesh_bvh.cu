@@ -13,7 +13,6 @@
 namespace mg {
 bool g_mesh_megakernel = false;
 int g_mesh_persistent = -1;
-int g_mesh_vf_records = 1;
 int g_mesh_tail = -1;
 bool g_mesh_scatter_agg = false;
 bool g_mesh_bvh8 = false;

@@ -2,6 +2,7 @@
 // SoA path state, per-depth isect / shade / shadow stages over compacted
 // queues, per-pixel adjoint scatter; bit-identical to the megakernel and the
 // oracle.  DESIGN.md §12.
+#include <type_traits>
 #include "mesh.cuh"
 
 namespace mg {
@@ -81,14 +82,14 @@ struct WF {
   // invalid fields are never read (the scatter substitutes zeros), so they
   // need not be written
   unsigned char *vnee, *vbnc;
-  // depths < vrec: [v][field][PS] planes (every path alive: coalesced);
-  // depths >= vrec: [v][PS][stride] records (few survivors: a path's fields
+  // depths < kVfRecFrom: [v][field][PS] planes (every path alive: coalesced);
+  // depths >= kVfRecFrom: [v][PS][stride] records (few survivors: a path's fields
   // share 4-7 sectors instead of one sector per field)
   T* vdat;
   // [4][kMaxV + 1]: queue counts, shadow-queue counts, and the fetch
   // counters of the persistent isect / shadow traversals
   unsigned int* cnt;
-  int P, PS, npix, pix0, nprop, nvf, vrec;
+  int P, PS, npix, pix0, nprop, nvf;
 };
 
 
@@ -181,33 +182,54 @@ __device__ __forceinline__ int enqueue(bool pred, unsigned int* counter) {
 }
 // (callers check the slot against their queue's capacity with MG_DCHECK)
 
+// Depths >= kVfRecFrom (0-based) store records, the others planes.  The
+// choice is a compile-time property of every access (REC): as a run-time
+// branch in the accessors it cost configs[4] 0.9 ms per iteration.
+// Build switch for A/B: 0 = records everywhere, 99 = planes everywhere.
+#ifndef MG_VF_REC_FROM
+#define MG_VF_REC_FROM 1
+#endif
+constexpr int kVfRecFrom = MG_VF_REC_FROM;
 // vertex header: the texel's parameter base and the NEE / bounce validity
-// bytes; at record depths they live in the record's two spare slots
+// bytes; at record depths they live in the record's first two slots
 // (slot 0: base, slot 1: validity bytes 0 and 1)
-template <class T>
+template <bool REC, class T>
 __device__ __forceinline__ int& vh_base(const WF<T>& w, int v, int p) {
   static_assert(sizeof(T) >= 4, "header slots");
-  if (v >= w.vrec)
+  if constexpr (REC)
     return *reinterpret_cast<int*>(&w.vdat[(size_t(v) * w.PS + p) * w.nvf]);
-  return w.vbase[size_t(v) * w.PS + p];
+  else
+    return w.vbase[size_t(v) * w.PS + p];
 }
-template <class T>
+template <bool REC, class T>
 __device__ __forceinline__ unsigned char& vh_nee(const WF<T>& w, int v, int p) {
-  if (v >= w.vrec)
+  if constexpr (REC)
     return reinterpret_cast<unsigned char*>(&w.vdat[(size_t(v) * w.PS + p) * w.nvf + 1])[0];
-  return w.vnee[size_t(v) * w.PS + p];
+  else
+    return w.vnee[size_t(v) * w.PS + p];
 }
-template <class T>
+template <bool REC, class T>
 __device__ __forceinline__ unsigned char& vh_bnc(const WF<T>& w, int v, int p) {
-  if (v >= w.vrec)
+  if constexpr (REC)
     return reinterpret_cast<unsigned char*>(&w.vdat[(size_t(v) * w.PS + p) * w.nvf + 1])[1];
-  return w.vbnc[size_t(v) * w.PS + p];
+  else
+    return w.vbnc[size_t(v) * w.PS + p];
 }
-template <int NCH, class T>
+// the shadow stages clear one validity byte: layout picked at run time
+template <class T>
+__device__ __forceinline__ void vh_nee_clear(const WF<T>& w, int v, int p) {
+  if (v >= kVfRecFrom)
+    vh_nee<true>(w, v, p) = 0;
+  else
+    vh_nee<false>(w, v, p) = 0;
+}
+template <int NCH, bool REC, class T>
 __device__ __forceinline__ T& vf(const WF<T>& w, int v, int f, int p) {
   using F = VF<NCH>;
-  if (v >= w.vrec) return w.vdat[(size_t(v) * w.PS + p) * F::stride + F::slot(f)];
-  return w.vdat[(size_t(v) * F::stride + f) * size_t(w.PS) + p];
+  if constexpr (REC)
+    return w.vdat[(size_t(v) * w.PS + p) * F::stride + F::slot(f)];
+  else
+    return w.vdat[(size_t(v) * F::stride + f) * size_t(w.PS) + p];
 }
 
 template <class T>
@@ -331,7 +353,7 @@ __global__ void __launch_bounds__(kMThreads, 8) wf_isect_p_kernel(MeshDev m, WF<
 // and the stored adjoint fields.  want_shadow / want_bounce: the path joins
 // this depth's shadow queue / the next depth's queue.  Shared by
 // wf_shade_kernel and wf_tail_kernel (identical per-path arithmetic).
-template <class T, int NCH>
+template <class T, int NCH, bool REC>
 __device__ __forceinline__ void shade_path(const MeshK& q, const MeshDev& m, const WF<T>& w, int v,
                                            int p, const T* __restrict__ th0,
                                            const T* __restrict__ th1, int maxv, int R2, double la,
@@ -383,7 +405,7 @@ __device__ __forceinline__ void shade_path(const MeshK& q, const MeshDev& m, con
     const int pbase = oid * NCH * R2 + tex;
     const size_t cell = size_t(oid) * R2 + tex;
     w.nv[p] = v + 1;
-    if (store) vh_base(w, v, p) = pbase;
+    if (store) vh_base<REC>(w, v, p) = pbase;
     bool nee_done = false, bounce_done = false;
     T base[2][3], rough[2], metal[2];
 #pragma unroll
@@ -448,19 +470,19 @@ __device__ __forceinline__ void shade_path(const MeshK& q, const MeshDev& m, con
 #pragma unroll
             for (int c = 0; c < 3; ++c)
 #pragma unroll
-              for (int kk = 0; kk < 3; ++kk) vf<NCH>(w, v, F::dfn + s * 9 + c * 3 + kk, p) = df[c][kk];
+              for (int kk = 0; kk < 3; ++kk) vf<NCH, REC>(w, v, F::dfn + s * 9 + c * 3 + kk, p) = df[c][kk];
         } else {
           T dS;
           bsdf_m0<T>(base[s], rough[s], nT, wT, woT, f, dS);
-          if (store) vf<NCH>(w, v, VF<4>::dSn + s, p) = dS;
+          if (store) vf<NCH, REC>(w, v, VF<4>::dSn + s, p) = dS;
         }
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
           const T A = beta[s][c] * T(gl * V[18 + c]);
           const T Cc = A * f[c];
           if (store) {
-            vf<NCH>(w, v, F::A + s * 3 + c, p) = A;
-            vf<NCH>(w, v, F::C + s * 3 + c, p) = Cc;
+            vf<NCH, REC>(w, v, F::A + s * 3 + c, p) = A;
+            vf<NCH, REC>(w, v, F::C + s * 3 + c, p) = Cc;
           }
           w.pendC[size_t(s * 3 + c) * w.P + p] = Cc;
         }
@@ -521,15 +543,15 @@ __device__ __forceinline__ void shade_path(const MeshK& q, const MeshDev& m, con
               for (int c = 0; c < 3; ++c)
 #pragma unroll
                 for (int kk = 0; kk < 3; ++kk)
-                  vf<NCH>(w, v, F::dfb + s * 9 + c * 3 + kk, p) = df[c][kk];
+                  vf<NCH, REC>(w, v, F::dfb + s * 9 + c * 3 + kk, p) = df[c][kk];
           } else {
             T dS;
             bsdf_m0<T>(base[s], rough[s], nT, wiT, woT, f, dS);
-            if (store) vf<NCH>(w, v, VF<4>::dSb + s, p) = dS;
+            if (store) vf<NCH, REC>(w, v, VF<4>::dSb + s, p) = dS;
           }
 #pragma unroll
           for (int c = 0; c < 3; ++c) {
-            if (store) vf<NCH>(w, v, F::invfb + s * 3 + c, p) = f[c] != T(0) ? T(1) / f[c] : T(0);
+            if (store) vf<NCH, REC>(w, v, F::invfb + s * 3 + c, p) = f[c] != T(0) ? T(1) / f[c] : T(0);
             w.beta[size_t(s * 3 + c) * w.P + p] = beta[s][c] * (f[c] * T(kPiM));
           }
         }
@@ -543,13 +565,13 @@ __device__ __forceinline__ void shade_path(const MeshK& q, const MeshDev& m, con
       }
     }
     if (store) {
-      vh_nee(w, v, p) = nee_done;
-      vh_bnc(w, v, p) = bounce_done;
+      vh_nee<REC>(w, v, p) = nee_done;
+      vh_bnc<REC>(w, v, p) = bounce_done;
     }
   }
 }
 
-template <class T, int NCH>
+template <class T, int NCH, bool REC>
 __global__ void __launch_bounds__(kMThreads)
     wf_shade_kernel(MeshK q, MeshDev m, WF<T> w, int v, const T* __restrict__ th0,
                     const T* __restrict__ th1) {
@@ -567,7 +589,7 @@ __global__ void __launch_bounds__(kMThreads)
     int p = -1;
     if (i < n) {
       p = qin[i];
-      shade_path<T, NCH>(q, m, w, v, p, th0, th1, maxv, R2, la, want_shadow, want_bounce);
+      shade_path<T, NCH, REC>(q, m, w, v, p, th0, th1, maxv, R2, la, want_shadow, want_bounce);
     }
     const int qs = enqueue(want_shadow, &w.cnt[kMaxV + 1 + v]);
     MG_DCHECK(qs < w.P);
@@ -591,7 +613,7 @@ __global__ void __launch_bounds__(kMThreads, 8) wf_shadow_kernel(MeshDev m, WF<T
       const int nj = (k == 0 || k == w.nprop) ? 6 : 3;
       for (int j = 0; j < nj; ++j) w.L[size_t(j) * w.P + p] += w.pendC[size_t(j) * w.P + p];
     } else if (p < w.PS) {  // occluded: no NEE data at this vertex
-      vh_nee(w, v, p) = 0;
+      vh_nee_clear(w, v, p);
     }
   }
 }
@@ -622,7 +644,7 @@ __global__ void __launch_bounds__(kMThreads, 8) wf_shadow_p_kernel(MeshDev m, WF
           const int nj = (k == 0 || k == w.nprop) ? 6 : 3;
           for (int j = 0; j < nj; ++j) w.L[size_t(j) * w.P + p] += w.pendC[size_t(j) * w.P + p];
         } else if (p < w.PS) {  // occluded: no NEE data at this vertex
-          vh_nee(w, v, p) = 0;
+          vh_nee_clear(w, v, p);
         }
       },
       sstk);
@@ -652,7 +674,7 @@ __global__ void __launch_bounds__(kMThreads, kP8Blocks) wf_shadow_p8_kernel(Mesh
           const int nj = (k == 0 || k == w.nprop) ? 6 : 3;
           for (int j = 0; j < nj; ++j) w.L[size_t(j) * w.P + p] += w.pendC[size_t(j) * w.P + p];
         } else if (p < w.PS) {  // occluded: no NEE data at this vertex
-          vh_nee(w, v, p) = 0;
+          vh_nee_clear(w, v, p);
         }
       });
 }
@@ -723,7 +745,12 @@ __global__ void __launch_bounds__(kMThreads, MG_TAIL_BLOCKS)
       w.hv[p] = bv;
     }
     bool want_shadow = false, want_bounce = false;
-    shade_path<float, NCH>(q, m, w, v, p, th0, th1, maxv, R2, la, want_shadow, want_bounce);
+    if (kVfRecFrom <= 1 || v >= kVfRecFrom)  // the tail starts at depth >= 1
+      shade_path<float, NCH, true>(q, m, w, v, p, th0, th1, maxv, R2, la, want_shadow,
+                                   want_bounce);
+    else
+      shade_path<float, NCH, false>(q, m, w, v, p, th0, th1, maxv, R2, la, want_shadow,
+                                    want_bounce);
     if (want_shadow) {
       const double o[3] = {w.sox[p], w.soy[p], w.soz[p]}, d[3] = {w.sdx[p], w.sdy[p], w.sdz[p]};
       double ts, tu, tv;
@@ -732,7 +759,7 @@ __global__ void __launch_bounds__(kMThreads, MG_TAIL_BLOCKS)
         const int nj = (k == 0 || k == w.nprop) ? 6 : 3;
         for (int j = 0; j < nj; ++j) w.L[size_t(j) * w.P + p] += w.pendC[size_t(j) * w.P + p];
       } else if (p < w.PS) {  // occluded: no NEE data at this vertex
-        vh_nee(w, v, p) = 0;
+        vh_nee_clear(w, v, p);
       }
     }
     if (want_bounce) {
@@ -826,14 +853,14 @@ __device__ __forceinline__ void cell_add(bool agg, const AccTable& acc,
 // base colour c, X[c][1] roughness, X[c][2] metalness (NCH 5); Q is the
 // suffix radiance.  combine() applies weights wt:
 //   g[c] = wt[c] X[c][0],  g[3] = sum_c wt[c] X[c][1],  g[4] = sum_c wt[c] X[c][2].
-template <class T, int NCH>
+template <class T, int NCH, bool REC>
 __device__ __forceinline__ void vertex_terms(const WF<T>& w, int v, int p, int s, const T Q[3],
                                              bool ne, bool bn, T X[3][NCH - 2]) {
   using F = VF<NCH>;
   // fields of an absent NEE / bounce event read as +0 (what the megakernel
   // and the oracle store for them)
-  auto fn = [&](int f) { return ne ? vf<NCH>(w, v, f, p) : T(0); };
-  auto fbn = [&](int f) { return bn ? vf<NCH>(w, v, f, p) : T(0); };
+  auto fn = [&](int f) { return ne ? vf<NCH, REC>(w, v, f, p) : T(0); };
+  auto fbn = [&](int f) { return bn ? vf<NCH, REC>(w, v, f, p) : T(0); };
   if constexpr (NCH == 5) {
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
@@ -897,20 +924,27 @@ MG_SCATTER_INLINE void wf_scatter(const WF<T>& w, int p, const T wt[3], int R2,
 #define MG_SCATTER_LOCKSTEP 1
 #endif
   const int vtop = MG_SCATTER_LOCKSTEP ? __reduce_max_sync(__activemask(), unsigned(nvp)) : nvp;
-  for (int v = vtop - 1; v >= 0; --v) {
-    if (v >= nvp) continue;
-    const AccCell<NCH, ILV> cell(acc, vh_base(w, v, p), R2);
-    const bool ne = vh_nee(w, v, p), bn = vh_bnc(w, v, p);
+  auto vertex = [&](int v, auto rec) {
+    constexpr bool REC = decltype(rec)::value;
+    const AccCell<NCH, ILV> cell(acc, vh_base<REC>(w, v, p), R2);
+    const bool ne = vh_nee<REC>(w, v, p), bn = vh_bnc<REC>(w, v, p);
     T X[3][NCH - 2], g[NCH];
-    vertex_terms<T, NCH>(w, v, p, 0, Q, ne, bn, X);
+    vertex_terms<T, NCH, REC>(w, v, p, 0, Q, ne, bn, X);
     combine<T, NCH>(X, wt, g);
     unsigned long long d[NCH];
 #pragma unroll
     for (int k = 0; k < NCH; ++k) d[k] = fixq(double(g[k]));
     cell_add<NCH, ILV>(agg, acc, cell, 0, d);
 #pragma unroll
-    for (int c = 0; c < 3; ++c) Q[c] = Q[c] + (ne ? vf<NCH>(w, v, F::C + c, p) : T(0));
-  }
+    for (int c = 0; c < 3; ++c) Q[c] = Q[c] + (ne ? vf<NCH, REC>(w, v, F::C + c, p) : T(0));
+  };
+  // record depths, then plane depths: the layout is a compile-time
+  // property of each loop
+  int v = vtop - 1;
+  for (; v >= kVfRecFrom; --v)
+    if (v < nvp) vertex(v, std::true_type{});
+  for (; v >= 0; --v)
+    if (v < nvp) vertex(v, std::false_type{});
 }
 
 // Path A (p = pixel i) in ONE walk: its proportional adjoint (set 0,
@@ -939,13 +973,13 @@ MG_SCATTER_INLINE void wf_scatter_a(const WF<T>& w, int p, const T wt[3], const 
 #define MG_SCATTER_LOCKSTEP 1
 #endif
   const int vtop = MG_SCATTER_LOCKSTEP ? __reduce_max_sync(__activemask(), unsigned(nvp)) : nvp;
-  for (int v = vtop - 1; v >= 0; --v) {
-    if (v >= nvp) continue;
-    const AccCell<NCH, ILV> cell(acc, vh_base(w, v, p), R2);
-    const bool ne = vh_nee(w, v, p), bn = vh_bnc(w, v, p);
+  auto vertex = [&](int v, auto rec) {
+    constexpr bool REC = decltype(rec)::value;
+    const AccCell<NCH, ILV> cell(acc, vh_base<REC>(w, v, p), R2);
+    const bool ne = vh_nee<REC>(w, v, p), bn = vh_bnc<REC>(w, v, p);
     T X[3][NCH - 2], g[NCH];
     unsigned long long d[NCH];
-    vertex_terms<T, NCH>(w, v, p, 0, Q0, ne, bn, X);
+    vertex_terms<T, NCH, REC>(w, v, p, 0, Q0, ne, bn, X);
     combine<T, NCH>(X, wt, g);
 #pragma unroll
     for (int k = 0; k < NCH; ++k) d[k] = fixq(double(g[k]));
@@ -953,17 +987,22 @@ MG_SCATTER_INLINE void wf_scatter_a(const WF<T>& w, int p, const T wt[3], const 
     combine<T, NCH>(X, wC0, g);
 #pragma unroll
     for (int k = 0; k < NCH; ++k) d[k] = fixq(double(g[k]));
-    vertex_terms<T, NCH>(w, v, p, 1, Q1, ne, bn, X);
+    vertex_terms<T, NCH, REC>(w, v, p, 1, Q1, ne, bn, X);
     combine<T, NCH>(X, wC1, g);
 #pragma unroll
     for (int k = 0; k < NCH; ++k) d[k] = d[k] + fixq(double(g[k]));
     cell_add<NCH, ILV>(agg, acc, cell, 1, d);
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
-      Q0[c] = Q0[c] + (ne ? vf<NCH>(w, v, F::C + c, p) : T(0));
-      Q1[c] = Q1[c] + (ne ? vf<NCH>(w, v, F::C + 3 + c, p) : T(0));
+      Q0[c] = Q0[c] + (ne ? vf<NCH, REC>(w, v, F::C + c, p) : T(0));
+      Q1[c] = Q1[c] + (ne ? vf<NCH, REC>(w, v, F::C + 3 + c, p) : T(0));
     }
-  }
+  };
+  int v = vtop - 1;
+  for (; v >= kVfRecFrom; --v)
+    if (v < nvp) vertex(v, std::true_type{});
+  for (; v >= 0; --v)
+    if (v < nvp) vertex(v, std::false_type{});
 }
 
 constexpr int kMaxProp = 8;
@@ -1139,7 +1178,6 @@ int wavefront_pair(mg_ctx* ctx, mg_mesh_scene* s, const MeshK& q, int nprop, con
     s->wf_cap = need;
   }
   WF<T> w = wf_carve<T>(static_cast<char*>(s->wf) + 2 * tex_bytes, npix, nprop, VF<NCH>::stride);
-  w.vrec = g_mesh_vf_records >= 0 ? g_mesh_vf_records : kMaxV;
   w.pix0 = q.row0 * q.W;
   T* slot[2];
   slot[0] = static_cast<T*>(s->wf);
@@ -1210,7 +1248,12 @@ int wavefront_pair(mg_ctx* ctx, mg_mesh_scene* s, const MeshK& q, int nprop, con
       wf_isect_kernel<T><<<grid, kMThreads, 0, ctx->stream>>>(m, w, v);
     }
     MG_LAUNCH_CHECK(ctx);
-    wf_shade_kernel<T, NCH><<<grid, kMThreads, 0, ctx->stream>>>(q, m, w, v, thI[0], thI[1]);
+    if (v >= kVfRecFrom)
+      wf_shade_kernel<T, NCH, true><<<grid, kMThreads, 0, ctx->stream>>>(q, m, w, v, thI[0],
+                                                                        thI[1]);
+    else
+      wf_shade_kernel<T, NCH, false><<<grid, kMThreads, 0, ctx->stream>>>(q, m, w, v, thI[0],
+                                                                         thI[1]);
     MG_LAUNCH_CHECK(ctx);
     if constexpr (sizeof(T) == 4) {
       if ((pmode & 2) && g_mesh_bvh8)

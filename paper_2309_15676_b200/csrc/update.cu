@@ -35,7 +35,6 @@ extern int g_render_fast_variant;
 int render_fast_variants();
 extern bool g_mesh_megakernel;
 extern int g_mesh_persistent;
-extern int g_mesh_vf_records;
 extern int g_mesh_tail;
 extern bool g_mesh_scatter_agg;
 extern bool g_mesh_bvh8;
@@ -1055,11 +1054,6 @@ int mg_set_option(const char* name, int64_t value) {
   if (std::string(name) == "mesh_persistent") {
     if (value < -1 || value > 3) return fail(MG_EINVAL, "mesh_persistent must lie in [-1, 3]");
     g_mesh_persistent = int(value);
-    return MG_OK;
-  }
-  if (std::string(name) == "mesh_vf_records") {
-    if (value < -1 || value > 8) return fail(MG_EINVAL, "mesh_vf_records must lie in [-1, 8]");
-    g_mesh_vf_records = int(value);
     return MG_OK;
   }
   if (std::string(name) == "mesh_tail") {
