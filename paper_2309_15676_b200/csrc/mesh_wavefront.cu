@@ -353,17 +353,42 @@ __global__ void __launch_bounds__(kMThreads, 8) wf_isect_p_kernel(MeshDev m, WF<
 // and the stored adjoint fields.  want_shadow / want_bounce: the path joins
 // this depth's shadow queue / the next depth's queue.  Shared by
 // wf_shade_kernel and wf_tail_kernel (identical per-path arithmetic).
-template <class T, int NCH, bool REC>
+// The path state one shade step consumes and produces.  The stage kernel
+// loads / stores it around the call; the tail kernel keeps it in registers
+// from one depth to the next.
+template <class T>
+struct PathIO {
+  int slot;                  // in: hit triangle slot (< 0: escaped)
+  double o[3], d[3];         // in: the ray
+  double t, bu, bv;          // in: hit distance and barycentrics (slot >= 0)
+  T beta[2][3];              // in: throughput of the evaluated sets; out (want_bounce): next depth's
+  double so[3], sd[3], stm;  // out (want_shadow): the NEE ray
+  T pendC[2][3];             // out (want_shadow): the NEE contribution if unoccluded
+  double on[3], dn[3];       // out (want_bounce): the next ray
+};
+
+// parameter sets a path evaluates: path 0 (A) and the FD path at theta_t
+// and theta_{t-1}; the other proportional paths at theta_t only
+template <class T>
+__device__ __forceinline__ int path_sets(const WF<T>& w, int p) {
+  const int k = p / w.npix;
+  return (k == 0 || k == w.nprop) ? 2 : 1;
+}
+
+// REGS: the outputs stay in io (tail kernel); otherwise each is stored to
+// the path-state arrays as soon as it is computed (stage kernel: holding
+// them to the end of the call cost 25 registers and a resident CTA).
+template <class T, int NCH, bool REC, bool REGS>
 __device__ __forceinline__ void shade_path(const MeshK& q, const MeshDev& m, const WF<T>& w, int v,
-                                           int p, const T* __restrict__ th0,
+                                           int p, PathIO<T>& io, const T* __restrict__ th0,
                                            const T* __restrict__ th1, int maxv, int R2, double la,
                                            bool& want_shadow, bool& want_bounce) {
+  const int slot = io.slot;
   constexpr int TS = TexIlv<T, NCH>::TS;  // th0 / th1: texel-major copies
   using F = VF<NCH>;
   const double* V = q.view;
   const T* th[2] = {th0, th1};
   const int k = p / w.npix, pix = w.pix0 + (p - k * w.npix);
-  const int slot = w.hslot[p];
   const bool store = p < w.PS;
   // parameter sets evaluated: path 0 (A) and the FD path at theta_t and
   // theta_{t-1}; the other proportional paths at theta_t only
@@ -373,7 +398,7 @@ __device__ __forceinline__ void shade_path(const MeshK& q, const MeshDev& m, con
   for (int s = 0; s < 2; ++s)
 #pragma unroll
     for (int c = 0; c < 3; ++c)
-      beta[s][c] = s < ns ? w.beta[size_t(s * 3 + c) * w.P + p] : T(0);
+      beta[s][c] = s < ns ? io.beta[s][c] : T(0);
   if (slot < 0) {  // escaped: environment
 #pragma unroll
     for (int s = 0; s < 2; ++s)
@@ -386,8 +411,8 @@ __device__ __forceinline__ void shade_path(const MeshK& q, const MeshDev& m, con
         w.E[size_t(s * 3 + c) * w.P + p] = beta[s][c] * T(V[21 + c]);
       }
   } else {
-    const double o[3] = {w.ox[p], w.oy[p], w.oz[p]}, d[3] = {w.dx[p], w.dy[p], w.dz[p]};
-    const double t = w.ht[p], bu = w.hu[p], bv = w.hv[p];
+    const double o[3] = {io.o[0], io.o[1], io.o[2]}, d[3] = {io.d[0], io.d[1], io.d[2]};
+    const double t = io.t, bu = io.bu, bv = io.bv;
     const double* r = m.tri + size_t(kRec) * slot;
     const double x[3] = {o[0] + t * d[0], o[1] + t * d[1], o[2] + t * d[2]};
     double nn[3] = {r[9], r[10], r[11]};
@@ -484,16 +509,28 @@ __device__ __forceinline__ void shade_path(const MeshK& q, const MeshDev& m, con
             vf<NCH, REC>(w, v, F::A + s * 3 + c, p) = A;
             vf<NCH, REC>(w, v, F::C + s * 3 + c, p) = Cc;
           }
-          w.pendC[size_t(s * 3 + c) * w.P + p] = Cc;
+          if constexpr (REGS)
+            io.pendC[s][c] = Cc;
+          else
+            w.pendC[size_t(s * 3 + c) * w.P + p] = Cc;
         }
       }
-      w.sox[p] = xo[0];
-      w.soy[p] = xo[1];
-      w.soz[p] = xo[2];
-      w.sdx[p] = wl3[0];
-      w.sdy[p] = wl3[1];
-      w.sdz[p] = wl3[2];
-      w.stm[p] = wl - kOff;
+      if constexpr (REGS) {
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+          io.so[c] = xo[c];
+          io.sd[c] = wl3[c];
+        }
+        io.stm = wl - kOff;
+      } else {
+        w.sox[p] = xo[0];
+        w.soy[p] = xo[1];
+        w.soz[p] = xo[2];
+        w.sdx[p] = wl3[0];
+        w.sdy[p] = wl3[1];
+        w.sdz[p] = wl3[2];
+        w.stm[p] = wl - kOff;
+      }
     }
     if (!(v == maxv - 1 || dot3d(nn, wo) <= 0.0)) {
       double dx = 0.0, dy = 0.0;
@@ -552,15 +589,26 @@ __device__ __forceinline__ void shade_path(const MeshK& q, const MeshDev& m, con
 #pragma unroll
           for (int c = 0; c < 3; ++c) {
             if (store) vf<NCH, REC>(w, v, F::invfb + s * 3 + c, p) = f[c] != T(0) ? T(1) / f[c] : T(0);
-            w.beta[size_t(s * 3 + c) * w.P + p] = beta[s][c] * (f[c] * T(kPiM));
+            if constexpr (REGS)
+              io.beta[s][c] = beta[s][c] * (f[c] * T(kPiM));
+            else
+              w.beta[size_t(s * 3 + c) * w.P + p] = beta[s][c] * (f[c] * T(kPiM));
           }
         }
-        w.ox[p] = xo[0];
-        w.oy[p] = xo[1];
-        w.oz[p] = xo[2];
-        w.dx[p] = wi[0];
-        w.dy[p] = wi[1];
-        w.dz[p] = wi[2];
+        if constexpr (REGS) {
+#pragma unroll
+          for (int c = 0; c < 3; ++c) {
+            io.on[c] = xo[c];
+            io.dn[c] = wi[c];
+          }
+        } else {
+          w.ox[p] = xo[0];
+          w.oy[p] = xo[1];
+          w.oz[p] = xo[2];
+          w.dx[p] = wi[0];
+          w.dy[p] = wi[1];
+          w.dz[p] = wi[2];
+        }
         want_bounce = true;
       }
     }
@@ -572,7 +620,7 @@ __device__ __forceinline__ void shade_path(const MeshK& q, const MeshDev& m, con
 }
 
 template <class T, int NCH, bool REC>
-__global__ void __launch_bounds__(kMThreads)
+__global__ void __launch_bounds__(kMThreads, sizeof(T) == 4 ? 4 : 1)
     wf_shade_kernel(MeshK q, MeshDev m, WF<T> w, int v, const T* __restrict__ th0,
                     const T* __restrict__ th1) {
   if (q.it_offset) q.iteration += __ldg(q.it_offset);
@@ -583,13 +631,64 @@ __global__ void __launch_bounds__(kMThreads)
   const int* qin = (v & 1) ? w.q1 : w.q0;
   int* qout = (v & 1) ? w.q0 : w.q1;
   const double la = (V[15] - V[14]) * (V[17] - V[16]);
-  for (int i = blockIdx.x * kMThreads + threadIdx.x; i - int(threadIdx.x) < n;
-       i += gridDim.x * kMThreads) {
+  // software pipeline: the next queue entry and its hit slot are requested
+  // (and the hit triangle's record prefetched into L2) one iteration ahead,
+  // so the dependent chain queue -> path -> slot -> triangle of an
+  // iteration overlaps the previous iteration's shading
+#ifndef MG_SHADE_PIPE
+#define MG_SHADE_PIPE 1
+#endif
+  const int stride = gridDim.x * kMThreads;
+  int i = blockIdx.x * kMThreads + threadIdx.x;
+  int pn = -1, slotn = -1;
+  auto fetch = [&](int j) {
+    pn = -1;
+    slotn = -1;
+    if (j < n) {
+      pn = qin[j];
+      slotn = w.hslot[pn];
+      if (slotn >= 0) {
+        const char* r = reinterpret_cast<const char*>(m.tri + size_t(kRec) * slotn);
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(r));
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(r + 128));
+      }
+    }
+  };
+  if (MG_SHADE_PIPE) fetch(i);
+  for (; i - int(threadIdx.x) < n; i += stride) {
     bool want_shadow = false, want_bounce = false;
     int p = -1;
-    if (i < n) {
+    int slot = -1;
+    if (MG_SHADE_PIPE) {
+      p = pn;
+      slot = slotn;
+      fetch(i + stride);
+    } else if (i < n) {
       p = qin[i];
-      shade_path<T, NCH, REC>(q, m, w, v, p, th0, th1, maxv, R2, la, want_shadow, want_bounce);
+      slot = w.hslot[p];
+    }
+    if (p >= 0) {
+      PathIO<T> io;
+      io.slot = slot;
+      const int ns = path_sets(w, p);
+#pragma unroll
+      for (int s = 0; s < 2; ++s)
+#pragma unroll
+        for (int c = 0; c < 3; ++c)
+          io.beta[s][c] = s < ns ? w.beta[size_t(s * 3 + c) * w.P + p] : T(0);
+      if (slot >= 0) {
+        io.o[0] = w.ox[p];
+        io.o[1] = w.oy[p];
+        io.o[2] = w.oz[p];
+        io.d[0] = w.dx[p];
+        io.d[1] = w.dy[p];
+        io.d[2] = w.dz[p];
+        io.t = w.ht[p];
+        io.bu = w.hu[p];
+        io.bv = w.hv[p];
+      }
+      shade_path<T, NCH, REC, false>(q, m, w, v, p, io, th0, th1, maxv, R2, la, want_shadow,
+                                     want_bounce);
     }
     const int qs = enqueue(want_shadow, &w.cnt[kMaxV + 1 + v]);
     MG_DCHECK(qs < w.P);
@@ -715,6 +814,12 @@ __global__ void __launch_bounds__(kMThreads, MG_TAIL_BLOCKS)
   const int lane = int(threadIdx.x & 31);
   int p = -1, v = v0;
   bool done = false;
+  // the path's ray and throughput stay in registers from depth to depth
+  // (and its hit, NEE ray and pending NEE term never reach memory): as
+  // global arrays every depth step paid their write, an L2 round trip to
+  // read them back and one sector per field
+  PathIO<float> io;
+  int ns = 1;
   for (;;) {
     const bool need = p < 0 && !done;
     const unsigned needm = __ballot_sync(0xffffffffu, need);
@@ -728,6 +833,18 @@ __global__ void __launch_bounds__(kMThreads, MG_TAIL_BLOCKS)
         if (idx < n) {
           p = qin[idx];
           v = v0;
+          ns = path_sets(w, p);
+          io.o[0] = w.ox[p];
+          io.o[1] = w.oy[p];
+          io.o[2] = w.oz[p];
+          io.d[0] = w.dx[p];
+          io.d[1] = w.dy[p];
+          io.d[2] = w.dz[p];
+#pragma unroll
+          for (int s = 0; s < 2; ++s)
+#pragma unroll
+            for (int c = 0; c < 3; ++c)
+              io.beta[s][c] = s < ns ? w.beta[size_t(s * 3 + c) * w.P + p] : 0.0f;
         } else {
           done = true;
         }
@@ -735,34 +852,35 @@ __global__ void __launch_bounds__(kMThreads, MG_TAIL_BLOCKS)
     }
     if (__all_sync(0xffffffffu, done)) break;
     if (p < 0) continue;
-    {
-      const double o[3] = {w.ox[p], w.oy[p], w.oz[p]}, d[3] = {w.dx[p], w.dy[p], w.dz[p]};
-      double t = INFINITY, bu = 0.0, bv = 0.0;
-      const int slot = trace32_impl<false, SSTK, QN>(m, sn, o, d, INFINITY, t, bu, bv, sstk);
-      w.hslot[p] = slot;
-      w.ht[p] = t;
-      w.hu[p] = bu;
-      w.hv[p] = bv;
-    }
+    io.t = INFINITY;
+    io.bu = 0.0;
+    io.bv = 0.0;
+    io.slot = trace32_impl<false, SSTK, QN>(m, sn, io.o, io.d, INFINITY, io.t, io.bu, io.bv, sstk);
     bool want_shadow = false, want_bounce = false;
     if (kVfRecFrom <= 1 || v >= kVfRecFrom)  // the tail starts at depth >= 1
-      shade_path<float, NCH, true>(q, m, w, v, p, th0, th1, maxv, R2, la, want_shadow,
+      shade_path<float, NCH, true, true>(q, m, w, v, p, io, th0, th1, maxv, R2, la, want_shadow,
                                    want_bounce);
     else
-      shade_path<float, NCH, false>(q, m, w, v, p, th0, th1, maxv, R2, la, want_shadow,
+      shade_path<float, NCH, false, true>(q, m, w, v, p, io, th0, th1, maxv, R2, la, want_shadow,
                                     want_bounce);
     if (want_shadow) {
-      const double o[3] = {w.sox[p], w.soy[p], w.soz[p]}, d[3] = {w.sdx[p], w.sdy[p], w.sdz[p]};
       double ts, tu, tv;
-      if (trace32_impl<true, SSTK, QN>(m, sn, o, d, w.stm[p], ts, tu, tv, sstk) < 0) {
-        const int k = p / w.npix;
-        const int nj = (k == 0 || k == w.nprop) ? 6 : 3;
-        for (int j = 0; j < nj; ++j) w.L[size_t(j) * w.P + p] += w.pendC[size_t(j) * w.P + p];
+      if (trace32_impl<true, SSTK, QN>(m, sn, io.so, io.sd, io.stm, ts, tu, tv, sstk) < 0) {
+#pragma unroll
+        for (int s = 0; s < 2; ++s)
+#pragma unroll
+          for (int c = 0; c < 3; ++c)
+            if (s < ns) w.L[size_t(s * 3 + c) * w.P + p] += io.pendC[s][c];
       } else if (p < w.PS) {  // occluded: no NEE data at this vertex
         vh_nee_clear(w, v, p);
       }
     }
     if (want_bounce) {
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        io.o[c] = io.on[c];
+        io.d[c] = io.dn[c];
+      }
       ++v;
     } else {
       p = -1;
