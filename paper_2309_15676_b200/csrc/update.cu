@@ -839,7 +839,12 @@ int launch_meta_update(mg_ctx* ctx, int64_t n, const MetaK& k, const MetaPtrs<T>
       else
         run_tma(meta_update_tma_kernel<T, false, v.threads, v.stages, v.ctas_per_sm>, vc);
     };
-    const int variant = g_tma_variant >= 0 ? g_tma_variant : (sizeof(T) == 4 ? 8 : 9);
+    // fp32: 640 threads x 2 stages from 2^26 parameters up (2^28: 2.24 ms
+    // against 2.35 for 512 x 2), 512 x 2 below (2^24: 0.153 against
+    // 0.167 ms, 2^25: 0.288 / 0.295; tools/update_variant_by_size.py)
+    const int variant = g_tma_variant >= 0 ? g_tma_variant
+                        : sizeof(T) == 4   ? (n >= (int64_t(3) << 24) ? 8 : 9)
+                                           : 9;
     switch (variant) {
       case 1: pick(std::integral_constant<int, 1>{}); break;
       case 2: pick(std::integral_constant<int, 2>{}); break;

@@ -3,7 +3,7 @@
 (Moment2 x2 + diff decoupling + MetaEstimator::step + update,
 moment2.hpp:30-39, meta.hpp:90-113, harness.cpp:144-187) against the
 oracle at N = 2^20 over all 100 steps, a strided subset at N = 2^24 over
-100 steps, and the TMA ring at sizes where every CTA wraps its ring at
+100 steps and at N = 2^28 (the bench size) over 12 steps, and the TMA ring at sizes where every CTA wraps its ring at
 least twice (all 10 schedule variants + Adam, fp32 and fp64).
 
 Bars: fp64 BIT-EXACT given the same step norm; fp32 vs the fp64 oracle on
@@ -125,14 +125,17 @@ def test_meta_update_f32_2p20_100_steps(api, oracle):
 
 
 @pytest.mark.parametrize("dt", [torch.float32, torch.float64])
-def test_meta_update_2p24_strided_subset(api, oracle, dt):
-    """N = 2^24, 100 steps with the device step norm (the bench path): a
-    stride-97 subset of every state array against the oracle run on that
-    subset with the step norm the device consumed (scalars.ssn_used) —
-    bit-exact in fp64, rel 1e-4 in fp32; the device step norm itself
-    against a full fp64 host sum at steps 1, 10 and 100."""
-    n, steps, pool, stride = 1 << 24, 100, 4, 97
-    props, diffs = device_pool(n, dt, pool, seed=24)
+@pytest.mark.parametrize("log2n,steps,pool,stride", [(24, 100, 4, 97), (28, 12, 2, 9973)],
+                         ids=["2p24", "2p28"])
+def test_meta_update_strided_subset(api, oracle, dt, log2n, steps, pool, stride):
+    """N = 2^24 over 100 steps and N = 2^28 — bench.py's headline size,
+    1,181 ring tiles per CTA — over 12 steps, with the device step norm
+    (the bench path): a strided subset of every state array against the
+    oracle run on that subset with the step norm the device consumed
+    (scalars.ssn_used) — bit-exact in fp64, rel 1e-4 in fp32; the device
+    step norm itself against a full fp64 host sum at steps 1, 10 and 100."""
+    n = 1 << log2n
+    props, diffs = device_pool(n, dt, pool, seed=log2n)
     idx = torch.arange(0, n, stride, device="cuda")
     hp = [host(x[idx]) for x in props]
     hd = [host(x[idx]) for x in diffs]
@@ -161,7 +164,7 @@ def test_meta_update_2p24_strided_subset(api, oracle, dt):
         got = host(pa[idx])
         if dt == torch.float64:
             assert bits_equal(got, p), t
-        elif t % 10 == 9:
+        elif t % 10 == 9 or t == steps - 1:
             assert rel_err(got, p) < 1e-4, t
     for name in STATE:
         got = host(getattr(upd, name)[idx])
