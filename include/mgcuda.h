@@ -360,6 +360,21 @@ int mg_meta_update_fixed(mg_ctx* ctx, int32_t dtype, int64_t cells, int32_t nch,
                          const mg_meta_update_args* a, void* accum, void* m2_prop, void* m2_diff,
                          void* mean, void* var, void* alpha_prev, const void* params_in,
                          void* params_out, mg_update_scalars* scalars, const mg_meta_extras* x);
+/* mg_meta_update_fixed with a touch map: touch_map holds one bit per texel
+ * cell (cells / 32 uint32 words, cell c = bit c % 32 of word c / 32; zero
+ * before first use) and bit c is set whenever accum's cell c may be
+ * non-zero — mg_meshscene_set_touch_map makes the accumulator-keeping sample
+ * pair maintain it.  Only the cells whose bit is set are read and zeroed
+ * (an untouched cell's pair is exactly 0 either way, so the results are
+ * identical to mg_meta_update_fixed) and their bits are cleared; in a large
+ * texture set most cells see no path in an iteration, so most of the 32
+ * accumulator bytes per parameter are never moved.  touch_map NULL: the same
+ * as mg_meta_update_fixed.  A stale set bit only costs its cell's read. */
+int mg_meta_update_fixed_touch(mg_ctx* ctx, int32_t dtype, int64_t cells, int32_t nch, int32_t r2,
+                               const mg_meta_update_args* a, void* accum, uint32_t* touch_map,
+                               void* m2_prop, void* m2_diff, void* mean, void* var,
+                               void* alpha_prev, const void* params_in, void* params_out,
+                               mg_update_scalars* scalars, const mg_meta_extras* x);
 
 /* Tile-sharded SHARED parameters (configs 4/5 shape), one rank's step as one
  * kernel over peer memory: for the parameter shard [shard_lo, shard_lo +
@@ -527,6 +542,11 @@ int mg_meshscene_info(const mg_mesh_scene* s, int32_t* nodes, int32_t* depth, in
  * The shade stage's texel-major copy of that buffer is then reused instead
  * of rebuilt (one relayout per iteration instead of two). */
 int mg_meshscene_set_prev_reuse(mg_mesh_scene* s, int32_t enable);
+/* touch_map (caller-owned, objects * R^2 / 32 uint32 words rounded up, or
+ * NULL to stop): sample pairs that leave their pair in accum (prop = diff =
+ * NULL) set the bit of every texel cell they add to, for
+ * mg_meta_update_fixed_touch.  The map belongs with ONE accumulator. */
+int mg_meshscene_set_touch_map(mg_mesh_scene* s, uint32_t* touch_map);
 /* Diagnostics (no reference counterpart): the queue counters of the scene's
  * last wavefront sample pair — paths entering each depth, then shadow rays
  * per depth (2 x (max depth + 1) entries, n_out >= 18).  Synchronises. */

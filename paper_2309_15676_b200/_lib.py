@@ -85,6 +85,9 @@ def load():
         "mg_meta_update_fixed": (C.c_int, [_vp, C.c_int32, C.c_int64, C.c_int32, C.c_int32,
                                            P(_abi.MetaUpdateArgs)] + [_vp] * 8 +
                                  [_vp, P(_abi.MetaExtras)]),
+        "mg_meta_update_fixed_touch": (C.c_int, [_vp, C.c_int32, C.c_int64, C.c_int32, C.c_int32,
+                                                 P(_abi.MetaUpdateArgs)] + [_vp] * 9 +
+                                       [_vp, P(_abi.MetaExtras)]),
         "mg_shared_meta_update": (C.c_int, [_vp, C.c_int32, C.c_int64, C.c_int64, C.c_int32,
                                             P(_abi.MetaUpdateArgs), _vp, _vp, _vp] +
                                   [_vp] * 7 + [_vp]),
@@ -121,6 +124,7 @@ def load():
         "mg_meshscene_destroy": (C.c_int, [_vp]),
         "mg_meshscene_info": (C.c_int, [_vp, _vp, _vp, _vp]),
         "mg_meshscene_set_prev_reuse": (C.c_int, [_vp, C.c_int32]),
+        "mg_meshscene_set_touch_map": (C.c_int, [_vp, _vp]),
         "mg_meshscene_queue_counts": (C.c_int, [_vp, _vp, C.c_int32, _vp]),
         "mg_ctx_set_iteration_offset": (C.c_int, [_vp, _vp]),
         "mg_iteration_offset_add": (C.c_int, [_vp, _vp, C.c_uint32]),

@@ -38,6 +38,9 @@ struct mg_mesh_scene {
   int last_now_slot = -1;          // ... the copy slot holding it (-1: none)
   int last_dtype = -1;
   unsigned int* last_cnt = nullptr;  // queue counters of the last wavefront call
+  // caller-owned bit per texel cell, set by the accumulator-keeping sample
+  // pair for every cell it adds to (mg_meshscene_set_touch_map)
+  unsigned int* touch = nullptr;
 };
 
 namespace mg {

@@ -905,6 +905,10 @@ struct AccTable {
   unsigned long long* ptr[kMaxRanks];
   int shard;  // parameters per rank
   int ilv;    // 1: single texel-interleaved accumulator
+  // ilv only, optional: one bit per texel cell, set with every vertex added
+  // to the cell (mg_meshscene_set_touch_map; consumed and cleared by
+  // mg_meta_update_fixed_touch)
+  unsigned int* touch;
 };
 
 __device__ __forceinline__ unsigned long long* acc_slot(const AccTable& a, int j, int which) {
@@ -920,7 +924,9 @@ struct AccCell {
   __device__ __forceinline__ AccCell(const AccTable& a, int b, int r2) : base(b), R2(r2) {
     if (ILV) {
       const int obj = b / (NCH * r2), tex = b - obj * NCH * r2;
-      q = a.ptr[0] + (size_t(obj) * r2 + tex) * (2 * NCH);
+      const size_t cell = size_t(obj) * r2 + tex;
+      q = a.ptr[0] + cell * (2 * NCH);
+      if (a.touch) atomicOr(&a.touch[cell >> 5], 1u << (cell & 31));
     }
   }
   __device__ __forceinline__ unsigned long long* at(const AccTable& a, int which, int k) const {
@@ -1453,6 +1459,7 @@ int mg_meshscene_sample_pair(mg_ctx* ctx, mg_mesh_scene* s, int32_t dtype, int32
   tbl.ptr[0] = acc;
   tbl.shard = int(np);
   tbl.ilv = 1;
+  tbl.touch = keep_acc ? s->touch : nullptr;
   // the megakernel implements the configs[3] form (4 channels, 2 proportional
   // paths) and accumulates in planar order
   const bool mega = g_mesh_megakernel && s->nch == 4 && prop_paths == 2 && !keep_acc;
@@ -1537,6 +1544,12 @@ int mg_meshscene_queue_counts(mg_ctx* ctx, const mg_mesh_scene* s, int32_t n_out
 #ifndef MG_PREV_REUSE
 #define MG_PREV_REUSE 1  // 0: ignore the opt-in (A/B builds)
 #endif
+int mg_meshscene_set_touch_map(mg_mesh_scene* s, uint32_t* touch_map) {
+  if (!s) return fail(MG_EINVAL, "mg_meshscene_set_touch_map: null scene");
+  s->touch = touch_map;
+  return MG_OK;
+}
+
 int mg_meshscene_set_prev_reuse(mg_mesh_scene* s, int32_t enable) {
   if (!s) return fail(MG_EINVAL, "mg_meshscene_set_prev_reuse: null scene");
   s->prev_reuse = MG_PREV_REUSE && enable != 0;

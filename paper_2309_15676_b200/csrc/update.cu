@@ -323,11 +323,23 @@ __host__ __device__ constexpr size_t fix_stage_bytes() {
 // (16-byte packs of 4 consecutive texels per thread, i.e. 4x fewer threads
 // for the same smem, measured 10-40 % slower: too few warps for the IEEE
 // division chains.)
-template <class T, bool FIRST, int NCH, int THREADS, int TPT, int STAGES, int MINB>
+//
+// TOUCH: a bit per texel cell says whether the cell's accumulator words may
+// be non-zero (the mesh scatter sets it with every vertex it adds).  Most
+// cells of a large texture set see no path in an iteration, so instead of
+// one bulk copy of the whole accumulator tile, thread t fetches its own
+// cell (NCH 16-byte cp.async's into the same stage, their completion
+// counted on the stage's mbarrier) only if its bit is set — otherwise it
+// writes zeros to the stage — and zeroes the global cell only if it read
+// it; the tile's bits are cleared.  32 B/param of accumulator traffic
+// become 32 B per TOUCHED parameter's sectors.
+template <class T, bool FIRST, bool TOUCH, int NCH, int THREADS, int TPT, int STAGES, int MINB>
 __global__ void __launch_bounds__(THREADS, MINB)
     meta_update_fixed_tma_kernel(int64_t tiles, int R2, MetaK k, MetaPtrs<T> q,
-                                 unsigned long long* __restrict__ acc, mg_update_scalars* sc,
+                                 unsigned long long* __restrict__ acc,
+                                 unsigned int* __restrict__ touch, mg_update_scalars* sc,
                                  ReducePartials* partials, unsigned int* counter) {
+  static_assert(!TOUCH || (TPT == 1 && THREADS % 32 == 0), "touch map: one cell per thread");
   extern __shared__ __align__(128) unsigned char smem_raw[];
   __shared__ __align__(8) uint64_t full[STAGES];
   constexpr int K = THREADS * TPT;
@@ -338,7 +350,7 @@ __global__ void __launch_bounds__(THREADS, MINB)
   const T* const src_arr[kFixArrays] = {q.m2p, q.m2d, q.mean, q.var, q.ap, q.pin};
   const bool use[kFixArrays] = {!FIRST, s.cnt0 > 0, !FIRST, !FIRST, !FIRST, true};
   (void)dst_arr;
-  uint32_t tx = uint32_t(kAccBytes);
+  uint32_t tx = TOUCH ? 0u : uint32_t(kAccBytes);
   int ncopy = 1;
 #pragma unroll
   for (int a = 0; a < kFixArrays; ++a)
@@ -349,11 +361,34 @@ __global__ void __launch_bounds__(THREADS, MINB)
   const int64_t my_tiles =
       int64_t(blockIdx.x) < tiles ? (tiles - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
   if (threadIdx.x == 0) {
-    for (int st = 0; st < STAGES; ++st) mbar_init(&full[st], 1);
+    for (int st = 0; st < STAGES; ++st) mbar_init(&full[st], TOUCH ? 1 + THREADS : 1);
     fence_mbar_init();
   }
   __syncthreads();
   const uint64_t pol = l2_evict_first_policy();
+  constexpr int kCellVecs = 2 * NCH * 8 / 16;  // 16-byte pieces of one cell
+  // TOUCH: the bits of local tile li (one word per warp)
+  auto tile_bits = [&](int64_t li) -> unsigned {
+    const int64_t cell0 = (int64_t(blockIdx.x) + li * gridDim.x) * K;
+    return touch[(cell0 + threadIdx.x) >> 5];
+  };
+  // TOUCH: every thread brings its own cell of local tile li into the stage
+  auto issue_cell = [&](int64_t li, unsigned bits) {
+    const int st = int(li % STAGES);
+    const int64_t cell0 = (int64_t(blockIdx.x) + li * gridDim.x) * K;
+    uint4* dst = reinterpret_cast<uint4*>(smem_raw + size_t(st) * kStage) +
+                 size_t(threadIdx.x) * kCellVecs;
+    if ((bits >> (threadIdx.x & 31)) & 1u) {
+      const uint4* src = reinterpret_cast<const uint4*>(acc + (cell0 + threadIdx.x) * 2 * NCH);
+#pragma unroll
+      for (int u = 0; u < kCellVecs; ++u) cp_async_16(dst + u, src + u);
+      cp_async_mbar_arrive_noinc(&full[st]);
+    } else {
+#pragma unroll
+      for (int u = 0; u < kCellVecs; ++u) dst[u] = make_uint4(0u, 0u, 0u, 0u);
+      mbar_arrive(&full[st]);
+    }
+  };
   // warp 0: lane 0 arms the stage's barrier, lanes 0..ncopy-1 issue one copy each
   auto issue = [&](int64_t li) {
     const int st = int(li % STAGES);
@@ -365,7 +400,7 @@ __global__ void __launch_bounds__(THREADS, MINB)
     if (lane == 0) mbar_arrive_expect_tx(&full[st], tx);
     __syncwarp();
     if (lane == 0) {
-      bulk_g2s_hint(sb, acc + cell0 * 2 * NCH, uint32_t(kAccBytes), &full[st], pol);
+      if (!TOUCH) bulk_g2s_hint(sb, acc + cell0 * 2 * NCH, uint32_t(kAccBytes), &full[st], pol);
     } else if (lane < ncopy) {
       // lane j >= 1: the (j-1)-th used (array, channel) run
       int r = lane - 1, a = 0;
@@ -385,20 +420,48 @@ __global__ void __launch_bounds__(THREADS, MINB)
                     uint32_t(K * sizeof(T)), &full[st], pol);
     }
   };
-  if (threadIdx.x < 32)
-    for (int64_t li = 0; li < my_tiles && li < STAGES; ++li) issue(li);
+  // the bits of the tiles in flight (their cells are zeroed / their words
+  // cleared when the tile is consumed) and of the next tile to issue
+  unsigned bits_ring[STAGES];
+#pragma unroll
+  for (int st = 0; st < STAGES; ++st) bits_ring[st] = 0u;
+  for (int64_t li = 0; li < my_tiles && li < STAGES; ++li) {
+    if (threadIdx.x < 32) issue(li);
+    if constexpr (TOUCH) {
+      const unsigned b = tile_bits(li);
+#pragma unroll
+      for (int st = 0; st < STAGES; ++st)
+        if (st == int(li)) bits_ring[st] = b;
+      issue_cell(li, b);
+    }
+  }
 
   Acc red;
   const int t = int(threadIdx.x);
   for (int64_t li = 0; li < my_tiles; ++li) {
     const int st = int(li % STAGES);
+    unsigned bits_now = 0u, bits_next = 0u;
+    if constexpr (TOUCH) {
+#pragma unroll
+      for (int s2 = 0; s2 < STAGES; ++s2)
+        if (s2 == st) bits_now = bits_ring[s2];
+      // requested now, used after this tile's arithmetic
+      if (li + STAGES < my_tiles) bits_next = tile_bits(li + STAGES);
+    }
     mbar_wait(&full[st], uint32_t((li / STAGES) & 1));
     const unsigned char* sb = smem_raw + size_t(st) * kStage;
     const int64_t tile = int64_t(blockIdx.x) + li * gridDim.x;
     const int64_t cell0 = tile * K;
     const int64_t obj = cell0 / R2, tex0 = cell0 - obj * R2;
     // zero the global accumulator tile (its words are in shared memory now)
-    {
+    if constexpr (TOUCH) {
+      if ((bits_now >> (t & 31)) & 1u) {
+        uint4* g = reinterpret_cast<uint4*>(acc + (cell0 + t) * 2 * NCH);
+#pragma unroll
+        for (int u = 0; u < kCellVecs; ++u) g[u] = make_uint4(0u, 0u, 0u, 0u);
+      }
+      if ((t & 31) == 0 && bits_now) touch[(cell0 + t) >> 5] = 0u;
+    } else {
       uint4* g = reinterpret_cast<uint4*>(acc + cell0 * 2 * NCH);
 #pragma unroll
       for (int u = 0; u < NCH * TPT; ++u) g[t + u * THREADS] = make_uint4(0u, 0u, 0u, 0u);
@@ -431,9 +494,17 @@ __global__ void __launch_bounds__(THREADS, MINB)
       }
     }
     __syncthreads();  // every thread is done reading stage st
-    if (threadIdx.x < 32 && li + STAGES < my_tiles) {
-      fence_proxy_async_smem();
-      issue(li + STAGES);
+    if (li + STAGES < my_tiles) {
+      if (threadIdx.x < 32) {
+        fence_proxy_async_smem();
+        issue(li + STAGES);
+      }
+      if constexpr (TOUCH) {
+#pragma unroll
+        for (int s2 = 0; s2 < STAGES; ++s2)
+          if (s2 == st) bits_ring[s2] = bits_next;
+        issue_cell(li + STAGES, bits_next);
+      }
     }
   }
   grid_reduce4<THREADS>(red.partials(), partials, counter, [&](const ReducePartials& r) {
@@ -985,7 +1056,7 @@ struct FixShape {
 template <class T, int NCH>
 int launch_meta_update_fixed(mg_ctx* ctx, int64_t cells, int R2, const MetaK& k,
                              const MetaPtrs<T>& q, bool first, unsigned long long* acc,
-                             mg_update_scalars* sc) {
+                             unsigned int* touch, mg_update_scalars* sc) {
   using S = FixShape<T, NCH>;
   const int64_t n = cells * NCH;
   const bool tma_ok = !g_disable_tma && R2 % S::texels == 0 && k.diff_norm == MG_DIFF_NORM_GLOBAL &&
@@ -1000,13 +1071,29 @@ int launch_meta_update_fixed(mg_ctx* ctx, int64_t cells, int R2, const MetaK& k,
     const int grid = int(tiles < want ? tiles : want);
     auto run = [&](auto kernel) {
       cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-      kernel<<<grid, S::threads, smem, ctx->stream>>>(tiles, R2, k, q, acc, sc, ctx->partials,
-                                                      ctx->counter);
+      kernel<<<grid, S::threads, smem, ctx->stream>>>(tiles, R2, k, q, acc, touch, sc,
+                                                      ctx->partials, ctx->counter);
     };
+    if constexpr (S::tpt == 1) {
+      if (touch) {
+        if (first)
+          run(meta_update_fixed_tma_kernel<T, true, true, NCH, S::threads, S::tpt, S::stages,
+                                           S::minb>);
+        else
+          run(meta_update_fixed_tma_kernel<T, false, true, NCH, S::threads, S::tpt, S::stages,
+                                           S::minb>);
+        MG_LAUNCH_CHECK(ctx);
+        return MG_OK;
+      }
+    }
+    // (a touch map with a multi-cell-per-thread shape: every cell is read
+    // and zeroed, the map is left as it is - stale bits are harmless)
     if (first)
-      run(meta_update_fixed_tma_kernel<T, true, NCH, S::threads, S::tpt, S::stages, S::minb>);
+      run(meta_update_fixed_tma_kernel<T, true, false, NCH, S::threads, S::tpt, S::stages,
+                                       S::minb>);
     else
-      run(meta_update_fixed_tma_kernel<T, false, NCH, S::threads, S::tpt, S::stages, S::minb>);
+      run(meta_update_fixed_tma_kernel<T, false, false, NCH, S::threads, S::tpt, S::stages,
+                                       S::minb>);
   } else {
     const int grid = grid_for(ctx, n, kThreads, 8);
     auto run = [&](auto kernel) {
@@ -1147,6 +1234,18 @@ int mg_meta_update_fixed(mg_ctx* ctx, int32_t dtype, int64_t cells, int32_t nch,
                          const mg_meta_update_args* a, void* accum, void* m2_prop, void* m2_diff,
                          void* mean, void* var, void* alpha_prev, const void* params_in,
                          void* params_out, mg_update_scalars* scalars, const mg_meta_extras* x) {
+  return mg_meta_update_fixed_touch(ctx, dtype, cells, nch, r2, a, accum, nullptr, m2_prop,
+                                    m2_diff, mean, var, alpha_prev, params_in, params_out, scalars,
+                                    x);
+}
+
+// touch_map (optional): bit c is set whenever cell c of accum may be
+// non-zero; only those cells are read and zeroed, and their bits cleared.
+int mg_meta_update_fixed_touch(mg_ctx* ctx, int32_t dtype, int64_t cells, int32_t nch, int32_t r2,
+                               const mg_meta_update_args* a, void* accum, uint32_t* touch_map,
+                               void* m2_prop, void* m2_diff, void* mean, void* var,
+                               void* alpha_prev, const void* params_in, void* params_out,
+                               mg_update_scalars* scalars, const mg_meta_extras* x) {
   MG_NVTX("mg_meta_update_fixed");
   if (!ctx || !a || !scalars) return fail(MG_EINVAL, "mg_meta_update_fixed: null argument");
   if (cells < 0 || r2 < 1 || (nch != 4 && nch != 5) || cells % r2 != 0)
@@ -1171,9 +1270,9 @@ int mg_meta_update_fixed(mg_ctx* ctx, int32_t dtype, int64_t cells, int32_t nch,
                   (T*)var, (T*)alpha_prev, (const T*)params_in, (T*)params_out,
                   (const T*)e.params_prev, (const T*)e.target, (T*)e.delta_out};
     return nch == 5 ? launch_meta_update_fixed<T, 5>(ctx, cells, r2, k, q, a->first_step != 0, acc,
-                                                     scalars)
+                                                     touch_map, scalars)
                     : launch_meta_update_fixed<T, 4>(ctx, cells, r2, k, q, a->first_step != 0, acc,
-                                                     scalars);
+                                                     touch_map, scalars);
   };
   if (dtype == MG_F32) return go(float{});
   if (dtype == MG_F64) return go(double{});

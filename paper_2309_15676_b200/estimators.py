@@ -199,18 +199,22 @@ class FusedMetaUpdate:
 
 
     def step_fixed(self, accum, cells: int, nch: int, r2: int, params_in, params_out,
-                   params_prev=None, target=None):
+                   params_prev=None, target=None, touch=None):
         """step() with the sample pair still in a mesh scene's texel-interleaved
         fixed-point accumulator (MeshTextureProblem.sample_pair(...,
         finalize=False)): converted, consumed and zeroed in the same pass
-        (mg_meta_update_fixed); every element as finalize + step()."""
+        (mg_meta_update_fixed); every element as finalize + step().
+        touch: the accumulator's touch map (MeshTextureProblem.enable_touch_map)
+        — only the cells a path reached are read and zeroed."""
         a = self.args(None)
         x = _abi.MetaExtras(None, None, _p(params_prev), _p(target), None)
-        check(load().mg_meta_update_fixed(self.ctx.h, _dtype_code(params_in), cells, nch, r2,
-                                          C.byref(a), _p(accum), _p(self.m2_prop),
-                                          _p(self.m2_diff), _p(self.mean), _p(self.var),
-                                          _p(self.alpha_prev), _p(params_in), _p(params_out),
-                                          _p(self.scalars_buf), C.byref(x)))
+        check(load().mg_meta_update_fixed_touch(self.ctx.h, _dtype_code(params_in), cells, nch,
+                                                r2, C.byref(a), _p(accum), _p(touch),
+                                                _p(self.m2_prop), _p(self.m2_diff),
+                                                _p(self.mean), _p(self.var),
+                                                _p(self.alpha_prev), _p(params_in),
+                                                _p(params_out), _p(self.scalars_buf),
+                                                C.byref(x)))
 
 
 class FusedAdamUpdate:

@@ -496,10 +496,25 @@ class MeshTextureProblem:
         self.target_img = self.scene.render(self.target_tex, width, height, target_spp,
                                             int(load().mg_mix64(target_seed)))
         self.accum = torch.zeros(2 * n, dtype=torch.int64, device="cuda")
+        self.touch = None
         self.loss_buf = torch.zeros(1, dtype=torch.float64, device="cuda")
 
     def dim(self) -> int:
         return self.scene.params()
+
+    def enable_touch_map(self, enable: bool = True):
+        """One bit per texel cell of self.accum, set by sample_pair(...,
+        finalize=False) for every cell it adds to and consumed by
+        FusedMetaUpdate.step_fixed(..., touch=self.touch)
+        (mg_meshscene_set_touch_map / mg_meta_update_fixed_touch)."""
+        if enable and self.touch is None:
+            cells = self.dim() // self.scene.channels
+            # set conservatively: accum may already hold a pair
+            self.touch = torch.full(((cells + 31) // 32,), -1, dtype=torch.int32, device="cuda")
+        elif not enable:
+            self.touch = None
+        check(load().mg_meshscene_set_touch_map(self.scene.h, _p(self.touch)))
+        return self.touch
 
     def draws_per_sample(self) -> int:
         """Paths per iteration: prop_paths proportional + 1 finite-difference spp."""
@@ -576,7 +591,7 @@ class MeshTextureRun(QuadTextureRun):
     iteration; texture values projected to [0, 1] (meta)."""
 
     def __init__(self, problem, optimizer: str = "meta", lr: float = 0.01, seed: int = 0,
-                 replicate: int = 0, fused: bool = True, **kw):
+                 replicate: int = 0, fused: bool = True, touch_map: bool = True, **kw):
         if optimizer == "meta":
             kw.setdefault("project_hi", 1.0)
         super().__init__(problem, optimizer, lr, seed, replicate, **kw)
@@ -587,6 +602,9 @@ class MeshTextureRun(QuadTextureRun):
         # directly (mg_meta_update_fixed) — step() then returns None;
         # fused=False keeps the planar pair (step() returns it)
         self.fused = bool(fused) and optimizer == "meta"
+        # ... and reads / zeroes only the accumulator cells a path reached
+        if self.fused:
+            problem.enable_touch_map(bool(touch_map))
 
     def step(self):
         if not self.fused:
@@ -601,5 +619,5 @@ class MeshTextureRun(QuadTextureRun):
         self.p.sample_pair(self.params, self.prev, iteration, self.key, finalize=False)
         new = self.prev
         cells, nch, r2 = self.p.fixed_layout()
-        self.upd.step_fixed(self.p.accum, cells, nch, r2, self.params, new)
+        self.upd.step_fixed(self.p.accum, cells, nch, r2, self.params, new, touch=self.p.touch)
         self.prev, self.params = self.params, new

@@ -338,6 +338,85 @@ def test_fused_fixed_update_matches_finalize_plus_update(api, dtype, nobj, nch, 
         pin = outA
 
 
+@pytest.mark.parametrize("dtype", [torch.float32, torch.float64])
+@pytest.mark.parametrize("nobj,nch,R,density", [(5, 5, 256, 0.3), (6, 4, 256, 0.05),
+                                                (5, 5, 256, 1.0), (5, 5, 256, 0.0),
+                                                (2, 5, 128, 0.3)])
+def test_fused_fixed_update_touch_map(api, dtype, nobj, nch, R, density):
+    """mg_meta_update_fixed_touch: with a touch map (bit per texel cell, set
+    where the accumulator may be non-zero, plus some stale bits over zero
+    cells) only the marked cells are fetched and zeroed; every output and
+    state element, the accumulator (all zero) and the map (all clear) equal
+    the map-less mg_meta_update_fixed from the same state, over four steps.
+    R = 256: >= 4 tiles per CTA (fp32; 17 in fp64), so the ring refill runs;
+    R = 128 x 2 objects: too few tiles for the TMA form — the per-parameter
+    kernel reads every cell and leaves the map alone."""
+    R2 = R * R
+    cells = nobj * R2
+    n = cells * nch
+    g = torch.Generator(device="cuda").manual_seed(7 * nobj + nch)
+    A = api.FusedMetaUpdate(n, dtype=dtype, lr=0.01, project_lo=0.0, project_hi=1.0)
+    B = api.FusedMetaUpdate(n, dtype=dtype, lr=0.01, project_lo=0.0, project_hi=1.0)
+    pin = torch.rand(n, generator=g, device="cuda", dtype=torch.float64).to(dtype)
+    names = ("m2_prop", "m2_diff", "mean", "var", "alpha_prev")
+    touch = torch.zeros((cells + 31) // 32, dtype=torch.int32, device="cuda")
+    ib = torch.int32 if dtype == torch.float32 else torch.int64
+    for step in range(4):
+        live = torch.rand(cells, generator=g, device="cuda") < density
+        acc = torch.randint(-(1 << 44), 1 << 44, (cells, 2, nch), generator=g, device="cuda",
+                            dtype=torch.int64)
+        acc *= live.view(cells, 1, 1)
+        if step == 0:
+            acc[:, 1, :] = 0
+        acc = acc.reshape(-1).contiguous()
+        stale = torch.rand(cells, generator=g, device="cuda") < 0.02
+        marked = (live | stale).view(-1, 32).to(torch.int64)
+        words = (marked << torch.arange(32, device="cuda")).sum(1)
+        touch.copy_(((words + (1 << 31)) % (1 << 32) - (1 << 31)).to(torch.int32))
+        accB = acc.clone()
+        for nm in names:
+            getattr(B, nm).copy_(getattr(A, nm))
+        B.scalars_buf.copy_(A.scalars_buf)
+        B.t, B.beta_f_pow = A.t, A.beta_f_pow
+        outA, outB = torch.empty_like(pin), torch.empty_like(pin)
+        A.step_fixed(acc, cells, nch, R2, pin, outA)
+        B.step_fixed(accB, cells, nch, R2, pin, outB, touch=touch)
+        torch.cuda.synchronize()
+        assert int(torch.count_nonzero(accB)) == 0, step
+        if R == 256:
+            assert int(torch.count_nonzero(touch)) == 0, step
+        assert torch.equal(outA.view(ib), outB.view(ib)), step
+        for nm in names:
+            assert torch.equal(getattr(A, nm).view(ib), getattr(B, nm).view(ib)), (step, nm)
+        sa, sb = A.scalars(), B.scalars()
+        assert sa.ssn == sb.ssn and sa.changed == sb.changed and sa.nonfinite == sb.nonfinite
+        pin = outA
+
+
+@pytest.mark.parametrize("channels,nprop,R", [(5, 4, 256), (4, 2, 256)])
+def test_mesh_run_touch_map_is_bit_identical(api, channels, nprop, R):
+    """MeshTextureRun with the touch map (the default: the scatter marks the
+    texel cells it adds to, the fused update fetches only those) against the
+    same run without it: parameters and estimator state bit for bit after
+    every iteration, accumulator zero and map clear in between."""
+    def make(tm):
+        prob = api.MeshTextureProblem(64, 48, R, (8, 12), (10, 12), max_vertices=4,
+                                      target_spp=4, dtype=torch.float32, channels=channels,
+                                      prop_paths=nprop)
+        return prob, api.MeshTextureRun(prob, "meta", lr=0.01, touch_map=tm)
+    (pa, a), (pb, b) = make(True), make(False)
+    assert pa.touch is not None and pb.touch is None
+    for k in range(5):
+        a.step()
+        b.step()
+        torch.cuda.synchronize()
+        assert torch.equal(a.params.view(torch.int32), b.params.view(torch.int32)), k
+        for nm in ("m2_prop", "m2_diff", "mean", "var", "alpha_prev"):
+            assert torch.equal(getattr(a.upd, nm).view(torch.int32),
+                               getattr(b.upd, nm).view(torch.int32)), (k, nm)
+        assert int(torch.count_nonzero(pa.accum)) == 0 and int(torch.count_nonzero(pa.touch)) == 0
+
+
 def test_fused_mesh_run_tracks_unfused(api):
     """MeshTextureRun's default fused update (sample pair left in the
     fixed-point accumulator) follows the finalize + update trajectory: the
