@@ -82,8 +82,8 @@ struct WF {
   // invalid fields are never read (the scatter substitutes zeros), so they
   // need not be written
   unsigned char *vnee, *vbnc;
-  // depths < kVfRecFrom: [v][field][PS] planes (every path alive: coalesced);
-  // depths >= kVfRecFrom: [v][PS][stride] records (few survivors: a path's fields
+  // depths < vf_rec_from<NCH>(): [v][field][PS] planes (every path alive: coalesced);
+  // depths >= vf_rec_from<NCH>(): [v][PS][stride] records (few survivors: a path's fields
   // share 4-7 sectors instead of one sector per field)
   T* vdat;
   // [4][kMaxV + 1]: queue counts, shadow-queue counts, and the fetch
@@ -182,14 +182,21 @@ __device__ __forceinline__ int enqueue(bool pred, unsigned int* counter) {
 }
 // (callers check the slot against their queue's capacity with MG_DCHECK)
 
-// Depths >= kVfRecFrom (0-based) store records, the others planes.  The
-// choice is a compile-time property of every access (REC): as a run-time
-// branch in the accessors it cost configs[4] 0.9 ms per iteration.
-// Build switch for A/B: 0 = records everywhere, 99 = planes everywhere.
+// Depths >= vf_rec_from<NCH>() (0-based) store records, the others planes.
+// The choice is a compile-time property of every access (REC): as a
+// run-time branch in the accessors it cost configs[4] 0.9 ms per iteration.
+// 5 channels (224-byte records): planes at depth 0, where every path is
+// alive (configs[4] 7.21 ms against 7.61 with records everywhere);
+// 4 channels (96-byte records): records everywhere (configs[3] 0.87 ms
+// against 0.895).  Build switch for A/B: MG_VF_REC_FROM = 0 records
+// everywhere, 99 planes everywhere, d records from depth d.
 #ifndef MG_VF_REC_FROM
-#define MG_VF_REC_FROM 1
+#define MG_VF_REC_FROM -1
 #endif
-constexpr int kVfRecFrom = MG_VF_REC_FROM;
+template <int NCH>
+__host__ __device__ constexpr int vf_rec_from() {
+  return MG_VF_REC_FROM >= 0 ? MG_VF_REC_FROM : (NCH == 4 ? 0 : 1);
+}
 // vertex header: the texel's parameter base and the NEE / bounce validity
 // bytes; at record depths they live in the record's first two slots
 // (slot 0: base, slot 1: validity bytes 0 and 1)
@@ -216,9 +223,9 @@ __device__ __forceinline__ unsigned char& vh_bnc(const WF<T>& w, int v, int p) {
     return w.vbnc[size_t(v) * w.PS + p];
 }
 // the shadow stages clear one validity byte: layout picked at run time
-template <class T>
+template <int NCH, class T>
 __device__ __forceinline__ void vh_nee_clear(const WF<T>& w, int v, int p) {
-  if (v >= kVfRecFrom)
+  if (v >= vf_rec_from<NCH>())
     vh_nee<true>(w, v, p) = 0;
   else
     vh_nee<false>(w, v, p) = 0;
@@ -712,7 +719,7 @@ __global__ void __launch_bounds__(kMThreads, 8) wf_shadow_kernel(MeshDev m, WF<T
       const int nj = (k == 0 || k == w.nprop) ? 6 : 3;
       for (int j = 0; j < nj; ++j) w.L[size_t(j) * w.P + p] += w.pendC[size_t(j) * w.P + p];
     } else if (p < w.PS) {  // occluded: no NEE data at this vertex
-      vh_nee_clear(w, v, p);
+      vh_nee_clear<NCH>(w, v, p);
     }
   }
 }
@@ -743,7 +750,7 @@ __global__ void __launch_bounds__(kMThreads, 8) wf_shadow_p_kernel(MeshDev m, WF
           const int nj = (k == 0 || k == w.nprop) ? 6 : 3;
           for (int j = 0; j < nj; ++j) w.L[size_t(j) * w.P + p] += w.pendC[size_t(j) * w.P + p];
         } else if (p < w.PS) {  // occluded: no NEE data at this vertex
-          vh_nee_clear(w, v, p);
+          vh_nee_clear<NCH>(w, v, p);
         }
       },
       sstk);
@@ -773,7 +780,7 @@ __global__ void __launch_bounds__(kMThreads, kP8Blocks) wf_shadow_p8_kernel(Mesh
           const int nj = (k == 0 || k == w.nprop) ? 6 : 3;
           for (int j = 0; j < nj; ++j) w.L[size_t(j) * w.P + p] += w.pendC[size_t(j) * w.P + p];
         } else if (p < w.PS) {  // occluded: no NEE data at this vertex
-          vh_nee_clear(w, v, p);
+          vh_nee_clear<NCH>(w, v, p);
         }
       });
 }
@@ -792,11 +799,17 @@ __global__ void __launch_bounds__(kMThreads, kP8Blocks) wf_shadow_p8_kernel(Mesh
 // result is bit-identical.
 // SSTK / QN: the traversal stack in shared memory, quantised nodes (as the
 // persistent stages).
+// CTAs per SM: 4 (128 registers) for 5 channels, 3 (168) for 4 channels
+// (configs[3] 0.895 -> 0.867 ms; configs[4] 7.22 -> 7.33 ms with 3)
 #ifndef MG_TAIL_BLOCKS
-#define MG_TAIL_BLOCKS 4
+#define MG_TAIL_BLOCKS -1
 #endif
+template <int NCH>
+__host__ __device__ constexpr int tail_blocks() {
+  return MG_TAIL_BLOCKS > 0 ? MG_TAIL_BLOCKS : (NCH == 4 ? 3 : 4);
+}
 template <int NCH, bool SSTK, bool QN>
-__global__ void __launch_bounds__(kMThreads, MG_TAIL_BLOCKS)
+__global__ void __launch_bounds__(kMThreads, tail_blocks<NCH>())
     wf_tail_kernel(MeshK q, MeshDev m, WF<float> w, int v0, const float* __restrict__ th0,
                    const float* __restrict__ th1) {
   __shared__ float4 sn[SSTK ? 1 : kNodeF4 * kSmemNodes];
@@ -857,7 +870,7 @@ __global__ void __launch_bounds__(kMThreads, MG_TAIL_BLOCKS)
     io.bv = 0.0;
     io.slot = trace32_impl<false, SSTK, QN>(m, sn, io.o, io.d, INFINITY, io.t, io.bu, io.bv, sstk);
     bool want_shadow = false, want_bounce = false;
-    if (kVfRecFrom <= 1 || v >= kVfRecFrom)  // the tail starts at depth >= 1
+    if (vf_rec_from<NCH>() <= 1 || v >= vf_rec_from<NCH>())  // the tail starts at depth >= 1
       shade_path<float, NCH, true, true>(q, m, w, v, p, io, th0, th1, maxv, R2, la, want_shadow,
                                    want_bounce);
     else
@@ -872,7 +885,7 @@ __global__ void __launch_bounds__(kMThreads, MG_TAIL_BLOCKS)
           for (int c = 0; c < 3; ++c)
             if (s < ns) w.L[size_t(s * 3 + c) * w.P + p] += io.pendC[s][c];
       } else if (p < w.PS) {  // occluded: no NEE data at this vertex
-        vh_nee_clear(w, v, p);
+        vh_nee_clear<NCH>(w, v, p);
       }
     }
     if (want_bounce) {
@@ -1065,7 +1078,7 @@ MG_SCATTER_INLINE void wf_scatter(const WF<T>& w, int p, const T wt[3], int R2,
   // record depths, then plane depths: the layout is a compile-time
   // property of each loop
   int v = vtop - 1;
-  for (; v >= kVfRecFrom; --v)
+  for (; v >= vf_rec_from<NCH>(); --v)
     if (v < nvp) vertex(v, std::true_type{});
   for (; v >= 0; --v)
     if (v < nvp) vertex(v, std::false_type{});
@@ -1123,7 +1136,7 @@ MG_SCATTER_INLINE void wf_scatter_a(const WF<T>& w, int p, const T wt[3], const 
     }
   };
   int v = vtop - 1;
-  for (; v >= kVfRecFrom; --v)
+  for (; v >= vf_rec_from<NCH>(); --v)
     if (v < nvp) vertex(v, std::true_type{});
   for (; v >= 0; --v)
     if (v < nvp) vertex(v, std::false_type{});
@@ -1346,7 +1359,7 @@ int wavefront_pair(mg_ctx* ctx, mg_mesh_scene* s, const MeshK& q, int nprop, con
     MG_NVTX(kDepthName[v]);
     if constexpr (sizeof(T) == 4) {
       if (tail_from > 0 && v >= tail_from) {
-        const int tgrid = grid_for(ctx, w.P, kMThreads, MG_TAIL_BLOCKS);
+        const int tgrid = grid_for(ctx, w.P, kMThreads, tail_blocks<NCH>());
         if (sstk && g_mesh_qnodes)
           wf_tail_kernel<NCH, true, true><<<tgrid, kMThreads, 0, ctx->stream>>>(q, m, w, v, thI[0],
                                                                                 thI[1]);
@@ -1372,7 +1385,7 @@ int wavefront_pair(mg_ctx* ctx, mg_mesh_scene* s, const MeshK& q, int nprop, con
       wf_isect_kernel<T><<<grid, kMThreads, 0, ctx->stream>>>(m, w, v);
     }
     MG_LAUNCH_CHECK(ctx);
-    if (v >= kVfRecFrom)
+    if (v >= vf_rec_from<NCH>())
       wf_shade_kernel<T, NCH, true><<<grid, kMThreads, 0, ctx->stream>>>(q, m, w, v, thI[0],
                                                                         thI[1]);
     else
