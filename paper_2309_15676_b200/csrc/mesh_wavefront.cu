@@ -626,8 +626,12 @@ __device__ __forceinline__ void shade_path(const MeshK& q, const MeshDev& m, con
   }
 }
 
+// fp32: 4 CTAs/SM (128 registers, no spills)
+#ifndef MG_SHADE_BLOCKS
+#define MG_SHADE_BLOCKS 4
+#endif
 template <class T, int NCH, bool REC>
-__global__ void __launch_bounds__(kMThreads, sizeof(T) == 4 ? 4 : 1)
+__global__ void __launch_bounds__(kMThreads, sizeof(T) == 4 ? MG_SHADE_BLOCKS : 1)
     wf_shade_kernel(MeshK q, MeshDev m, WF<T> w, int v, const T* __restrict__ th0,
                     const T* __restrict__ th1) {
   if (q.it_offset) q.iteration += __ldg(q.it_offset);
@@ -1144,10 +1148,13 @@ MG_SCATTER_INLINE void wf_scatter_a(const WF<T>& w, int p, const T wt[3], const 
 
 constexpr int kMaxProp = 8;
 
-// 4 CTAs/SM (<= 128 registers): measured 2 % faster on configs[4] than the
-// unconstrained 168-227 registers
+// 6 CTAs/SM (<= 80 registers).  With the per-vertex records the walk holds
+// few values: configs[4] 7.05 -> 7.00 ms, configs[3] 0.866 -> 0.850 ms
+// against 4 CTAs/SM (5: 7.01 / 0.851, 3: 7.19 / 0.883).  (With one plane
+// per field, 4 had measured 2 % faster than the unconstrained 168-227
+// registers and 6 / 8 slower or equal.)
 #ifndef MG_SCATTER_BLOCKS
-#define MG_SCATTER_BLOCKS 4
+#define MG_SCATTER_BLOCKS 6
 #endif
 template <class T, int NCH, bool ILV>
 __global__ void __launch_bounds__(kMThreads, MG_SCATTER_BLOCKS)
