@@ -412,6 +412,8 @@ def test_mesh_run_touch_map_is_bit_identical(api, channels, nprop, R):
         torch.cuda.synchronize()
         assert torch.equal(a.params.view(torch.int32), b.params.view(torch.int32)), k
         for nm in ("m2_prop", "m2_diff", "mean", "var", "alpha_prev"):
+            if k == 0 and nm == "m2_diff":
+                continue  # not written before the first FD sample: uninitialised memory
             assert torch.equal(getattr(a.upd, nm).view(torch.int32),
                                getattr(b.upd, nm).view(torch.int32)), (k, nm)
         assert int(torch.count_nonzero(pa.accum)) == 0 and int(torch.count_nonzero(pa.touch)) == 0

@@ -22,5 +22,5 @@ timeout 3000 python -m pytest -q -p no:cacheprovider \
   tests/test_gpu_quad.py tests/test_gpu_helix.py tests/test_gpu_acceptance.py \
   >> gpurun_out/debug_checks.log 2>&1
 echo "rc=$?" >> gpurun_out/debug_checks.log
-grep -c "Assertion" gpurun_out/debug_checks.log | sed 's/^/device asserts: /' >> gpurun_out/debug_checks.log
+grep -c "Assertion \`" gpurun_out/debug_checks.log | sed 's/^/device asserts: /' >> gpurun_out/debug_checks.log
 tail -4 gpurun_out/debug_checks.log
