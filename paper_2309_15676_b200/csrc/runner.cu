@@ -33,7 +33,15 @@ namespace mg {
 bool g_cluster_runner = true;
 namespace {
 
-constexpr int kThreads = 256;
+// threads of the one-CTA-per-replicate runner.  S1 shape by replicate count
+// (tools/runner_reps_probe.py, run_experiment wall): 256 threads 23.5 / 33.5 /
+// 76.6 ms at 148 / 296 / 592 replicates, 512 threads 19.7 / 40.5 / 85.0,
+// 1024 threads 19.5 / 39.1 / 77.1 - the device saturates near 1.5-1.8M
+// replicate-iterations/s (fp64 pow) either way; 256 keeps 2-3 CTAs per SM.
+#ifndef MG_RUN_THREADS
+#define MG_RUN_THREADS 256
+#endif
+constexpr int kThreads = MG_RUN_THREADS;
 constexpr int kNumSeries = 11;
 
 template <class T>
