@@ -79,6 +79,10 @@ extern bool g_mesh_scatter_agg;
 // mg_set_option("bvh_leaf_size", k): maximum triangles per BVH leaf (1..7),
 // applied to scenes created afterwards
 extern int g_bvh_leaf;
+// mg_set_option("bvh_sah_axes", 1 | 3): binned-SAH split candidates on the
+// longest centroid axis only, or on all three (default), for scenes created
+// afterwards
+extern int g_bvh_axes;
 
 namespace mesh {
 

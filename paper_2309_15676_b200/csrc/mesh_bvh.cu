@@ -18,6 +18,7 @@ bool g_mesh_scatter_agg = false;
 bool g_mesh_bvh8 = false;
 bool g_mesh_smem_stack = true;
 bool g_mesh_qnodes = true;
+int g_bvh_axes = 3;
 int g_bvh_leaf = 2;
 namespace mesh {
 namespace {
@@ -81,54 +82,62 @@ struct Builder {
     int axis = 0;
     for (int k = 1; k < 3; ++k)
       if (chi[k] - clo[k] > chi[axis] - clo[axis]) axis = k;
-    const double ext = chi[axis] - clo[axis];
+    // binned SAH over every axis with extent (g_bvh_axes = 1: the longest
+    // centroid axis only, the round-1 builder)
     int mid = -1;
-    if (ext > 0.0) {
+    {
       constexpr int kBins = 16;
-      int cnt[kBins] = {0};
-      double bl[kBins][3], bh[kBins][3];
-      for (int i = 0; i < kBins; ++i)
-        for (int k = 0; k < 3; ++k) {
-          bl[i][k] = INFINITY;
-          bh[i][k] = -INFINITY;
-        }
-      auto bin_of = [&](int t) {
-        int q = int(((cen[size_t(3 * t + axis)] - clo[axis]) / ext) * kBins);
+      double best = INFINITY;
+      int best_split = -1, best_axis = -1;
+      auto bin_of = [&](int t, int ax) {
+        const double ext = chi[ax] - clo[ax];
+        int q = int(((cen[size_t(3 * t + ax)] - clo[ax]) / ext) * kBins);
         return q < 0 ? 0 : (q >= kBins ? kBins - 1 : q);
       };
-      for (int i = b; i < e; ++i) {
-        const int t = idx[size_t(i)], q = bin_of(t);
-        cnt[q]++;
-        for (int k = 0; k < 3; ++k) {
-          bl[q][k] = std::min(bl[q][k], blo[size_t(3 * t + k)]);
-          bh[q][k] = std::max(bh[q][k], bhi[size_t(3 * t + k)]);
-        }
-      }
-      double best = INFINITY;
-      int best_split = -1;
-      for (int s = 1; s < kBins; ++s) {
-        double l0[3] = {INFINITY, INFINITY, INFINITY}, h0[3] = {-INFINITY, -INFINITY, -INFINITY};
-        double l1[3] = {INFINITY, INFINITY, INFINITY}, h1[3] = {-INFINITY, -INFINITY, -INFINITY};
-        int n0 = 0, n1 = 0;
-        for (int q = 0; q < kBins; ++q) {
-          double* L = q < s ? l0 : l1;
-          double* H = q < s ? h0 : h1;
-          (q < s ? n0 : n1) += cnt[q];
+      for (int ax = 0; ax < 3; ++ax) {
+        if (g_bvh_axes == 1 && ax != axis) continue;
+        if (!(chi[ax] - clo[ax] > 0.0)) continue;
+        int cnt[kBins] = {0};
+        double bl[kBins][3], bh[kBins][3];
+        for (int i = 0; i < kBins; ++i)
           for (int k = 0; k < 3; ++k) {
-            L[k] = std::min(L[k], bl[q][k]);
-            H[k] = std::max(H[k], bh[q][k]);
+            bl[i][k] = INFINITY;
+            bh[i][k] = -INFINITY;
+          }
+        for (int i = b; i < e; ++i) {
+          const int t = idx[size_t(i)], q = bin_of(t, ax);
+          cnt[q]++;
+          for (int k = 0; k < 3; ++k) {
+            bl[q][k] = std::min(bl[q][k], blo[size_t(3 * t + k)]);
+            bh[q][k] = std::max(bh[q][k], bhi[size_t(3 * t + k)]);
           }
         }
-        if (!n0 || !n1) continue;
-        const double c = area(l0, h0) * n0 + area(l1, h1) * n1;
-        if (c < best) {
-          best = c;
-          best_split = s;
+        for (int s = 1; s < kBins; ++s) {
+          double l0[3] = {INFINITY, INFINITY, INFINITY}, h0[3] = {-INFINITY, -INFINITY, -INFINITY};
+          double l1[3] = {INFINITY, INFINITY, INFINITY}, h1[3] = {-INFINITY, -INFINITY, -INFINITY};
+          int n0 = 0, n1 = 0;
+          for (int q = 0; q < kBins; ++q) {
+            double* L = q < s ? l0 : l1;
+            double* H = q < s ? h0 : h1;
+            (q < s ? n0 : n1) += cnt[q];
+            for (int k = 0; k < 3; ++k) {
+              L[k] = std::min(L[k], bl[q][k]);
+              H[k] = std::max(H[k], bh[q][k]);
+            }
+          }
+          if (!n0 || !n1) continue;
+          const double c = area(l0, h0) * n0 + area(l1, h1) * n1;
+          if (c < best) {
+            best = c;
+            best_split = s;
+            best_axis = ax;
+          }
         }
       }
       if (best_split > 0) {
-        auto it = std::partition(idx.begin() + b, idx.begin() + e,
-                                 [&](int t) { return bin_of(t) < best_split; });
+        auto it = std::partition(idx.begin() + b, idx.begin() + e, [&](int t) {
+          return bin_of(t, best_axis) < best_split;
+        });
         mid = int(it - idx.begin());
       }
     }
@@ -393,8 +402,9 @@ int mg_meshscene_create(mg_ctx* ctx, int32_t tri_count, const double* tri, const
       }
   }
   // each step pushes at most 7 children
-  if (7 * (depth8 + 1) + 1 > kStackDepth)
-    return fail(MG_EINVAL, "mg_meshscene_create: BVH8 deeper than the traversal stack");
+  // (the optional eight-wide traversal needs 7 pushes per level: a scene too
+  // deep for its stack keeps the four-wide traversal, depth8 = -1)
+  const bool bvh8_ok = 7 * (depth8 + 1) + 1 <= kStackDepth;
   const int nn8 = int(order8.size());
   std::vector<float4> nodes8(size_t(kNode8F4) * size_t(nn8));
   for (int i = 0; i < nn8; ++i) {
@@ -445,7 +455,7 @@ int mg_meshscene_create(mg_ctx* ctx, int32_t tri_count, const double* tri, const
   sc->nnodes = nn;
   sc->depth = depth4;
   sc->nnodes8 = nn8;
-  sc->depth8 = depth8;
+  sc->depth8 = bvh8_ok ? depth8 : -1;
   cudaError_t e = cudaMalloc(&sc->tri, sizeof(double) * stri.size());
   if (e == cudaSuccess) e = cudaMalloc(&sc->tri32, sizeof(float4) * stri32.size());
   if (e == cudaSuccess)

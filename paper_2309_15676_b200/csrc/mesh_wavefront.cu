@@ -1378,7 +1378,7 @@ int wavefront_pair(mg_ctx* ctx, mg_mesh_scene* s, const MeshK& q, int nprop, con
       }
     }
     if constexpr (sizeof(T) == 4) {
-      if ((pmode & 1) && g_mesh_bvh8)
+      if ((pmode & 1) && g_mesh_bvh8 && s->depth8 >= 0)
         wf_isect_p8_kernel<<<pgrid8, kMThreads, 0, ctx->stream>>>(m, w, v);
       else if ((pmode & 1) && sstk && g_mesh_qnodes)
         wf_isect_p_kernel<true, true><<<pgrid, kMThreads, 0, ctx->stream>>>(m, w, v);
@@ -1400,7 +1400,7 @@ int wavefront_pair(mg_ctx* ctx, mg_mesh_scene* s, const MeshK& q, int nprop, con
                                                                          thI[1]);
     MG_LAUNCH_CHECK(ctx);
     if constexpr (sizeof(T) == 4) {
-      if ((pmode & 2) && g_mesh_bvh8)
+      if ((pmode & 2) && g_mesh_bvh8 && s->depth8 >= 0)
         wf_shadow_p8_kernel<NCH><<<pgrid8, kMThreads, 0, ctx->stream>>>(m, w, v);
       else if ((pmode & 2) && sstk && g_mesh_qnodes)
         wf_shadow_p_kernel<NCH, true, true><<<pgrid, kMThreads, 0, ctx->stream>>>(m, w, v);

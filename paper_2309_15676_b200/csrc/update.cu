@@ -42,6 +42,7 @@ extern bool g_mesh_smem_stack;
 extern bool g_mesh_qnodes;
 extern bool g_helix_split;
 extern int g_bvh_leaf;
+extern int g_bvh_axes;
 // -1: per-dtype default measured on B200: fp32 -> variant 8 (1 CTA/SM x 640
 // threads, 2 stages of 10 KB tiles: 20 warps to issue the body and ~180 KB
 // in flight; interleaved A/B over 30 blocks of 20 launches,
@@ -1121,6 +1122,11 @@ int mg_set_option(const char* name, int64_t value) {
   if (std::string(name) == "bvh_leaf_size") {
     if (value < 1 || value > 7) return fail(MG_EINVAL, "bvh_leaf_size must lie in [1, 7]");
     g_bvh_leaf = int(value);
+    return MG_OK;
+  }
+  if (std::string(name) == "bvh_sah_axes") {
+    if (value != 1 && value != 3) return fail(MG_EINVAL, "bvh_sah_axes must be 1 or 3");
+    g_bvh_axes = int(value);
     return MG_OK;
   }
   if (std::string(name) == "helix_split") {
