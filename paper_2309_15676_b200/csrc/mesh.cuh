@@ -83,6 +83,9 @@ extern int g_bvh_leaf;
 // longest centroid axis only, or on all three (default), for scenes created
 // afterwards
 extern int g_bvh_axes;
+// mg_set_option("bvh_bins", n): SAH bins per axis (2..64, default 32:
+// configs[4] 6.80 -> 6.77 ms against 16, 6.92 with 8; configs[3] +-0)
+extern int g_bvh_bins;
 
 namespace mesh {
 

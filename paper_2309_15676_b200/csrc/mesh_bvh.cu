@@ -1,4 +1,4 @@
-// Host side of the mesh renderer: binned-SAH BVH build (16 bins, at most
+// Host side of the mesh renderer: binned-SAH BVH build (32 bins on each axis, at most
 // g_bvh_leaf triangles per leaf), breadth-first relabelling of the internal
 // nodes so the top levels form one block every CTA stages in shared memory,
 // 128-byte four-child nodes (the binary tree collapsed by opening the
@@ -19,6 +19,7 @@ bool g_mesh_bvh8 = false;
 bool g_mesh_smem_stack = true;
 bool g_mesh_qnodes = true;
 int g_bvh_axes = 3;
+int g_bvh_bins = 32;
 int g_bvh_leaf = 2;
 namespace mesh {
 namespace {
@@ -86,7 +87,8 @@ struct Builder {
     // centroid axis only, the round-1 builder)
     int mid = -1;
     {
-      constexpr int kBins = 16;
+      constexpr int kMaxBins = 64;
+      const int kBins = g_bvh_bins;
       double best = INFINITY;
       int best_split = -1, best_axis = -1;
       auto bin_of = [&](int t, int ax) {
@@ -97,8 +99,8 @@ struct Builder {
       for (int ax = 0; ax < 3; ++ax) {
         if (g_bvh_axes == 1 && ax != axis) continue;
         if (!(chi[ax] - clo[ax] > 0.0)) continue;
-        int cnt[kBins] = {0};
-        double bl[kBins][3], bh[kBins][3];
+        int cnt[kMaxBins] = {0};
+        double bl[kMaxBins][3], bh[kMaxBins][3];
         for (int i = 0; i < kBins; ++i)
           for (int k = 0; k < 3; ++k) {
             bl[i][k] = INFINITY;

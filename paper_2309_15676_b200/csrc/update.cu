@@ -43,6 +43,7 @@ extern bool g_mesh_qnodes;
 extern bool g_helix_split;
 extern int g_bvh_leaf;
 extern int g_bvh_axes;
+extern int g_bvh_bins;
 // -1: per-dtype default measured on B200: fp32 -> variant 8 (1 CTA/SM x 640
 // threads, 2 stages of 10 KB tiles: 20 warps to issue the body and ~180 KB
 // in flight; interleaved A/B over 30 blocks of 20 launches,
@@ -1127,6 +1128,11 @@ int mg_set_option(const char* name, int64_t value) {
   if (std::string(name) == "bvh_sah_axes") {
     if (value != 1 && value != 3) return fail(MG_EINVAL, "bvh_sah_axes must be 1 or 3");
     g_bvh_axes = int(value);
+    return MG_OK;
+  }
+  if (std::string(name) == "bvh_bins") {
+    if (value < 2 || value > 64) return fail(MG_EINVAL, "bvh_bins must lie in [2, 64]");
+    g_bvh_bins = int(value);
     return MG_OK;
   }
   if (std::string(name) == "helix_split") {
