@@ -514,6 +514,18 @@ def test_mesh_abi_rejects_bad_arguments(api):
         sc.render(th, 8, 8, 0, 1)
     pair(sc.view, rows=(3, 3))          # an empty tile is valid: zero pair, zero loss
     assert float(loss[0]) == 0.0 and int(torch.count_nonzero(out)) == 0
+    # touch map: a null scene is rejected, a null map switches it off; the
+    # touch update validates like mg_meta_update_fixed and takes a null map
+    with pytest.raises(InvalidArgument):
+        check(L.mg_meshscene_set_touch_map(None, None))
+    check(L.mg_meshscene_set_touch_map(sc.h, None))
+    upd = api.FusedMetaUpdate(n, dtype=torch.float64, lr=0.01)
+    cells, R2 = n // 4, (n // 4) // nobj
+    for bad in ((cells, 3, R2), (cells, 4, 0), (cells + 1, 4, R2), (-1, 4, R2)):
+        with pytest.raises(InvalidArgument):
+            upd.step_fixed(acc, bad[0], bad[1], bad[2], th, out)
+    upd.step_fixed(acc, cells, 4, R2, th, out, touch=None)
+    torch.cuda.synchronize()
 
 
 def test_mesh_f32_path_divergence_pixel_fraction(api, record_property):
